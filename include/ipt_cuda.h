@@ -1,0 +1,172 @@
+/*
+ * ipt_cuda.h — C ABI of the B200 IPT hot path (libipt_b200.so).
+ *
+ * This is the drop-in boundary under the reference's C++ solver API
+ * (proj/include/ipt/solver.hpp, kernels.hpp). Plain pointers and sizes only:
+ * no torch, no C++ types. Every function returns IPT_OK (0) or a negative
+ * code and never throws; ipt_last_error() holds the message of the last
+ * failure on the calling thread. The C++ layer (include/ipt/*.hpp,
+ * src/api/*.cpp) maps the codes back to the reference's exception types:
+ *   IPT_ERR_INVALID -> std::invalid_argument (solver.cpp:18-30,39-41,125,158,192-197)
+ *   IPT_ERR_CUDA / IPT_ERR_NCCL -> std::runtime_error
+ * Non-convergence is a status (IPT_STATUS_*), not an error.
+ *
+ * Host matrices are the reference's layout: dense row-major n x n
+ * (complex_matrix.hpp:48-49), given here as planar real / imaginary parts;
+ * an imaginary pointer of NULL means "all zero" and selects the real fp64
+ * fast path (the configs of BASELINE.json are real). CSR uses 64-bit row
+ * offsets and 32-bit column indices (n < 2^31), sorted, no duplicates.
+ */
+#ifndef IPT_CUDA_H
+#define IPT_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IPT_OK 0
+#define IPT_ERR_INVALID (-1)
+#define IPT_ERR_CUDA (-2)
+#define IPT_ERR_NCCL (-4)
+#define IPT_ERR_INTERNAL (-5)
+
+#define IPT_STATUS_CONVERGED 0
+#define IPT_STATUS_MAX_ITERATIONS 1
+#define IPT_STATUS_DIVERGED 2
+
+#define IPT_STOP_REL_FRO 0 /* |F(Z)-Z|_F / |Z|_F <= tol   (solver.cpp:236,246) */
+#define IPT_STOP_MAX_ABS 1 /* max |F(Z)-Z| < tol          (BASELINE.json configs) */
+
+#define IPT_SCHEDULE_PLAIN 0        /* solve_single                 (solver.cpp:132-136) */
+#define IPT_SCHEDULE_CONTINUATION 1 /* solve_single_continuation     (solver.cpp:138-154) */
+
+typedef struct ipt_ctx ipt_ctx;
+typedef struct ipt_full_problem ipt_full_problem;
+typedef struct ipt_single_problem ipt_single_problem;
+
+/* Mirrors ipt::IterationConfig (solver.hpp:10-20) plus the device-only knobs. */
+typedef struct {
+  double tolerance;            /* default 100 * DBL_EPSILON */
+  int32_t max_iterations;      /* default 1000 */
+  double divergence_threshold; /* default 1e8 */
+  int32_t record_trace;
+  int32_t stop_rule;           /* IPT_STOP_* (full spectrum only) */
+  int32_t want_sigma_min;      /* 1: smallest_singular_value_estimate (solver.cpp:271) */
+  int32_t schedule;            /* IPT_SCHEDULE_* (single pair only) */
+  double shrink_alpha;         /* continuation factor in [0, 1) */
+  int32_t ignore_convergence;  /* bench only: apply exactly max_iterations maps */
+} ipt_params;
+
+/* Mirrors ipt::SpectrumResult / EigenpairResult scalars (solver.hpp:28-52). */
+typedef struct {
+  int32_t iterations;
+  int32_t status;
+  double final_step;       /* relative step of the last map application */
+  double final_max_abs;    /* max |F(Z) - Z| of the last map application */
+  double residual;         /* full: |MZ - Z Lambda|_F ; single: |Mz - lambda z|_2/|z|_2 */
+  double min_singular_value_estimate;
+  int64_t product_count;   /* matmul_count (full) or matvec_count (single) */
+  double eigenvalue_re;    /* single pair only */
+  double eigenvalue_im;
+  double* trace;           /* caller buffer >= max_iterations doubles, or NULL */
+  double* trace_max_abs;   /* full only, caller buffer or NULL */
+  /* device timings (CUDA events), milliseconds */
+  double ms_upload, ms_loop, ms_final, ms_sigma, ms_download;
+} ipt_stats;
+
+const char* ipt_last_error(void);
+void ipt_default_params(ipt_params* p);
+
+/* ---- context: one CUDA device, one stream, optional NCCL communicator ---- */
+int ipt_ctx_create(int device, ipt_ctx** out);
+void ipt_ctx_destroy(ipt_ctx* ctx);
+int ipt_ctx_device(const ipt_ctx* ctx);
+/* 128-byte ncclUniqueId from rank 0, exchanged by the caller (torch.distributed). */
+int ipt_nccl_get_unique_id(void* out128);
+int ipt_ctx_init_comm(ipt_ctx* ctx, const void* unique_id128, int rank, int nranks);
+int ipt_ctx_rank(const ipt_ctx* ctx, int* rank, int* nranks);
+int ipt_ctx_synchronize(ipt_ctx* ctx);
+
+/* ---- full spectrum: solve_full (solver.cpp:180-273) ----
+ * With a communicator of g ranks, Z is column-sharded: rank r iterates columns
+ * [r*n/g, (r+1)*n/g) with Delta and d replicated, one all-reduce of the step
+ * scalars per iteration, and Z/eigenvalues are gathered to rank 0 (other ranks
+ * may pass NULL outputs). warm_* (nullable) is a full n x n start basis. */
+int ipt_full_solve(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                   const double* delta_re, const double* delta_im, const double* warm_re,
+                   const double* warm_im, const ipt_params* params, double* z_re, double* z_im,
+                   double* lam_re, double* lam_im, ipt_stats* stats);
+
+/* Device-resident pieces of the same solve, for timing with inputs in HBM. */
+int ipt_full_upload(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                    const double* delta_re, const double* delta_im, ipt_full_problem** out);
+int ipt_full_reset(ipt_ctx* ctx, ipt_full_problem* prob, const double* warm_re, const double* warm_im);
+int ipt_full_iterate(ipt_ctx* ctx, ipt_full_problem* prob, const ipt_params* params, ipt_stats* stats);
+int ipt_full_finalize(ipt_ctx* ctx, ipt_full_problem* prob, const ipt_params* params, ipt_stats* stats);
+int ipt_full_download(ipt_ctx* ctx, ipt_full_problem* prob, double* z_re, double* z_im,
+                      double* lam_re, double* lam_im);
+int ipt_full_local_columns(const ipt_full_problem* prob, int64_t* col_begin, int64_t* col_end);
+void ipt_full_free(ipt_full_problem* prob);
+
+/* apply_map_full (solver.cpp:156-178): one F application to a given Z. */
+int ipt_apply_map_full(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                       const double* delta_re, const double* delta_im, const double* z_re,
+                       const double* z_im, double* f_re, double* f_im);
+
+/* smallest_singular_value_estimate (solver.cpp:275-297). */
+int ipt_sigma_min(ipt_ctx* ctx, int64_t n, const double* z_re, const double* z_im,
+                  int32_t max_iters, double tol, double* out);
+
+/* ---- single eigenpair: run_single (solver.cpp:49-93) ----
+ * Dense (delta row-major n x n) or CSR (rowptr[n+1], cols[nnz], vals[nnz]).
+ * warm_* (nullable, length n) is renormalised to z[anchor] = 1 (solver.cpp:32-45).
+ * With a communicator the CSR rows are sharded and z is all-gathered per step. */
+int ipt_single_solve_dense(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                           const double* delta_re, const double* delta_im, int64_t anchor,
+                           const double* warm_re, const double* warm_im, const ipt_params* params,
+                           double* z_re, double* z_im, ipt_stats* stats);
+int ipt_single_solve_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                         const int64_t* rowptr, const int32_t* cols, const double* val_re,
+                         const double* val_im, int64_t anchor, const double* warm_re,
+                         const double* warm_im, const ipt_params* params, double* z_re,
+                         double* z_im, ipt_stats* stats);
+
+int ipt_single_upload_dense(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                            const double* delta_re, const double* delta_im,
+                            ipt_single_problem** out);
+int ipt_single_upload_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                          const int64_t* rowptr, const int32_t* cols, const double* val_re,
+                          const double* val_im, ipt_single_problem** out);
+int ipt_single_reset(ipt_ctx* ctx, ipt_single_problem* prob, int64_t anchor, const double* warm_re,
+                     const double* warm_im);
+int ipt_single_iterate(ipt_ctx* ctx, ipt_single_problem* prob, const ipt_params* params,
+                       ipt_stats* stats);
+int ipt_single_finalize(ipt_ctx* ctx, ipt_single_problem* prob, ipt_stats* stats);
+int ipt_single_download(ipt_ctx* ctx, ipt_single_problem* prob, double* z_re, double* z_im);
+void ipt_single_free(ipt_single_problem* prob);
+
+/* apply_map_single (solver.cpp:122-130). */
+int ipt_apply_map_single_dense(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                               const double* delta_re, const double* delta_im, int64_t anchor,
+                               const double* z_re, const double* z_im, double* f_re, double* f_im);
+
+/* ---- kernels::matmul / kernels::matvec (kernels.hpp:12-25) ---- */
+/* C (m x n) = A (m x k) B (k x n), all row-major; *_im nullable (zero). */
+int ipt_gemm(ipt_ctx* ctx, int64_t m, int64_t k, int64_t n, const double* a_re, const double* a_im,
+             const double* b_re, const double* b_im, double* c_re, double* c_im);
+int ipt_matvec_dense(ipt_ctx* ctx, int64_t m, int64_t n, const double* a_re, const double* a_im,
+                     const double* x_re, const double* x_im, double* y_re, double* y_im);
+int ipt_matvec_csr(ipt_ctx* ctx, int64_t m, int64_t n, const int64_t* rowptr, const int32_t* cols,
+                   const double* val_re, const double* val_im, const double* x_re,
+                   const double* x_im, double* y_re, double* y_im);
+
+/* Counters for gpu_launches accounting: kernels this library has launched. */
+int64_t ipt_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IPT_CUDA_H */

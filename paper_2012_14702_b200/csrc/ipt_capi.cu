@@ -1,0 +1,511 @@
+// extern "C" boundary (include/ipt_cuda.h): contexts, NCCL, and the solver /
+// kernel entry points. Exceptions never cross this file: every entry point maps
+// them to IPT_ERR_* and records the message for ipt_last_error().
+#include <cfloat>
+#include <cstring>
+#include <string>
+
+#include "dmma_gemm.cuh"
+#include "ipt_internal.cuh"
+
+using namespace iptb;
+
+namespace {
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return IPT_OK;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return IPT_ERR_INVALID;
+  } catch (const NcclError& e) {
+    g_last_error = e.what();
+    return IPT_ERR_NCCL;
+  } catch (const CudaError& e) {
+    g_last_error = e.what();
+    return IPT_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return IPT_ERR_INTERNAL;
+  }
+}
+
+ipt_params params_or_default(const ipt_params* p) {
+  ipt_params d;
+  ipt_default_params(&d);
+  return p ? *p : d;
+}
+
+void check_ctx(ipt_ctx* ctx) {
+  if (ctx == nullptr) throw InvalidArgument("null ipt_ctx");
+}
+
+// host row-major (rows x cols) -> device column-major with leading dimension ld (zero-padded dst)
+void upload_as_colmajor(Ctx& c, const double* host_rm, int64_t rows, int64_t cols, double* dst, int64_t ld) {
+  DevBuf tmp;
+  tmp.alloc(size_t(rows) * cols, false);
+  IPT_CUDA(cudaMemcpyAsync(tmp.get(), host_rm, sizeof(double) * rows * cols, cudaMemcpyHostToDevice, c.stream));
+  // row-major rows x cols == column-major cols x rows; transpose to column-major rows x cols
+  transpose_to_rowmajor(c.stream, tmp.get(), cols, cols, rows, dst, ld);
+  c.sync();
+}
+}  // namespace
+
+extern "C" {
+
+const char* ipt_last_error(void) { return g_last_error.c_str(); }
+
+void ipt_default_params(ipt_params* p) {
+  std::memset(p, 0, sizeof(*p));
+  p->tolerance = 100.0 * DBL_EPSILON;
+  p->max_iterations = 1000;
+  p->divergence_threshold = 1e8;
+  p->record_trace = 0;
+  p->stop_rule = IPT_STOP_REL_FRO;
+  p->want_sigma_min = 1;
+  p->schedule = IPT_SCHEDULE_PLAIN;
+  p->shrink_alpha = 0.9;
+  p->ignore_convergence = 0;
+}
+
+int64_t ipt_kernel_launch_count(void) { return g_launches.load(); }
+
+int ipt_ctx_create(int device, ipt_ctx** out) {
+  return guarded([&] {
+    if (out == nullptr) throw InvalidArgument("ipt_ctx_create: null out");
+    int count = 0;
+    IPT_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw InvalidArgument("ipt_ctx_create: bad device index");
+    IPT_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    IPT_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw CudaError("libipt_b200 is built for sm_100a (B200); device is sm_" +
+                                          std::to_string(prop.major) + std::to_string(prop.minor));
+    auto* ctx = new ipt_ctx();
+    ctx->c.device = device;
+    IPT_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+    IPT_CUDA(cudaMallocHost(&ctx->c.h_state, sizeof(LoopState)));
+    for (auto& e : ctx->c.ev) IPT_CUDA(cudaEventCreate(&e));
+    *out = ctx;
+  });
+}
+
+void ipt_ctx_destroy(ipt_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->c.device);
+  if (ctx->c.comm) ncclCommDestroy(ctx->c.comm);
+  for (auto& e : ctx->c.ev) cudaEventDestroy(e);
+  if (ctx->c.h_state) cudaFreeHost(ctx->c.h_state);
+  if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
+  delete ctx;
+}
+
+int ipt_ctx_device(const ipt_ctx* ctx) { return ctx ? ctx->c.device : -1; }
+
+int ipt_nccl_get_unique_id(void* out128) {
+  return guarded([&] {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    IPT_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int ipt_ctx_init_comm(ipt_ctx* ctx, const void* unique_id128, int rank, int nranks) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArgument("ipt_ctx_init_comm: bad rank");
+    DeviceGuard g(ctx->c.device);
+    if (ctx->c.comm) {
+      ncclCommDestroy(ctx->c.comm);
+      ctx->c.comm = nullptr;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id128, sizeof(id));
+    IPT_NCCL(ncclCommInitRank(&ctx->c.comm, nranks, id, rank));
+    ctx->c.rank = rank;
+    ctx->c.nranks = nranks;
+  });
+}
+
+int ipt_ctx_rank(const ipt_ctx* ctx, int* rank, int* nranks) {
+  if (!ctx) return IPT_ERR_INVALID;
+  if (rank) *rank = ctx->c.rank;
+  if (nranks) *nranks = ctx->c.nranks;
+  return IPT_OK;
+}
+
+int ipt_ctx_synchronize(ipt_ctx* ctx) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    ctx->c.sync();
+  });
+}
+
+// ------------------------------------------------------------------ full spectrum
+
+int ipt_full_upload(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                    const double* delta_re, const double* delta_im, ipt_full_problem** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    *out = reinterpret_cast<ipt_full_problem*>(full_upload(ctx->c, n, d_re, d_im, delta_re, delta_im));
+  });
+}
+
+int ipt_full_reset(ipt_ctx* ctx, ipt_full_problem* prob, const double* warm_re, const double* warm_im) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    full_reset(*reinterpret_cast<FullProblem*>(prob), warm_re, warm_im, 1000);
+  });
+}
+
+int ipt_full_iterate(ipt_ctx* ctx, ipt_full_problem* prob, const ipt_params* params, ipt_stats* stats) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    full_iterate(*reinterpret_cast<FullProblem*>(prob), params_or_default(params), stats);
+  });
+}
+
+int ipt_full_finalize(ipt_ctx* ctx, ipt_full_problem* prob, const ipt_params* params, ipt_stats* stats) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    full_finalize(*reinterpret_cast<FullProblem*>(prob), params_or_default(params), stats);
+  });
+}
+
+int ipt_full_download(ipt_ctx* ctx, ipt_full_problem* prob, double* z_re, double* z_im, double* lam_re,
+                      double* lam_im) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    full_download(*reinterpret_cast<FullProblem*>(prob), z_re, z_im, lam_re, lam_im);
+  });
+}
+
+int ipt_full_local_columns(const ipt_full_problem* prob, int64_t* col_begin, int64_t* col_end) {
+  if (!prob) return IPT_ERR_INVALID;
+  full_local_columns(*reinterpret_cast<const FullProblem*>(prob), col_begin, col_end);
+  return IPT_OK;
+}
+
+void ipt_full_free(ipt_full_problem* prob) { full_free(reinterpret_cast<FullProblem*>(prob)); }
+
+int ipt_full_solve(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                   const double* delta_re, const double* delta_im, const double* warm_re,
+                   const double* warm_im, const ipt_params* params, double* z_re, double* z_im,
+                   double* lam_re, double* lam_im, ipt_stats* stats) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    const ipt_params prm = params_or_default(params);
+    if (!(prm.tolerance > 0.0)) throw InvalidArgument("config: tolerance must be positive");
+    if (prm.max_iterations <= 0) throw InvalidArgument("config: max_iterations must be positive");
+    if (!(prm.divergence_threshold > 1.0)) throw InvalidArgument("config: divergence_threshold must exceed 1");
+    Ctx& c = ctx->c;
+    IPT_CUDA(cudaEventRecord(c.ev[2], c.stream));
+    std::unique_ptr<FullProblem, void (*)(FullProblem*)> P(full_upload(c, n, d_re, d_im, delta_re, delta_im),
+                                                           full_free);
+    full_reset(*P, warm_re, warm_im, prm.max_iterations);
+    IPT_CUDA(cudaEventRecord(c.ev[3], c.stream));
+    c.sync();
+    float ms_up = 0.f;
+    IPT_CUDA(cudaEventElapsedTime(&ms_up, c.ev[2], c.ev[3]));
+    full_iterate(*P, prm, stats);
+    full_finalize(*P, prm, stats);
+    IPT_CUDA(cudaEventRecord(c.ev[2], c.stream));
+    full_download(*P, z_re, z_im, lam_re, lam_im);
+    IPT_CUDA(cudaEventRecord(c.ev[3], c.stream));
+    c.sync();
+    float ms_down = 0.f;
+    IPT_CUDA(cudaEventElapsedTime(&ms_down, c.ev[2], c.ev[3]));
+    if (stats) {
+      stats->ms_upload = ms_up;
+      stats->ms_download = ms_down;
+    }
+  });
+}
+
+int ipt_apply_map_full(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                       const double* delta_re, const double* delta_im, const double* z_re,
+                       const double* z_im, double* f_re, double* f_im) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (ctx->c.nranks != 1) throw InvalidArgument("apply_map_full: single-device context required");
+    if (!z_re) throw InvalidArgument("apply_map_full: null Z");
+    std::unique_ptr<FullProblem, void (*)(FullProblem*)> P(full_upload(ctx->c, n, d_re, d_im, delta_re, delta_im),
+                                                           full_free);
+    bool zc = false;
+    if (z_im) for (int64_t t = 0; t < n * n && !zc; ++t) zc = z_im[t] != 0.0;
+    if (zc && !full_is_complex(*P)) {
+      // a complex Z on a real Delta: re-upload on the complex path
+      P.reset(full_upload(ctx->c, n, d_re, d_im, delta_re, delta_im, /*force_complex=*/true));
+    }
+    full_reset(*P, z_re, z_im, 1, /*renormalize=*/false);
+    ipt_params prm;
+    ipt_default_params(&prm);
+    prm.max_iterations = 1;
+    prm.ignore_convergence = 1;
+    prm.divergence_threshold = DBL_MAX;
+    full_iterate(*P, prm, nullptr);
+    full_download(*P, f_re, f_im, nullptr, nullptr);
+  });
+}
+
+int ipt_sigma_min(ipt_ctx* ctx, int64_t n, const double* z_re, const double* z_im, int32_t max_iters,
+                  double tol, double* out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (n <= 0) throw InvalidArgument("smallest_singular_value_estimate: square input required");
+    Ctx& c = ctx->c;
+    bool cplx = false;
+    if (z_im) for (int64_t t = 0; t < n * n && !cplx; ++t) cplx = z_im[t] != 0.0;
+    const int64_t ld = round_up(n, 16);
+    const int64_t ldz = cplx ? 2 * ld : ld;
+    DevBuf Z;
+    Z.alloc(size_t(round_up(n, kBN)) * ldz);
+    upload_as_colmajor(c, z_re, n, n, Z.get(), ldz);
+    if (cplx) upload_as_colmajor(c, z_im, n, n, Z.get() + ld, ldz);
+    *out = sigma_min_device(c, n, Z.get(), cplx ? Z.get() + ld : nullptr, ldz, max_iters, tol);
+  });
+}
+
+// ------------------------------------------------------------------ single pair
+
+static SingleProblem* as_single(ipt_single_problem* p) { return reinterpret_cast<SingleProblem*>(p); }
+
+int ipt_single_upload_dense(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                            const double* delta_re, const double* delta_im, ipt_single_problem** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    *out = reinterpret_cast<ipt_single_problem*>(single_upload(ctx->c, n, d_re, d_im, false, delta_re,
+                                                               delta_im, nullptr, nullptr, nullptr,
+                                                               nullptr, true));
+  });
+}
+
+int ipt_single_upload_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                          const int64_t* rowptr, const int32_t* cols, const double* val_re,
+                          const double* val_im, ipt_single_problem** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    *out = reinterpret_cast<ipt_single_problem*>(single_upload(ctx->c, n, d_re, d_im, true, nullptr,
+                                                               nullptr, rowptr, cols, val_re, val_im,
+                                                               false));
+  });
+}
+
+int ipt_single_reset(ipt_ctx* ctx, ipt_single_problem* prob, int64_t anchor, const double* warm_re,
+                     const double* warm_im) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    single_reset(*as_single(prob), anchor, warm_re, warm_im, 1000);
+  });
+}
+
+int ipt_single_iterate(ipt_ctx* ctx, ipt_single_problem* prob, const ipt_params* params, ipt_stats* stats) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    single_iterate(*as_single(prob), params_or_default(params), stats);
+  });
+}
+
+int ipt_single_finalize(ipt_ctx* ctx, ipt_single_problem* prob, ipt_stats* stats) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    single_finalize(*as_single(prob), stats);
+  });
+}
+
+int ipt_single_download(ipt_ctx* ctx, ipt_single_problem* prob, double* z_re, double* z_im) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    single_download(*as_single(prob), z_re, z_im);
+  });
+}
+
+void ipt_single_free(ipt_single_problem* prob) { single_free(as_single(prob)); }
+
+static int single_solve_common(ipt_ctx* ctx, SingleProblem* raw, int64_t anchor, const double* warm_re,
+                               const double* warm_im, const ipt_params* params, double* z_re,
+                               double* z_im, ipt_stats* stats) {
+  std::unique_ptr<SingleProblem, void (*)(SingleProblem*)> P(raw, single_free);
+  const ipt_params prm = params_or_default(params);
+  single_reset(*P, anchor, prm.schedule == IPT_SCHEDULE_CONTINUATION ? nullptr : warm_re,
+               prm.schedule == IPT_SCHEDULE_CONTINUATION ? nullptr : warm_im, prm.max_iterations);
+  single_iterate(*P, prm, stats);
+  single_finalize(*P, stats);
+  single_download(*P, z_re, z_im);
+  (void)ctx;
+  return IPT_OK;
+}
+
+int ipt_single_solve_dense(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                           const double* delta_re, const double* delta_im, int64_t anchor,
+                           const double* warm_re, const double* warm_im, const ipt_params* params,
+                           double* z_re, double* z_im, ipt_stats* stats) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    const ipt_params prm = params_or_default(params);
+    if (!(prm.tolerance > 0.0)) throw InvalidArgument("config: tolerance must be positive");
+    if (prm.max_iterations <= 0) throw InvalidArgument("config: max_iterations must be positive");
+    if (anchor < 0 || anchor >= n) throw InvalidArgument("solver: anchor out of range");
+    single_solve_common(ctx, single_upload(ctx->c, n, d_re, d_im, false, delta_re, delta_im, nullptr,
+                                           nullptr, nullptr, nullptr, true),
+                        anchor, warm_re, warm_im, params, z_re, z_im, stats);
+  });
+}
+
+int ipt_single_solve_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                         const int64_t* rowptr, const int32_t* cols, const double* val_re,
+                         const double* val_im, int64_t anchor, const double* warm_re,
+                         const double* warm_im, const ipt_params* params, double* z_re, double* z_im,
+                         ipt_stats* stats) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    const ipt_params prm = params_or_default(params);
+    if (!(prm.tolerance > 0.0)) throw InvalidArgument("config: tolerance must be positive");
+    if (prm.max_iterations <= 0) throw InvalidArgument("config: max_iterations must be positive");
+    if (anchor < 0 || anchor >= n) throw InvalidArgument("solver: anchor out of range");
+    single_solve_common(ctx, single_upload(ctx->c, n, d_re, d_im, true, nullptr, nullptr, rowptr, cols,
+                                           val_re, val_im, true),
+                        anchor, warm_re, warm_im, params, z_re, z_im, stats);
+  });
+}
+
+int ipt_apply_map_single_dense(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                               const double* delta_re, const double* delta_im, int64_t anchor,
+                               const double* z_re, const double* z_im, double* f_re, double* f_im) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (anchor < 0 || anchor >= n) throw InvalidArgument("solver: anchor out of range");
+    bool zc = false;
+    if (z_im) for (int64_t t = 0; t < n && !zc; ++t) zc = z_im[t] != 0.0;
+    std::unique_ptr<SingleProblem, void (*)(SingleProblem*)> P(
+        single_upload(ctx->c, n, d_re, d_im, false, delta_re, delta_im, nullptr, nullptr, nullptr, nullptr,
+                      true, /*force_complex=*/zc),
+        single_free);
+    single_reset(*P, anchor, z_re, z_im, 1, /*renormalize=*/false);
+    ipt_params prm;
+    ipt_default_params(&prm);
+    prm.max_iterations = 1;
+    prm.ignore_convergence = 1;
+    prm.divergence_threshold = DBL_MAX;
+    single_iterate(*P, prm, nullptr);
+    single_download(*P, f_re, f_im);
+  });
+}
+
+// ------------------------------------------------------------------ kernels::
+
+int ipt_gemm(ipt_ctx* ctx, int64_t m, int64_t k, int64_t n, const double* a_re, const double* a_im,
+             const double* b_re, const double* b_im, double* c_re, double* c_im) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (m < 0 || k < 0 || n < 0) throw InvalidArgument("matmul: negative shape");
+    Ctx& c = ctx->c;
+    cudaStream_t s = c.stream;
+    if (m == 0 || n == 0) return;
+    bool cplx = false;
+    if (a_im) for (int64_t t = 0; t < m * k && !cplx; ++t) cplx = a_im[t] != 0.0;
+    if (b_im) for (int64_t t = 0; t < k * n && !cplx; ++t) cplx = b_im[t] != 0.0;
+    const int64_t ldk = round_up(std::max<int64_t>(k, 1), 16);
+    const int64_t K = cplx ? 2 * ldk : ldk;
+    const int64_t mpad = round_up(m, kBM), npad = round_up(n, kBN);
+    DevBuf A1, A2, B, C1, C2, rm;
+    A1.alloc(size_t(mpad) * K);
+    B.alloc(size_t(npad) * K);
+    auto up2d = [&](double* dst, int64_t dpitch, const double* src) {
+      if (k == 0) return;
+      IPT_CUDA(cudaMemcpy2DAsync(dst, dpitch * sizeof(double), src, k * sizeof(double), k * sizeof(double), m,
+                                 cudaMemcpyHostToDevice, s));
+    };
+    up2d(A1.get(), K, a_re);
+    if (k > 0) upload_as_colmajor(c, b_re, k, n, B.get(), K);  // column-major k x n, ld K
+    if (cplx) {
+      A2.alloc(size_t(mpad) * K);
+      up2d(A2.get() + ldk, K, a_re);
+      if (a_im) {
+        up2d(A2.get(), K, a_im);
+        DevBuf tmp;
+        tmp.alloc(size_t(m) * k, false);
+        IPT_CUDA(cudaMemcpyAsync(tmp.get(), a_im, sizeof(double) * m * k, cudaMemcpyHostToDevice, s));
+        scale_copy(s, tmp.get(), tmp.get(), size_t(m) * k, -1.0);
+        IPT_CUDA(cudaMemcpy2DAsync(A1.get() + ldk, K * sizeof(double), tmp.get(), k * sizeof(double),
+                                   k * sizeof(double), m, cudaMemcpyDeviceToDevice, s));
+        c.sync();
+      }
+      if (b_im && k > 0) upload_as_colmajor(c, b_im, k, n, B.get() + ldk, K);
+    }
+    C1.alloc(size_t(n) * m, false);
+    rm.alloc(size_t(m) * n, false);
+    gemm_tn_store(s, m, n, K, A1.get(), K, B.get(), K, C1.get(), m);
+    transpose_to_rowmajor(s, C1.get(), m, m, n, rm.get(), n);
+    IPT_CUDA(cudaMemcpyAsync(c_re, rm.get(), sizeof(double) * m * n, cudaMemcpyDeviceToHost, s));
+    c.sync();
+    if (c_im) {
+      if (!cplx) {
+        std::memset(c_im, 0, sizeof(double) * m * n);
+      } else {
+        gemm_tn_store(s, m, n, K, A2.get(), K, B.get(), K, C1.get(), m);
+        transpose_to_rowmajor(s, C1.get(), m, m, n, rm.get(), n);
+        IPT_CUDA(cudaMemcpyAsync(c_im, rm.get(), sizeof(double) * m * n, cudaMemcpyDeviceToHost, s));
+        c.sync();
+      }
+    }
+  });
+}
+
+int ipt_matvec_dense(ipt_ctx* ctx, int64_t m, int64_t n, const double* a_re, const double* a_im,
+                     const double* x_re, const double* x_im, double* y_re, double* y_im) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (m != n) {  // rectangular: one-column product
+      const int rc = ipt_gemm(ctx, m, n, 1, a_re, a_im, x_re, x_im, y_re, y_im);
+      if (rc != IPT_OK) throw CudaError(g_last_error);
+      return;
+    }
+    std::vector<double> dz(size_t(std::max<int64_t>(n, 1)), 0.0);
+    std::unique_ptr<SingleProblem, void (*)(SingleProblem*)> P(
+        single_upload(ctx->c, n, dz.data(), nullptr, false, a_re, a_im, nullptr, nullptr, nullptr, nullptr, true),
+        single_free);
+    single_matvec(*P, x_re, x_im, y_re, y_im);
+  });
+}
+
+int ipt_matvec_csr(ipt_ctx* ctx, int64_t m, int64_t n, const int64_t* rowptr, const int32_t* cols,
+                   const double* val_re, const double* val_im, const double* x_re, const double* x_im,
+                   double* y_re, double* y_im) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (m != n) throw InvalidArgument("matvec_csr: square operator required");
+    std::vector<double> dz(size_t(std::max<int64_t>(n, 1)), 0.0);
+    std::unique_ptr<SingleProblem, void (*)(SingleProblem*)> P(
+        single_upload(ctx->c, n, dz.data(), nullptr, true, nullptr, nullptr, rowptr, cols, val_re, val_im, true),
+        single_free);
+    single_matvec(*P, x_re, x_im, y_re, y_im);
+  });
+}
+
+}  // extern "C"

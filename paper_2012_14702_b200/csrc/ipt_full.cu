@@ -1,0 +1,656 @@
+// Full-spectrum IPT on the device: solve_full / apply_map_full
+// (proj/src/solver.cpp:156-273), column-sharded over a NCCL communicator.
+//
+// HBM layout (per rank):
+//   Delta : rows_pad x ld, row-major, zero-padded (ld = round_up(n,16), rows_pad = round_up(n,128)).
+//           Complex inputs use the K-concatenated forms A1 = [Dr | -Di], A2 = [Di | Dr]
+//           (rows_pad x 2ld) so that W = Delta Z is two real DMMA GEMMs over K = 2ld.
+//   Z[2]  : ping-pong column blocks, column-major, ldz = ld (real) or 2ld ([re; im] per column),
+//           cols_pad = round_up(ncols,128) columns; this rank owns global columns [col0, col0+ncols).
+//   d     : n, replicated; wd / lam : per local column.
+// Per iteration: K2 diag pre-pass (wd_j = (Delta Z)_jj), K1 DMMA GEMM with the fused map
+// epilogue writing F(Z) into the other Z buffer and per-CTA partial sums, a fixed-order
+// reduction, [NCCL all-reduce of 3 sums + 1 max], and a single-thread decide kernel
+// that applies the reference's divergence-then-convergence tests (solver.cpp:236-249).
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "dmma_gemm.cuh"
+#include "ipt_internal.cuh"
+
+namespace iptb {
+
+struct FullProblem {
+  Ctx* ctx = nullptr;
+  int64_t n = 0, ld = 0, rows_pad = 0;
+  int64_t col0 = 0, ncols = 0, cols_pad = 0;
+  bool cplx = false;
+  DevBuf A1, A2;
+  int64_t lda = 0;  // = K of the GEMM
+  DevBuf dre, dim;
+  DevBuf Z[2];
+  int64_t ldz = 0;
+  DevBuf Wre, Wim;          // complex only
+  DevBuf wd, wdi, lam, lami;
+  DevBuf partials;
+  DevBuf sums;
+  LoopState* state = nullptr;
+  DevBuf trace, trace_max;
+  int trace_cap = 0;
+  int enq = 0;              // maps enqueued since reset
+  DevBuf gathered;          // rank 0 with nranks > 1: full Z (n columns, ldz)
+  bool finalized = false;
+  ~FullProblem() {
+    if (state) cudaFree(state);
+  }
+};
+
+// ----------------------------------------------------------------- kernels
+
+__global__ void identity_columns_kernel(double* Z, int64_t ldz, int64_t ncols, int64_t col0) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j < ncols) Z[j * ldz + col0 + j] = 1.0;
+}
+
+// K2: wd_j = sum_k A[col0+j, k] Z[k, j] over the zero-padded K; one warp per column,
+// 16-byte loads, fixed per-lane order + xor tree (deterministic). Optionally
+// lam_j = d_{col0+j} + wd_j (the eigenvalue formula of solver.cpp:256).
+__global__ void diag_dot_kernel(const double* __restrict__ A, int64_t lda,
+                                const double* __restrict__ Z, int64_t ldz, int64_t K,
+                                int64_t ncols, int64_t col0, double* __restrict__ wd,
+                                const double* __restrict__ d, double* __restrict__ lam,
+                                const LoopState* state) {
+  if (state != nullptr && state->done) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t j = blockIdx.x * int64_t(blockDim.x / 32) + (threadIdx.x >> 5);
+  if (j >= ncols) return;
+  const double2* a = reinterpret_cast<const double2*>(A + (col0 + j) * lda);
+  const double2* z = reinterpret_cast<const double2*>(Z + j * ldz);
+  const int64_t K2 = K / 2;
+  double sx = 0.0, sy = 0.0;
+  int64_t k = lane;
+  for (; k + 96 < K2; k += 128) {
+    const double2 a0 = __ldg(a + k), a1 = __ldg(a + k + 32), a2 = __ldg(a + k + 64), a3 = __ldg(a + k + 96);
+    const double2 z0 = z[k], z1 = z[k + 32], z2 = z[k + 64], z3 = z[k + 96];
+    sx = __fma_rn(a0.x, z0.x, sx); sy = __fma_rn(a0.y, z0.y, sy);
+    sx = __fma_rn(a1.x, z1.x, sx); sy = __fma_rn(a1.y, z1.y, sy);
+    sx = __fma_rn(a2.x, z2.x, sx); sy = __fma_rn(a2.y, z2.y, sy);
+    sx = __fma_rn(a3.x, z3.x, sx); sy = __fma_rn(a3.y, z3.y, sy);
+  }
+  for (; k < K2; k += 32) {
+    const double2 a0 = __ldg(a + k);
+    const double2 z0 = z[k];
+    sx = __fma_rn(a0.x, z0.x, sx); sy = __fma_rn(a0.y, z0.y, sy);
+  }
+  double s = sx + sy;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) {
+    wd[j] = s;
+    if (lam != nullptr) lam[j] = d[col0 + j] + s;
+  }
+}
+
+// The reference's stop logic, one thread (solver.cpp:236-249 + BASELINE max-abs rule).
+__global__ void decide_full_kernel(LoopState* st, const double* __restrict__ sums, int k,
+                                   double tol, int max_iter, double div_thr, int rule,
+                                   int ignore_conv, double* trace, double* trace_max) {
+  if (st->done) return;
+  const double diff2 = sums[0], cur2 = sums[1], new2 = sums[2], mx = sums[3];
+  const double step = sqrt(diff2) / sqrt(cur2);
+  st->iterations = k + 1;
+  st->final_step = step;
+  st->final_max_abs = mx;
+  st->sums[0] = diff2;
+  st->sums[1] = cur2;
+  st->sums[2] = new2;
+  st->sums[3] = mx;
+  if (trace) trace[k] = step;
+  if (trace_max) trace_max[k] = mx;
+  const double zn = sqrt(new2);
+  if (!isfinite(zn) || zn > div_thr) {
+    st->status = kDiverged;
+    st->done = 1;
+  } else if (!ignore_conv && (rule == kStopMaxAbs ? (mx < tol) : (step <= tol))) {
+    st->status = kConverged;
+    st->done = 1;
+  } else if (k + 1 >= max_iter) {
+    st->status = kMaxIterations;
+    st->done = 1;
+  }
+}
+
+// ---- complex correctness path (a16): unfused complex epilogue on W planes ----
+struct cd {
+  double re, im;
+};
+__device__ __forceinline__ cd cmul(cd a, cd b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+__device__ __forceinline__ cd csub(cd a, cd b) { return {a.re - b.re, a.im - b.im}; }
+__device__ __forceinline__ cd cadd(cd a, cd b) { return {a.re + b.re, a.im + b.im}; }
+// Scaled complex division (robust like libgcc's __divdc3 for finite inputs).
+__device__ __forceinline__ cd cdiv(cd a, cd b) {
+  if (b.im == 0.0) return {a.re / b.re, a.im / b.re};
+  if (fabs(b.re) >= fabs(b.im)) {
+    const double r = b.im / b.re, den = b.re + b.im * r;
+    return {(a.re + a.im * r) / den, (a.im - a.re * r) / den};
+  }
+  const double r = b.re / b.im, den = b.re * r + b.im;
+  return {(a.re * r + a.im) / den, (a.im * r - a.re) / den};
+}
+
+constexpr int kEpiBlocks = 1184;  // fixed grid => fixed element->block map => deterministic sums
+
+__global__ void complex_map_kernel(const double* __restrict__ Zsrc, int64_t ldz, int64_t ld,
+                                   const double* __restrict__ Wre, const double* __restrict__ Wim,
+                                   const double* __restrict__ wdr, const double* __restrict__ wdi,
+                                   const double* __restrict__ dr, const double* __restrict__ di,
+                                   int64_t n, int64_t ncols, int64_t col0, double* __restrict__ Zdst,
+                                   double* __restrict__ partials, const LoopState* state) {
+  if (state != nullptr && state->done) return;
+  __shared__ double red[8][4];
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  const int64_t total = n * ncols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = e / n, i = e - j * n;
+    const int64_t jg = col0 + j;
+    const cd z{Zsrc[j * ldz + i], Zsrc[j * ldz + ld + i]};
+    cd f;
+    if (i == jg) {
+      f = {1.0, 0.0};
+    } else {
+      const cd w{Wre[j * ld + i], Wim[j * ld + i]};
+      f = cdiv(csub(cmul(z, cd{wdr[j], wdi[j]}), w), csub(cd{dr[i], di[i]}, cd{dr[jg], di[jg]}));
+    }
+    Zdst[j * ldz + i] = f.re;
+    Zdst[j * ldz + ld + i] = f.im;
+    const cd df = csub(f, z);
+    v[0] += df.re * df.re + df.im * df.im;
+    v[1] += z.re * z.re + z.im * z.im;
+    v[2] += f.re * f.re + f.im * f.im;
+    v[3] = nan_max(v[3], hypot(df.re, df.im));
+  }
+  block_reduce4<8>(v, red);
+  if (threadIdx.x == 0) {
+    double* o = partials + size_t(blockIdx.x) * 4;
+    o[0] = v[0]; o[1] = v[1]; o[2] = v[2]; o[3] = v[3];
+  }
+}
+
+__global__ void complex_resid_kernel(const double* __restrict__ Z, int64_t ldz, int64_t ld,
+                                     const double* __restrict__ Wre, const double* __restrict__ Wim,
+                                     const double* __restrict__ lr, const double* __restrict__ li,
+                                     const double* __restrict__ dr, const double* __restrict__ di,
+                                     int64_t n, int64_t ncols, double* __restrict__ partials) {
+  __shared__ double red[8][4];
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  const int64_t total = n * ncols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = e / n, i = e - j * n;
+    const cd z{Z[j * ldz + i], Z[j * ldz + ld + i]};
+    const cd w{Wre[j * ld + i], Wim[j * ld + i]};
+    const cd r = csub(cadd(cmul(cd{dr[i], di[i]}, z), w), cmul(z, cd{lr[j], li[j]}));
+    v[0] += r.re * r.re + r.im * r.im;
+  }
+  block_reduce4<8>(v, red);
+  if (threadIdx.x == 0) {
+    double* o = partials + size_t(blockIdx.x) * 4;
+    o[0] = v[0]; o[1] = 0.0; o[2] = 0.0; o[3] = 0.0;
+  }
+}
+
+__global__ void complex_lambda_kernel(const double* wdr, const double* wdi, const double* dr,
+                                      const double* di, int64_t ncols, int64_t col0, double* lr,
+                                      double* li) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j < ncols) {
+    lr[j] = dr[col0 + j] + wdr[j];
+    li[j] = di[col0 + j] + wdi[j];
+  }
+}
+
+// Warm start renormalisation (solver.cpp:190-201): Z[:, j] /= Z[j, j]; Z[j, j] = 1.
+__global__ void renormalize_columns_kernel(double* Z, int64_t ldz, int64_t ld, int64_t n,
+                                           int64_t ncols, int64_t col0, int cplx) {
+  const int64_t j = blockIdx.x;
+  if (j >= ncols) return;
+  double* zr = Z + j * ldz;
+  const int64_t jg = col0 + j;
+  const cd zjj{zr[jg], cplx ? zr[ld + jg] : 0.0};
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    if (i == jg) continue;
+    if (cplx) {
+      const cd q = cdiv(cd{zr[i], zr[ld + i]}, zjj);
+      zr[i] = q.re;
+      zr[ld + i] = q.im;
+    } else {
+      zr[i] = __ddiv_rn(zr[i], zjj.re);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    zr[jg] = 1.0;
+    if (cplx) zr[ld + jg] = 0.0;
+  }
+}
+
+// --------------------------------------------------------------- host side
+
+namespace {
+
+void launch_diag(FullProblem& P, const double* A, const double* Zsrc, double* out, double* lam,
+                 const double* dvec, const LoopState* st) {
+  const int warps = 8;
+  const unsigned grid = static_cast<unsigned>(ceil_div(P.ncols, warps));
+  if (grid == 0) return;
+  diag_dot_kernel<<<grid, warps * 32, 0, P.ctx->stream>>>(A, P.lda, Zsrc, P.ldz, P.lda, P.ncols,
+                                                           P.col0, out, dvec, lam, st);
+  IPT_LAUNCH_CHECK();
+  count_launch();
+}
+
+GemmParams gemm_params(FullProblem& P, const double* A, const double* Bz, double* C, int64_t ldc) {
+  GemmParams g{};
+  g.K = P.lda;
+  g.A = A;
+  g.lda = P.lda;
+  g.B = Bz;
+  g.ldb = P.ldz;
+  g.C = C;
+  g.ldc = ldc;
+  g.tiles_m = static_cast<int>(ceil_div(P.n, kBM));
+  g.tiles_n = static_cast<int>(ceil_div(P.ncols, kBN));
+  g.d = P.dre.get();
+  g.wd = P.wd.get();
+  g.lam = P.lam.get();
+  g.col0 = P.col0;
+  g.row0 = 0;
+  g.n_rows = P.n;
+  g.n_cols = P.ncols;
+  g.partials = P.partials.get();
+  g.state = P.state;
+  return g;
+}
+
+int64_t num_partials(const FullProblem& P) {
+  return P.cplx ? kEpiBlocks : static_cast<int64_t>(gemm_tiles(P.n, P.ncols));
+}
+
+void allreduce_sums(FullProblem& P, bool with_max) {
+  Ctx& c = *P.ctx;
+  if (c.nranks <= 1) return;
+  IPT_NCCL(ncclAllReduce(P.sums.get(), P.sums.get(), 3, ncclDouble, ncclSum, c.comm, c.stream));
+  if (with_max)
+    IPT_NCCL(ncclAllReduce(P.sums.get() + 3, P.sums.get() + 3, 1, ncclDouble, ncclMax, c.comm, c.stream));
+}
+
+// Enqueue map application number k (reads Z[k&1], writes Z[(k+1)&1]).
+void enqueue_map(FullProblem& P, int k, const ipt_params& prm) {
+  Ctx& c = *P.ctx;
+  const double* zs = P.Z[k & 1].get();
+  double* zd = P.Z[(k + 1) & 1].get();
+  LoopState* st = P.state;
+  if (!P.cplx) {
+    launch_diag(P, P.A1.get(), zs, P.wd.get(), nullptr, nullptr, st);
+    GemmParams g = gemm_params(P, P.A1.get(), zs, zd, P.ldz);
+    launch_gemm(kGemmMap, g, c.stream);
+  } else {
+    launch_diag(P, P.A1.get(), zs, P.wd.get(), nullptr, nullptr, st);
+    launch_diag(P, P.A2.get(), zs, P.wdi.get(), nullptr, nullptr, st);
+    GemmParams g1 = gemm_params(P, P.A1.get(), zs, P.Wre.get(), P.ld);
+    launch_gemm(kGemmStore, g1, c.stream);
+    GemmParams g2 = gemm_params(P, P.A2.get(), zs, P.Wim.get(), P.ld);
+    launch_gemm(kGemmStore, g2, c.stream);
+    complex_map_kernel<<<kEpiBlocks, 256, 0, c.stream>>>(
+        zs, P.ldz, P.ld, P.Wre.get(), P.Wim.get(), P.wd.get(), P.wdi.get(), P.dre.get(),
+        P.dim.get(), P.n, P.ncols, P.col0, zd, P.partials.get(), st);
+    IPT_LAUNCH_CHECK();
+    count_launch();
+  }
+  reduce_partials(c.stream, P.partials.get(), num_partials(P), P.sums.get(), st);
+  allreduce_sums(P, true);
+  decide_full_kernel<<<1, 1, 0, c.stream>>>(
+      st, P.sums.get(), k, prm.tolerance, prm.max_iterations, prm.divergence_threshold,
+      prm.stop_rule, prm.ignore_convergence, prm.record_trace ? P.trace.get() : nullptr,
+      prm.record_trace ? P.trace_max.get() : nullptr);
+  IPT_LAUNCH_CHECK();
+  count_launch();
+}
+
+void upload_rowmajor(cudaStream_t s, double* dst, int64_t dpitch, const double* src, int64_t rows,
+                     int64_t cols, int64_t spitch) {
+  if (rows == 0 || cols == 0) return;
+  IPT_CUDA(cudaMemcpy2DAsync(dst, dpitch * sizeof(double), src, spitch * sizeof(double),
+                             cols * sizeof(double), rows, cudaMemcpyHostToDevice, s));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ C++ entry points
+
+FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_im,
+                         const double* delta_re, const double* delta_im, bool force_complex) {
+  if (n <= 0) throw InvalidArgument("solve_full: empty problem");
+  if (!d_re || !delta_re) throw InvalidArgument("solve_full: null input");
+  auto P = std::make_unique<FullProblem>();
+  P->ctx = &c;
+  P->n = n;
+  P->ld = round_up(n, 16);
+  P->rows_pad = round_up(n, kBM);
+  c.shard(n, P->col0, P->ncols);
+  P->ncols -= P->col0;
+  P->cols_pad = round_up(std::max<int64_t>(P->ncols, 1), kBN);
+  bool any_im = false;
+  if (d_im) for (int64_t i = 0; i < n && !any_im; ++i) any_im = d_im[i] != 0.0;
+  if (delta_im) for (int64_t t = 0; t < n * n && !any_im; ++t) any_im = delta_im[t] != 0.0;
+  P->cplx = any_im || force_complex;
+  P->lda = P->cplx ? 2 * P->ld : P->ld;
+  P->ldz = P->lda;
+  cudaStream_t s = c.stream;
+
+  P->A1.alloc(size_t(P->rows_pad) * P->lda);
+  if (!P->cplx) {
+    upload_rowmajor(s, P->A1.get(), P->lda, delta_re, n, n, n);
+  } else {
+    P->A2.alloc(size_t(P->rows_pad) * P->lda);
+    // A1 = [Dr | -Di], A2 = [Di | Dr]
+    upload_rowmajor(s, P->A1.get(), P->lda, delta_re, n, n, n);
+    upload_rowmajor(s, P->A2.get() + P->ld, P->lda, delta_re, n, n, n);
+    if (delta_im) {
+      upload_rowmajor(s, P->A2.get(), P->lda, delta_im, n, n, n);
+      DevBuf tmp;
+      tmp.alloc(size_t(n) * n, false);
+      IPT_CUDA(cudaMemcpyAsync(tmp.get(), delta_im, sizeof(double) * n * n, cudaMemcpyHostToDevice, s));
+      DevBuf neg;
+      neg.alloc(size_t(n) * n, false);
+      scale_copy(s, tmp.get(), neg.get(), size_t(n) * n, -1.0);
+      IPT_CUDA(cudaMemcpy2DAsync(P->A1.get() + P->ld, P->lda * sizeof(double), neg.get(),
+                                 n * sizeof(double), n * sizeof(double), n,
+                                 cudaMemcpyDeviceToDevice, s));
+      c.sync();
+    }
+  }
+  P->dre.alloc(n);
+  P->dim.alloc(n);
+  IPT_CUDA(cudaMemcpyAsync(P->dre.get(), d_re, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  if (d_im) IPT_CUDA(cudaMemcpyAsync(P->dim.get(), d_im, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  for (auto& z : P->Z) z.alloc(size_t(P->cols_pad) * P->ldz);
+  if (P->cplx) {
+    P->Wre.alloc(size_t(P->cols_pad) * P->ld);
+    P->Wim.alloc(size_t(P->cols_pad) * P->ld);
+  }
+  P->wd.alloc(P->cols_pad);
+  P->wdi.alloc(P->cols_pad);
+  P->lam.alloc(P->cols_pad);
+  P->lami.alloc(P->cols_pad);
+  P->partials.alloc(size_t(std::max<int64_t>(num_partials(*P), 1)) * 4);
+  P->sums.alloc(4);
+  IPT_CUDA(cudaMalloc(&P->state, sizeof(LoopState)));
+  c.sync();
+  return P.release();
+}
+
+void full_free(FullProblem* P) { delete P; }
+
+void full_reset(FullProblem& P, const double* warm_re, const double* warm_im, int max_iter_hint,
+                bool renormalize) {
+  Ctx& c = *P.ctx;
+  cudaStream_t s = c.stream;
+  const int64_t n = P.n;
+  fill_zero(s, P.Z[0].get(), P.Z[0].count);
+  if (warm_re == nullptr) {
+    const unsigned grid = static_cast<unsigned>(ceil_div(P.ncols, 256));
+    if (grid) {
+      identity_columns_kernel<<<grid, 256, 0, s>>>(P.Z[0].get(), P.ldz, P.ncols, P.col0);
+      IPT_LAUNCH_CHECK();
+      count_launch();
+    }
+  } else {
+    // Host row-major n x n -> this rank's column-major block: upload the row-major rows of
+    // the column slice, then transpose on the device.
+    for (int64_t j = 0; j < P.ncols && renormalize; ++j) {
+      const int64_t jg = P.col0 + j;
+      const bool zero = warm_re[jg * n + jg] == 0.0 && (warm_im == nullptr || warm_im[jg * n + jg] == 0.0);
+      if (zero) throw InvalidArgument("solve_full: warm start has zero diagonal entry");
+    }
+    DevBuf rm;
+    rm.alloc(size_t(n) * std::max<int64_t>(P.ncols, 1), false);
+    for (int part = 0; part < (warm_im && P.cplx ? 2 : 1); ++part) {
+      const double* src = part == 0 ? warm_re : warm_im;
+      // rm: n rows x ncols, row-major (ld = ncols)
+      upload_rowmajor(s, rm.get(), P.ncols, src + P.col0, n, P.ncols, n);
+      // row-major (n x ncols) is column-major (ncols x n): transpose into Z (column-major n x ncols)
+      transpose_to_rowmajor(s, rm.get(), P.ncols, P.ncols, n, P.Z[0].get() + (part ? P.ld : 0), P.ldz);
+    }
+    if (renormalize && P.ncols > 0) {
+      renormalize_columns_kernel<<<static_cast<unsigned>(P.ncols), 256, 0, s>>>(
+          P.Z[0].get(), P.ldz, P.ld, n, P.ncols, P.col0, P.cplx ? 1 : 0);
+      IPT_LAUNCH_CHECK();
+      count_launch();
+    }
+    c.sync();
+  }
+  LoopState init{};
+  init.status = kMaxIterations;
+  init.scale_ak = 1.0;
+  IPT_CUDA(cudaMemcpyAsync(P.state, &init, sizeof(LoopState), cudaMemcpyHostToDevice, s));
+  if (P.trace_cap < max_iter_hint) {
+    P.trace.alloc(max_iter_hint);
+    P.trace_max.alloc(max_iter_hint);
+    P.trace_cap = max_iter_hint;
+  }
+  P.enq = 0;
+  P.finalized = false;
+  P.gathered.release();
+}
+
+void full_iterate(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
+  Ctx& c = *P.ctx;
+  if (!(prm.tolerance > 0.0)) throw InvalidArgument("config: tolerance must be positive");
+  if (prm.max_iterations <= 0) throw InvalidArgument("config: max_iterations must be positive");
+  if (!(prm.divergence_threshold > 1.0)) throw InvalidArgument("config: divergence_threshold must exceed 1");
+  if (prm.record_trace && P.trace_cap < prm.max_iterations) {
+    P.trace.alloc(prm.max_iterations);
+    P.trace_max.alloc(prm.max_iterations);
+    P.trace_cap = prm.max_iterations;
+  }
+  // Large problems: one host check per iteration is free next to a >=10 ms GEMM.
+  // Small problems: enqueue several iterations per check; the done flag makes the
+  // surplus launches exit immediately.
+  const int batch = P.n * P.ncols >= (int64_t(2048) * 2048) ? 1 : 16;
+  IPT_CUDA(cudaEventRecord(c.ev[0], c.stream));
+  while (P.enq < prm.max_iterations) {
+    for (int b = 0; b < batch && P.enq < prm.max_iterations; ++b) enqueue_map(P, P.enq++, prm);
+    IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (c.h_state->done) break;
+  }
+  IPT_CUDA(cudaEventRecord(c.ev[1], c.stream));
+  IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  if (stats) {
+    float ms = 0.f;
+    IPT_CUDA(cudaEventElapsedTime(&ms, c.ev[0], c.ev[1]));
+    const LoopState& h = *c.h_state;
+    stats->iterations = h.iterations;
+    stats->status = h.status;
+    stats->final_step = h.final_step;
+    stats->final_max_abs = h.final_max_abs;
+    stats->product_count = h.iterations;
+    stats->ms_loop = ms;
+    if (prm.record_trace && h.iterations > 0) {
+      if (stats->trace)
+        IPT_CUDA(cudaMemcpy(stats->trace, P.trace.get(), sizeof(double) * h.iterations, cudaMemcpyDeviceToHost));
+      if (stats->trace_max_abs)
+        IPT_CUDA(cudaMemcpy(stats->trace_max_abs, P.trace_max.get(), sizeof(double) * h.iterations,
+                            cudaMemcpyDeviceToHost));
+    }
+  }
+}
+
+// Current iterate after the loop: map k wrote Z[(k+1)&1], so after `it` maps it is Z[it & 1].
+static const double* current_z(FullProblem& P) {
+  return P.Z[P.ctx->h_state->iterations & 1].get();
+}
+
+// Closing product: Lambda and |MZ - Z Lambda|_F (solver.cpp:252-270), then the
+// eigenvector gather to rank 0 and sigma_min (solver.cpp:271) on rank 0.
+void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
+  Ctx& c = *P.ctx;
+  cudaStream_t s = c.stream;
+  IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
+  c.sync();
+  const double* z = current_z(P);
+  IPT_CUDA(cudaEventRecord(c.ev[0], s));
+  if (!P.cplx) {
+    launch_diag(P, P.A1.get(), z, P.wd.get(), P.lam.get(), P.dre.get(), nullptr);
+    GemmParams g = gemm_params(P, P.A1.get(), z, nullptr, 0);
+    g.state = nullptr;
+    launch_gemm(kGemmResid, g, s);
+  } else {
+    launch_diag(P, P.A1.get(), z, P.wd.get(), nullptr, nullptr, nullptr);
+    launch_diag(P, P.A2.get(), z, P.wdi.get(), nullptr, nullptr, nullptr);
+    const unsigned gl = static_cast<unsigned>(ceil_div(P.ncols, 256));
+    if (gl) {
+      complex_lambda_kernel<<<gl, 256, 0, s>>>(P.wd.get(), P.wdi.get(), P.dre.get(), P.dim.get(),
+                                               P.ncols, P.col0, P.lam.get(), P.lami.get());
+      IPT_LAUNCH_CHECK();
+      count_launch();
+    }
+    GemmParams g1 = gemm_params(P, P.A1.get(), z, P.Wre.get(), P.ld);
+    g1.state = nullptr;
+    launch_gemm(kGemmStore, g1, s);
+    GemmParams g2 = gemm_params(P, P.A2.get(), z, P.Wim.get(), P.ld);
+    g2.state = nullptr;
+    launch_gemm(kGemmStore, g2, s);
+    complex_resid_kernel<<<kEpiBlocks, 256, 0, s>>>(z, P.ldz, P.ld, P.Wre.get(), P.Wim.get(),
+                                                     P.lam.get(), P.lami.get(), P.dre.get(),
+                                                     P.dim.get(), P.n, P.ncols, P.partials.get());
+    IPT_LAUNCH_CHECK();
+    count_launch();
+  }
+  reduce_partials(s, P.partials.get(), num_partials(P), P.sums.get(), nullptr);
+  allreduce_sums(P, false);
+  double h4[4];
+  IPT_CUDA(cudaMemcpyAsync(h4, P.sums.get(), sizeof(h4), cudaMemcpyDeviceToHost, s));
+  IPT_CUDA(cudaEventRecord(c.ev[1], s));
+  c.sync();
+  float ms_final = 0.f;
+  IPT_CUDA(cudaEventElapsedTime(&ms_final, c.ev[0], c.ev[1]));
+
+  // Gather the column shards on rank 0 (one final eigenvector gather).
+  if (c.nranks > 1) {
+    if (c.rank == 0) P.gathered.alloc(size_t(round_up(P.n, kBN)) * P.ldz);
+    IPT_NCCL(ncclGroupStart());
+    if (c.rank == 0) {
+      for (int r = 0; r < c.nranks; ++r) {
+        const int64_t r0 = P.n * r / c.nranks, r1 = P.n * (r + 1) / c.nranks;
+        if (r1 == r0) continue;
+        double* dst = P.gathered.get() + r0 * P.ldz;
+        if (r == 0)
+          IPT_CUDA(cudaMemcpyAsync(dst, z, sizeof(double) * (r1 - r0) * P.ldz, cudaMemcpyDeviceToDevice, s));
+        else
+          IPT_NCCL(ncclRecv(dst, size_t(r1 - r0) * P.ldz, ncclDouble, r, c.comm, s));
+      }
+    } else if (P.ncols > 0) {
+      IPT_NCCL(ncclSend(z, size_t(P.ncols) * P.ldz, ncclDouble, 0, c.comm, s));
+    }
+    // eigenvalues: each rank's lam block
+    IPT_NCCL(ncclGroupEnd());
+    c.sync();
+  }
+
+  double sig = 0.0;
+  float ms_sigma = 0.f;
+  if (prm.want_sigma_min && c.rank == 0) {
+    const double* zfull = c.nranks > 1 ? P.gathered.get() : z;
+    IPT_CUDA(cudaEventRecord(c.ev[2], s));
+    sig = sigma_min_device(c, P.n, zfull, P.cplx ? zfull + P.ld : nullptr, P.ldz, 50, 1e-4);
+    IPT_CUDA(cudaEventRecord(c.ev[3], s));
+    c.sync();
+    IPT_CUDA(cudaEventElapsedTime(&ms_sigma, c.ev[2], c.ev[3]));
+  }
+  P.finalized = true;
+  if (stats) {
+    stats->residual = std::sqrt(h4[0]);
+    stats->min_singular_value_estimate = sig;
+    stats->product_count = c.h_state->iterations + 1;
+    stats->ms_final = ms_final;
+    stats->ms_sigma = ms_sigma;
+  }
+}
+
+// Z (row-major planar) and eigenvalues to the host; rank 0 receives everything.
+void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, double* lam_im) {
+  Ctx& c = *P.ctx;
+  cudaStream_t s = c.stream;
+  IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
+  c.sync();
+  const int64_t n = P.n;
+  // eigenvalues: gather per-rank blocks (lam computed in finalize)
+  std::vector<double> lr(n, 0.0), li(n, 0.0);
+  if (c.nranks > 1) {
+    DevBuf all_r, all_i;
+    all_r.alloc(n);
+    all_i.alloc(n);
+    IPT_NCCL(ncclGroupStart());
+    if (c.rank == 0) {
+      for (int r = 0; r < c.nranks; ++r) {
+        const int64_t r0 = n * r / c.nranks, r1 = n * (r + 1) / c.nranks;
+        if (r1 == r0) continue;
+        if (r == 0) {
+          IPT_CUDA(cudaMemcpyAsync(all_r.get(), P.lam.get(), sizeof(double) * (r1 - r0), cudaMemcpyDeviceToDevice, s));
+          IPT_CUDA(cudaMemcpyAsync(all_i.get(), P.lami.get(), sizeof(double) * (r1 - r0), cudaMemcpyDeviceToDevice, s));
+        } else {
+          IPT_NCCL(ncclRecv(all_r.get() + r0, r1 - r0, ncclDouble, r, c.comm, s));
+          IPT_NCCL(ncclRecv(all_i.get() + r0, r1 - r0, ncclDouble, r, c.comm, s));
+        }
+      }
+    } else if (P.ncols > 0) {
+      IPT_NCCL(ncclSend(P.lam.get(), P.ncols, ncclDouble, 0, c.comm, s));
+      IPT_NCCL(ncclSend(P.lami.get(), P.ncols, ncclDouble, 0, c.comm, s));
+    }
+    IPT_NCCL(ncclGroupEnd());
+    if (c.rank == 0) {
+      IPT_CUDA(cudaMemcpyAsync(lr.data(), all_r.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+      IPT_CUDA(cudaMemcpyAsync(li.data(), all_i.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    }
+    c.sync();
+  } else {
+    IPT_CUDA(cudaMemcpyAsync(lr.data(), P.lam.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    IPT_CUDA(cudaMemcpyAsync(li.data(), P.lami.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    c.sync();
+  }
+  if (c.rank != 0) return;
+  if (lam_re) std::memcpy(lam_re, lr.data(), sizeof(double) * n);
+  if (lam_im) {
+    if (P.cplx) std::memcpy(lam_im, li.data(), sizeof(double) * n);
+    else std::memset(lam_im, 0, sizeof(double) * n);
+  }
+  const double* zsrc = c.nranks > 1 ? P.gathered.get() : current_z(P);
+  if (zsrc == nullptr) throw InvalidArgument("download: finalize must run before download");
+  DevBuf rm;
+  rm.alloc(size_t(n) * n, false);
+  for (int part = 0; part < 2; ++part) {
+    double* dst = part == 0 ? z_re : z_im;
+    if (dst == nullptr) continue;
+    if (part == 1 && !P.cplx) {
+      std::memset(dst, 0, sizeof(double) * n * n);
+      continue;
+    }
+    transpose_to_rowmajor(s, zsrc + (part ? P.ld : 0), P.ldz, n, n, rm.get(), n);
+    IPT_CUDA(cudaMemcpyAsync(dst, rm.get(), sizeof(double) * n * n, cudaMemcpyDeviceToHost, s));
+    c.sync();
+  }
+}
+
+bool full_is_complex(const FullProblem& P) { return P.cplx; }
+
+void full_local_columns(const FullProblem& P, int64_t* c0, int64_t* c1) {
+  *c0 = P.col0;
+  *c1 = P.col0 + P.ncols;
+}
+
+}  // namespace iptb

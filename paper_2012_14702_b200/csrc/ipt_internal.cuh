@@ -1,0 +1,121 @@
+// Internal host-side structures shared by the IPT CUDA translation units.
+#pragma once
+
+#include <nccl.h>
+
+#include <atomic>
+#include <memory>
+#include <vector>
+
+#include "ipt_common.cuh"
+#include "../../include/ipt_cuda.h"
+
+namespace iptb {
+
+extern std::atomic<int64_t> g_launches;
+inline void count_launch(int64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+inline void nccl_check(ncclResult_t r, const char* what, const char* file, int line) {
+  if (r != ncclSuccess)
+    throw NcclError(std::string("NCCL error ") + ncclGetErrorString(r) + " in " + what + " at " +
+                    file + ":" + std::to_string(line));
+}
+#define IPT_NCCL(x) ::iptb::nccl_check((x), #x, __FILE__, __LINE__)
+
+// Device buffer owned by a problem; freed in the destructor.
+struct DevBuf {
+  double* p = nullptr;
+  size_t count = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void alloc(size_t n, bool zero = true);
+  void release();
+  double* get() const { return p; }
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  LoopState* h_state = nullptr;  // pinned mirror of the device loop state
+  cudaEvent_t ev[4] = {};
+  void sync() { IPT_CUDA(cudaStreamSynchronize(stream)); }
+  // column range of this rank for an n-column sharded operand
+  void shard(int64_t n, int64_t& c0, int64_t& c1) const {
+    c0 = n * rank / nranks;
+    c1 = n * (rank + 1) / nranks;
+  }
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) IPT_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// ---------------- GEMM launch helpers (dmma_gemm.cu) ----------------
+struct GemmParams;
+void launch_gemm(int mode, const GemmParams& p, cudaStream_t s);
+size_t gemm_tiles(int64_t rows, int64_t cols);
+
+// Plain row-major C = A B through the DMMA kernel (host helpers, device pointers).
+// A: m x k row-major (lda), Bt: n x k row-major (= B col-major, ldb), C col-major (ldc).
+// Operands must be zero-padded to 128-row / 16-col tiles.
+void gemm_tn_store(cudaStream_t s, int64_t m, int64_t n, int64_t kpad, const double* A, int64_t lda,
+                   const double* Bt, int64_t ldb, double* C, int64_t ldc);
+
+// ---------------- small device utilities (ipt_util.cu) ----------------
+void transpose_to_rowmajor(cudaStream_t s, const double* src_colmajor, int64_t ld_src, int64_t rows,
+                           int64_t cols, double* dst, int64_t ld_dst, double scale_sign = 1.0);
+void fill_zero(cudaStream_t s, double* p, size_t count);
+void reduce_partials(cudaStream_t s, const double* partials, int64_t count, double* out4,
+                     const LoopState* state);
+void scale_copy(cudaStream_t s, const double* src, double* dst, size_t count, double factor);
+
+// Full-spectrum problem (ipt_full.cu)
+struct FullProblem;
+FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_im,
+                         const double* delta_re, const double* delta_im, bool force_complex = false);
+void full_free(FullProblem* P);
+void full_reset(FullProblem& P, const double* warm_re, const double* warm_im, int max_iter_hint,
+                bool renormalize = true);
+void full_iterate(FullProblem& P, const ipt_params& prm, ipt_stats* stats);
+void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats);
+void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, double* lam_im);
+void full_local_columns(const FullProblem& P, int64_t* c0, int64_t* c1);
+bool full_is_complex(const FullProblem& P);
+
+// Single-pair problem (ipt_single.cu)
+struct SingleProblem;
+SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double* d_im, bool csr,
+                             const double* dense_re, const double* dense_im, const int64_t* rowptr,
+                             const int32_t* cols, const double* val_re, const double* val_im,
+                             bool keep_host_anchor_source, bool force_complex = false);
+void single_free(SingleProblem* P);
+void single_reset(SingleProblem& P, int64_t anchor, const double* warm_re, const double* warm_im,
+                  int max_iter_hint, bool renormalize = true);
+void single_iterate(SingleProblem& P, const ipt_params& prm, ipt_stats* stats);
+void single_finalize(SingleProblem& P, ipt_stats* stats);
+void single_download(SingleProblem& P, double* z_re, double* z_im);
+void single_matvec(SingleProblem& P, const double* x_re, const double* x_im, double* y_re, double* y_im);
+
+// sigma_min (ipt_sigma.cu): Z column-major (ldz), real or complex (zi nullable).
+double sigma_min_device(Ctx& ctx, int64_t n, const double* zr, const double* zi, int64_t ldz,
+                        int max_iters, double tol);
+
+}  // namespace iptb
+
+struct ipt_ctx {
+  iptb::Ctx c;
+};

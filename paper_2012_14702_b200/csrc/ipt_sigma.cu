@@ -1,0 +1,380 @@
+// K6: smallest_singular_value_estimate (proj/src/solver.cpp:275-297) on the device.
+//
+// The reference forms H = Z^H Z, factors it with a serial partial-pivot LU
+// (lu.cpp:10-51) and runs <= 50 steps of inverse power iteration from the
+// fixed start vector deterministic_unit(n) (solver.cpp:95-109), stopping when
+// |u_k| changes by <= tol relative; the estimate is 1/sqrt(|u|).
+//
+// Here: H = Z^T Z through the DMMA GEMM, a blocked right-looking Cholesky
+// (H is symmetric positive definite for a full-rank Z; the reference's
+// "singular" outcome is reproduced by the same pivot threshold
+// max|H| * eps * n), and the same inverse power iteration with two blocked
+// triangular solves per step. The iterates match the reference's to rounding,
+// so the stopping step and the estimate agree. Complex Z uses the real
+// embedding [[Zr, -Zi], [Zi, Zr]], on which the iteration from [v; 0] is the
+// complex iteration from v written in real coordinates.
+#include <cmath>
+#include <vector>
+
+#include "dmma_gemm.cuh"
+#include "ipt_internal.cuh"
+
+namespace iptb {
+
+namespace {
+
+constexpr int NB = 128;          // Cholesky / triangular block
+constexpr int LDS = NB + 1;      // padded smem row
+
+// Factor the b x b diagonal block at (kb, kb) of column-major H in place (lower).
+__global__ void __launch_bounds__(512) potrf_block_kernel(double* H, int64_t ldh, int64_t kb, int b,
+                                                          double tiny, int* singular) {
+  extern __shared__ double S[];  // [NB][LDS], S[r*LDS + c] = H(kb+r, kb+c)
+  const int tid = threadIdx.x;
+  for (int e = tid; e < b * b; e += blockDim.x) {
+    const int c = e / b, r = e % b;
+    S[r * LDS + c] = (r >= c) ? H[(kb + c) * ldh + kb + r] : 0.0;
+  }
+  __syncthreads();
+  __shared__ int bad;
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int c = 0; c < b; ++c) {
+    if (tid == 0) {
+      const double v = S[c * LDS + c];
+      if (!(v > tiny)) {
+        bad = 1;
+        S[c * LDS + c] = 1.0;
+      } else {
+        S[c * LDS + c] = sqrt(v);
+      }
+    }
+    __syncthreads();
+    const double piv = S[c * LDS + c];
+    for (int r = c + 1 + tid; r < b; r += blockDim.x) S[r * LDS + c] = S[r * LDS + c] / piv;
+    __syncthreads();
+    // trailing lower update: rows r > c, cols q in (c, r]
+    const int m = b - c - 1;
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int r = c + 1 + e / m, q = c + 1 + e % m;
+      if (q <= r) S[r * LDS + q] = __fma_rn(-S[r * LDS + c], S[q * LDS + c], S[r * LDS + q]);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < b * b; e += blockDim.x) {
+    const int c = e / b, r = e % b;
+    if (r >= c) H[(kb + c) * ldh + kb + r] = S[r * LDS + c];
+  }
+  if (tid == 0 && bad) atomicExch(singular, 1);
+}
+
+// L21 = H21 L11^{-T}: rows [kb+b, kb+b+rem), 32 rows per CTA staged through smem,
+// 4 rows per warp, x distributed over lanes (x[p] on lane p%32, slot p/32).
+// Writes L21 back into H (column-major) and into the row-major panel P (ld NB,
+// zero-padded to NB columns) used as both operands of the trailing update.
+__global__ void __launch_bounds__(256) trsm_panel_kernel(double* H, int64_t ldh, int64_t kb, int b,
+                                                         int64_t rem, double* P) {
+  extern __shared__ double sm[];
+  double* L = sm;                 // [NB][LDS] lower factor of the diagonal block
+  double* R = sm + NB * LDS;      // [32][LDS] rows of H21
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i0 = int64_t(blockIdx.x) * 32;
+  for (int e = tid; e < b * b; e += blockDim.x) {
+    const int c = e / b, r = e % b;
+    L[r * LDS + c] = (r >= c) ? H[(kb + c) * ldh + kb + r] : 0.0;
+  }
+  for (int e = tid; e < 32 * b; e += blockDim.x) {
+    const int p = e / 32, r = e % 32;
+    const int64_t i = i0 + r;
+    R[r * LDS + p] = (i < rem) ? H[(kb + p) * ldh + kb + b + i] : 0.0;
+  }
+  __syncthreads();
+  for (int rr = 0; rr < 4; ++rr) {
+    const int r = warp * 4 + rr;
+    double x[NB / 32];
+#pragma unroll
+    for (int s = 0; s < NB / 32; ++s) {
+      const int p = s * 32 + lane;
+      x[s] = p < b ? R[r * LDS + p] : 0.0;
+    }
+    // solve x L11^T = h  <=>  L11 x^T = h^T (forward substitution, column oriented)
+    for (int p = 0; p < b; ++p) {
+      const int owner = p & 31, slot = p >> 5;
+      double xp = 0.0;
+#pragma unroll
+      for (int s = 0; s < NB / 32; ++s)
+        if (s == slot) xp = x[s];
+      xp = __shfl_sync(0xffffffffu, xp, owner);
+      xp = xp / L[p * LDS + p];
+#pragma unroll
+      for (int s = 0; s < NB / 32; ++s) {
+        const int q = s * 32 + lane;
+        if (q == p) x[s] = xp;
+        else if (q > p && q < b) x[s] = __fma_rn(-L[q * LDS + p], xp, x[s]);
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < NB / 32; ++s) R[r * LDS + s * 32 + lane] = (s * 32 + lane < b) ? x[s] : 0.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < 32 * NB; e += blockDim.x) {
+    const int r = e / NB, p = e % NB;
+    const int64_t i = i0 + r;
+    if (i < rem) P[i * NB + p] = p < b ? R[r * LDS + p] : 0.0;
+  }
+  for (int e = tid; e < 32 * b; e += blockDim.x) {
+    const int p = e / 32, r = e % 32;
+    const int64_t i = i0 + r;
+    if (i < rem) H[(kb + p) * ldh + kb + b + i] = R[r * LDS + p];
+  }
+}
+
+__global__ void absmax_kernel(const double* __restrict__ H, int64_t ldh, int64_t m, double* out) {
+  __shared__ double red[8][4];
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m * m;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t c = e / m, r = e % m;
+    v[3] = nan_max(v[3], fabs(H[c * ldh + r]));
+  }
+  block_reduce4<8>(v, red);
+  if (threadIdx.x == 0) out[blockIdx.x * 4 + 3] = v[3], out[blockIdx.x * 4 + 0] = 0.0,
+                        out[blockIdx.x * 4 + 1] = 0.0, out[blockIdx.x * 4 + 2] = 0.0;
+}
+
+// Triangular solve pieces on a vector x (in place), L lower in column-major H.
+// diag: x_b <- L_bb^{-1} x_b (forward) or L_bb^{-T} x_b (backward); one CTA.
+__global__ void tri_diag_kernel(const double* __restrict__ H, int64_t ldh, int64_t kb, int b,
+                                double* x, int transpose) {
+  extern __shared__ double L[];  // [NB][LDS]
+  __shared__ double xs[NB];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < b * b; e += blockDim.x) {
+    const int c = e / b, r = e % b;
+    L[r * LDS + c] = (r >= c) ? H[(kb + c) * ldh + kb + r] : 0.0;
+  }
+  for (int p = tid; p < b; p += blockDim.x) xs[p] = x[kb + p];
+  __syncthreads();
+  if (!transpose) {
+    for (int p = 0; p < b; ++p) {
+      if (tid == 0) xs[p] = xs[p] / L[p * LDS + p];
+      __syncthreads();
+      const double xp = xs[p];
+      for (int q = p + 1 + tid; q < b; q += blockDim.x) xs[q] = __fma_rn(-L[q * LDS + p], xp, xs[q]);
+      __syncthreads();
+    }
+  } else {
+    for (int p = b - 1; p >= 0; --p) {
+      if (tid == 0) xs[p] = xs[p] / L[p * LDS + p];
+      __syncthreads();
+      const double xp = xs[p];
+      for (int q = tid; q < p; q += blockDim.x) xs[q] = __fma_rn(-L[p * LDS + q], xp, xs[q]);
+      __syncthreads();
+    }
+  }
+  for (int p = tid; p < b; p += blockDim.x) x[kb + p] = xs[p];
+}
+
+// Forward update: x[r] -= sum_p L[r, kb+p] x[kb+p] for r in [kb+b, m); thread per row.
+__global__ void tri_fwd_update_kernel(const double* __restrict__ H, int64_t ldh, int64_t kb, int b,
+                                      int64_t m, double* x) {
+  __shared__ double xb[NB];
+  for (int p = threadIdx.x; p < b; p += blockDim.x) xb[p] = x[kb + p];
+  __syncthreads();
+  const int64_t r = kb + b + blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (r >= m) return;
+  double s = 0.0;
+  for (int p = 0; p < b; ++p) s = __fma_rn(H[(kb + p) * ldh + r], xb[p], s);
+  x[r] -= s;
+}
+
+// Backward update: x[r] -= sum_p L[kb+p, r] x[kb+p] for r in [0, kb); warp per row.
+__global__ void tri_bwd_update_kernel(const double* __restrict__ H, int64_t ldh, int64_t kb, int b,
+                                      double* x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = blockIdx.x * int64_t(blockDim.x / 32) + (threadIdx.x >> 5);
+  if (r >= kb) return;
+  double s = 0.0;
+  for (int p = lane; p < b; p += 32) s = __fma_rn(H[r * ldh + kb + p], x[kb + p], s);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) x[r] -= s;
+}
+
+__global__ void norm2_kernel(const double* __restrict__ u, int64_t m, double* out) {
+  __shared__ double red[32][4];
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) v[0] = __fma_rn(u[i], u[i], v[0]);
+  block_reduce4<32>(v, red);
+  if (threadIdx.x == 0) out[0] = sqrt(v[0]);
+}
+
+__global__ void normalize_kernel(const double* __restrict__ u, double* __restrict__ v, int64_t m,
+                                 const double* un) {
+  const double s = *un;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
+    v[i] = u[i] / s;
+}
+
+__global__ void embed_complex_kernel(const double* __restrict__ zr, const double* __restrict__ zi,
+                                     int64_t ldz, int64_t n, double* __restrict__ E, int64_t lde) {
+  // E = [[Zr, -Zi], [Zi, Zr]] (2n x 2n), column-major
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n * n;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = e / n, i = e % n;
+    const double a = zr[j * ldz + i], b = zi[j * ldz + i];
+    E[j * lde + i] = a;
+    E[j * lde + n + i] = b;
+    E[(n + j) * lde + i] = -b;
+    E[(n + j) * lde + n + i] = a;
+  }
+}
+
+// Host replica of deterministic_unit (solver.cpp:95-109).
+std::vector<double> deterministic_unit(int64_t n) {
+  std::vector<double> v(n);
+  uint64_t x = 0x243f6a8885a308d3ull;
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    x += 0x9e3779b97f4a7c15ull;
+    uint64_t z = x;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    v[i] = 0.5 + static_cast<double>(z >> 40) / static_cast<double>(1 << 24);
+  }
+  for (int64_t i = 0; i < n; ++i) s += v[i] * v[i];
+  const double nv = std::sqrt(s);
+  for (auto& e : v) e /= nv;
+  return v;
+}
+
+}  // namespace
+
+double sigma_min_device(Ctx& c, int64_t n, const double* zr, const double* zi, int64_t ldz,
+                        int max_iters, double tol) {
+  cudaStream_t s = c.stream;
+  const bool cplx = zi != nullptr;
+  const int64_t m = cplx ? 2 * n : n;
+  const double* Z = zr;
+  int64_t ld = ldz;
+  DevBuf E;
+  if (cplx) {
+    ld = round_up(m, 16);
+    E.alloc(size_t(round_up(m, kBN)) * ld);
+    embed_complex_kernel<<<1184, 256, 0, s>>>(zr, zi, ldz, n, E.get(), ld);
+    IPT_LAUNCH_CHECK();
+    count_launch();
+    Z = E.get();
+  }
+  const int64_t ldh = round_up(m, 16);
+  DevBuf H;
+  H.alloc(size_t(ldh) * m, false);
+  gemm_tn_store(s, m, m, ld, Z, ld, Z, ld, H.get(), ldh);
+
+  DevBuf scratch;
+  scratch.alloc(1184 * 4 + 8);
+  absmax_kernel<<<1184, 256, 0, s>>>(H.get(), ldh, m, scratch.get());
+  IPT_LAUNCH_CHECK();
+  count_launch();
+  reduce_partials(s, scratch.get(), 1184, scratch.get() + 1184 * 4, nullptr);
+  double hmax4[4];
+  IPT_CUDA(cudaMemcpyAsync(hmax4, scratch.get() + 1184 * 4, sizeof(hmax4), cudaMemcpyDeviceToHost, s));
+  c.sync();
+  const double tiny = hmax4[3] * 2.220446049250313e-16 * static_cast<double>(m);
+
+  int* d_sing = nullptr;
+  IPT_CUDA(cudaMalloc(&d_sing, sizeof(int)));
+  IPT_CUDA(cudaMemsetAsync(d_sing, 0, sizeof(int), s));
+  DevBuf Pb;
+  Pb.alloc(size_t(round_up(m, kBM)) * NB);
+  static bool attr = false;
+  if (!attr) {
+    IPT_CUDA(cudaFuncSetAttribute(potrf_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(NB * LDS * sizeof(double))));
+    IPT_CUDA(cudaFuncSetAttribute(trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int((NB + 32) * LDS * sizeof(double))));
+    IPT_CUDA(cudaFuncSetAttribute(tri_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(NB * LDS * sizeof(double))));
+    attr = true;
+  }
+  for (int64_t kb = 0; kb < m; kb += NB) {
+    const int b = static_cast<int>(std::min<int64_t>(NB, m - kb));
+    potrf_block_kernel<<<1, 512, NB * LDS * sizeof(double), s>>>(H.get(), ldh, kb, b, tiny, d_sing);
+    IPT_LAUNCH_CHECK();
+    count_launch();
+    const int64_t rem = m - kb - b;
+    if (rem <= 0) break;
+    trsm_panel_kernel<<<static_cast<unsigned>(ceil_div(rem, 32)), 256, (NB + 32) * LDS * sizeof(double), s>>>(
+        H.get(), ldh, kb, b, rem, Pb.get());
+    IPT_LAUNCH_CHECK();
+    count_launch();
+    GemmParams g{};
+    g.K = NB;
+    g.A = Pb.get();
+    g.lda = NB;
+    g.B = Pb.get();
+    g.ldb = NB;
+    g.C = H.get() + (kb + b) * ldh + (kb + b);
+    g.ldc = ldh;
+    g.tiles_m = static_cast<int>(ceil_div(rem, kBM));
+    g.tiles_n = g.tiles_m;
+    g.n_rows = rem;
+    g.n_cols = rem;
+    launch_gemm(kGemmSub, g, s);
+  }
+  int sing = 0;
+  IPT_CUDA(cudaMemcpyAsync(&sing, d_sing, sizeof(int), cudaMemcpyDeviceToHost, s));
+  c.sync();
+  cudaFree(d_sing);
+  if (sing) return 0.0;
+
+  // inverse power iteration (solver.cpp:283-296)
+  std::vector<double> v0 = deterministic_unit(n);
+  DevBuf v, u, un;
+  v.alloc(m);
+  u.alloc(m);
+  un.alloc(1);
+  IPT_CUDA(cudaMemcpyAsync(v.get(), v0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  double rho = 0.0;
+  for (int it = 0; it < max_iters; ++it) {
+    IPT_CUDA(cudaMemcpyAsync(u.get(), v.get(), sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    for (int64_t kb = 0; kb < m; kb += NB) {  // L y = v
+      const int b = static_cast<int>(std::min<int64_t>(NB, m - kb));
+      tri_diag_kernel<<<1, 256, NB * LDS * sizeof(double), s>>>(H.get(), ldh, kb, b, u.get(), 0);
+      count_launch();
+      const int64_t rem = m - kb - b;
+      if (rem > 0) {
+        tri_fwd_update_kernel<<<static_cast<unsigned>(ceil_div(rem, 256)), 256, 0, s>>>(H.get(), ldh, kb, b, m, u.get());
+        count_launch();
+      }
+    }
+    const int64_t last = (m - 1) / NB * NB;
+    for (int64_t kb = last; kb >= 0; kb -= NB) {  // L^T u = y
+      const int b = static_cast<int>(std::min<int64_t>(NB, m - kb));
+      tri_diag_kernel<<<1, 256, NB * LDS * sizeof(double), s>>>(H.get(), ldh, kb, b, u.get(), 1);
+      count_launch();
+      if (kb > 0) {
+        tri_bwd_update_kernel<<<static_cast<unsigned>(ceil_div(kb, 8)), 256, 0, s>>>(H.get(), ldh, kb, b, u.get());
+        count_launch();
+      }
+    }
+    IPT_LAUNCH_CHECK();
+    norm2_kernel<<<1, 1024, 0, s>>>(u.get(), m, un.get());
+    normalize_kernel<<<296, 256, 0, s>>>(u.get(), v.get(), m, un.get());
+    count_launch(2);
+    IPT_LAUNCH_CHECK();
+    double h_un = 0.0;
+    IPT_CUDA(cudaMemcpyAsync(&h_un, un.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+    c.sync();
+    if (!std::isfinite(h_un) || h_un == 0.0) return 0.0;
+    if (it > 0 && std::fabs(h_un - rho) <= tol * h_un) {
+      rho = h_un;
+      break;
+    }
+    rho = h_un;
+  }
+  return 1.0 / std::sqrt(rho);
+}
+
+}  // namespace iptb

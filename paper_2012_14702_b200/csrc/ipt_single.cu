@@ -1,0 +1,816 @@
+// Single-eigenpair IPT on the device: solve_single / solve_single_continuation /
+// apply_map_single (proj/src/solver.cpp:49-154) and kernels::matvec
+// (proj/src/kernels.cpp:112-140).
+//
+// One iteration = K7/K8 + K9 fused:
+//   anchor pre-pass : w_a = Delta[a, :] . z         (one warp, same summation order as below)
+//   map kernel      : w_i = Delta[i, :] . z (dense GEMV, 16-byte streaming loads, or CSR
+//                     SpMV, 16 lanes per row) and, in registers,
+//                     fz_i = scale * (g_i * (z_i * w_a - w_i)), fz_a = 1, g_i = 1/(d_i - d_a)
+//                     (single_step.hpp:11-17) plus the partial sums of |z-fz|^2, |z|^2, |fz|^2
+//   decide          : fixed-order reduction, rel_step (single_step.hpp:19-26), divergence
+//                     then convergence (solver.cpp:72-80), continuation schedule (:146-152).
+// With a communicator the rows are sharded in equal chunks, every rank keeps row a, and
+// the new iterate is all-gathered in place (one NCCL all-gather + one all-reduce / step).
+//
+// HBM layout: dense Delta row-major, ld = round_up(n,16) (rows of this rank only);
+// CSR int64 row offsets (rebased to the shard), int32 columns, fp64 values;
+// z ping-pong vectors of length nranks*chunk, replicated.
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <memory>
+
+#include "ipt_internal.cuh"
+
+namespace iptb {
+
+struct SingleProblem {
+  Ctx* ctx = nullptr;
+  int64_t n = 0;
+  bool csr = false, cplx = false;
+  int64_t chunk = 0, r0 = 0, r1 = 0;  // rows of this rank
+  // dense
+  DevBuf A, Ai;
+  int64_t lda = 0;
+  // csr
+  std::unique_ptr<int64_t, void (*)(void*)> rowptr{nullptr, [](void* p) { cudaFree(p); }};
+  std::unique_ptr<int32_t, void (*)(void*)> cols{nullptr, [](void* p) { cudaFree(p); }};
+  DevBuf vals, valsi;
+  // anchor row copy (dense: lda doubles; csr: its nonzeros)
+  DevBuf arow, arowi;
+  std::unique_ptr<int32_t, void (*)(void*)> acols{nullptr, [](void* p) { cudaFree(p); }};
+  int64_t annz = 0;
+  int64_t anchor = -1;
+  // host copies needed to (re)build the anchor row for a new anchor
+  std::vector<int64_t> h_rowptr;
+  const int32_t* h_cols = nullptr;
+  const double *h_vals = nullptr, *h_valsi = nullptr, *h_dense = nullptr, *h_densei = nullptr;
+  std::vector<int32_t> h_cols_copy;
+  std::vector<double> h_vals_copy, h_valsi_copy;
+  DevBuf dre, dim;
+  DevBuf z[2], zi[2];
+  DevBuf w, wi;              // complex path / matvec scratch
+  DevBuf wa;                 // anchor value (re, im)
+  DevBuf partials;
+  int64_t npart = 0;
+  DevBuf sums;
+  LoopState* state = nullptr;
+  DevBuf trace;
+  int trace_cap = 0;
+  int enq = 0;
+  ~SingleProblem() {
+    if (state) cudaFree(state);
+  }
+};
+
+namespace {
+
+constexpr int kGemvRows = 4;        // rows per warp (dense)
+constexpr int kGemvWarps = 8;
+constexpr int kRowsPerBlock = kGemvRows * kGemvWarps;
+constexpr int kSpmvLanes = 16;      // lanes per CSR row
+constexpr int kSpmvRowsPerBlock = 256 / kSpmvLanes;
+
+enum MapMode : int { kMvStore = 0, kMvMap = 1, kMvFinal = 2 };
+
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+// Row dot products of R consecutive rows against z (length K2 double2, zero padded),
+// lane-strided with two accumulators per row; the order per row does not depend on R.
+template <int R>
+__device__ __forceinline__ void rows_dot(const double* __restrict__ A, int64_t lda, int nrows,
+                                         const double* __restrict__ z, int64_t K2, double out[R]) {
+  const int lane = threadIdx.x & 31;
+  double ax[R], ay[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) ax[r] = ay[r] = 0.0;
+  const double2* z2 = reinterpret_cast<const double2*>(z);
+  int64_t k = lane;
+  for (; k + 96 < K2; k += 128) {
+    double2 zz[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) zz[u] = z2[k + 32 * u];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (r < nrows) {
+        const double2* a2 = reinterpret_cast<const double2*>(A + r * lda);
+        double2 av[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) av[u] = ld_stream(a2 + k + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ax[r] = __fma_rn(av[u].x, zz[u].x, ax[r]);
+          ay[r] = __fma_rn(av[u].y, zz[u].y, ay[r]);
+        }
+      }
+    }
+  }
+  for (; k < K2; k += 32) {
+    const double2 zz = z2[k];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (r < nrows) {
+        const double2 av = ld_stream(reinterpret_cast<const double2*>(A + r * lda) + k);
+        ax[r] = __fma_rn(av.x, zz.x, ax[r]);
+        ay[r] = __fma_rn(av.y, zz.y, ay[r]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    double s = ax[r] + ay[r];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    out[r] = s;
+  }
+}
+
+// One CSR row over a group of kSpmvLanes lanes (fixed per-lane order + xor tree).
+__device__ __forceinline__ double csr_row_dot(const int32_t* __restrict__ cols,
+                                              const double* __restrict__ vals, int64_t beg,
+                                              int64_t end, const double* __restrict__ z, int sl) {
+  double s = 0.0;
+  for (int64_t p = beg + sl; p < end; p += kSpmvLanes) {
+    int32_t c;
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(c) : "l"(cols + p));
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(vals + p));
+    s = __fma_rn(v, z[c], s);
+  }
+#pragma unroll
+  for (int off = kSpmvLanes / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  return s;
+}
+
+struct MapArgs {
+  const double* d;     // global diagonal
+  const double* z;     // current iterate (global indexing)
+  double* fz;          // next iterate (global indexing) / matvec output
+  const double* wa;    // anchor value
+  int64_t anchor;
+  int64_t row0;        // global index of local row 0
+  int64_t rows;        // local rows
+  const LoopState* state;
+  int schedule;
+  double snap;
+  double* partials;
+};
+
+// Per-row epilogue shared by dense and CSR kernels. Accumulates into v.
+template <int MODE>
+__device__ __forceinline__ void row_epilogue(const MapArgs& a, int64_t i, double w, double scale,
+                                             double lam, double v[4]) {
+  const double zi = a.z[i];
+  if (MODE == kMvStore) {
+    a.fz[i] = w;
+  } else if (MODE == kMvMap) {
+    double f;
+    if (i == a.anchor) {
+      f = 1.0;
+    } else {
+      const double g = __ddiv_rn(1.0, __dsub_rn(a.d[i], a.d[a.anchor]));
+      f = __dmul_rn(scale, __dmul_rn(g, __dsub_rn(__dmul_rn(zi, *a.wa), w)));
+    }
+    a.fz[i] = f;
+    const double df = __dsub_rn(zi, f);
+    v[0] = __fma_rn(df, df, v[0]);
+    v[1] = __fma_rn(zi, zi, v[1]);
+    v[2] = __fma_rn(f, f, v[2]);
+    v[3] = nan_max(v[3], fabs(df));
+  } else {  // kMvFinal: residual |d z + w - lam z|^2 and |z|^2 (solver.cpp:86-91)
+    const double r = __dsub_rn(__dadd_rn(__dmul_rn(a.d[i], zi), w), __dmul_rn(lam, zi));
+    v[0] = __fma_rn(r, r, v[0]);
+    v[1] = __fma_rn(zi, zi, v[1]);
+  }
+}
+
+__device__ __forceinline__ double schedule_scale(const MapArgs& a) {
+  if (a.schedule == IPT_SCHEDULE_PLAIN || a.state == nullptr) return 1.0;
+  const double ak = a.state->scale_ak;
+  return ak <= a.snap ? 1.0 : 1.0 - ak;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kGemvWarps * 32) gemv_map_kernel(const double* __restrict__ A,
+                                                                   int64_t lda, MapArgs a) {
+  if (a.state != nullptr && a.state->done) return;
+  __shared__ double red[kGemvWarps][4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t lr0 = int64_t(blockIdx.x) * kRowsPerBlock + warp * kGemvRows;
+  const int64_t left = a.rows - lr0;
+  const int nrows = left <= 0 ? 0 : (left >= kGemvRows ? kGemvRows : static_cast<int>(left));
+  double w[kGemvRows];
+  if (nrows > 0) rows_dot<kGemvRows>(A + lr0 * lda, lda, nrows, a.z, lda / 2, w);
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  const double scale = MODE == kMvMap ? schedule_scale(a) : 1.0;
+  const double lam = MODE == kMvFinal ? a.d[a.anchor] + *a.wa : 0.0;
+#pragma unroll
+  for (int r = 0; r < kGemvRows; ++r)
+    if (lane == r && r < nrows) row_epilogue<MODE>(a, a.row0 + lr0 + r, w[r], scale, lam, v);
+  if (MODE == kMvStore) return;
+  block_reduce4<kGemvWarps>(v, red);
+  if (threadIdx.x == 0) {
+    double* o = a.partials + size_t(blockIdx.x) * 4;
+    o[0] = v[0]; o[1] = v[1]; o[2] = v[2]; o[3] = v[3];
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) spmv_map_kernel(const int64_t* __restrict__ rowptr,
+                                                       const int32_t* __restrict__ cols,
+                                                       const double* __restrict__ vals, MapArgs a) {
+  if (a.state != nullptr && a.state->done) return;
+  __shared__ double red[8][4];
+  const int sl = threadIdx.x % kSpmvLanes;
+  const int64_t lr = int64_t(blockIdx.x) * kSpmvRowsPerBlock + threadIdx.x / kSpmvLanes;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  const double scale = MODE == kMvMap ? schedule_scale(a) : 1.0;
+  const double lam = MODE == kMvFinal ? a.d[a.anchor] + *a.wa : 0.0;
+  // all lanes of a row group take part in the shuffle even past the end
+  const bool valid = lr < a.rows;
+  const int64_t beg = valid ? rowptr[lr] : 0, end = valid ? rowptr[lr + 1] : 0;
+  const double w = csr_row_dot(cols, vals, beg, end, a.z, sl);
+  if (valid && sl == 0) row_epilogue<MODE>(a, a.row0 + lr, w, scale, lam, v);
+  if (MODE == kMvStore) return;
+  block_reduce4<8>(v, red);
+  if (threadIdx.x == 0) {
+    double* o = a.partials + size_t(blockIdx.x) * 4;
+    o[0] = v[0]; o[1] = v[1]; o[2] = v[2]; o[3] = v[3];
+  }
+}
+
+// w_a with exactly the per-row arithmetic of the map kernels.
+__global__ void anchor_dense_kernel(const double* __restrict__ arow, int64_t lda,
+                                    const double* __restrict__ z, double* wa, const LoopState* st) {
+  if (st != nullptr && st->done) return;
+  double w[1];
+  rows_dot<1>(arow, lda, 1, z, lda / 2, w);
+  if (threadIdx.x == 0) wa[0] = w[0];
+}
+__global__ void anchor_csr_kernel(const int32_t* __restrict__ cols, const double* __restrict__ vals,
+                                  int64_t nnz, const double* __restrict__ z, double* wa,
+                                  const LoopState* st) {
+  if (st != nullptr && st->done) return;
+  const double w = csr_row_dot(cols, vals, 0, nnz, z, threadIdx.x % kSpmvLanes);
+  if (threadIdx.x == 0) wa[0] = w;
+}
+
+__global__ void decide_single_kernel(LoopState* st, const double* __restrict__ sums, int k, double tol,
+                                     int max_iter, double div_thr, int schedule, double alpha,
+                                     double snap, int ignore_conv, double* trace) {
+  if (st->done) return;
+  const double diff2 = sums[0], base2 = sums[1], new2 = sums[2];
+  const double step = sqrt(diff2) / sqrt(base2);
+  st->iterations = k + 1;
+  st->final_step = step;
+  st->final_max_abs = sums[3];
+  if (trace) trace[k] = step;
+  const double ak = st->scale_ak;
+  const bool gate = schedule == IPT_SCHEDULE_PLAIN || ak <= snap;
+  const double zn = sqrt(new2);
+  if (!isfinite(zn) || zn > div_thr) {
+    st->status = kDiverged;
+    st->done = 1;
+  } else if (!ignore_conv && gate && step <= tol) {
+    st->status = kConverged;
+    st->done = 1;
+  } else if (k + 1 >= max_iter) {
+    st->status = kMaxIterations;
+    st->done = 1;
+  }
+  if (schedule == IPT_SCHEDULE_CONTINUATION) st->scale_ak = ak * alpha;
+}
+
+// ---- complex correctness path: generic complex matvec then an elementwise map ----
+__global__ void cmatvec_dense_kernel(const double* __restrict__ Ar, const double* __restrict__ Ai,
+                                     int64_t lda, int64_t rows, int64_t ncols,
+                                     const double* __restrict__ xr, const double* __restrict__ xi,
+                                     double* yr, double* yi, int64_t row0) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = blockIdx.x * int64_t(blockDim.x / 32) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  double sr = 0.0, si = 0.0;
+  for (int64_t j = lane; j < ncols; j += 32) {
+    const double ar = Ar[r * lda + j], ai = Ai ? Ai[r * lda + j] : 0.0;
+    sr += ar * xr[j] - ai * xi[j];
+    si += ar * xi[j] + ai * xr[j];
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    sr += __shfl_xor_sync(0xffffffffu, sr, off);
+    si += __shfl_xor_sync(0xffffffffu, si, off);
+  }
+  if (lane == 0) {
+    yr[row0 + r] = sr;
+    yi[row0 + r] = si;
+  }
+}
+__global__ void cmatvec_csr_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
+                                   const double* __restrict__ vr, const double* __restrict__ vi,
+                                   int64_t rows, const double* __restrict__ xr,
+                                   const double* __restrict__ xi, double* yr, double* yi, int64_t row0) {
+  const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (r >= rows) return;
+  double sr = 0.0, si = 0.0;
+  for (int64_t p = rowptr[r]; p < rowptr[r + 1]; ++p) {
+    const double ar = vr[p], ai = vi ? vi[p] : 0.0;
+    const int32_t c = cols[p];
+    sr += ar * xr[c] - ai * xi[c];
+    si += ar * xi[c] + ai * xr[c];
+  }
+  yr[row0 + r] = sr;
+  yi[row0 + r] = si;
+}
+
+struct cd {
+  double re, im;
+};
+__device__ __forceinline__ cd cmul(cd a, cd b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+__device__ __forceinline__ cd csub(cd a, cd b) { return {a.re - b.re, a.im - b.im}; }
+__device__ __forceinline__ cd cdiv(cd a, cd b) {
+  if (b.im == 0.0) return {a.re / b.re, a.im / b.re};
+  if (fabs(b.re) >= fabs(b.im)) {
+    const double r = b.im / b.re, den = b.re + b.im * r;
+    return {(a.re + a.im * r) / den, (a.im - a.re * r) / den};
+  }
+  const double r = b.re / b.im, den = b.re * r + b.im;
+  return {(a.re * r + a.im) / den, (a.im * r - a.re) / den};
+}
+
+// mode 1: map ; mode 2: final residual. Fixed grid => deterministic partials.
+__global__ void cmap_kernel(int mode, const double* __restrict__ zr, const double* __restrict__ zi,
+                            const double* __restrict__ wr, const double* __restrict__ wi,
+                            const double* __restrict__ dr, const double* __restrict__ di,
+                            int64_t anchor, int64_t row0, int64_t rows, double* fr, double* fi,
+                            const LoopState* st, int schedule, double snap, double* partials) {
+  if (st != nullptr && st->done && mode == 1) return;
+  __shared__ double red[8][4];
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  double scale = 1.0;
+  if (mode == 1 && schedule == IPT_SCHEDULE_CONTINUATION && st) {
+    const double ak = st->scale_ak;
+    scale = ak <= snap ? 1.0 : 1.0 - ak;
+  }
+  const cd wa{wr[anchor], wi[anchor]};
+  const cd da{dr[anchor], di[anchor]};
+  const cd lam{da.re + wa.re, da.im + wa.im};
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < rows; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = row0 + e;
+    const cd z{zr[i], zi[i]}, w{wr[i], wi[i]}, d{dr[i], di[i]};
+    if (mode == 1) {
+      cd f;
+      if (i == anchor) {
+        f = {1.0, 0.0};
+      } else {
+        const cd g = cdiv(cd{1.0, 0.0}, csub(d, da));
+        const cd t = cmul(g, csub(cmul(z, wa), w));
+        f = {scale * t.re, scale * t.im};
+      }
+      fr[i] = f.re;
+      fi[i] = f.im;
+      const cd df = csub(z, f);
+      v[0] += df.re * df.re + df.im * df.im;
+      v[1] += z.re * z.re + z.im * z.im;
+      v[2] += f.re * f.re + f.im * f.im;
+      v[3] = nan_max(v[3], hypot(df.re, df.im));
+    } else {
+      const cd dz = cmul(d, z), lz = cmul(lam, z);
+      const cd r{dz.re + w.re - lz.re, dz.im + w.im - lz.im};
+      v[0] += r.re * r.re + r.im * r.im;
+      v[1] += z.re * z.re + z.im * z.im;
+    }
+  }
+  block_reduce4<8>(v, red);
+  if (threadIdx.x == 0) {
+    double* o = partials + size_t(blockIdx.x) * 4;
+    o[0] = v[0]; o[1] = v[1]; o[2] = v[2]; o[3] = v[3];
+  }
+}
+constexpr int kCmapBlocks = 296;
+
+int64_t map_blocks(const SingleProblem& P) {
+  if (P.cplx) return kCmapBlocks;
+  const int64_t rows = P.r1 - P.r0;
+  return P.csr ? ceil_div(rows, kSpmvRowsPerBlock) : ceil_div(rows, kRowsPerBlock);
+}
+
+MapArgs map_args(SingleProblem& P, int src) {
+  MapArgs a{};
+  a.d = P.dre.get();
+  a.z = P.z[src].get();
+  a.fz = P.z[src ^ 1].get();
+  a.wa = P.wa.get();
+  a.anchor = P.anchor;
+  a.row0 = P.r0;
+  a.rows = P.r1 - P.r0;
+  a.state = P.state;
+  a.partials = P.partials.get();
+  return a;
+}
+
+void enqueue_anchor(SingleProblem& P, int src, const LoopState* st) {
+  cudaStream_t s = P.ctx->stream;
+  if (P.csr) {
+    anchor_csr_kernel<<<1, 32, 0, s>>>(P.acols.get(), P.arow.get(), P.annz, P.z[src].get(),
+                                              P.wa.get(), st);
+  } else {
+    anchor_dense_kernel<<<1, 32, 0, s>>>(P.arow.get(), P.lda, P.z[src].get(), P.wa.get(), st);
+  }
+  IPT_LAUNCH_CHECK();
+  count_launch();
+}
+
+// Complex path: w = Delta z (local rows) into P.w / P.wi (global indexing).
+void enqueue_cmatvec(SingleProblem& P, int src) {
+  cudaStream_t s = P.ctx->stream;
+  const int64_t rows = P.r1 - P.r0;
+  if (rows <= 0) return;
+  if (P.csr) {
+    cmatvec_csr_kernel<<<static_cast<unsigned>(ceil_div(rows, 256)), 256, 0, s>>>(
+        P.rowptr.get(), P.cols.get(), P.vals.get(), P.valsi.count ? P.valsi.get() : nullptr, rows,
+        P.z[src].get(), P.zi[src].get(), P.w.get(), P.wi.get(), P.r0);
+  } else {
+    cmatvec_dense_kernel<<<static_cast<unsigned>(ceil_div(rows, 8)), 256, 0, s>>>(
+        P.A.get(), P.Ai.count ? P.Ai.get() : nullptr, P.lda, rows, P.n, P.z[src].get(),
+        P.zi[src].get(), P.w.get(), P.wi.get(), P.r0);
+  }
+  IPT_LAUNCH_CHECK();
+  count_launch();
+}
+
+void allgather_z(SingleProblem& P, int buf) {
+  Ctx& c = *P.ctx;
+  if (c.nranks <= 1) return;
+  IPT_NCCL(ncclAllGather(P.z[buf].get() + c.rank * P.chunk, P.z[buf].get(), P.chunk, ncclDouble,
+                         c.comm, c.stream));
+  if (P.cplx)
+    IPT_NCCL(ncclAllGather(P.zi[buf].get() + c.rank * P.chunk, P.zi[buf].get(), P.chunk, ncclDouble,
+                           c.comm, c.stream));
+}
+void allgather_w(SingleProblem& P) {
+  Ctx& c = *P.ctx;
+  if (c.nranks <= 1) return;
+  IPT_NCCL(ncclAllGather(P.w.get() + c.rank * P.chunk, P.w.get(), P.chunk, ncclDouble, c.comm, c.stream));
+  IPT_NCCL(ncclAllGather(P.wi.get() + c.rank * P.chunk, P.wi.get(), P.chunk, ncclDouble, c.comm, c.stream));
+}
+
+void reduce_and_allreduce(SingleProblem& P, const LoopState* st, bool with_max) {
+  Ctx& c = *P.ctx;
+  reduce_partials(c.stream, P.partials.get(), map_blocks(P), P.sums.get(), st);
+  if (c.nranks > 1) {
+    IPT_NCCL(ncclAllReduce(P.sums.get(), P.sums.get(), 3, ncclDouble, ncclSum, c.comm, c.stream));
+    if (with_max)
+      IPT_NCCL(ncclAllReduce(P.sums.get() + 3, P.sums.get() + 3, 1, ncclDouble, ncclMax, c.comm, c.stream));
+  }
+}
+
+template <int MODE>
+void enqueue_real_map(SingleProblem& P, int src, const ipt_params* prm) {
+  cudaStream_t s = P.ctx->stream;
+  MapArgs a = map_args(P, src);
+  if (MODE == kMvFinal) a.state = nullptr;
+  if (prm) {
+    a.schedule = prm->schedule;
+    a.snap = 0.25 * prm->tolerance;
+  }
+  const unsigned grid = static_cast<unsigned>(map_blocks(P));
+  if (grid == 0) return;
+  if (P.csr)
+    spmv_map_kernel<MODE><<<grid, 256, 0, s>>>(P.rowptr.get(), P.cols.get(), P.vals.get(), a);
+  else
+    gemv_map_kernel<MODE><<<grid, kGemvWarps * 32, 0, s>>>(P.A.get(), P.lda, a);
+  IPT_LAUNCH_CHECK();
+  count_launch();
+}
+
+void enqueue_iteration(SingleProblem& P, int k, const ipt_params& prm) {
+  Ctx& c = *P.ctx;
+  const int src = k & 1;
+  LoopState* st = P.state;
+  if (!P.cplx) {
+    enqueue_anchor(P, src, st);
+    enqueue_real_map<kMvMap>(P, src, &prm);
+  } else {
+    enqueue_cmatvec(P, src);
+    allgather_w(P);
+    cmap_kernel<<<kCmapBlocks, 256, 0, c.stream>>>(
+        1, P.z[src].get(), P.zi[src].get(), P.w.get(), P.wi.get(), P.dre.get(), P.dim.get(),
+        P.anchor, P.r0, P.r1 - P.r0, P.z[src ^ 1].get(), P.zi[src ^ 1].get(), st, prm.schedule,
+        0.25 * prm.tolerance, P.partials.get());
+    IPT_LAUNCH_CHECK();
+    count_launch();
+  }
+  allgather_z(P, src ^ 1);
+  reduce_and_allreduce(P, st, true);
+  decide_single_kernel<<<1, 1, 0, c.stream>>>(
+      st, P.sums.get(), k, prm.tolerance, prm.max_iterations, prm.divergence_threshold, prm.schedule,
+      prm.shrink_alpha, 0.25 * prm.tolerance, prm.ignore_convergence,
+      prm.record_trace ? P.trace.get() : nullptr);
+  IPT_LAUNCH_CHECK();
+  count_launch();
+}
+
+void upload_anchor_row(SingleProblem& P) {
+  cudaStream_t s = P.ctx->stream;
+  const int64_t a = P.anchor;
+  if (!P.csr) {
+    P.arow.alloc(P.lda);
+    IPT_CUDA(cudaMemcpyAsync(P.arow.get(), P.h_dense + a * P.n, sizeof(double) * P.n, cudaMemcpyHostToDevice, s));
+  } else {
+    const int64_t b = P.h_rowptr[a], e = P.h_rowptr[a + 1];
+    P.annz = e - b;
+    P.arow.alloc(std::max<int64_t>(P.annz, 1));
+    int32_t* ac = nullptr;
+    IPT_CUDA(cudaMalloc(&ac, sizeof(int32_t) * std::max<int64_t>(P.annz, 1)));
+    P.acols.reset(ac);
+    if (P.annz) {
+      IPT_CUDA(cudaMemcpyAsync(P.arow.get(), P.h_vals + b, sizeof(double) * P.annz, cudaMemcpyHostToDevice, s));
+      IPT_CUDA(cudaMemcpyAsync(ac, P.h_cols + b, sizeof(int32_t) * P.annz, cudaMemcpyHostToDevice, s));
+    }
+  }
+  P.ctx->sync();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ C++ entry points
+
+SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double* d_im, bool csr,
+                             const double* dense_re, const double* dense_im, const int64_t* rowptr,
+                             const int32_t* cols, const double* val_re, const double* val_im,
+                             bool keep_host_anchor_source, bool force_complex) {
+  if (n <= 0) throw InvalidArgument("solve_single: empty problem");
+  auto P = std::make_unique<SingleProblem>();
+  P->ctx = &c;
+  P->n = n;
+  P->csr = csr;
+  bool any_im = false;
+  if (d_im) for (int64_t i = 0; i < n && !any_im; ++i) any_im = d_im[i] != 0.0;
+  if (!csr && dense_im) for (int64_t t = 0; t < n * n && !any_im; ++t) any_im = dense_im[t] != 0.0;
+  if (csr && val_im) for (int64_t t = 0; t < rowptr[n] && !any_im; ++t) any_im = val_im[t] != 0.0;
+  P->cplx = any_im || force_complex;
+  P->chunk = ceil_div(n, c.nranks);
+  P->r0 = std::min<int64_t>(n, c.rank * P->chunk);
+  P->r1 = std::min<int64_t>(n, (c.rank + 1) * P->chunk);
+  const int64_t rows = P->r1 - P->r0;
+  const int64_t vlen = P->chunk * c.nranks;
+  cudaStream_t s = c.stream;
+  if (!csr) {
+    P->lda = round_up(n, 16);
+    P->A.alloc(size_t(std::max<int64_t>(rows, 1)) * P->lda);
+    if (rows)
+      IPT_CUDA(cudaMemcpy2DAsync(P->A.get(), P->lda * sizeof(double), dense_re + P->r0 * n,
+                                 n * sizeof(double), n * sizeof(double), rows, cudaMemcpyHostToDevice, s));
+    if (P->cplx && dense_im) {
+      P->Ai.alloc(size_t(std::max<int64_t>(rows, 1)) * P->lda);
+      if (rows)
+        IPT_CUDA(cudaMemcpy2DAsync(P->Ai.get(), P->lda * sizeof(double), dense_im + P->r0 * n,
+                                   n * sizeof(double), n * sizeof(double), rows, cudaMemcpyHostToDevice, s));
+    }
+    P->h_dense = dense_re;
+    P->h_densei = dense_im;
+  } else {
+    for (int64_t i = 0; i < n; ++i)
+      if (rowptr[i + 1] < rowptr[i]) throw InvalidArgument("csr: row offsets must be non-decreasing");
+    const int64_t b = rowptr[P->r0], e = rowptr[P->r1];
+    const int64_t nnz = e - b;
+    std::vector<int64_t> rp(rows + 1);
+    for (int64_t i = 0; i <= rows; ++i) rp[i] = rowptr[P->r0 + i] - b;
+    int64_t* drp = nullptr;
+    IPT_CUDA(cudaMalloc(&drp, sizeof(int64_t) * (rows + 1)));
+    P->rowptr.reset(drp);
+    IPT_CUDA(cudaMemcpyAsync(drp, rp.data(), sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice, s));
+    int32_t* dc = nullptr;
+    IPT_CUDA(cudaMalloc(&dc, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+    P->cols.reset(dc);
+    P->vals.alloc(std::max<int64_t>(nnz, 1), false);
+    if (nnz) {
+      IPT_CUDA(cudaMemcpyAsync(dc, cols + b, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
+      IPT_CUDA(cudaMemcpyAsync(P->vals.get(), val_re + b, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+    }
+    if (P->cplx && val_im) {
+      P->valsi.alloc(std::max<int64_t>(nnz, 1), false);
+      if (nnz) IPT_CUDA(cudaMemcpyAsync(P->valsi.get(), val_im + b, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+    }
+    P->h_rowptr.assign(rowptr, rowptr + n + 1);
+    if (keep_host_anchor_source) {
+      P->h_cols = cols;
+      P->h_vals = val_re;
+      P->h_valsi = val_im;
+    } else {
+      P->h_cols_copy.assign(cols, cols + rowptr[n]);
+      P->h_vals_copy.assign(val_re, val_re + rowptr[n]);
+      P->h_cols = P->h_cols_copy.data();
+      P->h_vals = P->h_vals_copy.data();
+    }
+  }
+  P->dre.alloc(n);
+  P->dim.alloc(n);
+  IPT_CUDA(cudaMemcpyAsync(P->dre.get(), d_re, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  if (d_im) IPT_CUDA(cudaMemcpyAsync(P->dim.get(), d_im, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  // z vectors padded to a multiple of 2 for the 16-byte GEMV loads (pad stays zero)
+  const int64_t zlen = round_up(std::max(vlen, P->lda), 16);
+  for (int b2 = 0; b2 < 2; ++b2) {
+    P->z[b2].alloc(zlen);
+    P->zi[b2].alloc(zlen);
+  }
+  P->w.alloc(zlen);
+  P->wi.alloc(zlen);
+  P->wa.alloc(2);
+  P->npart = std::max<int64_t>(map_blocks(*P), 1);
+  P->partials.alloc(size_t(P->npart) * 4);
+  P->sums.alloc(4);
+  IPT_CUDA(cudaMalloc(&P->state, sizeof(LoopState)));
+  c.sync();
+  return P.release();
+}
+
+void single_free(SingleProblem* P) { delete P; }
+
+void single_reset(SingleProblem& P, int64_t anchor, const double* warm_re, const double* warm_im,
+                  int max_iter_hint, bool renormalize) {
+  Ctx& c = *P.ctx;
+  cudaStream_t s = c.stream;
+  if (anchor < 0 || anchor >= P.n) throw InvalidArgument("solver: anchor out of range");
+  if (anchor != P.anchor) {
+    P.anchor = anchor;
+    if (!P.cplx) upload_anchor_row(P);
+  }
+  const int64_t n = P.n;
+  std::vector<double> zr(n, 0.0), zi(n, 0.0);
+  if (warm_re == nullptr) {
+    zr[anchor] = 1.0;
+  } else if (!renormalize) {
+    for (int64_t j = 0; j < n; ++j) {
+      zr[j] = warm_re[j];
+      zi[j] = warm_im ? warm_im[j] : 0.0;
+    }
+  } else {
+    const double ar = warm_re[anchor], ai = warm_im ? warm_im[anchor] : 0.0;
+    if (ar == 0.0 && ai == 0.0) throw InvalidArgument("solver: warm start has zero anchor coordinate");
+    if (!P.cplx && (warm_im == nullptr || ai == 0.0)) {
+      for (int64_t j = 0; j < n; ++j) zr[j] = warm_re[j] / ar;
+      if (warm_im) for (int64_t j = 0; j < n; ++j) zi[j] = warm_im[j] / ar;
+    } else {
+      const double den = ar * ar + ai * ai;  // (x + iy) / (ar + i ai)
+      for (int64_t j = 0; j < n; ++j) {
+        const double x = warm_re[j], y = warm_im ? warm_im[j] : 0.0;
+        const std::complex<double> q = std::complex<double>(x, y) / std::complex<double>(ar, ai);
+        zr[j] = q.real();
+        zi[j] = q.imag();
+        (void)den;
+      }
+    }
+    zr[anchor] = 1.0;
+    zi[anchor] = 0.0;
+    bool im_nonzero = false;
+    for (int64_t j = 0; j < n && !im_nonzero; ++j) im_nonzero = zi[j] != 0.0;
+    if (im_nonzero && !P.cplx) throw InvalidArgument("solver: complex warm start on a real problem");
+  }
+  fill_zero(s, P.z[0].get(), P.z[0].count);
+  fill_zero(s, P.z[1].get(), P.z[1].count);
+  fill_zero(s, P.zi[0].get(), P.zi[0].count);
+  fill_zero(s, P.zi[1].get(), P.zi[1].count);
+  IPT_CUDA(cudaMemcpyAsync(P.z[0].get(), zr.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  IPT_CUDA(cudaMemcpyAsync(P.zi[0].get(), zi.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  LoopState init{};
+  init.status = kMaxIterations;
+  init.scale_ak = 1.0;
+  IPT_CUDA(cudaMemcpyAsync(P.state, &init, sizeof(LoopState), cudaMemcpyHostToDevice, s));
+  if (P.trace_cap < max_iter_hint) {
+    P.trace.alloc(max_iter_hint);
+    P.trace_cap = max_iter_hint;
+  }
+  P.enq = 0;
+  c.sync();
+}
+
+void single_iterate(SingleProblem& P, const ipt_params& prm, ipt_stats* stats) {
+  Ctx& c = *P.ctx;
+  if (!(prm.tolerance > 0.0)) throw InvalidArgument("config: tolerance must be positive");
+  if (prm.max_iterations <= 0) throw InvalidArgument("config: max_iterations must be positive");
+  if (!(prm.divergence_threshold > 1.0)) throw InvalidArgument("config: divergence_threshold must exceed 1");
+  if (prm.schedule == IPT_SCHEDULE_CONTINUATION && !(prm.shrink_alpha >= 0.0 && prm.shrink_alpha < 1.0))
+    throw InvalidArgument("continuation: shrink factor must lie in [0, 1)");
+  if (P.anchor < 0) throw InvalidArgument("single: reset() must set an anchor first");
+  if (prm.record_trace && P.trace_cap < prm.max_iterations) {
+    P.trace.alloc(prm.max_iterations);
+    P.trace_cap = prm.max_iterations;
+  }
+  // Iterations are enqueued in batches between host checks; iterations past the
+  // decision exit at their first instruction (LoopState::done).
+  const int64_t bytes_per_it = P.csr ? (P.h_rowptr.empty() ? 0 : P.h_rowptr.back() * 12) : P.n * P.n * 8;
+  const int batch = bytes_per_it >= (int64_t(1) << 31) ? 2 : 32;
+  IPT_CUDA(cudaEventRecord(c.ev[0], c.stream));
+  while (P.enq < prm.max_iterations) {
+    for (int b = 0; b < batch && P.enq < prm.max_iterations; ++b) enqueue_iteration(P, P.enq++, prm);
+    IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (c.h_state->done) break;
+  }
+  IPT_CUDA(cudaEventRecord(c.ev[1], c.stream));
+  IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  if (stats) {
+    float ms = 0.f;
+    IPT_CUDA(cudaEventElapsedTime(&ms, c.ev[0], c.ev[1]));
+    const LoopState& h = *c.h_state;
+    stats->iterations = h.iterations;
+    stats->status = h.status;
+    stats->final_step = h.final_step;
+    stats->final_max_abs = h.final_max_abs;
+    stats->product_count = h.iterations;
+    stats->ms_loop = ms;
+    if (prm.record_trace && stats->trace && h.iterations > 0)
+      IPT_CUDA(cudaMemcpy(stats->trace, P.trace.get(), sizeof(double) * h.iterations, cudaMemcpyDeviceToHost));
+  }
+}
+
+// Post-loop product, eigenvalue lambda = d_a + (Delta z)_a and residual (solver.cpp:83-91).
+void single_finalize(SingleProblem& P, ipt_stats* stats) {
+  Ctx& c = *P.ctx;
+  cudaStream_t s = c.stream;
+  IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
+  c.sync();
+  const int cur = c.h_state->iterations & 1;
+  IPT_CUDA(cudaEventRecord(c.ev[0], s));
+  double wa[2] = {0.0, 0.0};
+  if (!P.cplx) {
+    enqueue_anchor(P, cur, nullptr);
+    enqueue_real_map<kMvFinal>(P, cur, nullptr);
+    IPT_CUDA(cudaMemcpyAsync(wa, P.wa.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+  } else {
+    enqueue_cmatvec(P, cur);
+    allgather_w(P);
+    cmap_kernel<<<kCmapBlocks, 256, 0, s>>>(2, P.z[cur].get(), P.zi[cur].get(), P.w.get(), P.wi.get(),
+                                            P.dre.get(), P.dim.get(), P.anchor, P.r0, P.r1 - P.r0,
+                                            nullptr, nullptr, nullptr, 0, 0.0, P.partials.get());
+    IPT_LAUNCH_CHECK();
+    count_launch();
+    IPT_CUDA(cudaMemcpyAsync(wa, P.w.get() + P.anchor, sizeof(double), cudaMemcpyDeviceToHost, s));
+    IPT_CUDA(cudaMemcpyAsync(wa + 1, P.wi.get() + P.anchor, sizeof(double), cudaMemcpyDeviceToHost, s));
+  }
+  reduce_and_allreduce(P, nullptr, false);
+  double h4[4];
+  IPT_CUDA(cudaMemcpyAsync(h4, P.sums.get(), sizeof(h4), cudaMemcpyDeviceToHost, s));
+  IPT_CUDA(cudaEventRecord(c.ev[1], s));
+  c.sync();
+  if (stats) {
+    float ms = 0.f;
+    IPT_CUDA(cudaEventElapsedTime(&ms, c.ev[0], c.ev[1]));
+    std::vector<double> dr(1), di(1);
+    IPT_CUDA(cudaMemcpy(dr.data(), P.dre.get() + P.anchor, sizeof(double), cudaMemcpyDeviceToHost));
+    IPT_CUDA(cudaMemcpy(di.data(), P.dim.get() + P.anchor, sizeof(double), cudaMemcpyDeviceToHost));
+    stats->eigenvalue_re = dr[0] + wa[0];
+    stats->eigenvalue_im = P.cplx ? di[0] + wa[1] : 0.0;
+    stats->residual = std::sqrt(h4[0]) / std::sqrt(h4[1]);
+    stats->product_count = c.h_state->iterations + 1;
+    stats->ms_final = ms;
+  }
+}
+
+void single_download(SingleProblem& P, double* z_re, double* z_im) {
+  Ctx& c = *P.ctx;
+  const int cur = c.h_state->iterations & 1;
+  if (z_re) IPT_CUDA(cudaMemcpy(z_re, P.z[cur].get(), sizeof(double) * P.n, cudaMemcpyDeviceToHost));
+  if (z_im) {
+    if (P.cplx) IPT_CUDA(cudaMemcpy(z_im, P.zi[cur].get(), sizeof(double) * P.n, cudaMemcpyDeviceToHost));
+    else std::memset(z_im, 0, sizeof(double) * P.n);
+  }
+}
+
+// kernels::matvec on device-resident data: y = Delta x (one pass, no epilogue).
+void single_matvec(SingleProblem& P, const double* x_re, const double* x_im, double* y_re, double* y_im) {
+  Ctx& c = *P.ctx;
+  cudaStream_t s = c.stream;
+  const int64_t n = P.n;
+  IPT_CUDA(cudaMemcpyAsync(P.z[0].get(), x_re, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  if (x_im) IPT_CUDA(cudaMemcpyAsync(P.zi[0].get(), x_im, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  else fill_zero(s, P.zi[0].get(), n);
+  if (!P.cplx && (x_im == nullptr)) {
+    MapArgs a = map_args(P, 0);
+    a.state = nullptr;
+    a.fz = P.w.get();
+    const unsigned grid = static_cast<unsigned>(map_blocks(P));
+    if (grid) {
+      if (P.csr) spmv_map_kernel<kMvStore><<<grid, 256, 0, s>>>(P.rowptr.get(), P.cols.get(), P.vals.get(), a);
+      else gemv_map_kernel<kMvStore><<<grid, kGemvWarps * 32, 0, s>>>(P.A.get(), P.lda, a);
+      IPT_LAUNCH_CHECK();
+      count_launch();
+    }
+    fill_zero(s, P.wi.get(), n);
+  } else {
+    enqueue_cmatvec(P, 0);
+  }
+  if (c.nranks > 1) allgather_w(P);
+  IPT_CUDA(cudaMemcpyAsync(y_re, P.w.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  if (y_im) IPT_CUDA(cudaMemcpyAsync(y_im, P.wi.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  c.sync();
+}
+
+}  // namespace iptb

@@ -1,0 +1,594 @@
+"""Python host mirror of the reference's solver API (proj/include/ipt/*.hpp).
+
+Same names, argument meaning and error behaviour as the C++ library, backed by
+the B200 kernels through the C ABI (include/ipt_cuda.h). Matrices are numpy
+arrays (dense, row-major as ComplexMatrix stores them, complex_matrix.hpp:48) or
+`CsrMatrix`. Real inputs run the real fp64 fast path and return real arrays;
+complex inputs return complex128.
+
+Reference map:
+  IterationConfig / SolveStatus / results ... solver.hpp:10-52
+  partition / InverseGaps / build_gaps ...... partition.hpp:15-52, partition.cpp:16-94
+  apply_map_single / solve_single ........... solver.cpp:122-136 (run_single :49-93)
+  apply_map_full / solve_full ............... solver.cpp:156-273
+  solve_single_continuation ................. solver.cpp:138-154
+  smallest_singular_value_estimate .......... solver.cpp:275-297
+  kernels.matmul / kernels.matvec ........... kernels.cpp:112-181
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import sys
+import threading
+from dataclasses import dataclass, field
+from typing import Optional, Union
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, dptr, i32ptr, i64ptr
+
+EPS = sys.float_info.epsilon
+
+
+class SolveStatus(enum.IntEnum):
+    Converged = 0
+    MaxIterations = 1
+    Diverged = 2
+
+
+def to_string(s: SolveStatus) -> str:
+    return {0: "converged", 1: "max_iterations", 2: "diverged"}.get(int(s), "unknown")
+
+
+@dataclass
+class IterationConfig:
+    tolerance: float = 100.0 * EPS
+    max_iterations: int = 1000
+    divergence_threshold: float = 1e8
+    record_trace: bool = False
+    residual_tolerance: float = 1e-8
+    # B200 extension: "rel_fro" (reference, solver.cpp:236) or "max_abs" (BASELINE.json configs)
+    stop_rule: str = "rel_fro"
+
+
+def _validate(cfg: IterationConfig) -> None:  # solver.cpp:18-23
+    if not (cfg.tolerance > 0.0):
+        raise ValueError("config: tolerance must be positive")
+    if cfg.max_iterations <= 0:
+        raise ValueError("config: max_iterations must be positive")
+    if not (cfg.divergence_threshold > 1.0):
+        raise ValueError("config: divergence_threshold must exceed 1")
+
+
+def _params(cfg: IterationConfig, **kw) -> _lib.Params:
+    p = _lib.default_params()
+    p.tolerance = cfg.tolerance
+    p.max_iterations = cfg.max_iterations
+    p.divergence_threshold = cfg.divergence_threshold
+    p.record_trace = 1 if cfg.record_trace else 0
+    p.stop_rule = _lib.STOP_MAX_ABS if cfg.stop_rule == "max_abs" else _lib.STOP_REL_FRO
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p
+
+
+# ----------------------------------------------------------------- matrices
+
+
+class CsrMatrix:
+    """Compressed sparse rows (complex_matrix.hpp:23-76): sorted columns, no
+    explicit zeros, duplicates rejected. Indices are int64 offsets / int32 columns
+    (the device layout); values float64 or complex128."""
+
+    def __init__(self, n_rows: int, n_cols: int, row_offsets, col_indices, values):
+        self.shape = (int(n_rows), int(n_cols))
+        self.row_offsets = np.ascontiguousarray(row_offsets, dtype=np.int64)
+        self.col_indices = np.ascontiguousarray(col_indices, dtype=np.int32)
+        self.values = np.ascontiguousarray(values)
+        if self.row_offsets.shape != (n_rows + 1,):
+            raise ValueError("csr: row_offsets must have n_rows + 1 entries")
+        if self.col_indices.shape != self.values.shape:
+            raise ValueError("csr: column and value counts differ")
+
+    @staticmethod
+    def from_triplets(n_rows: int, n_cols: int, rows, cols, values) -> "CsrMatrix":
+        """sparse_from_triplets (complex_matrix.cpp:39-69)."""
+        rows = np.asarray(rows, dtype=np.int64)
+        cols = np.asarray(cols, dtype=np.int64)
+        values = np.asarray(values)
+        if rows.size and (rows.min() < 0 or rows.max() >= n_rows or cols.min() < 0 or cols.max() >= n_cols):
+            raise ValueError("sparse_from_triplets: index out of bounds")
+        order = np.lexsort((cols, rows))
+        rows, cols, values = rows[order], cols[order], values[order]
+        if rows.size > 1 and np.any((rows[1:] == rows[:-1]) & (cols[1:] == cols[:-1])):
+            raise ValueError("sparse_from_triplets: duplicate entry")
+        keep = values != 0
+        rows, cols, values = rows[keep], cols[keep], values[keep]
+        off = np.zeros(n_rows + 1, dtype=np.int64)
+        np.add.at(off, rows + 1, 1)
+        return CsrMatrix(n_rows, n_cols, np.cumsum(off), cols.astype(np.int32), values)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.values.size)
+
+    def to_dense(self) -> np.ndarray:
+        out = np.zeros(self.shape, dtype=self.values.dtype)
+        r = np.repeat(np.arange(self.shape[0]), np.diff(self.row_offsets))
+        out[r, self.col_indices] = self.values
+        return out
+
+    def is_complex(self) -> bool:
+        return np.iscomplexobj(self.values) and bool(np.any(self.values.imag != 0))
+
+
+Matrix = Union[np.ndarray, CsrMatrix]
+
+
+@dataclass
+class Partition:
+    """M = diag(d) + delta (partition.hpp:15-20)."""
+
+    d: np.ndarray
+    delta: Matrix
+
+    def size(self) -> int:
+        return int(np.asarray(self.d).shape[0])
+
+
+class DegenerateDiagonal(RuntimeError):
+    """partition.hpp:22-26: two diagonal entries closer than the tolerance."""
+
+    def __init__(self, i: int, j: int, gap: float, tol: float):
+        super().__init__(f"degenerate diagonal: |d[{i}] - d[{j}]| = {gap:.6f} <= tolerance {tol:.6f}")
+        self.i, self.j, self.gap, self.tol = i, j, gap, tol
+
+
+class InverseGaps:
+    """G_jk = 1/(d_j - d_k), zero diagonal, generated on demand (partition.hpp:33-52).
+    Construction sweeps the real-part-sorted diagonal for pairs within the
+    tolerance (partition.cpp:54-75); on the device G is never stored."""
+
+    def __init__(self, d, degeneracy_tol: float):
+        self._d = np.asarray(d)
+        self._tol = float(degeneracy_tol)
+        dc = self._d.astype(np.complex128)
+        order = np.lexsort((dc.imag, dc.real))
+        re = dc.real[order]
+        n = dc.shape[0]
+        for a in range(n):
+            b = a + 1
+            while b < n and re[b] - re[a] <= self._tol:
+                gap = abs(dc[order[a]] - dc[order[b]])
+                if gap <= self._tol:
+                    i, j = sorted((int(order[a]), int(order[b])))
+                    raise DegenerateDiagonal(i, j, gap, self._tol)
+                b += 1
+
+    def size(self) -> int:
+        return int(self._d.shape[0])
+
+    def diagonal(self) -> np.ndarray:
+        return self._d
+
+    def degeneracy_tolerance(self) -> float:
+        return self._tol
+
+    def entry(self, j: int, k: int):
+        return 0.0 if j == k else 1.0 / (self._d[j] - self._d[k])
+
+    def column(self, i: int) -> np.ndarray:
+        with np.errstate(divide="ignore"):
+            g = 1.0 / (self._d - self._d[i])
+        g[i] = 0.0
+        return g
+
+    def to_matrix(self) -> np.ndarray:
+        d = self._d
+        with np.errstate(divide="ignore"):
+            g = 1.0 / (d[:, None] - d[None, :])
+        np.fill_diagonal(g, 0.0)
+        return g
+
+
+def partition(m: Matrix) -> Partition:
+    """partition.cpp:16-46."""
+    if isinstance(m, CsrMatrix):
+        n = m.shape[0]
+        if m.shape[0] != m.shape[1]:
+            raise ValueError("partition: matrix must be square")
+        rows = np.repeat(np.arange(n), np.diff(m.row_offsets))
+        diag = rows == m.col_indices
+        d = np.zeros(n, dtype=m.values.dtype)
+        d[rows[diag]] = m.values[diag]
+        off = ~diag
+        return Partition(d, CsrMatrix.from_triplets(n, n, rows[off], m.col_indices[off], m.values[off]))
+    m = np.asarray(m)
+    if m.ndim != 2 or m.shape[0] != m.shape[1]:
+        raise ValueError("partition: matrix must be square")
+    delta = np.array(m, copy=True)
+    d = np.diag(m).copy()
+    np.fill_diagonal(delta, 0)
+    return Partition(d, delta)
+
+
+def reconstruct(p: Partition) -> np.ndarray:
+    m = p.delta.to_dense() if isinstance(p.delta, CsrMatrix) else np.array(p.delta, copy=True)
+    m = m.astype(np.result_type(m.dtype, np.asarray(p.d).dtype))
+    m[np.diag_indices(p.size())] += p.d
+    return m
+
+
+def build_gaps(p: Partition, degeneracy_tol: float = -1.0) -> InverseGaps:
+    """partition.cpp:91-94: a negative tolerance selects 1e-12 * max|d|."""
+    if degeneracy_tol < 0.0:
+        degeneracy_tol = 1e-12 * (float(np.max(np.abs(p.d))) if p.size() else 0.0)
+    return InverseGaps(p.d, degeneracy_tol)
+
+
+# ----------------------------------------------------------------- results
+
+
+@dataclass
+class EigenpairResult:
+    z: np.ndarray = None
+    eigenvalue: complex = 0.0
+    anchor: int = 0
+    iterations: int = 0
+    final_step: float = 0.0
+    residual: float = 0.0
+    status: SolveStatus = SolveStatus.MaxIterations
+    trace: list = field(default_factory=list)
+    matvec_count: int = 0
+    timings_ms: dict = field(default_factory=dict)
+
+
+@dataclass
+class SpectrumResult:
+    Z: np.ndarray = None
+    eigenvalues: np.ndarray = None
+    iterations: int = 0
+    final_step: float = 0.0
+    residual_frobenius: float = 0.0
+    min_singular_value_estimate: float = 0.0
+    status: SolveStatus = SolveStatus.MaxIterations
+    trace: list = field(default_factory=list)
+    matmul_count: int = 0
+    final_max_abs: float = 0.0
+    trace_max_abs: list = field(default_factory=list)
+    timings_ms: dict = field(default_factory=dict)
+
+
+# ----------------------------------------------------------------- device context
+
+
+class Context:
+    """One CUDA device + stream (+ optional NCCL communicator) of the C ABI."""
+
+    def __init__(self, device: int = 0):
+        lib = _lib.load()
+        h = C.c_void_p()
+        check(lib.ipt_ctx_create(int(device), C.byref(h)))
+        self.handle = h
+        self.device = device
+        self.rank, self.nranks = 0, 1
+
+    def init_comm(self, unique_id: bytes, rank: int, nranks: int) -> None:
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        check(_lib.load().ipt_ctx_init_comm(self.handle, buf, int(rank), int(nranks)))
+        self.rank, self.nranks = rank, nranks
+
+    def synchronize(self) -> None:
+        check(_lib.load().ipt_ctx_synchronize(self.handle))
+
+    def close(self) -> None:
+        if self.handle:
+            _lib.load().ipt_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_tls = threading.local()
+
+
+def default_context(device: int = 0) -> Context:
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    if device not in ctxs:
+        ctxs[device] = Context(device)
+    return ctxs[device]
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(_lib.load().ipt_nccl_get_unique_id(buf))
+    return buf.raw
+
+
+# ----------------------------------------------------------------- helpers
+
+
+def _planar(a, n_expected=None):
+    """(re, im|None) contiguous float64 planes of a real or complex array."""
+    a = np.asarray(a)
+    if np.iscomplexobj(a):
+        re = np.ascontiguousarray(a.real, dtype=np.float64)
+        im = np.ascontiguousarray(a.imag, dtype=np.float64)
+        return re, (im if np.any(im != 0) else None)
+    return np.ascontiguousarray(a, dtype=np.float64), None
+
+
+def _combine(re, im, cplx: bool):
+    return re + 1j * im if cplx else re
+
+
+def _check_sizes(p: Partition, g: InverseGaps, anchor: int = 0) -> None:  # solver.cpp:25-30
+    n = p.size()
+    if n != g.size():
+        raise ValueError("solver: partition/gaps size mismatch")
+    shape = p.delta.shape
+    if shape != (n, n):
+        raise ValueError("solver: residual must be square of matching size")
+    if anchor < 0 or anchor >= n:
+        raise ValueError("solver: anchor out of range")
+
+
+def _is_complex_problem(p: Partition, extra=None) -> bool:
+    cx = np.iscomplexobj(p.d) and bool(np.any(np.asarray(p.d).imag != 0))
+    if isinstance(p.delta, CsrMatrix):
+        cx = cx or p.delta.is_complex()
+    else:
+        cx = cx or (np.iscomplexobj(p.delta) and bool(np.any(np.asarray(p.delta).imag != 0)))
+    if extra is not None:
+        cx = cx or (np.iscomplexobj(extra) and bool(np.any(np.asarray(extra).imag != 0)))
+    return cx
+
+
+def _out_complex(p: Partition, extra=None) -> bool:
+    """Complex result if any input carries a complex dtype (as the reference always does)."""
+    return (np.iscomplexobj(p.d) or np.iscomplexobj(getattr(p.delta, "values", p.delta))
+            or (extra is not None and np.iscomplexobj(extra)))
+
+
+# ----------------------------------------------------------------- full spectrum
+
+
+def apply_map_full(p: Partition, g: InverseGaps, Z, ctx: Optional[Context] = None) -> np.ndarray:
+    """F(Z) = I + G o (Z D(Delta Z) - Delta Z), one product (solver.cpp:156-178)."""
+    _check_sizes(p, g, 0)
+    n = p.size()
+    Z = np.asarray(Z)
+    if Z.shape != (n, n):
+        raise ValueError("apply_map_full: size mismatch")
+    delta = p.delta.to_dense() if isinstance(p.delta, CsrMatrix) else p.delta
+    ctx = ctx or default_context()
+    dr, di = _planar(p.d)
+    ar, ai = _planar(delta)
+    zr, zi = _planar(Z)
+    cx = _out_complex(p, Z)
+    fr = np.empty((n, n))
+    fi = np.empty((n, n)) if cx else None
+    check(_lib.load().ipt_apply_map_full(ctx.handle, n, dptr(dr), dptr(di), dptr(ar), dptr(ai),
+                                         dptr(zr), dptr(zi), dptr(fr), dptr(fi)))
+    return _combine(fr, fi, cx)
+
+
+def solve_full(p: Partition, g: InverseGaps, config: IterationConfig = None, warm_start=None,
+               ctx: Optional[Context] = None, want_sigma_min: bool = True) -> SpectrumResult:
+    """Fixed-point iteration of F from I (or a renormalised warm start), then the
+    closing product, |MZ - Z Lambda|_F and sigma_min (solver.cpp:180-273)."""
+    config = config or IterationConfig()
+    _validate(config)
+    _check_sizes(p, g, 0)
+    n = p.size()
+    delta = p.delta.to_dense() if isinstance(p.delta, CsrMatrix) else p.delta
+    ctx = ctx or default_context()
+    dr, di = _planar(p.d)
+    ar, ai = _planar(delta)
+    wr = wi = None
+    if warm_start is not None:
+        warm_start = np.asarray(warm_start)
+        if warm_start.shape != (n, n):
+            raise ValueError("solve_full: warm start size mismatch")
+        wr, wi = _planar(warm_start)
+    cx = _out_complex(p, warm_start)
+    root = ctx.rank == 0
+    zr = np.empty((n, n)) if root else None
+    zi = np.empty((n, n)) if (root and cx) else None
+    lr = np.empty(n) if root else None
+    li = np.empty(n) if (root and cx) else None
+    prm = _params(config, want_sigma_min=1 if want_sigma_min else 0)
+    st = _lib.Stats()
+    tr = np.zeros(config.max_iterations) if config.record_trace else None
+    tm = np.zeros(config.max_iterations) if config.record_trace else None
+    st.trace = dptr(tr)
+    st.trace_max_abs = dptr(tm)
+    check(_lib.load().ipt_full_solve(ctx.handle, n, dptr(dr), dptr(di), dptr(ar), dptr(ai), dptr(wr),
+                                     dptr(wi), C.byref(prm), dptr(zr), dptr(zi), dptr(lr), dptr(li),
+                                     C.byref(st)))
+    res = SpectrumResult()
+    if root:
+        res.Z = _combine(zr, zi, cx)
+        res.eigenvalues = _combine(lr, li, cx)
+    res.iterations = st.iterations
+    res.final_step = st.final_step
+    res.final_max_abs = st.final_max_abs
+    res.residual_frobenius = st.residual
+    res.min_singular_value_estimate = st.min_singular_value_estimate
+    res.status = SolveStatus(st.status)
+    res.matmul_count = st.product_count
+    if config.record_trace:
+        res.trace = list(tr[: st.iterations])
+        res.trace_max_abs = list(tm[: st.iterations])
+    res.timings_ms = dict(upload=st.ms_upload, loop=st.ms_loop, final=st.ms_final, sigma=st.ms_sigma,
+                          download=st.ms_download)
+    return res
+
+
+def smallest_singular_value_estimate(z, max_iters: int = 50, tol: float = 1e-4,
+                                     ctx: Optional[Context] = None) -> float:
+    """solver.cpp:275-297 (Cholesky of Z^H Z on the device, same inverse iteration)."""
+    z = np.asarray(z)
+    n = z.shape[0]
+    if n == 0 or z.ndim != 2 or z.shape[1] != n:
+        raise ValueError("smallest_singular_value_estimate: square input required")
+    ctx = ctx or default_context()
+    zr, zi = _planar(z)
+    out = C.c_double()
+    check(_lib.load().ipt_sigma_min(ctx.handle, n, dptr(zr), dptr(zi), int(max_iters), float(tol),
+                                    C.byref(out)))
+    return out.value
+
+
+# ----------------------------------------------------------------- single pair
+
+
+def _single_call(p, g, anchor, config, warm, schedule, alpha, ctx):
+    config = config or IterationConfig()
+    _validate(config)
+    _check_sizes(p, g, anchor)
+    n = p.size()
+    ctx = ctx or default_context()
+    lib = _lib.load()
+    dr, di = _planar(p.d)
+    wr = wi = None
+    if warm is not None:
+        warm = np.asarray(warm)
+        if warm.shape != (n,):
+            raise ValueError("solver: warm start size mismatch")
+        if warm[anchor] == 0:
+            raise ValueError("solver: warm start has zero anchor coordinate")
+        wr, wi = _planar(warm)
+    cx = _out_complex(p, warm)
+    zr = np.empty(n)
+    zi = np.empty(n) if cx else None
+    prm = _params(config, schedule=schedule, shrink_alpha=alpha)
+    st = _lib.Stats()
+    tr = np.zeros(config.max_iterations) if config.record_trace else None
+    st.trace = dptr(tr)
+    if isinstance(p.delta, CsrMatrix):
+        vr, vi = _planar(p.delta.values)
+        check(lib.ipt_single_solve_csr(ctx.handle, n, dptr(dr), dptr(di), i64ptr(p.delta.row_offsets),
+                                       i32ptr(p.delta.col_indices), dptr(vr), dptr(vi), int(anchor),
+                                       dptr(wr), dptr(wi), C.byref(prm), dptr(zr), dptr(zi), C.byref(st)))
+    else:
+        ar, ai = _planar(p.delta)
+        check(lib.ipt_single_solve_dense(ctx.handle, n, dptr(dr), dptr(di), dptr(ar), dptr(ai), int(anchor),
+                                         dptr(wr), dptr(wi), C.byref(prm), dptr(zr), dptr(zi), C.byref(st)))
+    res = EigenpairResult()
+    res.z = _combine(zr, zi, cx)
+    res.eigenvalue = complex(st.eigenvalue_re, st.eigenvalue_im) if cx else st.eigenvalue_re
+    res.anchor = int(anchor)
+    res.iterations = st.iterations
+    res.final_step = st.final_step
+    res.residual = st.residual
+    res.status = SolveStatus(st.status)
+    res.matvec_count = st.product_count
+    if config.record_trace:
+        res.trace = list(tr[: st.iterations])
+    res.timings_ms = dict(loop=st.ms_loop, final=st.ms_final)
+    return res
+
+
+def solve_single(p: Partition, g: InverseGaps, anchor: int, config: IterationConfig = None,
+                 warm_start=None, ctx: Optional[Context] = None) -> EigenpairResult:
+    """solver.cpp:132-136."""
+    return _single_call(p, g, anchor, config, warm_start, _lib.SCHEDULE_PLAIN, 0.9, ctx)
+
+
+def solve_single_continuation(p: Partition, g: InverseGaps, anchor: int, config: IterationConfig = None,
+                              shrink_alpha: float = 0.9, ctx: Optional[Context] = None) -> EigenpairResult:
+    """solver.cpp:138-154."""
+    if not (0.0 <= shrink_alpha < 1.0):
+        raise ValueError("continuation: shrink factor must lie in [0, 1)")
+    return _single_call(p, g, anchor, config, None, _lib.SCHEDULE_CONTINUATION, shrink_alpha, ctx)
+
+
+def apply_map_single(p: Partition, g: InverseGaps, anchor: int, z, ctx: Optional[Context] = None) -> np.ndarray:
+    """f_i(z) = e_i + g_i o (z (Delta z)_i - Delta z) (solver.cpp:122-130)."""
+    _check_sizes(p, g, anchor)
+    n = p.size()
+    z = np.asarray(z)
+    if z.shape != (n,):
+        raise ValueError("apply_map_single: size mismatch")
+    delta = p.delta.to_dense() if isinstance(p.delta, CsrMatrix) else p.delta
+    ctx = ctx or default_context()
+    dr, di = _planar(p.d)
+    ar, ai = _planar(delta)
+    zr, zi = _planar(z)
+    cx = _out_complex(p, z)
+    fr = np.empty(n)
+    fi = np.empty(n) if cx else None
+    check(_lib.load().ipt_apply_map_single_dense(ctx.handle, n, dptr(dr), dptr(di), dptr(ar), dptr(ai),
+                                                 int(anchor), dptr(zr), dptr(zi), dptr(fr), dptr(fi)))
+    return _combine(fr, fi, cx)
+
+
+# ----------------------------------------------------------------- kernels::
+
+
+class kernels:  # noqa: N801  (namespace ipt::kernels)
+    @staticmethod
+    def matmul(a, b, ctx: Optional[Context] = None) -> np.ndarray:
+        """C = A B (kernels.cpp:175-181); deterministic run to run."""
+        if isinstance(a, CsrMatrix):
+            a = a.to_dense()
+        a, b = np.asarray(a), np.asarray(b)
+        if a.shape[1] != b.shape[0]:
+            raise ValueError("matmul: inner dimensions differ")
+        ctx = ctx or default_context()
+        m, k = a.shape
+        n = b.shape[1]
+        ar, ai = _planar(a)
+        br, bi = _planar(b)
+        cx = np.iscomplexobj(a) or np.iscomplexobj(b)
+        cr = np.empty((m, n))
+        ci = np.empty((m, n)) if cx else None
+        check(_lib.load().ipt_gemm(ctx.handle, m, k, n, dptr(ar), dptr(ai), dptr(br), dptr(bi), dptr(cr), dptr(ci)))
+        return _combine(cr, ci, cx)
+
+    @staticmethod
+    def matvec(a: Matrix, x, ctx: Optional[Context] = None) -> np.ndarray:
+        """y = A x, dense or CSR (kernels.cpp:112-140)."""
+        ctx = ctx or default_context()
+        x = np.asarray(x)
+        xr, xi = _planar(x)
+        lib = _lib.load()
+        if isinstance(a, CsrMatrix):
+            m, n = a.shape
+            vr, vi = _planar(a.values)
+            cx = np.iscomplexobj(a.values) or np.iscomplexobj(x)
+            yr = np.empty(m)
+            yi = np.empty(m) if cx else None
+            check(lib.ipt_matvec_csr(ctx.handle, m, n, i64ptr(a.row_offsets), i32ptr(a.col_indices), dptr(vr),
+                                     dptr(vi), dptr(xr), dptr(xi), dptr(yr), dptr(yi)))
+        else:
+            a = np.asarray(a)
+            m, n = a.shape
+            ar, ai = _planar(a)
+            cx = np.iscomplexobj(a) or np.iscomplexobj(x)
+            yr = np.empty(m)
+            yi = np.empty(m) if cx else None
+            check(lib.ipt_matvec_dense(ctx.handle, m, n, dptr(ar), dptr(ai), dptr(xr), dptr(xi), dptr(yr), dptr(yi)))
+        return _combine(yr, yi, cx)
+
+    @staticmethod
+    def frobenius_norm(m) -> float:
+        v = m.values if isinstance(m, CsrMatrix) else np.asarray(m)
+        return float(np.sqrt(np.sum(np.abs(v) ** 2)))
+
+    @staticmethod
+    def nrm2(v) -> float:
+        return float(np.sqrt(np.sum(np.abs(np.asarray(v)) ** 2)))
+
+    @staticmethod
+    def max_abs(v) -> float:
+        return float(np.max(np.abs(np.asarray(v)))) if np.asarray(v).size else 0.0
