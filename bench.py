@@ -1,0 +1,439 @@
+#!/usr/bin/env python3
+"""Headline benchmark: full-spectrum IPT (BASELINE.json metric) on B200.
+
+Workload (config.workload): BASELINE.json configs[2], full-spectrum IPT at
+N = 32768, fp64, D = diag(1..N), Delta symmetric zero-diagonal uniform[-1,1]
+(seed 42), eps = 0.32/sqrt(N), Z column-sharded over the ranks with Delta
+replicated (strong scaling: the same N for every GPU count). Synthetic data of
+exactly that construction (there is no dataset in the reference).
+
+A "step" is one IPT iteration (one map application F(Z)): K2 diagonal
+pre-pass + K1 fused DMMA GEMM/map epilogue + fixed-order reduction (+ NCCL
+all-reduce of the step scalars for N>1) + device-side stop decision. `value` is
+whole-job FP64 TFLOP/s = 2 N^3 per step / step time (max over ranks), inputs
+resident in HBM. `e2e` is the same metric through the drop-in C ABI
+(ipt_full_solve) with host buffers: H2D of Delta, the iterations to
+convergence, the closing product, sigma_min, and D2H of Z and Lambda.
+
+Secondary lines (same JSON object, "secondary"): the single-eigenpair paths
+(config 4 dense GEMV at N = 65536 and config 5 CSR SpMV at N = 2^21) in GB/s.
+
+`--impl reference` times the reference's own CPU implementation (oracle/_ref,
+built from the reference sources) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_FULL = 32768
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+METRIC = "IPT full-spectrum FP64 TFLOP/s (2N^3 per iteration), N=32768"
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def workload_config(world, n, extra=None):
+    cfg = {
+        "workload": f"BASELINE configs[2]: full-spectrum IPT fp64 dense symmetric N={n}, D=diag(1..N), "
+                    f"Delta uniform[-1,1] symmetric zero-diagonal, eps=0.32/sqrt(N), Z column-sharded over "
+                    f"{world} GPU(s), Delta replicated",
+        "n": n,
+        "eps": 0.32 / math.sqrt(n),
+        "seed": 42,
+        "step": "one IPT map application (diag pre-pass + fused DMMA GEMM/epilogue + reduction + stop decision)",
+        "parallelism": f"column-shard x{world}" if world > 1 else "single GPU",
+        "l2": "inputs exceed L2 (Delta 8.6 GB, Z 8.6 GB per buffer vs 126 MB L2); no flush needed",
+    }
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+# --------------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi equivalent via NVML: SM clock + throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device):
+        self.samples, self.reasons, self.stop_ev = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self.stop_ev.wait(0.2)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop_ev.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- peaks
+
+
+def fp64_peak(torch):
+    """cuBLAS DGEMM (torch float64 matmul) 8192^3 best of 5: the FP64 denominator.
+    MEASURED_PEAKS.json carries no FP64 figure; this is measured on the same GPU in
+    the same run (burst), beside the DMMA issue-rate probe (profiles/r01_fp64_probe.txt)."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    torch.matmul(a, b)
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    del a, b
+    torch.cuda.empty_cache()
+    return 2.0 * n ** 3 / best / 1e12
+
+
+def hbm_peak():
+    try:
+        return json.load(open(PEAKS_PATH))["hbm_gbs"], "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def traffic_for(kernel):
+    try:
+        return json.load(open(TRAFFIC_PATH)).get(kernel)
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------- CPU baseline
+
+
+def cpu_reference_sample(n=2048, reps=2):
+    """The reference's own apply_map_full (solver.cpp:156-178; kernels.cpp dgemm) on the
+    host cores, one map application at a bounded N of the same construction."""
+    import oracle
+    from paper_2012_14702_b200 import synth
+
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    R = oracle.ref()
+    p = synth.dense_uniform(n, 0.32 / math.sqrt(n), 42)
+    z = np.eye(n)
+    R.apply_map_full(p.d, p.delta, z)  # warm
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        z = R.apply_map_full(p.d, p.delta, z)
+        ts.append(time.perf_counter() - t0)
+    t = min(ts)
+    return {"value": 2.0 * n ** 3 / t / 1e12, "unit": "TFLOP/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
+            "kind": "reference",
+            "sample": f"reference apply_map_full (one IPT iteration) at N={n}, same construction, "
+                      f"best of {reps}: {t:.3f} s; metric counts 2N^3 useful flops"}
+
+
+def run_reference_arm(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    import oracle
+
+    n = args.ref_n
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    from paper_2012_14702_b200 import synth
+
+    R = oracle.ref()
+    p = synth.dense_uniform(n, 0.32 / math.sqrt(n), 42)
+    z = np.eye(n, dtype=np.complex128)
+    for _ in range(args.warmup):
+        z = R.apply_map_full(p.d, p.delta, z)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        z = R.apply_map_full(p.d, p.delta, z)
+    t = time.perf_counter() - t0
+    value = 2.0 * n ** 3 * args.steps / t / 1e12
+    sample = (f"reference apply_map_full (proj/src/solver.cpp:156-178, OpenMP kernels.cpp) at N={n} of the "
+              f"same construction per step (the N={N_FULL} workload needs ~120 GB and hours per iteration "
+              f"on the CPU); metric counts 2N^3 flops per step")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(world, N_FULL, {"reference_sample_n": n}),
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- secondary: single pair
+
+
+def bench_single(ipt, lib, ctx, which, steps, warmup, hbm):
+    from paper_2012_14702_b200 import synth
+    from paper_2012_14702_b200._lib import check, dptr, i32ptr, i64ptr
+
+    t0 = time.perf_counter()
+    if which == "gemv":
+        n = 65536
+        p = synth.config4()
+        nbytes = 8.0 * n * n + 3 * 8.0 * n
+        h = C.c_void_p()
+        check(lib.ipt_single_upload_dense(ctx.handle, n, dptr(p.d), None, dptr(p.delta), None, C.byref(h)))
+        kernel = "gemv_map_kernel<1>"
+        tol = 1e-12
+        gaps_tol = -1.0
+    else:
+        n = 1 << 21
+        p = synth.config5()
+        nnz = p.delta.nnz
+        nbytes = 12.0 * nnz + 8.0 * (n + 1) + 3 * 8.0 * n
+        h = C.c_void_p()
+        check(lib.ipt_single_upload_csr(ctx.handle, n, dptr(p.d), None, i64ptr(p.delta.row_offsets),
+                                        i32ptr(p.delta.col_indices), dptr(p.delta.values), None, C.byref(h)))
+        kernel = "spmv_map_kernel<1>"
+        tol = 1e-10
+        gaps_tol = 0.0
+    setup_s = time.perf_counter() - t0
+    # a real solve for the time-to-convergence line
+    check(lib.ipt_single_reset(ctx.handle, h, 0, None, None))
+    from paper_2012_14702_b200._lib import Stats
+    from paper_2012_14702_b200.ipt import _params
+
+    prm = _params(ipt.IterationConfig(tolerance=tol))
+    st = Stats()
+    check(lib.ipt_single_iterate(ctx.handle, h, C.byref(prm), C.byref(st)))
+    check(lib.ipt_single_finalize(ctx.handle, h, C.byref(st)))
+    solve = {"iterations": st.iterations, "status": ipt.to_string(st.status), "eigenvalue": st.eigenvalue_re,
+             "residual": st.residual, "loop_ms": st.ms_loop, "final_ms": st.ms_final}
+    check(lib.ipt_single_reset(ctx.handle, h, 0, None, None))
+    tot, dom = C.c_double(), C.c_double()
+    check(lib.ipt_single_run_steps(ctx.handle, h, warmup, C.byref(tot), C.byref(dom)))
+    check(lib.ipt_single_run_steps(ctx.handle, h, steps, C.byref(tot), C.byref(dom)))
+    lib.ipt_single_free(h)
+    step_ms = tot.value / steps
+    dom_ms = dom.value / steps
+    kbytes = nbytes - 8.0 * n  # the map kernel itself: matrix + z + d + fz
+    del p
+    return {
+        "workload": ("configs[3] dense GEMV single pair N=65536" if which == "gemv"
+                     else "configs[4] CSR SpMV single pair N=2^21 (~64 nnz/row)"),
+        "metric": "single-pair IPT iteration GB/s (algorithmic bytes)",
+        "value": nbytes / (step_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": step_ms,
+        "time_to_solution": solve, "setup_s": setup_s,
+        "roofline": {"bound": "hbm", "kernel": kernel, "achieved": kbytes / (dom_ms * 1e-3) / 1e9,
+                     "peak": hbm[0], "peak_source": hbm[1], "unit": "GB/s",
+                     "frac": kbytes / (dom_ms * 1e-3) / 1e9 / hbm[0], "kernel_ms": dom_ms,
+                     "bytes_per_launch": kbytes, "traffic": traffic_for(kernel)},
+    }
+
+
+# --------------------------------------------------------------------------- main arm
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=N_FULL)
+    ap.add_argument("--ref-n", type=int, default=2048)
+    ap.add_argument("--secondary", default="all", choices=["all", "none", "gemv", "spmv"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2012_14702_b200 as ipt
+    from paper_2012_14702_b200 import dist as idist
+    from paper_2012_14702_b200 import synth
+    from paper_2012_14702_b200._lib import check, dptr
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = idist.init_context_from_env()
+    lib = ipt.load_library()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    peak = fp64_peak(torch) if rank == 0 else 0.0
+    n = args.n
+    t0 = time.perf_counter()
+    p = synth.config3(n=n)
+    gen_s = time.perf_counter() - t0
+
+    # ---------------- device-resident timed steps
+    h = C.c_void_p()
+    check(lib.ipt_full_upload(ctx.handle, n, dptr(p.d), None, dptr(p.delta), None, C.byref(h)))
+    check(lib.ipt_full_reset(ctx.handle, h, None, None))
+    c0, c1 = C.c_int64(), C.c_int64()
+    lib.ipt_full_local_columns(h, C.byref(c0), C.byref(c1))
+    ncols = c1.value - c0.value
+    tot, gem = C.c_double(), C.c_double()
+    check(lib.ipt_full_run_maps(ctx.handle, h, args.warmup, C.byref(tot), C.byref(gem)))
+    launches0 = lib.ipt_kernel_launch_count()
+    barrier()
+    wall0 = time.perf_counter()
+    with ClockSampler(local) as clk:
+        check(lib.ipt_full_run_maps(ctx.handle, h, args.steps, C.byref(tot), C.byref(gem)))
+    barrier()
+    wall = time.perf_counter() - wall0
+    launches = lib.ipt_kernel_launch_count() - launches0
+    step_ms = max_over_ranks(tot.value / args.steps)
+    gemm_ms_local = gem.value / args.steps
+    gemm_ms = max_over_ranks(gemm_ms_local)
+    lib.ipt_full_free(h)
+    flops_step = 2.0 * n ** 3
+    value = flops_step / (step_ms * 1e-3) / 1e12
+    gemm_flops_local = 2.0 * n * n * ncols
+    achieved = gemm_flops_local / (gemm_ms_local * 1e-3) / 1e12
+
+    # ---------------- end to end through the C ABI with host buffers
+    e2e = None
+    solve_info = None
+    if not args.no_e2e:
+        torch.cuda.empty_cache()
+        barrier()
+        t0 = time.perf_counter()
+        r = ipt.solve_full(p, ipt.build_gaps(p), ipt.IterationConfig(tolerance=1e-12), ctx=ctx)
+        barrier()
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": flops_step * r.iterations / e2e_s / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": int(8 * n * n + 8 * n),
+               "d2h_bytes_per_step": int(8 * n * n + 8 * n) if rank == 0 else 0,
+               "step": "one drop-in solve_full call (C ABI ipt_full_solve, host buffers, pageable memory)",
+               "seconds": e2e_s}
+        solve_info = {"iterations": r.iterations, "status": ipt.to_string(r.status),
+                      "residual_frobenius": r.residual_frobenius,
+                      "residual_rel": r.residual_frobenius / math.sqrt(float(np.sum(p.delta ** 2)) + float(np.sum(p.d ** 2))),
+                      "sigma_min": r.min_singular_value_estimate, "timings_ms": r.timings_ms,
+                      "time_to_solution_s": e2e_s,
+                      "lambda0": float(r.eigenvalues[0]) if rank == 0 else None}
+        del r
+    del p
+
+    # ---------------- secondary: single-pair paths (rank 0, N = 1 only)
+    secondary = {}
+    if world == 1 and args.secondary != "none":
+        hbm = hbm_peak()
+        for which in (["gemv", "spmv"] if args.secondary == "all" else [args.secondary]):
+            try:
+                secondary[which] = bench_single(ipt, lib, ctx, which, max(args.steps, 10), 3, hbm)
+            except Exception as exc:  # report, never hide
+                secondary[which] = {"error": repr(exc)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_reference_sample()
+        except Exception as exc:
+            cpu = {"error": repr(exc)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE configs[2] construction, seed 42)",
+            "config": workload_config(world, n),
+            "roofline": {"bound": "tensor", "kernel": "dmma_gemm_kernel<1> (K1 fused DMMA GEMM + map epilogue)",
+                         "achieved": achieved, "peak": peak,
+                         "peak_source": "cuBLAS DGEMM 8192^3 on this GPU in this run (burst); DMMA issue-rate "
+                                        "probe 37.1 TF/s in profiles/r01_fp64_probe.txt",
+                         "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+                         "flops_per_launch": gemm_flops_local, "kernel_ms": gemm_ms_local,
+                         "kernel_share_of_step": gemm_ms / step_ms,
+                         "traffic": traffic_for("dmma_gemm_kernel<1>")},
+            "time_to_solution": solve_info,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "wall_s_timed": wall,
+            "setup": {"generate_s": gen_s},
+            "secondary": secondary,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -162,6 +162,17 @@ int ipt_matvec_csr(ipt_ctx* ctx, int64_t m, int64_t n, const int64_t* rowptr, co
                    const double* val_re, const double* val_im, const double* x_re,
                    const double* x_im, double* y_re, double* y_im);
 
+/* ---- measurement hooks (bench.py) ----
+ * Enqueue exactly `count` further map applications / single-pair steps on a resident
+ * problem (continuing from the current iterate, convergence ignored) and return the
+ * device time of the whole sequence and of the dominant kernel alone (K1 fused DMMA
+ * GEMM, or the fused GEMV / SpMV map kernel), both from CUDA events on the library
+ * stream. */
+int ipt_full_run_maps(ipt_ctx* ctx, ipt_full_problem* prob, int32_t count, double* ms_total,
+                      double* ms_dominant);
+int ipt_single_run_steps(ipt_ctx* ctx, ipt_single_problem* prob, int32_t count, double* ms_total,
+                         double* ms_dominant);
+
 /* Counters for gpu_launches accounting: kernels this library has launched. */
 int64_t ipt_kernel_launch_count(void);
 

@@ -126,6 +126,20 @@ class RefArm(_Arm):
         return dict(z=z, eigenvalue=lam[0], iterations=it, status=int(stats[1]), final_step=stats[2],
                     residual=stats[3], matvec_count=int(stats[4]), seconds=stats[5], trace=trace[:it].copy())
 
+    def solve_single_multi(self, d, delta, anchors, tol=100 * np.finfo(float).eps, max_iter=1000):
+        """solve_single for several anchors on one partition (builds the reference's
+        ComplexMatrix once). Returns (z[n, count], iterations, status, eigenvalues)."""
+        n = len(d)
+        anchors = np.ascontiguousarray(anchors, dtype=np.int64)
+        k = anchors.size
+        dd = _c(d)
+        dense = _c(delta)
+        z = np.empty((k, n), np.complex128)
+        meta = np.zeros((k, 4))
+        self._chk(self.lib.ref_solve_single_multi(C.c_int64(n), _p(dd), _p(dense), anchors.ctypes.data_as(_i64p),
+                                                  C.c_int64(k), C.c_double(tol), C.c_int(max_iter), _p(z), _p(meta)))
+        return z.T.copy(), meta[:, 0].astype(int), meta[:, 1].astype(int), meta[:, 2] + 1j * meta[:, 3]
+
     def apply_map_full(self, d, delta, z):
         n = len(d)
         out = np.empty((n, n), np.complex128)

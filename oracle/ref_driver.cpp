@@ -218,6 +218,27 @@ REF_API int ref_solve_single(int64_t n, const double* d, int is_csr, const doubl
   });
 }
 
+// solve_single for several anchors on one partition (column route of SURVEY §8c):
+// z_out is count x n (row k = anchor k's eigenvector), meta count x 4 =
+// {iterations, status, Re lambda, Im lambda}.
+REF_API int ref_solve_single_multi(int64_t n, const double* d, const double* dense,
+                                   const int64_t* anchors, int64_t count, double tol, int max_iter,
+                                   double* z_out, double* meta) {
+  return guarded([&] {
+    Partition p = make_partition(n, d, 0, dense, nullptr, nullptr, nullptr);
+    const InverseGaps g = build_gaps(p, -1.0);
+    const IterationConfig cfg = make_cfg(tol, max_iter, 1e8, 0);
+    for (int64_t k = 0; k < count; ++k) {
+      const EigenpairResult r = solve_single(p, g, static_cast<std::size_t>(anchors[k]), cfg);
+      from_cvec(r.z, z_out + 2 * k * n);
+      meta[4 * k + 0] = r.iterations;
+      meta[4 * k + 1] = static_cast<double>(static_cast<int>(r.status));
+      meta[4 * k + 2] = r.eigenvalue.real();
+      meta[4 * k + 3] = r.eigenvalue.imag();
+    }
+  });
+}
+
 REF_API int ref_apply_map_full(int64_t n, const double* d, const double* delta, const double* z,
                                double* out) {
   return guarded([&] {

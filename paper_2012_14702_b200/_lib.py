@@ -105,6 +105,8 @@ SIGNATURES = {
     "ipt_matvec_dense": (C.c_int, [_vp, C.c_int64, C.c_int64, _dp, _dp, _dp, _dp, _dp, _dp]),
     "ipt_matvec_csr": (C.c_int, [_vp, C.c_int64, C.c_int64, _i64p, _i32p, _dp, _dp, _dp, _dp, _dp,
                                  _dp]),
+    "ipt_full_run_maps": (C.c_int, [_vp, _vp, C.c_int32, _dp, _dp]),
+    "ipt_single_run_steps": (C.c_int, [_vp, _vp, C.c_int32, _dp, _dp]),
     "ipt_kernel_launch_count": (C.c_int64, []),
     "ipt_synth_dense_uniform": (C.c_int, [C.c_int64, C.c_double, C.c_uint64, _dp, _dp]),
     "ipt_synth_dense_normal": (C.c_int, [C.c_int64, C.c_double, C.c_uint64, C.c_int, _dp, _dp]),

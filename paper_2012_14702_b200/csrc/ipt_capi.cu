@@ -414,6 +414,26 @@ int ipt_apply_map_single_dense(ipt_ctx* ctx, int64_t n, const double* d_re, cons
   });
 }
 
+int ipt_full_run_maps(ipt_ctx* ctx, ipt_full_problem* prob, int32_t count, double* ms_total,
+                      double* ms_dominant) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (count < 0) throw InvalidArgument("run_maps: negative count");
+    full_run_maps(*reinterpret_cast<FullProblem*>(prob), count, ms_total, ms_dominant);
+  });
+}
+
+int ipt_single_run_steps(ipt_ctx* ctx, ipt_single_problem* prob, int32_t count, double* ms_total,
+                         double* ms_dominant) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (count < 0) throw InvalidArgument("run_steps: negative count");
+    single_run_steps(*as_single(prob), count, ms_total, ms_dominant);
+  });
+}
+
 // ------------------------------------------------------------------ kernels::
 
 int ipt_gemm(ipt_ctx* ctx, int64_t m, int64_t k, int64_t n, const double* a_re, const double* a_im,

@@ -287,7 +287,8 @@ void allreduce_sums(FullProblem& P, bool with_max) {
 }
 
 // Enqueue map application number k (reads Z[k&1], writes Z[(k+1)&1]).
-void enqueue_map(FullProblem& P, int k, const ipt_params& prm) {
+void enqueue_map(FullProblem& P, int k, const ipt_params& prm, cudaEvent_t ev_a = nullptr,
+                 cudaEvent_t ev_b = nullptr) {
   Ctx& c = *P.ctx;
   const double* zs = P.Z[k & 1].get();
   double* zd = P.Z[(k + 1) & 1].get();
@@ -295,7 +296,9 @@ void enqueue_map(FullProblem& P, int k, const ipt_params& prm) {
   if (!P.cplx) {
     launch_diag(P, P.A1.get(), zs, P.wd.get(), nullptr, nullptr, st);
     GemmParams g = gemm_params(P, P.A1.get(), zs, zd, P.ldz);
+    if (ev_a) IPT_CUDA(cudaEventRecord(ev_a, c.stream));
     launch_gemm(kGemmMap, g, c.stream);
+    if (ev_b) IPT_CUDA(cudaEventRecord(ev_b, c.stream));
   } else {
     launch_diag(P, P.A1.get(), zs, P.wd.get(), nullptr, nullptr, st);
     launch_diag(P, P.A2.get(), zs, P.wdi.get(), nullptr, nullptr, st);
@@ -647,6 +650,40 @@ void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, d
 }
 
 bool full_is_complex(const FullProblem& P) { return P.cplx; }
+
+// Bench / profiling: exactly `count` further map applications (convergence ignored),
+// timed with CUDA events on the library stream: the whole sequence and the K1 GEMM
+// launches alone (the dominant kernel of the roofline).
+void full_run_maps(FullProblem& P, int count, double* ms_total, double* ms_gemm) {
+  Ctx& c = *P.ctx;
+  ipt_params prm;
+  ipt_default_params(&prm);
+  prm.max_iterations = 0x7fffffff;
+  prm.ignore_convergence = 1;
+  prm.divergence_threshold = 1.0e300;
+  LoopState init{};
+  init.status = kMaxIterations;
+  init.scale_ak = 1.0;
+  IPT_CUDA(cudaMemcpyAsync(P.state, &init, sizeof(LoopState), cudaMemcpyHostToDevice, c.stream));
+  std::vector<cudaEvent_t> ev(2 * size_t(count) + 2);
+  for (auto& e : ev) IPT_CUDA(cudaEventCreate(&e));
+  c.sync();
+  IPT_CUDA(cudaEventRecord(ev[0], c.stream));
+  for (int i = 0; i < count; ++i) enqueue_map(P, P.enq++, prm, ev[2 + 2 * i], ev[3 + 2 * i]);
+  IPT_CUDA(cudaEventRecord(ev[1], c.stream));
+  c.sync();
+  float ms = 0.f;
+  IPT_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+  *ms_total = ms;
+  double g = 0.0;
+  for (int i = 0; i < count && !P.cplx; ++i) {
+    IPT_CUDA(cudaEventElapsedTime(&ms, ev[2 + 2 * i], ev[3 + 2 * i]));
+    g += ms;
+  }
+  *ms_gemm = g;
+  for (auto& e : ev) cudaEventDestroy(e);
+  IPT_CUDA(cudaMemcpy(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost));
+}
 
 void full_local_columns(const FullProblem& P, int64_t* c0, int64_t* c1) {
   *c0 = P.col0;

@@ -95,6 +95,7 @@ void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats);
 void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, double* lam_im);
 void full_local_columns(const FullProblem& P, int64_t* c0, int64_t* c1);
 bool full_is_complex(const FullProblem& P);
+void full_run_maps(FullProblem& P, int count, double* ms_total, double* ms_gemm);
 
 // Single-pair problem (ipt_single.cu)
 struct SingleProblem;
@@ -109,6 +110,7 @@ void single_iterate(SingleProblem& P, const ipt_params& prm, ipt_stats* stats);
 void single_finalize(SingleProblem& P, ipt_stats* stats);
 void single_download(SingleProblem& P, double* z_re, double* z_im);
 void single_matvec(SingleProblem& P, const double* x_re, const double* x_im, double* y_re, double* y_im);
+void single_run_steps(SingleProblem& P, int count, double* ms_total, double* ms_map);
 
 // sigma_min (ipt_sigma.cu): Z column-major (ldz), real or complex (zi nullable).
 double sigma_min_device(Ctx& ctx, int64_t n, const double* zr, const double* zi, int64_t ldz,

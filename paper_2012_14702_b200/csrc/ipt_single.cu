@@ -488,13 +488,16 @@ void enqueue_real_map(SingleProblem& P, int src, const ipt_params* prm) {
   count_launch();
 }
 
-void enqueue_iteration(SingleProblem& P, int k, const ipt_params& prm) {
+void enqueue_iteration(SingleProblem& P, int k, const ipt_params& prm, cudaEvent_t ev_a = nullptr,
+                       cudaEvent_t ev_b = nullptr) {
   Ctx& c = *P.ctx;
   const int src = k & 1;
   LoopState* st = P.state;
   if (!P.cplx) {
     enqueue_anchor(P, src, st);
+    if (ev_a) IPT_CUDA(cudaEventRecord(ev_a, c.stream));
     enqueue_real_map<kMvMap>(P, src, &prm);
+    if (ev_b) IPT_CUDA(cudaEventRecord(ev_b, c.stream));
   } else {
     enqueue_cmatvec(P, src);
     allgather_w(P);
@@ -782,6 +785,38 @@ void single_download(SingleProblem& P, double* z_re, double* z_im) {
     if (P.cplx) IPT_CUDA(cudaMemcpy(z_im, P.zi[cur].get(), sizeof(double) * P.n, cudaMemcpyDeviceToHost));
     else std::memset(z_im, 0, sizeof(double) * P.n);
   }
+}
+
+// Bench / profiling: exactly `count` further iterations (convergence ignored), timed on the
+// library stream: the whole sequence and the fused GEMV/SpMV map kernel alone.
+void single_run_steps(SingleProblem& P, int count, double* ms_total, double* ms_map) {
+  Ctx& c = *P.ctx;
+  ipt_params prm;
+  ipt_default_params(&prm);
+  prm.max_iterations = 0x7fffffff;
+  prm.ignore_convergence = 1;
+  prm.divergence_threshold = 1.0e300;
+  LoopState init{};
+  init.status = kMaxIterations;
+  init.scale_ak = 1.0;
+  IPT_CUDA(cudaMemcpyAsync(P.state, &init, sizeof(LoopState), cudaMemcpyHostToDevice, c.stream));
+  std::vector<cudaEvent_t> ev(2 * size_t(count) + 2);
+  for (auto& e : ev) IPT_CUDA(cudaEventCreate(&e));
+  c.sync();
+  IPT_CUDA(cudaEventRecord(ev[0], c.stream));
+  for (int i = 0; i < count; ++i) enqueue_iteration(P, P.enq++, prm, ev[2 + 2 * i], ev[3 + 2 * i]);
+  IPT_CUDA(cudaEventRecord(ev[1], c.stream));
+  c.sync();
+  float ms = 0.f;
+  IPT_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+  *ms_total = ms;
+  double m = 0.0;
+  for (int i = 0; i < count && !P.cplx; ++i) {
+    IPT_CUDA(cudaEventElapsedTime(&ms, ev[2 + 2 * i], ev[3 + 2 * i]));
+    m += ms;
+  }
+  *ms_map = m;
+  for (auto& e : ev) cudaEventDestroy(e);
 }
 
 // kernels::matvec on device-resident data: y = Delta x (one pass, no epilogue).
