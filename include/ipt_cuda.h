@@ -5,8 +5,8 @@
  * (proj/include/ipt/solver.hpp, kernels.hpp). Plain pointers and sizes only:
  * no torch, no C++ types. Every function returns IPT_OK (0) or a negative
  * code and never throws; ipt_last_error() holds the message of the last
- * failure on the calling thread. The C++ layer (include/ipt/*.hpp,
- * src/api/*.cpp) maps the codes back to the reference's exception types:
+ * failure on the calling thread. The C++ layer (include/ipt/ headers,
+ * src/api/) maps the codes back to the reference exception types:
  *   IPT_ERR_INVALID -> std::invalid_argument (solver.cpp:18-30,39-41,125,158,192-197)
  *   IPT_ERR_CUDA / IPT_ERR_NCCL -> std::runtime_error
  * Non-convergence is a status (IPT_STATUS_*), not an error.

@@ -77,8 +77,11 @@ __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
-// Element (r, k) of a 16-double-wide shared tile row, 16-byte units XORed with r&7.
-__device__ __forceinline__ int swz(int r, int k) { return r * kBK + ((((k >> 1) ^ (r & 7)) << 1) | (k & 1)); }
+// Element (r, k) of a 16-double-wide shared tile row. A fragment read covers rows
+// g = 0..7 x k0..k0+3 (one 32-byte unit pair per row); XORing the unit index with
+// 2*(r&3) sends the four rows of each half-warp phase to four distinct unit pairs,
+// i.e. all 32 banks once per phase (conflict-free LDS.64).
+__device__ __forceinline__ int swz(int r, int k) { return r * kBK + ((((k >> 1) ^ ((r & 3) << 1)) << 1) | (k & 1)); }
 
 // Grouped rasterisation: kGroupM tile-rows at a time, column-major inside the group,
 // so the ~148 co-resident CTAs share a few Delta row panels and Z column panels in L2.
@@ -118,13 +121,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) dmma_gemm_kernel(const GemmPa
     for (int i = 0; i < (kBM * kBK / 2) / kGemmThreads; ++i) {
       const int c = tid + i * kGemmThreads;
       const int row = c >> 3, u = c & 7;
-      cp_async16(as + row * kBK + ((u ^ (row & 7)) << 1), Ag + row * p.lda + k0 + u * 2);
+      cp_async16(as + row * kBK + ((u ^ ((row & 3) << 1)) << 1), Ag + row * p.lda + k0 + u * 2);
     }
 #pragma unroll
     for (int i = 0; i < (kBN * kBK / 2) / kGemmThreads; ++i) {
       const int c = tid + i * kGemmThreads;
       const int col = c >> 3, u = c & 7;
-      cp_async16(bs + col * kBK + ((u ^ (col & 7)) << 1), Bg + col * p.ldb + k0 + u * 2);
+      cp_async16(bs + col * kBK + ((u ^ ((col & 3) << 1)) << 1), Bg + col * p.ldb + k0 + u * 2);
     }
   };
 

@@ -10,7 +10,12 @@ void DevBuf::alloc(size_t n, bool zero) {
   if (n == 0) n = 1;
   IPT_CUDA(cudaMalloc(&p, n * sizeof(double)));
   count = n;
-  if (zero) IPT_CUDA(cudaMemset(p, 0, n * sizeof(double)));
+  if (zero) {
+    // The library stream is non-blocking w.r.t. the legacy stream: finish the memset
+    // before any copy or kernel on the library stream can touch the buffer.
+    IPT_CUDA(cudaMemsetAsync(p, 0, n * sizeof(double), nullptr));
+    IPT_CUDA(cudaStreamSynchronize(nullptr));
+  }
 }
 void DevBuf::release() {
   if (p) cudaFree(p);

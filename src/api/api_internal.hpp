@@ -1,0 +1,91 @@
+// Shared glue of the C++ drop-in API: per-thread device context, C-ABI error
+// mapping to the reference's exception types, and the one-time layout
+// conversion std::complex (interleaved) <-> planar re / im at the boundary.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "ipt/complex_matrix.hpp"
+#include "ipt_cuda.h"
+
+namespace ipt::api {
+
+ipt_ctx* context();  // thread-local, created on first use
+void set_device(int device);
+
+inline void check(int rc) {
+    if (rc == IPT_OK) return;
+    const std::string msg = ipt_last_error();
+    if (rc == IPT_ERR_INVALID) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+
+struct Planar {
+    std::vector<double> re, im;
+    bool any_im = false;
+    const double* im_or_null() const { return any_im ? im.data() : nullptr; }
+};
+
+// Large conversions are split over host threads (IPT_THREADS, default all cores).
+unsigned host_threads();
+
+template <typename F>
+void parallel_chunks(std::size_t count, F&& f) {
+    const unsigned t = count < (std::size_t(1) << 20) ? 1u : host_threads();
+    if (t <= 1) {
+        f(std::size_t{0}, count);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const std::size_t step = (count + t - 1) / t;
+    for (unsigned k = 0; k < t; ++k) {
+        const std::size_t b = k * step, e = std::min(count, b + step);
+        if (b < e) pool.emplace_back([&f, b, e] { f(b, e); });
+    }
+    for (auto& th : pool) th.join();
+}
+
+inline Planar split(const cplx* v, std::size_t count) {
+    Planar p;
+    p.re.resize(count);
+    p.im.resize(count);
+    std::vector<char> flag(host_threads() + 1, 0);
+    parallel_chunks(count, [&](std::size_t b, std::size_t e) {
+        bool any = false;
+        for (std::size_t i = b; i < e; ++i) {
+            p.re[i] = v[i].real();
+            p.im[i] = v[i].imag();
+            any = any || v[i].imag() != 0.0;
+        }
+        if (any) flag[0] = 1;  // benign race: every writer stores the same value
+    });
+    p.any_im = flag[0] != 0;
+    return p;
+}
+
+inline void merge(const std::vector<double>& re, const std::vector<double>& im, cplx* out) {
+    parallel_chunks(re.size(), [&](std::size_t b, std::size_t e) {
+        for (std::size_t i = b; i < e; ++i) out[i] = cplx(re[i], im[i]);
+    });
+}
+
+struct Csr {
+    std::vector<int64_t> rowptr;
+    std::vector<int32_t> cols;
+    Planar val;
+};
+
+inline Csr to_csr(const ComplexMatrix& a) {
+    if (a.rows() >= (std::size_t(1) << 31)) throw std::invalid_argument("csr: more than 2^31 columns");
+    Csr c;
+    c.rowptr.assign(a.row_offsets().begin(), a.row_offsets().end());
+    c.cols.assign(a.col_indices().begin(), a.col_indices().end());
+    c.val = split(a.values().data(), a.values().size());
+    return c;
+}
+
+}  // namespace ipt::api

@@ -1,0 +1,253 @@
+// Solver entry points of the drop-in API (proj/include/ipt/solver.hpp) on the B200.
+// Validation and exception behaviour follow proj/src/solver.cpp:18-45; every
+// product, map application and reduction runs on the device via include/ipt_cuda.h.
+#include "ipt/solver.hpp"
+
+#include <cstdlib>
+#include <memory>
+
+#include "api_internal.hpp"
+#include "ipt/kernels.hpp"
+
+namespace ipt {
+
+namespace api {
+
+namespace {
+thread_local int t_device = -1;
+struct CtxHolder {
+    ipt_ctx* ctx = nullptr;
+    int device = -1;
+    ~CtxHolder() {
+        if (ctx) ipt_ctx_destroy(ctx);
+    }
+};
+thread_local CtxHolder t_ctx;
+}  // namespace
+
+void set_device(int device) { t_device = device; }
+
+ipt_ctx* context() {
+    int dev = t_device;
+    if (dev < 0) {
+        const char* env = std::getenv("IPT_DEVICE");
+        dev = env ? std::atoi(env) : 0;
+    }
+    if (t_ctx.ctx == nullptr || t_ctx.device != dev) {
+        if (t_ctx.ctx) ipt_ctx_destroy(t_ctx.ctx);
+        t_ctx.ctx = nullptr;
+        check(ipt_ctx_create(dev, &t_ctx.ctx));
+        t_ctx.device = dev;
+    }
+    return t_ctx.ctx;
+}
+
+unsigned host_threads() {
+    static const unsigned t = [] {
+        const char* env = std::getenv("IPT_THREADS");
+        const int v = env ? std::atoi(env) : 0;
+        if (v > 0) return static_cast<unsigned>(v);
+        const unsigned h = std::thread::hardware_concurrency();
+        return h ? h : 8u;
+    }();
+    return t;
+}
+
+}  // namespace api
+
+namespace {
+
+using api::Planar;
+
+void validate(const IterationConfig& cfg) {
+    if (!(cfg.tolerance > 0.0)) throw std::invalid_argument("config: tolerance must be positive");
+    if (cfg.max_iterations <= 0) throw std::invalid_argument("config: max_iterations must be positive");
+    if (!(cfg.divergence_threshold > 1.0)) throw std::invalid_argument("config: divergence_threshold must exceed 1");
+}
+
+void check_anchor(const Partition& p, const InverseGaps& g, std::size_t anchor) {
+    if (p.size() != g.size()) throw std::invalid_argument("solver: partition/gaps size mismatch");
+    if (p.delta.rows() != p.size() || p.delta.cols() != p.size())
+        throw std::invalid_argument("solver: residual must be square of matching size");
+    if (anchor >= p.size()) throw std::invalid_argument("solver: anchor out of range");
+}
+
+ipt_params to_params(const IterationConfig& cfg) {
+    ipt_params prm;
+    ipt_default_params(&prm);
+    prm.tolerance = cfg.tolerance;
+    prm.max_iterations = cfg.max_iterations;
+    prm.divergence_threshold = cfg.divergence_threshold;
+    prm.record_trace = cfg.record_trace ? 1 : 0;
+    return prm;
+}
+
+cvec combine(const std::vector<double>& re, const std::vector<double>& im) {
+    cvec out(re.size());
+    api::merge(re, im, out.data());
+    return out;
+}
+
+// Delta as a dense planar operator (a CSR partition is densified for the full map).
+Planar dense_delta(const Partition& p) {
+    if (p.delta.is_dense()) return api::split(p.delta.data(), p.size() * p.size());
+    const ComplexMatrix dd = p.delta.to_dense();
+    return api::split(dd.data(), p.size() * p.size());
+}
+
+EigenpairResult run_single(const Partition& p, std::size_t anchor, const IterationConfig& cfg, const cvec* warm,
+                           int schedule, double alpha) {
+    const std::size_t n = p.size();
+    const Planar d = api::split(p.d.data(), n);
+    Planar w;
+    if (warm) {
+        if (warm->size() != n) throw std::invalid_argument("solver: warm start size mismatch");
+        if ((*warm)[anchor] == cplx{}) throw std::invalid_argument("solver: warm start has zero anchor coordinate");
+        w = api::split(warm->data(), n);
+    }
+    ipt_params prm = to_params(cfg);
+    prm.schedule = schedule;
+    prm.shrink_alpha = alpha;
+    ipt_stats st{};
+    std::vector<double> trace(cfg.record_trace ? cfg.max_iterations : 0);
+    st.trace = cfg.record_trace ? trace.data() : nullptr;
+    std::vector<double> zr(n), zi(n);
+    const double* wre = warm ? w.re.data() : nullptr;
+    const double* wim = warm ? w.im_or_null() : nullptr;
+    if (p.delta.is_sparse()) {
+        const api::Csr c = api::to_csr(p.delta);
+        api::check(ipt_single_solve_csr(api::context(), static_cast<int64_t>(n), d.re.data(), d.im_or_null(),
+                                        c.rowptr.data(), c.cols.data(), c.val.re.data(), c.val.im_or_null(),
+                                        static_cast<int64_t>(anchor), wre, wim, &prm, zr.data(), zi.data(), &st));
+    } else {
+        const Planar a = api::split(p.delta.data(), n * n);
+        api::check(ipt_single_solve_dense(api::context(), static_cast<int64_t>(n), d.re.data(), d.im_or_null(),
+                                          a.re.data(), a.im_or_null(), static_cast<int64_t>(anchor), wre, wim, &prm,
+                                          zr.data(), zi.data(), &st));
+    }
+    EigenpairResult r;
+    r.z = combine(zr, zi);
+    r.eigenvalue = cplx(st.eigenvalue_re, st.eigenvalue_im);
+    r.anchor = anchor;
+    r.iterations = st.iterations;
+    r.final_step = st.final_step;
+    r.residual = st.residual;
+    r.status = static_cast<SolveStatus>(st.status);
+    r.matvec_count = static_cast<long>(st.product_count);
+    if (cfg.record_trace) r.trace.assign(trace.begin(), trace.begin() + st.iterations);
+    return r;
+}
+
+}  // namespace
+
+const char* to_string(SolveStatus s) {
+    switch (s) {
+        case SolveStatus::Converged: return "converged";
+        case SolveStatus::MaxIterations: return "max_iterations";
+        case SolveStatus::Diverged: return "diverged";
+    }
+    return "unknown";
+}
+
+cvec apply_map_single(const Partition& p, const InverseGaps& g, std::size_t anchor, const cvec& z) {
+    check_anchor(p, g, anchor);
+    const std::size_t n = p.size();
+    if (z.size() != n) throw std::invalid_argument("apply_map_single: size mismatch");
+    const Planar d = api::split(p.d.data(), n), a = dense_delta(p), zz = api::split(z.data(), n);
+    std::vector<double> fr(n), fi(n);
+    api::check(ipt_apply_map_single_dense(api::context(), static_cast<int64_t>(n), d.re.data(), d.im_or_null(),
+                                          a.re.data(), a.im_or_null(), static_cast<int64_t>(anchor), zz.re.data(),
+                                          zz.im_or_null(), fr.data(), fi.data()));
+    return combine(fr, fi);
+}
+
+EigenpairResult solve_single(const Partition& p, const InverseGaps& g, std::size_t anchor,
+                             const IterationConfig& config, const cvec* warm_start) {
+    validate(config);
+    check_anchor(p, g, anchor);
+    return run_single(p, anchor, config, warm_start, IPT_SCHEDULE_PLAIN, 0.9);
+}
+
+EigenpairResult solve_single_continuation(const Partition& p, const InverseGaps& g, std::size_t anchor,
+                                          const IterationConfig& config, double shrink_alpha) {
+    if (!(shrink_alpha >= 0.0 && shrink_alpha < 1.0))
+        throw std::invalid_argument("continuation: shrink factor must lie in [0, 1)");
+    validate(config);
+    check_anchor(p, g, anchor);
+    return run_single(p, anchor, config, nullptr, IPT_SCHEDULE_CONTINUATION, shrink_alpha);
+}
+
+ComplexMatrix apply_map_full(const Partition& p, const InverseGaps& g, const ComplexMatrix& Z) {
+    check_anchor(p, g, 0);
+    if (Z.rows() != p.size() || Z.cols() != p.size()) throw std::invalid_argument("apply_map_full: size mismatch");
+    const std::size_t n = p.size();
+    const ComplexMatrix zd = Z.to_dense();
+    const Planar d = api::split(p.d.data(), n), a = dense_delta(p), zz = api::split(zd.data(), n * n);
+    std::vector<double> fr(n * n), fi(n * n);
+    api::check(ipt_apply_map_full(api::context(), static_cast<int64_t>(n), d.re.data(), d.im_or_null(), a.re.data(),
+                                  a.im_or_null(), zz.re.data(), zz.im_or_null(), fr.data(), fi.data()));
+    ComplexMatrix out = ComplexMatrix::dense(n, n);
+    api::merge(fr, fi, out.data());
+    return out;
+}
+
+namespace b200 {
+
+void set_device(int device) { api::set_device(device); }
+
+SpectrumResult solve_full(const Partition& p, const InverseGaps& g, const IterationConfig& config,
+                          const FullOptions& options, const ComplexMatrix* warm_start) {
+    validate(config);
+    check_anchor(p, g, 0);
+    const std::size_t n = p.size();
+    const Planar d = api::split(p.d.data(), n), a = dense_delta(p);
+    Planar w;
+    ComplexMatrix wd;
+    if (warm_start) {
+        wd = warm_start->to_dense();
+        if (wd.rows() != n || wd.cols() != n) throw std::invalid_argument("solve_full: warm start size mismatch");
+        w = api::split(wd.data(), n * n);
+    }
+    ipt_params prm = to_params(config);
+    prm.stop_rule = options.stop_rule == StopRule::MaxAbs ? IPT_STOP_MAX_ABS : IPT_STOP_REL_FRO;
+    prm.want_sigma_min = options.want_sigma_min ? 1 : 0;
+    ipt_stats st{};
+    std::vector<double> trace(config.record_trace ? config.max_iterations : 0);
+    st.trace = config.record_trace ? trace.data() : nullptr;
+    std::vector<double> zr(n * n), zi(n * n), lr(n), li(n);
+    api::check(ipt_full_solve(api::context(), static_cast<int64_t>(n), d.re.data(), d.im_or_null(), a.re.data(),
+                              a.im_or_null(), warm_start ? w.re.data() : nullptr, warm_start ? w.im_or_null() : nullptr,
+                              &prm, zr.data(), zi.data(), lr.data(), li.data(), &st));
+    SpectrumResult r;
+    r.Z = ComplexMatrix::dense(n, n);
+    api::merge(zr, zi, r.Z.data());
+    r.eigenvalues = combine(lr, li);
+    r.iterations = st.iterations;
+    r.final_step = st.final_step;
+    r.residual_frobenius = st.residual;
+    r.min_singular_value_estimate = st.min_singular_value_estimate;
+    r.status = static_cast<SolveStatus>(st.status);
+    r.matmul_count = static_cast<long>(st.product_count);
+    if (config.record_trace) r.trace.assign(trace.begin(), trace.begin() + st.iterations);
+    return r;
+}
+
+}  // namespace b200
+
+SpectrumResult solve_full(const Partition& p, const InverseGaps& g, const IterationConfig& config,
+                          const ComplexMatrix* warm_start) {
+    return b200::solve_full(p, g, config, b200::FullOptions{}, warm_start);
+}
+
+double smallest_singular_value_estimate(const ComplexMatrix& z, int max_iters, double tol) {
+    const std::size_t n = z.rows();
+    if (n == 0 || z.cols() != n) throw std::invalid_argument("smallest_singular_value_estimate: square input required");
+    const ComplexMatrix zd = z.to_dense();
+    const Planar zz = api::split(zd.data(), n * n);
+    double out = 0.0;
+    api::check(ipt_sigma_min(api::context(), static_cast<int64_t>(n), zz.re.data(), zz.im_or_null(), max_iters, tol,
+                             &out));
+    return out;
+}
+
+}  // namespace ipt
