@@ -1,24 +1,63 @@
-// Host launchers for the K1 DMMA GEMM (dmma_gemm.cuh).
+// Host launchers for the K1 DMMA GEMM (dmma_gemm.cuh): TMA descriptor encoding
+// (cuTensorMapEncodeTiled through the runtime's driver entry point, no -lcuda)
+// and the per-mode kernel launch.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "dmma_gemm.cuh"
 #include "ipt_internal.cuh"
 
 namespace iptb {
 
 namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    IPT_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || p == nullptr) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// K-major operand: `outer` rows of `inner` contiguous doubles, row pitch ld doubles;
+// boxes of 16 doubles (128 B, the swizzle span) x 128 rows, 128-byte swizzle.
+CUtensorMap make_map(const double* base, int64_t inner, int64_t outer, int64_t ld) {
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (ld * 8) % 16 != 0)
+    throw InvalidArgument("gemm: TMA operands need 16-byte aligned base and pitch");
+  CUtensorMap m;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * sizeof(double)};
+  cuuint32_t box[2] = {kBK, kBM};
+  cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return m;
+}
+
 template <int MODE>
 void launch_mode(const GemmParams& p, cudaStream_t s) {
-  static bool configured = false;  // per-device attribute; all devices get the same value
-  if (!configured) {
-    IPT_CUDA(cudaFuncSetAttribute(dmma_gemm_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static std::once_flag once;
+  std::call_once(once, [] {
+    IPT_CUDA(cudaFuncSetAttribute(dmma_tma_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kGemmSmemBytes)));
-    configured = true;
-  }
+  });
   const unsigned grid = static_cast<unsigned>(p.tiles_m) * static_cast<unsigned>(p.tiles_n);
   if (grid == 0) return;
-  dmma_gemm_kernel<MODE><<<grid, kGemmThreads, kGemmSmemBytes, s>>>(p);
+  const CUtensorMap ma = make_map(p.A, p.K, int64_t(p.tiles_m) * kBM, p.lda);
+  const CUtensorMap mb = make_map(p.B, p.K, int64_t(p.tiles_n) * kBN, p.ldb);
+  dmma_tma_kernel<MODE><<<grid, kGemmThreads, kGemmSmemBytes, s>>>(ma, mb, p);
   IPT_LAUNCH_CHECK();
   count_launch();
 }
+
 }  // namespace
 
 size_t gemm_tiles(int64_t rows, int64_t cols) {
@@ -26,6 +65,7 @@ size_t gemm_tiles(int64_t rows, int64_t cols) {
 }
 
 void launch_gemm(int mode, const GemmParams& p, cudaStream_t s) {
+  if (p.K % kBK != 0) throw InvalidArgument("launch_gemm: K must be a multiple of 16");
   switch (mode) {
     case kGemmStore: launch_mode<kGemmStore>(p, s); break;
     case kGemmMap: launch_mode<kGemmMap>(p, s); break;

@@ -1,11 +1,11 @@
 // K1: FP64 tensor-core (DMMA) TN GEMM for sm_100a with the IPT map epilogue.
 //
 // C[i, j] = sum_k A[i, k] * B[k, j]
-//   A : M x K row-major (K contiguous)      -> Delta, rows of the operator
-//   B : K x Ncols column-major (K contiguous)-> Z, the current eigenbasis block
+//   A : M x K row-major (K contiguous)       -> Delta, rows of the operator
+//   B : K x Ncols column-major (K contiguous) -> Z, the current eigenbasis block
 // Both operands are K-major, which is the `.row.col` form of
-// mma.sync.aligned.m16n8k4.row.col.f64 (8x8x4 DMMA in SASS). tcgen05 has no
-// f64 kind, so on B200 the FP64 tensor path is the warp-level DMMA; measured
+// mma.sync.aligned.m16n8k4.row.col.f64 (SASS DMMA.8x8x4). tcgen05 has no f64
+// kind, so on B200 the FP64 tensor path is the warp-level DMMA; measured issue
 // peak 37.1 TFLOP/s (profiles/r01_fp64_probe.txt).
 //
 // Epilogue modes (fused, no W = Delta Z round trip through HBM):
@@ -17,12 +17,18 @@
 //                -> proj/src/solver.cpp:258-267
 //   kGemmSub   : C -= W (blocked Cholesky trailing update, lower tiles only)
 //
-// Tiling: CTA 128x128, BK = 16 doubles, 4-stage cp.async pipeline into a
-// 128-byte-XOR-swizzled shared layout (conflict-free fragment reads), 8 warps
-// each owning a 64x32 accumulator tile (64 doubles / thread). All operands are
-// zero-padded by the caller to whole tiles, so the main loop has no bounds
-// checks; only the epilogue is predicated on the true (n_rows, n_cols).
+// Main loop (dmma_tma_kernel): CTA tile 128x128, BK = 16 doubles, a 6-stage
+// TMA pipeline (cp.async.bulk.tensor with 128-byte swizzle, one producer warp,
+// full/empty mbarriers) feeding 8 consumer warps, each owning a 64x32
+// accumulator tile (64 doubles / thread). Within a k-tile, mma slot t of step kk
+// takes k = 8*(t>>1) + 2*kk + (t&1): with the TMA 128B swizzle (16-byte unit u of
+// row r stored at u ^ (r&7)) every LDS.64 fragment phase then hits all 32 banks
+// once. The k order inside a tile is a permutation, so A and B agree and the sum
+// is unchanged. All operands are zero-padded by the caller to whole tiles, so the
+// main loop has no bounds checks; only the epilogue is predicated.
 #pragma once
+
+#include <cuda.h>
 
 #include "ipt_common.cuh"
 
@@ -33,11 +39,13 @@ enum GemmMode : int { kGemmStore = 0, kGemmMap = 1, kGemmResid = 2, kGemmSub = 3
 constexpr int kBM = 128;
 constexpr int kBN = 128;
 constexpr int kBK = 16;
-constexpr int kStages = 4;
-constexpr int kGemmThreads = 256;
+constexpr int kStages = 6;
+constexpr int kConsumerWarps = 8;
+constexpr int kGemmThreads = (kConsumerWarps + 1) * 32;  // + 1 TMA producer warp
 constexpr int kGroupM = 8;  // tile-row group for L2-friendly rasterisation
-constexpr int kStageDoubles = (kBM + kBN) * kBK;
-constexpr size_t kGemmSmemBytes = size_t(kStages) * kStageDoubles * sizeof(double);
+constexpr int kTileDoubles = kBM * kBK;                   // one operand tile = 16 KB
+constexpr int kStageBytes = 2 * kTileDoubles * 8;         // A + B
+constexpr size_t kGemmSmemBytes = size_t(kStages) * kStageBytes + 1024 /*align*/ + 2 * kStages * 8;
 
 struct GemmParams {
   int64_t K;                // loop length, multiple of kBK, operands zero-padded to it
@@ -48,6 +56,7 @@ struct GemmParams {
   double* C;
   int64_t ldc;
   int tiles_m, tiles_n;
+  int lower_only;           // symmetric result: compute only tiles with tile_n <= tile_m
   // IPT epilogue inputs
   const double* d;          // diagonal of M, global row/column index
   const double* wd;         // (Delta Z)_jj per local column
@@ -59,15 +68,7 @@ struct GemmParams {
   const LoopState* state;   // nullable; CTA exits if state->done
 };
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
+// ------------------------------------------------------------------ PTX helpers
 
 __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
   asm volatile(
@@ -77,11 +78,36 @@ __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
-// Element (r, k) of a 16-double-wide shared tile row. A fragment read covers rows
-// g = 0..7 x k0..k0+3 (one 32-byte unit pair per row); XORing the unit index with
-// 2*(r&3) sends the four rows of each half-warp phase to four distinct unit pairs,
-// i.e. all 32 banks once per phase (conflict-free LDS.64).
-__device__ __forceinline__ int swz(int r, int k) { return r * kBK + ((((k >> 1) ^ ((r & 3) << 1)) << 1) | (k & 1)); }
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
 
 // Grouped rasterisation: kGroupM tile-rows at a time, column-major inside the group,
 // so the ~148 co-resident CTAs share a few Delta row panels and Z column panels in L2.
@@ -95,87 +121,16 @@ __device__ __forceinline__ void tile_coords(int lin, int tiles_m, int tiles_n, i
   tn = in / gsize;
 }
 
+// Element (r, k) of a TMA SWIZZLE_128B tile with 16-double (128-byte) rows.
+__device__ __forceinline__ int swz128(int r, int k) { return r * kBK + ((((k >> 1) ^ (r & 7)) << 1) | (k & 1)); }
+
+// ------------------------------------------------------------------ epilogue
+
 template <int MODE>
-__global__ void __launch_bounds__(kGemmThreads, 1) dmma_gemm_kernel(const GemmParams p) {
-  if (p.state != nullptr && p.state->done) return;
-  extern __shared__ __align__(128) double smem[];
-
-  int tm, tn;
-  tile_coords(blockIdx.x, p.tiles_m, p.tiles_n, tm, tn);
-  if (MODE == kGemmSub && tn > tm) return;  // strictly-upper tiles of a symmetric update
-  const int64_t m0 = int64_t(tm) * kBM, n0 = int64_t(tn) * kBN;
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+__device__ __forceinline__ void gemm_epilogue(const GemmParams& p, double (&acc)[4][4][4], int64_t m0,
+                                              int64_t n0, int warp, int lane, double v[4]) {
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps, 64 x 32 each
-
-  const double* __restrict__ Ag = p.A + m0 * p.lda;
-  const double* __restrict__ Bg = p.B + n0 * p.ldb;
-  const int KT = static_cast<int>(p.K / kBK);
-
-  auto load_stage = [&](int s, int kt) {
-    double* as = smem + s * kStageDoubles;
-    double* bs = as + kBM * kBK;
-    const int64_t k0 = int64_t(kt) * kBK;
-#pragma unroll
-    for (int i = 0; i < (kBM * kBK / 2) / kGemmThreads; ++i) {
-      const int c = tid + i * kGemmThreads;
-      const int row = c >> 3, u = c & 7;
-      cp_async16(as + row * kBK + ((u ^ ((row & 3) << 1)) << 1), Ag + row * p.lda + k0 + u * 2);
-    }
-#pragma unroll
-    for (int i = 0; i < (kBN * kBK / 2) / kGemmThreads; ++i) {
-      const int c = tid + i * kGemmThreads;
-      const int col = c >> 3, u = c & 7;
-      cp_async16(bs + col * kBK + ((u ^ ((col & 3) << 1)) << 1), Bg + col * p.ldb + k0 + u * 2);
-    }
-  };
-
-  double acc[4][4][4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
-
-#pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) {
-    if (s < KT) load_stage(s, s);
-    cp_async_commit();
-  }
-
-  for (int kt = 0; kt < KT; ++kt) {
-    cp_async_wait<kStages - 2>();
-    __syncthreads();
-    {
-      const int nk = kt + kStages - 1;
-      if (nk < KT) load_stage(nk % kStages, nk);
-      cp_async_commit();
-    }
-    const double* as = smem + (kt % kStages) * kStageDoubles;
-    const double* bs = as + kBM * kBK;
-#pragma unroll
-    for (int kk = 0; kk < kBK / 4; ++kk) {
-      const int k = kk * 4 + t;
-      double af[4][2], bf[4];
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi) {
-        const int r = wm * 64 + mi * 16 + g;
-        af[mi][0] = as[swz(r, k)];
-        af[mi][1] = as[swz(r + 8, k)];
-      }
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni) bf[ni] = bs[swz(wn * 32 + ni * 8 + g, k)];
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma_16x8x4(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
-    }
-  }
-  cp_async_wait<0>();
-
-  // ------------------------------ epilogue ------------------------------
+  const int wm = warp >> 2, wn = warp & 3;
   if (MODE == kGemmStore || MODE == kGemmSub) {
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
@@ -193,9 +148,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1) dmma_gemm_kernel(const GemmPa
         }
     return;
   }
-
-  __shared__ double red[kGemmThreads / 32][4];
-  double v[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
@@ -232,7 +184,97 @@ __global__ void __launch_bounds__(kGemmThreads, 1) dmma_gemm_kernel(const GemmPa
           }
         }
     }
-  block_reduce4<kGemmThreads / 32>(v, red);
+}
+
+// ------------------------------------------------------------------ TMA pipeline kernel
+
+template <int MODE>
+__global__ void __maxnreg__(224)  // 9 warps x 224 regs fit the 64K register file (1 CTA / SM)
+    dmma_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const GemmParams p) {
+  if (p.state != nullptr && p.state->done) return;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte alignment for the 128B swizzle atoms
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  double* tiles = reinterpret_cast<double*>(base);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + size_t(kStages) * kStageBytes);
+  uint64_t* empty = full + kStages;
+
+  int tm, tn;
+  tile_coords(blockIdx.x, p.tiles_m, p.tiles_n, tm, tn);
+  if ((MODE == kGemmSub || p.lower_only) && tn > tm) return;  // strictly-upper tiles of a symmetric result
+  const int64_t m0 = int64_t(tm) * kBM, n0 = int64_t(tn) * kBN;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int KT = static_cast<int>(p.K / kBK);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  __shared__ double red[kConsumerWarps + 1][4];
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+
+  if (warp == kConsumerWarps) {
+    // ---------------- TMA producer (one elected lane)
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % kStages;
+        const uint32_t phase = (kt / kStages) & 1;
+        mbar_wait(&empty[s], phase ^ 1);  // fresh barrier: parity 1 counts as completed
+        double* as = tiles + size_t(s) * 2 * kTileDoubles;
+        mbar_expect_tx(&full[s], kStageBytes);
+        tma_load_2d(as, &tmA, &full[s], kt * kBK, static_cast<int>(m0));
+        tma_load_2d(as + kTileDoubles, &tmB, &full[s], kt * kBK, static_cast<int>(n0));
+      }
+    }
+  } else {
+    // ---------------- 8 DMMA consumer warps
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps, 64 x 32 each
+    double acc[4][4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
+    const int kt0 = 8 * (t >> 1) + (t & 1);
+    for (int kt = 0; kt < KT; ++kt) {
+      const int s = kt % kStages;
+      mbar_wait(&full[s], (kt / kStages) & 1);
+      const double* as = tiles + size_t(s) * 2 * kTileDoubles;
+      const double* bs = as + kTileDoubles;
+#pragma unroll
+      for (int kk = 0; kk < kBK / 4; ++kk) {
+        const int k = kt0 + 2 * kk;
+        double af[4][2], bf[4];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+          const int r = wm * 64 + mi * 16 + g;
+          af[mi][0] = as[swz128(r, k)];
+          af[mi][1] = as[swz128(r + 8, k)];
+        }
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) bf[ni] = bs[swz128(wn * 32 + ni * 8 + g, k)];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) dmma_16x8x4(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    gemm_epilogue<MODE>(p, acc, m0, n0, warp, lane, v);
+  }
+  if (MODE == kGemmStore || MODE == kGemmSub) return;
+  block_reduce4<kConsumerWarps + 1>(v, red);
   if (threadIdx.x == 0) {
     double* out = p.partials + size_t(blockIdx.x) * 4;
     out[0] = v[0];

@@ -99,6 +99,7 @@ void ipt_ctx_destroy(ipt_ctx* ctx) {
   if (ctx->c.comm) ncclCommDestroy(ctx->c.comm);
   for (auto& e : ctx->c.ev) cudaEventDestroy(e);
   if (ctx->c.h_state) cudaFreeHost(ctx->c.h_state);
+  release_staging(ctx->c);
   if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
   delete ctx;
 }

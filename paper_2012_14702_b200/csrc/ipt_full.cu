@@ -355,7 +355,7 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
 
   P->A1.alloc(size_t(P->rows_pad) * P->lda);
   if (!P->cplx) {
-    upload_rowmajor(s, P->A1.get(), P->lda, delta_re, n, n, n);
+    h2d_rows(c, P->A1.get(), P->lda, delta_re, n, n, n);  // pinned, double-buffered
   } else {
     P->A2.alloc(size_t(P->rows_pad) * P->lda);
     // A1 = [Dr | -Di], A2 = [Di | Dr]
@@ -644,8 +644,7 @@ void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, d
       continue;
     }
     transpose_to_rowmajor(s, zsrc + (part ? P.ld : 0), P.ldz, n, n, rm.get(), n);
-    IPT_CUDA(cudaMemcpyAsync(dst, rm.get(), sizeof(double) * n * n, cudaMemcpyDeviceToHost, s));
-    c.sync();
+    d2h_rows(c, dst, n, rm.get(), n, n, n);  // pinned, double-buffered
   }
 }
 

@@ -45,6 +45,10 @@ struct Ctx {
   int rank = 0, nranks = 1;
   LoopState* h_state = nullptr;  // pinned mirror of the device loop state
   cudaEvent_t ev[4] = {};
+  // pinned double-buffered staging for pageable host <-> device transfers
+  double* stage[2] = {nullptr, nullptr};
+  size_t stage_doubles = 0;
+  cudaEvent_t stage_ev[2] = {};
   void sync() { IPT_CUDA(cudaStreamSynchronize(stream)); }
   // column range of this rank for an n-column sharded operand
   void shard(int64_t n, int64_t& c0, int64_t& c1) const {
@@ -82,6 +86,15 @@ void fill_zero(cudaStream_t s, double* p, size_t count);
 void reduce_partials(cudaStream_t s, const double* partials, int64_t count, double* out4,
                      const LoopState* state);
 void scale_copy(cudaStream_t s, const double* src, double* dst, size_t count, double factor);
+
+// Pageable host <-> device copies of row blocks through the context's pinned double
+// buffer (multithreaded host memcpy overlapped with the DMA); synchronous on return.
+// Host rows have pitch spitch (doubles), device rows pitch dpitch.
+void h2d_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t rows,
+              int64_t cols);
+void d2h_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t rows,
+              int64_t cols);
+void release_staging(Ctx& c);
 
 // Full-spectrum problem (ipt_full.cu)
 struct FullProblem;

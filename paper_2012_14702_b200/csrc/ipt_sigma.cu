@@ -135,7 +135,7 @@ __global__ void absmax_kernel(const double* __restrict__ H, int64_t ldh, int64_t
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m * m;
        e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t c = e / m, r = e % m;
-    v[3] = nan_max(v[3], fabs(H[c * ldh + r]));
+    if (r >= c) v[3] = nan_max(v[3], fabs(H[c * ldh + r]));  // symmetric: lower triangle only
   }
   block_reduce4<8>(v, red);
   if (threadIdx.x == 0) out[blockIdx.x * 4 + 3] = v[3], out[blockIdx.x * 4 + 0] = 0.0,
@@ -270,7 +270,22 @@ double sigma_min_device(Ctx& c, int64_t n, const double* zr, const double* zi, i
   const int64_t ldh = round_up(m, 16);
   DevBuf H;
   H.alloc(size_t(ldh) * m, false);
-  gemm_tn_store(s, m, m, ld, Z, ld, Z, ld, H.get(), ldh);
+  {  // H = Z^T Z, lower tiles only (the Cholesky below reads the lower triangle): SYRK
+    GemmParams g{};
+    g.K = ld;
+    g.A = Z;
+    g.lda = ld;
+    g.B = Z;
+    g.ldb = ld;
+    g.C = H.get();
+    g.ldc = ldh;
+    g.tiles_m = static_cast<int>(ceil_div(m, kBM));
+    g.tiles_n = g.tiles_m;
+    g.lower_only = 1;
+    g.n_rows = m;
+    g.n_cols = m;
+    launch_gemm(kGemmStore, g, s);
+  }
 
   DevBuf scratch;
   scratch.alloc(1184 * 4 + 8);

@@ -615,9 +615,7 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
   if (!csr) {
     P->lda = round_up(n, 16);
     P->A.alloc(size_t(std::max<int64_t>(rows, 1)) * P->lda);
-    if (rows)
-      IPT_CUDA(cudaMemcpy2DAsync(P->A.get(), P->lda * sizeof(double), dense_re + P->r0 * n,
-                                 n * sizeof(double), n * sizeof(double), rows, cudaMemcpyHostToDevice, s));
+    if (rows) h2d_rows(c, P->A.get(), P->lda, dense_re + P->r0 * n, n, rows, n);  // pinned, double-buffered
     if (P->cplx && dense_im) {
       P->Ai.alloc(size_t(std::max<int64_t>(rows, 1)) * P->lda);
       if (rows)

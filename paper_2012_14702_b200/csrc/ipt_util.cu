@@ -1,4 +1,9 @@
 // Small device utilities: buffers, transposes, deterministic partial reduction.
+#include <algorithm>
+#include <cstring>
+#include <thread>
+#include <vector>
+
 #include "ipt_internal.cuh"
 
 namespace iptb {
@@ -21,6 +26,115 @@ void DevBuf::release() {
   if (p) cudaFree(p);
   p = nullptr;
   count = 0;
+}
+
+// ----------------------------------------------------------- staged transfers
+
+namespace {
+constexpr size_t kStageBytes = size_t(64) << 20;  // per buffer
+
+void ensure_staging(Ctx& c) {
+  if (c.stage[0]) return;
+  for (int b = 0; b < 2; ++b) {
+    IPT_CUDA(cudaMallocHost(&c.stage[b], kStageBytes));
+    IPT_CUDA(cudaEventCreateWithFlags(&c.stage_ev[b], cudaEventDisableTiming));
+  }
+  c.stage_doubles = kStageBytes / sizeof(double);
+}
+
+unsigned copy_threads() {
+  const unsigned h = std::thread::hardware_concurrency();
+  return std::max(1u, std::min(16u, h ? h : 8u));
+}
+
+// rows x cols doubles between two pitched host arrays, split over host threads
+void host_copy_rows(double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t rows, int64_t cols) {
+  const unsigned t = rows * cols >= (int64_t(1) << 18) ? copy_threads() : 1u;
+  auto work = [&](int64_t r0, int64_t r1) {
+    if (dpitch == cols && spitch == cols) {
+      std::memcpy(dst + r0 * dpitch, src + r0 * spitch, sizeof(double) * (r1 - r0) * cols);
+    } else {
+      for (int64_t r = r0; r < r1; ++r) std::memcpy(dst + r * dpitch, src + r * spitch, sizeof(double) * cols);
+    }
+  };
+  if (t <= 1 || rows < int64_t(t)) {
+    work(0, rows);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const int64_t step = (rows + t - 1) / t;
+  for (unsigned k = 0; k < t; ++k) {
+    const int64_t a = k * step, b = std::min(rows, a + step);
+    if (a < b) pool.emplace_back(work, a, b);
+  }
+  for (auto& th : pool) th.join();
+}
+}  // namespace
+
+void release_staging(Ctx& c) {
+  for (int b = 0; b < 2; ++b) {
+    if (c.stage[b]) cudaFreeHost(c.stage[b]);
+    if (c.stage_ev[b]) cudaEventDestroy(c.stage_ev[b]);
+    c.stage[b] = nullptr;
+    c.stage_ev[b] = nullptr;
+  }
+  c.stage_doubles = 0;
+}
+
+void h2d_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t rows,
+              int64_t cols) {
+  if (rows <= 0 || cols <= 0) return;
+  ensure_staging(c);
+  const int64_t per = std::max<int64_t>(1, static_cast<int64_t>(c.stage_doubles) / cols);
+  if (per < 1 || cols > static_cast<int64_t>(c.stage_doubles)) {  // a row larger than a buffer
+    IPT_CUDA(cudaMemcpy2DAsync(dst, dpitch * sizeof(double), src, spitch * sizeof(double), cols * sizeof(double),
+                               rows, cudaMemcpyHostToDevice, c.stream));
+    c.sync();
+    return;
+  }
+  int b = 0;
+  bool used[2] = {false, false};
+  for (int64_t r0 = 0; r0 < rows; r0 += per, b ^= 1) {
+    const int64_t nr = std::min(per, rows - r0);
+    if (used[b]) IPT_CUDA(cudaEventSynchronize(c.stage_ev[b]));  // DMA of this buffer done
+    host_copy_rows(c.stage[b], cols, src + r0 * spitch, spitch, nr, cols);
+    IPT_CUDA(cudaMemcpy2DAsync(dst + r0 * dpitch, dpitch * sizeof(double), c.stage[b], cols * sizeof(double),
+                               cols * sizeof(double), nr, cudaMemcpyHostToDevice, c.stream));
+    IPT_CUDA(cudaEventRecord(c.stage_ev[b], c.stream));
+    used[b] = true;
+  }
+  c.sync();
+}
+
+void d2h_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t rows,
+              int64_t cols) {
+  if (rows <= 0 || cols <= 0) return;
+  ensure_staging(c);
+  const int64_t per = static_cast<int64_t>(c.stage_doubles) / cols;
+  if (per < 1) {
+    IPT_CUDA(cudaMemcpy2DAsync(dst, dpitch * sizeof(double), src, spitch * sizeof(double), cols * sizeof(double),
+                               rows, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    return;
+  }
+  // DMA chunk k+1 into one buffer while the host drains chunk k from the other.
+  const int64_t nchunks = (rows + per - 1) / per;
+  auto issue = [&](int64_t k) {
+    const int64_t r0 = k * per, nr = std::min(per, rows - r0);
+    const int b = static_cast<int>(k & 1);
+    IPT_CUDA(cudaMemcpy2DAsync(c.stage[b], cols * sizeof(double), src + r0 * spitch, spitch * sizeof(double),
+                               cols * sizeof(double), nr, cudaMemcpyDeviceToHost, c.stream));
+    IPT_CUDA(cudaEventRecord(c.stage_ev[b], c.stream));
+  };
+  issue(0);
+  for (int64_t k = 0; k < nchunks; ++k) {
+    if (k + 1 < nchunks) issue(k + 1);
+    const int b = static_cast<int>(k & 1);
+    IPT_CUDA(cudaEventSynchronize(c.stage_ev[b]));
+    const int64_t r0 = k * per, nr = std::min(per, rows - r0);
+    host_copy_rows(dst + r0 * dpitch, dpitch, c.stage[b], cols, nr, cols);
+  }
+  c.sync();
 }
 
 // 32x32 tiles through shared memory; src column-major (element (r, c) at c*ld_src + r),
