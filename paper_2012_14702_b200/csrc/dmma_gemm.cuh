@@ -18,8 +18,9 @@
 //   kGemmSub   : C -= W (blocked Cholesky trailing update, lower tiles only)
 //
 // Main loop (dmma_tma_kernel): CTA tile 128x128, BK = 16 doubles, a 6-stage
-// TMA pipeline (cp.async.bulk.tensor with 128-byte swizzle, one producer warp,
-// full/empty mbarriers) feeding 8 consumer warps, each owning a 64x32
+// TMA pipeline (cp.async.bulk.tensor with 128-byte swizzle, full/empty mbarriers;
+// thread 0 issues the loads one stage behind the consumers, so no separate
+// producer warp competes for the 255-register budget) feeding 8 warps, each owning a 64x32
 // accumulator tile (64 doubles / thread). Within a k-tile, mma slot t of step kk
 // takes k = 8*(t>>1) + 2*kk + (t&1): with the TMA 128B swizzle (16-byte unit u of
 // row r stored at u ^ (r&7)) every LDS.64 fragment phase then hits all 32 banks
@@ -41,7 +42,7 @@ constexpr int kBN = 128;
 constexpr int kBK = 16;
 constexpr int kStages = 6;
 constexpr int kConsumerWarps = 8;
-constexpr int kGemmThreads = (kConsumerWarps + 1) * 32;  // + 1 TMA producer warp
+constexpr int kGemmThreads = kConsumerWarps * 32;  // thread 0 doubles as the TMA producer
 constexpr int kGroupM = 8;  // tile-row group for L2-friendly rasterisation
 constexpr int kTileDoubles = kBM * kBK;                   // one operand tile = 16 KB
 constexpr int kStageBytes = 2 * kTileDoubles * 8;         // A + B
@@ -80,6 +81,11 @@ __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
@@ -189,7 +195,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmParams& p, double (&acc)
 // ------------------------------------------------------------------ TMA pipeline kernel
 
 template <int MODE>
-__global__ void __maxnreg__(224)  // 9 warps x 224 regs fit the 64K register file (1 CTA / SM)
+__global__ void __launch_bounds__(kGemmThreads, 1)
     dmma_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmParams p) {
   if (p.state != nullptr && p.state->done) return;
@@ -206,75 +212,104 @@ __global__ void __maxnreg__(224)  // 9 warps x 224 regs fit the 64K register fil
   const int64_t m0 = int64_t(tm) * kBM, n0 = int64_t(tn) * kBN;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KT = static_cast<int>(p.K / kBK);
+  const bool producer = threadIdx.x == 0;  // one elected thread issues every TMA
 
-  if (threadIdx.x == 0) {
+  auto issue = [&](int kt) {
+    const int s = kt % kStages;
+    double* as = tiles + size_t(s) * 2 * kTileDoubles;
+    mbar_expect_tx(&full[s], kStageBytes);
+    tma_load_2d(as, &tmA, &full[s], kt * kBK, static_cast<int>(m0));
+    tma_load_2d(as + kTileDoubles, &tmB, &full[s], kt * kBK, static_cast<int>(n0));
+  };
+
+  if (producer) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
+    for (int kt = 0; kt < kStages - 1 && kt < KT; ++kt) issue(kt);  // fill S-1 stages
   }
   __syncthreads();
 
-  __shared__ double red[kConsumerWarps + 1][4];
+  __shared__ double red[kConsumerWarps][4];
   double v[4] = {0.0, 0.0, 0.0, 0.0};
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps, 64 x 32 each
+  double acc[4][4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
 
-  if (warp == kConsumerWarps) {
-    // ---------------- TMA producer (one elected lane)
-    if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
-      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % kStages;
-        const uint32_t phase = (kt / kStages) & 1;
-        mbar_wait(&empty[s], phase ^ 1);  // fresh barrier: parity 1 counts as completed
-        double* as = tiles + size_t(s) * 2 * kTileDoubles;
-        mbar_expect_tx(&full[s], kStageBytes);
-        tma_load_2d(as, &tmA, &full[s], kt * kBK, static_cast<int>(m0));
-        tma_load_2d(as + kTileDoubles, &tmB, &full[s], kt * kBK, static_cast<int>(n0));
-      }
-    }
-  } else {
-    // ---------------- 8 DMMA consumer warps
-    const int g = lane >> 2, t = lane & 3;
-    const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps, 64 x 32 each
-    double acc[4][4][4];
+  // 32-bit shared addresses: every fragment row r of this thread has r & 7 == g, so the
+  // swizzled column offset of step kk is shared by all its A and B loads, and the
+  // rows differ by compile-time immediates (LDS [R + imm]).
+  const uint32_t tiles_u32 = smem_u32(tiles);
+  const uint32_t a_row = static_cast<uint32_t>((wm * 64 + g) * kBK * 8);
+  const uint32_t b_row = static_cast<uint32_t>(kTileDoubles * 8 + (wn * 32 + g) * kBK * 8);
+  uint32_t xo[kBK / 4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
-    const int kt0 = 8 * (t >> 1) + (t & 1);
-    for (int kt = 0; kt < KT; ++kt) {
-      const int s = kt % kStages;
-      mbar_wait(&full[s], (kt / kStages) & 1);
-      const double* as = tiles + size_t(s) * 2 * kTileDoubles;
-      const double* bs = as + kTileDoubles;
-#pragma unroll
-      for (int kk = 0; kk < kBK / 4; ++kk) {
-        const int k = kt0 + 2 * kk;
-        double af[4][2], bf[4];
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi) {
-          const int r = wm * 64 + mi * 16 + g;
-          af[mi][0] = as[swz128(r, k)];
-          af[mi][1] = as[swz128(r + 8, k)];
-        }
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) bf[ni] = bs[swz128(wn * 32 + ni * 8 + g, k)];
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma_16x8x4(acc[mi][ni], af[mi][0], af[mi][1], bf[ni]);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    }
-    gemm_epilogue<MODE>(p, acc, m0, n0, warp, lane, v);
+  for (int kk = 0; kk < kBK / 4; ++kk) {
+    const int k = 8 * (t >> 1) + (t & 1) + 2 * kk;
+    xo[kk] = static_cast<uint32_t>(((((k >> 1) ^ g) << 1) | (k & 1)) * 8);
   }
+  auto load_frags = [&](uint32_t stage_base, int kk, double (&af)[4][2], double (&bf)[4]) {
+    const uint32_t a = stage_base + a_row + xo[kk];
+    const uint32_t b = stage_base + b_row + xo[kk];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      af[mi][0] = lds_f64(a + mi * 16 * kBK * 8);
+      af[mi][1] = lds_f64(a + (mi * 16 + 8) * kBK * 8);
+    }
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) bf[ni] = lds_f64(b + ni * 8 * kBK * 8);
+  };
+
+  // Fragments are double-buffered one step ahead (the next k-tile's first step is
+  // loaded while the last step of this one is still in the DMMA pipe).
+  double af[2][4][2], bf[2][4];
+  if (KT > 0) {
+    mbar_wait(&full[0], 0);
+    load_frags(tiles_u32, 0, af[0], bf[0]);
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    // Refill the stage consumed at kt-1 with k-tile kt+S-1 once all 8 warps released it.
+    if (producer) {
+      const int nk = kt + kStages - 1;
+      if (nk < KT) {
+        if (kt >= 1) mbar_wait(&empty[(kt - 1) % kStages], ((kt - 1) / kStages) & 1);
+        issue(nk);
+      }
+    }
+    const int s = kt % kStages;
+    const uint32_t sb = tiles_u32 + static_cast<uint32_t>(s * kStageBytes);
+#pragma unroll
+    for (int kk = 0; kk < kBK / 4; ++kk) {
+      const int cur = kk & 1, nxt = cur ^ 1;
+      if (kk + 1 < kBK / 4) {
+        load_frags(sb, kk + 1, af[nxt], bf[nxt]);
+      } else if (kt + 1 < KT) {
+        const int s1 = (kt + 1) % kStages;
+        mbar_wait(&full[s1], ((kt + 1) / kStages) & 1);
+        load_frags(tiles_u32 + static_cast<uint32_t>(s1 * kStageBytes), 0, af[nxt], bf[nxt]);
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma_16x8x4(acc[mi][ni], af[cur][mi][0], af[cur][mi][1], bf[cur][ni]);
+    }
+    // all reads of stage s have landed in registers (the DMMAs above consumed them)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  gemm_epilogue<MODE>(p, acc, m0, n0, warp, lane, v);
   if (MODE == kGemmStore || MODE == kGemmSub) return;
-  block_reduce4<kConsumerWarps + 1>(v, red);
+  block_reduce4<kConsumerWarps>(v, red);
   if (threadIdx.x == 0) {
     double* out = p.partials + size_t(blockIdx.x) * 4;
     out[0] = v[0];
