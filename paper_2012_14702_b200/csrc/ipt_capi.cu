@@ -47,7 +47,7 @@ void check_ctx(ipt_ctx* ctx) {
 void upload_as_colmajor(Ctx& c, const double* host_rm, int64_t rows, int64_t cols, double* dst, int64_t ld) {
   DevBuf tmp;
   tmp.alloc(size_t(rows) * cols, false);
-  IPT_CUDA(cudaMemcpyAsync(tmp.get(), host_rm, sizeof(double) * rows * cols, cudaMemcpyHostToDevice, c.stream));
+  h2d_rows(c, tmp.get(), cols, host_rm, cols, rows, cols);
   // row-major rows x cols == column-major cols x rows; transpose to column-major rows x cols
   transpose_to_rowmajor(c.stream, tmp.get(), cols, cols, rows, dst, ld);
   c.sync();
@@ -456,9 +456,7 @@ int ipt_gemm(ipt_ctx* ctx, int64_t m, int64_t k, int64_t n, const double* a_re, 
     A1.alloc(size_t(mpad) * K);
     B.alloc(size_t(npad) * K);
     auto up2d = [&](double* dst, int64_t dpitch, const double* src) {
-      if (k == 0) return;
-      IPT_CUDA(cudaMemcpy2DAsync(dst, dpitch * sizeof(double), src, k * sizeof(double), k * sizeof(double), m,
-                                 cudaMemcpyHostToDevice, s));
+      if (k > 0) h2d_rows(c, dst, dpitch, src, k, m, k);  // pinned, double-buffered
     };
     up2d(A1.get(), K, a_re);
     if (k > 0) upload_as_colmajor(c, b_re, k, n, B.get(), K);  // column-major k x n, ld K
@@ -469,7 +467,7 @@ int ipt_gemm(ipt_ctx* ctx, int64_t m, int64_t k, int64_t n, const double* a_re, 
         up2d(A2.get(), K, a_im);
         DevBuf tmp;
         tmp.alloc(size_t(m) * k, false);
-        IPT_CUDA(cudaMemcpyAsync(tmp.get(), a_im, sizeof(double) * m * k, cudaMemcpyHostToDevice, s));
+        h2d_rows(c, tmp.get(), k, a_im, k, m, k);
         scale_copy(s, tmp.get(), tmp.get(), size_t(m) * k, -1.0);
         IPT_CUDA(cudaMemcpy2DAsync(A1.get() + ldk, K * sizeof(double), tmp.get(), k * sizeof(double),
                                    k * sizeof(double), m, cudaMemcpyDeviceToDevice, s));
@@ -481,16 +479,14 @@ int ipt_gemm(ipt_ctx* ctx, int64_t m, int64_t k, int64_t n, const double* a_re, 
     rm.alloc(size_t(m) * n, false);
     gemm_tn_store(s, m, n, K, A1.get(), K, B.get(), K, C1.get(), m);
     transpose_to_rowmajor(s, C1.get(), m, m, n, rm.get(), n);
-    IPT_CUDA(cudaMemcpyAsync(c_re, rm.get(), sizeof(double) * m * n, cudaMemcpyDeviceToHost, s));
-    c.sync();
+    d2h_rows(c, c_re, n, rm.get(), n, m, n);
     if (c_im) {
       if (!cplx) {
         std::memset(c_im, 0, sizeof(double) * m * n);
       } else {
         gemm_tn_store(s, m, n, K, A2.get(), K, B.get(), K, C1.get(), m);
         transpose_to_rowmajor(s, C1.get(), m, m, n, rm.get(), n);
-        IPT_CUDA(cudaMemcpyAsync(c_im, rm.get(), sizeof(double) * m * n, cudaMemcpyDeviceToHost, s));
-        c.sync();
+        d2h_rows(c, c_im, n, rm.get(), n, m, n);
       }
     }
   });

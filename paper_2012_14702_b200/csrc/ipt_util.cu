@@ -1,6 +1,7 @@
 // Small device utilities: buffers, transposes, deterministic partial reduction.
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -10,20 +11,41 @@ namespace iptb {
 
 std::atomic<int64_t> g_launches{0};
 
+// Device buffers come from the stream-ordered pool (cudaMallocAsync on the legacy
+// stream) so the many small, short-lived buffers of the kernels:: / apply_map entry
+// points do not pay cudaMalloc / cudaFree (a device-wide sync) per call. Every entry
+// point synchronises the library stream before its buffers are released, so a free on
+// the legacy stream never races a kernel still reading the buffer.
+namespace {
+void configure_pool_once() {
+  static std::mutex mu;
+  static bool done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = uint64_t(4) << 30;  // retain up to 4 GB of freed memory for reuse
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
+}  // namespace
+
 void DevBuf::alloc(size_t n, bool zero) {
   release();
   if (n == 0) n = 1;
-  IPT_CUDA(cudaMalloc(&p, n * sizeof(double)));
+  configure_pool_once();
+  IPT_CUDA(cudaMallocAsync(&p, n * sizeof(double), nullptr));
   count = n;
-  if (zero) {
-    // The library stream is non-blocking w.r.t. the legacy stream: finish the memset
-    // before any copy or kernel on the library stream can touch the buffer.
-    IPT_CUDA(cudaMemsetAsync(p, 0, n * sizeof(double), nullptr));
-    IPT_CUDA(cudaStreamSynchronize(nullptr));
-  }
+  if (zero) IPT_CUDA(cudaMemsetAsync(p, 0, n * sizeof(double), nullptr));
+  // The library stream is non-blocking w.r.t. the legacy stream: the allocation (and the
+  // memset) must be complete before any copy or kernel on the library stream uses it.
+  IPT_CUDA(cudaStreamSynchronize(nullptr));
 }
 void DevBuf::release() {
-  if (p) cudaFree(p);
+  if (p) cudaFreeAsync(p, nullptr);
   p = nullptr;
   count = 0;
 }

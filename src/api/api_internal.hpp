@@ -24,8 +24,62 @@ inline void check(int rc) {
     throw std::runtime_error(msg);
 }
 
+// Host scratch buffer drawn from a thread-local pool: the layout conversions at the
+// boundary reuse pages that are already faulted in instead of first-touching fresh
+// memory on every call (buffers above kPoolMax doubles are not retained).
+class Vec {
+public:
+    explicit Vec(std::size_t n = 0) { acquire(n); }
+    ~Vec() { release(); }
+    Vec(const Vec&) = delete;
+    Vec& operator=(const Vec&) = delete;
+    Vec(Vec&& o) noexcept : v_(std::move(o.v_)) {}
+    Vec& operator=(Vec&& o) noexcept {
+        release();
+        v_ = std::move(o.v_);
+        return *this;
+    }
+    void resize(std::size_t n) {
+        release();
+        acquire(n);
+    }
+    double* data() { return v_.data(); }
+    const double* data() const { return v_.data(); }
+    std::size_t size() const { return v_.size(); }
+    double& operator[](std::size_t i) { return v_[i]; }
+    const double& operator[](std::size_t i) const { return v_[i]; }
+    double* begin() { return v_.data(); }
+    double* end() { return v_.data() + v_.size(); }
+
+private:
+    static constexpr std::size_t kPoolMax = std::size_t(1) << 25;  // 256 MB
+    static constexpr std::size_t kPoolSlots = 16;
+    static std::vector<std::vector<double>>& pool() {
+        thread_local std::vector<std::vector<double>> p;
+        return p;
+    }
+    void acquire(std::size_t n) {
+        auto& p = pool();
+        std::size_t best = p.size();
+        for (std::size_t i = 0; i < p.size(); ++i)
+            if (p[i].capacity() >= n && (best == p.size() || p[i].capacity() < p[best].capacity())) best = i;
+        if (best < p.size()) {
+            v_ = std::move(p[best]);
+            p.erase(p.begin() + static_cast<std::ptrdiff_t>(best));
+        }
+        v_.resize(n);
+    }
+    void release() {
+        if (v_.capacity() == 0) return;
+        auto& p = pool();
+        if (v_.capacity() <= kPoolMax && p.size() < kPoolSlots) p.push_back(std::move(v_));
+        v_ = std::vector<double>();
+    }
+    std::vector<double> v_;
+};
+
 struct Planar {
-    std::vector<double> re, im;
+    Vec re, im;
     bool any_im = false;
     const double* im_or_null() const { return any_im ? im.data() : nullptr; }
 };
@@ -67,7 +121,7 @@ inline Planar split(const cplx* v, std::size_t count) {
     return p;
 }
 
-inline void merge(const std::vector<double>& re, const std::vector<double>& im, cplx* out) {
+inline void merge(const Vec& re, const Vec& im, cplx* out) {
     parallel_chunks(re.size(), [&](std::size_t b, std::size_t e) {
         for (std::size_t i = b; i < e; ++i) out[i] = cplx(re[i], im[i]);
     });

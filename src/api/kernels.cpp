@@ -12,12 +12,13 @@
 namespace ipt::kernels {
 
 using api::Planar;
+using api::Vec;
 
 void matvec(const ComplexMatrix& a, const cplx* x, cplx* y) {
     const std::size_t m = a.rows(), n = a.cols();
     if (m == 0) return;
     const Planar px = api::split(x, n);
-    std::vector<double> yr(m), yi(m);
+    Vec yr(m), yi(m);
     if (a.is_dense()) {
         const Planar pa = api::split(a.data(), m * n);
         api::check(ipt_matvec_dense(api::context(), static_cast<int64_t>(m), static_cast<int64_t>(n), pa.re.data(),
@@ -57,7 +58,7 @@ void adjoint_matvec_dense(const ComplexMatrix& a, const cplx* x, cplx* y) {
     const Planar px = api::split(x, m);
     Planar pa = api::split(a.data(), m * n);
     for (double& v : pa.im) v = -v;
-    std::vector<double> yr(n), yi(n);
+    Vec yr(n), yi(n);
     api::check(ipt_gemm(api::context(), 1, static_cast<int64_t>(m), static_cast<int64_t>(n), px.re.data(),
                         px.im_or_null(), pa.re.data(), pa.im_or_null(), yr.data(), yi.data()));
     for (std::size_t j = 0; j < n; ++j) y[j] = cplx(yr[j], yi[j]);
@@ -69,9 +70,10 @@ void matmul(const ComplexMatrix& a, const ComplexMatrix& b, ComplexMatrix& c) {
     if (!c.is_dense() || c.rows() != a.rows() || c.cols() != b.cols()) c = ComplexMatrix::dense(a.rows(), b.cols());
     const std::size_t m = a.rows(), k = a.cols(), n = b.cols();
     if (m == 0 || n == 0) return;
-    const ComplexMatrix ad = a.to_dense();
-    const Planar pa = api::split(ad.data(), m * k), pb = api::split(b.data(), k * n);
-    std::vector<double> cr(m * n), ci(m * n);
+    ComplexMatrix densified;  // only a CSR left factor is densified
+    const cplx* av = a.is_dense() ? a.data() : (densified = a.to_dense()).data();
+    const Planar pa = api::split(av, m * k), pb = api::split(b.data(), k * n);
+    Vec cr(m * n), ci(m * n);
     api::check(ipt_gemm(api::context(), static_cast<int64_t>(m), static_cast<int64_t>(k), static_cast<int64_t>(n),
                         pa.re.data(), pa.im_or_null(), pb.re.data(), pb.im_or_null(), cr.data(), ci.data()));
     api::merge(cr, ci, c.data());

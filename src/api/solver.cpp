@@ -58,6 +58,7 @@ unsigned host_threads() {
 namespace {
 
 using api::Planar;
+using api::Vec;
 
 void validate(const IterationConfig& cfg) {
     if (!(cfg.tolerance > 0.0)) throw std::invalid_argument("config: tolerance must be positive");
@@ -82,7 +83,7 @@ ipt_params to_params(const IterationConfig& cfg) {
     return prm;
 }
 
-cvec combine(const std::vector<double>& re, const std::vector<double>& im) {
+cvec combine(const Vec& re, const Vec& im) {
     cvec out(re.size());
     api::merge(re, im, out.data());
     return out;
@@ -111,7 +112,7 @@ EigenpairResult run_single(const Partition& p, std::size_t anchor, const Iterati
     ipt_stats st{};
     std::vector<double> trace(cfg.record_trace ? cfg.max_iterations : 0);
     st.trace = cfg.record_trace ? trace.data() : nullptr;
-    std::vector<double> zr(n), zi(n);
+    Vec zr(n), zi(n);
     const double* wre = warm ? w.re.data() : nullptr;
     const double* wim = warm ? w.im_or_null() : nullptr;
     if (p.delta.is_sparse()) {
@@ -154,7 +155,7 @@ cvec apply_map_single(const Partition& p, const InverseGaps& g, std::size_t anch
     const std::size_t n = p.size();
     if (z.size() != n) throw std::invalid_argument("apply_map_single: size mismatch");
     const Planar d = api::split(p.d.data(), n), a = dense_delta(p), zz = api::split(z.data(), n);
-    std::vector<double> fr(n), fi(n);
+    Vec fr(n), fi(n);
     api::check(ipt_apply_map_single_dense(api::context(), static_cast<int64_t>(n), d.re.data(), d.im_or_null(),
                                           a.re.data(), a.im_or_null(), static_cast<int64_t>(anchor), zz.re.data(),
                                           zz.im_or_null(), fr.data(), fi.data()));
@@ -183,7 +184,7 @@ ComplexMatrix apply_map_full(const Partition& p, const InverseGaps& g, const Com
     const std::size_t n = p.size();
     const ComplexMatrix zd = Z.to_dense();
     const Planar d = api::split(p.d.data(), n), a = dense_delta(p), zz = api::split(zd.data(), n * n);
-    std::vector<double> fr(n * n), fi(n * n);
+    Vec fr(n * n), fi(n * n);
     api::check(ipt_apply_map_full(api::context(), static_cast<int64_t>(n), d.re.data(), d.im_or_null(), a.re.data(),
                                   a.im_or_null(), zz.re.data(), zz.im_or_null(), fr.data(), fi.data()));
     ComplexMatrix out = ComplexMatrix::dense(n, n);
@@ -214,7 +215,7 @@ SpectrumResult solve_full(const Partition& p, const InverseGaps& g, const Iterat
     ipt_stats st{};
     std::vector<double> trace(config.record_trace ? config.max_iterations : 0);
     st.trace = config.record_trace ? trace.data() : nullptr;
-    std::vector<double> zr(n * n), zi(n * n), lr(n), li(n);
+    Vec zr(n * n), zi(n * n), lr(n), li(n);
     api::check(ipt_full_solve(api::context(), static_cast<int64_t>(n), d.re.data(), d.im_or_null(), a.re.data(),
                               a.im_or_null(), warm_start ? w.re.data() : nullptr, warm_start ? w.im_or_null() : nullptr,
                               &prm, zr.data(), zi.data(), lr.data(), li.data(), &st));
