@@ -446,47 +446,79 @@ int ipt_gemm(ipt_ctx* ctx, int64_t m, int64_t k, int64_t n, const double* a_re, 
     Ctx& c = ctx->c;
     cudaStream_t s = c.stream;
     if (m == 0 || n == 0) return;
-    bool cplx = false;
-    if (a_im) for (int64_t t = 0; t < m * k && !cplx; ++t) cplx = a_im[t] != 0.0;
-    if (b_im) for (int64_t t = 0; t < k * n && !cplx; ++t) cplx = b_im[t] != 0.0;
+    bool a_cplx = false, b_cplx = false;
+    if (a_im) for (int64_t t = 0; t < m * k && !a_cplx; ++t) a_cplx = a_im[t] != 0.0;
+    if (b_im) for (int64_t t = 0; t < k * n && !b_cplx; ++t) b_cplx = b_im[t] != 0.0;
     const int64_t ldk = round_up(std::max<int64_t>(k, 1), 16);
-    const int64_t K = cplx ? 2 * ldk : ldk;
-    const int64_t mpad = round_up(m, kBM), npad = round_up(n, kBN);
-    DevBuf A1, A2, B, C1, C2, rm;
-    A1.alloc(size_t(mpad) * K);
-    B.alloc(size_t(npad) * K);
-    auto up2d = [&](double* dst, int64_t dpitch, const double* src) {
+    auto up_rows = [&](double* dst, int64_t dpitch, const double* src) {  // m x k row-major
       if (k > 0) h2d_rows(c, dst, dpitch, src, k, m, k);  // pinned, double-buffered
     };
-    up2d(A1.get(), K, a_re);
-    if (k > 0) upload_as_colmajor(c, b_re, k, n, B.get(), K);  // column-major k x n, ld K
-    if (cplx) {
+    auto up_cols = [&](double* dst, int64_t ld, const double* src) {  // k x n -> column-major
+      if (k > 0) upload_as_colmajor(c, src, k, n, dst, ld);
+    };
+    DevBuf A, B, C, rm;
+    rm.alloc(size_t(m) * n, false);
+    auto download = [&](const double* src, int64_t ldc, double* dst) {
+      transpose_to_rowmajor(s, src, ldc, m, n, rm.get(), n);
+      d2h_rows(c, dst, n, rm.get(), n, m, n);
+    };
+    if (!a_cplx && !b_cplx) {  // one real GEMM
+      A.alloc(size_t(round_up(m, kBM)) * ldk);
+      B.alloc(size_t(round_up(n, kBN)) * ldk);
+      up_rows(A.get(), ldk, a_re);
+      up_cols(B.get(), ldk, b_re);
+      C.alloc(size_t(n) * m, false);
+      gemm_tn_store(s, m, n, ldk, A.get(), ldk, B.get(), ldk, C.get(), m);
+      download(C.get(), m, c_re);
+      if (c_im) std::memset(c_im, 0, sizeof(double) * m * n);
+    } else if (!a_cplx) {  // real A: A [Br | Bi] as one m x 2n real GEMM
+      A.alloc(size_t(round_up(m, kBM)) * ldk);
+      B.alloc(size_t(round_up(2 * n, kBN)) * ldk);
+      up_rows(A.get(), ldk, a_re);
+      up_cols(B.get(), ldk, b_re);
+      up_cols(B.get() + n * ldk, ldk, b_im);
+      C.alloc(size_t(2 * n) * m, false);
+      gemm_tn_store(s, m, 2 * n, ldk, A.get(), ldk, B.get(), ldk, C.get(), m);
+      download(C.get(), m, c_re);
+      if (c_im) download(C.get() + n * m, m, c_im);
+    } else if (!b_cplx) {  // real B: [Ar; Ai] B as one 2m x n real GEMM
+      A.alloc(size_t(round_up(2 * m, kBM)) * ldk);
+      B.alloc(size_t(round_up(n, kBN)) * ldk);
+      up_rows(A.get(), ldk, a_re);
+      up_rows(A.get() + m * ldk, ldk, a_im);
+      up_cols(B.get(), ldk, b_re);
+      C.alloc(size_t(n) * 2 * m, false);
+      gemm_tn_store(s, 2 * m, n, ldk, A.get(), ldk, B.get(), ldk, C.get(), 2 * m);
+      download(C.get(), 2 * m, c_re);
+      if (c_im) download(C.get() + m, 2 * m, c_im);
+    } else {  // both complex: Cr = [Ar | -Ai][Br; Bi], Ci = [Ai | Ar][Br; Bi] (K = 2 ldk)
+      const int64_t K = 2 * ldk;
+      const int64_t mpad = round_up(m, kBM);
+      DevBuf A2;
+      A.alloc(size_t(mpad) * K);
       A2.alloc(size_t(mpad) * K);
-      up2d(A2.get() + ldk, K, a_re);
-      if (a_im) {
-        up2d(A2.get(), K, a_im);
+      B.alloc(size_t(round_up(n, kBN)) * K);
+      up_rows(A.get(), K, a_re);
+      up_rows(A2.get() + ldk, K, a_re);
+      up_rows(A2.get(), K, a_im);
+      {
         DevBuf tmp;
-        tmp.alloc(size_t(m) * k, false);
-        h2d_rows(c, tmp.get(), k, a_im, k, m, k);
+        tmp.alloc(size_t(m) * std::max<int64_t>(k, 1), false);
+        if (k > 0) h2d_rows(c, tmp.get(), k, a_im, k, m, k);
         scale_copy(s, tmp.get(), tmp.get(), size_t(m) * k, -1.0);
-        IPT_CUDA(cudaMemcpy2DAsync(A1.get() + ldk, K * sizeof(double), tmp.get(), k * sizeof(double),
-                                   k * sizeof(double), m, cudaMemcpyDeviceToDevice, s));
+        if (k > 0)
+          IPT_CUDA(cudaMemcpy2DAsync(A.get() + ldk, K * sizeof(double), tmp.get(), k * sizeof(double),
+                                     k * sizeof(double), m, cudaMemcpyDeviceToDevice, s));
         c.sync();
       }
-      if (b_im && k > 0) upload_as_colmajor(c, b_im, k, n, B.get() + ldk, K);
-    }
-    C1.alloc(size_t(n) * m, false);
-    rm.alloc(size_t(m) * n, false);
-    gemm_tn_store(s, m, n, K, A1.get(), K, B.get(), K, C1.get(), m);
-    transpose_to_rowmajor(s, C1.get(), m, m, n, rm.get(), n);
-    d2h_rows(c, c_re, n, rm.get(), n, m, n);
-    if (c_im) {
-      if (!cplx) {
-        std::memset(c_im, 0, sizeof(double) * m * n);
-      } else {
-        gemm_tn_store(s, m, n, K, A2.get(), K, B.get(), K, C1.get(), m);
-        transpose_to_rowmajor(s, C1.get(), m, m, n, rm.get(), n);
-        d2h_rows(c, c_im, n, rm.get(), n, m, n);
+      up_cols(B.get(), K, b_re);
+      up_cols(B.get() + ldk, K, b_im);
+      C.alloc(size_t(n) * m, false);
+      gemm_tn_store(s, m, n, K, A.get(), K, B.get(), K, C.get(), m);
+      download(C.get(), m, c_re);
+      if (c_im) {
+        gemm_tn_store(s, m, n, K, A2.get(), K, B.get(), K, C.get(), m);
+        download(C.get(), m, c_im);
       }
     }
   });

@@ -13,7 +13,10 @@
 // so the stopping step and the estimate agree. Complex Z uses the real
 // embedding [[Zr, -Zi], [Zi, Zr]], on which the iteration from [v; 0] is the
 // complex iteration from v written in real coordinates.
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "dmma_gemm.cuh"
@@ -297,6 +300,9 @@ double sigma_min_device(Ctx& c, int64_t n, const double* zr, const double* zi, i
   IPT_CUDA(cudaMemcpyAsync(hmax4, scratch.get() + 1184 * 4, sizeof(hmax4), cudaMemcpyDeviceToHost, s));
   c.sync();
   const double tiny = hmax4[3] * 2.220446049250313e-16 * static_cast<double>(m);
+  const bool prof = std::getenv("IPT_PROFILE") != nullptr;
+  auto wall = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  const double t_syrk = wall();
 
   int* d_sing = nullptr;
   IPT_CUDA(cudaMalloc(&d_sing, sizeof(int)));
@@ -342,6 +348,7 @@ double sigma_min_device(Ctx& c, int64_t n, const double* zr, const double* zi, i
   IPT_CUDA(cudaMemcpyAsync(&sing, d_sing, sizeof(int), cudaMemcpyDeviceToHost, s));
   c.sync();
   cudaFree(d_sing);
+  const double t_chol = wall();
   if (sing) return 0.0;
 
   // inverse power iteration (solver.cpp:283-296)
@@ -352,7 +359,9 @@ double sigma_min_device(Ctx& c, int64_t n, const double* zr, const double* zi, i
   un.alloc(1);
   IPT_CUDA(cudaMemcpyAsync(v.get(), v0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
   double rho = 0.0;
+  int iters_done = 0;
   for (int it = 0; it < max_iters; ++it) {
+    iters_done = it + 1;
     IPT_CUDA(cudaMemcpyAsync(u.get(), v.get(), sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
     for (int64_t kb = 0; kb < m; kb += NB) {  // L y = v
       const int b = static_cast<int>(std::min<int64_t>(NB, m - kb));
@@ -389,6 +398,9 @@ double sigma_min_device(Ctx& c, int64_t n, const double* zr, const double* zi, i
     }
     rho = h_un;
   }
+  if (prof)
+    std::fprintf(stderr, "[ipt] sigma_min n=%lld: cholesky %.1f ms, inverse iteration %.1f ms (%d steps)\n",
+                 static_cast<long long>(m), 1e3 * (t_chol - t_syrk), 1e3 * (wall() - t_chol), iters_done);
   return 1.0 / std::sqrt(rho);
 }
 
