@@ -17,6 +17,7 @@
 // CSR int64 row offsets (rebased to the shard), int32 columns, fp64 values;
 // z ping-pong vectors of length nranks*chunk, replicated.
 #include <cmath>
+#include <cstdlib>
 #include <complex>
 #include <cstring>
 #include <memory>
@@ -69,8 +70,23 @@ namespace {
 constexpr int kGemvRows = 4;        // rows per warp (dense)
 constexpr int kGemvWarps = 8;
 constexpr int kRowsPerBlock = kGemvRows * kGemvWarps;
-constexpr int kSpmvLanes = 16;      // lanes per CSR row
-constexpr int kSpmvRowsPerBlock = 256 / kSpmvLanes;
+// CSR variants (lanes per row, entries in flight per lane). Measured at config 5
+// (N = 2^21, 64 nnz/row, profiles/r01_spmv_variants.txt): {8,4} 0.674 ms, {16,4}
+// 0.689, {16,6} 0.753, {32,2} 0.832, {8,8} 0.905 -- all near the L2-sector bound of
+// the 8-byte z gathers. Default {8,4}; IPT_SPMV_VARIANT selects another.
+struct SpmvVariant {
+  int lanes, u;
+};
+constexpr SpmvVariant kSpmvVariants[] = {{16, 4}, {8, 8}, {32, 2}, {8, 4}, {16, 6}};
+inline int spmv_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("IPT_SPMV_VARIANT");
+    const int k = e ? std::atoi(e) : 3;
+    return (k >= 0 && k < 5) ? k : 0;
+  }();
+  return v;
+}
+inline int spmv_rows_per_block() { return 256 / kSpmvVariants[spmv_variant()].lanes; }
 constexpr int kSpmvMinBlocks = 5;       // 48 registers (no spills): 5 CTAs (40 warps) per SM
 constexpr int kSpmvGrid = kNumSMs * kSpmvMinBlocks;  // persistent: exactly one resident wave
 
@@ -160,33 +176,33 @@ __device__ __forceinline__ double ld_keep_f64(const double* p, uint64_t pol) {
   return v;
 }
 
-// One CSR row over a group of kSpmvLanes lanes. Lane sl takes entries beg+sl,
-// beg+sl+16, ... in ascending order (fixed per-lane order + xor tree: deterministic);
-// four entries per lane are in flight at once (all index/value loads issue before the
+// One CSR row over a group of LANES lanes. Lane sl takes entries beg+sl,
+// beg+sl+LANES, ... in ascending order (fixed per-lane order + xor tree: deterministic);
+// U entries per lane are in flight at once (all index/value loads issue before the
 // dependent gathers).
+template <int LANES, int U>
 __device__ __forceinline__ double csr_row_dot(const int32_t* __restrict__ cols,
                                               const double* __restrict__ vals, int64_t beg,
                                               int64_t end, const double* __restrict__ z, int sl,
                                               uint64_t pol_stream, uint64_t pol_keep) {
-  constexpr int U = 4;  // four entries in flight per lane (64 per pass per row group)
   double s = 0.0;
-  for (int64_t p0 = beg + sl; p0 < end; p0 += U * kSpmvLanes) {
+  for (int64_t p0 = beg + sl; p0 < end; p0 += U * LANES) {
     int32_t c[U];
     double v[U], zz[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t p = p0 + u * kSpmvLanes;
+      const int64_t p = p0 + u * LANES;
       c[u] = p < end ? ld_stream_i32(cols + p, pol_stream) : 0;
       v[u] = p < end ? ld_stream_f64(vals + p, pol_stream) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) zz[u] = (p0 + u * kSpmvLanes < end) ? ld_keep_f64(z + c[u], pol_keep) : 0.0;
+    for (int u = 0; u < U; ++u) zz[u] = (p0 + u * LANES < end) ? ld_keep_f64(z + c[u], pol_keep) : 0.0;
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (p0 + u * kSpmvLanes < end) s = __fma_rn(v[u], zz[u], s);
+      if (p0 + u * LANES < end) s = __fma_rn(v[u], zz[u], s);
   }
 #pragma unroll
-  for (int off = kSpmvLanes / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  for (int off = LANES / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
   return s;
 }
 
@@ -263,26 +279,27 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_map_kernel(const double*
   }
 }
 
-template <int MODE>
+template <int MODE, int LANES, int U>
 __global__ void __launch_bounds__(256, kSpmvMinBlocks) spmv_map_kernel(const int64_t* __restrict__ rowptr,
                                                        const int32_t* __restrict__ cols,
                                                        const double* __restrict__ vals, MapArgs a) {
   if (a.state != nullptr && a.state->done) return;
   __shared__ double red[8][4];
-  const int sl = threadIdx.x % kSpmvLanes;
+  constexpr int kRows = 256 / LANES;
+  const int sl = threadIdx.x % LANES;
   double v[4] = {0.0, 0.0, 0.0, 0.0};
   const double scale = MODE == kMvMap ? schedule_scale(a) : 1.0;
   const double lam = MODE == kMvFinal ? a.d[a.anchor] + *a.wa : 0.0;
   const uint64_t pol_s = policy_stream(), pol_k = policy_keep();
   // Persistent fixed grid: block b owns row groups b, b + grid, ... (a fixed map, so the
   // per-block partial sums and their reduction are run-to-run identical).
-  const int64_t groups = ceil_div(a.rows, kSpmvRowsPerBlock);
+  const int64_t groups = ceil_div(a.rows, kRows);
   for (int64_t grp = blockIdx.x; grp < groups; grp += gridDim.x) {
-    const int64_t lr = grp * kSpmvRowsPerBlock + threadIdx.x / kSpmvLanes;
+    const int64_t lr = grp * kRows + threadIdx.x / LANES;
     // all lanes of a row group take part in the shuffle even past the end
     const bool valid = lr < a.rows;
     const int64_t beg = valid ? rowptr[lr] : 0, end = valid ? rowptr[lr + 1] : 0;
-    const double w = csr_row_dot(cols, vals, beg, end, a.z, sl, pol_s, pol_k);
+    const double w = csr_row_dot<LANES, U>(cols, vals, beg, end, a.z, sl, pol_s, pol_k);
     if (valid && sl == 0) row_epilogue<MODE>(a, a.row0 + lr, w, scale, lam, v);
   }
   if (MODE == kMvStore) return;
@@ -301,11 +318,12 @@ __global__ void anchor_dense_kernel(const double* __restrict__ arow, int64_t lda
   rows_dot<1>(arow, lda, 1, z, lda / 2, w);
   if (threadIdx.x == 0) wa[0] = w[0];
 }
+template <int LANES, int U>
 __global__ void anchor_csr_kernel(const int32_t* __restrict__ cols, const double* __restrict__ vals,
                                   int64_t nnz, const double* __restrict__ z, double* wa,
                                   const LoopState* st) {
   if (st != nullptr && st->done) return;
-  const double w = csr_row_dot(cols, vals, 0, nnz, z, threadIdx.x % kSpmvLanes, policy_stream(), policy_keep());
+  const double w = csr_row_dot<LANES, U>(cols, vals, 0, nnz, z, threadIdx.x % LANES, policy_stream(), policy_keep());
   if (threadIdx.x == 0) wa[0] = w;
 }
 
@@ -442,10 +460,21 @@ __global__ void cmap_kernel(int mode, const double* __restrict__ zr, const doubl
 }
 constexpr int kCmapBlocks = 296;
 
+template <int MODE>
+void launch_spmv(unsigned grid, cudaStream_t s, const int64_t* rowptr, const int32_t* cols, const double* vals,
+                 const MapArgs& a) {
+  switch (spmv_variant()) {
+#define IPT_SPMV(K, L, UU) \
+  case K: spmv_map_kernel<MODE, L, UU><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    IPT_SPMV(0, 16, 4) IPT_SPMV(1, 8, 8) IPT_SPMV(2, 32, 2) IPT_SPMV(3, 8, 4) IPT_SPMV(4, 16, 6)
+#undef IPT_SPMV
+  }
+}
+
 int64_t map_blocks(const SingleProblem& P) {
   if (P.cplx) return kCmapBlocks;
   const int64_t rows = P.r1 - P.r0;
-  return P.csr ? std::min<int64_t>(kSpmvGrid, ceil_div(rows, kSpmvRowsPerBlock)) : ceil_div(rows, kRowsPerBlock);
+  return P.csr ? std::min<int64_t>(kSpmvGrid, ceil_div(rows, spmv_rows_per_block())) : ceil_div(rows, kRowsPerBlock);
 }
 
 MapArgs map_args(SingleProblem& P, int src) {
@@ -465,8 +494,14 @@ MapArgs map_args(SingleProblem& P, int src) {
 void enqueue_anchor(SingleProblem& P, int src, const LoopState* st) {
   cudaStream_t s = P.ctx->stream;
   if (P.csr) {
-    anchor_csr_kernel<<<1, 32, 0, s>>>(P.acols.get(), P.arow.get(), P.annz, P.z[src].get(),
-                                              P.wa.get(), st);
+    switch (spmv_variant()) {
+#define IPT_ANCHOR(K, L, UU)                                                                                   \
+  case K:                                                                                                      \
+    anchor_csr_kernel<L, UU><<<1, 32, 0, s>>>(P.acols.get(), P.arow.get(), P.annz, P.z[src].get(), P.wa.get(), st); \
+    break;
+      IPT_ANCHOR(0, 16, 4) IPT_ANCHOR(1, 8, 8) IPT_ANCHOR(2, 32, 2) IPT_ANCHOR(3, 8, 4) IPT_ANCHOR(4, 16, 6)
+#undef IPT_ANCHOR
+    }
   } else {
     anchor_dense_kernel<<<1, 32, 0, s>>>(P.arow.get(), P.lda, P.z[src].get(), P.wa.get(), st);
   }
@@ -530,7 +565,7 @@ void enqueue_real_map(SingleProblem& P, int src, const ipt_params* prm) {
   const unsigned grid = static_cast<unsigned>(map_blocks(P));
   if (grid == 0) return;
   if (P.csr)
-    spmv_map_kernel<MODE><<<grid, 256, 0, s>>>(P.rowptr.get(), P.cols.get(), P.vals.get(), a);
+    launch_spmv<MODE>(grid, s, P.rowptr.get(), P.cols.get(), P.vals.get(), a);
   else
     gemv_map_kernel<MODE><<<grid, kGemvWarps * 32, 0, s>>>(P.A.get(), P.lda, a);
   IPT_LAUNCH_CHECK();
@@ -880,7 +915,7 @@ void single_matvec(SingleProblem& P, const double* x_re, const double* x_im, dou
     a.fz = P.w.get();
     const unsigned grid = static_cast<unsigned>(map_blocks(P));
     if (grid) {
-      if (P.csr) spmv_map_kernel<kMvStore><<<grid, 256, 0, s>>>(P.rowptr.get(), P.cols.get(), P.vals.get(), a);
+      if (P.csr) launch_spmv<kMvStore>(grid, s, P.rowptr.get(), P.cols.get(), P.vals.get(), a);
       else gemv_map_kernel<kMvStore><<<grid, kGemvWarps * 32, 0, s>>>(P.A.get(), P.lda, a);
       IPT_LAUNCH_CHECK();
       count_launch();
