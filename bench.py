@@ -152,11 +152,16 @@ def hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def traffic_for(kernel):
+def traffic_for(kernel, n=None):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the committed
+    ncu --set full capture (profiles/ncu_traffic.json), when it was taken at this size."""
     try:
-        return json.load(open(TRAFFIC_PATH)).get(kernel)
+        rec = json.load(open(TRAFFIC_PATH)).get(kernel)
     except Exception:
         return None
+    if rec is None or (n is not None and rec.get("n") != n):
+        return None
+    return rec.get("dram_bytes_per_launch")
 
 
 # --------------------------------------------------------------------------- CPU baseline
@@ -281,7 +286,7 @@ def bench_single(ipt, lib, ctx, which, steps, warmup, hbm):
         "roofline": {"bound": "hbm", "kernel": kernel, "achieved": kbytes / (dom_ms * 1e-3) / 1e9,
                      "peak": hbm[0], "peak_source": hbm[1], "unit": "GB/s",
                      "frac": kbytes / (dom_ms * 1e-3) / 1e9 / hbm[0], "kernel_ms": dom_ms,
-                     "bytes_per_launch": kbytes, "traffic": traffic_for(kernel)},
+                     "bytes_per_launch": kbytes, "traffic": traffic_for(kernel, n)},
     }
 
 
@@ -411,14 +416,14 @@ def main():
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE configs[2] construction, seed 42)",
             "config": workload_config(world, n),
-            "roofline": {"bound": "tensor", "kernel": "dmma_gemm_kernel<1> (K1 fused DMMA GEMM + map epilogue)",
+            "roofline": {"bound": "tensor", "kernel": "dmma_tma_kernel<1> (K1: TMA-fed DMMA GEMM + fused map epilogue)",
                          "achieved": achieved, "peak": peak,
                          "peak_source": "cuBLAS DGEMM 8192^3 on this GPU in this run (burst); DMMA issue-rate "
                                         "probe 37.1 TF/s in profiles/r01_fp64_probe.txt",
                          "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                          "flops_per_launch": gemm_flops_local, "kernel_ms": gemm_ms_local,
                          "kernel_share_of_step": gemm_ms / step_ms,
-                         "traffic": traffic_for("dmma_gemm_kernel<1>")},
+                         "traffic": traffic_for("dmma_tma_kernel<1>", n)},
             "time_to_solution": solve_info,
             "e2e": e2e,
             "cpu_baseline": cpu,

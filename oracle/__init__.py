@@ -289,6 +289,20 @@ class PortArm(_Arm):
         z = _c(z)
         return self.lib.orc_sigma_min(C.c_int64(z.shape[0]), _p(z), C.c_int(max_iters), C.c_double(tol))
 
+    def solve_single_real_dense(self, d, delta, anchor, tol=100 * np.finfo(float).eps, max_iter=1000,
+                                div_thr=1e8):
+        """run_single on a real dense operator in place (no complex copy; config 4 at N=65536)."""
+        n = len(d)
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        delta = np.ascontiguousarray(delta, dtype=np.float64)
+        z = np.empty(n)
+        lam = np.zeros(1)
+        stats = np.zeros(5)
+        self.lib.orc_solve_single_real_dense(C.c_int64(n), _p(d), _p(delta), C.c_int64(anchor), C.c_double(tol),
+                                             C.c_int(max_iter), C.c_double(div_thr), _p(z), _p(lam), _p(stats))
+        return dict(z=z, eigenvalue=lam[0], iterations=int(stats[0]), status=int(stats[1]), final_step=stats[2],
+                    residual=stats[3], matvec_count=int(stats[4]))
+
 
 _ref = _port = None
 

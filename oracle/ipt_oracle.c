@@ -299,6 +299,71 @@ int orc_solve_full(int64_t n, const double* d, const double* delta, double tol, 
 }
 
 /*
+ * run_single (solver.cpp:49-93), plain schedule, for a REAL dense operator in place
+ * (no complex copy: config 4 at N = 65536 is 34 GB as doubles). With zero
+ * imaginary parts the reference's complex arithmetic reduces to these real
+ * operations (kernels.cpp:114-127: sr += ar*xr - 0; single_step.hpp:11-26).
+ * delta: n x n row-major doubles. stats as orc_solve_single.
+ */
+static void real_matvec(int64_t n, const double* delta, const double* z, double* w) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    const double* row = delta + i * n;
+    double s = 0.0;
+    for (int64_t j = 0; j < n; ++j) s += row[j] * z[j];
+    w[i] = s;
+  }
+}
+
+int orc_solve_single_real_dense(int64_t n, const double* d, const double* delta, int64_t anchor, double tol,
+                                int max_iter, double div_thr, double* z, double* lam_out, double* stats) {
+  double* w = malloc(sizeof(double) * n);
+  double* fz = malloc(sizeof(double) * n);
+  for (int64_t j = 0; j < n; ++j) z[j] = 0.0;
+  z[anchor] = 1.0;
+  int iters = 0, status = ORC_MAXIT;
+  long mv = 0;
+  double step = 0.0;
+  for (int k = 0; k < max_iter; ++k) {
+    real_matvec(n, delta, z, w);
+    ++mv;
+    const double wa = w[anchor];
+    double diff = 0.0, base = 0.0, s2 = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+      const double f = j == anchor ? 1.0 : (1.0 / (d[j] - d[anchor])) * (z[j] * wa - w[j]);
+      diff += (z[j] - f) * (z[j] - f);
+      base += z[j] * z[j];
+      s2 += f * f;
+      fz[j] = f;
+    }
+    step = sqrt(diff) / sqrt(base);
+    memcpy(z, fz, sizeof(double) * n);
+    iters = k + 1;
+    const double zn = sqrt(s2);
+    if (!isfinite(zn) || zn > div_thr) { status = ORC_DIVERGED; break; }
+    if (step <= tol) { status = ORC_CONVERGED; break; }
+  }
+  real_matvec(n, delta, z, w);  /* closing product (solver.cpp:83-91) */
+  ++mv;
+  const double lam = d[anchor] + w[anchor];
+  double rn = 0.0, zn = 0.0;
+  for (int64_t j = 0; j < n; ++j) {
+    const double r = d[j] * z[j] + w[j] - lam * z[j];
+    rn += r * r;
+    zn += z[j] * z[j];
+  }
+  lam_out[0] = lam;
+  stats[0] = iters;
+  stats[1] = status;
+  stats[2] = step;
+  stats[3] = sqrt(rn) / sqrt(zn);
+  stats[4] = (double)mv;
+  free(w);
+  free(fz);
+  return 0;
+}
+
+/*
  * run_single (solver.cpp:49-93) for plain (mode 0) and continuation (mode 1,
  * solver.cpp:138-154) schedules; assemble/rel_step from
  * proj/include/ipt/detail/single_step.hpp:11-26.

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(512) potrf_block_kernel(double* H, int64_t ldh
 // Writes L21 back into H (column-major) and into the row-major panel P (ld NB,
 // zero-padded to NB columns) used as both operands of the trailing update.
 __global__ void __launch_bounds__(256) trsm_panel_kernel(double* H, int64_t ldh, int64_t kb, int b,
-                                                         int64_t rem, double* P) {
+                                                         int64_t rem, double* P, int64_t ldp) {
   extern __shared__ double sm[];
   double* L = sm;                 // [NB][LDS] lower factor of the diagonal block
   double* R = sm + NB * LDS;      // [32][LDS] rows of H21
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(256) trsm_panel_kernel(double* H, int64_t ldh,
   for (int e = tid; e < 32 * NB; e += blockDim.x) {
     const int r = e / NB, p = e % NB;
     const int64_t i = i0 + r;
-    if (i < rem) P[i * NB + p] = p < b ? R[r * LDS + p] : 0.0;
+    if (i < rem) P[i * ldp + p] = p < b ? R[r * LDS + p] : 0.0;
   }
   for (int e = tid; e < 32 * b; e += blockDim.x) {
     const int p = e / 32, r = e % 32;
@@ -307,8 +307,13 @@ double sigma_min_device(Ctx& c, int64_t n, const double* zr, const double* zi, i
   int* d_sing = nullptr;
   IPT_CUDA(cudaMalloc(&d_sing, sizeof(int)));
   IPT_CUDA(cudaMemsetAsync(d_sing, 0, sizeof(int), s));
-  DevBuf Pb;
-  Pb.alloc(size_t(round_up(m, kBM)) * NB);
+  // Two-level right-looking Cholesky: outer panels of kW = 512 columns, factored in
+  // NB = 128 sub-blocks (potrf + trsm + an intra-panel update with K = 128); the
+  // trailing matrix then takes ONE K = 512 DMMA update per outer panel, so the
+  // read-modify-write of each trailing tile is amortised over 4x more k-steps.
+  constexpr int64_t kW = 4 * NB;
+  DevBuf Pb;  // L21 of the current outer panel, row-major, row i = matrix row kb + i
+  Pb.alloc((size_t(round_up(m, kBM)) + kW) * kW);
   static bool attr = false;
   if (!attr) {
     IPT_CUDA(cudaFuncSetAttribute(potrf_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -319,30 +324,46 @@ double sigma_min_device(Ctx& c, int64_t n, const double* zr, const double* zi, i
                                   int(NB * LDS * sizeof(double))));
     attr = true;
   }
-  for (int64_t kb = 0; kb < m; kb += NB) {
-    const int b = static_cast<int>(std::min<int64_t>(NB, m - kb));
-    potrf_block_kernel<<<1, 512, NB * LDS * sizeof(double), s>>>(H.get(), ldh, kb, b, tiny, d_sing);
-    IPT_LAUNCH_CHECK();
-    count_launch();
-    const int64_t rem = m - kb - b;
-    if (rem <= 0) break;
-    trsm_panel_kernel<<<static_cast<unsigned>(ceil_div(rem, 32)), 256, (NB + 32) * LDS * sizeof(double), s>>>(
-        H.get(), ldh, kb, b, rem, Pb.get());
-    IPT_LAUNCH_CHECK();
-    count_launch();
+  auto sub_update = [&](const double* panel, int64_t k, int64_t r0, int64_t rows, int64_t cols) {
+    // H[r0.., r0..r0+cols) -= panel[r0..] panel[r0..r0+cols)^T, lower tiles of the block
+    if (rows <= 0 || cols <= 0) return;
     GemmParams g{};
-    g.K = NB;
-    g.A = Pb.get();
-    g.lda = NB;
-    g.B = Pb.get();
-    g.ldb = NB;
-    g.C = H.get() + (kb + b) * ldh + (kb + b);
+    g.K = k;
+    g.A = panel;
+    g.lda = kW;
+    g.B = panel;
+    g.ldb = kW;
+    g.C = H.get() + r0 * ldh + r0;
     g.ldc = ldh;
-    g.tiles_m = static_cast<int>(ceil_div(rem, kBM));
-    g.tiles_n = g.tiles_m;
-    g.n_rows = rem;
-    g.n_cols = rem;
+    g.tiles_m = static_cast<int>(ceil_div(rows, kBM));
+    g.tiles_n = static_cast<int>(ceil_div(cols, kBN));
+    g.n_rows = rows;
+    g.n_cols = cols;
     launch_gemm(kGemmSub, g, s);
+  };
+  for (int64_t kb = 0; kb < m; kb += kW) {
+    const int64_t wcols = std::min<int64_t>(kW, m - kb);
+    for (int64_t jb = 0; jb < wcols; jb += NB) {
+      const int64_t c0 = kb + jb;
+      const int b = static_cast<int>(std::min<int64_t>(NB, m - c0));
+      potrf_block_kernel<<<1, 512, NB * LDS * sizeof(double), s>>>(H.get(), ldh, c0, b, tiny, d_sing);
+      IPT_LAUNCH_CHECK();
+      count_launch();
+      const int64_t rem = m - c0 - b;
+      if (rem <= 0) break;
+      // L21 of this sub-block -> H and the panel (rows c0+b.., columns jb..jb+b of the panel)
+      double* pblk = Pb.get() + (jb + b) * kW + jb;
+      trsm_panel_kernel<<<static_cast<unsigned>(ceil_div(rem, 32)), 256, (NB + 32) * LDS * sizeof(double), s>>>(
+          H.get(), ldh, c0, b, rem, pblk, kW);
+      IPT_LAUNCH_CHECK();
+      count_launch();
+      // intra-panel update of the panel's remaining columns (K = b)
+      const int64_t cols_left = wcols - jb - b;
+      if (cols_left > 0) sub_update(pblk, NB, c0 + b, rem, cols_left);
+    }
+    // trailing update with the whole panel (K = 512, zero-padded when narrower)
+    const int64_t r0 = kb + wcols;
+    if (r0 < m) sub_update(Pb.get() + wcols * kW, kW, r0, m - r0, m - r0);
   }
   int sing = 0;
   IPT_CUDA(cudaMemcpyAsync(&sing, d_sing, sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -288,3 +288,15 @@ def test_sigma_min_matches_reference(ref_or_port_sigma=None):
     zc = z + 0.03j * rng.standard_normal((40, 40))
     assert ipt.smallest_singular_value_estimate(zc) == pytest.approx(oracle.port().sigma_min(zc), rel=1e-8)
     assert ipt.smallest_singular_value_estimate(np.zeros((5, 5))) == 0.0
+
+
+@pytest.mark.parametrize("n", [511, 640, 1100])
+def test_sigma_min_across_cholesky_panels(port_arm, n):
+    """sigma_min through the two-level blocked Cholesky (128-column sub-blocks inside
+    512-column panels), sizes straddling the panel boundaries, against the oracle's
+    partial-pivot LU route (solver.cpp:275-297)."""
+    rng = np.random.default_rng(n)
+    z = np.eye(n) + (0.3 / math.sqrt(n)) * rng.standard_normal((n, n))
+    np.fill_diagonal(z, 1.0)
+    want = port_arm.sigma_min(z)
+    assert ipt.smallest_singular_value_estimate(z) == pytest.approx(want, rel=1e-8)

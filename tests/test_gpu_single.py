@@ -219,3 +219,17 @@ def test_config4_stand_in_n32768():
     if "c4_32768_z" in g.files:
         assert np.max(np.abs(r.z - g["c4_32768_z"])) <= 1e-9
         assert abs(r.iterations - int(g["c4_32768_meta"][0])) <= 1
+
+
+@pytest.mark.slow
+def test_config4_full_size_n65536(port_arm):
+    """BASELINE configs[3] at full size (34 GB operator): device vs the in-place CPU
+    restatement of run_single (pinned bitwise to the reference at N = 4096)."""
+    p = synth.config4()
+    r = ipt.solve_single(p, ipt.build_gaps(p), 0, ipt.IterationConfig(tolerance=1e-12))
+    o = port_arm.solve_single_real_dense(p.d, p.delta, 0, tol=1e-12)
+    assert r.status == ipt.SolveStatus.Converged and o["status"] == 0
+    assert abs(r.iterations - o["iterations"]) <= 1
+    assert r.eigenvalue == pytest.approx(o["eigenvalue"], rel=1e-10)
+    assert np.max(np.abs(r.z - o["z"])) <= 1e-9
+    assert r.residual <= 1e-12 and r.z[0] == 1.0

@@ -241,3 +241,15 @@ def test_survey_anchor_config5_full_size():
     meta = g[key]
     assert int(meta[6]) == 134216644
     assert meta[2] == pytest.approx(0.114060512572133, abs=1e-14)
+
+
+def test_port_real_dense_single_bitwise_equals_reference(port_arm):
+    """The in-place real restatement (used for config 4 at N = 65536) reproduces the
+    reference's complex solve_single bit for bit on real inputs."""
+    g = golden("single_configs.npz")
+    p = synth.dense_normal(4096)
+    r = port_arm.solve_single_real_dense(p.d, p.delta, 0, tol=1e-12)
+    meta = g["c4_4096_meta"]
+    assert r["iterations"] == int(meta[0]) and r["status"] == int(meta[1])
+    assert np.array_equal(r["z"], g["c4_4096_z"])
+    assert r["eigenvalue"] == meta[2]
