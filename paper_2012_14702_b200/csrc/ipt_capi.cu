@@ -2,6 +2,9 @@
 // kernel entry points. Exceptions never cross this file: every entry point maps
 // them to IPT_ERR_* and records the message for ipt_last_error().
 #include <cfloat>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -12,6 +15,29 @@ using namespace iptb;
 
 namespace {
 thread_local std::string g_last_error;
+
+// IPT_PROFILE=1: host wall time of each phase of an entry point, on stderr.
+struct HostPhases {
+  const char* name;
+  bool on;
+  double t0, last;
+  std::string line;
+  static double now() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  }
+  explicit HostPhases(const char* n) : name(n), on(std::getenv("IPT_PROFILE") != nullptr), t0(now()), last(t0) {}
+  void mark(const char* what) {
+    if (!on) return;
+    const double t = now();
+    char buf[96];
+    std::snprintf(buf, sizeof buf, " %s %.2f", what, 1e3 * (t - last));
+    line += buf;
+    last = t;
+  }
+  ~HostPhases() {
+    if (on) std::fprintf(stderr, "[ipt] %s ms:%s | total %.2f\n", name, line.c_str(), 1e3 * (now() - t0));
+  }
+};
 
 template <typename F>
 int guarded(F&& f) {
@@ -211,26 +237,35 @@ int ipt_full_solve(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_
     if (prm.max_iterations <= 0) throw InvalidArgument("config: max_iterations must be positive");
     if (!(prm.divergence_threshold > 1.0)) throw InvalidArgument("config: divergence_threshold must exceed 1");
     Ctx& c = ctx->c;
+    HostPhases ph("ipt_full_solve");
     IPT_CUDA(cudaEventRecord(c.ev[2], c.stream));
-    std::unique_ptr<FullProblem, void (*)(FullProblem*)> P(full_upload(c, n, d_re, d_im, delta_re, delta_im),
-                                                           full_free);
-    full_reset(*P, warm_re, warm_im, prm.max_iterations);
-    IPT_CUDA(cudaEventRecord(c.ev[3], c.stream));
-    c.sync();
-    float ms_up = 0.f;
-    IPT_CUDA(cudaEventElapsedTime(&ms_up, c.ev[2], c.ev[3]));
-    full_iterate(*P, prm, stats);
-    full_finalize(*P, prm, stats);
-    IPT_CUDA(cudaEventRecord(c.ev[2], c.stream));
-    full_download(*P, z_re, z_im, lam_re, lam_im);
-    IPT_CUDA(cudaEventRecord(c.ev[3], c.stream));
-    c.sync();
-    float ms_down = 0.f;
-    IPT_CUDA(cudaEventElapsedTime(&ms_down, c.ev[2], c.ev[3]));
-    if (stats) {
-      stats->ms_upload = ms_up;
-      stats->ms_download = ms_down;
+    {
+      std::unique_ptr<FullProblem, void (*)(FullProblem*)> P(full_upload(c, n, d_re, d_im, delta_re, delta_im),
+                                                             full_free);
+      ph.mark("upload");
+      full_reset(*P, warm_re, warm_im, prm.max_iterations);
+      IPT_CUDA(cudaEventRecord(c.ev[3], c.stream));
+      c.sync();
+      ph.mark("reset");
+      float ms_up = 0.f;
+      IPT_CUDA(cudaEventElapsedTime(&ms_up, c.ev[2], c.ev[3]));
+      full_iterate(*P, prm, stats);
+      ph.mark("iterate");
+      full_finalize(*P, prm, stats);
+      ph.mark("finalize+sigma");
+      IPT_CUDA(cudaEventRecord(c.ev[2], c.stream));
+      full_download(*P, z_re, z_im, lam_re, lam_im);
+      IPT_CUDA(cudaEventRecord(c.ev[3], c.stream));
+      c.sync();
+      ph.mark("download");
+      float ms_down = 0.f;
+      IPT_CUDA(cudaEventElapsedTime(&ms_down, c.ev[2], c.ev[3]));
+      if (stats) {
+        stats->ms_upload = ms_up;
+        stats->ms_download = ms_down;
+      }
     }
+    ph.mark("release");
   });
 }
 
