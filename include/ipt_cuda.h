@@ -147,6 +147,16 @@ int ipt_single_finalize(ipt_ctx* ctx, ipt_single_problem* prob, ipt_stats* stats
 int ipt_single_download(ipt_ctx* ctx, ipt_single_problem* prob, double* z_re, double* z_im);
 void ipt_single_free(ipt_single_problem* prob);
 
+/* solve_single_accelerated (anderson.cpp:184-247): memory-m Anderson mixing on the device
+ * (real inputs, one GPU), stop on the true residual |Mz - lambda z|_2 <= residual_tol. */
+int ipt_single_solve_accelerated_dense(ipt_ctx* ctx, int64_t n, const double* d, const double* delta,
+                                       int64_t anchor, const ipt_params* params, int32_t memory,
+                                       double residual_tol, double* z, ipt_stats* stats);
+int ipt_single_solve_accelerated_csr(ipt_ctx* ctx, int64_t n, const double* d, const int64_t* rowptr,
+                                     const int32_t* cols, const double* vals, int64_t anchor,
+                                     const ipt_params* params, int32_t memory, double residual_tol,
+                                     double* z, ipt_stats* stats);
+
 /* apply_map_single (solver.cpp:122-130). */
 int ipt_apply_map_single_dense(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
                                const double* delta_re, const double* delta_im, int64_t anchor,

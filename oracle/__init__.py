@@ -184,6 +184,22 @@ class RefArm(_Arm):
                                                  C.c_uint64(seed), _p(out)))
         return out
 
+    def gen_fci_like(self, n, density, gap_scale, seed):
+        """testgen.cpp:174-194, partitioned: (d, CSR off-diagonal part) as real arrays."""
+        from paper_2012_14702_b200.ipt import CsrMatrix
+
+        nnz = C.c_int64()
+        self._chk(self.lib.ref_gen_fci_like(C.c_int64(n), C.c_double(density), C.c_double(gap_scale),
+                                            C.c_uint64(seed), C.byref(nnz), None, None, None, None))
+        d = np.empty(n)
+        rp = np.empty(n + 1, np.int64)
+        ci = np.empty(nnz.value, np.int64)
+        va = np.empty(nnz.value)
+        self._chk(self.lib.ref_gen_fci_like(C.c_int64(n), C.c_double(density), C.c_double(gap_scale),
+                                            C.c_uint64(seed), C.byref(nnz), _p(d), rp.ctypes.data_as(_i64p),
+                                            ci.ctypes.data_as(_i64p), _p(va)))
+        return d, CsrMatrix(n, n, rp, ci.astype(np.int32), va)
+
     def dense_eigenvalues(self, m):
         m = _c(m)
         out = np.empty(m.shape[0], np.complex128)

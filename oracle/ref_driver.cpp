@@ -327,3 +327,20 @@ REF_API void ref_rng_draws(uint64_t seed, uint64_t stream, int use_stream, int k
     else static_cast<uint64_t*>(out)[i] = rng.below(bound);
   }
 }
+
+// The reference's CI-like sparse generator (testgen.cpp:174-194) as CSR arrays (partition
+// applied: d = diagonal, delta = off-diagonal). Call with rowptr == nullptr to get nnz.
+REF_API int ref_gen_fci_like(int64_t n, double density, double gap_scale, uint64_t seed, int64_t* nnz_out,
+                             double* d, int64_t* rowptr, int64_t* cols, double* vals) {
+  return guarded([&] {
+    const Partition p = partition(gen_fci_like(static_cast<std::size_t>(n), density, gap_scale, seed));
+    *nnz_out = static_cast<int64_t>(p.delta.values().size());
+    if (rowptr == nullptr) return;
+    for (int64_t i = 0; i < n; ++i) d[i] = p.d[i].real();
+    for (int64_t i = 0; i <= n; ++i) rowptr[i] = static_cast<int64_t>(p.delta.row_offsets()[i]);
+    for (int64_t k = 0; k < *nnz_out; ++k) {
+      cols[k] = static_cast<int64_t>(p.delta.col_indices()[k]);
+      vals[k] = p.delta.values()[k].real();
+    }
+  });
+}

@@ -24,6 +24,7 @@ from .ipt import (  # noqa: F401
     smallest_singular_value_estimate,
     solve_full,
     solve_single,
+    solve_single_accelerated,
     solve_single_continuation,
     to_string,
 )

@@ -105,6 +105,10 @@ SIGNATURES = {
     "ipt_matvec_dense": (C.c_int, [_vp, C.c_int64, C.c_int64, _dp, _dp, _dp, _dp, _dp, _dp]),
     "ipt_matvec_csr": (C.c_int, [_vp, C.c_int64, C.c_int64, _i64p, _i32p, _dp, _dp, _dp, _dp, _dp,
                                  _dp]),
+    "ipt_single_solve_accelerated_dense": (C.c_int, [_vp, C.c_int64, _dp, _dp, C.c_int64, C.POINTER(Params),
+                                                     C.c_int32, C.c_double, _dp, C.POINTER(Stats)]),
+    "ipt_single_solve_accelerated_csr": (C.c_int, [_vp, C.c_int64, _dp, _i64p, _i32p, _dp, C.c_int64,
+                                                   C.POINTER(Params), C.c_int32, C.c_double, _dp, C.POINTER(Stats)]),
     "ipt_full_run_maps": (C.c_int, [_vp, _vp, C.c_int32, _dp, _dp]),
     "ipt_single_run_steps": (C.c_int, [_vp, _vp, C.c_int32, _dp, _dp]),
     "ipt_kernel_launch_count": (C.c_int64, []),

@@ -426,6 +426,44 @@ int ipt_single_solve_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const doub
   });
 }
 
+static int accelerated_common(ipt_ctx* ctx, SingleProblem* raw, int64_t anchor, const ipt_params* params,
+                              int32_t memory, double residual_tol, double* z, ipt_stats* stats) {
+  std::unique_ptr<SingleProblem, void (*)(SingleProblem*)> P(raw, single_free);
+  const ipt_params prm = params_or_default(params);
+  single_reset(*P, anchor, nullptr, nullptr, prm.max_iterations);
+  single_accelerated(*P, prm, memory, residual_tol, 0.0, stats);
+  single_download(*P, z, nullptr);
+  (void)ctx;
+  return IPT_OK;
+}
+
+int ipt_single_solve_accelerated_dense(ipt_ctx* ctx, int64_t n, const double* d, const double* delta,
+                                       int64_t anchor, const ipt_params* params, int32_t memory,
+                                       double residual_tol, double* z, ipt_stats* stats) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (anchor < 0 || anchor >= n) throw InvalidArgument("solver: anchor out of range");
+    accelerated_common(ctx, single_upload(ctx->c, n, d, nullptr, false, delta, nullptr, nullptr, nullptr, nullptr,
+                                          nullptr, true),
+                       anchor, params, memory, residual_tol, z, stats);
+  });
+}
+
+int ipt_single_solve_accelerated_csr(ipt_ctx* ctx, int64_t n, const double* d, const int64_t* rowptr,
+                                     const int32_t* cols, const double* vals, int64_t anchor,
+                                     const ipt_params* params, int32_t memory, double residual_tol,
+                                     double* z, ipt_stats* stats) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (anchor < 0 || anchor >= n) throw InvalidArgument("solver: anchor out of range");
+    accelerated_common(ctx, single_upload(ctx->c, n, d, nullptr, true, nullptr, nullptr, rowptr, cols, vals,
+                                          nullptr, true),
+                       anchor, params, memory, residual_tol, z, stats);
+  });
+}
+
 int ipt_apply_map_single_dense(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
                                const double* delta_re, const double* delta_im, int64_t anchor,
                                const double* z_re, const double* z_im, double* f_re, double* f_im) {

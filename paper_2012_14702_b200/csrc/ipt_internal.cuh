@@ -124,6 +124,8 @@ void single_finalize(SingleProblem& P, ipt_stats* stats);
 void single_download(SingleProblem& P, double* z_re, double* z_im);
 void single_matvec(SingleProblem& P, const double* x_re, const double* x_im, double* y_re, double* y_im);
 void single_run_steps(SingleProblem& P, int count, double* ms_total, double* ms_map);
+void single_accelerated(SingleProblem& P, const ipt_params& prm, int memory, double residual_tol,
+                        double regularization, ipt_stats* stats);
 
 // sigma_min (ipt_sigma.cu): Z column-major (ldz), real or complex (zi nullable).
 double sigma_min_device(Ctx& ctx, int64_t n, const double* zr, const double* zi, int64_t ldz,

@@ -90,7 +90,7 @@ inline int spmv_rows_per_block() { return 256 / kSpmvVariants[spmv_variant()].la
 constexpr int kSpmvMinBlocks = 5;       // 48 registers (no spills): 5 CTAs (40 warps) per SM
 constexpr int kSpmvGrid = kNumSMs * kSpmvMinBlocks;  // persistent: exactly one resident wave
 
-enum MapMode : int { kMvStore = 0, kMvMap = 1, kMvFinal = 2 };
+enum MapMode : int { kMvStore = 0, kMvMap = 1, kMvFinal = 2, kMvAccel = 3 };
 
 __device__ __forceinline__ double2 ld_stream(const double2* p) {
   double2 v;
@@ -241,10 +241,25 @@ __device__ __forceinline__ void row_epilogue(const MapArgs& a, int64_t i, double
     v[1] = __fma_rn(zi, zi, v[1]);
     v[2] = __fma_rn(f, f, v[2]);
     v[3] = nan_max(v[3], fabs(df));
-  } else {  // kMvFinal: residual |d z + w - lam z|^2 and |z|^2 (solver.cpp:86-91)
+  } else if (MODE == kMvFinal) {  // residual |d z + w - lam z|^2 and |z|^2 (solver.cpp:86-91)
     const double r = __dsub_rn(__dadd_rn(__dmul_rn(a.d[i], zi), w), __dmul_rn(lam, zi));
     v[0] = __fma_rn(r, r, v[0]);
     v[1] = __fma_rn(zi, zi, v[1]);
+  } else {  // kMvAccel: true residual AND the plain image f(z) (anderson.cpp:204-223)
+    const double r = __dsub_rn(__dadd_rn(__dmul_rn(a.d[i], zi), w), __dmul_rn(lam, zi));
+    double f;
+    if (i == a.anchor) {
+      f = 1.0;
+    } else {
+      const double g = __ddiv_rn(1.0, __dsub_rn(a.d[i], a.d[a.anchor]));
+      f = __dmul_rn(g, __dsub_rn(__dmul_rn(zi, *a.wa), w));
+    }
+    a.fz[i] = f;
+    const double df = __dsub_rn(f, zi);
+    v[0] = __fma_rn(r, r, v[0]);
+    v[1] = __fma_rn(zi, zi, v[1]);
+    v[2] = __fma_rn(df, df, v[2]);
+    v[3] = nan_max(v[3], fabs(df));
   }
 }
 
@@ -267,7 +282,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_map_kernel(const double*
   if (nrows > 0) rows_dot<kGemvRows>(A + lr0 * lda, lda, nrows, a.z, lda / 2, w);
   double v[4] = {0.0, 0.0, 0.0, 0.0};
   const double scale = MODE == kMvMap ? schedule_scale(a) : 1.0;
-  const double lam = MODE == kMvFinal ? a.d[a.anchor] + *a.wa : 0.0;
+  const double lam = (MODE == kMvFinal || MODE == kMvAccel) ? a.d[a.anchor] + *a.wa : 0.0;
 #pragma unroll
   for (int r = 0; r < kGemvRows; ++r)
     if (lane == r && r < nrows) row_epilogue<MODE>(a, a.row0 + lr0 + r, w[r], scale, lam, v);
@@ -289,7 +304,7 @@ __global__ void __launch_bounds__(256, kSpmvMinBlocks) spmv_map_kernel(const int
   const int sl = threadIdx.x % LANES;
   double v[4] = {0.0, 0.0, 0.0, 0.0};
   const double scale = MODE == kMvMap ? schedule_scale(a) : 1.0;
-  const double lam = MODE == kMvFinal ? a.d[a.anchor] + *a.wa : 0.0;
+  const double lam = (MODE == kMvFinal || MODE == kMvAccel) ? a.d[a.anchor] + *a.wa : 0.0;
   const uint64_t pol_s = policy_stream(), pol_k = policy_keep();
   // Persistent fixed grid: block b owns row groups b, b + grid, ... (a fixed map, so the
   // per-block partial sums and their reduction are run-to-run identical).
@@ -554,10 +569,11 @@ void reduce_and_allreduce(SingleProblem& P, const LoopState* st, bool with_max) 
 }
 
 template <int MODE>
-void enqueue_real_map(SingleProblem& P, int src, const ipt_params* prm) {
+void enqueue_real_map(SingleProblem& P, int src, const ipt_params* prm, double* fz_out = nullptr) {
   cudaStream_t s = P.ctx->stream;
   MapArgs a = map_args(P, src);
-  if (MODE == kMvFinal) a.state = nullptr;
+  if (MODE == kMvFinal || MODE == kMvAccel) a.state = nullptr;
+  if (fz_out) a.fz = fz_out;
   if (prm) {
     a.schedule = prm->schedule;
     a.snap = 0.25 * prm->tolerance;
@@ -930,4 +946,375 @@ void single_matvec(SingleProblem& P, const double* x_re, const double* x_im, dou
   c.sync();
 }
 
+
+// ======================================================================================
+// Anderson-accelerated single pair (solve_single_accelerated, proj/src/anderson.cpp:15-247),
+// real inputs, one device. Per pass: the fused kMvAccel map kernel gives the true residual
+// |Dz + w - lambda z| (the stop test, anderson.cpp:204-215) and the plain image f(z) in
+// one sweep of Delta; the memory-m mixing (anderson.cpp:95-178) runs on device vectors:
+// difference columns, modified Gram-Schmidt with one reorthogonalisation pass, the
+// affine recombination of the stored images and the anchor re-pin. Every inner product is
+// a fixed-order reduction; the h x h triangular / Tikhonov solves run on the host.
+// ======================================================================================
+namespace {
+
+constexpr int kVecBlocks = 296;
+
+__global__ void vdot_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+                            double* __restrict__ partials) {
+  __shared__ double red[8][4];
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    v[0] = __fma_rn(a[i], b[i], v[0]);
+  block_reduce4<8>(v, red);
+  if (threadIdx.x == 0) {
+    double* o = partials + size_t(blockIdx.x) * 4;
+    o[0] = v[0]; o[1] = 0.0; o[2] = 0.0; o[3] = 0.0;
+  }
+}
+// y -= c[0] * x   (MGS projection, anderson.cpp:32)
+__global__ void vaxpy_kernel(double* __restrict__ y, const double* __restrict__ x, int64_t n, const double* c) {
+  const double cc = *c;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    y[i] = __fma_rn(-cc, x[i], y[i]);
+}
+// q = v / sqrt(nn[0])   (anderson.cpp:38-39)
+__global__ void vnormalize_kernel(double* __restrict__ q, const double* __restrict__ v, int64_t n, const double* nn) {
+  const double vn = sqrt(*nn);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    q[i] = v[i] / vn;
+}
+__global__ void vsub_kernel(double* __restrict__ d, const double* __restrict__ a, const double* __restrict__ b, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    d[i] = __dsub_rn(a[i], b[i]);
+}
+struct ImgList {
+  const double* img[17];
+  double w[17];
+  int count;
+};
+// next = sum_j w_j img_j, accumulated in j order from 0 (anderson.cpp:154-159)
+__global__ void vcombine_kernel(double* __restrict__ next, const ImgList L, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < L.count; ++j) s = __fma_rn(L.w[j], L.img[j][i], s);
+    next[i] = s;
+  }
+}
+// re-pin the chart coordinate (anderson.cpp:162-167): divide by next[a] unless it is 0 or 1
+__global__ void vrepin_kernel(double* __restrict__ next, int64_t n, int64_t anchor, const double* za_p) {
+  const double za = *za_p;
+  const bool div = za != 0.0 && za != 1.0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    if (i == anchor) next[i] = 1.0;
+    else if (div) next[i] = next[i] / za;
+  }
+}
+__global__ void copy_scalar_kernel(double* dst, const double* src) { *dst = *src; }
+
+struct AccelWork {
+  SingleProblem& P;
+  int64_t n;
+  cudaStream_t s;
+  DevBuf part, scal;
+  int next_slot = 0;
+  explicit AccelWork(SingleProblem& p) : P(p), n(p.n), s(p.ctx->stream) {
+    part.alloc(size_t(kVecBlocks) * 4);
+    scal.alloc(4 * 1024);
+  }
+  double* slot() {  // a fresh 4-double device scalar slot (reset each iteration)
+    if (next_slot >= 1024) throw InvalidArgument("anderson: scalar pool exhausted");
+    return scal.get() + 4 * (next_slot++);
+  }
+  double* dot(const double* a, const double* b) {
+    double* out = slot();
+    vdot_kernel<<<kVecBlocks, 256, 0, s>>>(a, b, n, part.get());
+    reduce_partials(s, part.get(), kVecBlocks, out, nullptr);
+    count_launch();
+    return out;
+  }
+  void axpy(double* y, const double* x, const double* c) {
+    vaxpy_kernel<<<kVecBlocks, 256, 0, s>>>(y, x, n, c);
+    count_launch();
+  }
+  void normalize(double* q, const double* v, const double* nn) {
+    vnormalize_kernel<<<kVecBlocks, 256, 0, s>>>(q, v, n, nn);
+    count_launch();
+  }
+  void sub(double* d, const double* a, const double* b) {
+    vsub_kernel<<<kVecBlocks, 256, 0, s>>>(d, a, b, n);
+    count_launch();
+  }
+  void copy(double* d, const double* a) { IPT_CUDA(cudaMemcpyAsync(d, a, sizeof(double) * n, cudaMemcpyDeviceToDevice, s)); }
+};
+
+// Host replica of lu_factor / lu_solve for the tiny Tikhonov system (lu.cpp:10-69).
+bool small_lu_solve(std::vector<double> a, int h, std::vector<double> b, std::vector<double>& x) {
+  std::vector<int> perm(h);
+  for (int i = 0; i < h; ++i) perm[i] = i;
+  double scale = 0.0;
+  for (double v : a) scale = std::max(scale, std::fabs(v));
+  const double tiny = scale * 2.220446049250313e-16 * h;
+  for (int k = 0; k < h; ++k) {
+    int piv = k;
+    double best = std::fabs(a[k * h + k]);
+    for (int i = k + 1; i < h; ++i)
+      if (std::fabs(a[i * h + k]) > best) best = std::fabs(a[i * h + k]), piv = i;
+    if (best <= tiny) return false;
+    if (piv != k) {
+      for (int j = 0; j < h; ++j) std::swap(a[k * h + j], a[piv * h + j]);
+      std::swap(perm[k], perm[piv]);
+    }
+    for (int i = k + 1; i < h; ++i) {
+      const double m = a[i * h + k] / a[k * h + k];
+      a[i * h + k] = m;
+      if (m != 0.0)
+        for (int j = k + 1; j < h; ++j) a[i * h + j] -= m * a[k * h + j];
+    }
+  }
+  x.assign(h, 0.0);
+  for (int i = 0; i < h; ++i) x[i] = b[perm[i]];
+  for (int i = 1; i < h; ++i)
+    for (int j = 0; j < i; ++j) x[i] -= a[i * h + j] * x[j];
+  for (int i = h - 1; i >= 0; --i) {
+    for (int j = i + 1; j < h; ++j) x[i] -= a[i * h + j] * x[j];
+    x[i] /= a[i * h + i];
+  }
+  for (double v : x)
+    if (!std::isfinite(v)) return false;
+  return true;
+}
+
+}  // namespace
+
+void single_accelerated(SingleProblem& P, const ipt_params& prm, int memory, double residual_tol,
+                        double regularization, ipt_stats* stats) {
+  Ctx& c = *P.ctx;
+  if (P.cplx) throw InvalidArgument("solve_single_accelerated (device): real inputs only");
+  if (c.nranks != 1) throw InvalidArgument("solve_single_accelerated (device): single GPU only");
+  if (memory < 0 || memory > 16) throw InvalidArgument("anderson: memory must lie in [0, 16]");
+  if (!(prm.tolerance > 0.0)) throw InvalidArgument("config: tolerance must be positive");
+  if (prm.max_iterations <= 0) throw InvalidArgument("config: max_iterations must be positive");
+  const int64_t n = P.n;
+  AccelWork W(P);
+  cudaStream_t s = W.s;
+  // work vectors (length of the padded iterate so the GEMV's 16-byte loads stay in bounds)
+  const size_t vlen = P.z[0].count;
+  DevBuf fzb, gcur, vtmp, nxt;
+  fzb.alloc(vlen);
+  gcur.alloc(vlen);
+  vtmp.alloc(vlen);
+  nxt.alloc(vlen);
+  std::vector<DevBuf> Hg(memory + 1), Hf(memory + 1), Q(std::max(memory, 1)), Cc(std::max(memory, 1));
+  for (auto& b : Hg) b.alloc(vlen);
+  for (auto& b : Hf) b.alloc(vlen);
+  for (auto& b : Q) b.alloc(vlen);
+  for (auto& b : Cc) b.alloc(vlen);
+  std::vector<int> hist;  // slot indices into Hg/Hf, oldest first
+  std::vector<int> free_slots;
+  for (int k = memory; k >= 0; --k) free_slots.push_back(k);
+  double prev_res = -1.0;
+  int streak = 0;
+  std::vector<double> trace;
+  int cur = 0;  // z lives in P.z[cur]
+  int iterations = 0, status = kMaxIterations;
+  long matvecs = 0;
+  double final_step = 0.0, lam = 0.0, resid = 0.0;
+  bool finished = false;
+  std::vector<double> h4(4);
+  auto fetch = [&](const double* dptr, double* out, int count) {
+    IPT_CUDA(cudaMemcpyAsync(out, dptr, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+  };
+  for (int k = 0; k < prm.max_iterations; ++k) {
+    W.next_slot = 0;
+    enqueue_anchor(P, cur, nullptr);
+    enqueue_real_map<kMvAccel>(P, cur, &prm, fzb.get());
+    reduce_partials(s, P.partials.get(), map_blocks(P), P.sums.get(), nullptr);
+    double wa = 0.0;
+    fetch(P.sums.get(), h4.data(), 4);
+    fetch(P.wa.get(), &wa, 1);
+    c.sync();
+    ++matvecs;
+    iterations = k + 1;
+    const double da = [&] {
+      double v = 0.0;
+      IPT_CUDA(cudaMemcpy(&v, P.dre.get() + P.anchor, sizeof(double), cudaMemcpyDeviceToHost));
+      return v;
+    }();
+    const double lambda = da + wa;
+    const double rnorm = std::sqrt(h4[0]), znorm = std::sqrt(h4[1]);
+    if (rnorm <= residual_tol) {
+      lam = lambda;
+      resid = rnorm / znorm;
+      status = kConverged;
+      finished = true;
+      break;
+    }
+    const double step = std::sqrt(h4[2]) / std::sqrt(h4[1]);  // rel_step(z, fz)
+    const double res = std::sqrt(h4[2]);                       // |f(z) - z|
+    // restart after three consecutive worsening residuals (anderson.cpp:99-112)
+    if (prev_res >= 0.0 && res > prev_res) {
+      if (++streak >= 3) {
+        for (int sl : hist) free_slots.push_back(sl);
+        hist.clear();
+        streak = 0;
+      }
+    } else {
+      streak = 0;
+    }
+    prev_res = res;
+    double* z = P.z[cur].get();
+    W.sub(gcur.get(), fzb.get(), z);  // g = f(z) - z
+    const int h = static_cast<int>(hist.size());
+    double* znew = nullptr;
+    if (memory == 0 || h == 0) {
+      znew = fzb.get();
+    } else {
+      // difference columns C_j = g_{j+1} - g_j over the history extended by the current g
+      for (int j = 0; j < h; ++j) W.sub(Cc[j].get(), j + 1 < h ? Hg[hist[j + 1]].get() : gcur.get(), Hg[hist[j]].get());
+      double* fro_parts[17];
+      for (int j = 0; j < h; ++j) fro_parts[j] = W.dot(Cc[j].get(), Cc[j].get());
+      // MGS with reorthogonalisation (anderson.cpp:26-40)
+      std::vector<std::vector<double*>> rc(h, std::vector<double*>(h * 2, nullptr));
+      std::vector<double*> vn2(h);
+      for (int j = 0; j < h; ++j) {
+        W.copy(vtmp.get(), Cc[j].get());
+        for (int pass = 0; pass < 2; ++pass)
+          for (int i = 0; i < j; ++i) {
+            double* cc = W.dot(Q[i].get(), vtmp.get());
+            rc[j][pass * h + i] = cc;
+            W.axpy(vtmp.get(), Q[i].get(), cc);
+          }
+        vn2[j] = W.dot(vtmp.get(), vtmp.get());
+        W.normalize(Q[j].get(), vtmp.get(), vn2[j]);
+      }
+      std::vector<double*> bq(h);
+      for (int i = 0; i < h; ++i) bq[i] = W.dot(Q[i].get(), gcur.get());
+      std::vector<double> S(4 * 1024);
+      fetch(W.scal.get(), S.data(), 4 * W.next_slot);
+      c.sync();
+      auto val = [&](double* d) { return S[static_cast<size_t>(d - W.scal.get())]; };
+      double fro = 0.0;
+      for (int j = 0; j < h; ++j) fro += val(fro_parts[j]);
+      fro = std::sqrt(fro);
+      const double rank_tol = 1e-13 * fro;
+      std::vector<double> R(h * h, 0.0), b(h), gamma;
+      bool ok = true;
+      for (int j = 0; j < h && ok; ++j) {
+        for (int pass = 0; pass < 2; ++pass)
+          for (int i = 0; i < j; ++i) R[i * h + j] += val(rc[j][pass * h + i]);
+        const double vn = std::sqrt(val(vn2[j]));
+        if (!(vn > rank_tol)) ok = false;
+        R[j * h + j] = vn;
+      }
+      if (ok) {
+        for (int i = 0; i < h; ++i) b[i] = val(bq[i]);
+        gamma.assign(h, 0.0);
+        for (int ii = h - 1; ii >= 0; --ii) {
+          double sacc = b[ii];
+          for (int j = ii + 1; j < h; ++j) sacc -= R[ii * h + j] * gamma[j];
+          gamma[ii] = sacc / R[ii * h + ii];
+        }
+      } else {  // Tikhonov-regularised normal equations (anderson.cpp:55-79)
+        W.next_slot = 0;
+        std::vector<double*> gram(h * h), gb(h);
+        for (int i = 0; i < h; ++i) {
+          for (int j = 0; j < h; ++j) gram[i * h + j] = W.dot(Cc[i].get(), Cc[j].get());
+          gb[i] = W.dot(Cc[i].get(), gcur.get());
+        }
+        fetch(W.scal.get(), S.data(), 4 * W.next_slot);
+        c.sync();
+        std::vector<double> A(h * h), bb(h);
+        double sc = 0.0;
+        for (int i = 0; i < h; ++i) {
+          for (int j = 0; j < h; ++j) A[i * h + j] = val(gram[i * h + j]);
+          sc = std::max(sc, std::fabs(A[i * h + i]));
+          bb[i] = val(gb[i]);
+        }
+        const double lambda_reg = (regularization > 0.0 ? regularization : 1e-12) * sc;
+        for (int i = 0; i < h; ++i) A[i * h + i] += lambda_reg;
+        ok = small_lu_solve(A, h, bb, gamma);
+      }
+      if (!ok) {
+        znew = fzb.get();
+      } else {
+        ImgList L{};
+        L.count = h + 1;
+        L.w[0] = gamma[0];
+        for (int j = 1; j < h; ++j) L.w[j] = gamma[j] - gamma[j - 1];
+        L.w[h] = 1.0 - gamma[h - 1];
+        for (int j = 0; j < h; ++j) L.img[j] = Hf[hist[j]].get();
+        L.img[h] = fzb.get();
+        vcombine_kernel<<<kVecBlocks, 256, 0, s>>>(nxt.get(), L, n);
+        double* za = W.slot();
+        copy_scalar_kernel<<<1, 1, 0, s>>>(za, nxt.get() + P.anchor);
+        vrepin_kernel<<<kVecBlocks, 256, 0, s>>>(nxt.get(), n, P.anchor, za);
+        count_launch(3);
+        znew = nxt.get();
+      }
+    }
+    // push (g, f(z)) and drop the oldest beyond the memory (anderson.cpp:169-175)
+    if (memory > 0) {
+      const int slot = free_slots.back();
+      free_slots.pop_back();
+      W.copy(Hg[slot].get(), gcur.get());
+      W.copy(Hf[slot].get(), fzb.get());
+      hist.push_back(slot);
+      while (static_cast<int>(hist.size()) > memory) {
+        free_slots.push_back(hist.front());
+        hist.erase(hist.begin());
+      }
+    }
+    W.copy(P.z[cur ^ 1].get(), znew);
+    cur ^= 1;
+    final_step = step;
+    if (prm.record_trace) trace.push_back(step);
+    double* zz = W.dot(P.z[cur].get(), P.z[cur].get());
+    double zn2 = 0.0;
+    fetch(zz, &zn2, 1);
+    c.sync();
+    const double zn = std::sqrt(zn2);
+    if (!std::isfinite(zn) || zn > prm.divergence_threshold) {
+      status = kDiverged;
+      break;
+    }
+  }
+  if (!finished) {  // closing product (anderson.cpp:238-245)
+    enqueue_anchor(P, cur, nullptr);
+    enqueue_real_map<kMvFinal>(P, cur, nullptr);
+    reduce_partials(s, P.partials.get(), map_blocks(P), P.sums.get(), nullptr);
+    double wa = 0.0, da = 0.0;
+    fetch(P.sums.get(), h4.data(), 4);
+    fetch(P.wa.get(), &wa, 1);
+    c.sync();
+    IPT_CUDA(cudaMemcpy(&da, P.dre.get() + P.anchor, sizeof(double), cudaMemcpyDeviceToHost));
+    ++matvecs;
+    lam = da + wa;
+    resid = std::sqrt(h4[0]) / std::sqrt(h4[1]);
+  }
+  // expose the result where single_download reads it (P.z[iterations & 1])
+  LoopState st{};
+  st.iterations = iterations;
+  st.status = status;
+  st.done = 1;
+  st.final_step = final_step;
+  if (cur != (iterations & 1)) {
+    IPT_CUDA(cudaMemcpyAsync(P.z[iterations & 1].get(), P.z[cur].get(), sizeof(double) * n,
+                             cudaMemcpyDeviceToDevice, s));
+  }
+  IPT_CUDA(cudaMemcpyAsync(P.state, &st, sizeof(LoopState), cudaMemcpyHostToDevice, s));
+  *c.h_state = st;
+  c.sync();
+  if (stats) {
+    stats->iterations = iterations;
+    stats->status = status;
+    stats->final_step = final_step;
+    stats->residual = resid;
+    stats->eigenvalue_re = lam;
+    stats->eigenvalue_im = 0.0;
+    stats->product_count = matvecs;
+    if (prm.record_trace && stats->trace)
+      std::memcpy(stats->trace, trace.data(), sizeof(double) * trace.size());
+  }
+}
 }  // namespace iptb

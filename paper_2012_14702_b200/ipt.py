@@ -512,6 +512,54 @@ def solve_single_continuation(p: Partition, g: InverseGaps, anchor: int, config:
     return _single_call(p, g, anchor, config, None, _lib.SCHEDULE_CONTINUATION, shrink_alpha, ctx)
 
 
+def solve_single_accelerated(p: Partition, g: InverseGaps, anchor: int, config: IterationConfig = None,
+                             memory: int = 5, ctx: Optional[Context] = None) -> EigenpairResult:
+    """Memory-m Anderson-mixed single pair on the device (anderson.cpp:184-247): stops on the
+    true residual |Mz - lambda z|_2 <= config.residual_tolerance. Real inputs, one GPU."""
+    config = config or IterationConfig()
+    _check_sizes(p, g, anchor)
+    if not (config.tolerance > 0.0):
+        raise ValueError("config: tolerance must be positive")
+    if config.max_iterations <= 0:
+        raise ValueError("config: max_iterations must be positive")
+    if memory < 0:
+        raise ValueError("anderson: memory must be non-negative")
+    if _is_complex_problem(p):
+        raise ValueError("solve_single_accelerated (device): real inputs only")
+    n = p.size()
+    ctx = ctx or default_context()
+    lib = _lib.load()
+    d = np.ascontiguousarray(np.real(p.d), dtype=np.float64)
+    z = np.empty(n)
+    prm = _params(config)
+    st = _lib.Stats()
+    tr = np.zeros(config.max_iterations) if config.record_trace else None
+    st.trace = dptr(tr)
+    if isinstance(p.delta, CsrMatrix):
+        vals = np.ascontiguousarray(np.real(p.delta.values), dtype=np.float64)
+        check(lib.ipt_single_solve_accelerated_csr(ctx.handle, n, dptr(d), i64ptr(p.delta.row_offsets),
+                                                   i32ptr(p.delta.col_indices), dptr(vals), int(anchor), C.byref(prm),
+                                                   int(memory), float(config.residual_tolerance), dptr(z),
+                                                   C.byref(st)))
+    else:
+        a = np.ascontiguousarray(np.real(p.delta), dtype=np.float64)
+        check(lib.ipt_single_solve_accelerated_dense(ctx.handle, n, dptr(d), dptr(a), int(anchor), C.byref(prm),
+                                                     int(memory), float(config.residual_tolerance), dptr(z),
+                                                     C.byref(st)))
+    res = EigenpairResult()
+    res.z = z
+    res.eigenvalue = st.eigenvalue_re
+    res.anchor = int(anchor)
+    res.iterations = st.iterations
+    res.final_step = st.final_step
+    res.residual = st.residual
+    res.status = SolveStatus(st.status)
+    res.matvec_count = st.product_count
+    if config.record_trace:
+        res.trace = list(tr[: max(st.iterations - (1 if res.status == SolveStatus.Converged else 0), 0)])
+    return res
+
+
 def apply_map_single(p: Partition, g: InverseGaps, anchor: int, z, ctx: Optional[Context] = None) -> np.ndarray:
     """f_i(z) = e_i + g_i o (z (Delta z)_i - Delta z) (solver.cpp:122-130)."""
     _check_sizes(p, g, anchor)

@@ -178,6 +178,31 @@ def single_configs(big):
     save("single_configs.npz", **out)
 
 
+def accelerated():
+    """solve_single_accelerated (anderson.cpp:184-247) on the acceptance #7 instance
+    (gen_fci_like N=4096, density 50/N, gap 20, seed 2718281828) and two variants."""
+    R = oracle.ref()
+    out = {}
+    for name, (n, dens, gap, seed) in {"acc7": (4096, 50.0 / 4096, 20.0, 2718281828),
+                                       "fci2k": (2048, 40.0 / 2048, 5.0, 77)}.items():
+        d, delta = R.gen_fci_like(n, dens, gap, seed)
+        out[name + "_d"] = d
+        out[name + "_rowptr"] = delta.row_offsets
+        out[name + "_cols"] = delta.col_indices
+        out[name + "_vals"] = delta.values
+        for mem in (0, 2, 5):
+            a = R.solve_single(d, delta, 0, mode="accelerated", memory=mem, residual_tol=1e-8, record_trace=True)
+            key = f"{name}_m{mem}"
+            out[key + "_z"] = a["z"].real
+            out[key + "_meta"] = np.array([a["iterations"], a["status"], a["eigenvalue"].real, a["residual"],
+                                           a["final_step"], a["matvec_count"]])
+            out[key + "_trace"] = a["trace"]
+            print(f"{key}: {a['matvec_count']} matvecs, status {a['status']}", flush=True)
+        p = R.solve_single(d, delta, 0, residual_tol=1e-8)
+        out[name + "_plain_meta"] = np.array([p["iterations"], p["status"], p["eigenvalue"].real, p["matvec_count"]])
+    save("accelerated.npz", **out)
+
+
 def full_columns(big):
     """Configs 2/3: reference solve_single(j) columns (test_solver.cpp:188-201 route)."""
     R = oracle.ref()
@@ -202,7 +227,7 @@ if __name__ == "__main__":
     ap.add_argument("--only", default="")
     a = ap.parse_args()
     oracle.build()
-    jobs = dict(small=small_cases, config1=config1, single=lambda: single_configs(a.big),
+    jobs = dict(small=small_cases, config1=config1, accel=accelerated, single=lambda: single_configs(a.big),
                 columns=lambda: full_columns(a.big))
     for name, fn in jobs.items():
         if a.only and name not in a.only.split(","):

@@ -233,3 +233,28 @@ def test_config4_full_size_n65536(port_arm):
     assert r.eigenvalue == pytest.approx(o["eigenvalue"], rel=1e-10)
     assert np.max(np.abs(r.z - o["z"])) <= 1e-9
     assert r.residual <= 1e-12 and r.z[0] == 1.0
+
+
+# ----------------------------------------------------------------- Anderson mixing on the device
+
+
+@pytest.mark.parametrize("name", ["acc7", "fci2k"])
+@pytest.mark.parametrize("memory", [0, 2, 5])
+def test_accelerated_matches_reference(name, memory):
+    """solve_single_accelerated (anderson.cpp:184-247) on the acceptance #7 instance
+    (gen_fci_like N=4096) and a second CI-like case, memory 0/2/5, against the reference."""
+    g = golden("accelerated.npz")
+    n = g[name + "_d"].size
+    p = ipt.Partition(g[name + "_d"], ipt.CsrMatrix(n, n, g[name + "_rowptr"], g[name + "_cols"], g[name + "_vals"]))
+    cfg = ipt.IterationConfig(residual_tolerance=1e-8, record_trace=True)
+    r = ipt.solve_single_accelerated(p, ipt.build_gaps(p), 0, cfg, memory)
+    meta = g[f"{name}_m{memory}_meta"]
+    assert int(r.status) == int(meta[1]) == 0
+    assert abs(r.matvec_count - int(meta[5])) <= 1
+    assert r.residual <= 1e-8 / np.linalg.norm(r.z) * 1.0001
+    assert r.eigenvalue == pytest.approx(meta[2], rel=1e-10)
+    assert np.max(np.abs(r.z - g[f"{name}_m{memory}_z"])) <= 1e-9
+    # memory 0 is the plain iteration with the residual stop (test_anderson.cpp:8-19)
+    if memory == 0:
+        plain = ipt.solve_single(p, ipt.build_gaps(p), 0, ipt.IterationConfig(tolerance=1e-12))
+        assert r.eigenvalue == pytest.approx(plain.eigenvalue, rel=1e-9)
