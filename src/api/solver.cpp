@@ -196,6 +196,49 @@ namespace b200 {
 
 void set_device(int device) { api::set_device(device); }
 
+EigenpairResult solve_single_accelerated(const Partition& p, const InverseGaps& g, std::size_t anchor,
+                                         const IterationConfig& config, int memory) {
+    if (!(config.tolerance > 0.0)) throw std::invalid_argument("config: tolerance must be positive");
+    if (config.max_iterations <= 0) throw std::invalid_argument("config: max_iterations must be positive");
+    check_anchor(p, g, anchor);
+    const std::size_t n = p.size();
+    const Planar d = api::split(p.d.data(), n);
+    ipt_params prm = to_params(config);
+    ipt_stats st{};
+    std::vector<double> trace(config.record_trace ? config.max_iterations : 0);
+    st.trace = config.record_trace ? trace.data() : nullptr;
+    Vec z(n);
+    if (p.delta.is_sparse()) {
+        const api::Csr c = api::to_csr(p.delta);
+        if (d.any_im || c.val.any_im) throw std::invalid_argument("solve_single_accelerated (device): real inputs only");
+        api::check(ipt_single_solve_accelerated_csr(api::context(), static_cast<int64_t>(n), d.re.data(),
+                                                    c.rowptr.data(), c.cols.data(), c.val.re.data(),
+                                                    static_cast<int64_t>(anchor), &prm, memory,
+                                                    config.residual_tolerance, z.data(), &st));
+    } else {
+        const Planar a = api::split(p.delta.data(), n * n);
+        if (d.any_im || a.any_im) throw std::invalid_argument("solve_single_accelerated (device): real inputs only");
+        api::check(ipt_single_solve_accelerated_dense(api::context(), static_cast<int64_t>(n), d.re.data(),
+                                                      a.re.data(), static_cast<int64_t>(anchor), &prm, memory,
+                                                      config.residual_tolerance, z.data(), &st));
+    }
+    EigenpairResult r;
+    r.z.resize(n);
+    for (std::size_t i = 0; i < n; ++i) r.z[i] = cplx(z[i], 0.0);
+    r.eigenvalue = cplx(st.eigenvalue_re, 0.0);
+    r.anchor = anchor;
+    r.iterations = st.iterations;
+    r.final_step = st.final_step;
+    r.residual = st.residual;
+    r.status = static_cast<SolveStatus>(st.status);
+    r.matvec_count = static_cast<long>(st.product_count);
+    if (config.record_trace) {
+        const int kept = st.iterations - (r.status == SolveStatus::Converged ? 1 : 0);
+        r.trace.assign(trace.begin(), trace.begin() + std::max(kept, 0));
+    }
+    return r;
+}
+
 SpectrumResult solve_full(const Partition& p, const InverseGaps& g, const IterationConfig& config,
                           const FullOptions& options, const ComplexMatrix* warm_start) {
     validate(config);
