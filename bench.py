@@ -167,7 +167,7 @@ def traffic_for(kernel, n=None):
 # --------------------------------------------------------------------------- CPU baseline
 
 
-def cpu_reference_sample(n=2048, reps=2):
+def cpu_reference_sample(n=4096, reps=2):
     """The reference's own apply_map_full (solver.cpp:156-178; kernels.cpp dgemm) on the
     host cores, one map application at a bounded N of the same construction."""
     import oracle
@@ -300,7 +300,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", type=int, default=N_FULL)
-    ap.add_argument("--ref-n", type=int, default=2048)
+    ap.add_argument("--ref-n", type=int, default=4096)
     ap.add_argument("--secondary", default="all", choices=["all", "none", "gemv", "spmv"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -402,6 +402,23 @@ def main():
                 secondary[which] = bench_single(ipt, lib, ctx, which, max(args.steps, 10), 3, hbm)
             except Exception as exc:  # report, never hide
                 secondary[which] = {"error": repr(exc)}
+        if args.secondary == "all":
+            try:  # the low end of the metric's N range: configs[1], N = 8192, through the C ABI
+                p2 = synth.config2()
+                ipt.solve_full(p2, ipt.build_gaps(p2), ipt.IterationConfig(tolerance=1e-12), ctx=ctx)  # warm
+                t0 = time.perf_counter()
+                r2 = ipt.solve_full(p2, ipt.build_gaps(p2), ipt.IterationConfig(tolerance=1e-12), ctx=ctx)
+                t2 = time.perf_counter() - t0
+                secondary["full_n8192"] = {
+                    "workload": "configs[1] full spectrum N=8192, eps=0.32/sqrt(N), tol 1e-12 (C ABI, host buffers)",
+                    "time_to_solution_s": t2, "iterations": r2.iterations, "status": ipt.to_string(r2.status),
+                    "e2e_tflops": 2.0 * 8192 ** 3 * r2.iterations / t2 / 1e12,
+                    "loop_tflops": 2.0 * 8192 ** 3 * r2.iterations / (r2.timings_ms["loop"] * 1e-3) / 1e12,
+                    "timings_ms": r2.timings_ms, "lambda0": float(r2.eigenvalues[0]),
+                    "residual_frobenius": r2.residual_frobenius, "sigma_min": r2.min_singular_value_estimate}
+                del p2, r2
+            except Exception as exc:
+                secondary["full_n8192"] = {"error": repr(exc)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -423,7 +440,7 @@ def main():
                          "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                          "flops_per_launch": gemm_flops_local, "kernel_ms": gemm_ms_local,
                          "kernel_share_of_step": gemm_ms / step_ms,
-                         "traffic": traffic_for("dmma_tma_kernel<1>", n)},
+                         "traffic": traffic_for("dmma_tma_kernel<1>", n) if world == 1 else None},
             "time_to_solution": solve_info,
             "e2e": e2e,
             "cpu_baseline": cpu,
