@@ -115,6 +115,24 @@ int ipt_apply_map_full(ipt_ctx* ctx, int64_t n, const double* d_re, const double
                        const double* delta_re, const double* delta_im, const double* z_re,
                        const double* z_im, double* f_re, double* f_im);
 
+/* Sparse Delta (CSR: rowptr[n+1], cols[nnz], vals[nnz]) for the same full-spectrum
+ * entry points: solve_full / apply_map_full when Partition::delta is CSR
+ * (partition.cpp:43 builds it; kernels.cpp:88-108 multiplies it). A real CSR Delta
+ * runs the fused SpMM map (Z row-major on the device); a complex one is densified
+ * and takes the dense complex path. */
+int ipt_full_solve_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                       const int64_t* rowptr, const int32_t* cols, const double* val_re,
+                       const double* val_im, const double* warm_re, const double* warm_im,
+                       const ipt_params* params, double* z_re, double* z_im, double* lam_re,
+                       double* lam_im, ipt_stats* stats);
+int ipt_full_upload_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                        const int64_t* rowptr, const int32_t* cols, const double* val_re,
+                        const double* val_im, ipt_full_problem** out);
+int ipt_apply_map_full_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                           const int64_t* rowptr, const int32_t* cols, const double* val_re,
+                           const double* val_im, const double* z_re, const double* z_im,
+                           double* f_re, double* f_im);
+
 /* smallest_singular_value_estimate (solver.cpp:275-297). */
 int ipt_sigma_min(ipt_ctx* ctx, int64_t n, const double* z_re, const double* z_im,
                   int32_t max_iters, double tol, double* out);

@@ -140,6 +140,29 @@ class RefArm(_Arm):
                                                   C.c_int64(k), C.c_double(tol), C.c_int(max_iter), _p(z), _p(meta)))
         return z.T.copy(), meta[:, 0].astype(int), meta[:, 1].astype(int), meta[:, 2] + 1j * meta[:, 3]
 
+    def solve_full_csr(self, d, delta, tol=100 * np.finfo(float).eps, max_iter=1000, div_thr=1e8):
+        """solve_full on a CSR Delta (the reference's sparse product, kernels.cpp:88-108)."""
+        n = len(d)
+        rp, ci, va = _csr_args(delta)
+        z = np.empty((n, n), np.complex128)
+        lam = np.empty(n, np.complex128)
+        stats = np.zeros(8)
+        self._chk(self.lib.ref_solve_full_csr(C.c_int64(n), _p(_c(d)), rp.ctypes.data_as(_i64p),
+                                              ci.ctypes.data_as(_i64p), _p(va), C.c_double(tol),
+                                              C.c_int(max_iter), C.c_double(div_thr), _p(z), _p(lam),
+                                              _p(stats)))
+        return dict(Z=z, eigenvalues=lam, iterations=int(stats[0]), status=int(stats[1]), final_step=stats[2],
+                    residual_frobenius=stats[3], sigma_min=stats[4], matmul_count=int(stats[5]),
+                    seconds=stats[6])
+
+    def apply_map_full_csr(self, d, delta, z):
+        n = len(d)
+        rp, ci, va = _csr_args(delta)
+        out = np.empty((n, n), np.complex128)
+        self._chk(self.lib.ref_apply_map_full_csr(C.c_int64(n), _p(_c(d)), rp.ctypes.data_as(_i64p),
+                                                  ci.ctypes.data_as(_i64p), _p(va), _p(_c(z)), _p(out)))
+        return out
+
     def apply_map_full(self, d, delta, z):
         n = len(d)
         out = np.empty((n, n), np.complex128)

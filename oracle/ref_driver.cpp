@@ -125,6 +125,41 @@ REF_API int ref_solve_full(int64_t n, const double* d, const double* delta, doub
   });
 }
 
+// solve_full on a CSR Delta: the reference's sparse product path (kernels.cpp:88-108).
+// vals interleaved complex (re, im) per nonzero.
+REF_API int ref_solve_full_csr(int64_t n, const double* d, const int64_t* rowptr, const int64_t* cols,
+                               const double* vals, double tol, int max_iter, double div_thr,
+                               double* z_out, double* lam_out, double* stats) {
+  return guarded([&] {
+    Partition p = make_partition(n, d, 1, nullptr, rowptr, cols, vals);
+    const InverseGaps g = build_gaps(p, 0.0);
+    const IterationConfig cfg = make_cfg(tol, max_iter, div_thr, 0);
+    const double t0 = now_s();
+    const SpectrumResult r = solve_full(p, g, cfg, nullptr);
+    const double t1 = now_s();
+    from_cvec(cvec(r.Z.data(), r.Z.data() + n * n), z_out);
+    from_cvec(r.eigenvalues, lam_out);
+    stats[0] = r.iterations;
+    stats[1] = static_cast<double>(static_cast<int>(r.status));
+    stats[2] = r.final_step;
+    stats[3] = r.residual_frobenius;
+    stats[4] = r.min_singular_value_estimate;
+    stats[5] = static_cast<double>(r.matmul_count);
+    stats[6] = t1 - t0;
+    stats[7] = 0.0;
+  });
+}
+
+REF_API int ref_apply_map_full_csr(int64_t n, const double* d, const int64_t* rowptr, const int64_t* cols,
+                                   const double* vals, const double* z, double* out) {
+  return guarded([&] {
+    Partition p = make_partition(n, d, 1, nullptr, rowptr, cols, vals);
+    const InverseGaps g = build_gaps(p, 0.0);
+    const ComplexMatrix f = apply_map_full(p, g, dense_from(z, n, n));
+    from_cvec(cvec(f.data(), f.data() + n * n), out);
+  });
+}
+
 // Max-abs stop rule (BASELINE.json configs): Z_{k+1} = apply_map_full(Z_k) until
 // max|Z_{k+1}-Z_k| < tol, divergence tested first on |Z_{k+1}|_F exactly as solve_full
 // does; then the reference's closing product for Lambda and |MZ-ZL|_F.

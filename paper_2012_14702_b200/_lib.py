@@ -86,6 +86,11 @@ SIGNATURES = {
     "ipt_full_local_columns": (C.c_int, [_vp, _i64p, _i64p]),
     "ipt_full_free": (None, [_vp]),
     "ipt_apply_map_full": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]),
+    "ipt_full_solve_csr": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, _i32p, _dp, _dp, _dp, _dp,
+                                     C.POINTER(Params), _dp, _dp, _dp, _dp, C.POINTER(Stats)]),
+    "ipt_full_upload_csr": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, _i32p, _dp, _dp, C.POINTER(_vp)]),
+    "ipt_apply_map_full_csr": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, _i32p, _dp, _dp, _dp, _dp,
+                                         _dp, _dp]),
     "ipt_sigma_min": (C.c_int, [_vp, C.c_int64, _dp, _dp, C.c_int32, C.c_double, _dp]),
     "ipt_single_solve_dense": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, _dp, C.c_int64, _dp, _dp,
                                          C.POINTER(Params), _dp, _dp, C.POINTER(Stats)]),

@@ -6,7 +6,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
+#include <vector>
 
 #include "dmma_gemm.cuh"
 #include "ipt_internal.cuh"
@@ -77,6 +79,87 @@ void upload_as_colmajor(Ctx& c, const double* host_rm, int64_t rows, int64_t col
   // row-major rows x cols == column-major cols x rows; transpose to column-major rows x cols
   transpose_to_rowmajor(c.stream, tmp.get(), cols, cols, rows, dst, ld);
   c.sync();
+}
+bool any_nonzero(const double* p, int64_t count) {
+  if (p == nullptr) return false;
+  for (int64_t t = 0; t < count; ++t)
+    if (p[t] != 0.0) return true;
+  return false;
+}
+
+// A CSR Delta for the full-spectrum entry points: real -> the sparse device map
+// (Z row-major, fused SpMM); complex (or a complex Z forced) -> densified onto the
+// dense complex path.
+FullProblem* open_full_csr(Ctx& c, int64_t n, const double* d_re, const double* d_im,
+                           const int64_t* rowptr, const int32_t* cols, const double* val_re,
+                           const double* val_im, bool force_complex) {
+  if (n <= 0) throw InvalidArgument("solve_full: empty problem");
+  if (!d_re || !rowptr) throw InvalidArgument("solve_full: null input");
+  const int64_t b = rowptr[0], nnz = rowptr[n] - rowptr[0];
+  if (nnz < 0) throw InvalidArgument("csr: row offsets must be non-decreasing");
+  const bool cplx = force_complex || any_nonzero(d_im, n) || any_nonzero(val_im ? val_im + b : nullptr, nnz);
+  if (!cplx) return full_upload_csr(c, n, d_re, rowptr, cols, val_re);
+  if (nnz > 0 && (!cols || !val_re)) throw InvalidArgument("solve_full: null input");
+  std::vector<double> re(size_t(n) * n, 0.0), im(size_t(n) * n, 0.0);
+  for (int64_t i = 0; i < n; ++i) {
+    if (rowptr[i + 1] < rowptr[i]) throw InvalidArgument("csr: row offsets must be non-decreasing");
+    for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) {
+      if (cols[p] < 0 || cols[p] >= n) throw InvalidArgument("csr: column index out of bounds");
+      re[size_t(i) * n + cols[p]] = val_re[p];
+      if (val_im) im[size_t(i) * n + cols[p]] = val_im[p];
+    }
+  }
+  return full_upload(c, n, d_re, d_im, re.data(), im.data(), /*force_complex=*/true);
+}
+
+// One F application to a host Z (apply_map_full, solver.cpp:156-178).
+void apply_one_map(FullProblem& P, const double* z_re, const double* z_im, double* f_re, double* f_im) {
+  full_reset(P, z_re, z_im, 1, /*renormalize=*/false);
+  ipt_params prm;
+  ipt_default_params(&prm);
+  prm.max_iterations = 1;
+  prm.ignore_convergence = 1;
+  prm.divergence_threshold = DBL_MAX;
+  full_iterate(P, prm, nullptr);
+  full_download(P, f_re, f_im, nullptr, nullptr);
+}
+
+template <typename Open>
+void solve_full_impl(Ctx& c, const ipt_params* params, Open&& open, const double* warm_re,
+                     const double* warm_im, double* z_re, double* z_im, double* lam_re, double* lam_im,
+                     ipt_stats* stats) {
+  const ipt_params prm = params_or_default(params);
+  if (!(prm.tolerance > 0.0)) throw InvalidArgument("config: tolerance must be positive");
+  if (prm.max_iterations <= 0) throw InvalidArgument("config: max_iterations must be positive");
+  if (!(prm.divergence_threshold > 1.0)) throw InvalidArgument("config: divergence_threshold must exceed 1");
+  HostPhases ph("ipt_full_solve");
+  IPT_CUDA(cudaEventRecord(c.ev[2], c.stream));
+  {
+    std::unique_ptr<FullProblem, void (*)(FullProblem*)> P(open(), full_free);
+    ph.mark("upload");
+    full_reset(*P, warm_re, warm_im, prm.max_iterations);
+    IPT_CUDA(cudaEventRecord(c.ev[3], c.stream));
+    c.sync();
+    ph.mark("reset");
+    float ms_up = 0.f;
+    IPT_CUDA(cudaEventElapsedTime(&ms_up, c.ev[2], c.ev[3]));
+    full_iterate(*P, prm, stats);
+    ph.mark("iterate");
+    full_finalize(*P, prm, stats);
+    ph.mark("finalize+sigma");
+    IPT_CUDA(cudaEventRecord(c.ev[2], c.stream));
+    full_download(*P, z_re, z_im, lam_re, lam_im);
+    IPT_CUDA(cudaEventRecord(c.ev[3], c.stream));
+    c.sync();
+    ph.mark("download");
+    float ms_down = 0.f;
+    IPT_CUDA(cudaEventElapsedTime(&ms_down, c.ev[2], c.ev[3]));
+    if (stats) {
+      stats->ms_upload = ms_up;
+      stats->ms_download = ms_down;
+    }
+  }
+  ph.mark("release");
 }
 }  // namespace
 
@@ -232,40 +315,51 @@ int ipt_full_solve(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_
   return guarded([&] {
     check_ctx(ctx);
     DeviceGuard g(ctx->c.device);
-    const ipt_params prm = params_or_default(params);
-    if (!(prm.tolerance > 0.0)) throw InvalidArgument("config: tolerance must be positive");
-    if (prm.max_iterations <= 0) throw InvalidArgument("config: max_iterations must be positive");
-    if (!(prm.divergence_threshold > 1.0)) throw InvalidArgument("config: divergence_threshold must exceed 1");
-    Ctx& c = ctx->c;
-    HostPhases ph("ipt_full_solve");
-    IPT_CUDA(cudaEventRecord(c.ev[2], c.stream));
-    {
-      std::unique_ptr<FullProblem, void (*)(FullProblem*)> P(full_upload(c, n, d_re, d_im, delta_re, delta_im),
-                                                             full_free);
-      ph.mark("upload");
-      full_reset(*P, warm_re, warm_im, prm.max_iterations);
-      IPT_CUDA(cudaEventRecord(c.ev[3], c.stream));
-      c.sync();
-      ph.mark("reset");
-      float ms_up = 0.f;
-      IPT_CUDA(cudaEventElapsedTime(&ms_up, c.ev[2], c.ev[3]));
-      full_iterate(*P, prm, stats);
-      ph.mark("iterate");
-      full_finalize(*P, prm, stats);
-      ph.mark("finalize+sigma");
-      IPT_CUDA(cudaEventRecord(c.ev[2], c.stream));
-      full_download(*P, z_re, z_im, lam_re, lam_im);
-      IPT_CUDA(cudaEventRecord(c.ev[3], c.stream));
-      c.sync();
-      ph.mark("download");
-      float ms_down = 0.f;
-      IPT_CUDA(cudaEventElapsedTime(&ms_down, c.ev[2], c.ev[3]));
-      if (stats) {
-        stats->ms_upload = ms_up;
-        stats->ms_download = ms_down;
-      }
-    }
-    ph.mark("release");
+    solve_full_impl(
+        ctx->c, params, [&] { return full_upload(ctx->c, n, d_re, d_im, delta_re, delta_im); }, warm_re,
+        warm_im, z_re, z_im, lam_re, lam_im, stats);
+  });
+}
+
+int ipt_full_solve_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                       const int64_t* rowptr, const int32_t* cols, const double* val_re,
+                       const double* val_im, const double* warm_re, const double* warm_im,
+                       const ipt_params* params, double* z_re, double* z_im, double* lam_re,
+                       double* lam_im, ipt_stats* stats) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    solve_full_impl(
+        ctx->c, params,
+        [&] { return open_full_csr(ctx->c, n, d_re, d_im, rowptr, cols, val_re, val_im, false); }, warm_re,
+        warm_im, z_re, z_im, lam_re, lam_im, stats);
+  });
+}
+
+int ipt_full_upload_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                        const int64_t* rowptr, const int32_t* cols, const double* val_re,
+                        const double* val_im, ipt_full_problem** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    *out = reinterpret_cast<ipt_full_problem*>(
+        open_full_csr(ctx->c, n, d_re, d_im, rowptr, cols, val_re, val_im, false));
+  });
+}
+
+int ipt_apply_map_full_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                           const int64_t* rowptr, const int32_t* cols, const double* val_re,
+                           const double* val_im, const double* z_re, const double* z_im,
+                           double* f_re, double* f_im) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (ctx->c.nranks != 1) throw InvalidArgument("apply_map_full: single-device context required");
+    if (!z_re) throw InvalidArgument("apply_map_full: null Z");
+    const bool zc = any_nonzero(z_im, n > 0 ? n * n : 0);
+    std::unique_ptr<FullProblem, void (*)(FullProblem*)> P(
+        open_full_csr(ctx->c, n, d_re, d_im, rowptr, cols, val_re, val_im, zc), full_free);
+    apply_one_map(*P, z_re, z_im, f_re, f_im);
   });
 }
 
@@ -285,14 +379,7 @@ int ipt_apply_map_full(ipt_ctx* ctx, int64_t n, const double* d_re, const double
       // a complex Z on a real Delta: re-upload on the complex path
       P.reset(full_upload(ctx->c, n, d_re, d_im, delta_re, delta_im, /*force_complex=*/true));
     }
-    full_reset(*P, z_re, z_im, 1, /*renormalize=*/false);
-    ipt_params prm;
-    ipt_default_params(&prm);
-    prm.max_iterations = 1;
-    prm.ignore_convergence = 1;
-    prm.divergence_threshold = DBL_MAX;
-    full_iterate(*P, prm, nullptr);
-    full_download(*P, f_re, f_im, nullptr, nullptr);
+    apply_one_map(*P, z_re, z_im, f_re, f_im);
   });
 }
 

@@ -12,9 +12,13 @@
 // epilogue writing F(Z) into the other Z buffer and per-CTA partial sums, a fixed-order
 // reduction, [NCCL all-reduce of 3 sums + 1 max], and a single-thread decide kernel
 // that applies the reference's divergence-then-convergence tests (solver.cpp:236-249).
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <utility>
+#include <vector>
 
 #include "dmma_gemm.cuh"
 #include "ipt_internal.cuh"
@@ -41,6 +45,15 @@ struct FullProblem {
   int enq = 0;              // maps enqueued since reset
   DevBuf gathered;          // rank 0 with nranks > 1: full Z (n columns, ldz)
   bool finalized = false;
+  // Sparse real Delta (CSR, f2): during the loop Z[2] hold the local columns ROW-major
+  // (n rows x cols_pad, ldr = cols_pad), the layout a CSR x dense product gathers
+  // contiguously; finalize/download convert the last iterate to column-major once.
+  bool sparse = false;
+  std::unique_ptr<int64_t, void (*)(void*)> rowptr{nullptr, [](void* p) { cudaFree(p); }};
+  std::unique_ptr<int32_t, void (*)(void*)> cidx{nullptr, [](void* p) { cudaFree(p); }};
+  DevBuf vals;
+  int64_t nnz = 0, ldr = 0;
+  const double* zcm = nullptr;  // sparse: column-major copy of the final iterate
   ~FullProblem() {
     if (state) cudaFree(state);
   }
@@ -236,9 +249,210 @@ __global__ void renormalize_columns_kernel(double* Z, int64_t ldz, int64_t ld, i
   }
 }
 
+// ---- sparse Delta (f2): CSR x row-major Z with the map epilogue fused ----
+// matmul_sparse_parallel (proj/src/kernels.cpp:88-108) accumulates W_ij over the CSR
+// entries of row i in storage order; every kernel below keeps that order with one
+// rounding per term (fma), so W_jj of the diagonal pre-pass and W_ij of the product
+// are the same numbers.
+
+struct SpmmArgs {
+  const int64_t* rowptr;
+  const int32_t* cols;
+  const double* vals;
+  const double* Z;  // row-major, ldr
+  int64_t ldr;
+  double* F;        // row-major, ldr (map mode)
+  const double* d;
+  const double* wd;   // map: (Delta Z)_jj per local column
+  const double* lam;  // resid: lambda_j per local column
+  int64_t n, ncols, col0;
+  double* partials;
+  const LoopState* state;
+};
+
+// K2 (sparse): wd_j = sum_p vals[p] Z[cols[p], j] over row col0+j, one thread per column.
+__global__ void sparse_diag_kernel(SpmmArgs a, double* __restrict__ wd, double* __restrict__ lam) {
+  if (a.state != nullptr && a.state->done) return;
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (j >= a.ncols) return;
+  const int64_t jg = a.col0 + j;
+  double s = 0.0;
+  for (int64_t p = a.rowptr[jg]; p < a.rowptr[jg + 1]; ++p)
+    s = __fma_rn(__ldg(a.vals + p), a.Z[int64_t(__ldg(a.cols + p)) * a.ldr + j], s);
+  wd[j] = s;
+  if (lam != nullptr) lam[j] = a.d[jg] + s;
+}
+
+// K1 (sparse): one warp per (row i, chunk of 32*VEC columns); lane l owns columns
+// chunk*32*VEC + l*VEC .. +VEC. The row's CSR entries are loaded 32 at a time and
+// broadcast by shuffle; each entry gathers VEC contiguous doubles of Z row k
+// (a full 32-byte sector per lane at VEC = 4). Work items run chunk-major, so the
+// warps in flight share one column chunk of Z (n x 1 KB) in L2. The persistent grid
+// is fixed (spmm_grid()), so the per-CTA partials and their reduction are deterministic.
+template <int MODE, int VEC>  // MODE 0: map (F and the 4 partial sums), 1: residual sum
+__global__ void __launch_bounds__(256) spmm_full_kernel(SpmmArgs a) {
+  if (a.state != nullptr && a.state->done) return;
+  __shared__ double red[8][4];
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  const int lane = threadIdx.x & 31;
+  constexpr int CW = 32 * VEC;
+  const int64_t nch = (a.ncols + CW - 1) / CW;
+  const int64_t items = nch * a.n;
+  const int64_t step = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t it = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); it < items; it += step) {
+    const int64_t ch = it / a.n, i = it - ch * a.n;
+    const int64_t j0 = ch * CW + lane * VEC;
+    const double* zc = a.Z + j0;
+    double acc[VEC];
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) acc[t] = 0.0;
+    const int64_t rb = a.rowptr[i], re = a.rowptr[i + 1];
+    for (int64_t base = rb; base < re; base += 32) {
+      const int cnt = static_cast<int>(re - base < 32 ? re - base : 32);
+      int kc = 0;
+      double kv = 0.0;
+      if (lane < cnt) {
+        kc = __ldg(a.cols + base + lane);
+        kv = __ldg(a.vals + base + lane);
+      }
+      int q = 0;
+      for (; q + 4 <= cnt; q += 4) {
+        double2 z[4][VEC / 2];
+        double vv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t k = __shfl_sync(0xffffffffu, kc, q + u);
+          vv[u] = __shfl_sync(0xffffffffu, kv, q + u);
+          const double2* src = reinterpret_cast<const double2*>(zc + k * a.ldr);
+#pragma unroll
+          for (int h = 0; h < VEC / 2; ++h) z[u][h] = __ldg(src + h);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int h = 0; h < VEC / 2; ++h) {
+            acc[2 * h] = __fma_rn(vv[u], z[u][h].x, acc[2 * h]);
+            acc[2 * h + 1] = __fma_rn(vv[u], z[u][h].y, acc[2 * h + 1]);
+          }
+      }
+      for (; q < cnt; ++q) {
+        const int64_t k = __shfl_sync(0xffffffffu, kc, q);
+        const double vq = __shfl_sync(0xffffffffu, kv, q);
+        const double2* src = reinterpret_cast<const double2*>(zc + k * a.ldr);
+#pragma unroll
+        for (int h = 0; h < VEC / 2; ++h) {
+          const double2 z = __ldg(src + h);
+          acc[2 * h] = __fma_rn(vq, z.x, acc[2 * h]);
+          acc[2 * h + 1] = __fma_rn(vq, z.y, acc[2 * h + 1]);
+        }
+      }
+    }
+    // epilogue: the dense K1 formulas (dmma_gemm.cuh), row-major addressing
+    const double di = a.d[i];
+    const double* zrow = zc + i * a.ldr;
+    double zi[VEC];
+#pragma unroll
+    for (int h = 0; h < VEC / 2; ++h) {
+      const double2 z = *reinterpret_cast<const double2*>(zrow + 2 * h);
+      zi[2 * h] = z.x;
+      zi[2 * h + 1] = z.y;
+    }
+#pragma unroll
+    for (int t = 0; t < VEC; ++t) {
+      const int64_t j = j0 + t;
+      if (j >= a.ncols) continue;
+      const double z = zi[t], w = acc[t];
+      if (MODE == 0) {
+        const int64_t jg = a.col0 + j;
+        const double f = (i == jg) ? 1.0 : __ddiv_rn(__dsub_rn(__dmul_rn(z, a.wd[j]), w), __dsub_rn(di, a.d[jg]));
+        a.F[i * a.ldr + j] = f;
+        const double df = __dsub_rn(f, z);
+        v[0] = __fma_rn(df, df, v[0]);
+        v[1] = __fma_rn(z, z, v[1]);
+        v[2] = __fma_rn(f, f, v[2]);
+        v[3] = nan_max(v[3], fabs(df));
+      } else {
+        const double r = __dsub_rn(__dadd_rn(__dmul_rn(di, z), w), __dmul_rn(z, a.lam[j]));
+        v[0] = __fma_rn(r, r, v[0]);
+      }
+    }
+  }
+  block_reduce4<8>(v, red);
+  if (threadIdx.x == 0) {
+    double* o = a.partials + size_t(blockIdx.x) * 4;
+    o[0] = v[0]; o[1] = v[1]; o[2] = v[2]; o[3] = v[3];
+  }
+}
+
 // --------------------------------------------------------------- host side
 
 namespace {
+
+int spmm_vec() {
+  static const int v = [] {
+    const char* e = std::getenv("IPT_SPMM_VEC");
+    return (e && std::atoi(e) == 2) ? 2 : 4;
+  }();
+  return v;
+}
+
+SpmmArgs spmm_args(FullProblem& P, const double* Zs, double* Fd, const LoopState* st) {
+  SpmmArgs a{};
+  a.rowptr = P.rowptr.get();
+  a.cols = P.cidx.get();
+  a.vals = P.vals.get();
+  a.Z = Zs;
+  a.ldr = P.ldr;
+  a.F = Fd;
+  a.d = P.dre.get();
+  a.wd = P.wd.get();
+  a.lam = P.lam.get();
+  a.n = P.n;
+  a.ncols = P.ncols;
+  a.col0 = P.col0;
+  a.partials = P.partials.get();
+  a.state = st;
+  return a;
+}
+
+void launch_sparse_diag(FullProblem& P, const double* Zs, double* lam, const LoopState* st) {
+  const unsigned grid = static_cast<unsigned>(ceil_div(P.ncols, 256));
+  if (grid == 0) return;
+  sparse_diag_kernel<<<grid, 256, 0, P.ctx->stream>>>(spmm_args(P, Zs, nullptr, st), P.wd.get(), lam);
+  IPT_LAUNCH_CHECK();
+  count_launch();
+}
+
+// Persistent grid: every resident CTA of the map kernel, once (a fixed number on a
+// given device, so the partial-sum order is fixed); both modes use it.
+int spmm_grid() {
+  static const int g = [] {
+    int dev = 0, sms = 0, per_sm = 0;
+    IPT_CUDA(cudaGetDevice(&dev));
+    IPT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (spmm_vec() == 2)
+      IPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_full_kernel<0, 2>, 256, 0));
+    else
+      IPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_full_kernel<0, 4>, 256, 0));
+    return std::max(1, std::min(kEpiBlocks, sms * std::max(per_sm, 1)));
+  }();
+  return g;
+}
+
+void launch_spmm(FullProblem& P, int mode, const double* Zs, double* Fd, const LoopState* st) {
+  const SpmmArgs a = spmm_args(P, Zs, Fd, st);
+  cudaStream_t s = P.ctx->stream;
+  const unsigned grid = static_cast<unsigned>(spmm_grid());
+  if (spmm_vec() == 2) {
+    if (mode == 0) spmm_full_kernel<0, 2><<<grid, 256, 0, s>>>(a);
+    else spmm_full_kernel<1, 2><<<grid, 256, 0, s>>>(a);
+  } else {
+    if (mode == 0) spmm_full_kernel<0, 4><<<grid, 256, 0, s>>>(a);
+    else spmm_full_kernel<1, 4><<<grid, 256, 0, s>>>(a);
+  }
+  IPT_LAUNCH_CHECK();
+  count_launch();
+}
 
 void launch_diag(FullProblem& P, const double* A, const double* Zsrc, double* out, double* lam,
                  const double* dvec, const LoopState* st) {
@@ -275,6 +489,7 @@ GemmParams gemm_params(FullProblem& P, const double* A, const double* Bz, double
 }
 
 int64_t num_partials(const FullProblem& P) {
+  if (P.sparse) return spmm_grid();
   return P.cplx ? kEpiBlocks : static_cast<int64_t>(gemm_tiles(P.n, P.ncols));
 }
 
@@ -293,7 +508,12 @@ void enqueue_map(FullProblem& P, int k, const ipt_params& prm, cudaEvent_t ev_a 
   const double* zs = P.Z[k & 1].get();
   double* zd = P.Z[(k + 1) & 1].get();
   LoopState* st = P.state;
-  if (!P.cplx) {
+  if (P.sparse) {
+    launch_sparse_diag(P, zs, nullptr, st);
+    if (ev_a) IPT_CUDA(cudaEventRecord(ev_a, c.stream));
+    launch_spmm(P, 0, zs, zd, st);
+    if (ev_b) IPT_CUDA(cudaEventRecord(ev_b, c.stream));
+  } else if (!P.cplx) {
     launch_diag(P, P.A1.get(), zs, P.wd.get(), nullptr, nullptr, st);
     GemmParams g = gemm_params(P, P.A1.get(), zs, zd, P.ldz);
     if (ev_a) IPT_CUDA(cudaEventRecord(ev_a, c.stream));
@@ -395,6 +615,64 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
   return P.release();
 }
 
+// Real CSR Delta (rowptr[n+1] with any base, cols in [0, n)): the sparse map path.
+FullProblem* full_upload_csr(Ctx& c, int64_t n, const double* d, const int64_t* rowptr,
+                             const int32_t* cols, const double* vals) {
+  if (n <= 0) throw InvalidArgument("solve_full: empty problem");
+  if (!d || !rowptr) throw InvalidArgument("solve_full: null input");
+  const int64_t b = rowptr[0], nnz = rowptr[n] - rowptr[0];
+  for (int64_t i = 0; i < n; ++i)
+    if (rowptr[i + 1] < rowptr[i]) throw InvalidArgument("csr: row offsets must be non-decreasing");
+  if (nnz > 0 && (!cols || !vals)) throw InvalidArgument("solve_full: null input");
+  for (int64_t p = 0; p < nnz; ++p)
+    if (cols[b + p] < 0 || cols[b + p] >= n) throw InvalidArgument("csr: column index out of bounds");
+  auto P = std::make_unique<FullProblem>();
+  P->ctx = &c;
+  P->n = n;
+  P->ld = round_up(n, 16);
+  P->rows_pad = round_up(n, kBM);
+  c.shard(n, P->col0, P->ncols);
+  P->ncols -= P->col0;
+  P->cols_pad = round_up(std::max<int64_t>(P->ncols, 1), kBN);
+  P->cplx = false;
+  P->sparse = true;
+  P->lda = P->ld;
+  P->ldz = P->ld;
+  P->ldr = P->cols_pad;
+  P->nnz = nnz;
+  cudaStream_t s = c.stream;
+  std::vector<int64_t> rp(n + 1);
+  for (int64_t i = 0; i <= n; ++i) rp[i] = rowptr[i] - b;
+  int64_t* drp = nullptr;
+  IPT_CUDA(cudaMalloc(&drp, sizeof(int64_t) * (n + 1)));
+  P->rowptr.reset(drp);
+  IPT_CUDA(cudaMemcpyAsync(drp, rp.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+  int32_t* dc = nullptr;
+  IPT_CUDA(cudaMalloc(&dc, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+  P->cidx.reset(dc);
+  P->vals.alloc(std::max<int64_t>(nnz, 1), false);
+  if (nnz) {
+    IPT_CUDA(cudaMemcpyAsync(dc, cols + b, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
+    IPT_CUDA(cudaMemcpyAsync(P->vals.get(), vals + b, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+  }
+  P->dre.alloc(n);
+  P->dim.alloc(n);
+  IPT_CUDA(cudaMemcpyAsync(P->dre.get(), d, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  // n rows x cols_pad (row-major) fits in cols_pad x ldz (ldz >= n)
+  for (auto& z : P->Z) z.alloc(size_t(P->cols_pad) * P->ldz);
+  P->wd.alloc(P->cols_pad);
+  P->wdi.alloc(P->cols_pad);
+  P->lam.alloc(P->cols_pad);
+  P->lami.alloc(P->cols_pad);
+  P->partials.alloc(size_t(kEpiBlocks) * 4);
+  P->sums.alloc(4);
+  IPT_CUDA(cudaMalloc(&P->state, sizeof(LoopState)));
+  c.sync();
+  return P.release();
+}
+
+bool full_is_sparse(const FullProblem& P) { return P.sparse; }
+
 void full_free(FullProblem* P) { delete P; }
 
 void full_reset(FullProblem& P, const double* warm_re, const double* warm_im, int max_iter_hint,
@@ -434,6 +712,14 @@ void full_reset(FullProblem& P, const double* warm_re, const double* warm_im, in
       count_launch();
     }
     c.sync();
+  }
+  if (P.sparse) {
+    // column-major start -> the row-major loop layout (Z[1] becomes Z[0])
+    fill_zero(s, P.Z[1].get(), P.Z[1].count);
+    transpose_to_rowmajor(s, P.Z[0].get(), P.ldz, n, P.ncols, P.Z[1].get(), P.ldr);
+    std::swap(P.Z[0].p, P.Z[1].p);
+    fill_zero(s, P.Z[1].get(), P.Z[1].count);
+    P.zcm = nullptr;
   }
   LoopState init{};
   init.status = kMaxIterations;
@@ -498,6 +784,22 @@ static const double* current_z(FullProblem& P) {
   return P.Z[P.ctx->h_state->iterations & 1].get();
 }
 
+// Sparse path: the column-major form of the current (row-major) iterate, built once
+// in the other ping-pong buffer. Dense path: the current iterate itself.
+static const double* final_colmajor_z(FullProblem& P) {
+  if (!P.sparse) return current_z(P);
+  if (P.zcm == nullptr) {
+    const int cur = P.ctx->h_state->iterations & 1;
+    double* dst = P.Z[cur ^ 1].get();
+    cudaStream_t s = P.ctx->stream;
+    fill_zero(s, dst, P.Z[cur ^ 1].count);
+    // row-major n x ncols (ldr) == column-major ncols x n -> column-major n x ncols (ldz)
+    transpose_to_rowmajor(s, P.Z[cur].get(), P.ldr, P.ncols, P.n, dst, P.ldz);
+    P.zcm = dst;
+  }
+  return P.zcm;
+}
+
 // Closing product: Lambda and |MZ - Z Lambda|_F (solver.cpp:252-270), then the
 // eigenvector gather to rank 0 and sigma_min (solver.cpp:271) on rank 0.
 void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
@@ -507,7 +809,10 @@ void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
   c.sync();
   const double* z = current_z(P);
   IPT_CUDA(cudaEventRecord(c.ev[0], s));
-  if (!P.cplx) {
+  if (P.sparse) {
+    launch_sparse_diag(P, z, P.lam.get(), nullptr);
+    launch_spmm(P, 1, z, nullptr, nullptr);
+  } else if (!P.cplx) {
     launch_diag(P, P.A1.get(), z, P.wd.get(), P.lam.get(), P.dre.get(), nullptr);
     GemmParams g = gemm_params(P, P.A1.get(), z, nullptr, 0);
     g.state = nullptr;
@@ -542,6 +847,7 @@ void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
   c.sync();
   float ms_final = 0.f;
   IPT_CUDA(cudaEventElapsedTime(&ms_final, c.ev[0], c.ev[1]));
+  z = final_colmajor_z(P);
 
   // Gather the column shards on rank 0 (one final eigenvector gather).
   if (c.nranks > 1) {
@@ -632,7 +938,7 @@ void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, d
     if (P.cplx) std::memcpy(lam_im, li.data(), sizeof(double) * n);
     else std::memset(lam_im, 0, sizeof(double) * n);
   }
-  const double* zsrc = c.nranks > 1 ? P.gathered.get() : current_z(P);
+  const double* zsrc = c.nranks > 1 ? P.gathered.get() : final_colmajor_z(P);
   if (zsrc == nullptr) throw InvalidArgument("download: finalize must run before download");
   DevBuf rm;
   rm.alloc(size_t(n) * n, false);
@@ -675,7 +981,7 @@ void full_run_maps(FullProblem& P, int count, double* ms_total, double* ms_gemm)
   IPT_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
   *ms_total = ms;
   double g = 0.0;
-  for (int i = 0; i < count && !P.cplx; ++i) {
+  for (int i = 0; i < count && (!P.cplx || P.sparse); ++i) {
     IPT_CUDA(cudaEventElapsedTime(&ms, ev[2 + 2 * i], ev[3 + 2 * i]));
     g += ms;
   }

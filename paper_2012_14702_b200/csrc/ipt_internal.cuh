@@ -100,6 +100,9 @@ void release_staging(Ctx& c);
 struct FullProblem;
 FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_im,
                          const double* delta_re, const double* delta_im, bool force_complex = false);
+FullProblem* full_upload_csr(Ctx& c, int64_t n, const double* d, const int64_t* rowptr,
+                             const int32_t* cols, const double* vals);
+bool full_is_sparse(const FullProblem& P);
 void full_free(FullProblem* P);
 void full_reset(FullProblem& P, const double* warm_re, const double* warm_im, int max_iter_hint,
                 bool renormalize = true);

@@ -368,16 +368,22 @@ def apply_map_full(p: Partition, g: InverseGaps, Z, ctx: Optional[Context] = Non
     Z = np.asarray(Z)
     if Z.shape != (n, n):
         raise ValueError("apply_map_full: size mismatch")
-    delta = p.delta.to_dense() if isinstance(p.delta, CsrMatrix) else p.delta
     ctx = ctx or default_context()
     dr, di = _planar(p.d)
-    ar, ai = _planar(delta)
     zr, zi = _planar(Z)
     cx = _out_complex(p, Z)
     fr = np.empty((n, n))
     fi = np.empty((n, n)) if cx else None
-    check(_lib.load().ipt_apply_map_full(ctx.handle, n, dptr(dr), dptr(di), dptr(ar), dptr(ai),
-                                         dptr(zr), dptr(zi), dptr(fr), dptr(fi)))
+    lib = _lib.load()
+    if isinstance(p.delta, CsrMatrix):  # kernels.cpp:88-108 (SpMM) on the device
+        vr, vi = _planar(p.delta.values)
+        check(lib.ipt_apply_map_full_csr(ctx.handle, n, dptr(dr), dptr(di), i64ptr(p.delta.row_offsets),
+                                         i32ptr(p.delta.col_indices), dptr(vr), dptr(vi), dptr(zr), dptr(zi),
+                                         dptr(fr), dptr(fi)))
+    else:
+        ar, ai = _planar(p.delta)
+        check(lib.ipt_apply_map_full(ctx.handle, n, dptr(dr), dptr(di), dptr(ar), dptr(ai),
+                                     dptr(zr), dptr(zi), dptr(fr), dptr(fi)))
     return _combine(fr, fi, cx)
 
 
@@ -389,10 +395,8 @@ def solve_full(p: Partition, g: InverseGaps, config: IterationConfig = None, war
     _validate(config)
     _check_sizes(p, g, 0)
     n = p.size()
-    delta = p.delta.to_dense() if isinstance(p.delta, CsrMatrix) else p.delta
     ctx = ctx or default_context()
     dr, di = _planar(p.d)
-    ar, ai = _planar(delta)
     wr = wi = None
     if warm_start is not None:
         warm_start = np.asarray(warm_start)
@@ -411,9 +415,17 @@ def solve_full(p: Partition, g: InverseGaps, config: IterationConfig = None, war
     tm = np.zeros(config.max_iterations) if config.record_trace else None
     st.trace = dptr(tr)
     st.trace_max_abs = dptr(tm)
-    check(_lib.load().ipt_full_solve(ctx.handle, n, dptr(dr), dptr(di), dptr(ar), dptr(ai), dptr(wr),
-                                     dptr(wi), C.byref(prm), dptr(zr), dptr(zi), dptr(lr), dptr(li),
-                                     C.byref(st)))
+    lib = _lib.load()
+    if isinstance(p.delta, CsrMatrix):  # sparse Delta: fused SpMM map (real) on the device
+        vr, vi = _planar(p.delta.values)
+        check(lib.ipt_full_solve_csr(ctx.handle, n, dptr(dr), dptr(di), i64ptr(p.delta.row_offsets),
+                                     i32ptr(p.delta.col_indices), dptr(vr), dptr(vi), dptr(wr), dptr(wi),
+                                     C.byref(prm), dptr(zr), dptr(zi), dptr(lr), dptr(li), C.byref(st)))
+    else:
+        ar, ai = _planar(p.delta)
+        check(lib.ipt_full_solve(ctx.handle, n, dptr(dr), dptr(di), dptr(ar), dptr(ai), dptr(wr),
+                                 dptr(wi), C.byref(prm), dptr(zr), dptr(zi), dptr(lr), dptr(li),
+                                 C.byref(st)))
     res = SpectrumResult()
     if root:
         res.Z = _combine(zr, zi, cx)

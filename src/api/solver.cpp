@@ -89,7 +89,7 @@ cvec combine(const Vec& re, const Vec& im) {
     return out;
 }
 
-// Delta as a dense planar operator (a CSR partition is densified for the full map).
+// Delta as a dense planar operator (apply_map_single and the dense full path).
 Planar dense_delta(const Partition& p) {
     if (p.delta.is_dense()) return api::split(p.delta.data(), p.size() * p.size());
     const ComplexMatrix dd = p.delta.to_dense();
@@ -183,10 +183,19 @@ ComplexMatrix apply_map_full(const Partition& p, const InverseGaps& g, const Com
     if (Z.rows() != p.size() || Z.cols() != p.size()) throw std::invalid_argument("apply_map_full: size mismatch");
     const std::size_t n = p.size();
     const ComplexMatrix zd = Z.to_dense();
-    const Planar d = api::split(p.d.data(), n), a = dense_delta(p), zz = api::split(zd.data(), n * n);
+    const Planar d = api::split(p.d.data(), n), zz = api::split(zd.data(), n * n);
     Vec fr(n * n), fi(n * n);
-    api::check(ipt_apply_map_full(api::context(), static_cast<int64_t>(n), d.re.data(), d.im_or_null(), a.re.data(),
-                                  a.im_or_null(), zz.re.data(), zz.im_or_null(), fr.data(), fi.data()));
+    if (p.delta.is_sparse()) {  // CSR Delta: the device SpMM map (kernels.cpp:88-108)
+        const api::Csr c = api::to_csr(p.delta);
+        api::check(ipt_apply_map_full_csr(api::context(), static_cast<int64_t>(n), d.re.data(), d.im_or_null(),
+                                          c.rowptr.data(), c.cols.data(), c.val.re.data(), c.val.im_or_null(),
+                                          zz.re.data(), zz.im_or_null(), fr.data(), fi.data()));
+    } else {
+        const Planar a = dense_delta(p);
+        api::check(ipt_apply_map_full(api::context(), static_cast<int64_t>(n), d.re.data(), d.im_or_null(),
+                                      a.re.data(), a.im_or_null(), zz.re.data(), zz.im_or_null(), fr.data(),
+                                      fi.data()));
+    }
     ComplexMatrix out = ComplexMatrix::dense(n, n);
     api::merge(fr, fi, out.data());
     return out;
@@ -244,7 +253,7 @@ SpectrumResult solve_full(const Partition& p, const InverseGaps& g, const Iterat
     validate(config);
     check_anchor(p, g, 0);
     const std::size_t n = p.size();
-    const Planar d = api::split(p.d.data(), n), a = dense_delta(p);
+    const Planar d = api::split(p.d.data(), n);
     Planar w;
     ComplexMatrix wd;
     if (warm_start) {
@@ -259,9 +268,18 @@ SpectrumResult solve_full(const Partition& p, const InverseGaps& g, const Iterat
     std::vector<double> trace(config.record_trace ? config.max_iterations : 0);
     st.trace = config.record_trace ? trace.data() : nullptr;
     Vec zr(n * n), zi(n * n), lr(n), li(n);
-    api::check(ipt_full_solve(api::context(), static_cast<int64_t>(n), d.re.data(), d.im_or_null(), a.re.data(),
-                              a.im_or_null(), warm_start ? w.re.data() : nullptr, warm_start ? w.im_or_null() : nullptr,
-                              &prm, zr.data(), zi.data(), lr.data(), li.data(), &st));
+    const double* wre = warm_start ? w.re.data() : nullptr;
+    const double* wim = warm_start ? w.im_or_null() : nullptr;
+    if (p.delta.is_sparse()) {  // CSR Delta: fused SpMM map on the device (real), else densified
+        const api::Csr c = api::to_csr(p.delta);
+        api::check(ipt_full_solve_csr(api::context(), static_cast<int64_t>(n), d.re.data(), d.im_or_null(),
+                                      c.rowptr.data(), c.cols.data(), c.val.re.data(), c.val.im_or_null(), wre, wim,
+                                      &prm, zr.data(), zi.data(), lr.data(), li.data(), &st));
+    } else {
+        const Planar a = dense_delta(p);
+        api::check(ipt_full_solve(api::context(), static_cast<int64_t>(n), d.re.data(), d.im_or_null(), a.re.data(),
+                                  a.im_or_null(), wre, wim, &prm, zr.data(), zi.data(), lr.data(), li.data(), &st));
+    }
     SpectrumResult r;
     r.Z = ComplexMatrix::dense(n, n);
     api::merge(zr, zi, r.Z.data());

@@ -221,6 +221,41 @@ def full_columns(big):
     save("full_columns.npz", **out)
 
 
+def sparse_full():
+    """solve_full / apply_map_full on CSR partitions: the reference's sparse product
+    path (kernels.cpp:88-108) on gen_fci_like instances (testgen.cpp:174-194), and the
+    config 5 CI-like construction at N=4096 (diverges: meta only)."""
+    R = oracle.ref()
+    out = {}
+    for name, (n, dens, gap, seed) in {"f256": (256, 16 / 256, 20.0, 11),
+                                       "f1024": (1024, 24 / 1024, 20.0, 12)}.items():
+        d, delta = R.gen_fci_like(n, dens, gap, seed)
+        out[name + "_d"] = d
+        out[name + "_rowptr"] = delta.row_offsets
+        out[name + "_cols"] = delta.col_indices
+        out[name + "_vals"] = delta.values
+        r = R.solve_full_csr(d, delta)
+        if n <= 256:
+            out[name + "_Z"] = r["Z"].real
+            z0 = np.random.default_rng(seed).standard_normal((n, n))
+            np.fill_diagonal(z0, 1.0)
+            out[name + "_map_in"] = z0
+            out[name + "_map_out"] = R.apply_map_full_csr(d, delta, z0).real
+        else:
+            cols = np.array([0, 1, n // 2, n - 1])
+            out[name + "_zcols_idx"] = cols
+            out[name + "_zcols"] = r["Z"].real[:, cols]
+        out[name + "_lam"] = r["eigenvalues"].real
+        out[name + "_meta"] = np.array([r["iterations"], r["status"], r["final_step"], r["residual_frobenius"],
+                                        r["sigma_min"], r["matmul_count"]])
+        print(f"sparse full {name}: nnz={delta.nnz} {r['iterations']} it status {r['status']}", flush=True)
+    p = synth.csr_ci(4096)
+    r = R.solve_full_csr(p.d, p.delta, tol=1e-10)
+    out["ci4096_meta"] = np.array([r["iterations"], r["status"], p.delta.nnz])
+    print(f"sparse full ci4096: {r['iterations']} it status {r['status']}", flush=True)
+    save("sparse_full.npz", **out)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
@@ -228,7 +263,7 @@ if __name__ == "__main__":
     a = ap.parse_args()
     oracle.build()
     jobs = dict(small=small_cases, config1=config1, accel=accelerated, single=lambda: single_configs(a.big),
-                columns=lambda: full_columns(a.big))
+                columns=lambda: full_columns(a.big), sparse=sparse_full)
     for name, fn in jobs.items():
         if a.only and name not in a.only.split(","):
             continue
