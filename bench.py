@@ -290,6 +290,37 @@ def bench_single(ipt, lib, ctx, which, steps, warmup, hbm):
     }
 
 
+def bench_sparse_full(lib, ctx, n, per_row, steps, dense_step_ms):
+    """Sparse-Delta full map: CSR Delta with per_row entries per row at the
+    headline N, fused SpMM map (spmm_full_kernel<0,4>), Z row-major in HBM. Bound: the
+    L2->SM gather of nnz * N * 8 bytes per map (the Z chunk in flight stays in L2)."""
+    from paper_2012_14702_b200._lib import check, dptr, i32ptr, i64ptr
+
+    rng = np.random.default_rng(7)
+    cols = np.sort(rng.integers(0, n, (n, per_row)), axis=1).astype(np.int32)
+    vals = 0.01 * rng.standard_normal((n, per_row))
+    vals[cols == np.arange(n)[:, None]] = 0.0
+    rowptr = np.arange(0, n * per_row + 1, per_row, dtype=np.int64)
+    d = np.arange(n, dtype=float)
+    h = C.c_void_p()
+    check(lib.ipt_full_upload_csr(ctx.handle, n, dptr(d), None, i64ptr(rowptr), i32ptr(cols.ravel()),
+                                  dptr(vals.ravel()), None, C.byref(h)))
+    check(lib.ipt_full_reset(ctx.handle, h, None, None))
+    tot, ker = C.c_double(), C.c_double()
+    check(lib.ipt_full_run_maps(ctx.handle, h, 3, C.byref(tot), C.byref(ker)))
+    check(lib.ipt_full_run_maps(ctx.handle, h, steps, C.byref(tot), C.byref(ker)))
+    lib.ipt_full_free(h)
+    nnz = n * per_row
+    ms = tot.value / steps
+    ms_k = ker.value / steps
+    gather = nnz * n * 8.0
+    return {"workload": f"sparse Delta full map N={n}, {per_row} nnz/row (random columns), Z row-major",
+            "ms_per_map": ms, "kernel_ms": ms_k, "kernel": "spmm_full_kernel<0,4>",
+            "gather_bytes_per_launch": gather, "gather_TBps": gather / (ms_k * 1e-3) / 1e12,
+            "roofline_note": "L2 (LTS) bound: ~6300 B/clk full chip (B300_MICROARCH.md) ~ 12 TB/s",
+            "speedup_vs_dense_map": dense_step_ms / ms if dense_step_ms else None}
+
+
 # --------------------------------------------------------------------------- main arm
 
 
@@ -419,6 +450,10 @@ def main():
                 del p2, r2
             except Exception as exc:
                 secondary["full_n8192"] = {"error": repr(exc)}
+            try:
+                secondary["sparse_full"] = bench_sparse_full(lib, ctx, n, 64, max(args.steps, 5), step_ms)
+            except Exception as exc:
+                secondary["sparse_full"] = {"error": repr(exc)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
