@@ -197,6 +197,7 @@ int ipt_ctx_create(int device, ipt_ctx** out) {
     ctx->c.device = device;
     IPT_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
     IPT_CUDA(cudaMallocHost(&ctx->c.h_state, sizeof(LoopState)));
+    IPT_CUDA(cudaMallocHost(&ctx->c.h_aux, 256));
     for (auto& e : ctx->c.ev) IPT_CUDA(cudaEventCreate(&e));
     *out = ctx;
   });
@@ -208,6 +209,7 @@ void ipt_ctx_destroy(ipt_ctx* ctx) {
   if (ctx->c.comm) ncclCommDestroy(ctx->c.comm);
   for (auto& e : ctx->c.ev) cudaEventDestroy(e);
   if (ctx->c.h_state) cudaFreeHost(ctx->c.h_state);
+  if (ctx->c.h_aux) cudaFreeHost(ctx->c.h_aux);
   release_staging(ctx->c);
   if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
   delete ctx;

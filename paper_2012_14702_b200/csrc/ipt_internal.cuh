@@ -44,6 +44,7 @@ struct Ctx {
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
   LoopState* h_state = nullptr;  // pinned mirror of the device loop state
+  double* h_aux = nullptr;       // pinned scratch (256 B) for other device -> host scalars
   cudaEvent_t ev[4] = {};
   // pinned double-buffered staging for pageable host <-> device transfers
   double* stage[2] = {nullptr, nullptr};

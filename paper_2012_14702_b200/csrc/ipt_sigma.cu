@@ -5,7 +5,12 @@
 // fixed start vector deterministic_unit(n) (solver.cpp:95-109), stopping when
 // |u_k| changes by <= tol relative; the estimate is 1/sqrt(|u|).
 //
-// Here: H = Z^T Z through the DMMA GEMM, a blocked right-looking Cholesky
+// Here, first: the same iteration with each solve H u = v done matrix-free by
+// conjugate gradients on Z^T Z (two GEMV passes over Z in HBM per CG step; the
+// converged IPT basis Z = I + small makes H so well conditioned that CG reaches
+// |r| <= 1e-15 |v| in a handful of steps). If any solve misses that within 64
+// steps, the factorisation path runs instead:
+// H = Z^T Z through the DMMA GEMM, a blocked right-looking Cholesky
 // (H is symmetric positive definite for a full-rank Z; the reference's
 // "singular" outcome is reproduced by the same pivot threshold
 // max|H| * eps * n), and the same inverse power iteration with two blocked
@@ -17,6 +22,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <memory>
 #include <vector>
 
 #include "dmma_gemm.cuh"
@@ -233,6 +240,185 @@ __global__ void embed_complex_kernel(const double* __restrict__ zr, const double
   }
 }
 
+// ---------------------------------------------------------------------------
+// Matrix-free inverse iteration: u = (Z^T Z)^{-1} v by conjugate gradients with
+// Z resident in HBM (two GEMV passes over Z per CG step, no SYRK, no factor).
+// Used when CG reaches |r| <= 1e-15 |b| within kCgMaxIters steps, which it does in
+// a handful of steps for the well-conditioned bases IPT converges to (Z = I + small);
+// otherwise the Cholesky path below runs. Every reduction is fixed-order.
+
+constexpr int kCgMaxIters = 64;
+constexpr int kCgBatch = 8;
+constexpr int kZpRows = 512;       // rows per CTA of the Z p pass (2 per thread)
+constexpr int kZpCols = 1024;      // columns per CTA of the Z p pass
+constexpr int kVecBlocks = 296;    // fixed grid of the vector kernels
+constexpr double kCgRelTol = 1e-15;
+
+struct CgState {
+  double rr, bb, alpha, beta;
+  int done, iters;
+};
+
+// ypart[c][i] = sum_{j in chunk c} Z[i, j] p_j (column-major Z, 2 rows per thread).
+__global__ void __launch_bounds__(256) cg_zp_kernel(const double* __restrict__ Z, int64_t ld, int64_t m,
+                                                    const double* __restrict__ p, double* __restrict__ ypart,
+                                                    const CgState* st) {
+  if (st->done) return;
+  const int64_t i = int64_t(blockIdx.x) * kZpRows + 2 * threadIdx.x;
+  const int64_t j0 = int64_t(blockIdx.y) * kZpCols;
+  const int64_t j1 = j0 + kZpCols < m ? j0 + kZpCols : m;
+  if (i >= m) return;
+  double a0 = 0.0, a1 = 0.0;
+  const double* zc = Z + i;
+  int64_t j = j0;
+  for (; j + 4 <= j1; j += 4) {
+    const double2 z0 = *reinterpret_cast<const double2*>(zc + j * ld);
+    const double2 z1 = *reinterpret_cast<const double2*>(zc + (j + 1) * ld);
+    const double2 z2 = *reinterpret_cast<const double2*>(zc + (j + 2) * ld);
+    const double2 z3 = *reinterpret_cast<const double2*>(zc + (j + 3) * ld);
+    const double p0 = __ldg(p + j), p1 = __ldg(p + j + 1), p2 = __ldg(p + j + 2), p3 = __ldg(p + j + 3);
+    a0 = __fma_rn(z0.x, p0, a0); a1 = __fma_rn(z0.y, p0, a1);
+    a0 = __fma_rn(z1.x, p1, a0); a1 = __fma_rn(z1.y, p1, a1);
+    a0 = __fma_rn(z2.x, p2, a0); a1 = __fma_rn(z2.y, p2, a1);
+    a0 = __fma_rn(z3.x, p3, a0); a1 = __fma_rn(z3.y, p3, a1);
+  }
+  for (; j < j1; ++j) {
+    const double2 z0 = *reinterpret_cast<const double2*>(zc + j * ld);
+    const double pj = __ldg(p + j);
+    a0 = __fma_rn(z0.x, pj, a0);
+    a1 = __fma_rn(z0.y, pj, a1);
+  }
+  double* out = ypart + int64_t(blockIdx.y) * (m + 2) + i;
+  out[0] = a0;
+  if (i + 1 < m) out[1] = a1;
+}
+
+__global__ void cg_yreduce_kernel(const double* __restrict__ ypart, int64_t m, int nchunks, double* __restrict__ y,
+                                  const CgState* st) {
+  if (st->done) return;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < nchunks; ++c) s += ypart[int64_t(c) * (m + 2) + i];
+    y[i] = s;
+  }
+}
+
+// q_j = Z[:, j] . y (warp per column, y zero beyond m) and per-CTA partials of p . q.
+__global__ void __launch_bounds__(256) cg_ztq_kernel(const double* __restrict__ Z, int64_t ld, int64_t m,
+                                                     const double* __restrict__ y, const double* __restrict__ p,
+                                                     double* __restrict__ q, double* __restrict__ partials,
+                                                     const CgState* st) {
+  if (st->done) return;
+  __shared__ double red[8][4];
+  const int lane = threadIdx.x & 31;
+  const int64_t j = blockIdx.x * int64_t(8) + (threadIdx.x >> 5);
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  if (j < m) {
+    const double2* zc = reinterpret_cast<const double2*>(Z + j * ld);
+    const double2* yy = reinterpret_cast<const double2*>(y);
+    const int64_t K2 = (m + 1) / 2;
+    double sx = 0.0, sy = 0.0;
+    int64_t k = lane;
+    for (; k + 96 < K2; k += 128) {
+      const double2 a0 = zc[k], a1 = zc[k + 32], a2 = zc[k + 64], a3 = zc[k + 96];
+      const double2 b0 = yy[k], b1 = yy[k + 32], b2 = yy[k + 64], b3 = yy[k + 96];
+      sx = __fma_rn(a0.x, b0.x, sx); sy = __fma_rn(a0.y, b0.y, sy);
+      sx = __fma_rn(a1.x, b1.x, sx); sy = __fma_rn(a1.y, b1.y, sy);
+      sx = __fma_rn(a2.x, b2.x, sx); sy = __fma_rn(a2.y, b2.y, sy);
+      sx = __fma_rn(a3.x, b3.x, sx); sy = __fma_rn(a3.y, b3.y, sy);
+    }
+    for (; k < K2; k += 32) {
+      const double2 a0 = zc[k], b0 = yy[k];
+      sx = __fma_rn(a0.x, b0.x, sx); sy = __fma_rn(a0.y, b0.y, sy);
+    }
+    double s = sx + sy;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) q[j] = s;
+    v[0] = lane == 0 ? p[j] * s : 0.0;
+  }
+  block_reduce4<8>(v, red);
+  if (threadIdx.x == 0) partials[blockIdx.x * 4] = v[0];
+}
+
+// one thread block: fixed-order sum of `count` strided partials
+__device__ double cg_sum_partials(const double* __restrict__ partials, int64_t count) {
+  __shared__ double red[16][4];
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) v[0] += partials[4 * i];
+  block_reduce4<16>(v, red);
+  return v[0];  // valid in thread 0
+}
+
+__global__ void cg_alpha_kernel(const double* __restrict__ partials, int64_t count, CgState* st) {
+  if (st->done) return;
+  const double pq = cg_sum_partials(partials, count);
+  if (threadIdx.x == 0) st->alpha = st->rr / pq;
+}
+
+// x += alpha p, r -= alpha q, partials of r . r
+__global__ void cg_update_kernel(int64_t m, const double* __restrict__ p, const double* __restrict__ q,
+                                 double* __restrict__ x, double* __restrict__ r, double* __restrict__ partials,
+                                 const CgState* st) {
+  if (st->done) return;
+  __shared__ double red[8][4];
+  const double a = st->alpha;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
+    x[i] = __fma_rn(a, p[i], x[i]);
+    const double ri = __fma_rn(-a, q[i], r[i]);
+    r[i] = ri;
+    v[0] = __fma_rn(ri, ri, v[0]);
+  }
+  block_reduce4<8>(v, red);
+  if (threadIdx.x == 0) partials[blockIdx.x * 4] = v[0];
+}
+
+__global__ void cg_beta_kernel(const double* __restrict__ partials, int64_t count, CgState* st) {
+  if (st->done) return;
+  const double rr = cg_sum_partials(partials, count);
+  if (threadIdx.x == 0) {
+    st->beta = rr / st->rr;
+    st->rr = rr;
+    st->iters += 1;
+    if (!(rr > kCgRelTol * kCgRelTol * st->bb)) st->done = 1;  // also stops on NaN
+  }
+}
+
+__global__ void cg_p_kernel(int64_t m, const double* __restrict__ r, double* __restrict__ p, const CgState* st) {
+  if (st->done) return;
+  const double b = st->beta;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = __fma_rn(b, p[i], r[i]);
+}
+
+// x = 0, r = p = b, partials of b . b
+__global__ void cg_init_kernel(int64_t m, const double* __restrict__ b, double* __restrict__ x,
+                               double* __restrict__ r, double* __restrict__ p, double* __restrict__ partials) {
+  __shared__ double red[8][4];
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
+    const double bi = b[i];
+    x[i] = 0.0;
+    r[i] = bi;
+    p[i] = bi;
+    v[0] = __fma_rn(bi, bi, v[0]);
+  }
+  block_reduce4<8>(v, red);
+  if (threadIdx.x == 0) partials[blockIdx.x * 4] = v[0];
+}
+
+__global__ void cg_start_kernel(const double* __restrict__ partials, int64_t count, CgState* st) {
+  const double bb = cg_sum_partials(partials, count);
+  if (threadIdx.x == 0) {
+    st->rr = bb;
+    st->bb = bb;
+    st->alpha = st->beta = 0.0;
+    st->iters = 0;
+    st->done = (bb > 0.0) ? 0 : 1;
+  }
+}
+
 // Host replica of deterministic_unit (solver.cpp:95-109).
 std::vector<double> deterministic_unit(int64_t n) {
   std::vector<double> v(n);
@@ -252,6 +438,93 @@ std::vector<double> deterministic_unit(int64_t n) {
   return v;
 }
 
+// The reference's inverse power iteration (solver.cpp:283-296) with the solves done
+// by CG on Z^T Z. Returns false (caller factors instead) if any inner solve misses
+// the tolerance within kCgMaxIters steps.
+bool sigma_min_cg(Ctx& c, int64_t m, int64_t n_start, const double* Z, int64_t ld, int max_iters, double tol,
+                  double* estimate, int* outer_steps, int* cg_steps) {
+  cudaStream_t s = c.stream;
+  const bool prof = std::getenv("IPT_PROFILE") != nullptr;
+  auto wall = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  double t_mark = wall();
+  const int nchunks = static_cast<int>(ceil_div(m, kZpCols));
+  const int64_t vlen = m + 2;
+  DevBuf x, r, p, q, y, ypart, v, un, parts;
+  x.alloc(vlen);
+  r.alloc(vlen);
+  p.alloc(vlen);
+  q.alloc(vlen);
+  y.alloc(vlen);
+  v.alloc(vlen);
+  un.alloc(1);
+  ypart.alloc(size_t(nchunks) * vlen, false);
+  const int64_t ztq_blocks = ceil_div(m, 8);
+  parts.alloc(size_t(std::max<int64_t>(ztq_blocks, kVecBlocks)) * 4);
+  CgState* st = nullptr;
+  IPT_CUDA(cudaMalloc(&st, sizeof(CgState)));
+  std::unique_ptr<CgState, void (*)(CgState*)> st_guard(st, [](CgState* p) { cudaFree(p); });
+  CgState* h_st = reinterpret_cast<CgState*>(c.h_aux);  // pinned scratch
+  static_assert(sizeof(CgState) <= 256, "pinned scratch too small");
+
+  std::vector<double> v0 = deterministic_unit(n_start);
+  IPT_CUDA(cudaMemcpyAsync(v.get(), v0.data(), sizeof(double) * n_start, cudaMemcpyHostToDevice, s));
+  if (prof) {
+    c.sync();
+    std::fprintf(stderr, "[ipt]   cg setup %.1f ms\n", 1e3 * (wall() - t_mark));
+    t_mark = wall();
+  }
+  const dim3 zp_grid(static_cast<unsigned>(ceil_div(m, kZpRows)), static_cast<unsigned>(nchunks));
+  double rho = 0.0;
+  int steps = 0, total_cg = 0;
+  for (int it = 0; it < max_iters; ++it) {
+    steps = it + 1;
+    cg_init_kernel<<<kVecBlocks, 256, 0, s>>>(m, v.get(), x.get(), r.get(), p.get(), parts.get());
+    cg_start_kernel<<<1, 512, 0, s>>>(parts.get(), kVecBlocks, st);
+    count_launch(2);
+    int done = 0;
+    for (int k = 0; k < kCgMaxIters && !done; k += kCgBatch) {
+      for (int b = 0; b < kCgBatch; ++b) {
+        cg_zp_kernel<<<zp_grid, 256, 0, s>>>(Z, ld, m, p.get(), ypart.get(), st);
+        cg_yreduce_kernel<<<kVecBlocks, 256, 0, s>>>(ypart.get(), m, nchunks, y.get(), st);
+        cg_ztq_kernel<<<static_cast<unsigned>(ztq_blocks), 256, 0, s>>>(Z, ld, m, y.get(), p.get(), q.get(),
+                                                                        parts.get(), st);
+        cg_alpha_kernel<<<1, 512, 0, s>>>(parts.get(), ztq_blocks, st);
+        cg_update_kernel<<<kVecBlocks, 256, 0, s>>>(m, p.get(), q.get(), x.get(), r.get(), parts.get(), st);
+        cg_beta_kernel<<<1, 512, 0, s>>>(parts.get(), kVecBlocks, st);
+        cg_p_kernel<<<kVecBlocks, 256, 0, s>>>(m, r.get(), p.get(), st);
+        count_launch(7);
+      }
+      IPT_LAUNCH_CHECK();
+      IPT_CUDA(cudaMemcpyAsync(h_st, st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
+      c.sync();
+      done = h_st->done;
+      if (prof) {
+        std::fprintf(stderr, "[ipt]   cg batch %.1f ms (done %d, iters %d)\n", 1e3 * (wall() - t_mark), done, h_st->iters);
+        t_mark = wall();
+      }
+    }
+    total_cg += h_st->iters;
+    if (!done || !(h_st->rr <= kCgRelTol * kCgRelTol * h_st->bb)) return false;
+    norm2_kernel<<<1, 1024, 0, s>>>(x.get(), m, un.get());
+    normalize_kernel<<<kVecBlocks, 256, 0, s>>>(x.get(), v.get(), m, un.get());
+    count_launch(2);
+    IPT_LAUNCH_CHECK();
+    double h_un = 0.0;
+    IPT_CUDA(cudaMemcpyAsync(&h_un, un.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+    c.sync();
+    if (!std::isfinite(h_un) || h_un == 0.0) return false;
+    if (it > 0 && std::fabs(h_un - rho) <= tol * h_un) {
+      rho = h_un;
+      break;
+    }
+    rho = h_un;
+  }
+  *estimate = 1.0 / std::sqrt(rho);
+  *outer_steps = steps;
+  *cg_steps = total_cg;
+  return true;
+}
+
 }  // namespace
 
 double sigma_min_device(Ctx& c, int64_t n, const double* zr, const double* zi, int64_t ldz,
@@ -269,6 +542,22 @@ double sigma_min_device(Ctx& c, int64_t n, const double* zr, const double* zi, i
     IPT_LAUNCH_CHECK();
     count_launch();
     Z = E.get();
+  }
+  const bool prof = std::getenv("IPT_PROFILE") != nullptr;
+  auto wall = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  {
+    // IPT_SIGMA=factor skips the matrix-free attempt (tests compare the two paths)
+    const char* mode = std::getenv("IPT_SIGMA");
+    if (!(mode && std::strcmp(mode, "factor") == 0)) {
+      const double t0 = wall();
+      double est = 0.0;
+      int outer = 0, inner = 0;
+      const bool ok = sigma_min_cg(c, m, n, Z, ld, max_iters, tol, &est, &outer, &inner);
+      if (prof)
+        std::fprintf(stderr, "[ipt] sigma_min n=%lld: matrix-free CG %s, %.1f ms (%d outer steps, %d CG steps)\n",
+                     static_cast<long long>(m), ok ? "converged" : "fell back", 1e3 * (wall() - t0), outer, inner);
+      if (ok) return est;
+    }
   }
   const int64_t ldh = round_up(m, 16);
   DevBuf H;
@@ -300,8 +589,6 @@ double sigma_min_device(Ctx& c, int64_t n, const double* zr, const double* zi, i
   IPT_CUDA(cudaMemcpyAsync(hmax4, scratch.get() + 1184 * 4, sizeof(hmax4), cudaMemcpyDeviceToHost, s));
   c.sync();
   const double tiny = hmax4[3] * 2.220446049250313e-16 * static_cast<double>(m);
-  const bool prof = std::getenv("IPT_PROFILE") != nullptr;
-  auto wall = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   const double t_syrk = wall();
 
   int* d_sing = nullptr;
