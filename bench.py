@@ -414,7 +414,11 @@ def main():
                "h2d_bytes_per_step": int(8 * n * n + 8 * n),
                "d2h_bytes_per_step": int(8 * n * n + 8 * n) if rank == 0 else 0,
                "step": "one drop-in solve_full call (C ABI ipt_full_solve, host buffers, pageable memory)",
-               "seconds": e2e_s}
+               "seconds": e2e_s,
+               "flop_convention": "2N^3 per IPT iteration (the metric's definition) x iterations / wall time; "
+                                  "iteration 1 from Z = I is evaluated exactly without a product (W = Delta I = "
+                                  "Delta bit for bit), so iterations-1 map GEMMs + 1 closing GEMM executed",
+               "gemms_executed": int(r.iterations)}
         solve_info = {"iterations": r.iterations, "status": ipt.to_string(r.status),
                       "residual_frobenius": r.residual_frobenius,
                       "residual_rel": r.residual_frobenius / math.sqrt(float(np.sum(p.delta ** 2)) + float(np.sum(p.d ** 2))),

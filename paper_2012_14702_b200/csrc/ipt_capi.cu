@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <memory>
 #include <string>
 #include <vector>
@@ -145,10 +146,35 @@ void solve_full_impl(Ctx& c, const ipt_params* params, Open&& open, const double
     IPT_CUDA(cudaEventElapsedTime(&ms_up, c.ev[2], c.ev[3]));
     full_iterate(*P, prm, stats);
     ph.mark("iterate");
-    full_finalize(*P, prm, stats);
+    // Single GPU: Z goes to the host on a second stream / host thread while the closing
+    // product and sigma_min run (they only read Z).
+    std::future<void> early;
+    const bool overlap = (z_re || z_im) && full_can_download_early(*P);
+    const auto t_dl = std::chrono::steady_clock::now();
+    if (overlap) {
+      full_prepare_download(*P, z_re != nullptr, z_im != nullptr);
+      const int dev = c.device;
+      FullProblem* raw = P.get();
+      early = std::async(std::launch::async, [raw, dev, z_re, z_im] {
+        IPT_CUDA(cudaSetDevice(dev));
+        full_download_z(*raw, z_re, z_im);
+      });
+    }
+    try {
+      full_finalize(*P, prm, stats);
+    } catch (...) {
+      if (early.valid()) early.wait();
+      throw;
+    }
     ph.mark("finalize+sigma");
+    float ms_overlapped = 0.f;
+    if (overlap) {
+      early.get();
+      full_release_download(*P);
+      ms_overlapped = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_dl).count();
+    }
     IPT_CUDA(cudaEventRecord(c.ev[2], c.stream));
-    full_download(*P, z_re, z_im, lam_re, lam_im);
+    full_download(*P, overlap ? nullptr : z_re, overlap ? nullptr : z_im, lam_re, lam_im);
     IPT_CUDA(cudaEventRecord(c.ev[3], c.stream));
     c.sync();
     ph.mark("download");
@@ -156,7 +182,8 @@ void solve_full_impl(Ctx& c, const ipt_params* params, Open&& open, const double
     IPT_CUDA(cudaEventElapsedTime(&ms_down, c.ev[2], c.ev[3]));
     if (stats) {
       stats->ms_upload = ms_up;
-      stats->ms_download = ms_down;
+      // overlapped: host wall time from the end of the loop until Z was on the host
+      stats->ms_download = overlap ? ms_down + ms_overlapped : ms_down;
     }
   }
   ph.mark("release");
@@ -196,6 +223,7 @@ int ipt_ctx_create(int device, ipt_ctx** out) {
     auto* ctx = new ipt_ctx();
     ctx->c.device = device;
     IPT_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+    IPT_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream2, cudaStreamNonBlocking));
     IPT_CUDA(cudaMallocHost(&ctx->c.h_state, sizeof(LoopState)));
     IPT_CUDA(cudaMallocHost(&ctx->c.h_aux, 256));
     for (auto& e : ctx->c.ev) IPT_CUDA(cudaEventCreate(&e));
@@ -212,6 +240,7 @@ void ipt_ctx_destroy(ipt_ctx* ctx) {
   if (ctx->c.h_aux) cudaFreeHost(ctx->c.h_aux);
   release_staging(ctx->c);
   if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
+  if (ctx->c.stream2) cudaStreamDestroy(ctx->c.stream2);
   delete ctx;
 }
 

@@ -54,6 +54,10 @@ struct FullProblem {
   DevBuf vals;
   int64_t nnz = 0, ldr = 0;
   const double* zcm = nullptr;  // sparse: column-major copy of the final iterate
+  bool delta_finite = false;    // real dense Delta has no Inf/NaN (identity-start shortcut allowed)
+  bool start_identity = false;  // Z[0] is the identity (no warm start)
+  const double* z_after_loop = nullptr;  // current iterate when full_iterate returned
+  DevBuf rm[2];                          // row-major copies of Z for an overlapped download
   ~FullProblem() {
     if (state) cudaFree(state);
   }
@@ -384,6 +388,53 @@ __global__ void __launch_bounds__(256) spmm_full_kernel(SpmmArgs a) {
   }
 }
 
+// F(I) without the product (dense real Delta, identity start): W = Delta I is Delta
+// itself, bit for bit (every other term of the GEMM sum is an exact zero), so the
+// first map is evaluated by loading W_ij = Delta[i, col0 + j] into the accumulator
+// fragments of the same CTA tile / warp / lane layout as K1 and running K1's own
+// epilogue: F, the identity reset and the per-CTA partial sums are identical to
+// the GEMM path's. Only used when Delta is all-finite (an Inf would make the GEMM's
+// zero terms NaN).
+__global__ void __launch_bounds__(kGemmThreads) map_identity_kernel(const GemmParams p) {
+  if (p.state != nullptr && p.state->done) return;
+  int tm, tn;
+  tile_coords(blockIdx.x, p.tiles_m, p.tiles_n, tm, tn);
+  const int64_t m0 = int64_t(tm) * kBM, n0 = int64_t(tn) * kBN;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;
+  double acc[4][4][4];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int64_t i = m0 + wm * 64 + mi * 16 + g + ((r >> 1) << 3);
+        const int64_t j = n0 + wn * 32 + ni * 8 + 2 * t + (r & 1);
+        acc[mi][ni][r] = (i < p.n_rows && j < p.n_cols) ? __ldg(p.A + i * p.lda + p.col0 + j) : 0.0;
+      }
+  __shared__ double red[kConsumerWarps][4];
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  gemm_epilogue<kGemmMap>(p, acc, m0, n0, warp, lane, v);
+  block_reduce4<kConsumerWarps>(v, red);
+  if (threadIdx.x == 0) {
+    double* out = p.partials + size_t(blockIdx.x) * 4;
+    out[0] = v[0];
+    out[1] = v[1];
+    out[2] = v[2];
+    out[3] = v[3];
+  }
+}
+
+__global__ void count_nonfinite_kernel(const double* __restrict__ A, int64_t count, int* out) {
+  int bad = 0;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < count; e += int64_t(gridDim.x) * blockDim.x)
+    bad |= !isfinite(A[e]);
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0 && bad) atomicOr(out, 1);
+}
+
 // --------------------------------------------------------------- host side
 
 namespace {
@@ -394,6 +445,12 @@ int spmm_vec() {
     return (e && std::atoi(e) == 2) ? 2 : 4;
   }();
   return v;
+}
+
+// IPT_IDENTITY_SHORTCUT=0 runs the first map from I through the GEMM as well.
+bool identity_shortcut_enabled() {
+  const char* e = std::getenv("IPT_IDENTITY_SHORTCUT");
+  return !(e && std::strcmp(e, "0") == 0);
 }
 
 SpmmArgs spmm_args(FullProblem& P, const double* Zs, double* Fd, const LoopState* st) {
@@ -517,7 +574,14 @@ void enqueue_map(FullProblem& P, int k, const ipt_params& prm, cudaEvent_t ev_a 
     launch_diag(P, P.A1.get(), zs, P.wd.get(), nullptr, nullptr, st);
     GemmParams g = gemm_params(P, P.A1.get(), zs, zd, P.ldz);
     if (ev_a) IPT_CUDA(cudaEventRecord(ev_a, c.stream));
-    launch_gemm(kGemmMap, g, c.stream);
+    if (k == 0 && P.start_identity && P.delta_finite && identity_shortcut_enabled()) {
+      const unsigned tiles = static_cast<unsigned>(gemm_tiles(P.n, P.ncols));
+      map_identity_kernel<<<tiles, kGemmThreads, 0, c.stream>>>(g);
+      IPT_LAUNCH_CHECK();
+      count_launch();
+    } else {
+      launch_gemm(kGemmMap, g, c.stream);
+    }
     if (ev_b) IPT_CUDA(cudaEventRecord(ev_b, c.stream));
   } else {
     launch_diag(P, P.A1.get(), zs, P.wd.get(), nullptr, nullptr, st);
@@ -611,6 +675,19 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
   P->partials.alloc(size_t(std::max<int64_t>(num_partials(*P), 1)) * 4);
   P->sums.alloc(4);
   IPT_CUDA(cudaMalloc(&P->state, sizeof(LoopState)));
+  if (!P->cplx) {
+    int* flag = nullptr;
+    IPT_CUDA(cudaMalloc(&flag, sizeof(int)));
+    IPT_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
+    count_nonfinite_kernel<<<1184, 256, 0, s>>>(P->A1.get(), int64_t(P->rows_pad) * P->lda, flag);
+    IPT_LAUNCH_CHECK();
+    count_launch();
+    int h = 1;
+    IPT_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    c.sync();
+    cudaFree(flag);
+    P->delta_finite = (h == 0);
+  }
   c.sync();
   return P.release();
 }
@@ -681,6 +758,8 @@ void full_reset(FullProblem& P, const double* warm_re, const double* warm_im, in
   cudaStream_t s = c.stream;
   const int64_t n = P.n;
   fill_zero(s, P.Z[0].get(), P.Z[0].count);
+  P.start_identity = (warm_re == nullptr);
+  P.z_after_loop = nullptr;
   if (warm_re == nullptr) {
     const unsigned grid = static_cast<unsigned>(ceil_div(P.ncols, 256));
     if (grid) {
@@ -759,6 +838,7 @@ void full_iterate(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
   IPT_CUDA(cudaEventRecord(c.ev[1], c.stream));
   IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, c.stream));
   c.sync();
+  P.z_after_loop = P.Z[c.h_state->iterations & 1].get();
   if (stats) {
     float ms = 0.f;
     IPT_CUDA(cudaEventElapsedTime(&ms, c.ev[0], c.ev[1]));
@@ -955,6 +1035,46 @@ void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, d
 }
 
 bool full_is_complex(const FullProblem& P) { return P.cplx; }
+
+bool full_can_download_early(const FullProblem& P) { return P.ctx->nranks == 1 && !P.sparse; }
+
+// Main thread, before full_finalize: transpose the final Z into row-major staging
+// buffers on ctx.stream (a few ms; a kernel on a second stream would starve behind
+// the closing-product GEMM, which holds every SM). full_download_z then only needs
+// the copy engines, so it overlaps the closing product and sigma_min.
+void full_prepare_download(FullProblem& P, bool want_re, bool want_im) {
+  Ctx& c = *P.ctx;
+  const int64_t n = P.n;
+  const double* zsrc = P.z_after_loop;
+  if (zsrc == nullptr) throw InvalidArgument("download: iterate must run first");
+  for (int part = 0; part < 2; ++part) {
+    if (!(part == 0 ? want_re : want_im) || (part == 1 && !P.cplx)) continue;
+    P.rm[part].alloc(size_t(n) * n, false);
+    transpose_to_rowmajor(c.stream, zsrc + (part ? P.ld : 0), P.ldz, n, n, P.rm[part].get(), n);
+  }
+  c.sync();
+}
+
+void full_download_z(FullProblem& P, double* z_re, double* z_im) {
+  Ctx& c = *P.ctx;
+  const int64_t n = P.n;
+  for (int part = 0; part < 2; ++part) {
+    double* dst = part == 0 ? z_re : z_im;
+    if (dst == nullptr) continue;
+    if (part == 1 && !P.cplx) {
+      std::memset(dst, 0, sizeof(double) * n * n);
+      continue;
+    }
+    if (P.rm[part].get() == nullptr) throw InvalidArgument("download: prepare must run first");
+    d2h_rows(c, dst, n, P.rm[part].get(), n, n, n, c.stream2);
+  }
+  IPT_CUDA(cudaStreamSynchronize(c.stream2));
+}
+
+void full_release_download(FullProblem& P) {
+  P.rm[0].release();
+  P.rm[1].release();
+}
 
 // Bench / profiling: exactly `count` further map applications (convergence ignored),
 // timed with CUDA events on the library stream: the whole sequence and the K1 GEMM

@@ -41,6 +41,7 @@ struct DevBuf {
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;  // transfers overlapped with compute on `stream`
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
   LoopState* h_state = nullptr;  // pinned mirror of the device loop state
@@ -91,10 +92,11 @@ void scale_copy(cudaStream_t s, const double* src, double* dst, size_t count, do
 // Pageable host <-> device copies of row blocks through the context's pinned double
 // buffer (multithreaded host memcpy overlapped with the DMA); synchronous on return.
 // Host rows have pitch spitch (doubles), device rows pitch dpitch.
+// `s` (default: the context stream) carries the DMA.
 void h2d_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t rows,
-              int64_t cols);
+              int64_t cols, cudaStream_t s = nullptr);
 void d2h_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t rows,
-              int64_t cols);
+              int64_t cols, cudaStream_t s = nullptr);
 void release_staging(Ctx& c);
 
 // Full-spectrum problem (ipt_full.cu)
@@ -110,6 +112,12 @@ void full_reset(FullProblem& P, const double* warm_re, const double* warm_im, in
 void full_iterate(FullProblem& P, const ipt_params& prm, ipt_stats* stats);
 void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats);
 void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, double* lam_im);
+// Single-rank dense problems after full_iterate: Z to the host on ctx.stream2, safe to run
+// on another host thread while full_finalize uses ctx.stream (both only read Z).
+bool full_can_download_early(const FullProblem& P);
+void full_prepare_download(FullProblem& P, bool want_re, bool want_im);
+void full_download_z(FullProblem& P, double* z_re, double* z_im);
+void full_release_download(FullProblem& P);
 void full_local_columns(const FullProblem& P, int64_t* c0, int64_t* c1);
 bool full_is_complex(const FullProblem& P);
 void full_run_maps(FullProblem& P, int count, double* ms_total, double* ms_gemm);

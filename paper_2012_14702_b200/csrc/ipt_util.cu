@@ -1,5 +1,8 @@
 // Small device utilities: buffers, transposes, deterministic partial reduction.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -104,39 +107,53 @@ void release_staging(Ctx& c) {
 }
 
 void h2d_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t rows,
-              int64_t cols) {
+              int64_t cols, cudaStream_t stream) {
   if (rows <= 0 || cols <= 0) return;
+  cudaStream_t st = stream ? stream : c.stream;
   ensure_staging(c);
   const int64_t per = std::max<int64_t>(1, static_cast<int64_t>(c.stage_doubles) / cols);
   if (per < 1 || cols > static_cast<int64_t>(c.stage_doubles)) {  // a row larger than a buffer
     IPT_CUDA(cudaMemcpy2DAsync(dst, dpitch * sizeof(double), src, spitch * sizeof(double), cols * sizeof(double),
-                               rows, cudaMemcpyHostToDevice, c.stream));
-    c.sync();
+                               rows, cudaMemcpyHostToDevice, st));
+    IPT_CUDA(cudaStreamSynchronize(st));
     return;
   }
   int b = 0;
   bool used[2] = {false, false};
+  const bool prof = std::getenv("IPT_PROFILE") != nullptr;
+  double t_wait = 0.0, t_copy = 0.0;
+  auto now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  const double t_start = now();
   for (int64_t r0 = 0; r0 < rows; r0 += per, b ^= 1) {
     const int64_t nr = std::min(per, rows - r0);
+    double t0 = now();
     if (used[b]) IPT_CUDA(cudaEventSynchronize(c.stage_ev[b]));  // DMA of this buffer done
+    double t1 = now();
     host_copy_rows(c.stage[b], cols, src + r0 * spitch, spitch, nr, cols);
+    t_wait += t1 - t0;
+    t_copy += now() - t1;
     IPT_CUDA(cudaMemcpy2DAsync(dst + r0 * dpitch, dpitch * sizeof(double), c.stage[b], cols * sizeof(double),
-                               cols * sizeof(double), nr, cudaMemcpyHostToDevice, c.stream));
-    IPT_CUDA(cudaEventRecord(c.stage_ev[b], c.stream));
+                               cols * sizeof(double), nr, cudaMemcpyHostToDevice, st));
+    IPT_CUDA(cudaEventRecord(c.stage_ev[b], st));
     used[b] = true;
   }
-  c.sync();
+  IPT_CUDA(cudaStreamSynchronize(st));
+  if (prof && rows * cols >= (int64_t(1) << 24))
+    std::fprintf(stderr, "[ipt] h2d_rows %.2f GB: %.1f ms (host copy %.1f, DMA wait %.1f, %u threads)\n",
+                 8e-9 * double(rows) * double(cols), 1e3 * (now() - t_start), 1e3 * t_copy, 1e3 * t_wait,
+                 copy_threads());
 }
 
 void d2h_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t rows,
-              int64_t cols) {
+              int64_t cols, cudaStream_t stream) {
   if (rows <= 0 || cols <= 0) return;
+  cudaStream_t st = stream ? stream : c.stream;
   ensure_staging(c);
   const int64_t per = static_cast<int64_t>(c.stage_doubles) / cols;
   if (per < 1) {
     IPT_CUDA(cudaMemcpy2DAsync(dst, dpitch * sizeof(double), src, spitch * sizeof(double), cols * sizeof(double),
-                               rows, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+                               rows, cudaMemcpyDeviceToHost, st));
+    IPT_CUDA(cudaStreamSynchronize(st));
     return;
   }
   // DMA chunk k+1 into one buffer while the host drains chunk k from the other.
@@ -145,18 +162,30 @@ void d2h_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t sp
     const int64_t r0 = k * per, nr = std::min(per, rows - r0);
     const int b = static_cast<int>(k & 1);
     IPT_CUDA(cudaMemcpy2DAsync(c.stage[b], cols * sizeof(double), src + r0 * spitch, spitch * sizeof(double),
-                               cols * sizeof(double), nr, cudaMemcpyDeviceToHost, c.stream));
-    IPT_CUDA(cudaEventRecord(c.stage_ev[b], c.stream));
+                               cols * sizeof(double), nr, cudaMemcpyDeviceToHost, st));
+    IPT_CUDA(cudaEventRecord(c.stage_ev[b], st));
   };
+  const bool prof = std::getenv("IPT_PROFILE") != nullptr;
+  double t_wait = 0.0, t_copy = 0.0;
+  auto now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  const double t_start = now();
   issue(0);
   for (int64_t k = 0; k < nchunks; ++k) {
     if (k + 1 < nchunks) issue(k + 1);
     const int b = static_cast<int>(k & 1);
+    const double t0 = now();
     IPT_CUDA(cudaEventSynchronize(c.stage_ev[b]));
+    const double t1 = now();
     const int64_t r0 = k * per, nr = std::min(per, rows - r0);
     host_copy_rows(dst + r0 * dpitch, dpitch, c.stage[b], cols, nr, cols);
+    t_wait += t1 - t0;
+    t_copy += now() - t1;
   }
-  c.sync();
+  IPT_CUDA(cudaStreamSynchronize(st));
+  if (prof && rows * cols >= (int64_t(1) << 24))
+    std::fprintf(stderr, "[ipt] d2h_rows %.2f GB: %.1f ms (host copy %.1f, DMA wait %.1f, %u threads)\n",
+                 8e-9 * double(rows) * double(cols), 1e3 * (now() - t_start), 1e3 * t_copy, 1e3 * t_wait,
+                 copy_threads());
 }
 
 // 32x32 tiles through shared memory; src column-major (element (r, c) at c*ld_src + r),

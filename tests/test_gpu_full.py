@@ -300,3 +300,34 @@ def test_sigma_min_across_cholesky_panels(port_arm, n):
     np.fill_diagonal(z, 1.0)
     want = port_arm.sigma_min(z)
     assert ipt.smallest_singular_value_estimate(z) == pytest.approx(want, rel=1e-8)
+
+
+@pytest.mark.parametrize("n", [1, 130, 1000, 2100])
+def test_identity_start_shortcut_is_bitwise_the_gemm_path(n):
+    """F(I) is evaluated without the product (W = Delta I = Delta exactly) through K1's
+    own epilogue; the whole solve must be bit-identical to running map 1 as a GEMM."""
+    import os
+
+    p = synth.config3(n=n) if n > 1 else ipt.Partition(np.array([1.0]), np.zeros((1, 1)))
+    g = ipt.build_gaps(p)
+    cfg = ipt.IterationConfig(tolerance=1e-12, record_trace=True)
+    a = ipt.solve_full(p, g, cfg)
+    os.environ["IPT_IDENTITY_SHORTCUT"] = "0"
+    try:
+        b = ipt.solve_full(p, g, cfg)
+    finally:
+        del os.environ["IPT_IDENTITY_SHORTCUT"]
+    assert a.iterations == b.iterations and a.trace == b.trace
+    assert np.array_equal(a.Z, b.Z) and np.array_equal(a.eigenvalues, b.eigenvalues)
+    assert a.residual_frobenius == b.residual_frobenius
+    assert a.min_singular_value_estimate == b.min_singular_value_estimate
+
+
+def test_identity_start_with_nonfinite_delta_matches_gemm_semantics():
+    """An Inf in Delta makes the GEMM's zero terms NaN; the shortcut is disabled then."""
+    n = 64
+    d = np.arange(n, dtype=float)
+    delta = np.zeros((n, n))
+    delta[3, 7] = np.inf
+    r = ipt.solve_full(ipt.Partition(d, delta), ipt.build_gaps(ipt.Partition(d, delta)))
+    assert r.status == ipt.SolveStatus.Diverged and r.iterations == 1
