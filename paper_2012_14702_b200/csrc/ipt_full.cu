@@ -293,8 +293,9 @@ __global__ void sparse_diag_kernel(SpmmArgs a, double* __restrict__ wd, double* 
 // (a full 32-byte sector per lane at VEC = 4). Work items run chunk-major, so the
 // warps in flight share one column chunk of Z (n x 1 KB) in L2. The persistent grid
 // is fixed (spmm_grid()), so the per-CTA partials and their reduction are deterministic.
-template <int MODE, int VEC>  // MODE 0: map (F and the 4 partial sums), 1: residual sum
-__global__ void __launch_bounds__(256) spmm_full_kernel(SpmmArgs a) {
+// MODE 0: map (F and the 4 partial sums), 1: residual sum; U entries in flight per lane.
+template <int MODE, int VEC, int MINB, int U>
+__global__ void __launch_bounds__(256, MINB) spmm_full_kernel(SpmmArgs a) {
   if (a.state != nullptr && a.state->done) return;
   __shared__ double red[8][4];
   double v[4] = {0.0, 0.0, 0.0, 0.0};
@@ -320,11 +321,11 @@ __global__ void __launch_bounds__(256) spmm_full_kernel(SpmmArgs a) {
         kv = __ldg(a.vals + base + lane);
       }
       int q = 0;
-      for (; q + 4 <= cnt; q += 4) {
-        double2 z[4][VEC / 2];
-        double vv[4];
+      for (; q + U <= cnt; q += U) {
+        double2 z[U][VEC / 2];
+        double vv[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < U; ++u) {
           const int64_t k = __shfl_sync(0xffffffffu, kc, q + u);
           vv[u] = __shfl_sync(0xffffffffu, kv, q + u);
           const double2* src = reinterpret_cast<const double2*>(zc + k * a.ldr);
@@ -332,7 +333,7 @@ __global__ void __launch_bounds__(256) spmm_full_kernel(SpmmArgs a) {
           for (int h = 0; h < VEC / 2; ++h) z[u][h] = __ldg(src + h);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < U; ++u)
 #pragma unroll
           for (int h = 0; h < VEC / 2; ++h) {
             acc[2 * h] = __fma_rn(vv[u], z[u][h].x, acc[2 * h]);
@@ -439,12 +440,31 @@ __global__ void count_nonfinite_kernel(const double* __restrict__ A, int64_t cou
 
 namespace {
 
-int spmm_vec() {
+// Tuned variants of K10 (IPT_SPMM_VARIANT selects one; profiles/r01_spmm_variants.txt).
+struct SpmmVariant {
+  void (*map)(SpmmArgs);
+  void (*resid)(SpmmArgs);
+  const char* name;
+};
+const SpmmVariant kSpmmVariants[] = {
+    {spmm_full_kernel<0, 4, 2, 4>, spmm_full_kernel<1, 4, 2, 4>, "vec4 minb2 u4"},
+    {spmm_full_kernel<0, 4, 3, 4>, spmm_full_kernel<1, 4, 3, 4>, "vec4 minb3 u4"},
+    {spmm_full_kernel<0, 4, 4, 4>, spmm_full_kernel<1, 4, 4, 4>, "vec4 minb4 u4"},
+    {spmm_full_kernel<0, 2, 4, 4>, spmm_full_kernel<1, 2, 4, 4>, "vec2 minb4 u4"},
+    {spmm_full_kernel<0, 4, 2, 8>, spmm_full_kernel<1, 4, 2, 8>, "vec4 minb2 u8"},
+    {spmm_full_kernel<0, 4, 3, 8>, spmm_full_kernel<1, 4, 3, 8>, "vec4 minb3 u8"},
+    {spmm_full_kernel<0, 2, 6, 8>, spmm_full_kernel<1, 2, 6, 8>, "vec2 minb6 u8"},
+};
+constexpr int kSpmmDefault = 0;
+
+const SpmmVariant& spmm_variant() {
   static const int v = [] {
-    const char* e = std::getenv("IPT_SPMM_VEC");
-    return (e && std::atoi(e) == 2) ? 2 : 4;
+    const char* e = std::getenv("IPT_SPMM_VARIANT");
+    const int k = e ? std::atoi(e) : kSpmmDefault;
+    const int nv = static_cast<int>(sizeof(kSpmmVariants) / sizeof(kSpmmVariants[0]));
+    return (k >= 0 && k < nv) ? k : kSpmmDefault;
   }();
-  return v;
+  return kSpmmVariants[v];
 }
 
 // IPT_IDENTITY_SHORTCUT=0 runs the first map from I through the GEMM as well.
@@ -487,10 +507,7 @@ int spmm_grid() {
     int dev = 0, sms = 0, per_sm = 0;
     IPT_CUDA(cudaGetDevice(&dev));
     IPT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    if (spmm_vec() == 2)
-      IPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_full_kernel<0, 2>, 256, 0));
-    else
-      IPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_full_kernel<0, 4>, 256, 0));
+    IPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmm_variant().map, 256, 0));
     return std::max(1, std::min(kEpiBlocks, sms * std::max(per_sm, 1)));
   }();
   return g;
@@ -500,13 +517,8 @@ void launch_spmm(FullProblem& P, int mode, const double* Zs, double* Fd, const L
   const SpmmArgs a = spmm_args(P, Zs, Fd, st);
   cudaStream_t s = P.ctx->stream;
   const unsigned grid = static_cast<unsigned>(spmm_grid());
-  if (spmm_vec() == 2) {
-    if (mode == 0) spmm_full_kernel<0, 2><<<grid, 256, 0, s>>>(a);
-    else spmm_full_kernel<1, 2><<<grid, 256, 0, s>>>(a);
-  } else {
-    if (mode == 0) spmm_full_kernel<0, 4><<<grid, 256, 0, s>>>(a);
-    else spmm_full_kernel<1, 4><<<grid, 256, 0, s>>>(a);
-  }
+  const SpmmVariant& v = spmm_variant();
+  (mode == 0 ? v.map : v.resid)<<<grid, 256, 0, s>>>(a);
   IPT_LAUNCH_CHECK();
   count_launch();
 }
