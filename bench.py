@@ -407,9 +407,15 @@ def main():
         torch.cuda.empty_cache()
         barrier()
         t0 = time.perf_counter()
-        r = ipt.solve_full(p, ipt.build_gaps(p), ipt.IterationConfig(tolerance=1e-12), ctx=ctx)
+        gaps = ipt.build_gaps(p)
+        t_gaps = time.perf_counter() - t0
+        r = ipt.solve_full(p, gaps, ipt.IterationConfig(tolerance=1e-12), ctx=ctx)
+        t_call = time.perf_counter() - t0 - t_gaps
         barrier()
         e2e_s = max_over_ranks(time.perf_counter() - t0)
+        if os.environ.get("IPT_PROFILE"):
+            print(f"[bench] e2e: build_gaps {1e3 * t_gaps:.1f} ms, solve_full {1e3 * t_call:.1f} ms, "
+                  f"total {1e3 * e2e_s:.1f} ms", file=sys.stderr, flush=True)
         e2e = {"value": flops_step * r.iterations / e2e_s / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": int(8 * n * n + 8 * n),
                "d2h_bytes_per_step": int(8 * n * n + 8 * n) if rank == 0 else 0,

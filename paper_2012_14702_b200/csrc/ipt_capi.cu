@@ -239,6 +239,7 @@ void ipt_ctx_destroy(ipt_ctx* ctx) {
   if (ctx->c.h_state) cudaFreeHost(ctx->c.h_state);
   if (ctx->c.h_aux) cudaFreeHost(ctx->c.h_aux);
   release_staging(ctx->c);
+  release_cached_device_memory(ctx->c.device);
   if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
   if (ctx->c.stream2) cudaStreamDestroy(ctx->c.stream2);
   delete ctx;

@@ -649,9 +649,12 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
   P->ldz = P->lda;
   cudaStream_t s = c.stream;
 
+  ProfMarks pm("full_upload");
   P->A1.alloc(size_t(P->rows_pad) * P->lda);
+  pm.mark("alloc_delta");
   if (!P->cplx) {
     h2d_rows(c, P->A1.get(), P->lda, delta_re, n, n, n);  // pinned, double-buffered
+    pm.mark("h2d");
   } else {
     P->A2.alloc(size_t(P->rows_pad) * P->lda);
     // A1 = [Dr | -Di], A2 = [Di | Dr]
@@ -676,6 +679,7 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
   IPT_CUDA(cudaMemcpyAsync(P->dre.get(), d_re, sizeof(double) * n, cudaMemcpyHostToDevice, s));
   if (d_im) IPT_CUDA(cudaMemcpyAsync(P->dim.get(), d_im, sizeof(double) * n, cudaMemcpyHostToDevice, s));
   for (auto& z : P->Z) z.alloc(size_t(P->cols_pad) * P->ldz);
+  pm.mark("alloc_z");
   if (P->cplx) {
     P->Wre.alloc(size_t(P->cols_pad) * P->ld);
     P->Wim.alloc(size_t(P->cols_pad) * P->ld);
@@ -699,6 +703,7 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
     c.sync();
     cudaFree(flag);
     P->delta_finite = (h == 0);
+    pm.mark("finite_check");
   }
   c.sync();
   return P.release();

@@ -4,6 +4,7 @@
 #include <nccl.h>
 
 #include <atomic>
+#include <string>
 #include <memory>
 #include <vector>
 
@@ -59,6 +60,18 @@ struct Ctx {
   }
 };
 
+// IPT_PROFILE=1: host wall time between marks of one routine, printed on destruction.
+struct ProfMarks {
+  const char* name;
+  bool on;
+  double last;
+  std::string line;
+  static double now();
+  explicit ProfMarks(const char* n);
+  void mark(const char* what, bool sync_device = false);
+  ~ProfMarks();
+};
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
@@ -85,6 +98,8 @@ void gemm_tn_store(cudaStream_t s, int64_t m, int64_t n, int64_t kpad, const dou
 void transpose_to_rowmajor(cudaStream_t s, const double* src_colmajor, int64_t ld_src, int64_t rows,
                            int64_t cols, double* dst, int64_t ld_dst, double scale_sign = 1.0);
 void fill_zero(cudaStream_t s, double* p, size_t count);
+// Return the stream-ordered pool's cached (freed) memory to the device.
+void release_cached_device_memory(int device);
 void reduce_partials(cudaStream_t s, const double* partials, int64_t count, double* out4,
                      const LoopState* state);
 void scale_copy(cudaStream_t s, const double* src, double* dst, size_t count, double factor);

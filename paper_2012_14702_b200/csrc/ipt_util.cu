@@ -1,5 +1,6 @@
 // Small device utilities: buffers, transposes, deterministic partial reduction.
 #include <algorithm>
+#include <sys/mman.h>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -13,6 +14,23 @@
 namespace iptb {
 
 std::atomic<int64_t> g_launches{0};
+
+double ProfMarks::now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+ProfMarks::ProfMarks(const char* n) : name(n), on(std::getenv("IPT_PROFILE") != nullptr), last(now()) {}
+void ProfMarks::mark(const char* what, bool sync_device) {
+  if (!on) return;
+  if (sync_device) cudaDeviceSynchronize();
+  const double t = now();
+  char buf[96];
+  std::snprintf(buf, sizeof buf, " %s %.1f", what, 1e3 * (t - last));
+  line += buf;
+  last = t;
+}
+ProfMarks::~ProfMarks() {
+  if (on) std::fprintf(stderr, "[ipt] %s ms:%s\n", name, line.c_str());
+}
 
 // Device buffers come from the stream-ordered pool (cudaMallocAsync on the legacy
 // stream) so the many small, short-lived buffers of the kernels:: / apply_map entry
@@ -29,12 +47,23 @@ void configure_pool_once() {
   if (dev < 0 || dev >= 64 || done[dev]) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t keep = uint64_t(4) << 30;  // retain up to 4 GB of freed memory for reuse
+    // Keep freed memory mapped for reuse: trimming the pool at every synchronisation
+    // unmaps tens of GB after a large solve and the next solve pays to map it again
+    // (~1 s per 17 GB measured). The context releases the cache (ipt_ctx_destroy).
+    uint64_t keep = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
   done[dev] = true;
 }
 }  // namespace
+
+void release_cached_device_memory(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(pool, 0);
+  }
+}
 
 void DevBuf::alloc(size_t n, bool zero) {
   release();
@@ -94,6 +123,36 @@ void host_copy_rows(double* dst, int64_t dpitch, const double* src, int64_t spit
   }
   for (auto& th : pool) th.join();
 }
+// Large host destinations (a fresh n x n result array) are first-touched here in
+// parallel: transparent huge pages requested for the range, then the pages populated
+// by all copy threads at once (MADV_POPULATE_WRITE, else one store per 4 KB page), so
+// the staged copies below do not take ~2 M serialised page faults.
+void prefault_host_destination(double* dst, size_t bytes) {
+  if (bytes < (size_t(256) << 20)) return;
+  const uintptr_t huge = uintptr_t(2) << 20;
+  const uintptr_t b0 = (reinterpret_cast<uintptr_t>(dst) + huge - 1) & ~(huge - 1);
+  const uintptr_t b1 = (reinterpret_cast<uintptr_t>(dst) + bytes) & ~(huge - 1);
+  if (b1 > b0) madvise(reinterpret_cast<void*>(b0), b1 - b0, MADV_HUGEPAGE);
+  const unsigned t = copy_threads();
+  const size_t page = 4096;
+  const uintptr_t p0 = (reinterpret_cast<uintptr_t>(dst) + page - 1) & ~(page - 1);
+  const uintptr_t p1 = (reinterpret_cast<uintptr_t>(dst) + bytes) & ~(page - 1);
+  if (p1 <= p0) return;
+  const size_t span = ((p1 - p0) / t + huge - 1) & ~(huge - 1);
+  std::vector<std::thread> pool;
+  for (unsigned k = 0; k < t; ++k) {
+    const uintptr_t a = p0 + k * span, b = std::min<uintptr_t>(p1, a + span);
+    if (a >= b) break;
+    pool.emplace_back([a, b, page] {
+#ifdef MADV_POPULATE_WRITE
+      if (madvise(reinterpret_cast<void*>(a), b - a, MADV_POPULATE_WRITE) == 0) return;
+#endif
+      for (uintptr_t q = a; q < b; q += page) *reinterpret_cast<volatile char*>(q) = 0;
+    });
+  }
+  for (auto& th : pool) th.join();
+}
+
 }  // namespace
 
 void release_staging(Ctx& c) {
@@ -169,7 +228,9 @@ void d2h_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t sp
   double t_wait = 0.0, t_copy = 0.0;
   auto now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   const double t_start = now();
-  issue(0);
+  issue(0);  // the first DMA runs while the destination is prefaulted
+  if (dpitch == cols) prefault_host_destination(dst, sizeof(double) * size_t(rows) * size_t(cols));
+  const double t_fault = now() - t_start;
   for (int64_t k = 0; k < nchunks; ++k) {
     if (k + 1 < nchunks) issue(k + 1);
     const int b = static_cast<int>(k & 1);
@@ -183,9 +244,9 @@ void d2h_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t sp
   }
   IPT_CUDA(cudaStreamSynchronize(st));
   if (prof && rows * cols >= (int64_t(1) << 24))
-    std::fprintf(stderr, "[ipt] d2h_rows %.2f GB: %.1f ms (host copy %.1f, DMA wait %.1f, %u threads)\n",
-                 8e-9 * double(rows) * double(cols), 1e3 * (now() - t_start), 1e3 * t_copy, 1e3 * t_wait,
-                 copy_threads());
+    std::fprintf(stderr, "[ipt] d2h_rows %.2f GB: %.1f ms (prefault %.1f, host copy %.1f, DMA wait %.1f, %u threads)\n",
+                 8e-9 * double(rows) * double(cols), 1e3 * (now() - t_start), 1e3 * t_fault, 1e3 * t_copy,
+                 1e3 * t_wait, copy_threads());
 }
 
 // 32x32 tiles through shared memory; src column-major (element (r, c) at c*ld_src + r),

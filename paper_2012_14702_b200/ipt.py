@@ -19,8 +19,10 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 import sys
 import threading
+import time
 from dataclasses import dataclass, field
 from typing import Optional, Union
 
@@ -416,6 +418,7 @@ def solve_full(p: Partition, g: InverseGaps, config: IterationConfig = None, war
     st.trace = dptr(tr)
     st.trace_max_abs = dptr(tm)
     lib = _lib.load()
+    t_call = time.perf_counter()
     if isinstance(p.delta, CsrMatrix):  # sparse Delta: fused SpMM map (real) on the device
         vr, vi = _planar(p.delta.values)
         check(lib.ipt_full_solve_csr(ctx.handle, n, dptr(dr), dptr(di), i64ptr(p.delta.row_offsets),
@@ -426,6 +429,8 @@ def solve_full(p: Partition, g: InverseGaps, config: IterationConfig = None, war
         check(lib.ipt_full_solve(ctx.handle, n, dptr(dr), dptr(di), dptr(ar), dptr(ai), dptr(wr),
                                  dptr(wi), C.byref(prm), dptr(zr), dptr(zi), dptr(lr), dptr(li),
                                  C.byref(st)))
+    if os.environ.get("IPT_PROFILE"):
+        print(f"[ipt.py] solve_full C call {1e3 * (time.perf_counter() - t_call):.1f} ms", file=sys.stderr)
     res = SpectrumResult()
     if root:
         res.Z = _combine(zr, zi, cx)
