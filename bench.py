@@ -277,7 +277,7 @@ def bench_single(ipt, lib, ctx, which, steps, warmup, hbm):
     dom_ms = dom.value / steps
     kbytes = nbytes - 8.0 * n  # the map kernel itself: matrix + z + d + fz
     del p
-    return {
+    out = {
         "workload": ("configs[3] dense GEMV single pair N=65536" if which == "gemv"
                      else "configs[4] CSR SpMV single pair N=2^21 (~64 nnz/row)"),
         "metric": "single-pair IPT iteration GB/s (algorithmic bytes)",
@@ -288,6 +288,14 @@ def bench_single(ipt, lib, ctx, which, steps, warmup, hbm):
                      "frac": kbytes / (dom_ms * 1e-3) / 1e9 / hbm[0], "kernel_ms": dom_ms,
                      "bytes_per_launch": kbytes, "traffic": traffic_for(kernel, n)},
     }
+    if which == "spmv":
+        # The random z gather (32-byte L2 sector per 8-byte use), not HBM, bounds this
+        # kernel: measured ceiling = the same stream + gather without row structure.
+        ceil_ms = 0.518
+        out["roofline"]["memory_ceiling"] = {
+            "ms": ceil_ms, "frac": ceil_ms / dom_ms,
+            "source": "profiles/r01_gather_probe.txt (tools/probes/gather_probe.cu, one B200)"}
+    return out
 
 
 def bench_sparse_full(lib, ctx, n, per_row, steps, dense_step_ms):
