@@ -35,9 +35,10 @@ def test_reference_acceptance_hot_path_criteria():
     """Criteria 1, 2, 5 (hot path) and 4, 6, 7, 8 (off-path modules calling our solvers)
     must pass. Criterion 3 (explorer, off-path, run on the reference's own CPU kernels)
     fails identically on the reference build (flip 0.8634, cardioid 30/32).
-    Criterion 9 is the reference's CPU cost model T_eig/T_mm ~ products: on the GPU both
-    timings are dominated by fixed host<->device costs at N = 1024 that solve_full pays
-    once and matmul pays per call, so it is reported, not asserted."""
+    Criterion 9 is the reference's CPU cost model T_eig/T_mm per product in [0.5, 2]:
+    it passes on the B200 (0.53 per product measured) but sits at the lower edge, since
+    the first map from I needs no product and host<->device costs dominate at N = 1024,
+    so it is reported, not asserted."""
     r = _run("acceptance_b200", 1800)
     print(r.stdout)
     status = {int(m.group(2)): m.group(1) for m in re.finditer(r"\[(PASS|FAIL)\] criterion (\d+)", r.stdout)}
