@@ -331,3 +331,38 @@ def test_identity_start_with_nonfinite_delta_matches_gemm_semantics():
     delta[3, 7] = np.inf
     r = ipt.solve_full(ipt.Partition(d, delta), ipt.build_gaps(ipt.Partition(d, delta)))
     assert r.status == ipt.SolveStatus.Diverged and r.iterations == 1
+
+
+def test_divergence_status_and_step_match_oracle(port_arm):
+    """A strongly perturbed instance: divergence is tested before convergence
+    (solver.cpp:241-249) and reported at the same iteration as the restatement."""
+    n = 96
+    rng = np.random.default_rng(4)
+    delta = 2.0 * rng.uniform(-1, 1, (n, n))
+    delta = 0.5 * (delta + delta.T)
+    np.fill_diagonal(delta, 0)
+    d = np.arange(1.0, n + 1)
+    p = ipt.Partition(d, delta)
+    r = ipt.solve_full(p, ipt.build_gaps(p), ipt.IterationConfig(divergence_threshold=1e6), want_sigma_min=False)
+    o = port_arm.solve_full(d, delta, div_thr=1e6, sigma=False)
+    assert int(r.status) == o["status"] == int(ipt.SolveStatus.Diverged)
+    assert r.iterations == o["iterations"]
+
+
+@pytest.mark.parametrize("max_iter", [1, 2, 3])
+def test_max_iterations_returns_the_last_iterate(port_arm, max_iter):
+    n = 150
+    p = synth.dense_uniform(n, 0.3 / np.sqrt(n), 5)
+    r = ipt.solve_full(p, ipt.build_gaps(p), ipt.IterationConfig(max_iterations=max_iter, tolerance=1e-15))
+    o = port_arm.solve_full(p.d, p.delta, tol=1e-15, max_iter=max_iter)
+    assert r.status == ipt.SolveStatus.MaxIterations and int(o["status"]) == 1
+    assert r.iterations == o["iterations"] == max_iter
+    assert r.matmul_count == o["matmul_count"] == max_iter + 1
+    assert np.max(np.abs(r.Z - o["Z"].real)) <= VEC_ABS
+    np.testing.assert_allclose(r.eigenvalues, o["eigenvalues"].real, rtol=LAM_REL, atol=0)
+
+
+def test_empty_problem_is_rejected():
+    p = ipt.Partition(np.zeros(0), np.zeros((0, 0)))
+    with pytest.raises(ValueError):
+        ipt.solve_full(p, ipt.build_gaps(p))
