@@ -42,6 +42,7 @@ struct SingleProblem {
   DevBuf arow, arowi;
   std::unique_ptr<int32_t, void (*)(void*)> acols{nullptr, [](void* p) { cudaFree(p); }};
   int64_t annz = 0;
+  int anchor_phase = 0;  // grouped CSR kernels: lane phase of the anchor row in its row group
   int64_t anchor = -1;
   // host copies needed to (re)build the anchor row for a new anchor
   std::vector<int64_t> h_rowptr;
@@ -70,25 +71,36 @@ namespace {
 constexpr int kGemvRows = 4;        // rows per warp (dense)
 constexpr int kGemvWarps = 8;
 constexpr int kRowsPerBlock = kGemvRows * kGemvWarps;
-// CSR variants (lanes per row, entries in flight per lane). Measured at config 5
-// (N = 2^21, 64 nnz/row, profiles/r01_spmv_variants.txt): {8,4} 0.674 ms, {16,4}
-// 0.689, {16,6} 0.753, {32,2} 0.832, {8,8} 0.905 -- all near the L2-sector bound of
-// the 8-byte z gathers. Default {8,4}; IPT_SPMV_VARIANT selects another.
+// CSR variants. Row kernels (lanes per row, entries in flight per lane), measured at
+// config 5 (N = 2^21, 64 nnz/row, profiles/r01_spmv_variants.txt): {8,4} 0.674 ms,
+// {16,4} 0.689, {16,6} 0.753, {32,2} 0.832, {8,8} 0.905. Warp-contiguous row groups
+// (spmv_group_kernel): 4 rows x 4 in flight 0.644 ms with L2 cache hints, 0.632 ms
+// without (default, variant 9); the memory ceiling of the same traffic is 0.518 ms
+// (profiles/r01_gather_probe.txt). IPT_SPMV_VARIANT selects another.
+// Variants 5-7: warp-contiguous row groups (spmv_group_kernel), lanes = 0 marks them,
+// u = entries in flight per lane, rows = rows per warp.
 struct SpmvVariant {
-  int lanes, u;
+  int lanes, u, rows, minb;
 };
-constexpr SpmvVariant kSpmvVariants[] = {{16, 4}, {8, 8}, {32, 2}, {8, 4}, {16, 6}};
+constexpr SpmvVariant kSpmvVariants[] = {{16, 4, 0, 5}, {8, 8, 0, 5}, {32, 2, 0, 5}, {8, 4, 0, 5}, {16, 6, 0, 5},
+                                         {0, 4, 4, 4},  {0, 2, 8, 4}, {0, 2, 4, 5}, {0, 4, 4, 3},
+                                         {0, 4, 4, 4},  {0, 4, 16, 3}, {0, 8, 4, 3}};
+constexpr int kNumSpmvVariants = sizeof(kSpmvVariants) / sizeof(kSpmvVariants[0]);
+constexpr int kSpmvDefault = 9;  // warp-contiguous groups of 4 rows, 4 in flight, plain nc loads
 inline int spmv_variant() {
   static const int v = [] {
     const char* e = std::getenv("IPT_SPMV_VARIANT");
-    const int k = e ? std::atoi(e) : 3;
-    return (k >= 0 && k < 5) ? k : 0;
+    const int k = e ? std::atoi(e) : kSpmvDefault;
+    return (k >= 0 && k < kNumSpmvVariants) ? k : kSpmvDefault;
   }();
   return v;
 }
-inline int spmv_rows_per_block() { return 256 / kSpmvVariants[spmv_variant()].lanes; }
+inline bool spmv_grouped() { return kSpmvVariants[spmv_variant()].lanes == 0; }
+inline int spmv_rows_per_block() {
+  const SpmvVariant& v = kSpmvVariants[spmv_variant()];
+  return v.lanes ? 256 / v.lanes : 8 * v.rows;
+}
 constexpr int kSpmvMinBlocks = 5;       // 48 registers (no spills): 5 CTAs (40 warps) per SM
-constexpr int kSpmvGrid = kNumSMs * kSpmvMinBlocks;  // persistent: exactly one resident wave
 
 enum MapMode : int { kMvStore = 0, kMvMap = 1, kMvFinal = 2, kMvAccel = 3 };
 
@@ -204,6 +216,71 @@ __device__ __forceinline__ double csr_row_dot(const int32_t* __restrict__ cols,
 #pragma unroll
   for (int off = LANES / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
   return s;
+}
+
+// R consecutive CSR rows per warp, streamed as ONE contiguous entry range: lane l takes
+// entries beg+l, beg+l+32, ... (fully coalesced index/value loads, one misaligned
+// sector per instruction at most) and adds each product to the accumulator of the row
+// it falls in; each row's 32 lane sums are then combined by the xor tree. A row's sum
+// is fixed by the lane phase (rowptr[row] - rowptr[group start]) mod 32, which the
+// anchor kernel reproduces (anchor_csr_phase_kernel), so w_a is the same number.
+__device__ __forceinline__ int32_t ld_nc_i32(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_nc_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+template <int R, int U, bool POL = true>
+__device__ __forceinline__ void group_row_sums(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
+                                               const double* __restrict__ vals, const double* __restrict__ z,
+                                               int64_t lr0, int64_t rows, int lane, uint64_t pol_stream,
+                                               uint64_t pol_keep, double (&s)[R]) {
+  const long long mine = lane <= R ? rowptr[lr0 + lane < rows ? lr0 + lane : rows] : 0;
+  int64_t rb[R + 1];
+#pragma unroll
+  for (int k = 0; k <= R; ++k) rb[k] = __shfl_sync(0xffffffffu, mine, k);
+#pragma unroll
+  for (int k = 0; k < R; ++k) s[k] = 0.0;
+  const int64_t end = rb[R];
+  for (int64_t p0 = rb[0] + lane; p0 < end; p0 += 32 * U) {
+    int32_t c[U];
+    double v[U], zz[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = p0 + 32 * u;
+      if (POL) {
+        c[u] = p < end ? ld_stream_i32(cols + p, pol_stream) : 0;
+        v[u] = p < end ? ld_stream_f64(vals + p, pol_stream) : 0.0;
+      } else {
+        c[u] = p < end ? ld_nc_i32(cols + p) : 0;
+        v[u] = p < end ? ld_nc_f64(vals + p) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      zz[u] = (p0 + 32 * u < end) ? (POL ? ld_keep_f64(z + c[u], pol_keep) : __ldg(z + c[u])) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = p0 + 32 * u;
+      if (p < end) {
+        int r = 0;
+#pragma unroll
+        for (int k = 1; k < R; ++k) r += p >= rb[k];
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+          if (k == r) s[k] = __fma_rn(v[u], zz[u], s[k]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s[k] += __shfl_xor_sync(0xffffffffu, s[k], off);
 }
 
 struct MapArgs {
@@ -323,6 +400,54 @@ __global__ void __launch_bounds__(256, kSpmvMinBlocks) spmv_map_kernel(const int
     double* o = a.partials + size_t(blockIdx.x) * 4;
     o[0] = v[0]; o[1] = v[1]; o[2] = v[2]; o[3] = v[3];
   }
+}
+
+template <int MODE, int R, int U, int MINB, bool POL = true>
+__global__ void __launch_bounds__(256, MINB) spmv_group_kernel(const int64_t* __restrict__ rowptr,
+                                                                         const int32_t* __restrict__ cols,
+                                                                         const double* __restrict__ vals, MapArgs a) {
+  if (a.state != nullptr && a.state->done) return;
+  __shared__ double red[8][4];
+  const int lane = threadIdx.x & 31;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  const double scale = MODE == kMvMap ? schedule_scale(a) : 1.0;
+  const double lam = (MODE == kMvFinal || MODE == kMvAccel) ? a.d[a.anchor] + *a.wa : 0.0;
+  const uint64_t pol_s = policy_stream(), pol_k = policy_keep();
+  // Persistent fixed grid: warp w of block b owns row groups (b*8 + w) + k*(grid*8).
+  const int64_t groups = ceil_div(a.rows, int64_t(R));
+  const int64_t nwarps = int64_t(gridDim.x) * 8;
+  for (int64_t grp = blockIdx.x * int64_t(8) + (threadIdx.x >> 5); grp < groups; grp += nwarps) {
+    const int64_t lr0 = grp * R;
+    double sum[R];
+    group_row_sums<R, U, POL>(rowptr, cols, vals, a.z, lr0, a.rows, lane, pol_s, pol_k, sum);
+    if (lane < R && lr0 + lane < a.rows) {
+      double w = sum[0];
+#pragma unroll
+      for (int k = 1; k < R; ++k)
+        if (lane == k) w = sum[k];
+      row_epilogue<MODE>(a, a.row0 + lr0 + lane, w, scale, lam, v);
+    }
+  }
+  if (MODE == kMvStore) return;
+  block_reduce4<8>(v, red);
+  if (threadIdx.x == 0) {
+    double* o = a.partials + size_t(blockIdx.x) * 4;
+    o[0] = v[0]; o[1] = v[1]; o[2] = v[2]; o[3] = v[3];
+  }
+}
+
+// The anchor row's sum exactly as spmv_group_kernel forms it: entry k of the row on
+// lane (phase + k) mod 32, ascending per lane, then the xor tree.
+__global__ void anchor_csr_phase_kernel(const int32_t* __restrict__ cols, const double* __restrict__ vals,
+                                        int64_t nnz, int phase, const double* __restrict__ z, double* wa,
+                                        const LoopState* st) {
+  if (st != nullptr && st->done) return;
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int64_t k = (lane - phase + 32) & 31; k < nnz; k += 32) s = __fma_rn(vals[k], z[cols[k]], s);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) wa[0] = s;
 }
 
 // w_a with exactly the per-row arithmetic of the map kernels.
@@ -481,15 +606,22 @@ void launch_spmv(unsigned grid, cudaStream_t s, const int64_t* rowptr, const int
   switch (spmv_variant()) {
 #define IPT_SPMV(K, L, UU) \
   case K: spmv_map_kernel<MODE, L, UU><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+#define IPT_SPMVG(K, R, UU, MB) \
+  case K: spmv_group_kernel<MODE, R, UU, MB><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
     IPT_SPMV(0, 16, 4) IPT_SPMV(1, 8, 8) IPT_SPMV(2, 32, 2) IPT_SPMV(3, 8, 4) IPT_SPMV(4, 16, 6)
+    IPT_SPMVG(5, 4, 4, 4) IPT_SPMVG(6, 8, 2, 4) IPT_SPMVG(7, 4, 2, 5) IPT_SPMVG(8, 4, 4, 3)
+    case 9: spmv_group_kernel<MODE, 4, 4, 4, false><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    IPT_SPMVG(10, 16, 4, 3) IPT_SPMVG(11, 4, 8, 3)
 #undef IPT_SPMV
+#undef IPT_SPMVG
   }
 }
 
 int64_t map_blocks(const SingleProblem& P) {
   if (P.cplx) return kCmapBlocks;
   const int64_t rows = P.r1 - P.r0;
-  return P.csr ? std::min<int64_t>(kSpmvGrid, ceil_div(rows, spmv_rows_per_block())) : ceil_div(rows, kRowsPerBlock);
+  const int64_t spmv_grid = int64_t(kNumSMs) * kSpmvVariants[spmv_variant()].minb;
+  return P.csr ? std::min<int64_t>(spmv_grid, ceil_div(rows, spmv_rows_per_block())) : ceil_div(rows, kRowsPerBlock);
 }
 
 MapArgs map_args(SingleProblem& P, int src) {
@@ -516,6 +648,10 @@ void enqueue_anchor(SingleProblem& P, int src, const LoopState* st) {
     break;
       IPT_ANCHOR(0, 16, 4) IPT_ANCHOR(1, 8, 8) IPT_ANCHOR(2, 32, 2) IPT_ANCHOR(3, 8, 4) IPT_ANCHOR(4, 16, 6)
 #undef IPT_ANCHOR
+      default:
+        anchor_csr_phase_kernel<<<1, 32, 0, s>>>(P.acols.get(), P.arow.get(), P.annz, P.anchor_phase,
+                                                 P.z[src].get(), P.wa.get(), st);
+        break;
     }
   } else {
     anchor_dense_kernel<<<1, 32, 0, s>>>(P.arow.get(), P.lda, P.z[src].get(), P.wa.get(), st);
@@ -627,6 +763,12 @@ void upload_anchor_row(SingleProblem& P) {
   } else {
     const int64_t b = P.h_rowptr[a], e = P.h_rowptr[a + 1];
     P.annz = e - b;
+    if (spmv_grouped()) {  // row group of the anchor on its owner rank (equal row chunks)
+      const int64_t R = kSpmvVariants[spmv_variant()].rows;
+      const int64_t r0o = (a / P.chunk) * P.chunk;
+      const int64_t gstart = r0o + R * ((a - r0o) / R);
+      P.anchor_phase = static_cast<int>((b - P.h_rowptr[gstart]) & 31);
+    }
     P.arow.alloc(std::max<int64_t>(P.annz, 1));
     int32_t* ac = nullptr;
     IPT_CUDA(cudaMalloc(&ac, sizeof(int32_t) * std::max<int64_t>(P.annz, 1)));
