@@ -71,6 +71,8 @@ void launch_gemm(int mode, const GemmParams& p, cudaStream_t s) {
     case kGemmMap: launch_mode<kGemmMap>(p, s); break;
     case kGemmResid: launch_mode<kGemmResid>(p, s); break;
     case kGemmSub: launch_mode<kGemmSub>(p, s); break;
+    case kGemmMapC: launch_mode<kGemmMapC>(p, s); break;
+    case kGemmResidC: launch_mode<kGemmResidC>(p, s); break;
     default: throw InvalidArgument("launch_gemm: bad mode");
   }
 }

@@ -16,6 +16,10 @@
 //   kGemmResid : partial sum |d_i Z_ij + W_ij - Z_ij lam_j|^2, nothing stored
 //                -> proj/src/solver.cpp:258-267
 //   kGemmSub   : C -= W (blocked Cholesky trailing update, lower tiles only)
+//   kGemmMapC / kGemmResidC : complex Delta Z by three real GEMMs (3M): T1 = Dr Zr and
+//                T2 = Di Zi stored, this launch computes T3 = (Dr + Di)(Zr + Zi) and forms
+//                W = (T1 - T2) + i (T3 - T1 - T2) in the epilogue, then the complex map
+//                (F stored to C / Cim) or the complex residual, with the same partials.
 //
 // Main loop (dmma_tma_kernel): CTA tile 128x128, BK = 16 doubles, a 6-stage
 // TMA pipeline (cp.async.bulk.tensor with 128-byte swizzle, full/empty mbarriers;
@@ -35,7 +39,7 @@
 
 namespace iptb {
 
-enum GemmMode : int { kGemmStore = 0, kGemmMap = 1, kGemmResid = 2, kGemmSub = 3 };
+enum GemmMode : int { kGemmStore = 0, kGemmMap = 1, kGemmResid = 2, kGemmSub = 3, kGemmMapC = 4, kGemmResidC = 5 };
 
 constexpr int kBM = 128;
 constexpr int kBN = 128;
@@ -67,6 +71,17 @@ struct GemmParams {
   int64_t n_rows, n_cols;   // true extents of C
   double* partials;         // [tiles_m * tiles_n][4]
   const LoopState* state;   // nullable; CTA exits if state->done
+  // complex epilogues (kGemmMapC / kGemmResidC)
+  const double* T1;         // Dr Zr, column-major (ldt)
+  const double* T2;         // Di Zi
+  int64_t ldt;
+  const double* zre;        // current Z planes, column-major (ldzz)
+  const double* zim;
+  int64_t ldzz;
+  const double* wdi;        // imaginary parts of wd, d, lam
+  const double* di;
+  const double* lami;
+  double* Cim;              // imaginary plane of F (map), ldc
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -152,6 +167,44 @@ __device__ __forceinline__ void gemm_epilogue(const GemmParams& p, double (&acc)
             else *cp = __dsub_rn(*cp, acc[mi][ni][r]);
           }
         }
+    return;
+  }
+  if (MODE == kGemmMapC || MODE == kGemmResidC) {
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t j = n0 + wn * 32 + ni * 8 + 2 * t + e;
+        if (j >= p.n_cols) continue;
+        const int64_t jg = p.col0 + j;
+        const cd dj{p.d[jg], p.di[jg]};
+        const cd wj = MODE == kGemmMapC ? cd{p.wd[j], p.wdi[j]} : cd{p.lam[j], p.lami[j]};
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t i = m0 + wm * 64 + mi * 16 + g + h * 8;
+            if (i >= p.n_rows) continue;
+            const int64_t ig = p.row0 + i;
+            const double t1 = p.T1[j * p.ldt + i], t2 = p.T2[j * p.ldt + i];
+            const cd w{t1 - t2, acc[mi][ni][h * 2 + e] - t1 - t2};
+            const cd z{p.zre[j * p.ldzz + i], p.zim[j * p.ldzz + i]};
+            const cd di{p.d[ig], p.di[ig]};
+            if (MODE == kGemmMapC) {
+              const cd f = (ig == jg) ? cd{1.0, 0.0} : cdiv(csub(cmul(z, wj), w), csub(di, dj));
+              p.C[j * p.ldc + i] = f.re;
+              p.Cim[j * p.ldc + i] = f.im;
+              const cd df = csub(f, z);
+              v[0] += df.re * df.re + df.im * df.im;
+              v[1] += z.re * z.re + z.im * z.im;
+              v[2] += f.re * f.re + f.im * f.im;
+              v[3] = nan_max(v[3], hypot(df.re, df.im));
+            } else {
+              const cd r = csub(cadd(cmul(di, z), w), cmul(z, wj));
+              v[0] += r.re * r.re + r.im * r.im;
+            }
+          }
+      }
     return;
   }
 #pragma unroll

@@ -87,4 +87,23 @@ __device__ __forceinline__ void block_reduce4(double v[4], double (*smem)[4]) {
   }
 }
 
+// Complex scalars of the complex paths: the reference's std::complex<double> arithmetic
+// (products as written, scaled division like libgcc's __divdc3 for finite inputs).
+struct cd {
+  double re, im;
+};
+__device__ __forceinline__ cd cmul(cd a, cd b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+__device__ __forceinline__ cd csub(cd a, cd b) { return {a.re - b.re, a.im - b.im}; }
+__device__ __forceinline__ cd cadd(cd a, cd b) { return {a.re + b.re, a.im + b.im}; }
+// Scaled complex division (robust like libgcc's __divdc3 for finite inputs).
+__device__ __forceinline__ cd cdiv(cd a, cd b) {
+  if (b.im == 0.0) return {a.re / b.re, a.im / b.re};
+  if (fabs(b.re) >= fabs(b.im)) {
+    const double r = b.im / b.re, den = b.re + b.im * r;
+    return {(a.re + a.im * r) / den, (a.im - a.re * r) / den};
+  }
+  const double r = b.re / b.im, den = b.re * r + b.im;
+  return {(a.re * r + a.im) / den, (a.im * r - a.re) / den};
+}
+
 }  // namespace iptb

@@ -3,8 +3,9 @@
 //
 // HBM layout (per rank):
 //   Delta : rows_pad x ld, row-major, zero-padded (ld = round_up(n,16), rows_pad = round_up(n,128)).
-//           Complex inputs use the K-concatenated forms A1 = [Dr | -Di], A2 = [Di | Dr]
-//           (rows_pad x 2ld) so that W = Delta Z is two real DMMA GEMMs over K = 2ld.
+//           Complex inputs keep A1 = Dr, A2 = Di, A3 = Dr + Di (rows_pad x ld each) so
+//           that W = Delta Z is three real DMMA GEMMs (3M): T1 = Dr Zr, T2 = Di Zi, and
+//           T3 = A3 (Zr + Zi) whose epilogue forms W and applies the complex map.
 //   Z[2]  : ping-pong column blocks, column-major, ldz = ld (real) or 2ld ([re; im] per column),
 //           cols_pad = round_up(ncols,128) columns; this rank owns global columns [col0, col0+ncols).
 //   d     : n, replicated; wd / lam : per local column.
@@ -30,12 +31,12 @@ struct FullProblem {
   int64_t n = 0, ld = 0, rows_pad = 0;
   int64_t col0 = 0, ncols = 0, cols_pad = 0;
   bool cplx = false;
-  DevBuf A1, A2;
+  DevBuf A1, A2, A3;        // real: A1 = Delta; complex: Dr, Di, Dr + Di
   int64_t lda = 0;  // = K of the GEMM
   DevBuf dre, dim;
   DevBuf Z[2];
   int64_t ldz = 0;
-  DevBuf Wre, Wim;          // complex only
+  DevBuf T1, T2, S;         // complex only: Dr Zr, Di Zi, Zr + Zi (cols_pad x ld)
   DevBuf wd, wdi, lam, lami;
   DevBuf partials;
   DevBuf sums;
@@ -139,83 +140,57 @@ __global__ void decide_full_kernel(LoopState* st, const double* __restrict__ sum
 }
 
 // ---- complex correctness path (a16): unfused complex epilogue on W planes ----
-struct cd {
-  double re, im;
-};
-__device__ __forceinline__ cd cmul(cd a, cd b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
-__device__ __forceinline__ cd csub(cd a, cd b) { return {a.re - b.re, a.im - b.im}; }
-__device__ __forceinline__ cd cadd(cd a, cd b) { return {a.re + b.re, a.im + b.im}; }
-// Scaled complex division (robust like libgcc's __divdc3 for finite inputs).
-__device__ __forceinline__ cd cdiv(cd a, cd b) {
-  if (b.im == 0.0) return {a.re / b.re, a.im / b.re};
-  if (fabs(b.re) >= fabs(b.im)) {
-    const double r = b.im / b.re, den = b.re + b.im * r;
-    return {(a.re + a.im * r) / den, (a.im - a.re * r) / den};
-  }
-  const double r = b.re / b.im, den = b.re * r + b.im;
-  return {(a.re * r + a.im) / den, (a.im * r - a.re) / den};
-}
 
 constexpr int kEpiBlocks = 1184;  // fixed grid => fixed element->block map => deterministic sums
 
-__global__ void complex_map_kernel(const double* __restrict__ Zsrc, int64_t ldz, int64_t ld,
-                                   const double* __restrict__ Wre, const double* __restrict__ Wim,
-                                   const double* __restrict__ wdr, const double* __restrict__ wdi,
-                                   const double* __restrict__ dr, const double* __restrict__ di,
-                                   int64_t n, int64_t ncols, int64_t col0, double* __restrict__ Zdst,
-                                   double* __restrict__ partials, const LoopState* state) {
+// K2 (complex): wd_j = sum_k Delta[jg, k] Z[k, j] with Delta = Dr + i Di and Z = Zr + i Zi
+// (planes ld apart in a column of Z); warp per column, fixed lane order + xor tree.
+__global__ void complex_diag_kernel(const double* __restrict__ Dr, const double* __restrict__ Di, int64_t lda,
+                                    const double* __restrict__ Z, int64_t ldz, int64_t ld, int64_t n,
+                                    int64_t ncols, int64_t col0, double* __restrict__ wdr,
+                                    double* __restrict__ wdi, const LoopState* state) {
   if (state != nullptr && state->done) return;
-  __shared__ double red[8][4];
-  double v[4] = {0.0, 0.0, 0.0, 0.0};
-  const int64_t total = n * ncols;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t j = e / n, i = e - j * n;
-    const int64_t jg = col0 + j;
-    const cd z{Zsrc[j * ldz + i], Zsrc[j * ldz + ld + i]};
-    cd f;
-    if (i == jg) {
-      f = {1.0, 0.0};
-    } else {
-      const cd w{Wre[j * ld + i], Wim[j * ld + i]};
-      f = cdiv(csub(cmul(z, cd{wdr[j], wdi[j]}), w), csub(cd{dr[i], di[i]}, cd{dr[jg], di[jg]}));
-    }
-    Zdst[j * ldz + i] = f.re;
-    Zdst[j * ldz + ld + i] = f.im;
-    const cd df = csub(f, z);
-    v[0] += df.re * df.re + df.im * df.im;
-    v[1] += z.re * z.re + z.im * z.im;
-    v[2] += f.re * f.re + f.im * f.im;
-    v[3] = nan_max(v[3], hypot(df.re, df.im));
+  const int lane = threadIdx.x & 31;
+  const int64_t j = blockIdx.x * int64_t(blockDim.x / 32) + (threadIdx.x >> 5);
+  if (j >= ncols) return;
+  const double* ar = Dr + (col0 + j) * lda;
+  const double* ai = Di + (col0 + j) * lda;
+  const double* zr = Z + j * ldz;
+  const double* zi = zr + ld;
+  double sr = 0.0, si = 0.0;
+  for (int64_t k = lane; k < n; k += 32) {
+    const double a = __ldg(ar + k), b = __ldg(ai + k), x = zr[k], y = zi[k];
+    sr = __fma_rn(a, x, sr);
+    sr = __fma_rn(-b, y, sr);
+    si = __fma_rn(a, y, si);
+    si = __fma_rn(b, x, si);
   }
-  block_reduce4<8>(v, red);
-  if (threadIdx.x == 0) {
-    double* o = partials + size_t(blockIdx.x) * 4;
-    o[0] = v[0]; o[1] = v[1]; o[2] = v[2]; o[3] = v[3];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    sr += __shfl_xor_sync(0xffffffffu, sr, off);
+    si += __shfl_xor_sync(0xffffffffu, si, off);
+  }
+  if (lane == 0) {
+    wdr[j] = sr;
+    wdi[j] = si;
   }
 }
 
-__global__ void complex_resid_kernel(const double* __restrict__ Z, int64_t ldz, int64_t ld,
-                                     const double* __restrict__ Wre, const double* __restrict__ Wim,
-                                     const double* __restrict__ lr, const double* __restrict__ li,
-                                     const double* __restrict__ dr, const double* __restrict__ di,
-                                     int64_t n, int64_t ncols, double* __restrict__ partials) {
-  __shared__ double red[8][4];
-  double v[4] = {0.0, 0.0, 0.0, 0.0};
-  const int64_t total = n * ncols;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t j = e / n, i = e - j * n;
-    const cd z{Z[j * ldz + i], Z[j * ldz + ld + i]};
-    const cd w{Wre[j * ld + i], Wim[j * ld + i]};
-    const cd r = csub(cadd(cmul(cd{dr[i], di[i]}, z), w), cmul(z, cd{lr[j], li[j]}));
-    v[0] += r.re * r.re + r.im * r.im;
+// S[:, j] = Zr[:, j] + Zi[:, j] over the padded ld rows (the B operand of the T3 GEMM).
+__global__ void plane_sum_kernel(const double* __restrict__ Z, int64_t ldz, int64_t ld, int64_t ncols,
+                                 double* __restrict__ S, const LoopState* state) {
+  if (state != nullptr && state->done) return;
+  const int64_t total = ld * ncols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = e / ld, i = e - j * ld;
+    S[j * ld + i] = Z[j * ldz + i] + Z[j * ldz + ld + i];
   }
-  block_reduce4<8>(v, red);
-  if (threadIdx.x == 0) {
-    double* o = partials + size_t(blockIdx.x) * 4;
-    o[0] = v[0]; o[1] = 0.0; o[2] = 0.0; o[3] = 0.0;
-  }
+}
+
+__global__ void add_planes_kernel(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ c,
+                                  int64_t count) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < count; e += int64_t(gridDim.x) * blockDim.x)
+    c[e] = a[e] + b[e];
 }
 
 __global__ void complex_lambda_kernel(const double* wdr, const double* wdi, const double* dr,
@@ -559,7 +534,49 @@ GemmParams gemm_params(FullProblem& P, const double* A, const double* Bz, double
 
 int64_t num_partials(const FullProblem& P) {
   if (P.sparse) return spmm_grid();
-  return P.cplx ? kEpiBlocks : static_cast<int64_t>(gemm_tiles(P.n, P.ncols));
+  return static_cast<int64_t>(gemm_tiles(P.n, P.ncols));
+}
+
+// Complex 3M product for the current Z (zs): wd (K2), S = Zr + Zi, T1 = Dr Zr, T2 = Di Zi,
+// then the T3 GEMM with the complex epilogue `mode` (map into zd, or the residual).
+void launch_complex_products(FullProblem& P, const double* zs, double* zd, int mode, const LoopState* st,
+                             cudaEvent_t ev_a, cudaEvent_t ev_b) {
+  Ctx& c = *P.ctx;
+  const unsigned gd = static_cast<unsigned>(ceil_div(P.ncols, 8));
+  if (gd == 0) return;
+  complex_diag_kernel<<<gd, 256, 0, c.stream>>>(P.A1.get(), P.A2.get(), P.lda, zs, P.ldz, P.ld, P.n, P.ncols,
+                                                P.col0, P.wd.get(), P.wdi.get(), st);
+  plane_sum_kernel<<<1184, 256, 0, c.stream>>>(zs, P.ldz, P.ld, P.ncols, P.S.get(), st);
+  IPT_LAUNCH_CHECK();
+  count_launch(2);
+  if (mode == kGemmResidC) {
+    complex_lambda_kernel<<<static_cast<unsigned>(ceil_div(P.ncols, 256)), 256, 0, c.stream>>>(
+        P.wd.get(), P.wdi.get(), P.dre.get(), P.dim.get(), P.ncols, P.col0, P.lam.get(), P.lami.get());
+    IPT_LAUNCH_CHECK();
+    count_launch();
+  }
+  if (ev_a) IPT_CUDA(cudaEventRecord(ev_a, c.stream));
+  GemmParams g1 = gemm_params(P, P.A1.get(), zs, P.T1.get(), P.ld);
+  g1.state = st;
+  launch_gemm(kGemmStore, g1, c.stream);
+  GemmParams g2 = gemm_params(P, P.A2.get(), zs + P.ld, P.T2.get(), P.ld);
+  g2.state = st;
+  launch_gemm(kGemmStore, g2, c.stream);
+  GemmParams g3 = gemm_params(P, P.A3.get(), P.S.get(), zd, P.ldz);
+  g3.ldb = P.ld;
+  g3.state = st;
+  g3.T1 = P.T1.get();
+  g3.T2 = P.T2.get();
+  g3.ldt = P.ld;
+  g3.zre = zs;
+  g3.zim = zs + P.ld;
+  g3.ldzz = P.ldz;
+  g3.wdi = P.wdi.get();
+  g3.di = P.dim.get();
+  g3.lami = P.lami.get();
+  g3.Cim = zd ? zd + P.ld : nullptr;
+  launch_gemm(mode, g3, c.stream);
+  if (ev_b) IPT_CUDA(cudaEventRecord(ev_b, c.stream));
 }
 
 void allreduce_sums(FullProblem& P, bool with_max) {
@@ -596,17 +613,7 @@ void enqueue_map(FullProblem& P, int k, const ipt_params& prm, cudaEvent_t ev_a 
     }
     if (ev_b) IPT_CUDA(cudaEventRecord(ev_b, c.stream));
   } else {
-    launch_diag(P, P.A1.get(), zs, P.wd.get(), nullptr, nullptr, st);
-    launch_diag(P, P.A2.get(), zs, P.wdi.get(), nullptr, nullptr, st);
-    GemmParams g1 = gemm_params(P, P.A1.get(), zs, P.Wre.get(), P.ld);
-    launch_gemm(kGemmStore, g1, c.stream);
-    GemmParams g2 = gemm_params(P, P.A2.get(), zs, P.Wim.get(), P.ld);
-    launch_gemm(kGemmStore, g2, c.stream);
-    complex_map_kernel<<<kEpiBlocks, 256, 0, c.stream>>>(
-        zs, P.ldz, P.ld, P.Wre.get(), P.Wim.get(), P.wd.get(), P.wdi.get(), P.dre.get(),
-        P.dim.get(), P.n, P.ncols, P.col0, zd, P.partials.get(), st);
-    IPT_LAUNCH_CHECK();
-    count_launch();
+    launch_complex_products(P, zs, zd, kGemmMapC, st, ev_a, ev_b);
   }
   reduce_partials(c.stream, P.partials.get(), num_partials(P), P.sums.get(), st);
   allreduce_sums(P, true);
@@ -645,8 +652,8 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
   if (d_im) for (int64_t i = 0; i < n && !any_im; ++i) any_im = d_im[i] != 0.0;
   if (delta_im) for (int64_t t = 0; t < n * n && !any_im; ++t) any_im = delta_im[t] != 0.0;
   P->cplx = any_im || force_complex;
-  P->lda = P->cplx ? 2 * P->ld : P->ld;
-  P->ldz = P->lda;
+  P->lda = P->ld;                          // K of every real GEMM
+  P->ldz = P->cplx ? 2 * P->ld : P->ld;    // Z columns: [re] or [re; im]
   cudaStream_t s = c.stream;
 
   ProfMarks pm("full_upload");
@@ -656,23 +663,16 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
     h2d_rows(c, P->A1.get(), P->lda, delta_re, n, n, n);  // pinned, double-buffered
     pm.mark("h2d");
   } else {
+    // A1 = Dr, A2 = Di, A3 = Dr + Di (zero padded): the operands of the 3M product
+    h2d_rows(c, P->A1.get(), P->lda, delta_re, n, n, n);
     P->A2.alloc(size_t(P->rows_pad) * P->lda);
-    // A1 = [Dr | -Di], A2 = [Di | Dr]
-    upload_rowmajor(s, P->A1.get(), P->lda, delta_re, n, n, n);
-    upload_rowmajor(s, P->A2.get() + P->ld, P->lda, delta_re, n, n, n);
-    if (delta_im) {
-      upload_rowmajor(s, P->A2.get(), P->lda, delta_im, n, n, n);
-      DevBuf tmp;
-      tmp.alloc(size_t(n) * n, false);
-      IPT_CUDA(cudaMemcpyAsync(tmp.get(), delta_im, sizeof(double) * n * n, cudaMemcpyHostToDevice, s));
-      DevBuf neg;
-      neg.alloc(size_t(n) * n, false);
-      scale_copy(s, tmp.get(), neg.get(), size_t(n) * n, -1.0);
-      IPT_CUDA(cudaMemcpy2DAsync(P->A1.get() + P->ld, P->lda * sizeof(double), neg.get(),
-                                 n * sizeof(double), n * sizeof(double), n,
-                                 cudaMemcpyDeviceToDevice, s));
-      c.sync();
-    }
+    if (delta_im) h2d_rows(c, P->A2.get(), P->lda, delta_im, n, n, n);
+    P->A3.alloc(size_t(P->rows_pad) * P->lda, false);
+    const int64_t cnt = P->rows_pad * P->lda;
+    add_planes_kernel<<<1184, 256, 0, s>>>(P->A1.get(), P->A2.get(), P->A3.get(), cnt);
+    IPT_LAUNCH_CHECK();
+    count_launch();
+    pm.mark("h2d");
   }
   P->dre.alloc(n);
   P->dim.alloc(n);
@@ -681,8 +681,9 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
   for (auto& z : P->Z) z.alloc(size_t(P->cols_pad) * P->ldz);
   pm.mark("alloc_z");
   if (P->cplx) {
-    P->Wre.alloc(size_t(P->cols_pad) * P->ld);
-    P->Wim.alloc(size_t(P->cols_pad) * P->ld);
+    P->T1.alloc(size_t(P->cols_pad) * P->ld);
+    P->T2.alloc(size_t(P->cols_pad) * P->ld);
+    P->S.alloc(size_t(P->cols_pad) * P->ld);
   }
   P->wd.alloc(P->cols_pad);
   P->wdi.alloc(P->cols_pad);
@@ -915,26 +916,7 @@ void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
     g.state = nullptr;
     launch_gemm(kGemmResid, g, s);
   } else {
-    launch_diag(P, P.A1.get(), z, P.wd.get(), nullptr, nullptr, nullptr);
-    launch_diag(P, P.A2.get(), z, P.wdi.get(), nullptr, nullptr, nullptr);
-    const unsigned gl = static_cast<unsigned>(ceil_div(P.ncols, 256));
-    if (gl) {
-      complex_lambda_kernel<<<gl, 256, 0, s>>>(P.wd.get(), P.wdi.get(), P.dre.get(), P.dim.get(),
-                                               P.ncols, P.col0, P.lam.get(), P.lami.get());
-      IPT_LAUNCH_CHECK();
-      count_launch();
-    }
-    GemmParams g1 = gemm_params(P, P.A1.get(), z, P.Wre.get(), P.ld);
-    g1.state = nullptr;
-    launch_gemm(kGemmStore, g1, s);
-    GemmParams g2 = gemm_params(P, P.A2.get(), z, P.Wim.get(), P.ld);
-    g2.state = nullptr;
-    launch_gemm(kGemmStore, g2, s);
-    complex_resid_kernel<<<kEpiBlocks, 256, 0, s>>>(z, P.ldz, P.ld, P.Wre.get(), P.Wim.get(),
-                                                     P.lam.get(), P.lami.get(), P.dre.get(),
-                                                     P.dim.get(), P.n, P.ncols, P.partials.get());
-    IPT_LAUNCH_CHECK();
-    count_launch();
+    launch_complex_products(P, z, nullptr, kGemmResidC, nullptr, nullptr, nullptr);
   }
   reduce_partials(s, P.partials.get(), num_partials(P), P.sums.get(), nullptr);
   allreduce_sums(P, false);
@@ -1118,7 +1100,7 @@ void full_run_maps(FullProblem& P, int count, double* ms_total, double* ms_gemm)
   IPT_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
   *ms_total = ms;
   double g = 0.0;
-  for (int i = 0; i < count && (!P.cplx || P.sparse); ++i) {
+  for (int i = 0; i < count; ++i) {
     IPT_CUDA(cudaEventElapsedTime(&ms, ev[2 + 2 * i], ev[3 + 2 * i]));
     g += ms;
   }

@@ -534,20 +534,6 @@ __global__ void cmatvec_csr_kernel(const int64_t* __restrict__ rowptr, const int
   yi[row0 + r] = si;
 }
 
-struct cd {
-  double re, im;
-};
-__device__ __forceinline__ cd cmul(cd a, cd b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
-__device__ __forceinline__ cd csub(cd a, cd b) { return {a.re - b.re, a.im - b.im}; }
-__device__ __forceinline__ cd cdiv(cd a, cd b) {
-  if (b.im == 0.0) return {a.re / b.re, a.im / b.re};
-  if (fabs(b.re) >= fabs(b.im)) {
-    const double r = b.im / b.re, den = b.re + b.im * r;
-    return {(a.re + a.im * r) / den, (a.im - a.re * r) / den};
-  }
-  const double r = b.re / b.im, den = b.re * r + b.im;
-  return {(a.re * r + a.im) / den, (a.im * r - a.re) / den};
-}
 
 // mode 1: map ; mode 2: final residual. Fixed grid => deterministic partials.
 __global__ void cmap_kernel(int mode, const double* __restrict__ zr, const double* __restrict__ zi,
