@@ -133,6 +133,25 @@ int ipt_apply_map_full_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const do
                            const double* val_im, const double* z_re, const double* z_im,
                            double* f_re, double* f_im);
 
+/* ---- dense LU with partial pivoting: lu_factor / lu_solve / lu_solve_adjoint /
+ * lu_solve_matrix (lu.cpp:10-104), the factorisation behind refine_spectrum
+ * (refine.cpp:61-106) and the Anderson normal equations (anderson.cpp:55-79).
+ * a: row-major n x n planar (a_im nullable). The factors stay on the device. */
+typedef struct ipt_lu ipt_lu;
+int ipt_lu_factor(ipt_ctx* ctx, int64_t n, const double* a_re, const double* a_im, ipt_lu** out);
+/* Factors packed the reference's way (L\U row-major, perm[i] = source row of pivoted row i). */
+int ipt_lu_from_host(ipt_ctx* ctx, int64_t n, const double* lu_re, const double* lu_im, const int64_t* perm,
+                     int singular, ipt_lu** out);
+int ipt_lu_info(const ipt_lu* lu, int64_t* n, int* singular);
+int ipt_lu_download(ipt_ctx* ctx, ipt_lu* lu, double* lu_re, double* lu_im, int64_t* perm);
+/* X = A^{-1} B, B and X row-major n x nrhs planar (nrhs = 1: lu_solve). */
+int ipt_lu_solve(ipt_ctx* ctx, ipt_lu* lu, int64_t nrhs, const double* b_re, const double* b_im, double* x_re,
+                 double* x_im);
+/* X = A^{-H} B (lu_solve_adjoint). */
+int ipt_lu_solve_adjoint(ipt_ctx* ctx, ipt_lu* lu, int64_t nrhs, const double* b_re, const double* b_im,
+                         double* x_re, double* x_im);
+void ipt_lu_free(ipt_lu* lu);
+
 /* smallest_singular_value_estimate (solver.cpp:275-297). */
 int ipt_sigma_min(ipt_ctx* ctx, int64_t n, const double* z_re, const double* z_im,
                   int32_t max_iters, double tol, double* out);

@@ -67,6 +67,7 @@ class RefArm(_Arm):
         L = self.lib
         L.ref_last_error.restype = C.c_char_p
         L.ref_sigma_min.restype = C.c_double
+        L.ref_condition_estimate.restype = C.c_double
 
     def _chk(self, rc):
         if rc != 0:
@@ -162,6 +163,29 @@ class RefArm(_Arm):
         self._chk(self.lib.ref_apply_map_full_csr(C.c_int64(n), _p(_c(d)), rp.ctypes.data_as(_i64p),
                                                   ci.ctypes.data_as(_i64p), _p(va), _p(_c(z)), _p(out)))
         return out
+
+    def lu_factor(self, a):
+        a = _c(a)
+        n = a.shape[0]
+        lu = np.empty((n, n), np.complex128)
+        perm = np.empty(n, np.int64)
+        sing = C.c_int()
+        self._chk(self.lib.ref_lu_factor(C.c_int64(n), _p(a), _p(lu), perm.ctypes.data_as(_i64p), C.byref(sing)))
+        return lu, perm, bool(sing.value)
+
+    def lu_solve(self, a, b, adjoint=False):
+        a = _c(a)
+        b = _c(b)
+        n = a.shape[0]
+        b2 = b.reshape(n, -1)
+        x = np.empty_like(b2)
+        self._chk(self.lib.ref_lu_solve(C.c_int64(n), _p(a), C.c_int64(b2.shape[1]), _p(b2),
+                                        C.c_int(1 if adjoint else 0), _p(x)))
+        return x.reshape(b.shape)
+
+    def condition_estimate(self, a):
+        a = _c(a)
+        return self.lib.ref_condition_estimate(C.c_int64(a.shape[0]), _p(a))
 
     def apply_map_full(self, d, delta, z):
         n = len(d)

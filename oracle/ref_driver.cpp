@@ -160,6 +160,42 @@ REF_API int ref_apply_map_full_csr(int64_t n, const double* d, const int64_t* ro
   });
 }
 
+// Dense LU of the reference (lu.cpp): packed factors, permutation, singular flag.
+REF_API int ref_lu_factor(int64_t n, const double* a, double* lu_out, int64_t* perm_out, int* singular) {
+  return guarded([&] {
+    const LuFactors f = lu_factor(dense_from(a, n, n));
+    from_cvec(f.lu, lu_out);
+    for (int64_t i = 0; i < n; ++i) perm_out[i] = static_cast<int64_t>(f.perm[i]);
+    *singular = f.singular ? 1 : 0;
+  });
+}
+
+// X = A^{-1} B (lu_solve_matrix), B n x r row-major; adjoint != 0: column-wise A^{-H} b.
+REF_API int ref_lu_solve(int64_t n, const double* a, int64_t r, const double* b, int adjoint, double* x_out) {
+  return guarded([&] {
+    const LuFactors f = lu_factor(dense_from(a, n, n));
+    if (!adjoint) {
+      const ComplexMatrix x = lu_solve_matrix(f, dense_from(b, n, r));
+      from_cvec(cvec(x.data(), x.data() + n * r), x_out);
+    } else {
+      const cvec bb = to_cvec(b, n * r);
+      cvec out(n * r);
+      for (int64_t c = 0; c < r; ++c) {
+        cvec col(n);
+        for (int64_t i = 0; i < n; ++i) col[i] = bb[i * r + c];
+        const cvec xc = lu_solve_adjoint(f, col);
+        for (int64_t i = 0; i < n; ++i) out[i * r + c] = xc[i];
+      }
+      from_cvec(out, x_out);
+    }
+  });
+}
+
+REF_API double ref_condition_estimate(int64_t n, const double* a) {
+  const ComplexMatrix m = dense_from(a, n, n);
+  return condition_estimate_1norm(lu_factor(m), m);
+}
+
 // Max-abs stop rule (BASELINE.json configs): Z_{k+1} = apply_map_full(Z_k) until
 // max|Z_{k+1}-Z_k| < tol, divergence tested first on |Z_{k+1}|_F exactly as solve_full
 // does; then the reference's closing product for Lambda and |MZ-ZL|_F.

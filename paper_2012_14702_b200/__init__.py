@@ -10,6 +10,7 @@ from .ipt import (  # noqa: F401
     EigenpairResult,
     InverseGaps,
     IterationConfig,
+    LuFactors,
     Partition,
     SolveStatus,
     SpectrumResult,
@@ -18,6 +19,10 @@ from .ipt import (  # noqa: F401
     build_gaps,
     default_context,
     kernels,
+    lu_factor,
+    lu_solve,
+    lu_solve_adjoint,
+    lu_solve_matrix,
     nccl_unique_id,
     partition,
     reconstruct,

@@ -91,6 +91,13 @@ SIGNATURES = {
     "ipt_full_upload_csr": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, _i32p, _dp, _dp, C.POINTER(_vp)]),
     "ipt_apply_map_full_csr": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, _i32p, _dp, _dp, _dp, _dp,
                                          _dp, _dp]),
+    "ipt_lu_factor": (C.c_int, [_vp, C.c_int64, _dp, _dp, C.POINTER(_vp)]),
+    "ipt_lu_from_host": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, C.c_int, C.POINTER(_vp)]),
+    "ipt_lu_info": (C.c_int, [_vp, _i64p, C.POINTER(C.c_int)]),
+    "ipt_lu_download": (C.c_int, [_vp, _vp, _dp, _dp, _i64p]),
+    "ipt_lu_solve": (C.c_int, [_vp, _vp, C.c_int64, _dp, _dp, _dp, _dp]),
+    "ipt_lu_solve_adjoint": (C.c_int, [_vp, _vp, C.c_int64, _dp, _dp, _dp, _dp]),
+    "ipt_lu_free": (None, [_vp]),
     "ipt_sigma_min": (C.c_int, [_vp, C.c_int64, _dp, _dp, C.c_int32, C.c_double, _dp]),
     "ipt_single_solve_dense": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, _dp, C.c_int64, _dp, _dp,
                                          C.POINTER(Params), _dp, _dp, C.POINTER(Stats)]),

@@ -415,6 +415,66 @@ int ipt_apply_map_full(ipt_ctx* ctx, int64_t n, const double* d_re, const double
   });
 }
 
+// ------------------------------------------------------------------ dense LU
+
+int ipt_lu_factor(ipt_ctx* ctx, int64_t n, const double* a_re, const double* a_im, ipt_lu** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (!out) throw InvalidArgument("lu_factor: null out");
+    *out = reinterpret_cast<ipt_lu*>(lu_factor_device(ctx->c, n, a_re, a_im));
+  });
+}
+
+int ipt_lu_from_host(ipt_ctx* ctx, int64_t n, const double* lu_re, const double* lu_im, const int64_t* perm,
+                     int singular, ipt_lu** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (!out) throw InvalidArgument("lu: null out");
+    *out = reinterpret_cast<ipt_lu*>(lu_from_host(ctx->c, n, lu_re, lu_im, perm, singular != 0));
+  });
+}
+
+int ipt_lu_info(const ipt_lu* lu, int64_t* n, int* singular) {
+  if (!lu) return IPT_ERR_INVALID;
+  const LuProblem& F = *reinterpret_cast<const LuProblem*>(lu);
+  if (n) *n = lu_size(F);
+  if (singular) *singular = lu_singular(F) ? 1 : 0;
+  return IPT_OK;
+}
+
+int ipt_lu_download(ipt_ctx* ctx, ipt_lu* lu, double* lu_re, double* lu_im, int64_t* perm) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!lu) throw InvalidArgument("lu: null factors");
+    DeviceGuard g(ctx->c.device);
+    lu_download(*reinterpret_cast<LuProblem*>(lu), lu_re, lu_im, perm);
+  });
+}
+
+int ipt_lu_solve(ipt_ctx* ctx, ipt_lu* lu, int64_t nrhs, const double* b_re, const double* b_im, double* x_re,
+                 double* x_im) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!lu) throw InvalidArgument("lu_solve: null factors");
+    DeviceGuard g(ctx->c.device);
+    lu_solve_device(*reinterpret_cast<LuProblem*>(lu), nrhs, b_re, b_im, x_re, x_im, false);
+  });
+}
+
+int ipt_lu_solve_adjoint(ipt_ctx* ctx, ipt_lu* lu, int64_t nrhs, const double* b_re, const double* b_im,
+                         double* x_re, double* x_im) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (!lu) throw InvalidArgument("lu_solve_adjoint: null factors");
+    DeviceGuard g(ctx->c.device);
+    lu_solve_device(*reinterpret_cast<LuProblem*>(lu), nrhs, b_re, b_im, x_re, x_im, true);
+  });
+}
+
+void ipt_lu_free(ipt_lu* lu) { lu_free(reinterpret_cast<LuProblem*>(lu)); }
+
 int ipt_sigma_min(ipt_ctx* ctx, int64_t n, const double* z_re, const double* z_im, int32_t max_iters,
                   double tol, double* out) {
   return guarded([&] {

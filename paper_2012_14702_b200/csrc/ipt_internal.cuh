@@ -154,6 +154,18 @@ void single_run_steps(SingleProblem& P, int count, double* ms_total, double* ms_
 void single_accelerated(SingleProblem& P, const ipt_params& prm, int memory, double residual_tol,
                         double regularization, ipt_stats* stats);
 
+// Dense complex LU with partial pivoting (ipt_lu.cu), row-major planar.
+struct LuProblem;
+LuProblem* lu_factor_device(Ctx& c, int64_t n, const double* a_re, const double* a_im);
+LuProblem* lu_from_host(Ctx& c, int64_t n, const double* lu_re, const double* lu_im, const int64_t* perm,
+                        bool singular);
+void lu_free(LuProblem* F);
+int64_t lu_size(const LuProblem& F);
+bool lu_singular(const LuProblem& F);
+void lu_download(LuProblem& F, double* lu_re, double* lu_im, int64_t* perm);
+void lu_solve_device(LuProblem& F, int64_t nrhs, const double* b_re, const double* b_im, double* x_re, double* x_im,
+                     bool adjoint);
+
 // sigma_min (ipt_sigma.cu): Z column-major (ldz), real or complex (zi nullable).
 double sigma_min_device(Ctx& ctx, int64_t n, const double* zr, const double* zi, int64_t ldz,
                         int max_iters, double tol);

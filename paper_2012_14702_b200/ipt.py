@@ -465,6 +465,76 @@ def smallest_singular_value_estimate(z, max_iters: int = 50, tol: float = 1e-4,
     return out.value
 
 
+# ----------------------------------------------------------------- dense LU (lu.hpp)
+
+
+class LuFactors:
+    """PA = LU with unit lower L (lu.hpp): packed `lu` (n x n), `perm[i]` = source row of
+    pivoted row i, `singular`; the factors also stay on the device for the solves."""
+
+    def __init__(self, n, lu, perm, singular, handle, ctx):
+        self.n, self.lu, self.perm, self.singular = n, lu, perm, singular
+        self._h, self._ctx = handle, ctx
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _lib.load().ipt_lu_free(h)
+            except Exception:  # interpreter shutdown
+                pass
+            self._h = None
+
+
+def lu_factor(a, ctx: Optional[Context] = None) -> LuFactors:
+    """lu_factor (lu.cpp:10-49) on the device: partial pivoting by the largest |a_ik|."""
+    a = np.asarray(a)
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise ValueError("lu_factor: matrix must be square")
+    n = a.shape[0]
+    ctx = ctx or default_context()
+    lib = _lib.load()
+    ar, ai = _planar(a)
+    h = C.c_void_p()
+    check(lib.ipt_lu_factor(ctx.handle, n, dptr(ar), dptr(ai), C.byref(h)))
+    sing = C.c_int()
+    check(lib.ipt_lu_info(h, None, C.byref(sing)))
+    lr, li = np.empty((n, n)), np.empty((n, n))
+    perm = np.empty(n, np.int64)
+    check(lib.ipt_lu_download(ctx.handle, h, dptr(lr), dptr(li), i64ptr(perm)))
+    return LuFactors(n, lr + 1j * li, perm, bool(sing.value), h, ctx)
+
+
+def _lu_solve(f: LuFactors, b, adjoint: bool):
+    b = np.asarray(b)
+    if b.shape[0] != f.n:
+        raise ValueError("lu_solve: size mismatch")
+    b2 = b.reshape(f.n, -1)
+    br, bi = _planar(b2)
+    xr, xi = np.empty(b2.shape), np.empty(b2.shape)
+    fn = _lib.load().ipt_lu_solve_adjoint if adjoint else _lib.load().ipt_lu_solve
+    check(fn(f._ctx.handle, f._h, b2.shape[1], dptr(br), dptr(bi), dptr(xr), dptr(xi)))
+    return (xr + 1j * xi).reshape(b.shape)
+
+
+def lu_solve(f: LuFactors, b):
+    """x = A^{-1} b (lu.cpp:51-66)."""
+    return _lu_solve(f, b, False)
+
+
+def lu_solve_adjoint(f: LuFactors, b):
+    """x = A^{-H} b (lu.cpp:68-86)."""
+    return _lu_solve(f, b, True)
+
+
+def lu_solve_matrix(f: LuFactors, b):
+    """A X = B for all columns of B at once (lu.cpp:88-103)."""
+    b = np.asarray(b)
+    if b.ndim != 2:
+        raise ValueError("lu_solve_matrix: matrix right-hand side required")
+    return _lu_solve(f, b, False)
+
+
 # ----------------------------------------------------------------- single pair
 
 

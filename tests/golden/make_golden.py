@@ -256,6 +256,17 @@ def sparse_full():
     save("sparse_full.npz", **out)
 
 
+def lu_case():
+    """lu_factor / lu_solve_matrix (lu.cpp:10-103) on a seeded complex 96 x 96 matrix."""
+    R = oracle.ref()
+    rng = np.random.default_rng(2024)
+    a = rng.standard_normal((96, 96)) + 1j * rng.standard_normal((96, 96))
+    b = rng.standard_normal((96, 5)) + 1j * rng.standard_normal((96, 5))
+    lu, perm, sing = R.lu_factor(a)
+    x = R.lu_solve(a, b)
+    save("lu.npz", a=a, lu=lu, perm=perm, b=b, x=x, singular=np.array([sing]))
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
@@ -263,7 +274,7 @@ if __name__ == "__main__":
     a = ap.parse_args()
     oracle.build()
     jobs = dict(small=small_cases, config1=config1, accel=accelerated, single=lambda: single_configs(a.big),
-                columns=lambda: full_columns(a.big), sparse=sparse_full)
+                columns=lambda: full_columns(a.big), sparse=sparse_full, lu=lu_case)
     for name, fn in jobs.items():
         if a.only and name not in a.only.split(","):
             continue
