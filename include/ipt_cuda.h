@@ -115,6 +115,21 @@ int ipt_apply_map_full(ipt_ctx* ctx, int64_t n, const double* d_re, const double
                        const double* delta_re, const double* delta_im, const double* z_re,
                        const double* z_im, double* f_re, double* f_im);
 
+/* Column block [col_begin, col_end) of the full-spectrum problem on a single-rank
+ * context: the unit a rank iterates under the column sharding, as an independent
+ * sub-problem (the map of a column needs only that column of Z; the stop scalars are
+ * the block's). reset takes the full n x n warm start (its columns are used) or NULL;
+ * iterate / finalize as for the full problem (no sigma_min); the block download writes
+ * Z[:, col_begin:col_end] (n x ncols row-major planar) and its eigenvalues. */
+int ipt_full_upload_columns(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                            const double* delta_re, const double* delta_im, int64_t col_begin,
+                            int64_t col_end, ipt_full_problem** out);
+int ipt_full_upload_csr_columns(ipt_ctx* ctx, int64_t n, const double* d, const int64_t* rowptr,
+                                const int32_t* cols, const double* vals, int64_t col_begin, int64_t col_end,
+                                ipt_full_problem** out);
+int ipt_full_download_block(ipt_ctx* ctx, ipt_full_problem* prob, double* z_re, double* z_im,
+                            double* lam_re, double* lam_im);
+
 /* Sparse Delta (CSR: rowptr[n+1], cols[nnz], vals[nnz]) for the same full-spectrum
  * entry points: solve_full / apply_map_full when Partition::delta is CSR
  * (partition.cpp:43 builds it; kernels.cpp:88-108 multiplies it). A real CSR Delta
@@ -173,6 +188,17 @@ int ipt_single_solve_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const doub
 int ipt_single_upload_dense(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
                             const double* delta_re, const double* delta_im,
                             ipt_single_problem** out);
+/* Row block [row_begin, row_end) on a single-rank context: the rows one rank maps under
+ * the row sharding (every rank keeps the anchor row). Without the all-gather the other
+ * rows of the iterate are not refreshed: run one step from a warm start, or assemble
+ * the blocks' rows on the host between steps. */
+int ipt_single_upload_dense_rows(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                                 const double* delta_re, const double* delta_im, int64_t row_begin,
+                                 int64_t row_end, ipt_single_problem** out);
+int ipt_single_upload_csr_rows(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                               const int64_t* rowptr, const int32_t* cols, const double* val_re,
+                               const double* val_im, int64_t row_begin, int64_t row_end,
+                               ipt_single_problem** out);
 int ipt_single_upload_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
                           const int64_t* rowptr, const int32_t* cols, const double* val_re,
                           const double* val_im, ipt_single_problem** out);

@@ -86,6 +86,11 @@ SIGNATURES = {
     "ipt_full_local_columns": (C.c_int, [_vp, _i64p, _i64p]),
     "ipt_full_free": (None, [_vp]),
     "ipt_apply_map_full": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]),
+    "ipt_full_upload_columns": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, _dp, C.c_int64, C.c_int64,
+                                          C.POINTER(_vp)]),
+    "ipt_full_upload_csr_columns": (C.c_int, [_vp, C.c_int64, _dp, _i64p, _i32p, _dp, C.c_int64, C.c_int64,
+                                              C.POINTER(_vp)]),
+    "ipt_full_download_block": (C.c_int, [_vp, _vp, _dp, _dp, _dp, _dp]),
     "ipt_full_solve_csr": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, _i32p, _dp, _dp, _dp, _dp,
                                      C.POINTER(Params), _dp, _dp, _dp, _dp, C.POINTER(Stats)]),
     "ipt_full_upload_csr": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, _i32p, _dp, _dp, C.POINTER(_vp)]),
@@ -106,6 +111,10 @@ SIGNATURES = {
     "ipt_single_upload_dense": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, _dp, C.POINTER(_vp)]),
     "ipt_single_upload_csr": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, _i32p, _dp, _dp,
                                         C.POINTER(_vp)]),
+    "ipt_single_upload_dense_rows": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, _dp, C.c_int64, C.c_int64,
+                                               C.POINTER(_vp)]),
+    "ipt_single_upload_csr_rows": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, _i32p, _dp, _dp, C.c_int64,
+                                             C.c_int64, C.POINTER(_vp)]),
     "ipt_single_reset": (C.c_int, [_vp, _vp, C.c_int64, _dp, _dp]),
     "ipt_single_iterate": (C.c_int, [_vp, _vp, C.POINTER(Params), C.POINTER(Stats)]),
     "ipt_single_finalize": (C.c_int, [_vp, _vp, C.POINTER(Stats)]),

@@ -299,6 +299,38 @@ int ipt_full_upload(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d
   });
 }
 
+int ipt_full_upload_columns(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                            const double* delta_re, const double* delta_im, int64_t col_begin,
+                            int64_t col_end, ipt_full_problem** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (col_begin < 0) throw InvalidArgument("solve_full: bad column block");
+    *out = reinterpret_cast<ipt_full_problem*>(
+        full_upload(ctx->c, n, d_re, d_im, delta_re, delta_im, false, col_begin, col_end));
+  });
+}
+
+int ipt_full_upload_csr_columns(ipt_ctx* ctx, int64_t n, const double* d, const int64_t* rowptr,
+                                const int32_t* cols, const double* vals, int64_t col_begin, int64_t col_end,
+                                ipt_full_problem** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (col_begin < 0) throw InvalidArgument("solve_full: bad column block");
+    *out = reinterpret_cast<ipt_full_problem*>(full_upload_csr(ctx->c, n, d, rowptr, cols, vals, col_begin, col_end));
+  });
+}
+
+int ipt_full_download_block(ipt_ctx* ctx, ipt_full_problem* prob, double* z_re, double* z_im, double* lam_re,
+                            double* lam_im) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    full_download_block(*reinterpret_cast<FullProblem*>(prob), z_re, z_im, lam_re, lam_im);
+  });
+}
+
 int ipt_full_reset(ipt_ctx* ctx, ipt_full_problem* prob, const double* warm_re, const double* warm_im) {
   return guarded([&] {
     check_ctx(ctx);
@@ -518,6 +550,33 @@ int ipt_single_upload_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const dou
     *out = reinterpret_cast<ipt_single_problem*>(single_upload(ctx->c, n, d_re, d_im, true, nullptr,
                                                                nullptr, rowptr, cols, val_re, val_im,
                                                                false));
+  });
+}
+
+int ipt_single_upload_dense_rows(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                                 const double* delta_re, const double* delta_im, int64_t row_begin,
+                                 int64_t row_end, ipt_single_problem** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (row_begin < 0) throw InvalidArgument("solve_single: bad row block");
+    *out = reinterpret_cast<ipt_single_problem*>(single_upload(ctx->c, n, d_re, d_im, false, delta_re, delta_im,
+                                                               nullptr, nullptr, nullptr, nullptr, true, false,
+                                                               row_begin, row_end));
+  });
+}
+
+int ipt_single_upload_csr_rows(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                               const int64_t* rowptr, const int32_t* cols, const double* val_re,
+                               const double* val_im, int64_t row_begin, int64_t row_end,
+                               ipt_single_problem** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (row_begin < 0) throw InvalidArgument("solve_single: bad row block");
+    *out = reinterpret_cast<ipt_single_problem*>(single_upload(ctx->c, n, d_re, d_im, true, nullptr, nullptr,
+                                                               rowptr, cols, val_re, val_im, false, false,
+                                                               row_begin, row_end));
   });
 }
 

@@ -636,8 +636,24 @@ void upload_rowmajor(cudaStream_t s, double* dst, int64_t dpitch, const double* 
 
 // ------------------------------------------------------------ C++ entry points
 
+// This rank's column block: the communicator's shard, or an explicit [begin, end)
+// on a single-rank context (a column block is an independent sub-problem of the map).
+static void column_block(const Ctx& c, int64_t n, int64_t begin, int64_t end, int64_t& col0, int64_t& ncols) {
+  if (begin < 0) {
+    int64_t c1 = 0;
+    c.shard(n, col0, c1);
+    ncols = c1 - col0;
+    return;
+  }
+  if (c.nranks != 1) throw InvalidArgument("solve_full: explicit column blocks need a single-rank context");
+  if (!(begin < end && end <= n)) throw InvalidArgument("solve_full: bad column block");
+  col0 = begin;
+  ncols = end - begin;
+}
+
 FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_im,
-                         const double* delta_re, const double* delta_im, bool force_complex) {
+                         const double* delta_re, const double* delta_im, bool force_complex,
+                         int64_t col_begin, int64_t col_end) {
   if (n <= 0) throw InvalidArgument("solve_full: empty problem");
   if (!d_re || !delta_re) throw InvalidArgument("solve_full: null input");
   auto P = std::make_unique<FullProblem>();
@@ -645,8 +661,7 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
   P->n = n;
   P->ld = round_up(n, 16);
   P->rows_pad = round_up(n, kBM);
-  c.shard(n, P->col0, P->ncols);
-  P->ncols -= P->col0;
+  column_block(c, n, col_begin, col_end, P->col0, P->ncols);
   P->cols_pad = round_up(std::max<int64_t>(P->ncols, 1), kBN);
   bool any_im = false;
   if (d_im) for (int64_t i = 0; i < n && !any_im; ++i) any_im = d_im[i] != 0.0;
@@ -712,7 +727,7 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
 
 // Real CSR Delta (rowptr[n+1] with any base, cols in [0, n)): the sparse map path.
 FullProblem* full_upload_csr(Ctx& c, int64_t n, const double* d, const int64_t* rowptr,
-                             const int32_t* cols, const double* vals) {
+                             const int32_t* cols, const double* vals, int64_t col_begin, int64_t col_end) {
   if (n <= 0) throw InvalidArgument("solve_full: empty problem");
   if (!d || !rowptr) throw InvalidArgument("solve_full: null input");
   const int64_t b = rowptr[0], nnz = rowptr[n] - rowptr[0];
@@ -726,8 +741,7 @@ FullProblem* full_upload_csr(Ctx& c, int64_t n, const double* d, const int64_t* 
   P->n = n;
   P->ld = round_up(n, 16);
   P->rows_pad = round_up(n, kBM);
-  c.shard(n, P->col0, P->ncols);
-  P->ncols -= P->col0;
+  column_block(c, n, col_begin, col_end, P->col0, P->ncols);
   P->cols_pad = round_up(std::max<int64_t>(P->ncols, 1), kBN);
   P->cplx = false;
   P->sparse = true;
@@ -952,7 +966,7 @@ void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
 
   double sig = 0.0;
   float ms_sigma = 0.f;
-  if (prm.want_sigma_min && c.rank == 0) {
+  if (prm.want_sigma_min && c.rank == 0 && (c.nranks > 1 || P.ncols == P.n)) {
     const double* zfull = c.nranks > 1 ? P.gathered.get() : z;
     IPT_CUDA(cudaEventRecord(c.ev[2], s));
     sig = sigma_min_device(c, P.n, zfull, P.cplx ? zfull + P.ld : nullptr, P.ldz, 50, 1e-4);
@@ -970,9 +984,43 @@ void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
   }
 }
 
+// Single-rank column block [col0, col0 + ncols): Z block (n x ncols, row-major planar)
+// and its eigenvalues.
+void full_download_block(FullProblem& P, double* z_re, double* z_im, double* lam_re, double* lam_im) {
+  Ctx& c = *P.ctx;
+  if (c.nranks != 1) throw InvalidArgument("download: column blocks are single-rank");
+  cudaStream_t s = c.stream;
+  IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
+  c.sync();
+  const int64_t n = P.n, nc = P.ncols;
+  std::vector<double> lr(nc), li(nc);
+  IPT_CUDA(cudaMemcpyAsync(lr.data(), P.lam.get(), sizeof(double) * nc, cudaMemcpyDeviceToHost, s));
+  IPT_CUDA(cudaMemcpyAsync(li.data(), P.lami.get(), sizeof(double) * nc, cudaMemcpyDeviceToHost, s));
+  c.sync();
+  if (lam_re) std::memcpy(lam_re, lr.data(), sizeof(double) * nc);
+  if (lam_im) {
+    if (P.cplx) std::memcpy(lam_im, li.data(), sizeof(double) * nc);
+    else std::memset(lam_im, 0, sizeof(double) * nc);
+  }
+  const double* zsrc = final_colmajor_z(P);
+  DevBuf rm;
+  rm.alloc(size_t(n) * nc, false);
+  for (int part = 0; part < 2; ++part) {
+    double* dst = part == 0 ? z_re : z_im;
+    if (dst == nullptr) continue;
+    if (part == 1 && !P.cplx) {
+      std::memset(dst, 0, sizeof(double) * n * nc);
+      continue;
+    }
+    transpose_to_rowmajor(s, zsrc + (part ? P.ld : 0), P.ldz, n, nc, rm.get(), nc);
+    d2h_rows(c, dst, nc, rm.get(), nc, n, nc);
+  }
+}
+
 // Z (row-major planar) and eigenvalues to the host; rank 0 receives everything.
 void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, double* lam_im) {
   Ctx& c = *P.ctx;
+  if (c.nranks == 1 && P.ncols != P.n) throw InvalidArgument("download: column block problem (use the block download)");
   cudaStream_t s = c.stream;
   IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
   c.sync();
@@ -1035,7 +1083,7 @@ void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, d
 
 bool full_is_complex(const FullProblem& P) { return P.cplx; }
 
-bool full_can_download_early(const FullProblem& P) { return P.ctx->nranks == 1 && !P.sparse; }
+bool full_can_download_early(const FullProblem& P) { return P.ctx->nranks == 1 && !P.sparse && P.ncols == P.n; }
 
 // Main thread, before full_finalize: transpose the final Z into row-major staging
 // buffers on ctx.stream (a few ms; a kernel on a second stream would starve behind

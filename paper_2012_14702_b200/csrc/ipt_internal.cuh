@@ -117,9 +117,12 @@ void release_staging(Ctx& c);
 // Full-spectrum problem (ipt_full.cu)
 struct FullProblem;
 FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_im,
-                         const double* delta_re, const double* delta_im, bool force_complex = false);
+                         const double* delta_re, const double* delta_im, bool force_complex = false,
+                         int64_t col_begin = -1, int64_t col_end = -1);
 FullProblem* full_upload_csr(Ctx& c, int64_t n, const double* d, const int64_t* rowptr,
-                             const int32_t* cols, const double* vals);
+                             const int32_t* cols, const double* vals, int64_t col_begin = -1,
+                             int64_t col_end = -1);
+void full_download_block(FullProblem& P, double* z_re, double* z_im, double* lam_re, double* lam_im);
 bool full_is_sparse(const FullProblem& P);
 void full_free(FullProblem* P);
 void full_reset(FullProblem& P, const double* warm_re, const double* warm_im, int max_iter_hint,
@@ -142,7 +145,8 @@ struct SingleProblem;
 SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double* d_im, bool csr,
                              const double* dense_re, const double* dense_im, const int64_t* rowptr,
                              const int32_t* cols, const double* val_re, const double* val_im,
-                             bool keep_host_anchor_source, bool force_complex = false);
+                             bool keep_host_anchor_source, bool force_complex = false, int64_t row_begin = -1,
+                             int64_t row_end = -1);
 void single_free(SingleProblem* P);
 void single_reset(SingleProblem& P, int64_t anchor, const double* warm_re, const double* warm_im,
                   int max_iter_hint, bool renormalize = true);

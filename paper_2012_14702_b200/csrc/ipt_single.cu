@@ -774,7 +774,8 @@ void upload_anchor_row(SingleProblem& P) {
 SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double* d_im, bool csr,
                              const double* dense_re, const double* dense_im, const int64_t* rowptr,
                              const int32_t* cols, const double* val_re, const double* val_im,
-                             bool keep_host_anchor_source, bool force_complex) {
+                             bool keep_host_anchor_source, bool force_complex, int64_t row_begin,
+                             int64_t row_end) {
   if (n <= 0) throw InvalidArgument("solve_single: empty problem");
   auto P = std::make_unique<SingleProblem>();
   P->ctx = &c;
@@ -788,6 +789,12 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
   P->chunk = ceil_div(n, c.nranks);
   P->r0 = std::min<int64_t>(n, c.rank * P->chunk);
   P->r1 = std::min<int64_t>(n, (c.rank + 1) * P->chunk);
+  if (row_begin >= 0) {  // explicit row block on a single-rank context (the unit a rank maps)
+    if (c.nranks != 1) throw InvalidArgument("solve_single: explicit row blocks need a single-rank context");
+    if (!(row_begin < row_end && row_end <= n)) throw InvalidArgument("solve_single: bad row block");
+    P->r0 = row_begin;
+    P->r1 = row_end;
+  }
   const int64_t rows = P->r1 - P->r0;
   const int64_t vlen = P->chunk * c.nranks;
   cudaStream_t s = c.stream;
