@@ -9,6 +9,8 @@
 //   Z[2]  : ping-pong column blocks, column-major, ldz = ld (real) or 2ld ([re; im] per column),
 //           cols_pad = round_up(ncols,128) columns; this rank owns global columns [col0, col0+ncols).
 //   d     : n, replicated; wd / lam : per local column.
+//   Sparse real Delta (CSR, f2): int64 row offsets, int32 columns, fp64 values; Z[2]
+//           hold the local columns ROW-major during the loop (see FullProblem).
 // Per iteration: K2 diag pre-pass (wd_j = (Delta Z)_jj), K1 DMMA GEMM with the fused map
 // epilogue writing F(Z) into the other Z buffer and per-CTA partial sums, a fixed-order
 // reduction, [NCCL all-reduce of 3 sums + 1 max], and a single-thread decide kernel
@@ -139,9 +141,9 @@ __global__ void decide_full_kernel(LoopState* st, const double* __restrict__ sum
   }
 }
 
-// ---- complex correctness path (a16): unfused complex epilogue on W planes ----
+// ---- complex full spectrum (a16/f3): K2 pre-pass and operand preparation of the 3M product ----
 
-constexpr int kEpiBlocks = 1184;  // fixed grid => fixed element->block map => deterministic sums
+constexpr int kEpiBlocks = 1184;  // cap of the persistent sparse-map grid (8 CTAs x 148 SMs)
 
 // K2 (complex): wd_j = sum_k Delta[jg, k] Z[k, j] with Delta = Dr + i Di and Z = Zr + i Zi
 // (planes ld apart in a column of Z); warp per column, fixed lane order + xor tree.
