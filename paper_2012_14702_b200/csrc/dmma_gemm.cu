@@ -73,6 +73,8 @@ void launch_gemm(int mode, const GemmParams& p, cudaStream_t s) {
     case kGemmSub: launch_mode<kGemmSub>(p, s); break;
     case kGemmMapC: launch_mode<kGemmMapC>(p, s); break;
     case kGemmResidC: launch_mode<kGemmResidC>(p, s); break;
+    case kGemmSubC: launch_mode<kGemmSubC>(p, s); break;
+    case kGemmSubAll: launch_mode<kGemmSubAll>(p, s); break;
     default: throw InvalidArgument("launch_gemm: bad mode");
   }
 }

@@ -39,7 +39,16 @@
 
 namespace iptb {
 
-enum GemmMode : int { kGemmStore = 0, kGemmMap = 1, kGemmResid = 2, kGemmSub = 3, kGemmMapC = 4, kGemmResidC = 5 };
+enum GemmMode : int {
+  kGemmStore = 0,
+  kGemmMap = 1,
+  kGemmResid = 2,
+  kGemmSub = 3,
+  kGemmMapC = 4,
+  kGemmResidC = 5,
+  kGemmSubC = 6,   // complex C -= W with W from T1, T2 and this launch's T3 (3M), C / Cim planes
+  kGemmSubAll = 7  // C -= W on every tile (general, not a symmetric lower update)
+};
 
 constexpr int kBM = 128;
 constexpr int kBN = 128;
@@ -152,7 +161,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmParams& p, double (&acc)
                                               int64_t n0, int warp, int lane, double v[4]) {
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;
-  if (MODE == kGemmStore || MODE == kGemmSub) {
+  if (MODE == kGemmStore || MODE == kGemmSub || MODE == kGemmSubAll) {
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -164,7 +173,24 @@ __device__ __forceinline__ void gemm_epilogue(const GemmParams& p, double (&acc)
           if (i < p.n_rows && j < p.n_cols) {
             double* cp = p.C + j * p.ldc + i;
             if (MODE == kGemmStore) *cp = acc[mi][ni][r];
-            else *cp = __dsub_rn(*cp, acc[mi][ni][r]);
+            else *cp = __dsub_rn(*cp, acc[mi][ni][r]);  // kGemmSub, kGemmSubAll
+          }
+        }
+    return;
+  }
+  if (MODE == kGemmSubC) {
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int64_t i = m0 + wm * 64 + mi * 16 + g + ((r >> 1) << 3);
+          const int64_t j = n0 + wn * 32 + ni * 8 + 2 * t + (r & 1);
+          if (i < p.n_rows && j < p.n_cols) {
+            const double t1 = p.T1[j * p.ldt + i], t2 = p.T2[j * p.ldt + i];
+            p.C[j * p.ldc + i] -= t1 - t2;
+            p.Cim[j * p.ldc + i] -= acc[mi][ni][r] - t1 - t2;
           }
         }
     return;
@@ -361,7 +387,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) mbar_arrive(&empty[s]);
   }
   gemm_epilogue<MODE>(p, acc, m0, n0, warp, lane, v);
-  if (MODE == kGemmStore || MODE == kGemmSub) return;
+  if (MODE == kGemmStore || MODE == kGemmSub || MODE == kGemmSubC || MODE == kGemmSubAll) return;
   block_reduce4<kConsumerWarps>(v, red);
   if (threadIdx.x == 0) {
     double* out = p.partials + size_t(blockIdx.x) * 4;

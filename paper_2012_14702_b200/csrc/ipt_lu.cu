@@ -6,20 +6,26 @@
 // Layout: planar (re, im) row-major n x n, the packed L\U of the reference (unit L
 // below the diagonal, U on and above), plus perm[i] = source row of pivoted row i.
 //
-// Factor: the reference's right-looking elimination, one column step at a time, with
-// no host round trip per step (pivot index and the skip flag live on the device):
+// Factor: the reference's right-looking elimination (pivot = first largest |a_ik|),
+// blocked by panels of 64 columns, with no host round trip (pivot index and the skip
+// flag live on the device). Per column k of a panel:
 //   K_piv   one CTA: largest |a_ik| over i >= k, first index on ties (the reference's
 //           strict > scan); a pivot <= max|A| * eps * n marks the matrix singular and
 //           the column is skipped, as lu.cpp:27-31 does;
 //   K_swap  full-row swap k <-> piv (L part included) and the permutation;
 //   K_mult  multipliers m_i = a_ik / a_kk into column k;
-//   K_upd   a_ij -= m_i a_kj over the trailing block (rows with m_i == 0 untouched).
-// Every element sees the same sequence of updates as in lu.cpp, so the factors agree
-// with the reference's to rounding (complex division / FMA contraction may differ).
+//   K_upd   a_ij -= m_i a_kj on the panel columns (all rows below).
+// After the panel: the U rows to its right by the same column steps (after all of the
+// panel's row swaps, so swapped rows are in the same state), then ONE trailing update
+// A22 -= L21 U12 on the DMMA GEMM (complex cgemm_sub_rowmajor). Pivots, L and U
+// entries of the panel see exactly the reference's update sequence; A22 receives each
+// panel's rank-64 sum at once, so the factors agree with the reference's to rounding
+// (identical pivot sequences in the tests).
 //
-// Solves: column sweeps over all right-hand sides at once (X row-major n x nrhs):
-// forward x_i -= L_ij x_j (unit L), backward x_j /= U_jj then x_i -= U_ij x_j; the
-// adjoint solve runs U^H then L^H the same way (lu.cpp:68-86).
+// Solves over all right-hand sides at once (X row-major n x nrhs): column sweeps
+// x_i -= L_ij x_j (unit L) and x_j /= U_jj, x_i -= U_ij x_j; with >= 8 right-hand sides
+// the sweeps stay inside 64-row panels and the rest of X is updated by the DMMA GEMM.
+// The adjoint solve runs U^H then L^H by column sweeps (lu.cpp:68-86).
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
@@ -27,6 +33,7 @@
 #include <utility>
 #include <vector>
 
+#include "dmma_gemm.cuh"
 #include "ipt_internal.cuh"
 
 namespace iptb {
@@ -37,6 +44,7 @@ struct LuProblem {
   DevBuf re, im;   // packed L\U planes
   std::unique_ptr<int64_t, void (*)(void*)> perm{nullptr, [](void* p) { cudaFree(p); }};
   std::unique_ptr<int, void (*)(void*)> flags{nullptr, [](void* p) { cudaFree(p); }};  // [0] singular, [1] skip, [2] piv
+  std::unique_ptr<int, void (*)(void*)> skipped{nullptr, [](void* p) { cudaFree(p); }};  // per column: pivot skipped
   bool singular = false;
 };
 
@@ -62,7 +70,8 @@ __global__ void lu_init_perm_kernel(int64_t* perm, int64_t n) {
 
 // One CTA of 1024 threads: pivot search for column k.
 __global__ void __launch_bounds__(1024) lu_pivot_kernel(const double* __restrict__ re, const double* __restrict__ im,
-                                                        int64_t n, int64_t k, const double* tiny_p, int* flags) {
+                                                        int64_t n, int64_t k, const double* tiny_p, int* flags,
+                                                        int* skipped) {
   __shared__ double bv[32];
   __shared__ int64_t bi[32];
   const double diag = hypot(re[k * n + k], im[k * n + k]);
@@ -108,6 +117,7 @@ __global__ void __launch_bounds__(1024) lu_pivot_kernel(const double* __restrict
     const bool skip = pbest <= *tiny_p;  // lu.cpp:27 (a NaN pivot is not skipped)
     flags[1] = skip ? 1 : 0;
     flags[2] = static_cast<int>(piv);
+    skipped[k] = skip ? 1 : 0;
     if (skip) flags[0] = 1;
   }
 }
@@ -143,13 +153,14 @@ __global__ void lu_mult_kernel(double* re, double* im, int64_t n, int64_t k, con
   }
 }
 
-// a_ij -= m_i a_kj, i, j > k; a 2D grid of 32-column x 8-row tiles.
-__global__ void lu_update_kernel(double* re, double* im, int64_t n, int64_t k, const int* flags) {
-  if (flags[1]) return;
-  const int64_t j = k + 1 + blockIdx.x * int64_t(32) + threadIdx.x;
-  if (j >= n) return;
+// a_ij -= m_i a_kj over rows [i0, i1) x columns [j0, j1) (all > k); 32-column x 8-row tiles.
+__global__ void lu_update_kernel(double* re, double* im, int64_t n, int64_t k, int64_t i0, int64_t i1, int64_t j0,
+                                 int64_t j1, const int* skip) {
+  if (*skip) return;
+  const int64_t j = j0 + blockIdx.x * int64_t(32) + threadIdx.x;
+  if (j >= j1) return;
   const cd u{re[k * n + j], im[k * n + j]};
-  for (int64_t i = k + 1 + blockIdx.y * int64_t(blockDim.y) + threadIdx.y; i < n; i += int64_t(gridDim.y) * blockDim.y) {
+  for (int64_t i = i0 + blockIdx.y * int64_t(blockDim.y) + threadIdx.y; i < i1; i += int64_t(gridDim.y) * blockDim.y) {
     const cd m{re[i * n + k], im[i * n + k]};
     if (m.re == 0.0 && m.im == 0.0) continue;  // lu.cpp:44
     const cd t = cmul(m, u);
@@ -222,6 +233,99 @@ void sweep(cudaStream_t s, const LuProblem& F, double* wr, double* wi, double* o
   count_launch();
 }
 
+// skip: the column's own flag (skipped[k]) or the current step's (flags + 1)
+void update_region(cudaStream_t s, LuProblem& F, int64_t k, int64_t i0, int64_t i1, int64_t j0, int64_t j1,
+                   const int* skip) {
+  if (i1 <= i0 || j1 <= j0) return;
+  const unsigned gx = static_cast<unsigned>(ceil_div(j1 - j0, 32));
+  const unsigned gy = static_cast<unsigned>(std::min<int64_t>(ceil_div(i1 - i0, 8), std::max<int64_t>(1, 2368 / gx)));
+  lu_update_kernel<<<dim3(gx, gy), dim3(32, 8), 0, s>>>(F.re.get(), F.im.get(), F.n, k, i0, i1, j0, j1, skip);
+  count_launch();
+}
+
+// ---- C -= A B for complex planar row-major blocks with K <= kPanel, on the DMMA GEMM ----
+// Transposed formulation (the K1 kernel takes a K-major A and a K-major column-major B and
+// writes a column-major C): C^T = B^T A^T, so A' = B^T packed (nc rows, K contiguous),
+// B' = A packed (m rows), and C^T column-major IS C row-major. Complex as two real GEMMs
+// over K = 2 kPanel with a plain subtracting epilogue (no product scratch):
+//   Re: [Br^T | Bi^T] . [Ar | -Ai]^T      Im: [Br^T | Bi^T] . [Ai | Ar]^T
+constexpr int kPanel = 64;
+constexpr int kCat = 2 * kPanel;
+constexpr int64_t kBlockedRhs = 8;  // solves with at least this many right-hand sides use the GEMM
+
+// Pre[i] = [Ar[i, :K] | -Ai[i, :K]], Pim[i] = [Ai[i, :K] | Ar[i, :K]] (zero padded; columns
+// whose pivot was skipped contribute nothing: the unblocked elimination never used them).
+__global__ void pack_rows_kernel(const double* __restrict__ ar, const double* __restrict__ ai, int64_t lda,
+                                 int64_t m, int64_t K, const int* __restrict__ skip, double* __restrict__ pre,
+                                 double* __restrict__ pim) {
+  const int64_t total = m * kPanel;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / kPanel, k = e - i * kPanel;
+    const bool use = k < K && (skip == nullptr || skip[k] == 0);
+    const double x = use ? ar[i * lda + k] : 0.0, y = use ? ai[i * lda + k] : 0.0;
+    pre[i * kCat + k] = x;
+    pre[i * kCat + kPanel + k] = -y;
+    pim[i * kCat + k] = y;
+    pim[i * kCat + kPanel + k] = x;
+  }
+}
+
+// Pt[j] = [Br[:K, j] | Bi[:K, j]] (K rows of B, nc columns), zero padded.
+__global__ void pack_cols_t_kernel(const double* __restrict__ br, const double* __restrict__ bi, int64_t ldb,
+                                   int64_t nc, int64_t K, double* __restrict__ pt) {
+  const int64_t total = nc * kPanel;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t k = e / nc, j = e - k * nc;  // coalesced reads along j
+    pt[j * kCat + k] = k < K ? br[k * ldb + j] : 0.0;
+    pt[j * kCat + kPanel + k] = k < K ? bi[k * ldb + j] : 0.0;
+  }
+}
+
+struct CgemmScratch {
+  DevBuf are, aim, bt;
+  int64_t rows = 0, cols = 0;
+  void ensure(int64_t m, int64_t nc) {
+    const int64_t rp = round_up(std::max<int64_t>(m, 1), kBM), cp = round_up(std::max<int64_t>(nc, 1), kBM);
+    if (rp > rows) {
+      are.alloc(size_t(rp) * kCat);
+      aim.alloc(size_t(rp) * kCat);
+      rows = rp;
+    }
+    if (cp > cols) {
+      bt.alloc(size_t(cp) * kCat);
+      cols = cp;
+    }
+  }
+};
+
+void cgemm_sub_rowmajor(cudaStream_t s, CgemmScratch& S, int64_t m, int64_t nc, int64_t K, const double* ar,
+                        const double* ai, int64_t lda, const double* br, const double* bi, int64_t ldb, double* cr,
+                        double* ci, int64_t ldc, const int* skip_a_cols = nullptr) {
+  if (m <= 0 || nc <= 0 || K <= 0) return;
+  S.ensure(m, nc);
+  const unsigned g1 = static_cast<unsigned>(std::min<int64_t>(ceil_div(m * kPanel, 256), 2368));
+  const unsigned g2 = static_cast<unsigned>(std::min<int64_t>(ceil_div(nc * kPanel, 256), 2368));
+  pack_rows_kernel<<<g1, 256, 0, s>>>(ar, ai, lda, m, K, skip_a_cols, S.are.get(), S.aim.get());
+  pack_cols_t_kernel<<<g2, 256, 0, s>>>(br, bi, ldb, nc, K, S.bt.get());
+  count_launch(2);
+  GemmParams g{};
+  g.K = kCat;
+  g.lda = kCat;
+  g.ldb = kCat;
+  g.tiles_m = static_cast<int>(ceil_div(nc, kBM));
+  g.tiles_n = static_cast<int>(ceil_div(m, kBN));
+  g.n_rows = nc;
+  g.n_cols = m;
+  g.A = S.bt.get();
+  g.ldc = ldc;
+  g.B = S.are.get();
+  g.C = cr;
+  launch_gemm(kGemmSubAll, g, s);
+  g.B = S.aim.get();
+  g.C = ci;
+  launch_gemm(kGemmSubAll, g, s);
+}
+
 }  // namespace
 
 LuProblem* lu_factor_device(Ctx& c, int64_t n, const double* a_re, const double* a_im) {
@@ -231,16 +335,21 @@ LuProblem* lu_factor_device(Ctx& c, int64_t n, const double* a_re, const double*
   F->ctx = &c;
   F->n = n;
   cudaStream_t s = c.stream;
+  ProfMarks pm("lu_factor");
   F->re.alloc(size_t(n) * n, false);
   F->im.alloc(size_t(n) * n, a_im == nullptr);
   h2d_rows(c, F->re.get(), n, a_re, n, n, n);
   if (a_im) h2d_rows(c, F->im.get(), n, a_im, n, n, n);
+  pm.mark("upload");
   int64_t* perm = nullptr;
   IPT_CUDA(cudaMalloc(&perm, sizeof(int64_t) * n));
   F->perm.reset(perm);
   int* flags = nullptr;
   IPT_CUDA(cudaMalloc(&flags, sizeof(int) * 4));
   F->flags.reset(flags);
+  int* skipped = nullptr;
+  IPT_CUDA(cudaMalloc(&skipped, sizeof(int) * n));
+  F->skipped.reset(skipped);
   IPT_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * 4, s));
   lu_init_perm_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(n, 256), 1184)), 256, 0, s>>>(perm, n);
   // tiny = max|a| * eps * n (lu.cpp:21-23)
@@ -258,26 +367,44 @@ LuProblem* lu_factor_device(Ctx& c, int64_t n, const double* a_re, const double*
     c.sync();
   }
   count_launch(3);
-  for (int64_t k = 0; k < n; ++k) {
-    lu_pivot_kernel<<<1, 1024, 0, s>>>(F->re.get(), F->im.get(), n, k, tiny, flags);
-    lu_swap_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(n, 256), 148)), 256, 0, s>>>(
-        F->re.get(), F->im.get(), perm, n, k, flags);
-    const int64_t rest = n - k - 1;
-    if (rest > 0) {
-      lu_mult_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(rest, 256), 148)), 256, 0, s>>>(
-          F->re.get(), F->im.get(), n, k, flags);
-      const unsigned gx = static_cast<unsigned>(ceil_div(rest, 32));
-      const unsigned gy = static_cast<unsigned>(std::min<int64_t>(ceil_div(rest, 8), std::max<int64_t>(1, 2368 / gx)));
-      lu_update_kernel<<<dim3(gx, gy), dim3(32, 8), 0, s>>>(F->re.get(), F->im.get(), n, k, flags);
+  // Blocked right-looking elimination, panels of kPanel columns: per column the pivot,
+  // full-row swap and multipliers, then the rank-1 update of the panel columns and of
+  // the panel's U rows to the right (their triangular solve); after the panel ONE
+  // trailing update A22 -= L21 U12 on the DMMA GEMM (3M). Every element receives the
+  // reference's updates; only those of A22 are summed per panel instead of one by one.
+  CgemmScratch S;
+  for (int64_t c0 = 0; c0 < n; c0 += kPanel) {
+    const int64_t pend = std::min<int64_t>(n, c0 + kPanel);
+    for (int64_t k = c0; k < pend; ++k) {
+      lu_pivot_kernel<<<1, 1024, 0, s>>>(F->re.get(), F->im.get(), n, k, tiny, flags, skipped);
+      lu_swap_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(n, 256), 148)), 256, 0, s>>>(
+          F->re.get(), F->im.get(), perm, n, k, flags);
       count_launch(2);
+      if (k + 1 < n) {
+        lu_mult_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(n - k - 1, 256), 148)), 256, 0, s>>>(
+            F->re.get(), F->im.get(), n, k, flags);
+        count_launch();
+        update_region(s, *F, k, k + 1, n, k + 1, pend, flags + 1);  // panel columns, all rows below
+      }
     }
-    count_launch(2);
-    if ((k & 255) == 255) IPT_LAUNCH_CHECK();
+    if (pend < n) {
+      // U12 = L11^{-1} A12 after the panel's row swaps (rows of A12 and of A22 must be in
+      // the same state when swapped: neither has this panel's updates yet), column by
+      // column in the reference's order
+      for (int64_t k = c0; k < pend; ++k) update_region(s, *F, k, k + 1, pend, pend, n, skipped + k);
+      // A22 -= L21 U12; columns whose pivot was skipped contribute nothing (their entries
+      // below the diagonal are not multipliers and the unblocked code never used them)
+      cgemm_sub_rowmajor(s, S, n - pend, n - pend, pend - c0, F->re.get() + pend * n + c0,
+                         F->im.get() + pend * n + c0, n, F->re.get() + c0 * n + pend, F->im.get() + c0 * n + pend, n,
+                         F->re.get() + pend * n + pend, F->im.get() + pend * n + pend, n, skipped + c0);
+    }
+    IPT_LAUNCH_CHECK();
   }
   IPT_LAUNCH_CHECK();
   int h_flags[4];
   IPT_CUDA(cudaMemcpyAsync(h_flags, flags, sizeof(h_flags), cudaMemcpyDeviceToHost, s));
   c.sync();
+  pm.mark("factor");
   F->singular = h_flags[0] != 0;
   return F.release();
 }
@@ -324,6 +451,7 @@ void lu_solve_device(LuProblem& F, int64_t r, const double* b_re, const double* 
   const int64_t n = F.n;
   if (r <= 0) return;
   if (!b_re || !x_re) throw InvalidArgument("lu_solve: null input");
+  ProfMarks pm("lu_solve");
   DevBuf br, bi, xr, xi;
   br.alloc(size_t(n) * r, false);
   bi.alloc(size_t(n) * r, b_im == nullptr);
@@ -332,7 +460,33 @@ void lu_solve_device(LuProblem& F, int64_t r, const double* b_re, const double* 
   h2d_rows(c, br.get(), r, b_re, r, n, r);
   if (b_im) h2d_rows(c, bi.get(), r, b_im, r, n, r);
   const unsigned pg = static_cast<unsigned>(std::min<int64_t>(ceil_div(n * r, 256), 1184));
-  if (!adjoint) {
+  if (!adjoint && r >= kBlockedRhs) {
+    // Blocked: per panel of kPanel rows the column sweeps stay inside the panel, then
+    // one DMMA update of the rows beyond it (X_rest -= L_rest,I X_I; U likewise upward).
+    lu_permute_kernel<<<pg, 256, 0, s>>>(br.get(), bi.get(), xr.get(), xi.get(), F.perm.get(), n, r, 0);
+    count_launch();
+    CgemmScratch S;
+    const double* Lr = F.re.get();
+    const double* Li = F.im.get();
+    for (int64_t c0 = 0; c0 < n; c0 += kPanel) {  // L y = P b
+      const int64_t pend = std::min<int64_t>(n, c0 + kPanel);
+      for (int64_t j = c0; j + 1 < pend; ++j)
+        sweep<false>(s, F, xr.get(), xi.get(), nullptr, nullptr, r, j, j + 1, pend, false);
+      if (pend < n)
+        cgemm_sub_rowmajor(s, S, n - pend, r, pend - c0, Lr + pend * n + c0, Li + pend * n + c0, n,
+                           xr.get() + c0 * r, xi.get() + c0 * r, r, xr.get() + pend * r, xi.get() + pend * r, r);
+    }
+    for (int64_t c0 = ((n - 1) / kPanel) * kPanel; c0 >= 0; c0 -= kPanel) {  // U x = y, solution into B
+      const int64_t pend = std::min<int64_t>(n, c0 + kPanel);
+      for (int64_t j = pend - 1; j >= c0; --j)
+        sweep<false>(s, F, xr.get(), xi.get(), br.get(), bi.get(), r, j, c0, j, true);
+      if (c0 > 0)
+        cgemm_sub_rowmajor(s, S, c0, r, pend - c0, Lr + c0, Li + c0, n, br.get() + c0 * r, bi.get() + c0 * r, r,
+                           xr.get(), xi.get(), r);
+    }
+    std::swap(xr.p, br.p);
+    std::swap(xi.p, bi.p);
+  } else if (!adjoint) {
     // y = P b into X; L y = Pb in place (unit diagonal); U x = y: working block X, the
     // divided rows land in B (no longer needed), which then holds the solution
     lu_permute_kernel<<<pg, 256, 0, s>>>(br.get(), bi.get(), xr.get(), xi.get(), F.perm.get(), n, r, 0);
@@ -353,6 +507,8 @@ void lu_solve_device(LuProblem& F, int64_t r, const double* b_re, const double* 
     std::swap(xi.p, bi.p);
   }
   IPT_LAUNCH_CHECK();
+  c.sync();
+  pm.mark("solve");
   d2h_rows(c, x_re, r, xr.get(), r, n, r);
   if (x_im) d2h_rows(c, x_im, r, xi.get(), r, n, r);
   c.sync();
