@@ -28,15 +28,20 @@
 // The adjoint solve runs U^H then L^H by column sweeps (lu.cpp:68-86).
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 #include <cmath>
 #include <memory>
 #include <utility>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "dmma_gemm.cuh"
 #include "ipt_internal.cuh"
 
 namespace iptb {
+
+namespace cg = cooperative_groups;
 
 struct LuProblem {
   Ctx* ctx = nullptr;
@@ -326,6 +331,183 @@ void cgemm_sub_rowmajor(cudaStream_t s, CgemmScratch& S, int64_t m, int64_t nc, 
   launch_gemm(kGemmSubAll, g, s);
 }
 
+// ---- one 64-column panel in a single cooperative launch (grid-wide barriers between the
+// column steps instead of four launches per column). One CTA per SM, and every read of
+// data other CTAs write inside the launch goes through L2 (ld.global.cg): the SM's L1 is
+// not coherent with them between barriers. ----
+constexpr int kPanelThreads = 512;
+struct PanelArgs {
+  double* re;
+  double* im;
+  int64_t* perm;
+  int64_t n, c0, pend;
+  const double* tiny;
+  int* flags;      // [0] singular
+  int* skipped;    // per column
+  double* pv;      // per-block pivot candidates
+  int64_t* pi;
+};
+
+__device__ __forceinline__ void argmax_merge(double& best, int64_t& arg, double v, int64_t i) {
+  if (v > best || (v == best && i < arg)) {
+    best = v;
+    arg = i;
+  }
+}
+
+__global__ void __launch_bounds__(kPanelThreads) lu_panel_kernel(PanelArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sv[kPanelThreads / 32];
+  __shared__ int64_t si[kPanelThreads / 32];
+  const int64_t n = a.n;
+  const int64_t gt = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t G = int64_t(gridDim.x) * blockDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t k = a.c0; k < a.pend; ++k) {
+    // (1) pivot candidates over rows k+1.. (ascending per thread, strict >)
+    double best = -1.0;
+    int64_t arg = n;
+    for (int64_t i = k + 1 + gt; i < n; i += G) {
+      const double v = hypot(__ldcg(a.re + i * n + k), __ldcg(a.im + i * n + k));
+      if (v > best) {
+        best = v;
+        arg = i;
+      }
+    }
+    for (int off = 16; off > 0; off >>= 1)
+      argmax_merge(best, arg, __shfl_xor_sync(0xffffffffu, best, off), __shfl_xor_sync(0xffffffffu, arg, off));
+    if (lane == 0) {
+      sv[warp] = best;
+      si[warp] = arg;
+    }
+    __syncthreads();
+    // |a_kk| is read here, before the barrier: after it, some CTA may already be
+    // swapping row k in step (3)
+    __shared__ double s_diag;
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < kPanelThreads / 32; ++w) argmax_merge(best, arg, sv[w], si[w]);
+      a.pv[blockIdx.x] = best;
+      a.pi[blockIdx.x] = arg;
+      s_diag = hypot(__ldcg(a.re + k * n + k), __ldcg(a.im + k * n + k));
+    }
+    grid.sync();
+    // (2) every block reduces the same candidates in the same order -> same pivot
+    __shared__ int64_t s_piv;
+    __shared__ int s_skip;
+    if (threadIdx.x == 0) {
+      double b = -1.0;
+      int64_t ar = n;
+      for (unsigned q = 0; q < gridDim.x; ++q) argmax_merge(b, ar, __ldcg(a.pv + q), __ldcg(a.pi + q));
+      const double diag = s_diag;
+      int64_t piv = k;
+      double pbest = diag;
+      if (!(diag != diag) && ar < n && b > diag) {
+        piv = ar;
+        pbest = b;
+      }
+      const int skip = pbest <= *a.tiny ? 1 : 0;  // lu.cpp:27
+      s_piv = piv;
+      s_skip = skip;
+      if (blockIdx.x == 0) {
+        a.skipped[k] = skip;
+        if (skip) a.flags[0] = 1;
+        if (!skip && piv != k) {
+          const int64_t t = a.perm[k];
+          a.perm[k] = a.perm[piv];
+          a.perm[piv] = t;
+        }
+      }
+    }
+    __syncthreads();
+    const int64_t piv = s_piv;
+    const int skip = s_skip;
+    if (skip) {  // the column is left as is (every block took the same branch)
+      grid.sync();
+      continue;
+    }
+    // (3) full-row swap k <-> piv
+    if (piv != k)
+      for (int64_t j = gt; j < n; j += G) {
+        const double tr = __ldcg(a.re + k * n + j), ti = __ldcg(a.im + k * n + j);
+        a.re[k * n + j] = __ldcg(a.re + piv * n + j);
+        a.im[k * n + j] = __ldcg(a.im + piv * n + j);
+        a.re[piv * n + j] = tr;
+        a.im[piv * n + j] = ti;
+      }
+    grid.sync();
+    // (4) multipliers
+    {
+      const cd p{__ldcg(a.re + k * n + k), __ldcg(a.im + k * n + k)};
+      for (int64_t i = k + 1 + gt; i < n; i += G) {
+        const cd m = cdiv(cd{__ldcg(a.re + i * n + k), __ldcg(a.im + i * n + k)}, p);
+        a.re[i * n + k] = m.re;
+        a.im[i * n + k] = m.im;
+      }
+    }
+    grid.sync();
+    // (5) rank-1 update of the panel columns k+1 .. pend-1, all rows below
+    const int64_t w = a.pend - k - 1;
+    if (w > 0) {
+      const int64_t total = (n - k - 1) * w;
+      for (int64_t e = gt; e < total; e += G) {
+        const int64_t i = k + 1 + e / w, j = k + 1 + e % w;
+        const cd m{__ldcg(a.re + i * n + k), __ldcg(a.im + i * n + k)};
+        if (m.re == 0.0 && m.im == 0.0) continue;  // lu.cpp:44
+        const cd t = cmul(m, cd{__ldcg(a.re + k * n + j), __ldcg(a.im + k * n + j)});
+        a.re[i * n + j] = __ldcg(a.re + i * n + j) - t.re;
+        a.im[i * n + j] = __ldcg(a.im + i * n + j) - t.im;
+      }
+    }
+    grid.sync();
+  }
+}
+
+// U12 = L11^{-1} A12 for the panel rows [c0, pend) and columns [pend, n): every column is
+// independent; one thread per column runs the panel's column steps in the reference's
+// order (k ascending, rows k+1.. of the panel), the L11 block and the 64-row column
+// tiles staged in shared memory. Columns whose pivot was skipped are not applied.
+__global__ void __launch_bounds__(128) lu_trsm_panel_kernel(double* re, double* im, int64_t n, int64_t c0,
+                                                            int64_t pend, const int* __restrict__ skipped) {
+  extern __shared__ double sm[];
+  const int w = static_cast<int>(pend - c0);
+  double* lr = sm;                       // [kPanel][kPanel]
+  double* li = lr + kPanel * kPanel;
+  double* xr = li + kPanel * kPanel;     // [kPanel][128]
+  double* xi = xr + kPanel * 128;
+  __shared__ int sk[kPanel];
+  for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+    const int r = e / w, q = e % w;
+    lr[r * kPanel + q] = re[(c0 + r) * n + c0 + q];
+    li[r * kPanel + q] = im[(c0 + r) * n + c0 + q];
+  }
+  for (int q = threadIdx.x; q < w; q += blockDim.x) sk[q] = skipped[c0 + q];
+  const int64_t j = pend + blockIdx.x * int64_t(128) + threadIdx.x;
+  const bool valid = j < n;
+  for (int r = 0; r < w; ++r) {
+    xr[r * 128 + threadIdx.x] = valid ? re[(c0 + r) * n + j] : 0.0;
+    xi[r * 128 + threadIdx.x] = valid ? im[(c0 + r) * n + j] : 0.0;
+  }
+  __syncthreads();
+  if (valid) {
+    for (int k = 0; k < w; ++k) {
+      if (sk[k]) continue;
+      const cd u{xr[k * 128 + threadIdx.x], xi[k * 128 + threadIdx.x]};
+      for (int r = k + 1; r < w; ++r) {
+        const cd m{lr[r * kPanel + k], li[r * kPanel + k]};
+        if (m.re == 0.0 && m.im == 0.0) continue;
+        const cd t = cmul(m, u);
+        xr[r * 128 + threadIdx.x] -= t.re;
+        xi[r * 128 + threadIdx.x] -= t.im;
+      }
+    }
+    for (int r = 0; r < w; ++r) {
+      re[(c0 + r) * n + j] = xr[r * 128 + threadIdx.x];
+      im[(c0 + r) * n + j] = xi[r * 128 + threadIdx.x];
+    }
+  }
+}
+constexpr size_t kTrsmSmem = sizeof(double) * (2 * kPanel * kPanel + 2 * kPanel * 128);
+
 }  // namespace
 
 LuProblem* lu_factor_device(Ctx& c, int64_t n, const double* a_re, const double* a_im) {
@@ -373,25 +555,55 @@ LuProblem* lu_factor_device(Ctx& c, int64_t n, const double* a_re, const double*
   // trailing update A22 -= L21 U12 on the DMMA GEMM (3M). Every element receives the
   // reference's updates; only those of A22 are summed per panel instead of one by one.
   CgemmScratch S;
+  // cooperative grid for the panel kernel: every resident CTA, one wave
+  static int panel_grid = 0;
+  if (panel_grid == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    IPT_CUDA(cudaGetDevice(&dev));
+    IPT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    IPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lu_panel_kernel, kPanelThreads, 0));
+    if (per_sm < 1) throw CudaError("lu: panel kernel cannot be resident");
+    panel_grid = sms;  // one CTA per SM
+    IPT_CUDA(cudaFuncSetAttribute(lu_trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kTrsmSmem)));
+  }
+  DevBuf pv, pidx;
+  pv.alloc(panel_grid, false);
+  pidx.alloc(panel_grid, false);
   for (int64_t c0 = 0; c0 < n; c0 += kPanel) {
     const int64_t pend = std::min<int64_t>(n, c0 + kPanel);
-    for (int64_t k = c0; k < pend; ++k) {
-      lu_pivot_kernel<<<1, 1024, 0, s>>>(F->re.get(), F->im.get(), n, k, tiny, flags, skipped);
-      lu_swap_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(n, 256), 148)), 256, 0, s>>>(
-          F->re.get(), F->im.get(), perm, n, k, flags);
-      count_launch(2);
-      if (k + 1 < n) {
-        lu_mult_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(n - k - 1, 256), 148)), 256, 0, s>>>(
-            F->re.get(), F->im.get(), n, k, flags);
-        count_launch();
-        update_region(s, *F, k, k + 1, n, k + 1, pend, flags + 1);  // panel columns, all rows below
+    // IPT_LU_COOP=0 / IPT_LU_TRSM=0: the per-column launches instead of the cooperative
+    // panel kernel / the per-panel TRSM kernel (same arithmetic; for A/B checks)
+    if (std::getenv("IPT_LU_COOP") && std::getenv("IPT_LU_COOP")[0] == '0') {
+      for (int64_t k = c0; k < pend; ++k) {
+        lu_pivot_kernel<<<1, 1024, 0, s>>>(F->re.get(), F->im.get(), n, k, tiny, flags, skipped);
+        lu_swap_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(n, 256), 148)), 256, 0, s>>>(
+            F->re.get(), F->im.get(), perm, n, k, flags);
+        if (k + 1 < n) {
+          lu_mult_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(n - k - 1, 256), 148)), 256, 0, s>>>(
+              F->re.get(), F->im.get(), n, k, flags);
+          update_region(s, *F, k, k + 1, n, k + 1, pend, flags + 1);
+        }
       }
+    } else {
+      PanelArgs pa{F->re.get(), F->im.get(), perm, n, c0, pend, tiny, flags, skipped, pv.get(),
+                   reinterpret_cast<int64_t*>(pidx.get())};
+      void* args[] = {&pa};
+      IPT_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lu_panel_kernel), dim3(panel_grid),
+                                           dim3(kPanelThreads), args, 0, s));
+      count_launch();
     }
     if (pend < n) {
       // U12 = L11^{-1} A12 after the panel's row swaps (rows of A12 and of A22 must be in
       // the same state when swapped: neither has this panel's updates yet), column by
       // column in the reference's order
-      for (int64_t k = c0; k < pend; ++k) update_region(s, *F, k, k + 1, pend, pend, n, skipped + k);
+      if (std::getenv("IPT_LU_TRSM") && std::getenv("IPT_LU_TRSM")[0] == '0') {
+        for (int64_t k = c0; k < pend; ++k) update_region(s, *F, k, k + 1, pend, pend, n, skipped + k);
+      } else {
+        lu_trsm_panel_kernel<<<static_cast<unsigned>(ceil_div(n - pend, 128)), 128, kTrsmSmem, s>>>(
+            F->re.get(), F->im.get(), n, c0, pend, skipped);
+        count_launch();
+      }
       // A22 -= L21 U12; columns whose pivot was skipped contribute nothing (their entries
       // below the diagonal are not multipliers and the unblocked code never used them)
       cgemm_sub_rowmajor(s, S, n - pend, n - pend, pend - c0, F->re.get() + pend * n + c0,
