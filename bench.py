@@ -510,6 +510,7 @@ def main():
                          "peak_source": "cuBLAS DGEMM 8192^3 on this GPU in this run (burst); DMMA issue-rate "
                                         "probe 37.1 TF/s in profiles/r01_fp64_probe.txt",
                          "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+                         "frac_of_dmma_issue_peak": achieved / 37.1,  # profiles/r01_fp64_probe.txt
                          "flops_per_launch": gemm_flops_local, "kernel_ms": gemm_ms_local,
                          "kernel_share_of_step": gemm_ms / step_ms,
                          "traffic": traffic_for("dmma_tma_kernel<1>", n) if world == 1 else None},
