@@ -84,7 +84,8 @@ struct SpmvVariant {
 };
 constexpr SpmvVariant kSpmvVariants[] = {{16, 4, 0, 5}, {8, 8, 0, 5}, {32, 2, 0, 5}, {8, 4, 0, 5}, {16, 6, 0, 5},
                                          {0, 4, 4, 4},  {0, 2, 8, 4}, {0, 2, 4, 5}, {0, 4, 4, 3},
-                                         {0, 4, 4, 4},  {0, 4, 16, 3}, {0, 8, 4, 3}};
+                                         {0, 4, 4, 4},  {0, 4, 16, 3}, {0, 8, 4, 3},  {0, 4, 2, 4},
+                                         {0, 8, 2, 4},  {0, 8, 4, 4},  {0, 4, 8, 4}};
 constexpr int kNumSpmvVariants = sizeof(kSpmvVariants) / sizeof(kSpmvVariants[0]);
 constexpr int kSpmvDefault = 9;  // warp-contiguous groups of 4 rows, 4 in flight, plain nc loads
 inline int spmv_variant() {
@@ -598,6 +599,10 @@ void launch_spmv(unsigned grid, cudaStream_t s, const int64_t* rowptr, const int
     IPT_SPMVG(5, 4, 4, 4) IPT_SPMVG(6, 8, 2, 4) IPT_SPMVG(7, 4, 2, 5) IPT_SPMVG(8, 4, 4, 3)
     case 9: spmv_group_kernel<MODE, 4, 4, 4, false><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
     IPT_SPMVG(10, 16, 4, 3) IPT_SPMVG(11, 4, 8, 3)
+    case 12: spmv_group_kernel<MODE, 2, 4, 4, false><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 13: spmv_group_kernel<MODE, 2, 8, 4, false><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 14: spmv_group_kernel<MODE, 4, 8, 4, false><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 15: spmv_group_kernel<MODE, 8, 4, 4, false><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
 #undef IPT_SPMV
 #undef IPT_SPMVG
   }
