@@ -348,6 +348,38 @@ def bench_sparse_full(lib, ctx, n, per_row, steps, dense_step_ms):
             "speedup_vs_dense_map": dense_step_ms / ms if dense_step_ms else None}
 
 
+def bench_ozaki(ipt, lib, ctx, n, dense_step_ms, dmma_solve):
+    """The same map and solve with W = Delta Z by Ozaki scheme II on the tcgen05 INT8
+    datapath (16 exact modular GEMMs + CRT reconstruction, ozaki.cu): FP64-accurate, so
+    reported with its agreement to the DMMA (FP64 tensor core) solve."""
+    from paper_2012_14702_b200 import synth
+    from paper_2012_14702_b200._lib import check, dptr
+
+    p = synth.config3(n=n)
+    h = C.c_void_p()
+    check(lib.ipt_full_upload(ctx.handle, n, dptr(p.d), None, dptr(p.delta), None, C.byref(h)))
+    check(lib.ipt_full_reset(ctx.handle, h, None, None))
+    check(lib.ipt_full_set_product(h, 1))
+    tot, ker = C.c_double(), C.c_double()
+    check(lib.ipt_full_run_maps(ctx.handle, h, 2, C.byref(tot), C.byref(ker)))
+    steps = 3
+    check(lib.ipt_full_run_maps(ctx.handle, h, steps, C.byref(tot), C.byref(ker)))
+    lib.ipt_full_free(h)
+    ms = tot.value / steps
+    t0 = time.perf_counter()
+    r = ipt.solve_full(p, ipt.build_gaps(p), ipt.IterationConfig(tolerance=1e-12), ctx=ctx, product="ozaki")
+    tts = time.perf_counter() - t0
+    out = {"workload": f"configs[2] N={n}, W = Delta Z by Ozaki scheme II on tcgen05 kind::i8 (16 moduli)",
+           "ms_per_map": ms, "fp64_equivalent_TFs": 2.0 * n ** 3 / (ms * 1e-3) / 1e12,
+           "speedup_vs_dmma_map": dense_step_ms / ms,
+           "time_to_solution_s": tts, "iterations": r.iterations, "status": ipt.to_string(r.status),
+           "timings_ms": r.timings_ms, "residual_frobenius": r.residual_frobenius}
+    if dmma_solve is not None and dmma_solve.get("lambda0") is not None:
+        out["lambda0"] = float(r.eigenvalues[0])
+        out["lambda0_rel_diff_vs_dmma"] = abs(float(r.eigenvalues[0]) - dmma_solve["lambda0"]) / abs(dmma_solve["lambda0"])
+    return out
+
+
 # --------------------------------------------------------------------------- main arm
 
 
@@ -491,6 +523,10 @@ def main():
                 secondary["sparse_full"] = bench_sparse_full(lib, ctx, n, 64, max(args.steps, 5), step_ms)
             except Exception as exc:
                 secondary["sparse_full"] = {"error": repr(exc)}
+            try:
+                secondary["ozaki"] = bench_ozaki(ipt, lib, ctx, n, step_ms, solve_info)
+            except Exception as exc:
+                secondary["ozaki"] = {"error": repr(exc)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -57,7 +57,14 @@ typedef struct {
   int32_t schedule;            /* IPT_SCHEDULE_* (single pair only) */
   double shrink_alpha;         /* continuation factor in [0, 1) */
   int32_t ignore_convergence;  /* bench only: apply exactly max_iterations maps */
+  int32_t product;             /* IPT_PRODUCT_*: how the full-spectrum map forms W = Delta Z */
 } ipt_params;
+
+/* W = Delta Z of the real dense full-spectrum map: FP64 tensor cores (DMMA, default), or
+ * FP64-accurate Ozaki scheme II on the tcgen05 INT8 datapath (16 exact modular products,
+ * Chinese-remainder reconstruction; falls back to DMMA for non-finite Delta). */
+#define IPT_PRODUCT_DMMA 0
+#define IPT_PRODUCT_OZAKI 1
 
 /* Mirrors ipt::SpectrumResult / EigenpairResult scalars (solver.hpp:28-52). */
 typedef struct {
@@ -108,6 +115,8 @@ int ipt_full_finalize(ipt_ctx* ctx, ipt_full_problem* prob, const ipt_params* pa
 int ipt_full_download(ipt_ctx* ctx, ipt_full_problem* prob, double* z_re, double* z_im,
                       double* lam_re, double* lam_im);
 int ipt_full_local_columns(const ipt_full_problem* prob, int64_t* col_begin, int64_t* col_end);
+/* Product used by ipt_full_run_maps (the solve calls take ipt_params.product). */
+int ipt_full_set_product(ipt_full_problem* prob, int32_t product);
 void ipt_full_free(ipt_full_problem* prob);
 
 /* apply_map_full (solver.cpp:156-178): one F application to a given Z. */
@@ -166,6 +175,13 @@ int ipt_lu_solve(ipt_ctx* ctx, ipt_lu* lu, int64_t nrhs, const double* b_re, con
 int ipt_lu_solve_adjoint(ipt_ctx* ctx, ipt_lu* lu, int64_t nrhs, const double* b_re, const double* b_im,
                          double* x_re, double* x_im);
 void ipt_lu_free(ipt_lu* lu);
+
+/* 5th-gen tensor-core INT8 GEMM (tcgen05.mma kind::i8, exact int32 accumulation), the
+ * building block of FP64-accurate products by modular arithmetic: C (M x N int32,
+ * row-major) = A (M x K int8, row-major) . B (N x K int8, row-major)^T; M % 128 == 0,
+ * N % 256 == 0, K % 128 == 0. With iters > 0 also times that many launches. */
+int ipt_i8_gemm(ipt_ctx* ctx, int64_t M, int64_t N, int64_t K, const int8_t* A, const int8_t* B, int32_t* C,
+                int32_t iters, double* ms_per_gemm);
 
 /* smallest_singular_value_estimate (solver.cpp:275-297). */
 int ipt_sigma_min(ipt_ctx* ctx, int64_t n, const double* z_re, const double* z_im,

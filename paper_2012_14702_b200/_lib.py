@@ -30,6 +30,10 @@ _i32p = C.POINTER(C.c_int32)
 _vp = C.c_void_p
 
 
+PRODUCT_DMMA = 0
+PRODUCT_OZAKI = 1
+
+
 class Params(C.Structure):
     _fields_ = [
         ("tolerance", C.c_double),
@@ -41,6 +45,7 @@ class Params(C.Structure):
         ("schedule", C.c_int32),
         ("shrink_alpha", C.c_double),
         ("ignore_convergence", C.c_int32),
+        ("product", C.c_int32),
     ]
 
 
@@ -83,6 +88,7 @@ SIGNATURES = {
     "ipt_full_iterate": (C.c_int, [_vp, _vp, C.POINTER(Params), C.POINTER(Stats)]),
     "ipt_full_finalize": (C.c_int, [_vp, _vp, C.POINTER(Params), C.POINTER(Stats)]),
     "ipt_full_download": (C.c_int, [_vp, _vp, _dp, _dp, _dp, _dp]),
+    "ipt_full_set_product": (C.c_int, [_vp, C.c_int32]),
     "ipt_full_local_columns": (C.c_int, [_vp, _i64p, _i64p]),
     "ipt_full_free": (None, [_vp]),
     "ipt_apply_map_full": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]),
@@ -96,6 +102,7 @@ SIGNATURES = {
     "ipt_full_upload_csr": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, _i32p, _dp, _dp, C.POINTER(_vp)]),
     "ipt_apply_map_full_csr": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, _i32p, _dp, _dp, _dp, _dp,
                                          _dp, _dp]),
+    "ipt_i8_gemm": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, _vp, _vp, _vp, C.c_int32, _dp]),
     "ipt_lu_factor": (C.c_int, [_vp, C.c_int64, _dp, _dp, C.POINTER(_vp)]),
     "ipt_lu_from_host": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, C.c_int, C.POINTER(_vp)]),
     "ipt_lu_info": (C.c_int, [_vp, _i64p, C.POINTER(C.c_int)]),

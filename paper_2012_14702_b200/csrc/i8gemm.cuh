@@ -1,0 +1,178 @@
+// 5th-generation tensor-core INT8 GEMM for sm_100a (tcgen05.mma kind::i8, int32 TMEM
+// accumulators): the building block of FP64-accurate products by modular integer
+// arithmetic (Ozaki scheme II, see ozaki.cu). tcgen05 has no f64 kind; exact integer
+// products on the INT8 datapath are how FP64 GEMMs use the 5th-gen tensor cores.
+//
+// C[m, n] = sum_k A[m, k] * B[n, k]     A: M x K int8 (K contiguous), B: N x K int8 (K
+// contiguous), exact int32 accumulation (|sum| < K * 2^14 for residues in [-128, 127]).
+//
+// CTA tile 128 x 256 x 128 bytes, 4-stage TMA pipeline (SWIZZLE_128B, 48 KB per stage),
+// warp roles: warp 0 issues TMA, warp 1 allocates 256 TMEM columns and one elected lane
+// issues 4 tcgen05.mma (K = 32 each) per stage, committing stage release and accumulator
+// completion to mbarriers; warps 2-5 drain TMEM (tcgen05.ld 32x32b) in the epilogue. The
+// epilogue is a functor applied to each row's 32-column chunk of int32 results.
+#pragma once
+
+#include "dmma_gemm.cuh"
+#include "ipt_internal.cuh"
+
+namespace iptb {
+
+constexpr int kI8BM = 128;
+constexpr int kI8BN = 256;
+constexpr int kI8BK = 128;  // bytes = int8 elements per stage along K
+constexpr int kI8Stages = 4;
+constexpr int kI8Threads = 192;  // 6 warps
+constexpr int kI8StageBytes = (kI8BM + kI8BN) * kI8BK;
+constexpr size_t kI8SmemBytes = size_t(kI8Stages) * kI8StageBytes + 1024 + 256;
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
+  // SM100 shared-memory matrix descriptor, K-major, 128-byte swizzle: start address
+  // (>> 4), LBO unused (1), SBO = 1024 B between 8-row core-matrix groups, version 1.
+  uint64_t d = 0;
+  d |= uint64_t((smem_addr & 0x3FFFF) >> 4);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(1024 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(2) << 61;
+  return d;
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t tmem_c, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(tmem_c),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(0u), "r"(0u), "r"(0u), "r"(0u));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// instruction descriptor: int32 accumulate, signed int8 A and B, both K-major, M = 128, N = 256
+constexpr uint32_t kI8Idesc = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kI8BN >> 3) << 17) |
+                              (uint32_t(kI8BM >> 4) << 24);
+
+// Epi(row, col0, v[32]) consumes columns col0..col0+31 of one row.
+template <class Epi>
+__global__ void __launch_bounds__(kI8Threads, 1)
+    i8gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K, int tiles_m,
+                  Epi epi) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + size_t(kI8Stages) * kI8StageBytes);
+  uint64_t* empty = full + kI8Stages;
+  uint64_t* acc_full = empty + kI8Stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tm = blockIdx.x % tiles_m, tn = blockIdx.x / tiles_m;
+  const int m0 = tm * kI8BM, n0 = tn * kI8BN;
+  const int KB = K / kI8BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kI8Stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(uint32_t(kI8BN)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % kI8Stages;
+        if (kb >= kI8Stages) mbar_wait(&empty[s], ((kb / kI8Stages) - 1) & 1);
+        unsigned char* sa = base + size_t(s) * kI8StageBytes;
+        mbar_expect_tx(&full[s], kI8StageBytes);
+        tma_load_2d(sa, &tmA, &full[s], kb * kI8BK, m0);
+        tma_load_2d(sa + kI8BM * kI8BK, &tmB, &full[s], kb * kI8BK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % kI8Stages;
+        mbar_wait(&full[s], (kb / kI8Stages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t sa = smem_u32(base + size_t(s) * kI8StageBytes);
+        const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + kI8BM * kI8BK);
+#pragma unroll
+        for (int k = 0; k < kI8BK / 32; ++k)  // 32 bytes of K per MMA: +2 in the (>>4) start field
+          umma_i8(tmem, da + 2 * k, db + 2 * k, kI8Idesc, (kb | k) ? 1u : 0u);
+        umma_commit(&empty[s]);
+      }
+      umma_commit(acc_full);
+    }
+    __syncwarp();
+  } else {
+    // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (its rows), 32 columns at a time
+    mbar_wait(acc_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int quarter = warp & 3;
+    const int row = m0 + quarter * 32 + lane;
+    const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16);
+#pragma unroll 1
+    for (int c = 0; c < kI8BN; c += 32) {
+      uint32_t v[32];
+      tmem_ld32(trow + uint32_t(c), v);
+      epi(row, n0 + c, v);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(uint32_t(kI8BN)));
+}
+
+// `rows` x `k` int8 (K contiguous, pitch ld bytes), TMA boxes of 128 bytes x box_rows rows.
+CUtensorMap make_map_i8(const void* base, int64_t k, int64_t rows, int64_t ld, int box_rows);
+
+// Launch C-tile epilogue `epi` over A (M x K) . B (N x K)^T; M % 128, N % 256, K % 128 == 0,
+// lda / ldb in bytes.
+template <class Epi>
+void launch_i8gemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, const int8_t* A, int64_t lda, const int8_t* B,
+                   int64_t ldb, const Epi& epi) {
+  if (M % kI8BM || N % kI8BN || K % kI8BK || M <= 0 || N <= 0 || K <= 0)
+    throw InvalidArgument("i8 gemm: M % 128, N % 256 and K % 128 must be 0");
+  static bool attr = false;
+  if (!attr) {
+    IPT_CUDA(cudaFuncSetAttribute(i8gemm_kernel<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kI8SmemBytes)));
+    attr = true;
+  }
+  const CUtensorMap ma = make_map_i8(A, K, M, lda, kI8BM);
+  const CUtensorMap mb = make_map_i8(B, K, N, ldb, kI8BN);
+  const int tiles_m = static_cast<int>(M / kI8BM);
+  const unsigned grid = static_cast<unsigned>(tiles_m * (N / kI8BN));
+  i8gemm_kernel<Epi><<<grid, kI8Threads, kI8SmemBytes, s>>>(ma, mb, static_cast<int>(K), tiles_m, epi);
+  IPT_LAUNCH_CHECK();
+  count_launch();
+}
+
+}  // namespace iptb

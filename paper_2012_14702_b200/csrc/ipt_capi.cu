@@ -205,6 +205,7 @@ void ipt_default_params(ipt_params* p) {
   p->schedule = IPT_SCHEDULE_PLAIN;
   p->shrink_alpha = 0.9;
   p->ignore_convergence = 0;
+  p->product = IPT_PRODUCT_DMMA;
 }
 
 int64_t ipt_kernel_launch_count(void) { return g_launches.load(); }
@@ -364,6 +365,12 @@ int ipt_full_download(ipt_ctx* ctx, ipt_full_problem* prob, double* z_re, double
   });
 }
 
+int ipt_full_set_product(ipt_full_problem* prob, int32_t product) {
+  if (!prob || (product != IPT_PRODUCT_DMMA && product != IPT_PRODUCT_OZAKI)) return IPT_ERR_INVALID;
+  full_set_product(*reinterpret_cast<FullProblem*>(prob), product);
+  return IPT_OK;
+}
+
 int ipt_full_local_columns(const ipt_full_problem* prob, int64_t* col_begin, int64_t* col_end) {
   if (!prob) return IPT_ERR_INVALID;
   full_local_columns(*reinterpret_cast<const FullProblem*>(prob), col_begin, col_end);
@@ -444,6 +451,39 @@ int ipt_apply_map_full(ipt_ctx* ctx, int64_t n, const double* d_re, const double
       P.reset(full_upload(ctx->c, n, d_re, d_im, delta_re, delta_im, /*force_complex=*/true));
     }
     apply_one_map(*P, z_re, z_im, f_re, f_im);
+  });
+}
+
+// ------------------------------------------------------------------ tcgen05 INT8 GEMM
+
+int ipt_i8_gemm(ipt_ctx* ctx, int64_t M, int64_t N, int64_t K, const int8_t* A, const int8_t* B, int32_t* C,
+                int32_t iters, double* ms_per_gemm) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    Ctx& c = ctx->c;
+    if (!A || !B) throw InvalidArgument("i8 gemm: null input");
+    DevBuf dA, dB, dC;  // byte buffers carried in double-sized DevBufs
+    dA.alloc(size_t(ceil_div(M * K, 8)), false);
+    dB.alloc(size_t(ceil_div(N * K, 8)), false);
+    dC.alloc(size_t(ceil_div(M * N * 4, 8)), false);
+    IPT_CUDA(cudaMemcpyAsync(dA.get(), A, size_t(M) * K, cudaMemcpyHostToDevice, c.stream));
+    IPT_CUDA(cudaMemcpyAsync(dB.get(), B, size_t(N) * K, cudaMemcpyHostToDevice, c.stream));
+    auto* a8 = reinterpret_cast<const int8_t*>(dA.get());
+    auto* b8 = reinterpret_cast<const int8_t*>(dB.get());
+    auto* c32 = reinterpret_cast<int32_t*>(dC.get());
+    i8_gemm_device(c.stream, M, N, K, a8, b8, c32);
+    c.sync();
+    if (iters > 0 && ms_per_gemm) {
+      IPT_CUDA(cudaEventRecord(c.ev[0], c.stream));
+      for (int i = 0; i < iters; ++i) i8_gemm_device(c.stream, M, N, K, a8, b8, c32);
+      IPT_CUDA(cudaEventRecord(c.ev[1], c.stream));
+      c.sync();
+      float ms = 0.f;
+      IPT_CUDA(cudaEventElapsedTime(&ms, c.ev[0], c.ev[1]));
+      *ms_per_gemm = ms / iters;
+    }
+    if (C) IPT_CUDA(cudaMemcpy(C, dC.get(), size_t(M) * N * 4, cudaMemcpyDeviceToHost));
   });
 }
 

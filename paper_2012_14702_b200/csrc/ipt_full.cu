@@ -25,6 +25,7 @@
 
 #include "dmma_gemm.cuh"
 #include "ipt_internal.cuh"
+#include "ozaki.cuh"
 
 namespace iptb {
 
@@ -61,6 +62,12 @@ struct FullProblem {
   bool start_identity = false;  // Z[0] is the identity (no warm start)
   const double* z_after_loop = nullptr;  // current iterate when full_iterate returned
   DevBuf rm[2];                          // row-major copies of Z for an overlapped download
+  // Ozaki scheme II product (IPT_PRODUCT_OZAKI): Delta's residues (built once), the current
+  // Z's residues, the product residues
+  int product = IPT_PRODUCT_DMMA;
+  OzakiOperand oz_delta, oz_z;
+  DevBuf oz_R;
+  bool oz_delta_ready = false;
   ~FullProblem() {
     if (state) cudaFree(state);
   }
@@ -589,6 +596,43 @@ void allreduce_sums(FullProblem& P, bool with_max) {
     IPT_NCCL(ncclAllReduce(P.sums.get() + 3, P.sums.get() + 3, 1, ncclDouble, ncclMax, c.comm, c.stream));
 }
 
+bool use_ozaki(const FullProblem& P) {
+  return P.product == IPT_PRODUCT_OZAKI && !P.cplx && !P.sparse && P.delta_finite;
+}
+
+// W = Delta Z by Ozaki scheme II, then the map (mode 0) or the closing residual (mode 1).
+void ozaki_apply(FullProblem& P, const double* zs, double* zd, int mode, const LoopState* st) {
+  cudaStream_t s = P.ctx->stream;
+  const int64_t kpad = round_up(P.n, kOzakiKPad);
+  const int64_t arows = round_up(P.n, 256);
+  if (!P.oz_delta_ready) {
+    P.oz_delta.build(s, P.A1.get(), P.lda, P.n, P.n, arows, kpad);
+    P.oz_delta_ready = true;
+  }
+  P.oz_z.build(s, zs, P.ldz, P.ncols, P.n, P.cols_pad, kpad);
+  int64_t plane = 0;
+  ozaki_products(s, P.oz_z, P.oz_delta, P.cols_pad, arows, P.oz_R, plane);
+  OzakiMapArgs a{};
+  a.R = reinterpret_cast<const int8_t*>(P.oz_R.get());
+  a.plane = plane;
+  a.ldr = arows;
+  a.eA = P.oz_delta.exps();
+  a.eB = P.oz_z.exps();
+  a.Z = zs;
+  a.ldz = P.ldz;
+  a.F = zd;
+  a.d = P.dre.get();
+  a.wd = P.wd.get();
+  a.lam = P.lam.get();
+  a.n = P.n;
+  a.ncols = P.ncols;
+  a.col0 = P.col0;
+  a.mode = mode;
+  a.partials = P.partials.get();
+  a.state = st;
+  ozaki_reconstruct(s, a);
+}
+
 // Enqueue map application number k (reads Z[k&1], writes Z[(k+1)&1]).
 void enqueue_map(FullProblem& P, int k, const ipt_params& prm, cudaEvent_t ev_a = nullptr,
                  cudaEvent_t ev_b = nullptr) {
@@ -605,15 +649,28 @@ void enqueue_map(FullProblem& P, int k, const ipt_params& prm, cudaEvent_t ev_a 
     launch_diag(P, P.A1.get(), zs, P.wd.get(), nullptr, nullptr, st);
     GemmParams g = gemm_params(P, P.A1.get(), zs, zd, P.ldz);
     if (ev_a) IPT_CUDA(cudaEventRecord(ev_a, c.stream));
+    int64_t nparts = num_partials(P);
     if (k == 0 && P.start_identity && P.delta_finite && identity_shortcut_enabled()) {
       const unsigned tiles = static_cast<unsigned>(gemm_tiles(P.n, P.ncols));
       map_identity_kernel<<<tiles, kGemmThreads, 0, c.stream>>>(g);
       IPT_LAUNCH_CHECK();
       count_launch();
+    } else if (use_ozaki(P)) {
+      ozaki_apply(P, zs, zd, 0, st);
+      nparts = kOzakiGrid;
     } else {
       launch_gemm(kGemmMap, g, c.stream);
     }
     if (ev_b) IPT_CUDA(cudaEventRecord(ev_b, c.stream));
+    reduce_partials(c.stream, P.partials.get(), nparts, P.sums.get(), st);
+    allreduce_sums(P, true);
+    decide_full_kernel<<<1, 1, 0, c.stream>>>(
+        st, P.sums.get(), k, prm.tolerance, prm.max_iterations, prm.divergence_threshold,
+        prm.stop_rule, prm.ignore_convergence, prm.record_trace ? P.trace.get() : nullptr,
+        prm.record_trace ? P.trace_max.get() : nullptr);
+    IPT_LAUNCH_CHECK();
+    count_launch();
+    return;
   } else {
     launch_complex_products(P, zs, zd, kGemmMapC, st, ev_a, ev_b);
   }
@@ -706,7 +763,7 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
   P->wdi.alloc(P->cols_pad);
   P->lam.alloc(P->cols_pad);
   P->lami.alloc(P->cols_pad);
-  P->partials.alloc(size_t(std::max<int64_t>(num_partials(*P), 1)) * 4);
+  P->partials.alloc(size_t(std::max<int64_t>(num_partials(*P), kOzakiGrid)) * 4);
   P->sums.alloc(4);
   IPT_CUDA(cudaMalloc(&P->state, sizeof(LoopState)));
   if (!P->cplx) {
@@ -848,8 +905,11 @@ void full_reset(FullProblem& P, const double* warm_re, const double* warm_im, in
   P.gathered.release();
 }
 
+void full_set_product(FullProblem& P, int product) { P.product = product; }
+
 void full_iterate(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
   Ctx& c = *P.ctx;
+  P.product = prm.product;
   if (!(prm.tolerance > 0.0)) throw InvalidArgument("config: tolerance must be positive");
   if (prm.max_iterations <= 0) throw InvalidArgument("config: max_iterations must be positive");
   if (!(prm.divergence_threshold > 1.0)) throw InvalidArgument("config: divergence_threshold must exceed 1");
@@ -926,6 +986,9 @@ void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
   if (P.sparse) {
     launch_sparse_diag(P, z, P.lam.get(), nullptr);
     launch_spmm(P, 1, z, nullptr, nullptr);
+  } else if (!P.cplx && use_ozaki(P)) {
+    launch_diag(P, P.A1.get(), z, P.wd.get(), P.lam.get(), P.dre.get(), nullptr);
+    ozaki_apply(P, z, nullptr, 1, nullptr);
   } else if (!P.cplx) {
     launch_diag(P, P.A1.get(), z, P.wd.get(), P.lam.get(), P.dre.get(), nullptr);
     GemmParams g = gemm_params(P, P.A1.get(), z, nullptr, 0);
@@ -934,7 +997,8 @@ void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
   } else {
     launch_complex_products(P, z, nullptr, kGemmResidC, nullptr, nullptr, nullptr);
   }
-  reduce_partials(s, P.partials.get(), num_partials(P), P.sums.get(), nullptr);
+  reduce_partials(s, P.partials.get(), (!P.cplx && use_ozaki(P)) ? kOzakiGrid : num_partials(P), P.sums.get(),
+                  nullptr);
   allreduce_sums(P, false);
   double h4[4];
   IPT_CUDA(cudaMemcpyAsync(h4, P.sums.get(), sizeof(h4), cudaMemcpyDeviceToHost, s));

@@ -137,6 +137,7 @@ void full_prepare_download(FullProblem& P, bool want_re, bool want_im);
 void full_download_z(FullProblem& P, double* z_re, double* z_im);
 void full_release_download(FullProblem& P);
 void full_local_columns(const FullProblem& P, int64_t* c0, int64_t* c1);
+void full_set_product(FullProblem& P, int product);
 bool full_is_complex(const FullProblem& P);
 void full_run_maps(FullProblem& P, int count, double* ms_total, double* ms_gemm);
 
@@ -169,6 +170,9 @@ bool lu_singular(const LuProblem& F);
 void lu_download(LuProblem& F, double* lu_re, double* lu_im, int64_t* perm);
 void lu_solve_device(LuProblem& F, int64_t nrhs, const double* b_re, const double* b_im, double* x_re, double* x_im,
                      bool adjoint);
+
+// tcgen05 INT8 GEMM (i8gemm.cu): C (M x N int32 row-major) = A (M x K) . B (N x K)^T.
+void i8_gemm_device(cudaStream_t s, int64_t M, int64_t N, int64_t K, const int8_t* A, const int8_t* B, int32_t* C);
 
 // sigma_min (ipt_sigma.cu): Z column-major (ldz), real or complex (zi nullable).
 double sigma_min_device(Ctx& ctx, int64_t n, const double* zr, const double* zi, int64_t ldz,

@@ -390,7 +390,7 @@ def apply_map_full(p: Partition, g: InverseGaps, Z, ctx: Optional[Context] = Non
 
 
 def solve_full(p: Partition, g: InverseGaps, config: IterationConfig = None, warm_start=None,
-               ctx: Optional[Context] = None, want_sigma_min: bool = True) -> SpectrumResult:
+               ctx: Optional[Context] = None, want_sigma_min: bool = True, product: str = "dmma") -> SpectrumResult:
     """Fixed-point iteration of F from I (or a renormalised warm start), then the
     closing product, |MZ - Z Lambda|_F and sigma_min (solver.cpp:180-273)."""
     config = config or IterationConfig()
@@ -411,7 +411,10 @@ def solve_full(p: Partition, g: InverseGaps, config: IterationConfig = None, war
     zi = np.empty((n, n)) if (root and cx) else None
     lr = np.empty(n) if root else None
     li = np.empty(n) if (root and cx) else None
-    prm = _params(config, want_sigma_min=1 if want_sigma_min else 0)
+    if product not in ("dmma", "ozaki"):
+        raise ValueError("solve_full: product must be 'dmma' or 'ozaki'")
+    prm = _params(config, want_sigma_min=1 if want_sigma_min else 0,
+                  product=_lib.PRODUCT_OZAKI if product == "ozaki" else _lib.PRODUCT_DMMA)
     st = _lib.Stats()
     tr = np.zeros(config.max_iterations) if config.record_trace else None
     tm = np.zeros(config.max_iterations) if config.record_trace else None

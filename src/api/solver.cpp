@@ -264,6 +264,7 @@ SpectrumResult solve_full(const Partition& p, const InverseGaps& g, const Iterat
     ipt_params prm = to_params(config);
     prm.stop_rule = options.stop_rule == StopRule::MaxAbs ? IPT_STOP_MAX_ABS : IPT_STOP_REL_FRO;
     prm.want_sigma_min = options.want_sigma_min ? 1 : 0;
+    prm.product = options.product == Product::Ozaki ? IPT_PRODUCT_OZAKI : IPT_PRODUCT_DMMA;
     ipt_stats st{};
     std::vector<double> trace(config.record_trace ? config.max_iterations : 0);
     st.trace = config.record_trace ? trace.data() : nullptr;
