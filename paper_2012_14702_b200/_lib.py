@@ -11,7 +11,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libipt_b200.so")
+LIB_PATH = os.environ.get("IPT_B200_LIB") or os.path.join(_HERE, "libipt_b200.so")
 
 IPT_OK = 0
 IPT_ERR_INVALID = -1

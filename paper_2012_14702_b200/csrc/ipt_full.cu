@@ -604,7 +604,7 @@ bool use_ozaki(const FullProblem& P) {
 void ozaki_apply(FullProblem& P, const double* zs, double* zd, int mode, const LoopState* st) {
   cudaStream_t s = P.ctx->stream;
   const int64_t kpad = round_up(P.n, kOzakiKPad);
-  const int64_t arows = round_up(P.n, 256);
+  const int64_t arows = round_up(P.n, 512);  // the 256 x 512 pair tile of the INT8 GEMM
   if (!P.oz_delta_ready) {
     P.oz_delta.build(s, P.A1.get(), P.lda, P.n, P.n, arows, kpad);
     P.oz_delta_ready = true;

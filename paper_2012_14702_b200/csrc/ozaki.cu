@@ -66,20 +66,11 @@ constexpr Garner make_garner() {
 
 constexpr Garner kG = make_garner();
 
-template <int L>
-__device__ __forceinline__ int sym_mod_c(int x) {
-  constexpr int m = kG.m[L];
-  int r = x % m;
-  if (r < -(m >> 1)) r += m;
-  if (r >= (m - (m >> 1))) r -= m;  // even m: [-m/2, m/2); odd m: [-(m-1)/2, (m-1)/2]
-  return r;
-}
-
-__device__ __forceinline__ int sym_mod(int x, int m) {
-  int r = x % m;
-  if (r < -(m >> 1)) r += m;
-  if (r >= (m - (m >> 1))) r -= m;
-  return r;
+// |x| < m (a remainder after a rounded quotient) -> the symmetric range of m
+__device__ __forceinline__ int sym_fix_rt(int x, int m) {
+  const int lo = -(m >> 1), hi = m - (m >> 1) - 1;
+  x = x > hi ? x - m : x;
+  return x < lo ? x + m : x;
 }
 
 // compile-time loops over the moduli
@@ -107,22 +98,43 @@ __global__ void exponent_kernel(const double* __restrict__ X, int64_t ldx, int64
   }
 }
 
+// Symmetric remainder for a quotient estimate already applied: one correction step each way.
+template <int L, class T>
+__device__ __forceinline__ T sym_fix(T t) {
+  constexpr int m = kG.m[L];
+  constexpr T fm = T(m), lo = -T(m >> 1), hi = T(m - (m >> 1) - 1);
+  t = t > hi ? t - fm : t;
+  return t < lo ? t + fm : t;
+}
+
 // out[l][r][k] = sym(rint(x_rk 2^e_r) mod m_l) for all 16 moduli; zero padding for k >= len.
-__global__ void residues_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows, int64_t len,
-                                const int* __restrict__ e, int8_t* __restrict__ out, int64_t ldo, int64_t plane) {
-  const int64_t total = rows * ldo;
+// Eight consecutive k per thread (one 8-byte store per modulus plane).
+__global__ void __launch_bounds__(256) residues_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows,
+                                                       int64_t len, const int* __restrict__ e,
+                                                       int8_t* __restrict__ out, int64_t ldo, int64_t plane) {
+  const int64_t per_row = ldo >> 3;
+  const int64_t total = rows * per_row;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t r = t / ldo, k = t - r * ldo;
-    double y = 0.0;
+    const int64_t r = t / per_row, k0 = (t - r * per_row) << 3;
     const int er = e[r];
-    if (k < len && er != kOzakiNonFinite) y = rint(ldexp(X[r * ldx + k], er));
+    double y[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t k = k0 + q;
+      y[q] = (k < len && er != kOzakiNonFinite) ? rint(ldexp(X[r * ldx + k], er)) : 0.0;
+    }
+    int8_t* dst = out + r * ldo + k0;
     static_for<0, kMods>([&](auto L) {
       constexpr int l = decltype(L)::value;
-      constexpr int m = kG.m[l];
-      constexpr double minv = 1.0 / m;
-      const double q = rint(y * minv);
-      const int v = static_cast<int>(fma(-q, double(m), y));  // exact: |y - q m| < 2 m
-      out[l * plane + t] = static_cast<int8_t>(sym_mod_c<l>(v));
+      constexpr double m = kG.m[l], minv = 1.0 / kG.m[l];
+      uint32_t w[2] = {0u, 0u};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        // |y - rint(y/m) m| <= m/2 + 1 and the fma is exact, so one symmetric fix suffices
+        const double v = sym_fix<l>(fma(-rint(y[q] * minv), m, y[q]));
+        w[q >> 2] |= uint32_t(uint8_t(int8_t(static_cast<int>(v)))) << (8 * (q & 3));
+      }
+      *reinterpret_cast<uint2*>(dst + l * plane) = make_uint2(w[0], w[1]);
     });
   }
 }
@@ -142,7 +154,7 @@ struct ModStore {
       for (int b = 0; b < 4; ++b) {
         const int x = static_cast<int>(v[4 * q + b]);
         const int qq = __double2int_rn(double(x) * minv);
-        const int r = sym_mod(x - qq * m, m);
+        const int r = sym_fix_rt(x - qq * m, m);
         packed |= (uint32_t(uint8_t(int8_t(r)))) << (8 * b);
       }
       w[q] = packed;
@@ -153,60 +165,97 @@ struct ModStore {
   }
 };
 
+// W_8 = m_0 ... m_7 (< 2^64): the weight of the upper Horner half.
+constexpr unsigned long long kW8 = [] {
+  unsigned long long w = 1;
+  for (int l = 0; l < 8; ++l) w *= static_cast<unsigned long long>(kG.m[l]);
+  return w;
+}();
+
+// Exact signed value of the residue vector r (|value| < M/2), rounded to FP64 and scaled by 2^-es.
+// Garner mixed-radix digits in FP32: every intermediate is an integer below 2^24 in
+// magnitude (|sum of digit * c| < 15 * 128 * 255), so each FP32 operation is exact.
+__device__ __forceinline__ double garner_value(const int (&r)[kMods], int es) {
+  float dig[kMods] = {};
+  static_for<0, kMods>([&](auto L) {
+    constexpr int l = decltype(L)::value;
+    float s = float(r[l]);
+    static_for<0, l>([&](auto U) {
+      constexpr int u = decltype(U)::value;
+      constexpr float cu = float(kG.c[l][u]);
+      s = fmaf(-dig[u], cu, s);
+    });
+    constexpr float fm = float(kG.m[l]), minv = 1.0f / float(kG.m[l]), inv = float(kG.inv[l]);
+    const float t = sym_fix<l>(fmaf(-rintf(s * minv), fm, s)) * inv;
+    dig[l] = sym_fix<l>(fmaf(-rintf(t * minv), fm, t));
+  });
+  // value = hi * W_8 + lo, each half a Horner sum exact in int64 (|lo| < W_8 / 2, |hi| < 2^61)
+  long long lo = static_cast<long long>(dig[7]);
+  static_for<0, 7>([&](auto L) {
+    constexpr int l = 6 - decltype(L)::value;
+    constexpr long long m = kG.m[l];
+    lo = lo * m + static_cast<long long>(dig[l]);
+  });
+  long long hi = static_cast<long long>(dig[kMods - 1]);
+  static_for<0, kMods - 9>([&](auto L) {
+    constexpr int l = kMods - 2 - decltype(L)::value;
+    constexpr long long m = kG.m[l];
+    hi = hi * m + static_cast<long long>(dig[l]);
+  });
+  const __int128 p = static_cast<__int128>(hi) * static_cast<__int128>(kW8) + lo;
+  const bool neg = p < 0;
+  const unsigned __int128 mag = neg ? (unsigned __int128)(-p) : (unsigned __int128)p;
+  const double mg = double(uint64_t(mag >> 64)) * 18446744073709551616.0 + double(uint64_t(mag));
+  return ldexp(neg ? -mg : mg, -es);
+}
+
 // Reconstruct W_ij from the residues (R[l][j][i], j = column of B / Z, i = row of A) and
 // apply the IPT map (mode 0) or the closing residual (mode 1) with the K1 formulas.
+// Four consecutive rows i per thread (one 4-byte load per modulus plane; ldr % 4 == 0).
 __global__ void __launch_bounds__(256) reconstruct_map_kernel(OzakiMapArgs a) {
   if (a.state != nullptr && a.state->done) return;
   __shared__ double red[8][4];
   double v[4] = {0.0, 0.0, 0.0, 0.0};
-  const int64_t total = a.n * a.ncols;
+  const int64_t n4 = (a.n + 3) >> 2;
+  const int64_t total = n4 * a.ncols;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t j = t / a.n, i = t - j * a.n;
-    const int ea = a.eA[i], eb = a.eB[j];
-    double w;
-    if (ea == kOzakiNonFinite || eb == kOzakiNonFinite) {
-      w = __longlong_as_double(0x7ff8000000000000LL);  // NaN, as the FP64 product would give
-    } else {
-      int dig[kMods];
-      const int8_t* rp = a.R + j * a.ldr + i;
-      static_for<0, kMods>([&](auto L) {
-        constexpr int l = decltype(L)::value;
-        const int r = rp[l * a.plane];
-        int s = 0;
-        static_for<0, l>([&](auto U) {
-          constexpr int u = decltype(U)::value;
-          constexpr int cu = kG.c[l][u];
-          s += dig[u] * cu;
-        });
-        constexpr int inv = kG.inv[l];
-        dig[l] = sym_mod_c<l>(sym_mod_c<l>(r - s) * inv);
-      });
-      __int128 p = dig[kMods - 1];
-      static_for<0, kMods - 1>([&](auto L) {  // Horner from the top digit, exact in 128 bits
-        constexpr int l = kMods - 2 - decltype(L)::value;
-        constexpr int m = kG.m[l];
-        p = p * m + dig[l];
-      });
-      const bool neg = p < 0;
-      const unsigned __int128 mag = neg ? (unsigned __int128)(-p) : (unsigned __int128)p;
-      const double hi = double(uint64_t(mag >> 64)) * 18446744073709551616.0;
-      const double mg = hi + double(uint64_t(mag));
-      w = ldexp(neg ? -mg : mg, -(ea + eb));
-    }
-    const double z = a.Z[j * a.ldz + i];
+    const int64_t j = t / n4, i0 = (t - j * n4) << 2;
+    const int eb = a.eB[j];
+    const int8_t* rp = a.R + j * a.ldr + i0;
+    char4 res[kMods];
+#pragma unroll
+    for (int l = 0; l < kMods; ++l) res[l] = *reinterpret_cast<const char4*>(rp + l * a.plane);
     const int64_t jg = a.col0 + j;
-    const double di = a.d[i];
-    if (a.mode == 0) {
-      const double f = (i == jg) ? 1.0 : __ddiv_rn(__dsub_rn(__dmul_rn(z, a.wd[j]), w), __dsub_rn(di, a.d[jg]));
-      a.F[j * a.ldz + i] = f;
-      const double df = __dsub_rn(f, z);
-      v[0] = __fma_rn(df, df, v[0]);
-      v[1] = __fma_rn(z, z, v[1]);
-      v[2] = __fma_rn(f, f, v[2]);
-      v[3] = nan_max(v[3], fabs(df));
-    } else {
-      const double r = __dsub_rn(__dadd_rn(__dmul_rn(di, z), w), __dmul_rn(z, a.lam[j]));
-      v[0] = __fma_rn(r, r, v[0]);
+    const double dj = a.d[jg];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = i0 + q;
+      if (i >= a.n) break;
+      const int ea = a.eA[i];
+      double w;
+      if (ea == kOzakiNonFinite || eb == kOzakiNonFinite) {
+        w = __longlong_as_double(0x7ff8000000000000LL);  // NaN, as the FP64 product would give
+      } else {
+        int r[kMods];
+#pragma unroll
+        for (int l = 0; l < kMods; ++l)
+          r[l] = q == 0 ? res[l].x : q == 1 ? res[l].y : q == 2 ? res[l].z : res[l].w;
+        w = garner_value(r, ea + eb);
+      }
+      const double z = a.Z[j * a.ldz + i];
+      const double di = a.d[i];
+      if (a.mode == 0) {
+        const double f = (i == jg) ? 1.0 : __ddiv_rn(__dsub_rn(__dmul_rn(z, a.wd[j]), w), __dsub_rn(di, dj));
+        a.F[j * a.ldz + i] = f;
+        const double df = __dsub_rn(f, z);
+        v[0] = __fma_rn(df, df, v[0]);
+        v[1] = __fma_rn(z, z, v[1]);
+        v[2] = __fma_rn(f, f, v[2]);
+        v[3] = nan_max(v[3], fabs(df));
+      } else {
+        const double rr = __dsub_rn(__dadd_rn(__dmul_rn(di, z), w), __dmul_rn(z, a.lam[j]));
+        v[0] = __fma_rn(rr, rr, v[0]);
+      }
     }
   }
   block_reduce4<8>(v, red);
