@@ -183,6 +183,15 @@ void ipt_lu_free(ipt_lu* lu);
 int ipt_i8_gemm(ipt_ctx* ctx, int64_t M, int64_t N, int64_t K, const int8_t* A, const int8_t* B, int32_t* C,
                 int32_t iters, double* ms_per_gemm);
 
+/* FP64 GEMM by Ozaki scheme II on the INT8 tensor cores (the product behind
+ * IPT_PRODUCT_OZAKI): C (M x N, row-major) = A (M x K, row-major) . B (N x K, row-major)^T.
+ * Each row of A and of B is scaled by a power of two to 53-bit integers (row max in
+ * [2^52, 2^53)); every C_ij is the correctly rounded exact dot product of those integers,
+ * scaled back. Rows holding Inf or NaN give NaN. Host buffers; with iters > 0 also times
+ * that many device-resident products (kernels.cpp:23-86 is the FP64 product it stands for). */
+int ipt_ozaki_dgemm(ipt_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* A, const double* B, double* C,
+                    int32_t iters, double* ms_per_gemm);
+
 /* smallest_singular_value_estimate (solver.cpp:275-297). */
 int ipt_sigma_min(ipt_ctx* ctx, int64_t n, const double* z_re, const double* z_im,
                   int32_t max_iters, double tol, double* out);

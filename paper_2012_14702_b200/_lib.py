@@ -103,6 +103,7 @@ SIGNATURES = {
     "ipt_apply_map_full_csr": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, _i32p, _dp, _dp, _dp, _dp,
                                          _dp, _dp]),
     "ipt_i8_gemm": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, _vp, _vp, _vp, C.c_int32, _dp]),
+    "ipt_ozaki_dgemm": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, _dp, _dp, _dp, C.c_int32, _dp]),
     "ipt_lu_factor": (C.c_int, [_vp, C.c_int64, _dp, _dp, C.POINTER(_vp)]),
     "ipt_lu_from_host": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, C.c_int, C.POINTER(_vp)]),
     "ipt_lu_info": (C.c_int, [_vp, _i64p, C.POINTER(C.c_int)]),

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "dmma_gemm.cuh"
+#include "ozaki.cuh"
 #include "ipt_internal.cuh"
 
 using namespace iptb;
@@ -484,6 +485,37 @@ int ipt_i8_gemm(ipt_ctx* ctx, int64_t M, int64_t N, int64_t K, const int8_t* A, 
       *ms_per_gemm = ms / iters;
     }
     if (C) IPT_CUDA(cudaMemcpy(C, dC.get(), size_t(M) * N * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int ipt_ozaki_dgemm(ipt_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* A, const double* B, double* C,
+                    int32_t iters, double* ms_per_gemm) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    Ctx& c = ctx->c;
+    if (M < 0 || N < 0 || K < 0) throw InvalidArgument("ozaki dgemm: negative size");
+    if ((M * K > 0 && !A) || (N * K > 0 && !B) || (M * N > 0 && !C)) throw InvalidArgument("ozaki dgemm: null buffer");
+    if (M == 0 || N == 0) return;
+    DevBuf dA, dB, dC, part;
+    dA.alloc(size_t(std::max<int64_t>(M * K, 1)), false);
+    dB.alloc(size_t(std::max<int64_t>(N * K, 1)), false);
+    dC.alloc(size_t(M * N), false);
+    if (K > 0) {
+      h2d_rows(c, dA.get(), K, A, K, M, K);
+      h2d_rows(c, dB.get(), K, B, K, N, K);
+    }
+    ozaki_dgemm_device(c.stream, M, N, K, dA.get(), dB.get(), dC.get(), part);
+    if (iters > 0 && ms_per_gemm) {
+      IPT_CUDA(cudaEventRecord(c.ev[0], c.stream));
+      for (int i = 0; i < iters; ++i) ozaki_dgemm_device(c.stream, M, N, K, dA.get(), dB.get(), dC.get(), part);
+      IPT_CUDA(cudaEventRecord(c.ev[1], c.stream));
+      c.sync();
+      float ms = 0.f;
+      IPT_CUDA(cudaEventElapsedTime(&ms, c.ev[0], c.ev[1]));
+      *ms_per_gemm = ms / iters;
+    }
+    d2h_rows(c, C, N, dC.get(), N, M, N);
   });
 }
 

@@ -19,6 +19,7 @@
 // Everything is integer-exact up to the single rounding of P and of the scaling, so the
 // result is deterministic and as accurate as an FP64 GEMM; non-finite inputs are routed
 // to the DMMA path by the caller.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <type_traits>
@@ -107,6 +108,24 @@ __device__ __forceinline__ T sym_fix(T t) {
   return t < lo ? t + fm : t;
 }
 
+// Rounding and conversion of integer-valued floats by the 1.5 * 2^p shifter: plain adds on
+// the FMA pipes instead of FRND / F2I on the conversion pipe. Exact for |x| < 2^22 (FP32)
+// and |x| < 2^51 (FP64); ties to even like rint.
+__device__ __forceinline__ float rint_small(float x) { return __fsub_rn(__fadd_rn(x, 12582912.0f), 12582912.0f); }
+__device__ __forceinline__ int int_small(float x) { return __float_as_int(__fadd_rn(x, 12582912.0f)) - 0x4B400000; }
+__device__ __forceinline__ float float_small(int x) { return __fsub_rn(__int_as_float(0x4B400000 + x), 12582912.0f); }
+__device__ __forceinline__ double rint_small(double x) {
+  return __dsub_rn(__dadd_rn(x, 6755399441055744.0), 6755399441055744.0);
+}
+__device__ __forceinline__ int int_small(double x) { return __double2loint(__dadd_rn(x, 6755399441055744.0)); }
+
+// x * 2^k: a multiplication by an exact power of two is correctly rounded, so it equals
+// ldexp whenever 2^k is a normal double.
+__device__ __forceinline__ double scale2(double x, int k) {
+  if (k >= -1022 && k <= 1023) return x * __longlong_as_double(static_cast<long long>(k + 1023) << 52);
+  return ldexp(x, k);
+}
+
 // out[l][r][k] = sym(rint(x_rk 2^e_r) mod m_l) for all 16 moduli; zero padding for k >= len.
 // Eight consecutive k per thread (one 8-byte store per modulus plane).
 __global__ void __launch_bounds__(256) residues_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows,
@@ -121,7 +140,7 @@ __global__ void __launch_bounds__(256) residues_kernel(const double* __restrict_
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int64_t k = k0 + q;
-      y[q] = (k < len && er != kOzakiNonFinite) ? rint(ldexp(X[r * ldx + k], er)) : 0.0;
+      y[q] = (k < len && er != kOzakiNonFinite) ? rint(scale2(X[r * ldx + k], er)) : 0.0;
     }
     int8_t* dst = out + r * ldo + k0;
     static_for<0, kMods>([&](auto L) {
@@ -130,9 +149,10 @@ __global__ void __launch_bounds__(256) residues_kernel(const double* __restrict_
       uint32_t w[2] = {0u, 0u};
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        // |y - rint(y/m) m| <= m/2 + 1 and the fma is exact, so one symmetric fix suffices
-        const double v = sym_fix<l>(fma(-rint(y[q] * minv), m, y[q]));
-        w[q >> 2] |= uint32_t(uint8_t(int8_t(static_cast<int>(v)))) << (8 * (q & 3));
+        // |y / m| < 2^46; |y - rint(y/m) m| <= m/2 + 1 and the fma is exact, so one symmetric
+        // fix suffices
+        const int v = sym_fix<l>(int_small(fma(-rint_small(y[q] * minv), m, y[q])));
+        w[q >> 2] |= uint32_t(uint8_t(int8_t(v))) << (8 * (q & 3));
       }
       *reinterpret_cast<uint2*>(dst + l * plane) = make_uint2(w[0], w[1]);
     });
@@ -172,45 +192,70 @@ constexpr unsigned long long kW8 = [] {
   return w;
 }();
 
-// Exact signed value of the residue vector r (|value| < M/2), rounded to FP64 and scaled by 2^-es.
-// Garner mixed-radix digits in FP32: every intermediate is an integer below 2^24 in
-// magnitude (|sum of digit * c| < 15 * 128 * 255), so each FP32 operation is exact.
+// The nearest double to an unsigned 128-bit integer (ties to even): its 64 leading bits with
+// a sticky LSB for everything below, one correctly rounded U64 -> F64 conversion, and an
+// exact power-of-two scaling.
+__device__ __forceinline__ double u128_to_double(unsigned __int128 x) {
+  const uint64_t hi = uint64_t(x >> 64), lo = uint64_t(x);
+  if (hi == 0) return __ull2double_rn(lo);
+  const int lz = __clzll(static_cast<long long>(hi));
+  const uint64_t top = lz ? (hi << lz) | (lo >> (64 - lz)) : hi;
+  const uint64_t rest = lo << lz;
+  const double t = __ull2double_rn(top | (rest != 0 ? 1ull : 0ull));
+  return t * __longlong_as_double(static_cast<long long>(64 - lz + 1023) << 52);
+}
+
+// Exact signed value of the residue vector r (canonical residues, |value| < M/2), rounded to
+// the nearest FP64 and scaled by 2^-es (a second rounding only for a subnormal result). Garner mixed-radix digits in FP32: every intermediate is an
+// integer below 2^24 in magnitude (|sum of digit * c| < 15 * 128 * 255), so each FP32
+// operation is exact.
 __device__ __forceinline__ double garner_value(const int (&r)[kMods], int es) {
   float dig[kMods] = {};
   static_for<0, kMods>([&](auto L) {
     constexpr int l = decltype(L)::value;
-    float s = float(r[l]);
+    float s = float_small(r[l]);
     static_for<0, l>([&](auto U) {
       constexpr int u = decltype(U)::value;
       constexpr float cu = float(kG.c[l][u]);
       s = fmaf(-dig[u], cu, s);
     });
-    constexpr float fm = float(kG.m[l]), minv = 1.0f / float(kG.m[l]), inv = float(kG.inv[l]);
-    const float t = sym_fix<l>(fmaf(-rintf(s * minv), fm, s)) * inv;
-    dig[l] = sym_fix<l>(fmaf(-rintf(t * minv), fm, t));
+    if constexpr (l == 0) {
+      dig[0] = s;  // m_0 = 256 and the stored residue is already canonical
+    } else {
+      // any small representative of (r - s) mod m will do before the multiply by the inverse
+      constexpr float fm = float(kG.m[l]), minv = 1.0f / float(kG.m[l]), inv = float(kG.inv[l]);
+      const float t = fmaf(-rint_small(s * minv), fm, s) * inv;  // |t| < 1.5 m * inv < 2^17
+      // m odd: the exact t / m is >= 1 / (2m) from a half-integer and the computed quotient is
+      // within 3e-4 of it, so rint gives the exact nearest quotient and the symmetric digit
+      dig[l] = fmaf(-rint_small(t * minv), fm, t);
+    }
   });
-  // value = hi * W_8 + lo, each half a Horner sum exact in int64 (|lo| < W_8 / 2, |hi| < 2^61)
-  long long lo = static_cast<long long>(dig[7]);
-  static_for<0, 7>([&](auto L) {
-    constexpr int l = 6 - decltype(L)::value;
-    constexpr long long m = kG.m[l];
-    lo = lo * m + static_cast<long long>(dig[l]);
+  // Digit pairs P_k = dig_2k + m_2k dig_2k+1 (|P_k| < 2^16, exact in FP32), then
+  // value = hi * W_8 + lo with each half a Horner sum over pairs, exact in int64
+  // (|lo| < W_8 / 2, |hi| < 2^61).
+  int pr[kMods / 2];
+  static_for<0, kMods / 2>([&](auto K) {
+    constexpr int k = decltype(K)::value;
+    constexpr float m = float(kG.m[2 * k]);
+    pr[k] = int_small(fmaf(dig[2 * k + 1], m, dig[2 * k]));
   });
-  long long hi = static_cast<long long>(dig[kMods - 1]);
-  static_for<0, kMods - 9>([&](auto L) {
-    constexpr int l = kMods - 2 - decltype(L)::value;
-    constexpr long long m = kG.m[l];
-    hi = hi * m + static_cast<long long>(dig[l]);
+  long long lo = pr[3], hi = pr[7];
+  static_for<0, 3>([&](auto K) {
+    constexpr int k = 2 - decltype(K)::value;
+    constexpr long long ml = static_cast<long long>(kG.m[2 * k]) * kG.m[2 * k + 1];
+    constexpr long long mh = static_cast<long long>(kG.m[2 * k + 8]) * kG.m[2 * k + 9];
+    lo = lo * ml + pr[k];
+    hi = hi * mh + pr[k + 4];
   });
   const __int128 p = static_cast<__int128>(hi) * static_cast<__int128>(kW8) + lo;
   const bool neg = p < 0;
-  const unsigned __int128 mag = neg ? (unsigned __int128)(-p) : (unsigned __int128)p;
-  const double mg = double(uint64_t(mag >> 64)) * 18446744073709551616.0 + double(uint64_t(mag));
-  return ldexp(neg ? -mg : mg, -es);
+  const double mg = u128_to_double(neg ? (unsigned __int128)(-p) : (unsigned __int128)p);
+  return scale2(neg ? -mg : mg, -es);
 }
 
 // Reconstruct W_ij from the residues (R[l][j][i], j = column of B / Z, i = row of A) and
-// apply the IPT map (mode 0) or the closing residual (mode 1) with the K1 formulas.
+// apply the IPT map (mode 0) or the closing residual (mode 1) with the K1 formulas, or
+// store W itself (mode 2).
 // Four consecutive rows i per thread (one 4-byte load per modulus plane; ldr % 4 == 0).
 __global__ void __launch_bounds__(256) reconstruct_map_kernel(OzakiMapArgs a) {
   if (a.state != nullptr && a.state->done) return;
@@ -226,7 +271,7 @@ __global__ void __launch_bounds__(256) reconstruct_map_kernel(OzakiMapArgs a) {
 #pragma unroll
     for (int l = 0; l < kMods; ++l) res[l] = *reinterpret_cast<const char4*>(rp + l * a.plane);
     const int64_t jg = a.col0 + j;
-    const double dj = a.d[jg];
+    const double dj = a.mode == 0 ? a.d[jg] : 0.0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int64_t i = i0 + q;
@@ -241,6 +286,10 @@ __global__ void __launch_bounds__(256) reconstruct_map_kernel(OzakiMapArgs a) {
         for (int l = 0; l < kMods; ++l)
           r[l] = q == 0 ? res[l].x : q == 1 ? res[l].y : q == 2 ? res[l].z : res[l].w;
         w = garner_value(r, ea + eb);
+      }
+      if (a.mode == 2) {
+        a.F[j * a.ldz + i] = w;
+        continue;
       }
       const double z = a.Z[j * a.ldz + i];
       const double di = a.d[i];
@@ -303,6 +352,36 @@ void ozaki_reconstruct(cudaStream_t s, const OzakiMapArgs& a) {
   reconstruct_map_kernel<<<kOzakiGrid, 256, 0, s>>>(a);
   IPT_LAUNCH_CHECK();
   count_launch();
+}
+
+void ozaki_dgemm_device(cudaStream_t s, int64_t M, int64_t N, int64_t K, const double* A, const double* B,
+                        double* C, DevBuf& partials) {
+  if (M <= 0 || N <= 0) return;
+  const int64_t kpad = round_up(std::max<int64_t>(K, 1), kOzakiKPad);
+  // product rows = rows of A (the GEMM's M side, 256-row pair tiles), columns = rows of B
+  // (N side, 512-wide tiles), so the reconstruction writes C row-major
+  const int64_t mpad = round_up(M, 256), npad = round_up(N, 512);
+  OzakiOperand opa, opb;
+  opa.build(s, A, K, M, K, mpad, kpad);
+  opb.build(s, B, K, N, K, npad, kpad);
+  DevBuf R;
+  int64_t plane = 0;
+  ozaki_products(s, opa, opb, mpad, npad, R, plane);
+  if (partials.count < size_t(kOzakiGrid) * 4) partials.alloc(size_t(kOzakiGrid) * 4, false);
+  OzakiMapArgs a{};
+  a.R = reinterpret_cast<const int8_t*>(R.get());
+  a.plane = plane;
+  a.ldr = npad;
+  a.eA = opb.exps();
+  a.eB = opa.exps();
+  a.F = C;
+  a.ldz = N;
+  a.n = N;
+  a.ncols = M;
+  a.mode = 2;
+  a.partials = partials.get();
+  ozaki_reconstruct(s, a);
+  IPT_CUDA(cudaStreamSynchronize(s));  // the local operand and residue buffers die here
 }
 
 }  // namespace iptb

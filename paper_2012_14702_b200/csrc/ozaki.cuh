@@ -33,7 +33,7 @@ struct OzakiMapArgs {
   const double* wd;
   const double* lam;
   int64_t n, ncols, col0;
-  int mode;  // 0: map, 1: closing residual
+  int mode;  // 0: map, 1: closing residual, 2: store W
   double* partials;
   const LoopState* state;
 };
@@ -41,5 +41,11 @@ struct OzakiMapArgs {
 void ozaki_products(cudaStream_t s, const OzakiOperand& Zop, const OzakiOperand& Aop, int64_t zrows_pad,
                     int64_t arows_pad, DevBuf& R, int64_t& plane);
 void ozaki_reconstruct(cudaStream_t s, const OzakiMapArgs& a);
+
+// C (M x N, row-major, ldc = N) = A (M x K, row-major) . B (N x K, row-major)^T in FP64 by
+// Ozaki scheme II, device pointers: each element is the correctly rounded exact dot product
+// of the rows scaled to 53-bit integers (row max in [2^52, 2^53)).
+void ozaki_dgemm_device(cudaStream_t s, int64_t M, int64_t N, int64_t K, const double* A, const double* B,
+                        double* C, DevBuf& partials);
 
 }  // namespace iptb

@@ -694,6 +694,26 @@ class kernels:  # noqa: N801  (namespace ipt::kernels)
         return _combine(cr, ci, cx)
 
     @staticmethod
+    def matmul_ozaki(a, b, ctx: Optional[Context] = None) -> np.ndarray:
+        """C = A B for real A, B by Ozaki scheme II on the INT8 tensor cores (B200
+        extension; the product of `product="ozaki"`): each row of A and column of B is
+        scaled by a power of two to 53-bit integers and every C_ij is the correctly rounded
+        exact dot product of those integers, scaled back."""
+        a, b = np.asarray(a), np.asarray(b)
+        if np.iscomplexobj(a) or np.iscomplexobj(b):
+            raise ValueError("matmul_ozaki: real operands only")
+        if a.ndim != 2 or b.ndim != 2 or a.shape[1] != b.shape[0]:
+            raise ValueError("matmul_ozaki: inner dimensions differ")
+        ctx = ctx or default_context()
+        m, k = a.shape
+        n = b.shape[1]
+        ar = np.ascontiguousarray(a, dtype=np.float64)
+        bt = np.ascontiguousarray(b.T, dtype=np.float64)
+        c = np.empty((m, n))
+        check(_lib.load().ipt_ozaki_dgemm(ctx.handle, m, n, k, dptr(ar), dptr(bt), dptr(c), 0, None))
+        return c
+
+    @staticmethod
     def matvec(a: Matrix, x, ctx: Optional[Context] = None) -> np.ndarray:
         """y = A x, dense or CSR (kernels.cpp:112-140)."""
         ctx = ctx or default_context()

@@ -2,6 +2,8 @@
 INT8 GEMM is exact, and the full-spectrum solve with product='ozaki' matches the DMMA
 solve (and therefore the reference) far inside the north_star tolerances."""
 import ctypes as C
+import math
+import os
 
 import numpy as np
 import pytest
@@ -24,6 +26,86 @@ def test_i8_gemm_is_exact(shape):
     ctx = ipt.default_context()
     check(_lib.load().ipt_i8_gemm(ctx.handle, M, N, K, a.ctypes.data, b.ctypes.data, c.ctypes.data, 0, C.byref(ms)))
     assert np.array_equal(c, a.astype(np.int64) @ b.astype(np.int64).T)
+
+
+@pytest.mark.parametrize("kind", ["1sm", "mc", "2sm", "2sm512"])
+def test_i8_gemm_kernel_variants_are_exact(kind, monkeypatch):
+    """Every tile schedule (one SM, B multicast over a CTA pair, cta_group::2 with
+    256 x 256 and 256 x 512 pair tiles) gives the exact int32 product."""
+    monkeypatch.setenv("IPT_I8_KERNEL", kind)
+    M, N, K = 512, 1024, 640
+    rng = np.random.default_rng(7)
+    a = rng.integers(-128, 128, (M, K), dtype=np.int8)
+    b = rng.integers(-128, 128, (N, K), dtype=np.int8)
+    c = np.empty((M, N), np.int32)
+    ctx = ipt.default_context()
+    check(_lib.load().ipt_i8_gemm(ctx.handle, M, N, K, a.ctypes.data, b.ctypes.data, c.ctypes.data, 0, None))
+    assert np.array_equal(c, a.astype(np.int64) @ b.astype(np.int64).T)
+
+
+def _row_exponents(x):
+    """52 - ilogb(row max): the row scaling of ozaki.cu's exponent_kernel (None: non-finite)."""
+    out = []
+    for row in x:
+        mx = float(np.max(np.abs(row))) if row.size else 0.0
+        out.append(None if not math.isfinite(mx) else 0 if mx == 0.0 else 52 - (math.frexp(mx)[1] - 1))
+    return out
+
+
+def _exact_ozaki(a, bt):
+    """C_ij = the correctly rounded exact dot product of row i of A and row j of B^T, both
+    scaled to 53-bit integers, scaled back: Python integers, CPython's correctly rounded
+    int -> float, and ldexp (exact but for subnormal results)."""
+    ea, eb = _row_exponents(a), _row_exponents(bt)
+
+    def ints(x, e):
+        return np.array([[int(np.rint(math.ldexp(float(v), e[i]))) if e[i] is not None else 0 for v in x[i]]
+                         for i in range(x.shape[0])], dtype=object).reshape(x.shape)
+
+    p = ints(a, ea).dot(ints(bt, eb).T) if a.shape[1] else np.zeros((a.shape[0], bt.shape[0]), dtype=object)
+    c = np.empty(p.shape)
+    for i in range(p.shape[0]):
+        for j in range(p.shape[1]):
+            c[i, j] = math.nan if ea[i] is None or eb[j] is None else math.ldexp(float(p[i, j]), -(ea[i] + eb[j]))
+    return c
+
+
+@pytest.mark.parametrize("m,n,k", [(70, 45, 300), (33, 130, 2000), (1, 1, 1), (5, 7, 0)])
+def test_ozaki_dgemm_is_the_rounded_exact_product(m, n, k):
+    """Bitwise: the Garner reconstruction, the 128-bit Horner sum and the int128 -> FP64
+    rounding reproduce the exact integer product of the scaled operands, rounded once."""
+    rng = np.random.default_rng(m * 1000 + n + k)
+    a = rng.standard_normal((m, k)) * np.exp2(rng.integers(-40, 40, (m, 1)))
+    b = rng.standard_normal((k, n)) * np.exp2(rng.integers(-40, 40, (1, n)))
+    if k > 4:
+        a[0, :3] *= 2.0 ** -45  # far below the row max: truncated by the 53-bit scaling
+        b[1, -1] = 0.0
+    if m > 3:
+        a[2] = 0.0  # zero row
+    c = ipt.kernels.matmul_ozaki(a, b)
+    ref = _exact_ozaki(a, np.ascontiguousarray(b.T))
+    assert c.shape == (m, n)
+    assert np.array_equal(c.view(np.int64), ref.view(np.int64)), np.max(np.abs(c - ref))
+    if k:
+        bound = 4 * k * np.finfo(float).eps * (np.abs(a) @ np.abs(b))
+        assert np.all(np.abs(c - a @ b) <= bound + 1e-300)
+
+
+def test_ozaki_dgemm_nonfinite_rows_give_nan():
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((9, 50))
+    b = rng.standard_normal((50, 6))
+    a[4, 7] = np.inf
+    b[3, 2] = np.nan
+    c = ipt.kernels.matmul_ozaki(a, b)
+    assert np.all(np.isnan(c[4, :])) and np.all(np.isnan(c[:, 2]))
+    mask = np.ones_like(c, bool)
+    mask[4, :] = False
+    mask[:, 2] = False
+    assert np.all(np.isfinite(c[mask]))
+    with np.errstate(invalid="ignore"):
+        ref = a @ b
+    assert np.allclose(c[mask], ref[mask], rtol=1e-13, atol=1e-13)
 
 
 @pytest.mark.parametrize("n", [64, 300, 1000, 2048])
