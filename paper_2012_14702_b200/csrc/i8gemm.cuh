@@ -70,11 +70,23 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 constexpr uint32_t kI8Idesc = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kI8BN >> 3) << 17) |
                               (uint32_t(kI8BM >> 4) << 24);
 
+// Grouped rasterisation: `group` consecutive M tiles sweep the N tiles together, so the
+// CTAs resident at one time share both their A and their B tiles in L2 (M-fastest order
+// over all of M re-streams A from DRAM once per N tile).
+__device__ __forceinline__ void grouped_tile(int t, int tiles_m, int tiles_n, int group, int& tm, int& tn) {
+  const int per_group = group * tiles_n;
+  const int g = t / per_group, first = g * group;
+  const int gs = min(group, tiles_m - first);
+  const int r = t - g * per_group;
+  tm = first + r % gs;
+  tn = r / gs;
+}
+
 // Epi(row, col0, v[32]) consumes columns col0..col0+31 of one row.
 template <class Epi>
 __global__ void __launch_bounds__(kI8Threads, 1)
     i8gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K, int tiles_m,
-                  Epi epi) {
+                  int tiles_n, int group, Epi epi) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -83,7 +95,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
   uint64_t* acc_full = empty + kI8Stages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tm = blockIdx.x % tiles_m, tn = blockIdx.x / tiles_m;
+  int tm, tn;
+  grouped_tile(blockIdx.x, tiles_m, tiles_n, group, tm, tn);
   const int m0 = tm * kI8BM, n0 = tn * kI8BN;
   const int KB = K / kI8BK;
 
@@ -188,7 +201,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 template <class Epi>
 __global__ void __launch_bounds__(kI8Threads, 1)
     i8gemm_mc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
-                     int tiles_m, Epi epi) {
+                     int tiles_m, int tiles_n, int group, Epi epi) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -200,7 +213,9 @@ __global__ void __launch_bounds__(kI8Threads, 1)
   const int rank = static_cast<int>(cluster_rank());
   const int pairs_m = tiles_m / 2;
   const int cl = blockIdx.x >> 1;
-  const int tm = 2 * (cl % pairs_m) + rank, tn = cl / pairs_m;
+  int pm, tn;
+  grouped_tile(cl, pairs_m, tiles_n, group, pm, tn);
+  const int tm = 2 * pm + rank;
   const int m0 = tm * kI8BM, n0 = tn * kI8BN;
   const int KB = K / kI8BK;
   constexpr uint16_t kBoth = 0x3;
@@ -320,7 +335,7 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* ma
 template <class Epi, int NB>
 __global__ void __launch_bounds__(kI8Threads, 1)
     i8gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
-                      int pairs_m, Epi epi) {
+                      int pairs_m, int tiles_n, int group, Epi epi) {
   using Cfg = I8S2<NB>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base =
@@ -332,7 +347,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = static_cast<int>(cluster_rank());
   const int cl = blockIdx.x >> 1;
-  const int pm = cl % pairs_m, tn = cl / pairs_m;
+  int pm, tn;
+  grouped_tile(cl, pairs_m, tiles_n, group, pm, tn);
   const int m0 = pm * 256 + rank * 128;  // this CTA's accumulator rows
   const int n0 = tn * (256 * NB);
   const int KB = K / kI8BK;
@@ -433,6 +449,9 @@ void launch_i8gemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, const int8_t
     attr = true;
   }
   const int tiles_m = static_cast<int>(M / kI8BM);
+  // IPT_I8_GROUP: M tiles (pairs for the 2-SM kernels) per rasterisation group
+  const char* genv = std::getenv("IPT_I8_GROUP");
+  const int group = genv && std::atoi(genv) > 0 ? std::atoi(genv) : 8;
   const unsigned grid = static_cast<unsigned>(tiles_m * (N / kI8BN));
   // IPT_I8_KERNEL: 2sm (default when M % 256 == 0), mc (B multicast pair), 1sm
   const char* kenv = std::getenv("IPT_I8_KERNEL");
@@ -454,9 +473,11 @@ void launch_i8gemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, const int8_t
     cfg.attrs = at;
     cfg.numAttrs = 1;
     if (wide)
-      IPT_CUDA(cudaLaunchKernelEx(&cfg, i8gemm_2sm_kernel<Epi, 2>, ma2, mb2, static_cast<int>(K), tiles_m / 2, epi));
+      IPT_CUDA(cudaLaunchKernelEx(&cfg, i8gemm_2sm_kernel<Epi, 2>, ma2, mb2, static_cast<int>(K), tiles_m / 2,
+                                  static_cast<int>(N / 512), group, epi));
     else
-      IPT_CUDA(cudaLaunchKernelEx(&cfg, i8gemm_2sm_kernel<Epi, 1>, ma2, mb2, static_cast<int>(K), tiles_m / 2, epi));
+      IPT_CUDA(cudaLaunchKernelEx(&cfg, i8gemm_2sm_kernel<Epi, 1>, ma2, mb2, static_cast<int>(K), tiles_m / 2,
+                                  static_cast<int>(N / 256), group, epi));
     IPT_LAUNCH_CHECK();
     count_launch();
     return;
@@ -477,9 +498,11 @@ void launch_i8gemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, const int8_t
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    IPT_CUDA(cudaLaunchKernelEx(&cfg, i8gemm_mc_kernel<Epi>, ma, mb, static_cast<int>(K), tiles_m, epi));
+    IPT_CUDA(cudaLaunchKernelEx(&cfg, i8gemm_mc_kernel<Epi>, ma, mb, static_cast<int>(K), tiles_m,
+                                static_cast<int>(N / kI8BN), group, epi));
   } else {
-    i8gemm_kernel<Epi><<<grid, kI8Threads, kI8SmemBytes, s>>>(ma, mb, static_cast<int>(K), tiles_m, epi);
+    i8gemm_kernel<Epi><<<grid, kI8Threads, kI8SmemBytes, s>>>(ma, mb, static_cast<int>(K), tiles_m,
+                                                                   static_cast<int>(N / kI8BN), group, epi);
   }
   IPT_LAUNCH_CHECK();
   count_launch();

@@ -21,12 +21,13 @@ from paper_2012_14702_b200.ipt import _params
 pytestmark = pytest.mark.gpu
 
 
-def _run(upload, n, warm, iters, want_block, ncols):
+def _run(upload, n, warm, iters, want_block, ncols, product=_lib.PRODUCT_DMMA):
     lib = _lib.load()
     ctx = ipt.default_context()
     h = C.c_void_p()
     check(upload(ctx, C.byref(h)))
     try:
+        check(lib.ipt_full_set_product(h, product))
         wr = None if warm is None else np.ascontiguousarray(warm.real)
         wi = None if warm is None or not np.iscomplexobj(warm) else np.ascontiguousarray(warm.imag)
         check(lib.ipt_full_reset(ctx.handle, h, dptr(wr), dptr(wi)))
@@ -46,19 +47,19 @@ def _run(upload, n, warm, iters, want_block, ncols):
         lib.ipt_full_free(h)
 
 
-def dense_runs(d, dr, di, warm, iters, blocks):
+def dense_runs(d, dr, di, warm, iters, blocks, product=_lib.PRODUCT_DMMA):
     lib = _lib.load()
     n = len(d)
 
     def full(ctx, out):
         return lib.ipt_full_upload(ctx.handle, n, dptr(d), None, dptr(dr), dptr(di), out)
 
-    ref = _run(full, n, warm, iters, False, n)
+    ref = _run(full, n, warm, iters, False, n, product)
     outs = []
     for b, e in blocks:
         def up(ctx, out, b=b, e=e):
             return lib.ipt_full_upload_columns(ctx.handle, n, dptr(d), None, dptr(dr), dptr(di), b, e, out)
-        outs.append(((b, e), _run(up, n, warm, iters, True, e - b)))
+        outs.append(((b, e), _run(up, n, warm, iters, True, e - b, product)))
     return ref, outs
 
 
@@ -94,6 +95,20 @@ def test_real_dense_blocks_from_warm_start():
     np.fill_diagonal(warm, 1.0)
     ref, outs = dense_runs(p.d, np.ascontiguousarray(p.delta), None, warm, 3, BLOCKS)
     check_blocks(ref, outs, n)
+
+
+@pytest.mark.parametrize("iters", [1, 3])
+def test_ozaki_blocks(iters):
+    """The Ozaki-product map (residues per Z column, exact integer products, one rounding
+    per entry) is column-local too: blocks reproduce the whole run bit for bit."""
+    n = 700
+    p = synth.dense_uniform(n, 0.3 / np.sqrt(n), 9)
+    rng = np.random.default_rng(2)
+    warm = np.eye(n) + 1e-3 * rng.standard_normal((n, n))
+    np.fill_diagonal(warm, 1.0)
+    for w in (None, warm):
+        ref, outs = dense_runs(p.d, np.ascontiguousarray(p.delta), None, w, iters, BLOCKS, _lib.PRODUCT_OZAKI)
+        check_blocks(ref, outs, n)
 
 
 def test_complex_blocks():

@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 import paper_2012_14702_b200 as ipt
+from conftest import golden
 from paper_2012_14702_b200 import _lib, synth
 from paper_2012_14702_b200._lib import check
 
@@ -29,11 +30,14 @@ def test_i8_gemm_is_exact(shape):
 
 
 @pytest.mark.parametrize("kind", ["1sm", "mc", "2sm", "2sm512"])
-def test_i8_gemm_kernel_variants_are_exact(kind, monkeypatch):
+@pytest.mark.parametrize("group", ["1", "3", "8", "1000"])
+def test_i8_gemm_kernel_variants_are_exact(kind, group, monkeypatch):
     """Every tile schedule (one SM, B multicast over a CTA pair, cta_group::2 with
-    256 x 256 and 256 x 512 pair tiles) gives the exact int32 product."""
+    256 x 256 and 256 x 512 pair tiles) under every rasterisation grouping (including a
+    ragged last group) gives the exact int32 product."""
     monkeypatch.setenv("IPT_I8_KERNEL", kind)
-    M, N, K = 512, 1024, 640
+    monkeypatch.setenv("IPT_I8_GROUP", group)
+    M, N, K = 1280, 1024, 640
     rng = np.random.default_rng(7)
     a = rng.integers(-128, 128, (M, K), dtype=np.int8)
     b = rng.integers(-128, 128, (N, K), dtype=np.int8)
@@ -152,3 +156,43 @@ def test_ozaki_nonfinite_delta_falls_back():
     p = ipt.Partition(d, delta)
     r = ipt.solve_full(p, ipt.build_gaps(p), product="ozaki")
     assert r.status == ipt.SolveStatus.Diverged and r.iterations == 1
+
+
+# ------------------------------------------------ parity with the reference (golden fixtures)
+
+
+def _frob(p):
+    return math.sqrt(np.sum(p.delta ** 2) + np.sum(p.d ** 2))
+
+
+@pytest.mark.parametrize("tag", ["rel_fro_tol12", "max_abs_tol12", "rel_fro_default"])
+def test_ozaki_config1_matches_reference(tag):
+    """configs[0] (N = 1024) with W = Delta Z by Ozaki scheme II against the reference
+    build's own solve_full (tests/golden/config1.npz), north_star tolerances."""
+    g = golden("config1.npz")
+    p = synth.config1()
+    rule = "max_abs" if tag.startswith("max_abs") else "rel_fro"
+    tol = 100 * np.finfo(float).eps if tag.endswith("default") else 1e-12
+    r = ipt.solve_full(p, ipt.build_gaps(p), ipt.IterationConfig(tolerance=tol, stop_rule=rule), product="ozaki")
+    meta = g[tag + "_meta"]
+    assert r.status == ipt.SolveStatus.Converged
+    assert abs(r.iterations - int(meta[0])) <= 1
+    lam = g[tag + "_lam"]
+    assert np.max(np.abs(r.eigenvalues - lam) / np.abs(lam)) <= 1e-10
+    assert np.max(np.abs(r.Z[:, g["cols"]] - g[tag + "_cols"])) <= 1e-9
+    assert r.residual_frobenius <= 1e-10 * _frob(p)
+    assert np.all(np.diag(r.Z) == 1.0)
+
+
+def test_ozaki_config2_matches_reference_columns():
+    """configs[1] (N = 8192): columns of the reference's solve_single(j) (the column route
+    of SURVEY 8c, tests/golden/full_columns.npz) and the SURVEY 8(d) anchor."""
+    p = synth.config2()
+    r = ipt.solve_full(p, ipt.build_gaps(p), ipt.IterationConfig(tolerance=1e-12), product="ozaki")
+    assert r.status == ipt.SolveStatus.Converged and abs(r.iterations - 5) <= 1
+    assert r.eigenvalues[0] == pytest.approx(0.999960499073907, abs=1e-13)
+    assert r.residual_frobenius <= 1e-10 * _frob(p)
+    g = golden("full_columns.npz")
+    cols, lam = g["n8192_cols"], g["n8192_lam"]
+    assert np.max(np.abs(r.eigenvalues[cols] - lam) / np.abs(lam)) <= 1e-10
+    assert np.max(np.abs(r.Z[:, cols] - g["n8192_z"])) <= 1e-9
