@@ -597,7 +597,7 @@ void allreduce_sums(FullProblem& P, bool with_max) {
 }
 
 bool use_ozaki(const FullProblem& P) {
-  return P.product == IPT_PRODUCT_OZAKI && !P.cplx && !P.sparse && P.delta_finite;
+  return P.product == IPT_PRODUCT_OZAKI && !P.cplx && !P.sparse && P.delta_finite && P.n <= kOzakiMaxK;
 }
 
 // W = Delta Z by Ozaki scheme II, then the map (mode 0) or the closing residual (mode 1).

@@ -159,12 +159,36 @@ __global__ void __launch_bounds__(256) residues_kernel(const double* __restrict_
   }
 }
 
+// Division by a modulus m <= 256 without conversions: for 0 <= u < 2^31,
+// floor(u / m) = umulhi(u, magic) >> 7 with magic = floor(2^39 / m) + 1 (< 2^32): the
+// excess u (magic - 2^39 / m) / 2^39 < 2^31 / 2^39 = 1/256 <= 1/m cannot carry the
+// quotient past the next integer. Integer pipes only (no I2F / F2I).
+struct ModMagic {
+  uint32_t m, magic, bias;  // bias = m floor(2^30 / m): a multiple of m, u = x + bias
+};
+
+inline ModMagic mod_magic(int m) {
+  ModMagic r;
+  r.m = static_cast<uint32_t>(m);
+  r.magic = static_cast<uint32_t>((uint64_t(1) << 39) / uint64_t(m) + 1);
+  r.bias = static_cast<uint32_t>(m) * ((uint32_t(1) << 30) / static_cast<uint32_t>(m));
+  return r;
+}
+
+// x mod m in the symmetric range [-(m >> 1), m - (m >> 1) - 1], for |x| <= 2^30 - 256
+__device__ __forceinline__ int sym_mod_magic(int x, const ModMagic& mm) {
+  const uint32_t u = static_cast<uint32_t>(x) + mm.bias;  // in [0, 2^31)
+  const uint32_t q = __umulhi(u, mm.magic) >> 7;
+  const int r = static_cast<int>(u - q * mm.m);  // [0, m)
+  return r > static_cast<int>(mm.m - (mm.m >> 1) - 1) ? r - static_cast<int>(mm.m) : r;
+}
+
 // GEMM epilogue: int32 product chunk -> symmetric residue mod m (int8), 32 bytes per row chunk.
+// |x| <= K 2^14 <= 2^30 - 2^14 for K <= kOzakiMaxK.
 struct ModStore {
   int8_t* out;
   int64_t ld;
-  int m;
-  double minv;
+  ModMagic mm;
   __device__ void operator()(int row, int col0, const uint32_t (&v)[32]) const {
     uint32_t w[8];
 #pragma unroll
@@ -172,9 +196,7 @@ struct ModStore {
       uint32_t packed = 0;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        const int x = static_cast<int>(v[4 * q + b]);
-        const int qq = __double2int_rn(double(x) * minv);
-        const int r = sym_fix_rt(x - qq * m, m);
+        const int r = sym_mod_magic(static_cast<int>(v[4 * q + b]), mm);
         packed |= (uint32_t(uint8_t(int8_t(r)))) << (8 * b);
       }
       w[q] = packed;
@@ -205,39 +227,117 @@ __device__ __forceinline__ double u128_to_double(unsigned __int128 x) {
   return t * __longlong_as_double(static_cast<long long>(64 - lz + 1023) << 52);
 }
 
-// Exact signed value of the residue vector r (canonical residues, |value| < M/2), rounded to
-// the nearest FP64 and scaled by 2^-es (a second rounding only for a subnormal result). Garner mixed-radix digits in FP32: every intermediate is an
-// integer below 2^24 in magnitude (|sum of digit * c| < 15 * 128 * 255), so each FP32
-// operation is exact.
-__device__ __forceinline__ double garner_value(const int (&r)[kMods], int es) {
-  float dig[kMods] = {};
-  static_for<0, kMods>([&](auto L) {
-    constexpr int l = decltype(L)::value;
-    float s = float_small(r[l]);
-    static_for<0, l>([&](auto U) {
-      constexpr int u = decltype(U)::value;
-      constexpr float cu = float(kG.c[l][u]);
-      s = fmaf(-dig[u], cu, s);
-    });
-    if constexpr (l == 0) {
-      dig[0] = s;  // m_0 = 256 and the stored residue is already canonical
-    } else {
-      // any small representative of (r - s) mod m will do before the multiply by the inverse
-      constexpr float fm = float(kG.m[l]), minv = 1.0f / float(kG.m[l]), inv = float(kG.inv[l]);
-      const float t = fmaf(-rint_small(s * minv), fm, s) * inv;  // |t| < 1.5 m * inv < 2^17
-      // m odd: the exact t / m is >= 1 / (2m) from a half-integer and the computed quotient is
-      // within 3e-4 of it, so rint gives the exact nearest quotient and the symmetric digit
-      dig[l] = fmaf(-rint_small(t * minv), fm, t);
+// Garner tables for the integer digit recurrence: with t_l = (m_0 ... m_{l-1})^-1 mod m_l,
+//   dig_l = sym( r_l t_l + sum_{u<l} dig_u k[l][u] ),  k[l][u] = sym(-c[l][u] t_l) mod m_l,
+// where sym() is the symmetric residue mod m_l. Residues, digits, t and k are all in
+// [-128, 127], so every product-sum is four-way SIMD: dp4a of int8x4 words (the four
+// elements' residues against t placed in byte q; packed digits against packed k).
+struct GarnerInt {
+  int kw[kMods][4];    // k[l][4w .. 4w+3] packed (zero for u >= l)
+  int tw[kMods][4];    // sym(t_l) in byte q, zero elsewhere
+  uint32_t magic[kMods], off[kMods];
+};
+
+constexpr int sym_c(long long x, int m) {
+  long long r = x % m;
+  if (r < 0) r += m;
+  return static_cast<int>(r > m - (m >> 1) - 1 ? r - m : r);
+}
+
+constexpr uint32_t pack_i8(int b) { return static_cast<uint32_t>(static_cast<uint8_t>(static_cast<int8_t>(b))); }
+
+constexpr GarnerInt make_garner_int() {
+  GarnerInt g{};
+  for (int l = 0; l < kMods; ++l) {
+    const int m = kG.m[l];
+    g.magic[l] = static_cast<uint32_t>((1ull << 39) / static_cast<unsigned long long>(m) + 1);
+    // m floor(2^30 / m) (a multiple of m) + floor(m / 2): x + off lies in [0, 2^31) for
+    // |x| <= 2^30 - 256, and floor((x + off) / m) rounds x / m to the symmetric range
+    g.off[l] = static_cast<uint32_t>(m) * ((1u << 30) / static_cast<uint32_t>(m)) + static_cast<uint32_t>(m >> 1);
+    for (int q = 0; q < 4; ++q) g.tw[l][q] = static_cast<int>(pack_i8(sym_c(kG.inv[l], m)) << (8 * q));
+    for (int w = 0; w < 4; ++w) {
+      uint32_t word = 0;
+      for (int b = 0; b < 4; ++b) {
+        const int u = 4 * w + b;
+        word |= pack_i8(u < l ? sym_c(-static_cast<long long>(kG.c[l][u]) * kG.inv[l], m) : 0) << (8 * b);
+      }
+      g.kw[l][w] = static_cast<int>(word);
     }
+  }
+  return g;
+}
+
+constexpr GarnerInt kGI = make_garner_int();
+
+// sym(x) mod m_L from u = x + off_L in [0, 2^31): u - m floor(u / m) - floor(m / 2) (the
+// magic division of ModMagic; integer pipes only)
+template <int L>
+__device__ __forceinline__ int sym_from_biased(uint32_t u) {
+  constexpr uint32_t m = kG.m[L], magic = kGI.magic[L];
+  const uint32_t q = __umulhi(u, magic) >> 7;
+  return static_cast<int>(u - q * m) - static_cast<int>(m >> 1);
+}
+
+// sign-extended byte k of w (prmt with sign-replicating selector nibbles)
+template <int K>
+__device__ __forceinline__ int sbyte(uint32_t w) {
+  constexpr uint32_t sel = K | ((K | 8) << 4) | ((K | 8) << 8) | ((K | 8) << 12);
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(w), "n"(sel));
+  return static_cast<int>(r);
+}
+
+// w with byte K replaced by the low byte of x
+template <int K>
+__device__ __forceinline__ uint32_t put_byte(uint32_t w, int x) {
+  constexpr uint32_t sel = (K == 0 ? 0x3214u : K == 1 ? 0x3240u : K == 2 ? 0x3410u : 0x4210u);
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(x), "n"(sel));
+  return r;
+}
+
+// Mixed-radix digits of four residue vectors at once (res[l] = the four elements' residues
+// mod m_l as int8x4), packed four digits per word: D[q][w] byte b = dig_{4w+b} of element q.
+// Every step is exact integer arithmetic; the four chains are independent (ILP).
+__device__ __forceinline__ void garner_digits4(const uint32_t (&res)[kMods], uint32_t (&D)[4][4]) {
+  // dig_0 = r_0 (m_0 = 256: the stored residue is already the symmetric digit)
+  D[0][0] = res[0] & 0xffu;
+  D[1][0] = (res[0] >> 8) & 0xffu;
+  D[2][0] = (res[0] >> 16) & 0xffu;
+  D[3][0] = res[0] >> 24;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) D[q][1] = D[q][2] = D[q][3] = 0u;
+  static_for<1, kMods>([&](auto L) {
+    constexpr int l = decltype(L)::value;
+    int acc[4];
+    static_for<0, 4>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      constexpr int tw = kGI.tw[l][q], off = static_cast<int>(kGI.off[l]);
+      acc[q] = __dp4a(static_cast<int>(res[l]), tw, off);
+    });
+    static_for<0, (l + 3) / 4>([&](auto W) {
+      constexpr int w = decltype(W)::value;
+      constexpr int kw = kGI.kw[l][w];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = __dp4a(static_cast<int>(D[q][w]), kw, acc[q]);
+    });
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      D[q][l / 4] = put_byte<l % 4>(D[q][l / 4], sym_from_biased<l>(static_cast<uint32_t>(acc[q])));
   });
-  // Digit pairs P_k = dig_2k + m_2k dig_2k+1 (|P_k| < 2^16, exact in FP32), then
-  // value = hi * W_8 + lo with each half a Horner sum over pairs, exact in int64
-  // (|lo| < W_8 / 2, |hi| < 2^61).
+}
+
+// Exact signed value of the digits of one element (|value| < M/2), rounded to the nearest
+// FP64 and scaled by 2^-es (a second rounding only for a subnormal result).
+__device__ __forceinline__ double garner_value(const uint32_t (&D)[4], int es) {
+  // Digit pairs P_k = dig_2k + m_2k dig_2k+1 (|P_k| < 2^16), then value = hi * W_8 + lo with
+  // each half a Horner sum over pairs, exact in int64 (|lo| < W_8 / 2, |hi| < 2^61).
   int pr[kMods / 2];
   static_for<0, kMods / 2>([&](auto K) {
     constexpr int k = decltype(K)::value;
-    constexpr float m = float(kG.m[2 * k]);
-    pr[k] = int_small(fmaf(dig[2 * k + 1], m, dig[2 * k]));
+    constexpr int m = kG.m[2 * k];
+    const uint32_t w = D[k / 2];
+    pr[k] = sbyte<(2 * k) % 4>(w) + m * sbyte<(2 * k + 1) % 4>(w);
   });
   long long lo = pr[3], hi = pr[7];
   static_for<0, 3>([&](auto K) {
@@ -261,17 +361,21 @@ __global__ void __launch_bounds__(256) reconstruct_map_kernel(OzakiMapArgs a) {
   if (a.state != nullptr && a.state->done) return;
   __shared__ double red[8][4];
   double v[4] = {0.0, 0.0, 0.0, 0.0};
-  const int64_t n4 = (a.n + 3) >> 2;
-  const int64_t total = n4 * a.ncols;
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t j = t / n4, i0 = (t - j * n4) << 2;
+  // n, ncols <= kOzakiMaxK: the work index fits 32 bits (32-bit division, not 64)
+  const uint32_t n4 = static_cast<uint32_t>((a.n + 3) >> 2);
+  const uint32_t total = n4 * static_cast<uint32_t>(a.ncols);
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const uint32_t jj = t / n4;
+    const int64_t j = jj, i0 = int64_t(t - jj * n4) << 2;
     const int eb = a.eB[j];
     const int8_t* rp = a.R + j * a.ldr + i0;
-    char4 res[kMods];
+    uint32_t res[kMods];
 #pragma unroll
-    for (int l = 0; l < kMods; ++l) res[l] = *reinterpret_cast<const char4*>(rp + l * a.plane);
+    for (int l = 0; l < kMods; ++l) res[l] = *reinterpret_cast<const uint32_t*>(rp + l * a.plane);
     const int64_t jg = a.col0 + j;
     const double dj = a.mode == 0 ? a.d[jg] : 0.0;
+    uint32_t D[4][4];
+    garner_digits4(res, D);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int64_t i = i0 + q;
@@ -281,11 +385,7 @@ __global__ void __launch_bounds__(256) reconstruct_map_kernel(OzakiMapArgs a) {
       if (ea == kOzakiNonFinite || eb == kOzakiNonFinite) {
         w = __longlong_as_double(0x7ff8000000000000LL);  // NaN, as the FP64 product would give
       } else {
-        int r[kMods];
-#pragma unroll
-        for (int l = 0; l < kMods; ++l)
-          r[l] = q == 0 ? res[l].x : q == 1 ? res[l].y : q == 2 ? res[l].z : res[l].w;
-        w = garner_value(r, ea + eb);
+        w = garner_value(D[q], ea + eb);
       }
       if (a.mode == 2) {
         a.F[j * a.ldz + i] = w;
@@ -338,17 +438,19 @@ void OzakiOperand::build(cudaStream_t s, const double* X, int64_t ldx, int64_t r
 // columns), columns = rows of Aop (the Delta rows).
 void ozaki_products(cudaStream_t s, const OzakiOperand& Zop, const OzakiOperand& Aop, int64_t zrows_pad,
                     int64_t arows_pad, DevBuf& R, int64_t& plane) {
+  if (Zop.kpad != Aop.kpad || Zop.len > kOzakiMaxK)
+    throw InvalidArgument("ozaki: inner dimension must match and be at most 65535");
   plane = zrows_pad * arows_pad;
   if (R.count * 8 < size_t(kMods) * plane) R.alloc(ceil_div(int64_t(kMods) * plane, 8), false);
   for (int l = 0; l < kMods; ++l) {
-    const int m = kG.m[l];  // host read of the constexpr table
-    ModStore epi{reinterpret_cast<int8_t*>(R.get()) + l * plane, arows_pad, m, 1.0 / m};
+    ModStore epi{reinterpret_cast<int8_t*>(R.get()) + l * plane, arows_pad, mod_magic(kG.m[l])};
     launch_i8gemm(s, zrows_pad, arows_pad, Zop.kpad, reinterpret_cast<const int8_t*>(Zop.res.get()) + l * Zop.plane,
                   Zop.kpad, reinterpret_cast<const int8_t*>(Aop.res.get()) + l * Aop.plane, Aop.kpad, epi);
   }
 }
 
 void ozaki_reconstruct(cudaStream_t s, const OzakiMapArgs& a) {
+  if (((a.n + 3) >> 2) * a.ncols >= (int64_t(1) << 32)) throw InvalidArgument("ozaki: product too large");
   reconstruct_map_kernel<<<kOzakiGrid, 256, 0, s>>>(a);
   IPT_LAUNCH_CHECK();
   count_launch();
@@ -357,6 +459,7 @@ void ozaki_reconstruct(cudaStream_t s, const OzakiMapArgs& a) {
 void ozaki_dgemm_device(cudaStream_t s, int64_t M, int64_t N, int64_t K, const double* A, const double* B,
                         double* C, DevBuf& partials) {
   if (M <= 0 || N <= 0) return;
+  if (K > kOzakiMaxK) throw InvalidArgument("ozaki_dgemm: K must be at most 65535");
   const int64_t kpad = round_up(std::max<int64_t>(K, 1), kOzakiKPad);
   // product rows = rows of A (the GEMM's M side, 256-row pair tiles), columns = rows of B
   // (N side, 512-wide tiles), so the reconstruction writes C row-major

@@ -9,6 +9,7 @@ constexpr int kOzakiMods = 16;
 constexpr int kOzakiNonFinite = 0x7fffffff;  // exponent marker of a row / column with Inf or NaN
 constexpr int kOzakiGrid = 1184;             // fixed reconstruction grid (deterministic partials)
 constexpr int64_t kOzakiKPad = 128;          // K padding of the residue operands (the INT8 GEMM's BK)
+constexpr int64_t kOzakiMaxK = 65535;        // |int32 sums| <= K 2^14 <= 2^30 - 2^14 (epilogue reduction range)
 
 // One operand in residue form: rows x kpad int8 per modulus (K contiguous, zero padded),
 // and the per-row binary exponent of its scaling.
