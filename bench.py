@@ -348,10 +348,22 @@ def bench_sparse_full(lib, ctx, n, per_row, steps, dense_step_ms):
             "speedup_vs_dense_map": dense_step_ms / ms if dense_step_ms else None}
 
 
+def int8_peak():
+    """Dense INT8 tensor peak for the roofline: twice MEASURED_PEAKS' bf16 figures (the
+    tcgen05 kind::i8 rate is 2x kind::f16 per SM per clock), burst and sustained."""
+    try:
+        pk = json.load(open(PEAKS_PATH))
+        return 2.0 * pk["bf16_tflops"], 2.0 * pk.get("bf16_tflops_sustained", pk["bf16_tflops"]), \
+            "2 x MEASURED_PEAKS.json bf16_tflops (burst) / bf16_tflops_sustained"
+    except Exception:
+        return 4500.0, 4500.0, "nominal dense INT8 4.5 POPS (B200_PROFILING.md fallback)"
+
+
 def bench_ozaki(ipt, lib, ctx, n, dense_step_ms, dmma_solve):
     """The same map and solve with W = Delta Z by Ozaki scheme II on the tcgen05 INT8
     datapath (16 exact modular GEMMs + CRT reconstruction, ozaki.cu): FP64-accurate, so
-    reported with its agreement to the DMMA (FP64 tensor core) solve."""
+    reported with its agreement to the DMMA (FP64 tensor core) solve. The roofline kernel
+    is the INT8 GEMM (i8gemm_2sm_kernel), timed with events around its 16 launches per map."""
     from paper_2012_14702_b200 import synth
     from paper_2012_14702_b200._lib import check, dptr
 
@@ -366,12 +378,21 @@ def bench_ozaki(ipt, lib, ctx, n, dense_step_ms, dmma_solve):
     check(lib.ipt_full_run_maps(ctx.handle, h, steps, C.byref(tot), C.byref(ker)))
     lib.ipt_full_free(h)
     ms = tot.value / steps
+    gemm_ms = ker.value / steps
+    int8_ops = 16 * 2.0 * n ** 3  # 16 moduli x 2N^3 int8 ops per map
+    burst, sustained, src = int8_peak()
+    achieved = int8_ops / (gemm_ms * 1e-3) / 1e12
     t0 = time.perf_counter()
     r = ipt.solve_full(p, ipt.build_gaps(p), ipt.IterationConfig(tolerance=1e-12), ctx=ctx, product="ozaki")
     tts = time.perf_counter() - t0
     out = {"workload": f"configs[2] N={n}, W = Delta Z by Ozaki scheme II on tcgen05 kind::i8 (16 moduli)",
            "ms_per_map": ms, "fp64_equivalent_TFs": 2.0 * n ** 3 / (ms * 1e-3) / 1e12,
            "speedup_vs_dmma_map": dense_step_ms / ms,
+           "roofline": {"bound": "tensor", "kernel": "i8gemm_2sm_kernel<ModStore, 2> (16 launches per map)",
+                        "achieved": achieved, "peak": burst, "peak_sustained": sustained, "unit": "TOPS (int8)",
+                        "frac": achieved / burst, "frac_of_sustained": achieved / sustained,
+                        "ops_per_map": int8_ops, "gemm_ms_per_map": gemm_ms,
+                        "gemm_share_of_map": gemm_ms / ms, "peak_source": src},
            "time_to_solution_s": tts, "iterations": r.iterations, "status": ipt.to_string(r.status),
            "timings_ms": r.timings_ms, "residual_frobenius": r.residual_frobenius}
     if dmma_solve is not None and dmma_solve.get("lambda0") is not None:

@@ -601,7 +601,9 @@ bool use_ozaki(const FullProblem& P) {
 }
 
 // W = Delta Z by Ozaki scheme II, then the map (mode 0) or the closing residual (mode 1).
-void ozaki_apply(FullProblem& P, const double* zs, double* zd, int mode, const LoopState* st) {
+// ev_a / ev_b (optional) bracket the 16 INT8 GEMMs alone (the roofline kernel).
+void ozaki_apply(FullProblem& P, const double* zs, double* zd, int mode, const LoopState* st,
+                 cudaEvent_t ev_a = nullptr, cudaEvent_t ev_b = nullptr) {
   cudaStream_t s = P.ctx->stream;
   const int64_t kpad = round_up(P.n, kOzakiKPad);
   const int64_t arows = round_up(P.n, 512);  // the 256 x 512 pair tile of the INT8 GEMM
@@ -611,7 +613,9 @@ void ozaki_apply(FullProblem& P, const double* zs, double* zd, int mode, const L
   }
   P.oz_z.build(s, zs, P.ldz, P.ncols, P.n, P.cols_pad, kpad);
   int64_t plane = 0;
+  if (ev_a) IPT_CUDA(cudaEventRecord(ev_a, s));
   ozaki_products(s, P.oz_z, P.oz_delta, P.cols_pad, arows, P.oz_R, plane);
+  if (ev_b) IPT_CUDA(cudaEventRecord(ev_b, s));
   OzakiMapArgs a{};
   a.R = reinterpret_cast<const int8_t*>(P.oz_R.get());
   a.plane = plane;
@@ -648,20 +652,22 @@ void enqueue_map(FullProblem& P, int k, const ipt_params& prm, cudaEvent_t ev_a 
   } else if (!P.cplx) {
     launch_diag(P, P.A1.get(), zs, P.wd.get(), nullptr, nullptr, st);
     GemmParams g = gemm_params(P, P.A1.get(), zs, zd, P.ldz);
-    if (ev_a) IPT_CUDA(cudaEventRecord(ev_a, c.stream));
     int64_t nparts = num_partials(P);
     if (k == 0 && P.start_identity && P.delta_finite && identity_shortcut_enabled()) {
       const unsigned tiles = static_cast<unsigned>(gemm_tiles(P.n, P.ncols));
+      if (ev_a) IPT_CUDA(cudaEventRecord(ev_a, c.stream));
       map_identity_kernel<<<tiles, kGemmThreads, 0, c.stream>>>(g);
       IPT_LAUNCH_CHECK();
       count_launch();
+      if (ev_b) IPT_CUDA(cudaEventRecord(ev_b, c.stream));
     } else if (use_ozaki(P)) {
-      ozaki_apply(P, zs, zd, 0, st);
+      ozaki_apply(P, zs, zd, 0, st, ev_a, ev_b);  // events around the INT8 GEMMs only
       nparts = kOzakiGrid;
     } else {
+      if (ev_a) IPT_CUDA(cudaEventRecord(ev_a, c.stream));
       launch_gemm(kGemmMap, g, c.stream);
+      if (ev_b) IPT_CUDA(cudaEventRecord(ev_b, c.stream));
     }
-    if (ev_b) IPT_CUDA(cudaEventRecord(ev_b, c.stream));
     reduce_partials(c.stream, P.partials.get(), nparts, P.sums.get(), st);
     allreduce_sums(P, true);
     decide_full_kernel<<<1, 1, 0, c.stream>>>(
@@ -1191,7 +1197,8 @@ void full_release_download(FullProblem& P) {
 
 // Bench / profiling: exactly `count` further map applications (convergence ignored),
 // timed with CUDA events on the library stream: the whole sequence and the K1 GEMM
-// launches alone (the dominant kernel of the roofline).
+// launches alone (the dominant kernel of the roofline; with the Ozaki product, its 16
+// INT8 GEMM launches).
 void full_run_maps(FullProblem& P, int count, double* ms_total, double* ms_gemm) {
   Ctx& c = *P.ctx;
   ipt_params prm;
