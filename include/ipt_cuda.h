@@ -117,6 +117,10 @@ int ipt_full_download(ipt_ctx* ctx, ipt_full_problem* prob, double* z_re, double
 int ipt_full_local_columns(const ipt_full_problem* prob, int64_t* col_begin, int64_t* col_end);
 /* Product used by ipt_full_run_maps (the solve calls take ipt_params.product). */
 int ipt_full_set_product(ipt_full_problem* prob, int32_t product);
+/* Moduli the last Ozaki product used (0: not an Ozaki product). With Z_jj = 1 split off,
+ * the exact product needs only as many moduli as the off-diagonal column norms require
+ * (IPT_OZAKI_SPLIT=0: all 16). */
+int ipt_full_ozaki_moduli(ipt_full_problem* prob, int32_t* moduli);
 void ipt_full_free(ipt_full_problem* prob);
 
 /* apply_map_full (solver.cpp:156-178): one F application to a given Z. */

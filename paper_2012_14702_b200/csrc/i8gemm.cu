@@ -28,6 +28,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_i8() {
 struct StoreI32 {
   int32_t* C;
   int64_t ldc;
+  __device__ bool skip() const { return false; }
   __device__ void operator()(int row, int col0, const uint32_t (&v)[32]) const {
     int4* p = reinterpret_cast<int4*>(C + int64_t(row) * ldc + col0);
 #pragma unroll

@@ -82,11 +82,13 @@ __device__ __forceinline__ void grouped_tile(int t, int tiles_m, int tiles_n, in
   tn = r / gs;
 }
 
-// Epi(row, col0, v[32]) consumes columns col0..col0+31 of one row.
+// Epi(row, col0, v[32]) consumes columns col0..col0+31 of one row; Epi::skip() (read once,
+// uniform) lets a launch exit before any setup.
 template <class Epi>
 __global__ void __launch_bounds__(kI8Threads, 1)
     i8gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K, int tiles_m,
                   int tiles_n, int group, Epi epi) {
+  if (epi.skip()) return;  // uniform over the grid (e.g. an unused Ozaki modulus)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -202,6 +204,7 @@ template <class Epi>
 __global__ void __launch_bounds__(kI8Threads, 1)
     i8gemm_mc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
                      int tiles_m, int tiles_n, int group, Epi epi) {
+  if (epi.skip()) return;  // uniform over the grid (e.g. an unused Ozaki modulus)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -336,6 +339,7 @@ template <class Epi, int NB>
 __global__ void __launch_bounds__(kI8Threads, 1)
     i8gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
                       int pairs_m, int tiles_n, int group, Epi epi) {
+  if (epi.skip()) return;  // uniform over the grid (e.g. an unused Ozaki modulus)
   using Cfg = I8S2<NB>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base =

@@ -372,6 +372,11 @@ int ipt_full_set_product(ipt_full_problem* prob, int32_t product) {
   return IPT_OK;
 }
 
+int ipt_full_ozaki_moduli(ipt_full_problem* prob, int32_t* moduli) {
+  if (!prob || !moduli) return IPT_ERR_INVALID;
+  return guarded([&] { *moduli = full_ozaki_moduli(*reinterpret_cast<FullProblem*>(prob)); });
+}
+
 int ipt_full_local_columns(const ipt_full_problem* prob, int64_t* col_begin, int64_t* col_end) {
   if (!prob) return IPT_ERR_INVALID;
   full_local_columns(*reinterpret_cast<const FullProblem*>(prob), col_begin, col_end);

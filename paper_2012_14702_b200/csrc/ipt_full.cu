@@ -68,6 +68,9 @@ struct FullProblem {
   OzakiOperand oz_delta, oz_z;
   DevBuf oz_R;
   bool oz_delta_ready = false;
+  DevBuf oz_dt;     // Delta transposed (the split-off diagonal term reads Delta_ij by column)
+  DevBuf oz_mods;   // device int: moduli the current product needs
+  bool oz_split = true;
   ~FullProblem() {
     if (state) cudaFree(state);
   }
@@ -609,12 +612,20 @@ void ozaki_apply(FullProblem& P, const double* zs, double* zd, int mode, const L
   const int64_t arows = round_up(P.n, 512);  // the 256 x 512 pair tile of the INT8 GEMM
   if (!P.oz_delta_ready) {
     P.oz_delta.build(s, P.A1.get(), P.lda, P.n, P.n, arows, kpad);
+    if (P.oz_split) {
+      P.oz_dt.alloc(P.n * P.lda, false);
+      ozaki_transpose(s, P.A1.get(), P.lda, P.n, P.oz_dt.get(), P.lda);
+      P.oz_mods.alloc(1, false);
+    }
     P.oz_delta_ready = true;
   }
-  P.oz_z.build(s, zs, P.ldz, P.ncols, P.n, P.cols_pad, kpad);
+  // Z'_jj is split off (Z_jj = 1 in every iterate), so the product needs only as many
+  // moduli as the off-diagonal column norms require (ozaki.cuh)
+  int* mods = P.oz_split ? reinterpret_cast<int*>(P.oz_mods.get()) : nullptr;
+  P.oz_z.build(s, zs, P.ldz, P.ncols, P.n, P.cols_pad, kpad, P.oz_split ? P.col0 : -1, mods);
   int64_t plane = 0;
   if (ev_a) IPT_CUDA(cudaEventRecord(ev_a, s));
-  ozaki_products(s, P.oz_z, P.oz_delta, P.cols_pad, arows, P.oz_R, plane);
+  ozaki_products(s, P.oz_z, P.oz_delta, P.cols_pad, arows, P.oz_R, plane, mods);
   if (ev_b) IPT_CUDA(cudaEventRecord(ev_b, s));
   OzakiMapArgs a{};
   a.R = reinterpret_cast<const int8_t*>(P.oz_R.get());
@@ -624,6 +635,12 @@ void ozaki_apply(FullProblem& P, const double* zs, double* zd, int mode, const L
   a.eB = P.oz_z.exps();
   a.Z = zs;
   a.ldz = P.ldz;
+  if (P.oz_split) {
+    a.dZ = P.oz_z.diag.get();
+    a.DT = P.oz_dt.get();
+    a.lddt = P.lda;
+    a.moduli = mods;
+  }
   a.F = zd;
   a.d = P.dre.get();
   a.wd = P.wd.get();
@@ -724,6 +741,10 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
   auto P = std::make_unique<FullProblem>();
   P->ctx = &c;
   P->n = n;
+  {
+    const char* e = std::getenv("IPT_OZAKI_SPLIT");  // 0: all 16 moduli, no diagonal split
+    P->oz_split = !(e && e[0] == '0');
+  }
   P->ld = round_up(n, 16);
   P->rows_pad = round_up(n, kBM);
   column_block(c, n, col_begin, col_end, P->col0, P->ncols);
@@ -912,6 +933,15 @@ void full_reset(FullProblem& P, const double* warm_re, const double* warm_im, in
 }
 
 void full_set_product(FullProblem& P, int product) { P.product = product; }
+
+int full_ozaki_moduli(FullProblem& P) {
+  if (!use_ozaki(P)) return 0;
+  if (!P.oz_split) return kOzakiMods;
+  int m = 0;
+  IPT_CUDA(cudaMemcpyAsync(&m, P.oz_mods.get(), sizeof(int), cudaMemcpyDeviceToHost, P.ctx->stream));
+  IPT_CUDA(cudaStreamSynchronize(P.ctx->stream));
+  return m;
+}
 
 void full_iterate(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
   Ctx& c = *P.ctx;

@@ -138,6 +138,7 @@ void full_download_z(FullProblem& P, double* z_re, double* z_im);
 void full_release_download(FullProblem& P);
 void full_local_columns(const FullProblem& P, int64_t* c0, int64_t* c1);
 void full_set_product(FullProblem& P, int product);
+int full_ozaki_moduli(FullProblem& P);
 bool full_is_complex(const FullProblem& P);
 void full_run_maps(FullProblem& P, int count, double* ms_total, double* ms_gemm);
 

@@ -83,19 +83,45 @@ __device__ __forceinline__ void static_for(F&& f) {
   }
 }
 
+// log2(m_0 ... m_{L-1}) rounded down, L = 1 .. 16 (tests/test_ozaki_math.py checks them)
+__constant__ double kLog2M[kMods] = {8.0,       15.994353, 23.977347, 31.94889,  39.897257,  47.810147,
+                                     55.711013, 63.5752,   71.414403, 79.240952, 87.041852,  94.803403,
+                                     102.524502, 110.161127, 117.783179, 125.375636};
+
 // Row (or column) exponent: max |x| * 2^e in [2^52, 2^53); flag non-finite rows.
+// Split operands (diag0 >= 0) also bound the row's off-diagonal integer 1-norm and raise
+// *moduli to the count that keeps |Delta' Y'| < 2^53 |Y'|_1 below M / 2.
 __global__ void exponent_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows, int64_t len,
-                                int* __restrict__ e) {
+                                int* __restrict__ e, int64_t diag0, int* __restrict__ moduli) {
   const int lane = threadIdx.x & 31;
   const int64_t r = blockIdx.x * int64_t(blockDim.x / 32) + (threadIdx.x >> 5);
   if (r >= rows) return;
-  double mx = 0.0;
-  for (int64_t k = lane; k < len; k += 32) mx = nan_max(mx, fabs(X[r * ldx + k]));
-  for (int off = 16; off > 0; off >>= 1) mx = nan_max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  const int64_t kd = diag0 >= 0 ? diag0 + r : -1;
+  double mx = 0.0, off = 0.0;
+  for (int64_t k = lane; k < len; k += 32) {
+    const double a = fabs(X[r * ldx + k]);
+    mx = nan_max(mx, a);
+    off += k == kd ? 0.0 : a;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = nan_max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    off += __shfl_xor_sync(0xffffffffu, off, o);
+  }
   if (lane == 0) {
-    if (!isfinite(mx)) e[r] = kOzakiNonFinite;
-    else if (mx == 0.0) e[r] = 0;
-    else e[r] = 52 - ilogb(mx);
+    int er;
+    if (!isfinite(mx)) er = kOzakiNonFinite;
+    else if (mx == 0.0) er = 0;
+    else er = 52 - ilogb(mx);
+    e[r] = er;
+    if (moduli != nullptr && er != kOzakiNonFinite) {
+      // |Y'|_1 <= 2^e sum |x| (1 + K u) + K / 2 (rounding to integers); 2^-40 covers the
+      // floating-point sum for K < 2^17
+      const double bound = ldexp(off * (1.0 + 0x1p-40), er) + double(len);
+      const double need = 54.0 + log2(bound) + 1e-3;
+      int L = kOzakiMinMods;
+      while (L < kMods && kLog2M[L - 1] < need) ++L;
+      atomicMax(moduli, L);
+    }
   }
 }
 
@@ -128,9 +154,11 @@ __device__ __forceinline__ double scale2(double x, int k) {
 
 // out[l][r][k] = sym(rint(x_rk 2^e_r) mod m_l) for all 16 moduli; zero padding for k >= len.
 // Eight consecutive k per thread (one 8-byte store per modulus plane).
+// Split operands (diag0 >= 0): the entry at k = diag0 + r goes to diag[r] instead.
 __global__ void __launch_bounds__(256) residues_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows,
                                                        int64_t len, const int* __restrict__ e,
-                                                       int8_t* __restrict__ out, int64_t ldo, int64_t plane) {
+                                                       int8_t* __restrict__ out, int64_t ldo, int64_t plane,
+                                                       int64_t diag0, double* __restrict__ diag) {
   const int64_t per_row = ldo >> 3;
   const int64_t total = rows * per_row;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
@@ -141,6 +169,10 @@ __global__ void __launch_bounds__(256) residues_kernel(const double* __restrict_
     for (int q = 0; q < 8; ++q) {
       const int64_t k = k0 + q;
       y[q] = (k < len && er != kOzakiNonFinite) ? rint(scale2(X[r * ldx + k], er)) : 0.0;
+      if (diag0 >= 0 && k == diag0 + r) {
+        diag[r] = y[q];
+        y[q] = 0.0;
+      }
     }
     int8_t* dst = out + r * ldo + k0;
     static_for<0, kMods>([&](auto L) {
@@ -189,6 +221,9 @@ struct ModStore {
   int8_t* out;
   int64_t ld;
   ModMagic mm;
+  const int* moduli;  // device count of moduli in use (nullptr: all)
+  int l;
+  __device__ bool skip() const { return moduli != nullptr && *moduli <= l; }
   __device__ void operator()(int row, int col0, const uint32_t (&v)[32]) const {
     uint32_t w[8];
 #pragma unroll
@@ -299,6 +334,9 @@ __device__ __forceinline__ uint32_t put_byte(uint32_t w, int x) {
 // Mixed-radix digits of four residue vectors at once (res[l] = the four elements' residues
 // mod m_l as int8x4), packed four digits per word: D[q][w] byte b = dig_{4w+b} of element q.
 // Every step is exact integer arithmetic; the four chains are independent (ILP).
+// Only the first L moduli are used (digits L .. 15 stay zero, so the value below is the
+// same mixed-radix sum).
+template <int L>
 __device__ __forceinline__ void garner_digits4(const uint32_t (&res)[kMods], uint32_t (&D)[4][4]) {
   // dig_0 = r_0 (m_0 = 256: the stored residue is already the symmetric digit)
   D[0][0] = res[0] & 0xffu;
@@ -307,8 +345,8 @@ __device__ __forceinline__ void garner_digits4(const uint32_t (&res)[kMods], uin
   D[3][0] = res[0] >> 24;
 #pragma unroll
   for (int q = 0; q < 4; ++q) D[q][1] = D[q][2] = D[q][3] = 0u;
-  static_for<1, kMods>([&](auto L) {
-    constexpr int l = decltype(L)::value;
+  static_for<1, L>([&](auto LL) {
+    constexpr int l = decltype(LL)::value;
     int acc[4];
     static_for<0, 4>([&](auto Q) {
       constexpr int q = decltype(Q)::value;
@@ -329,7 +367,8 @@ __device__ __forceinline__ void garner_digits4(const uint32_t (&res)[kMods], uin
 
 // Exact signed value of the digits of one element (|value| < M/2), rounded to the nearest
 // FP64 and scaled by 2^-es (a second rounding only for a subnormal result).
-__device__ __forceinline__ double garner_value(const uint32_t (&D)[4], int es) {
+// `extra` (the split-off diagonal term Delta'_ij Z'_jj) is added before the rounding.
+__device__ __forceinline__ double garner_value(const uint32_t (&D)[4], int es, __int128 extra) {
   // Digit pairs P_k = dig_2k + m_2k dig_2k+1 (|P_k| < 2^16), then value = hi * W_8 + lo with
   // each half a Horner sum over pairs, exact in int64 (|lo| < W_8 / 2, |hi| < 2^61).
   int pr[kMods / 2];
@@ -347,7 +386,7 @@ __device__ __forceinline__ double garner_value(const uint32_t (&D)[4], int es) {
     lo = lo * ml + pr[k];
     hi = hi * mh + pr[k + 4];
   });
-  const __int128 p = static_cast<__int128>(hi) * static_cast<__int128>(kW8) + lo;
+  const __int128 p = static_cast<__int128>(hi) * static_cast<__int128>(kW8) + lo + extra;
   const bool neg = p < 0;
   const double mg = u128_to_double(neg ? (unsigned __int128)(-p) : (unsigned __int128)p);
   return scale2(neg ? -mg : mg, -es);
@@ -357,10 +396,8 @@ __device__ __forceinline__ double garner_value(const uint32_t (&D)[4], int es) {
 // apply the IPT map (mode 0) or the closing residual (mode 1) with the K1 formulas, or
 // store W itself (mode 2).
 // Four consecutive rows i per thread (one 4-byte load per modulus plane; ldr % 4 == 0).
-__global__ void __launch_bounds__(256) reconstruct_map_kernel(OzakiMapArgs a) {
-  if (a.state != nullptr && a.state->done) return;
-  __shared__ double red[8][4];
-  double v[4] = {0.0, 0.0, 0.0, 0.0};
+template <int L>
+__device__ __forceinline__ void reconstruct_body(const OzakiMapArgs& a, double (&v)[4]) {
   // n, ncols <= kOzakiMaxK: the work index fits 32 bits (32-bit division, not 64)
   const uint32_t n4 = static_cast<uint32_t>((a.n + 3) >> 2);
   const uint32_t total = n4 * static_cast<uint32_t>(a.ncols);
@@ -371,11 +408,12 @@ __global__ void __launch_bounds__(256) reconstruct_map_kernel(OzakiMapArgs a) {
     const int8_t* rp = a.R + j * a.ldr + i0;
     uint32_t res[kMods];
 #pragma unroll
-    for (int l = 0; l < kMods; ++l) res[l] = *reinterpret_cast<const uint32_t*>(rp + l * a.plane);
+    for (int l = 0; l < kMods; ++l) res[l] = l < L ? *reinterpret_cast<const uint32_t*>(rp + l * a.plane) : 0u;
     const int64_t jg = a.col0 + j;
     const double dj = a.mode == 0 ? a.d[jg] : 0.0;
+    const long long zjj = a.dZ != nullptr ? static_cast<long long>(a.dZ[j]) : 0;
     uint32_t D[4][4];
-    garner_digits4(res, D);
+    garner_digits4<L>(res, D);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int64_t i = i0 + q;
@@ -385,7 +423,12 @@ __global__ void __launch_bounds__(256) reconstruct_map_kernel(OzakiMapArgs a) {
       if (ea == kOzakiNonFinite || eb == kOzakiNonFinite) {
         w = __longlong_as_double(0x7ff8000000000000LL);  // NaN, as the FP64 product would give
       } else {
-        w = garner_value(D[q], ea + eb);
+        __int128 extra = 0;
+        if (a.dZ != nullptr) {  // Delta'_ij exactly as residues_kernel rounded it
+          const long long dij = static_cast<long long>(rint(scale2(a.DT[jg * a.lddt + i], ea)));
+          extra = static_cast<__int128>(dij) * zjj;
+        }
+        w = garner_value(D[q], ea + eb, extra);
       }
       if (a.mode == 2) {
         a.F[j * a.ldz + i] = w;
@@ -407,6 +450,22 @@ __global__ void __launch_bounds__(256) reconstruct_map_kernel(OzakiMapArgs a) {
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(256) reconstruct_map_kernel(OzakiMapArgs a) {
+  if (a.state != nullptr && a.state->done) return;
+  __shared__ double red[8][4];
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  switch (a.moduli != nullptr ? *a.moduli : kMods) {  // uniform across the grid
+    case 9: reconstruct_body<9>(a, v); break;
+    case 10: reconstruct_body<10>(a, v); break;
+    case 11: reconstruct_body<11>(a, v); break;
+    case 12: reconstruct_body<12>(a, v); break;
+    case 13: reconstruct_body<13>(a, v); break;
+    case 14: reconstruct_body<14>(a, v); break;
+    case 15: reconstruct_body<15>(a, v); break;
+    default: reconstruct_body<16>(a, v); break;
+  }
   block_reduce4<8>(v, red);
   if (threadIdx.x == 0) {
     double* o = a.partials + size_t(blockIdx.x) * 4;
@@ -417,36 +476,64 @@ __global__ void __launch_bounds__(256) reconstruct_map_kernel(OzakiMapArgs a) {
   }
 }
 
+// DT = A^T through 32 x 32 shared-memory tiles (coalesced both ways)
+__global__ void transpose_kernel(const double* __restrict__ A, int64_t lda, int64_t n, double* __restrict__ DT,
+                                 int64_t ldt) {
+  __shared__ double tile[32][33];
+  const int64_t bx = int64_t(blockIdx.x) * 32, by = int64_t(blockIdx.y) * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t r = by + y, c = bx + threadIdx.x;
+    if (r < n && c < n) tile[y][threadIdx.x] = A[r * lda + c];
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t r = bx + y, c = by + threadIdx.x;
+    if (r < n && c < n) DT[r * ldt + c] = tile[threadIdx.x][y];
+  }
+}
+
 }  // namespace
 
 void OzakiOperand::build(cudaStream_t s, const double* X, int64_t ldx, int64_t rows_, int64_t len_, int64_t rows_pad,
-                         int64_t kpad_) {
+                         int64_t kpad_, int64_t diag0, int* moduli) {
   rows = rows_;
   len = len_;
   kpad = kpad_;
   plane = rows_pad * kpad;
   if (res.count * 8 < size_t(kMods) * plane) res.alloc(ceil_div(int64_t(kMods) * plane, 8));  // zeroed padding rows
   if (e.count < size_t(rows_pad)) e.alloc(rows_pad);
+  if (diag0 >= 0 && diag.count < size_t(rows_pad)) diag.alloc(rows_pad);
   int* ep = reinterpret_cast<int*>(e.get());
-  exponent_kernel<<<static_cast<unsigned>(ceil_div(rows, 8)), 256, 0, s>>>(X, ldx, rows, len, ep);
-  residues_kernel<<<2368, 256, 0, s>>>(X, ldx, rows, len, ep, reinterpret_cast<int8_t*>(res.get()), kpad, plane);
+  if (moduli != nullptr) IPT_CUDA(cudaMemsetAsync(moduli, 0, sizeof(int), s));
+  exponent_kernel<<<static_cast<unsigned>(ceil_div(rows, 8)), 256, 0, s>>>(X, ldx, rows, len, ep, diag0,
+                                                                            diag0 >= 0 ? moduli : nullptr);
+  residues_kernel<<<2368, 256, 0, s>>>(X, ldx, rows, len, ep, reinterpret_cast<int8_t*>(res.get()), kpad, plane,
+                                       diag0, diag0 >= 0 ? diag.get() : nullptr);
   IPT_LAUNCH_CHECK();
   count_launch(2);
 }
 
 // R[l] = (Bop . Aop^T) mod m_l for all moduli: rows of the product = rows of Bop (the Z
 // columns), columns = rows of Aop (the Delta rows).
+// Moduli at or past *moduli (when given) are skipped on the device: their GEMMs exit at once.
 void ozaki_products(cudaStream_t s, const OzakiOperand& Zop, const OzakiOperand& Aop, int64_t zrows_pad,
-                    int64_t arows_pad, DevBuf& R, int64_t& plane) {
+                    int64_t arows_pad, DevBuf& R, int64_t& plane, const int* moduli) {
   if (Zop.kpad != Aop.kpad || Zop.len > kOzakiMaxK)
     throw InvalidArgument("ozaki: inner dimension must match and be at most 65535");
   plane = zrows_pad * arows_pad;
   if (R.count * 8 < size_t(kMods) * plane) R.alloc(ceil_div(int64_t(kMods) * plane, 8), false);
   for (int l = 0; l < kMods; ++l) {
-    ModStore epi{reinterpret_cast<int8_t*>(R.get()) + l * plane, arows_pad, mod_magic(kG.m[l])};
+    ModStore epi{reinterpret_cast<int8_t*>(R.get()) + l * plane, arows_pad, mod_magic(kG.m[l]), moduli, l};
     launch_i8gemm(s, zrows_pad, arows_pad, Zop.kpad, reinterpret_cast<const int8_t*>(Zop.res.get()) + l * Zop.plane,
                   Zop.kpad, reinterpret_cast<const int8_t*>(Aop.res.get()) + l * Aop.plane, Aop.kpad, epi);
   }
+}
+
+void ozaki_transpose(cudaStream_t s, const double* A, int64_t lda, int64_t n, double* DT, int64_t ldt) {
+  const dim3 grid(static_cast<unsigned>(ceil_div(n, 32)), static_cast<unsigned>(ceil_div(n, 32)));
+  transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(A, lda, n, DT, ldt);
+  IPT_LAUNCH_CHECK();
+  count_launch();
 }
 
 void ozaki_reconstruct(cudaStream_t s, const OzakiMapArgs& a) {

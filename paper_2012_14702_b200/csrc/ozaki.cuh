@@ -13,12 +13,26 @@ constexpr int64_t kOzakiMaxK = 65535;        // |int32 sums| <= K 2^14 <= 2^30 -
 
 // One operand in residue form: rows x kpad int8 per modulus (K contiguous, zero padded),
 // and the per-row binary exponent of its scaling.
+constexpr int kOzakiMinMods = 9;             // fewest moduli the reconstruction is instantiated for
+
+// One operand in residue form: rows x kpad int8 per modulus (K contiguous, zero padded),
+// and the per-row binary exponent of its scaling.
+//
+// Diagonal split (diag0 >= 0, the Z operand of the IPT map): row r's entry at k = diag0 + r
+// (Z_jj = 1 for every iterate) is left out of the residues and kept as an exact integer
+// in diag[r]; the product then only carries the off-diagonal part Y' = Z' - Z'_jj e_j,
+// whose column 1-norm bounds |Delta' Y'| < 2^53 |Y'_j|_1. exponent_kernel turns that bound
+// into the number of moduli the exact product needs (atomicMax into *moduli), and the
+// GEMMs / reconstruction of moduli past it are skipped; the reconstruction adds
+// Delta'_ij Z'_jj back in 128-bit integers before the single rounding, so W is the same
+// correctly rounded exact product as with all 16 moduli (bitwise).
 struct OzakiOperand {
-  DevBuf res;  // kOzakiMods planes of rows_pad x kpad bytes
-  DevBuf e;    // int per row (in a double-sized buffer)
+  DevBuf res;   // kOzakiMods planes of rows_pad x kpad bytes
+  DevBuf e;     // int per row (in a double-sized buffer)
+  DevBuf diag;  // split operands: the removed diagonal entry of each row (integer-valued)
   int64_t rows = 0, len = 0, kpad = 0, plane = 0;
   void build(cudaStream_t s, const double* X, int64_t ldx, int64_t rows, int64_t len, int64_t rows_pad,
-             int64_t kpad);
+             int64_t kpad, int64_t diag0 = -1, int* moduli = nullptr);
   const int* exps() const { return reinterpret_cast<const int*>(e.get()); }
 };
 
@@ -29,6 +43,10 @@ struct OzakiMapArgs {
   const int* eB;    // per column j (Z)
   const double* Z;
   int64_t ldz;
+  const double* dZ;   // split: Z'_jj per local column (nullptr: no split)
+  const double* DT;   // split: Delta transposed, DT[jg * lddt + i] = Delta_ij
+  int64_t lddt;
+  const int* moduli;  // device count of moduli in use (nullptr: all 16)
   double* F;
   const double* d;
   const double* wd;
@@ -40,7 +58,9 @@ struct OzakiMapArgs {
 };
 
 void ozaki_products(cudaStream_t s, const OzakiOperand& Zop, const OzakiOperand& Aop, int64_t zrows_pad,
-                    int64_t arows_pad, DevBuf& R, int64_t& plane);
+                    int64_t arows_pad, DevBuf& R, int64_t& plane, const int* moduli = nullptr);
+// DT (n x ldt, row-major) = A^T for A (n x n, row-major, lda)
+void ozaki_transpose(cudaStream_t s, const double* A, int64_t lda, int64_t n, double* DT, int64_t ldt);
 void ozaki_reconstruct(cudaStream_t s, const OzakiMapArgs& a);
 
 // C (M x N, row-major, ldc = N) = A (M x K, row-major) . B (N x K, row-major)^T in FP64 by

@@ -196,3 +196,72 @@ def test_ozaki_config2_matches_reference_columns():
     cols, lam = g["n8192_cols"], g["n8192_lam"]
     assert np.max(np.abs(r.eigenvalues[cols] - lam) / np.abs(lam)) <= 1e-10
     assert np.max(np.abs(r.Z[:, cols] - g["n8192_z"])) <= 1e-9
+
+
+# ------------------------------------- diagonal split: fewer moduli, the same exact product
+
+
+def _moduli_after_maps(p, maps, warm=None):
+    lib = _lib.load()
+    ctx = ipt.default_context()
+    n = len(p.d)
+    h = C.c_void_p()
+    check(lib.ipt_full_upload(ctx.handle, n, _lib.dptr(p.d), None, _lib.dptr(np.ascontiguousarray(p.delta)), None,
+                              C.byref(h)))
+    try:
+        check(lib.ipt_full_reset(ctx.handle, h, _lib.dptr(warm), None))
+        check(lib.ipt_full_set_product(h, _lib.PRODUCT_OZAKI))
+        tot, ker = C.c_double(), C.c_double()
+        check(lib.ipt_full_run_maps(ctx.handle, h, maps, C.byref(tot), C.byref(ker)))
+        m = C.c_int32()
+        check(lib.ipt_full_ozaki_moduli(h, C.byref(m)))
+        return m.value
+    finally:
+        lib.ipt_full_free(h)
+
+
+def test_split_needs_fewer_moduli_on_the_ipt_iterates():
+    """Z_jj = 1 split off: the IPT iterates' off-diagonal column norms need 13 moduli at the
+    config-3 construction (|Y_j|_1 ~ 0.04); a dense O(1) warm start needs 15-16
+    (|Y'_j|_1 ~ n 2^51 > 2^61)."""
+    n = 2048
+    p = synth.dense_uniform(n, 0.32 / np.sqrt(n), 21)
+    assert _moduli_after_maps(p, 3) <= 13
+    rng = np.random.default_rng(4)
+    warm = np.eye(n) + rng.standard_normal((n, n))
+    np.fill_diagonal(warm, 1.0)
+    assert _moduli_after_maps(p, 1, np.ascontiguousarray(warm)) >= 15
+
+
+@pytest.mark.parametrize("n", [300, 1000, 2049])
+def test_split_is_bitwise_the_16_moduli_product(n, monkeypatch):
+    """The split product (fewer moduli + the diagonal term added in 128-bit integers) is the
+    same correctly rounded exact product: solves agree bit for bit with IPT_OZAKI_SPLIT=0."""
+    p = synth.dense_uniform(n, 0.3 / np.sqrt(n), 31)
+    g = ipt.build_gaps(p)
+    cfg = ipt.IterationConfig(tolerance=1e-13)
+    a = ipt.solve_full(p, g, cfg, product="ozaki")
+    monkeypatch.setenv("IPT_OZAKI_SPLIT", "0")
+    b = ipt.solve_full(p, g, cfg, product="ozaki")
+    assert a.iterations == b.iterations
+    assert np.array_equal(a.Z, b.Z) and np.array_equal(a.eigenvalues, b.eigenvalues)
+    assert a.residual_frobenius == b.residual_frobenius
+
+
+def test_split_is_bitwise_on_a_nonsymmetric_delta_and_wide_warm_start(monkeypatch):
+    """Delta_ij for the diagonal term comes from the transposed copy (nonsymmetric Delta),
+    and a warm start whose columns span many binades (Z'_jj not a power of two)."""
+    n = 700
+    rng = np.random.default_rng(9)
+    d = np.arange(1.0, n + 1.0)
+    delta = 0.01 * rng.uniform(-1, 1, (n, n))
+    np.fill_diagonal(delta, 0.0)
+    p = ipt.Partition(d, delta)
+    g = ipt.build_gaps(p)
+    z = np.eye(n) + rng.standard_normal((n, n)) * np.exp(rng.uniform(-20, 0, (n, n)))
+    np.fill_diagonal(z, 1.0)
+    cfg = ipt.IterationConfig(max_iterations=2, divergence_threshold=1e300)
+    a = ipt.solve_full(p, g, cfg, warm_start=z, want_sigma_min=False, product="ozaki")
+    monkeypatch.setenv("IPT_OZAKI_SPLIT", "0")
+    b = ipt.solve_full(p, g, cfg, warm_start=z, want_sigma_min=False, product="ozaki")
+    assert np.array_equal(a.Z, b.Z) and np.array_equal(a.eigenvalues, b.eigenvalues)

@@ -82,3 +82,16 @@ def test_integer_garner_recurrence_reconstructs_the_value():
             total += dig[l] * w
             w *= MODS[l]
         assert total == v
+
+
+def test_log2_table_in_the_kernel_source_is_rounded_down():
+    """exponent_kernel's kLog2M (the moduli count decision) never overstates log2(M_L)."""
+    import os
+    import re
+    src = open(os.path.join(os.path.dirname(__file__), "..", "paper_2012_14702_b200", "csrc", "ozaki.cu")).read()
+    body = re.search(r"kLog2M\[kMods\] = \{([^}]*)\}", src).group(1)
+    vals = [float(v) for v in body.replace("\n", " ").split(",")]
+    assert len(vals) == 16
+    for L, v in enumerate(vals, start=1):
+        exact = math.log2(math.prod(MODS[:L]))
+        assert v <= exact < v + 1e-5
