@@ -158,7 +158,9 @@ __device__ __forceinline__ double scale2(double x, int k) {
 __global__ void __launch_bounds__(256) residues_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows,
                                                        int64_t len, const int* __restrict__ e,
                                                        int8_t* __restrict__ out, int64_t ldo, int64_t plane,
-                                                       int64_t diag0, double* __restrict__ diag) {
+                                                       int64_t diag0, double* __restrict__ diag,
+                                                       const int* __restrict__ moduli) {
+  const int nm = moduli != nullptr ? *moduli : kMods;  // planes past it are never read
   const int64_t per_row = ldo >> 3;
   const int64_t total = rows * per_row;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
@@ -178,6 +180,7 @@ __global__ void __launch_bounds__(256) residues_kernel(const double* __restrict_
     static_for<0, kMods>([&](auto L) {
       constexpr int l = decltype(L)::value;
       constexpr double m = kG.m[l], minv = 1.0 / kG.m[l];
+      if (l >= nm) return;
       uint32_t w[2] = {0u, 0u};
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -508,7 +511,7 @@ void OzakiOperand::build(cudaStream_t s, const double* X, int64_t ldx, int64_t r
   exponent_kernel<<<static_cast<unsigned>(ceil_div(rows, 8)), 256, 0, s>>>(X, ldx, rows, len, ep, diag0,
                                                                             diag0 >= 0 ? moduli : nullptr);
   residues_kernel<<<2368, 256, 0, s>>>(X, ldx, rows, len, ep, reinterpret_cast<int8_t*>(res.get()), kpad, plane,
-                                       diag0, diag0 >= 0 ? diag.get() : nullptr);
+                                       diag0, diag0 >= 0 ? diag.get() : nullptr, diag0 >= 0 ? moduli : nullptr);
   IPT_LAUNCH_CHECK();
   count_launch(2);
 }
