@@ -25,10 +25,11 @@ prm = _params(ipt.IterationConfig(tolerance=1e-10))
 st = Stats()
 check(lib.ipt_single_iterate(ctx.handle, h, C.byref(prm), C.byref(st)))
 check(lib.ipt_single_finalize(ctx.handle, h, C.byref(st)))
-solve = dict(iterations=st.iterations, eigenvalue=st.eigenvalue_re, residual=st.residual)
+solve = dict(iterations=st.iterations, eigenvalue=repr(st.eigenvalue_re), residual=st.residual)
 check(lib.ipt_single_reset(ctx.handle, h, 0, None, None))
 tot, dom = C.c_double(), C.c_double()
 check(lib.ipt_single_run_steps(ctx.handle, h, 5, C.byref(tot), C.byref(dom)))
 check(lib.ipt_single_run_steps(ctx.handle, h, 20, C.byref(tot), C.byref(dom)))
-print(json.dumps(dict(variant=os.environ.get("IPT_SPMV_VARIANT", "default"), ms_step=tot.value / 20,
+print(json.dumps(dict(variant=os.environ.get("IPT_SPMV_VARIANT", "default"), tiles=os.environ.get("IPT_SPMV_TILES", "0"),
+                      ms_step=tot.value / 20,
                       ms_kernel=dom.value / 20, **solve)), flush=True)
