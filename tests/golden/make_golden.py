@@ -210,7 +210,7 @@ def full_columns(big):
     for n in ([8192, 32768] if big else [8192]):
         p = synth.config3(n=n)
         rng = np.random.default_rng(n)
-        cols = np.unique(np.concatenate([[0, 1, n // 2, n - 2, n - 1], rng.integers(0, n, 3)]))
+        cols = np.unique(np.concatenate([[0, 1, n // 2, n - 2, n - 1], rng.integers(0, n, 11)]))  # >= 16
         out[f"n{n}_cols"] = cols
         z, its, status, lam = R.solve_single_multi(p.d, p.delta, cols, tol=1e-12)
         del p

@@ -46,9 +46,12 @@ def test_config2_max_abs_rule():
 
 
 @pytest.mark.slow
-def test_config3_n32768():
+@pytest.mark.parametrize("product", ["dmma", "ozaki"])
+def test_config3_n32768(product):
+    """configs[2] at full size against 16 columns of the reference's own solve_single(j)
+    (tests/golden/full_columns.npz), with either FP64 product (DMMA / Ozaki on tcgen05)."""
     p = synth.config3()
-    r = ipt.solve_full(p, ipt.build_gaps(p), ipt.IterationConfig(tolerance=1e-12))
+    r = ipt.solve_full(p, ipt.build_gaps(p), ipt.IterationConfig(tolerance=1e-12), product=product)
     assert r.status == ipt.SolveStatus.Converged
     assert r.residual_frobenius <= 1e-10 * _frob(p)
     assert np.all(np.diag(r.Z) == 1.0)
