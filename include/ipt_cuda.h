@@ -274,6 +274,12 @@ int ipt_full_run_maps(ipt_ctx* ctx, ipt_full_problem* prob, int32_t count, doubl
                       double* ms_dominant);
 int ipt_single_run_steps(ipt_ctx* ctx, ipt_single_problem* prob, int32_t count, double* ms_total,
                          double* ms_dominant);
+/* Test hooks of the fused all-gather (row-sharded single pair with a communicator: the
+ * map kernel stores its rows of the new iterate into every peer's z over NVLink, CUDA
+ * IPC, instead of an NCCL all-gather). On a single-rank context, npeers local buffers
+ * stand in for the peers' z; ipt_single_debug_peer_z reads one back (n doubles). */
+int ipt_single_debug_peers(ipt_single_problem* prob, int32_t npeers);
+int ipt_single_debug_peer_z(ipt_single_problem* prob, int32_t peer, int32_t buf, double* out);
 
 /* Counters for gpu_launches accounting: kernels this library has launched. */
 int64_t ipt_kernel_launch_count(void);

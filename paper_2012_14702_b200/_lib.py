@@ -90,6 +90,8 @@ SIGNATURES = {
     "ipt_full_download": (C.c_int, [_vp, _vp, _dp, _dp, _dp, _dp]),
     "ipt_full_set_product": (C.c_int, [_vp, C.c_int32]),
     "ipt_full_ozaki_moduli": (C.c_int, [_vp, C.POINTER(C.c_int32)]),
+    "ipt_single_debug_peers": (C.c_int, [_vp, C.c_int32]),
+    "ipt_single_debug_peer_z": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp]),
     "ipt_full_local_columns": (C.c_int, [_vp, _i64p, _i64p]),
     "ipt_full_free": (None, [_vp]),
     "ipt_apply_map_full": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]),

@@ -813,6 +813,16 @@ int ipt_full_run_maps(ipt_ctx* ctx, ipt_full_problem* prob, int32_t count, doubl
   });
 }
 
+int ipt_single_debug_peers(ipt_single_problem* prob, int32_t npeers) {
+  if (!prob) return IPT_ERR_INVALID;
+  return guarded([&] { single_debug_peers(*reinterpret_cast<SingleProblem*>(prob), npeers); });
+}
+
+int ipt_single_debug_peer_z(ipt_single_problem* prob, int32_t peer, int32_t buf, double* out) {
+  if (!prob || !out) return IPT_ERR_INVALID;
+  return guarded([&] { single_debug_peer_z(*reinterpret_cast<SingleProblem*>(prob), peer, buf, out); });
+}
+
 int ipt_single_run_steps(ipt_ctx* ctx, ipt_single_problem* prob, int32_t count, double* ms_total,
                          double* ms_dominant) {
   return guarded([&] {

@@ -34,7 +34,9 @@ struct DevBuf {
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
+  bool plain = false;  // cudaMalloc'd (exportable by CUDA IPC) instead of the stream-ordered pool
   void alloc(size_t n, bool zero = true);
+  void alloc_plain(size_t n);  // zeroed
   void release();
   double* get() const { return p; }
 };
@@ -149,6 +151,8 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
                              const int32_t* cols, const double* val_re, const double* val_im,
                              bool keep_host_anchor_source, bool force_complex = false, int64_t row_begin = -1,
                              int64_t row_end = -1);
+void single_debug_peers(SingleProblem& P, int npeers);
+void single_debug_peer_z(SingleProblem& P, int peer, int buf, double* out);
 void single_free(SingleProblem* P);
 void single_reset(SingleProblem& P, int64_t anchor, const double* warm_re, const double* warm_im,
                   int max_iter_hint, bool renormalize = true);

@@ -26,6 +26,8 @@
 
 namespace iptb {
 
+constexpr int kMaxPeers = 7;  // one 8-GPU node
+
 struct SingleProblem {
   Ctx* ctx = nullptr;
   int64_t n = 0;
@@ -61,8 +63,22 @@ struct SingleProblem {
   DevBuf trace;
   int trace_cap = 0;
   int enq = 0;
+  // Fused all-gather over peer memory (real maps with a communicator): the map kernel
+  // stores its rows of the new iterate straight into every peer's z buffer (CUDA IPC
+  // over NVLink) instead of an NCCL all-gather after it; z[b] are then cudaMalloc'd
+  // (exportable). peer_z[b][q]: peer q's z[b].
+  bool p2p = false;
+  int npeers = 0;
+  double* peer_z[2][kMaxPeers] = {};
+  bool peer_ipc = false;  // peer_z opened by cudaIpcOpenMemHandle (else: local emulation)
   ~SingleProblem() {
     if (state) cudaFree(state);
+    for (int b = 0; b < 2; ++b)
+      for (int q = 0; q < npeers; ++q)
+        if (peer_z[b][q]) {
+          if (peer_ipc) cudaIpcCloseMemHandle(peer_z[b][q]);
+          else cudaFree(peer_z[b][q]);
+        }
   }
 };
 
@@ -296,7 +312,15 @@ struct MapArgs {
   int schedule;
   double snap;
   double* partials;
+  double* peer[kMaxPeers];  // kMvMap: the same rows of the new iterate in every peer's z
+  int npeers;
 };
+
+// Remote stores of the fused all-gather must be visible system-wide before the
+// collective that orders the next step (reduce_and_allreduce) starts.
+__device__ __forceinline__ void peer_fence(const MapArgs& a) {
+  if (a.npeers > 0) __threadfence_system();
+}
 
 // Per-row epilogue shared by dense and CSR kernels. Accumulates into v.
 template <int MODE>
@@ -314,6 +338,7 @@ __device__ __forceinline__ void row_epilogue(const MapArgs& a, int64_t i, double
       f = __dmul_rn(scale, __dmul_rn(g, __dsub_rn(__dmul_rn(zi, *a.wa), w)));
     }
     a.fz[i] = f;
+    for (int q = 0; q < a.npeers; ++q) a.peer[q][i] = f;  // fused all-gather (NVLink stores)
     const double df = __dsub_rn(zi, f);
     v[0] = __fma_rn(df, df, v[0]);
     v[1] = __fma_rn(zi, zi, v[1]);
@@ -365,6 +390,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_map_kernel(const double*
   for (int r = 0; r < kGemvRows; ++r)
     if (lane == r && r < nrows) row_epilogue<MODE>(a, a.row0 + lr0 + r, w[r], scale, lam, v);
   if (MODE == kMvStore) return;
+  if (MODE == kMvMap) peer_fence(a);
   block_reduce4<kGemvWarps>(v, red);
   if (threadIdx.x == 0) {
     double* o = a.partials + size_t(blockIdx.x) * 4;
@@ -396,6 +422,7 @@ __global__ void __launch_bounds__(256, kSpmvMinBlocks) spmv_map_kernel(const int
     if (valid && sl == 0) row_epilogue<MODE>(a, a.row0 + lr, w, scale, lam, v);
   }
   if (MODE == kMvStore) return;
+  if (MODE == kMvMap) peer_fence(a);
   block_reduce4<8>(v, red);
   if (threadIdx.x == 0) {
     double* o = a.partials + size_t(blockIdx.x) * 4;
@@ -430,6 +457,7 @@ __global__ void __launch_bounds__(256, MINB) spmv_group_kernel(const int64_t* __
     }
   }
   if (MODE == kMvStore) return;
+  if (MODE == kMvMap) peer_fence(a);
   block_reduce4<8>(v, red);
   if (threadIdx.x == 0) {
     double* o = a.partials + size_t(blockIdx.x) * 4;
@@ -620,6 +648,10 @@ MapArgs map_args(SingleProblem& P, int src) {
   a.d = P.dre.get();
   a.z = P.z[src].get();
   a.fz = P.z[src ^ 1].get();
+  if (P.p2p && !P.cplx) {
+    a.npeers = P.npeers;
+    for (int q = 0; q < P.npeers; ++q) a.peer[q] = P.peer_z[src ^ 1][q];
+  }
   a.wa = P.wa.get();
   a.anchor = P.anchor;
   a.row0 = P.r0;
@@ -700,7 +732,10 @@ void enqueue_real_map(SingleProblem& P, int src, const ipt_params* prm, double* 
   cudaStream_t s = P.ctx->stream;
   MapArgs a = map_args(P, src);
   if (MODE == kMvFinal || MODE == kMvAccel) a.state = nullptr;
-  if (fz_out) a.fz = fz_out;
+  if (fz_out) {
+    a.fz = fz_out;
+    a.npeers = 0;  // not the next iterate: no fused all-gather
+  }
   if (prm) {
     a.schedule = prm->schedule;
     a.snap = 0.25 * prm->tolerance;
@@ -735,7 +770,10 @@ void enqueue_iteration(SingleProblem& P, int k, const ipt_params& prm, cudaEvent
     IPT_LAUNCH_CHECK();
     count_launch();
   }
-  allgather_z(P, src ^ 1);
+  // Real maps with peer buffers stored their rows into every rank's z in the map kernel
+  // (fused all-gather); the all-reduce of the stop sums right after orders those stores
+  // before any rank's next step.
+  if (!(P.p2p && !P.cplx)) allgather_z(P, src ^ 1);
   reduce_and_allreduce(P, st, true);
   decide_single_kernel<<<1, 1, 0, c.stream>>>(
       st, P.sums.get(), k, prm.tolerance, prm.max_iterations, prm.divergence_threshold, prm.schedule,
@@ -772,7 +810,93 @@ void upload_anchor_row(SingleProblem& P) {
   P.ctx->sync();
 }
 
+// Fused all-gather setup: both z buffers become cudaMalloc'd (IPC-exportable), their
+// handles are all-gathered over the library communicator and every rank maps its peers'
+// buffers. The outcome is agreed by a min all-reduce, so if any rank cannot map a peer all
+// of them keep the NCCL all-gather. IPT_P2P=0 keeps it too.
+void setup_peer_gather(SingleProblem& P, int64_t zlen) {
+  Ctx& c = *P.ctx;
+  const int g = c.nranks;
+  if (g <= 1 || P.cplx || g - 1 > kMaxPeers) return;
+  const char* e = std::getenv("IPT_P2P");
+  if (e && e[0] == '0') return;
+  cudaStream_t s = c.stream;
+  for (int b = 0; b < 2; ++b) P.z[b].alloc_plain(zlen);
+  struct Handles {
+    cudaIpcMemHandle_t h[2];
+  };
+  Handles mine{};
+  int ok = 1;
+  for (int b = 0; b < 2; ++b)
+    if (cudaIpcGetMemHandle(&mine.h[b], P.z[b].get()) != cudaSuccess) ok = 0;
+  cudaGetLastError();
+  const size_t hb = sizeof(Handles);
+  DevBuf dev;
+  dev.alloc(ceil_div(int64_t(hb) * g, 8) + 1);
+  char* dv = reinterpret_cast<char*>(dev.get());
+  IPT_CUDA(cudaMemcpyAsync(dv + hb * c.rank, &mine, hb, cudaMemcpyHostToDevice, s));
+  IPT_NCCL(ncclAllGather(dv + hb * c.rank, dv, hb, ncclChar, c.comm, s));
+  std::vector<Handles> all(g);
+  IPT_CUDA(cudaMemcpyAsync(all.data(), dv, hb * g, cudaMemcpyDeviceToHost, s));
+  IPT_CUDA(cudaStreamSynchronize(s));
+  int q = 0;
+  for (int r = 0; r < g && ok; ++r) {
+    if (r == c.rank) continue;
+    for (int b = 0; b < 2 && ok; ++b) {
+      void* ptr = nullptr;
+      if (cudaIpcOpenMemHandle(&ptr, all[r].h[b], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = 0;
+      } else {
+        P.peer_z[b][q] = static_cast<double*>(ptr);
+      }
+    }
+    ++q;
+  }
+  P.npeers = q;
+  P.peer_ipc = true;
+  int* dok = reinterpret_cast<int*>(dev.get());
+  IPT_CUDA(cudaMemcpyAsync(dok, &ok, sizeof(int), cudaMemcpyHostToDevice, s));
+  IPT_NCCL(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, c.comm, s));
+  int all_ok = 0;
+  IPT_CUDA(cudaMemcpyAsync(&all_ok, dok, sizeof(int), cudaMemcpyDeviceToHost, s));
+  IPT_CUDA(cudaStreamSynchronize(s));
+  if (all_ok) {
+    P.p2p = true;
+    return;
+  }
+  for (int b = 0; b < 2; ++b)
+    for (int k = 0; k < kMaxPeers; ++k)
+      if (P.peer_z[b][k]) {
+        cudaIpcCloseMemHandle(P.peer_z[b][k]);
+        P.peer_z[b][k] = nullptr;
+      }
+  P.npeers = 0;
+}
+
 }  // namespace
+
+// Tests on one GPU: npeers local buffer pairs stand in for the peers' z (the map kernel
+// stores its rows into them exactly as into IPC-mapped peer memory).
+void single_debug_peers(SingleProblem& P, int npeers) {
+  if (npeers < 0 || npeers > kMaxPeers || P.cplx || P.ctx->nranks != 1)
+    throw InvalidArgument("debug peers: 0..7 peers on a real single-rank problem");
+  for (int b = 0; b < 2; ++b)
+    for (int q = 0; q < npeers; ++q) {
+      IPT_CUDA(cudaMalloc(&P.peer_z[b][q], sizeof(double) * P.z[b].count));
+      IPT_CUDA(cudaMemset(P.peer_z[b][q], 0, sizeof(double) * P.z[b].count));
+    }
+  P.npeers = npeers;
+  P.peer_ipc = false;
+  P.p2p = npeers > 0;
+}
+
+void single_debug_peer_z(SingleProblem& P, int peer, int buf, double* out) {
+  if (peer < 0 || peer >= P.npeers || buf < 0 || buf > 1) throw InvalidArgument("debug peers: bad index");
+  IPT_CUDA(cudaMemcpy(out, P.peer_z[buf][peer], sizeof(double) * P.n, cudaMemcpyDeviceToHost));
+}
+
+
 
 // ------------------------------------------------------------ C++ entry points
 
@@ -860,6 +984,7 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
     P->z[b2].alloc(zlen);
     P->zi[b2].alloc(zlen);
   }
+  setup_peer_gather(*P, zlen);
   P->w.alloc(zlen);
   P->wi.alloc(zlen);
   P->wa.alloc(2);

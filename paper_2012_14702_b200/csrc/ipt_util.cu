@@ -76,9 +76,21 @@ void DevBuf::alloc(size_t n, bool zero) {
   // memset) must be complete before any copy or kernel on the library stream uses it.
   IPT_CUDA(cudaStreamSynchronize(nullptr));
 }
+void DevBuf::alloc_plain(size_t n) {
+  release();
+  if (n == 0) n = 1;
+  IPT_CUDA(cudaMalloc(&p, n * sizeof(double)));
+  plain = true;
+  count = n;
+  IPT_CUDA(cudaMemset(p, 0, n * sizeof(double)));
+}
 void DevBuf::release() {
-  if (p) cudaFreeAsync(p, nullptr);
+  if (p) {
+    if (plain) cudaFree(p);
+    else cudaFreeAsync(p, nullptr);
+  }
   p = nullptr;
+  plain = false;
   count = 0;
 }
 

@@ -119,3 +119,67 @@ def test_bad_row_blocks_rejected():
     for b, e in [(4, 4), (2, 9), (-1, 3)]:
         with pytest.raises(ValueError):
             check(lib.ipt_single_upload_dense_rows(ctx.handle, n, dptr(d), None, dptr(delta), None, b, e, C.byref(h)))
+
+
+def _steps_with_peers(upload, n, warm, steps, npeers):
+    """As _steps, with npeers local buffers standing in for the peers' z: the map kernel
+    stores its rows of every new iterate into them (the fused all-gather of a
+    multi-GPU run, ipt_single.cu setup_peer_gather)."""
+    lib = _lib.load()
+    ctx = ipt.default_context()
+    h = C.c_void_p()
+    check(upload(ctx, C.byref(h)))
+    try:
+        check(lib.ipt_single_debug_peers(h, npeers))
+        check(lib.ipt_single_reset(ctx.handle, h, 0, dptr(warm), None))
+        prm = _params(ipt.IterationConfig(max_iterations=steps), ignore_convergence=1, divergence_threshold=1e300)
+        st = Stats()
+        check(lib.ipt_single_iterate(ctx.handle, h, C.byref(prm), C.byref(st)))
+        z = np.empty(n)
+        check(lib.ipt_single_download(ctx.handle, h, dptr(z), None))
+        peers = []
+        for q in range(npeers):
+            pz = np.empty(n)
+            check(lib.ipt_single_debug_peer_z(h, q, steps & 1, dptr(pz)))
+            peers.append(pz)
+        return z, peers
+    finally:
+        lib.ipt_single_free(h)
+
+
+@pytest.mark.parametrize("kind", ["dense", "csr"])
+@pytest.mark.parametrize("steps", [1, 2, 3])
+def test_fused_allgather_stores_reach_every_peer(kind, steps):
+    """Each rank's map kernel writes its rows of the new iterate into all peers' z: with
+    3 stand-in peers every one holds exactly the block's rows of the current iterate, and
+    the run itself is unchanged (bit for bit)."""
+    if kind == "dense":
+        p = synth.dense_normal(2048)
+        whole, block, keep = _dense(p)
+        b, e = 512, 1536
+    else:
+        p = synth.csr_ci(8192, 32, 0.01, 42)
+        whole, block, keep = _csr(p)
+        b, e = 2048, 6144
+    n = p.size()
+    warm = _warm(n, 3)
+    plain = _steps(block(b, e), n, warm, steps)
+    z, peers = _steps_with_peers(block(b, e), n, warm, steps, 3)
+    assert np.array_equal(z, plain)
+    for pz in peers:
+        assert np.array_equal(pz[b:e], z[b:e])
+
+
+def test_debug_peers_rejected_on_complex_or_too_many():
+    lib = _lib.load()
+    ctx = ipt.default_context()
+    n = 64
+    p = synth.dense_normal(n)
+    h = C.c_void_p()
+    check(lib.ipt_single_upload_dense(ctx.handle, n, dptr(p.d), None, dptr(np.ascontiguousarray(p.delta)), None,
+                                      C.byref(h)))
+    try:
+        with pytest.raises(ValueError):
+            check(lib.ipt_single_debug_peers(h, 8))
+    finally:
+        lib.ipt_single_free(h)

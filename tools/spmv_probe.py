@@ -30,6 +30,6 @@ check(lib.ipt_single_reset(ctx.handle, h, 0, None, None))
 tot, dom = C.c_double(), C.c_double()
 check(lib.ipt_single_run_steps(ctx.handle, h, 5, C.byref(tot), C.byref(dom)))
 check(lib.ipt_single_run_steps(ctx.handle, h, 20, C.byref(tot), C.byref(dom)))
-print(json.dumps(dict(variant=os.environ.get("IPT_SPMV_VARIANT", "default"), tiles=os.environ.get("IPT_SPMV_TILES", "0"),
+print(json.dumps(dict(variant=os.environ.get("IPT_SPMV_VARIANT", "default"),
                       ms_step=tot.value / 20,
                       ms_kernel=dom.value / 20, **solve)), flush=True)
