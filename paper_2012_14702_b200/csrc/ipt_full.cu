@@ -758,9 +758,20 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
   cudaStream_t s = c.stream;
 
   ProfMarks pm("full_upload");
-  P->A1.alloc(size_t(P->rows_pad) * P->lda);
+  // With a communicator every rank passes the same Delta (replicated); each uploads only
+  // its 1/g slice of rows over PCIe and an in-place NCCL all-gather over NVLink assembles
+  // the whole matrix on every GPU (g x less host traffic than g full uploads).
+  const bool sharded_upload = c.nranks > 1 && !P->cplx;
+  const int64_t up_chunk = ceil_div(P->rows_pad, int64_t(c.nranks));
+  P->A1.alloc(size_t(sharded_upload ? std::max(P->rows_pad, up_chunk * c.nranks) : P->rows_pad) * P->lda);
   pm.mark("alloc_delta");
-  if (!P->cplx) {
+  if (sharded_upload) {
+    const int64_t r0 = std::min<int64_t>(n, c.rank * up_chunk), r1 = std::min<int64_t>(n, (c.rank + 1) * up_chunk);
+    if (r1 > r0) h2d_rows(c, P->A1.get() + r0 * P->lda, P->lda, delta_re + r0 * n, n, r1 - r0, n);
+    IPT_NCCL(ncclAllGather(P->A1.get() + c.rank * up_chunk * P->lda, P->A1.get(), size_t(up_chunk * P->lda),
+                           ncclDouble, c.comm, s));
+    pm.mark("h2d+allgather");
+  } else if (!P->cplx) {
     h2d_rows(c, P->A1.get(), P->lda, delta_re, n, n, n);  // pinned, double-buffered
     pm.mark("h2d");
   } else {
