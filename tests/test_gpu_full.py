@@ -203,16 +203,18 @@ def test_complex_certified_instances_converge_geometrically():
         assert r.residual_frobenius == pytest.approx(res, rel=0.5, abs=1e-13)
 
 
+@pytest.mark.parametrize("product", ["dmma", "ozaki"])
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 33, 129, 200])
-def test_odd_sizes_match_oracle(port_arm, n):
-    """Arbitrary N (predicated tails, no CPU fallback) against the restatement."""
+def test_odd_sizes_match_oracle(port_arm, n, product):
+    """Arbitrary N (predicated tails, no CPU fallback) against the restatement, with
+    either FP64 product."""
     rng = np.random.default_rng(n)
     delta = 0.05 * rng.uniform(-1, 1, (n, n))
     delta = 0.5 * (delta + delta.T)
     np.fill_diagonal(delta, 0)
     d = np.arange(1.0, n + 1)
     p = ipt.Partition(d, delta)
-    r = ipt.solve_full(p, ipt.build_gaps(p), ipt.IterationConfig(tolerance=1e-13))
+    r = ipt.solve_full(p, ipt.build_gaps(p), ipt.IterationConfig(tolerance=1e-13), product=product)
     o = port_arm.solve_full(d, delta, tol=1e-13)
     assert abs(r.iterations - o["iterations"]) <= 1
     assert np.max(np.abs(r.eigenvalues - o["eigenvalues"].real) / np.abs(o["eigenvalues"].real)) <= LAM_REL
