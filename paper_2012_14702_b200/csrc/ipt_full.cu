@@ -943,7 +943,24 @@ void full_reset(FullProblem& P, const double* warm_re, const double* warm_im, in
   P.gathered.release();
 }
 
-void full_set_product(FullProblem& P, int product) { P.product = product; }
+// The Ozaki product needs residue planes of Delta, Z and the products (16 bytes per
+// element each) and Delta transposed: when they do not fit next to what the solve holds,
+// W = Delta Z stays on the DMMA path (FP64 either way).
+int effective_product(const FullProblem& P, int product) {
+  if (product != IPT_PRODUCT_OZAKI || P.oz_delta_ready) return product;
+  const int64_t kpad = round_up(P.n, kOzakiKPad), arows = round_up(P.n, 512);
+  const double need = double(kOzakiMods) * (double(arows) * kpad + double(P.cols_pad) * kpad +
+                                            double(P.cols_pad) * arows) +
+                      (P.oz_split ? 8.0 * double(P.n) * double(P.lda) : 0.0) + double(1 << 30);
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+    cudaGetLastError();
+    return product;
+  }
+  return need <= double(free_b) ? product : IPT_PRODUCT_DMMA;
+}
+
+void full_set_product(FullProblem& P, int product) { P.product = effective_product(P, product); }
 
 int full_ozaki_moduli(FullProblem& P) {
   if (!use_ozaki(P)) return 0;
@@ -956,7 +973,7 @@ int full_ozaki_moduli(FullProblem& P) {
 
 void full_iterate(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
   Ctx& c = *P.ctx;
-  P.product = prm.product;
+  P.product = effective_product(P, prm.product);
   if (!(prm.tolerance > 0.0)) throw InvalidArgument("config: tolerance must be positive");
   if (prm.max_iterations <= 0) throw InvalidArgument("config: max_iterations must be positive");
   if (!(prm.divergence_threshold > 1.0)) throw InvalidArgument("config: divergence_threshold must exceed 1");
