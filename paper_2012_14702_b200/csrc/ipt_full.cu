@@ -67,6 +67,8 @@ struct FullProblem {
   int product = IPT_PRODUCT_DMMA;
   OzakiOperand oz_delta, oz_z;
   DevBuf oz_R;
+  OzakiOperand oz_delta_i, oz_delta_s;  // complex 3M: Di and Dr + Di
+  bool oz_finite = false;                // Delta has no Inf / NaN (the Ozaki product is exact)
   bool oz_delta_ready = false;
   DevBuf oz_dt;     // Delta transposed (the split-off diagonal term reads Delta_ij by column)
   DevBuf oz_mods;   // device int: moduli the current product needs
@@ -551,6 +553,84 @@ int64_t num_partials(const FullProblem& P) {
 
 // Complex 3M product for the current Z (zs): wd (K2), S = Zr + Zi, T1 = Dr Zr, T2 = Di Zi,
 // then the T3 GEMM with the complex epilogue `mode` (map into zd, or the residual).
+bool use_ozaki(const FullProblem& P);
+
+// Complex 3M with each real product by Ozaki scheme II: T1 = Dr Zr and T2 = Di Zi are
+// reconstructed into P.T1 / P.T2, then T3 = (Dr + Di)(Zr + Zi) is reconstructed with the
+// complex map (mode 3) or closing residual (mode 4) epilogue, the same formulas as the
+// kGemmMapC / kGemmResidC GEMM epilogues. Each product takes the moduli its operand's
+// column 1-norms require (no diagonal split: 14 on the IPT iterates).
+void ozaki_apply_complex(FullProblem& P, const double* zs, double* zd, int mode, const LoopState* st,
+                         cudaEvent_t ev_a, cudaEvent_t ev_b) {
+  cudaStream_t s = P.ctx->stream;
+  const int64_t kpad = round_up(P.n, kOzakiKPad);
+  const int64_t arows = round_up(P.n, 512);
+  if (!P.oz_delta_ready) {
+    P.oz_delta.build(s, P.A1.get(), P.lda, P.n, P.n, arows, kpad);
+    P.oz_delta_i.build(s, P.A2.get(), P.lda, P.n, P.n, arows, kpad);
+    P.oz_delta_s.build(s, P.A3.get(), P.lda, P.n, P.n, arows, kpad);
+    P.oz_mods.alloc(2, false);
+    P.oz_delta_ready = true;
+  }
+  int* mods = reinterpret_cast<int*>(P.oz_mods.get());
+  int64_t plane = 0;
+  if (ev_a) IPT_CUDA(cudaEventRecord(ev_a, s));
+  const OzakiOperand* ops[2] = {&P.oz_delta, &P.oz_delta_i};
+  const double* xs[2] = {zs, zs + P.ld};
+  double* outs[2] = {P.T1.get(), P.T2.get()};
+  for (int t = 0; t < 2; ++t) {
+    P.oz_z.build(s, xs[t], P.ldz, P.ncols, P.n, P.cols_pad, kpad, -1, mods + t);
+    ozaki_products(s, P.oz_z, *ops[t], P.cols_pad, arows, P.oz_R, plane, mods + t);
+    OzakiMapArgs a{};
+    a.R = reinterpret_cast<const int8_t*>(P.oz_R.get());
+    a.plane = plane;
+    a.ldr = arows;
+    a.eA = ops[t]->exps();
+    a.eB = P.oz_z.exps();
+    a.F = outs[t];
+    a.ldz = P.ld;
+    a.n = P.n;
+    a.ncols = P.ncols;
+    a.col0 = P.col0;
+    a.mode = 2;
+    a.partials = P.partials.get();
+    a.state = st;
+    a.moduli = mods + t;
+    ozaki_reconstruct(s, a);
+  }
+  P.oz_z.build(s, P.S.get(), P.ld, P.ncols, P.n, P.cols_pad, kpad, -1, mods + 2);
+  ozaki_products(s, P.oz_z, P.oz_delta_s, P.cols_pad, arows, P.oz_R, plane, mods + 2);
+  if (ev_b) IPT_CUDA(cudaEventRecord(ev_b, s));
+  OzakiMapArgs a{};
+  a.R = reinterpret_cast<const int8_t*>(P.oz_R.get());
+  a.plane = plane;
+  a.ldr = arows;
+  a.eA = P.oz_delta_s.exps();
+  a.eB = P.oz_z.exps();
+  a.Z = zs;
+  a.Zi = zs + P.ld;
+  a.ldz = P.ldz;
+  a.T1 = P.T1.get();
+  a.T2 = P.T2.get();
+  a.ldt = P.ld;
+  a.d = P.dre.get();
+  a.di = P.dim.get();
+  a.wd = P.wd.get();
+  a.wdi = P.wdi.get();
+  a.lam = P.lam.get();
+  a.lami = P.lami.get();
+  a.F = zd;
+  a.Fi = zd ? zd + P.ld : nullptr;
+  a.n = P.n;
+  a.ncols = P.ncols;
+  a.col0 = P.col0;
+  a.mode = mode == kGemmMapC ? 3 : 4;
+  a.partials = P.partials.get();
+  a.state = st;
+  a.moduli = mods + 2;
+  ozaki_reconstruct(s, a);
+}
+
 void launch_complex_products(FullProblem& P, const double* zs, double* zd, int mode, const LoopState* st,
                              cudaEvent_t ev_a, cudaEvent_t ev_b) {
   Ctx& c = *P.ctx;
@@ -566,6 +646,10 @@ void launch_complex_products(FullProblem& P, const double* zs, double* zd, int m
         P.wd.get(), P.wdi.get(), P.dre.get(), P.dim.get(), P.ncols, P.col0, P.lam.get(), P.lami.get());
     IPT_LAUNCH_CHECK();
     count_launch();
+  }
+  if (use_ozaki(P)) {
+    ozaki_apply_complex(P, zs, zd, mode, st, ev_a, ev_b);
+    return;
   }
   if (ev_a) IPT_CUDA(cudaEventRecord(ev_a, c.stream));
   GemmParams g1 = gemm_params(P, P.A1.get(), zs, P.T1.get(), P.ld);
@@ -600,8 +684,10 @@ void allreduce_sums(FullProblem& P, bool with_max) {
 }
 
 bool use_ozaki(const FullProblem& P) {
-  return P.product == IPT_PRODUCT_OZAKI && !P.cplx && !P.sparse && P.delta_finite && P.n <= kOzakiMaxK;
+  return P.product == IPT_PRODUCT_OZAKI && !P.sparse && P.oz_finite && P.n <= kOzakiMaxK;
 }
+
+int64_t map_partials(const FullProblem& P) { return use_ozaki(P) ? kOzakiGrid : num_partials(P); }
 
 // W = Delta Z by Ozaki scheme II, then the map (mode 0) or the closing residual (mode 1).
 // ev_a / ev_b (optional) bracket the 16 INT8 GEMMs alone (the roofline kernel).
@@ -697,7 +783,7 @@ void enqueue_map(FullProblem& P, int k, const ipt_params& prm, cudaEvent_t ev_a 
   } else {
     launch_complex_products(P, zs, zd, kGemmMapC, st, ev_a, ev_b);
   }
-  reduce_partials(c.stream, P.partials.get(), num_partials(P), P.sums.get(), st);
+  reduce_partials(c.stream, P.partials.get(), map_partials(P), P.sums.get(), st);
   allreduce_sums(P, true);
   decide_full_kernel<<<1, 1, 0, c.stream>>>(
       st, P.sums.get(), k, prm.tolerance, prm.max_iterations, prm.divergence_threshold,
@@ -804,18 +890,20 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
   P->partials.alloc(size_t(std::max<int64_t>(num_partials(*P), kOzakiGrid)) * 4);
   P->sums.alloc(4);
   IPT_CUDA(cudaMalloc(&P->state, sizeof(LoopState)));
-  if (!P->cplx) {
+  {
     int* flag = nullptr;
     IPT_CUDA(cudaMalloc(&flag, sizeof(int)));
     IPT_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
     count_nonfinite_kernel<<<1184, 256, 0, s>>>(P->A1.get(), int64_t(P->rows_pad) * P->lda, flag);
+    if (P->cplx) count_nonfinite_kernel<<<1184, 256, 0, s>>>(P->A2.get(), int64_t(P->rows_pad) * P->lda, flag);
     IPT_LAUNCH_CHECK();
-    count_launch();
+    count_launch(P->cplx ? 2 : 1);
     int h = 1;
     IPT_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
     c.sync();
     cudaFree(flag);
-    P->delta_finite = (h == 0);
+    P->delta_finite = !P->cplx && h == 0;  // (the real identity-start shortcut)
+    P->oz_finite = h == 0;
     pm.mark("finite_check");
   }
   c.sync();
@@ -949,9 +1037,10 @@ void full_reset(FullProblem& P, const double* warm_re, const double* warm_im, in
 int effective_product(const FullProblem& P, int product) {
   if (product != IPT_PRODUCT_OZAKI || P.oz_delta_ready) return product;
   const int64_t kpad = round_up(P.n, kOzakiKPad), arows = round_up(P.n, 512);
-  const double need = double(kOzakiMods) * (double(arows) * kpad + double(P.cols_pad) * kpad +
+  const double ndelta = P.cplx ? 3.0 : 1.0;
+  const double need = double(kOzakiMods) * (ndelta * double(arows) * kpad + double(P.cols_pad) * kpad +
                                             double(P.cols_pad) * arows) +
-                      (P.oz_split ? 8.0 * double(P.n) * double(P.lda) : 0.0) + double(1 << 30);
+                      (P.oz_split && !P.cplx ? 8.0 * double(P.n) * double(P.lda) : 0.0) + double(1 << 30);
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
     cudaGetLastError();
@@ -964,11 +1053,12 @@ void full_set_product(FullProblem& P, int product) { P.product = effective_produ
 
 int full_ozaki_moduli(FullProblem& P) {
   if (!use_ozaki(P)) return 0;
-  if (!P.oz_split) return kOzakiMods;
-  int m = 0;
-  IPT_CUDA(cudaMemcpyAsync(&m, P.oz_mods.get(), sizeof(int), cudaMemcpyDeviceToHost, P.ctx->stream));
+  if (!P.cplx && !P.oz_split) return kOzakiMods;
+  int m[3] = {0, 0, 0};
+  IPT_CUDA(cudaMemcpyAsync(m, P.oz_mods.get(), sizeof(int) * (P.cplx ? 3 : 1), cudaMemcpyDeviceToHost,
+                           P.ctx->stream));
   IPT_CUDA(cudaStreamSynchronize(P.ctx->stream));
-  return m;
+  return std::max(m[0], std::max(m[1], m[2]));  // complex: the largest of T1, T2, T3
 }
 
 void full_iterate(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
@@ -1061,8 +1151,7 @@ void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
   } else {
     launch_complex_products(P, z, nullptr, kGemmResidC, nullptr, nullptr, nullptr);
   }
-  reduce_partials(s, P.partials.get(), (!P.cplx && use_ozaki(P)) ? kOzakiGrid : num_partials(P), P.sums.get(),
-                  nullptr);
+  reduce_partials(s, P.partials.get(), map_partials(P), P.sums.get(), nullptr);
   allreduce_sums(P, false);
   double h4[4];
   IPT_CUDA(cudaMemcpyAsync(h4, P.sums.get(), sizeof(h4), cudaMemcpyDeviceToHost, s));

@@ -89,8 +89,9 @@ __constant__ double kLog2M[kMods] = {8.0,       15.994353, 23.977347, 31.94889, 
                                      102.524502, 110.161127, 117.783179, 125.375636};
 
 // Row (or column) exponent: max |x| * 2^e in [2^52, 2^53); flag non-finite rows.
-// Split operands (diag0 >= 0) also bound the row's off-diagonal integer 1-norm and raise
-// *moduli to the count that keeps |Delta' Y'| < 2^53 |Y'|_1 below M / 2.
+// With a moduli counter the kernel also bounds the row's integer 1-norm (off the diagonal
+// for split operands, diag0 >= 0) and raises *moduli to the count that keeps
+// |A' X'| < 2^53 |X'|_1 below M / 2.
 __global__ void exponent_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows, int64_t len,
                                 int* __restrict__ e, int64_t diag0, int* __restrict__ moduli) {
   const int lane = threadIdx.x & 31;
@@ -437,6 +438,27 @@ __device__ __forceinline__ void reconstruct_body(const OzakiMapArgs& a, double (
         a.F[j * a.ldz + i] = w;
         continue;
       }
+      if (a.mode >= 3) {  // complex 3M: this product is T3 = (Dr + Di)(Zr + Zi)
+        const double t1 = a.T1[j * a.ldt + i], t2 = a.T2[j * a.ldt + i];
+        const cd wc{t1 - t2, w - t1 - t2};
+        const cd z{a.Z[j * a.ldz + i], a.Zi[j * a.ldz + i]};
+        const cd di{a.d[i], a.di[i]};
+        if (a.mode == 3) {
+          const cd dj{a.d[jg], a.di[jg]}, wj{a.wd[j], a.wdi[j]};
+          const cd f = (i == jg) ? cd{1.0, 0.0} : cdiv(csub(cmul(z, wj), wc), csub(di, dj));
+          a.F[j * a.ldz + i] = f.re;
+          a.Fi[j * a.ldz + i] = f.im;
+          const cd df = csub(f, z);
+          v[0] += df.re * df.re + df.im * df.im;
+          v[1] += z.re * z.re + z.im * z.im;
+          v[2] += f.re * f.re + f.im * f.im;
+          v[3] = nan_max(v[3], hypot(df.re, df.im));
+        } else {
+          const cd r = csub(cadd(cmul(di, z), wc), cmul(z, cd{a.lam[j], a.lami[j]}));
+          v[0] += r.re * r.re + r.im * r.im;
+        }
+        continue;
+      }
       const double z = a.Z[j * a.ldz + i];
       const double di = a.d[i];
       if (a.mode == 0) {
@@ -508,10 +530,9 @@ void OzakiOperand::build(cudaStream_t s, const double* X, int64_t ldx, int64_t r
   if (diag0 >= 0 && diag.count < size_t(rows_pad)) diag.alloc(rows_pad);
   int* ep = reinterpret_cast<int*>(e.get());
   if (moduli != nullptr) IPT_CUDA(cudaMemsetAsync(moduli, 0, sizeof(int), s));
-  exponent_kernel<<<static_cast<unsigned>(ceil_div(rows, 8)), 256, 0, s>>>(X, ldx, rows, len, ep, diag0,
-                                                                            diag0 >= 0 ? moduli : nullptr);
+  exponent_kernel<<<static_cast<unsigned>(ceil_div(rows, 8)), 256, 0, s>>>(X, ldx, rows, len, ep, diag0, moduli);
   residues_kernel<<<2368, 256, 0, s>>>(X, ldx, rows, len, ep, reinterpret_cast<int8_t*>(res.get()), kpad, plane,
-                                       diag0, diag0 >= 0 ? diag.get() : nullptr, diag0 >= 0 ? moduli : nullptr);
+                                       diag0, diag0 >= 0 ? diag.get() : nullptr, moduli);
   IPT_LAUNCH_CHECK();
   count_launch(2);
 }

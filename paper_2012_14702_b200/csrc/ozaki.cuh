@@ -52,7 +52,16 @@ struct OzakiMapArgs {
   const double* wd;
   const double* lam;
   int64_t n, ncols, col0;
-  int mode;  // 0: map, 1: closing residual, 2: store W
+  // complex 3M (modes 3 / 4): this product is T3, T1 = Dr Zr and T2 = Di Zi already stored
+  const double* T1;
+  const double* T2;
+  int64_t ldt;
+  const double* Zi;
+  const double* di;
+  const double* wdi;
+  const double* lami;
+  double* Fi;
+  int mode;  // 0: map, 1: closing residual, 2: store W, 3: complex map, 4: complex residual
   double* partials;
   const LoopState* state;
 };

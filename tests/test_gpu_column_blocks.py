@@ -111,7 +111,8 @@ def test_ozaki_blocks(iters):
         check_blocks(ref, outs, n)
 
 
-def test_complex_blocks():
+@pytest.mark.parametrize("product", [_lib.PRODUCT_DMMA, _lib.PRODUCT_OZAKI])
+def test_complex_blocks(product):
     n = 300
     rng = np.random.default_rng(2)
     d = np.arange(1.0, n + 1)
@@ -119,7 +120,7 @@ def test_complex_blocks():
     di = 0.02 * rng.standard_normal((n, n))
     np.fill_diagonal(dr, 0)
     np.fill_diagonal(di, 0)
-    ref, outs = dense_runs(d, dr, di, None, 3, [(0, 128), (128, 300), (37, 201)])
+    ref, outs = dense_runs(d, dr, di, None, 3, [(0, 128), (128, 300), (37, 201)], product)
     check_blocks(ref, outs, n)
 
 

@@ -107,13 +107,14 @@ def test_zero_residual_one_iteration():
 
 
 @pytest.mark.parametrize("case", [(8, 2024), (10, 7), (16, 8), (256, 9000)])
-def test_solve_full_near_diagonal_matches_reference(small, case):
-    """test_solver.cpp:158-209 instances (gen_near_diagonal, normal R)."""
+@pytest.mark.parametrize("product", ["dmma", "ozaki"])
+def test_solve_full_near_diagonal_matches_reference(small, case, product):
+    """test_solver.cpp:158-209 instances (gen_near_diagonal, normal R), either FP64 product."""
     n, seed = case
     key = f"nd_{n}_{seed}"
     p = split(small[key + "_M"])
     cfg = ipt.IterationConfig(record_trace=True)
-    r = ipt.solve_full(p, ipt.build_gaps(p), cfg)
+    r = ipt.solve_full(p, ipt.build_gaps(p), cfg, product=product)
     meta = small[key + "_meta"]
     assert abs(r.iterations - int(meta[0])) <= 1 and r.status == ipt.SolveStatus.Converged
     lam = small[key + "_lam"]

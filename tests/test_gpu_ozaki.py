@@ -265,3 +265,53 @@ def test_split_is_bitwise_on_a_nonsymmetric_delta_and_wide_warm_start(monkeypatc
     monkeypatch.setenv("IPT_OZAKI_SPLIT", "0")
     b = ipt.solve_full(p, g, cfg, warm_start=z, want_sigma_min=False, product="ozaki")
     assert np.array_equal(a.Z, b.Z) and np.array_equal(a.eigenvalues, b.eigenvalues)
+
+
+# ------------------------------------------------------------- complex inputs (3M)
+
+
+@pytest.mark.parametrize("n", [4, 33, 64, 300, 700])
+def test_ozaki_complex_matches_dmma(n):
+    """Complex d and Delta (acceptance.cpp:80-88 style): the 3M product with each real
+    product by Ozaki scheme II agrees with the DMMA 3M product and with the direct check."""
+    rng = np.random.default_rng(n + 7)
+    delta = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) * (0.02 / math.sqrt(n))
+    np.fill_diagonal(delta, 0)
+    d = np.arange(n) + 0.4j * rng.uniform(size=n)
+    p = ipt.Partition(d, delta)
+    g = ipt.build_gaps(p)
+    cfg = ipt.IterationConfig(tolerance=1e-13)
+    a = ipt.solve_full(p, g, cfg, product="dmma")
+    b = ipt.solve_full(p, g, cfg, product="ozaki")
+    assert b.status == ipt.SolveStatus.Converged and a.iterations == b.iterations
+    assert np.max(np.abs(a.eigenvalues - b.eigenvalues) / np.abs(a.eigenvalues)) <= 1e-13
+    assert np.max(np.abs(a.Z - b.Z)) <= 1e-13
+    m = ipt.reconstruct(p)
+    res = np.linalg.norm(m @ b.Z - b.Z * b.eigenvalues[None, :])  # (host rounding of d_i z dominates)
+    assert res <= 1e-12 * np.linalg.norm(m)
+    # the device residual is the reference's |d_i Z_ij + W_ij - Z_ij Lambda_j| form
+    assert b.residual_frobenius <= 10 * max(a.residual_frobenius, 1e-15)
+
+
+def test_ozaki_complex_uses_fewer_than_16_moduli():
+    n = 1024
+    rng = np.random.default_rng(3)
+    delta = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) * (0.02 / math.sqrt(n))
+    np.fill_diagonal(delta, 0)
+    d = np.arange(n) + 0.4j * rng.uniform(size=n)
+    lib = _lib.load()
+    ctx = ipt.default_context()
+    h = C.c_void_p()
+    dr, di = np.ascontiguousarray(delta.real), np.ascontiguousarray(delta.imag)
+    check(lib.ipt_full_upload(ctx.handle, n, _lib.dptr(np.ascontiguousarray(d.real)),
+                              _lib.dptr(np.ascontiguousarray(d.imag)), _lib.dptr(dr), _lib.dptr(di), C.byref(h)))
+    try:
+        check(lib.ipt_full_reset(ctx.handle, h, None, None))
+        check(lib.ipt_full_set_product(h, _lib.PRODUCT_OZAKI))
+        tot, ker = C.c_double(), C.c_double()
+        check(lib.ipt_full_run_maps(ctx.handle, h, 3, C.byref(tot), C.byref(ker)))
+        m = C.c_int32()
+        check(lib.ipt_full_ozaki_moduli(h, C.byref(m)))
+        assert 9 <= m.value <= 15
+    finally:
+        lib.ipt_full_free(h)

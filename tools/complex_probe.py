@@ -1,7 +1,8 @@
 """Complex full-spectrum map rate (3M: three real DMMA GEMMs, the complex map fused
 into the third GEMM's epilogue) against the real map at the same N. The complex rate
 is quoted as 4M-equivalent real flops (8N^3 per map, what the reference's four real
-GEMMs perform) and as executed flops (6N^3).
+GEMMs perform) and as executed flops (6N^3). Each map with the DMMA product and with the
+Ozaki product (tcgen05 INT8) for the real GEMMs.
 
     python tools/complex_probe.py [n]
 """
@@ -27,10 +28,11 @@ di = (0.3 / np.sqrt(n)) * rng.standard_normal((n, n))
 np.fill_diagonal(dr, 0.0)
 np.fill_diagonal(di, 0.0)
 out = {}
-for name, im in (("real", None), ("complex", di)):
+for name, im, prod in (("real", None, 0), ("complex", di, 0), ("real_ozaki", None, 1), ("complex_ozaki", di, 1)):
     h = C.c_void_p()
     check(lib.ipt_full_upload(ctx.handle, n, dptr(d), None, dptr(dr), dptr(im), C.byref(h)))
     check(lib.ipt_full_reset(ctx.handle, h, None, None))
+    check(lib.ipt_full_set_product(h, prod))
     tot, dom = C.c_double(), C.c_double()
     check(lib.ipt_full_run_maps(ctx.handle, h, 2, C.byref(tot), C.byref(dom)))
     check(lib.ipt_full_run_maps(ctx.handle, h, 4, C.byref(tot), C.byref(dom)))
