@@ -541,7 +541,19 @@ def main():
                     "loop_tflops": 2.0 * 8192 ** 3 * r2.iterations / (r2.timings_ms["loop"] * 1e-3) / 1e12,
                     "timings_ms": r2.timings_ms, "lambda0": float(r2.eigenvalues[0]),
                     "residual_frobenius": r2.residual_frobenius, "sigma_min": r2.min_singular_value_estimate}
-                del p2, r2
+                # the same solve with the Ozaki product (tcgen05 INT8)
+                ipt.solve_full(p2, ipt.build_gaps(p2), ipt.IterationConfig(tolerance=1e-12), ctx=ctx,
+                               product="ozaki")  # warm
+                t0 = time.perf_counter()
+                r3 = ipt.solve_full(p2, ipt.build_gaps(p2), ipt.IterationConfig(tolerance=1e-12), ctx=ctx,
+                                    product="ozaki")
+                t3 = time.perf_counter() - t0
+                secondary["full_n8192"]["ozaki"] = {
+                    "time_to_solution_s": t3, "iterations": r3.iterations, "status": ipt.to_string(r3.status),
+                    "e2e_tflops_fp64_equivalent": 2.0 * 8192 ** 3 * r3.iterations / t3 / 1e12,
+                    "timings_ms": r3.timings_ms, "lambda0": float(r3.eigenvalues[0]),
+                    "residual_frobenius": r3.residual_frobenius}
+                del p2, r2, r3
             except Exception as exc:
                 secondary["full_n8192"] = {"error": repr(exc)}
             try:
