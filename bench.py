@@ -199,6 +199,52 @@ def cpu_reference_sample(n=4096, reps=2):
                       f"best of {reps}: {t:.3f} s; metric counts 2N^3 useful flops"}
 
 
+def per_config_e2e(ipt, ctx):
+    """End-to-end time to solution of the configs the reference runs whole on the host
+    (BASELINE configs[0]: full spectrum N=1024; configs[4]: CSR single pair N=2^21): the
+    drop-in call with host buffers on the B200 vs the reference build's own solve on all
+    host cores, same inputs and stop rule (SURVEY 8d: configs 1, 2, 5 run end to end;
+    config 2 needs ~15 min per reference iteration here, so it is left out)."""
+    import oracle
+    from paper_2012_14702_b200 import synth
+
+    if not oracle.have_ref():
+        return {"error": "reference build absent (oracle/_ref)"}
+    R = oracle.ref()
+    out = {"cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))}
+    p1 = synth.config1()
+    cfg1 = ipt.IterationConfig(tolerance=1e-12)
+    ipt.solve_full(p1, ipt.build_gaps(p1), cfg1, ctx=ctx)  # warm
+    t0 = time.perf_counter()
+    g1 = ipt.solve_full(p1, ipt.build_gaps(p1), cfg1, ctx=ctx)
+    tg = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    r1 = R.solve_full(p1.d, p1.delta, tol=1e-12)
+    tr = time.perf_counter() - t0
+    out["config1_full_n1024"] = {
+        "gpu_s": tg, "reference_s": tr, "reference_inner_s": r1["seconds"], "speedup": r1["seconds"] / tg,
+        "iterations": [g1.iterations, r1["iterations"]],
+        "lambda0_rel_diff": abs(float(g1.eigenvalues[0]) - r1["eigenvalues"][0].real) / abs(r1["eigenvalues"][0].real)}
+    del p1, g1, r1
+    p5 = synth.config5()
+    g5gaps = ipt.build_gaps(p5, 0.0)
+    cfg5 = ipt.IterationConfig(tolerance=1e-10)
+    t0 = time.perf_counter()
+    g5 = ipt.solve_single(p5, g5gaps, 0, cfg5, ctx=ctx)
+    tg = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    r5 = R.solve_single(p5.d, p5.delta, 0, tol=1e-10, degeneracy_tol=0.0)
+    tr = time.perf_counter() - t0
+    out["config5_csr_single_n2097152"] = {
+        "gpu_s": tg, "reference_s": tr, "reference_inner_s": r5["seconds"], "speedup": r5["seconds"] / tg,
+        "iterations": [g5.iterations, r5["iterations"]],
+        "eigenvalue_rel_diff": abs(g5.eigenvalue - r5["eigenvalue"].real) / abs(r5["eigenvalue"].real),
+        "note": "gpu_s: the drop-in call with host buffers (H2D of the 1.6 GB CSR arrays included); "
+                "reference_inner_s: the reference solve itself (its timer, inputs already in its CSR "
+                "ComplexMatrix); speedup = reference_inner_s / gpu_s"}
+    return out
+
+
 def run_reference_arm(args):
     rank, world, _ = env_rank()
     if rank != 0:
@@ -571,6 +617,11 @@ def main():
             cpu = cpu_reference_sample()
         except Exception as exc:
             cpu = {"error": repr(exc)}
+        if args.secondary == "all":
+            try:
+                secondary["per_config_e2e_vs_reference"] = per_config_e2e(ipt, ctx)
+            except Exception as exc:
+                secondary["per_config_e2e_vs_reference"] = {"error": repr(exc)}
 
     if rank == 0:
         line = {

@@ -110,6 +110,7 @@ void scale_copy(cudaStream_t s, const double* src, double* dst, size_t count, do
 // buffer (multithreaded host memcpy overlapped with the DMA); synchronous on return.
 // Host rows have pitch spitch (doubles), device rows pitch dpitch.
 // `s` (default: the context stream) carries the DMA.
+void h2d_bytes(Ctx& c, void* dst, const void* src, size_t bytes);
 void h2d_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t rows,
               int64_t cols, cudaStream_t s = nullptr);
 void d2h_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t rows,

@@ -954,9 +954,9 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
     IPT_CUDA(cudaMalloc(&dc, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
     P->cols.reset(dc);
     P->vals.alloc(std::max<int64_t>(nnz, 1), false);
-    if (nnz) {
-      IPT_CUDA(cudaMemcpyAsync(dc, cols + b, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
-      IPT_CUDA(cudaMemcpyAsync(P->vals.get(), val_re + b, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+    if (nnz) {  // pinned staging: ~4x the pageable copy rate for the 1.6 GB of config 5
+      h2d_bytes(c, dc, cols + b, sizeof(int32_t) * nnz);
+      h2d_bytes(c, P->vals.get(), val_re + b, sizeof(double) * nnz);
     }
     if (P->cplx && val_im) {
       P->valsi.alloc(std::max<int64_t>(nnz, 1), false);

@@ -214,6 +214,25 @@ void h2d_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t sp
                  copy_threads());
 }
 
+// A flat pageable host buffer to the device through the same pinned, double-buffered,
+// multi-threaded staging as h2d_rows (8 MB rows; the sub-8-byte tail by a plain copy).
+void h2d_bytes(Ctx& c, void* dst, const void* src, size_t bytes) {
+  constexpr int64_t kRow = int64_t(1) << 20;  // doubles per staged row
+  const int64_t nd = static_cast<int64_t>(bytes / sizeof(double));
+  const int64_t rows = nd / kRow;
+  auto* d8 = static_cast<double*>(dst);
+  const auto* s8 = static_cast<const double*>(src);
+  if (rows > 0) h2d_rows(c, d8, kRow, s8, kRow, rows, kRow);
+  const int64_t done = rows * kRow;
+  if (nd > done) h2d_rows(c, d8 + done, nd - done, s8 + done, nd - done, 1, nd - done);
+  const size_t tail = bytes - sizeof(double) * size_t(nd);
+  if (tail) {
+    IPT_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(dst) + bytes - tail, reinterpret_cast<const char*>(src) + bytes - tail,
+                             tail, cudaMemcpyHostToDevice, c.stream));
+    IPT_CUDA(cudaStreamSynchronize(c.stream));
+  }
+}
+
 void d2h_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t rows,
               int64_t cols, cudaStream_t stream) {
   if (rows <= 0 || cols <= 0) return;
