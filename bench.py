@@ -549,7 +549,9 @@ def main():
         e2e = {"value": flops_step * r.iterations / e2e_s / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": int(8 * n * n + 8 * n),
                "d2h_bytes_per_step": int(8 * n * n + 8 * n) if rank == 0 else 0,
-               "step": "one drop-in solve_full call (C ABI ipt_full_solve, host buffers, pageable memory)",
+               "step": "one drop-in solve_full call (C ABI ipt_full_solve, host buffers, pageable memory); "
+                       "h2d bytes are the whole job's (with g GPUs each rank uploads 1/g of Delta's rows "
+                       "and an NVLink all-gather replicates it)",
                "seconds": e2e_s,
                "flop_convention": "2N^3 per IPT iteration (the metric's definition) x iterations / wall time; "
                                   "iteration 1 from Z = I is evaluated exactly without a product (W = Delta I = "
