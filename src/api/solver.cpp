@@ -299,7 +299,12 @@ SpectrumResult solve_full(const Partition& p, const InverseGaps& g, const Iterat
 
 SpectrumResult solve_full(const Partition& p, const InverseGaps& g, const IterationConfig& config,
                           const ComplexMatrix* warm_start) {
-    return b200::solve_full(p, g, config, b200::FullOptions{}, warm_start);
+    // IPT_PRODUCT=ozaki lets unmodified reference callers (refine, cli, bench) take the
+    // FP64-accurate tcgen05 product; the default is the DMMA product
+    b200::FullOptions options;
+    const char* e = std::getenv("IPT_PRODUCT");
+    if (e && std::string(e) == "ozaki") options.product = b200::Product::Ozaki;
+    return b200::solve_full(p, g, config, options, warm_start);
 }
 
 double smallest_singular_value_estimate(const ComplexMatrix& z, int max_iters, double tol) {

@@ -8,6 +8,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include <ipt/complex_matrix.hpp>
 #include <ipt/partition.hpp>
@@ -85,4 +86,19 @@ TEST_CASE("b200::solve_full max-abs stop rule") {
     const ipt::SpectrumResult r = ipt::b200::solve_full(p, g, cfg, o);
     CHECK(r.status == ipt::SolveStatus::Converged);
     CHECK(r.final_step < 1e-12);  // (relative step; the rule itself stopped on max|F - Z| < tol)
+}
+
+TEST_CASE("IPT_PRODUCT=ozaki routes the drop-in ipt::solve_full to the tcgen05 product") {
+    const ipt::Partition p = near_diagonal(400, 0.02, 23);
+    const ipt::InverseGaps g = ipt::build_gaps(p);
+    ipt::b200::FullOptions oz;
+    oz.product = ipt::b200::Product::Ozaki;
+    const ipt::SpectrumResult want = ipt::b200::solve_full(p, g, ipt::IterationConfig{}, oz);
+    setenv("IPT_PRODUCT", "ozaki", 1);
+    const ipt::SpectrumResult got = ipt::solve_full(p, g);
+    unsetenv("IPT_PRODUCT");
+    const ipt::SpectrumResult dmma = ipt::solve_full(p, g);
+    CHECK(max_abs_diff(got.Z, want.Z) == 0.0);  // the same (deterministic) Ozaki path
+    CHECK(got.iterations == want.iterations);
+    CHECK(max_abs_diff(dmma.Z, want.Z) <= 1e-13);
 }
