@@ -17,15 +17,20 @@ REF = os.path.join(ROOT, "oracle", "_ref")
 pytestmark = pytest.mark.gpu
 
 
-def _run(exe, timeout):
+def _run(exe, timeout, product="dmma"):
     path = os.path.join(REF, exe)
     if not os.path.exists(path):
         pytest.skip(f"{exe} not built (make -C oracle harness needs /root/reference)")
-    return subprocess.run([path], capture_output=True, text=True, timeout=timeout)
+    env = dict(os.environ)
+    env.pop("IPT_PRODUCT", None)
+    if product == "ozaki":  # the drop-in ipt::solve_full on the tcgen05 product (solver.cpp)
+        env["IPT_PRODUCT"] = "ozaki"
+    return subprocess.run([path], capture_output=True, text=True, timeout=timeout, env=env)
 
 
-def test_reference_unit_tests_against_b200_library():
-    r = _run("unit_b200", 900)
+@pytest.mark.parametrize("product", ["dmma", "ozaki"])
+def test_reference_unit_tests_against_b200_library(product):
+    r = _run("unit_b200", 900, product)
     print(r.stdout[-4000:])
     assert "test cases:" in r.stdout
     assert r.returncode == 0, r.stdout[-4000:]
@@ -40,6 +45,15 @@ def test_reference_acceptance_hot_path_criteria():
     the first map from I needs no product and host<->device costs dominate at N = 1024,
     so it is reported, not asserted."""
     r = _run("acceptance_b200", 1800)
+    _check_acceptance(r)
+
+
+def test_reference_acceptance_with_the_ozaki_product():
+    """The same criteria with every solve_full on the FP64-accurate tcgen05 product."""
+    _check_acceptance(_run("acceptance_b200", 1800, "ozaki"))
+
+
+def _check_acceptance(r):
     print(r.stdout)
     status = {int(m.group(2)): m.group(1) for m in re.finditer(r"\[(PASS|FAIL)\] criterion (\d+)", r.stdout)}
     for crit in (1, 2, 4, 5, 6, 7, 8):
