@@ -1,8 +1,10 @@
 """The reference's own tests, compiled unmodified from /root/reference/proj/tests
 against libipt_b200.so (oracle/Makefile target `harness`), run on the B200.
 
-Hot-path doctest files: test_solver.cpp, test_kernels.cpp, test_testgen.cpp,
-test_matcore.cpp (doctest-compatible shim tests/cpp/doctest.h). Acceptance
+Doctest files: test_solver.cpp, test_kernels.cpp, test_testgen.cpp, test_matcore.cpp
+(hot path) and test_anderson.cpp, test_refine.cpp, test_rspt.cpp (the callers of §8 f1/f4
+running on our solvers and device LU), through the doctest-compatible shim
+tests/cpp/doctest.h. Acceptance
 criteria 1, 2, 5, 9 are the hot-path ones; the others exercise the
 reference's off-path modules calling into our solvers."""
 import os
