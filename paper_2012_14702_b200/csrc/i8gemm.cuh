@@ -26,6 +26,7 @@ constexpr int kI8BN = 256;
 constexpr int kI8BK = 128;  // bytes = int8 elements per stage along K
 constexpr int kI8Stages = 4;
 constexpr int kI8Threads = 192;  // 6 warps
+constexpr int kI8Threads2 = 256;  // cta_group::2 kernels: 8 warps, all of them drain TMEM in the epilogue
 constexpr int kI8StageBytes = (kI8BM + kI8BN) * kI8BK;
 constexpr size_t kI8SmemBytes = size_t(kI8Stages) * kI8StageBytes + 1024 + 256;
 
@@ -336,7 +337,7 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* ma
 }
 
 template <class Epi, int NB>
-__global__ void __launch_bounds__(kI8Threads, 1)
+__global__ void __launch_bounds__(kI8Threads2, 1)
     i8gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
                       int pairs_m, int tiles_n, int group, Epi epi) {
   if (epi.skip()) return;  // uniform over the grid (e.g. an unused Ozaki modulus)
@@ -410,15 +411,19 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       }
       umma_commit_2sm(acc_full, kBoth);
     }
-    __syncwarp();
-  } else {
-    mbar_wait(acc_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int quarter = warp & 3;
+  }
+  __syncwarp();
+  // Epilogue on all 8 warps (the producer and MMA warps included once their loops end):
+  // warp w drains TMEM lane quarter w % 4 (its rows), column half w / 4.
+  mbar_wait(acc_full, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  {
+    const int quarter = warp & 3, half = warp >> 2;
     const int row = m0 + quarter * 32 + lane;
     const uint32_t trow = tmem + (uint32_t(quarter * 32) << 16);
+    constexpr int kHalf = int(kCols) / 2;
 #pragma unroll 1
-    for (int c = 0; c < int(kCols); c += 32) {
+    for (int c = half * kHalf; c < (half + 1) * kHalf; c += 32) {
       uint32_t v[32];
       tmem_ld32(trow + uint32_t(c), v);
       epi(row, n0 + c, v);
@@ -466,7 +471,7 @@ void launch_i8gemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, const int8_t
     const CUtensorMap mb2 = make_map_i8(B, K, N, ldb, 128);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(wide ? grid / 2 : grid);
-    cfg.blockDim = dim3(kI8Threads);
+    cfg.blockDim = dim3(kI8Threads2);
     cfg.dynamicSmemBytes = wide ? I8S2<2>::kSmem : I8S2<1>::kSmem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
