@@ -145,7 +145,22 @@ void solve_full_impl(Ctx& c, const ipt_params* params, Open&& open, const double
     ph.mark("reset");
     float ms_up = 0.f;
     IPT_CUDA(cudaEventElapsedTime(&ms_up, c.ev[2], c.ev[3]));
-    full_iterate(*P, prm, stats);
+    // First-touch the (large, usually fresh) host result arrays on a host thread while the
+    // device iterates, instead of inside the download.
+    std::future<void> touch;
+    const size_t zbytes = sizeof(double) * size_t(full_n(*P)) * size_t(full_n(*P));
+    if ((z_re || z_im) && zbytes >= (size_t(256) << 20))
+      touch = std::async(std::launch::async, [z_re, z_im, zbytes] {
+        if (z_re) prefault_host_async_part(z_re, zbytes);
+        if (z_im) prefault_host_async_part(z_im, zbytes);
+      });
+    try {
+      full_iterate(*P, prm, stats);
+    } catch (...) {
+      if (touch.valid()) touch.wait();
+      throw;
+    }
+    if (touch.valid()) touch.get();
     ph.mark("iterate");
     // Single GPU: Z goes to the host on a second stream / host thread while the closing
     // product and sigma_min run (they only read Z).

@@ -1303,6 +1303,7 @@ void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, d
 bool full_is_complex(const FullProblem& P) { return P.cplx; }
 
 bool full_can_download_early(const FullProblem& P) { return P.ctx->nranks == 1 && !P.sparse && P.ncols == P.n; }
+int64_t full_n(const FullProblem& P) { return P.n; }
 
 // Main thread, before full_finalize: transpose the final Z into row-major staging
 // buffers on ctx.stream (a few ms; a kernel on a second stream would starve behind

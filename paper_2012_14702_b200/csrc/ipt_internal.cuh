@@ -110,6 +110,8 @@ void scale_copy(cudaStream_t s, const double* src, double* dst, size_t count, do
 // buffer (multithreaded host memcpy overlapped with the DMA); synchronous on return.
 // Host rows have pitch spitch (doubles), device rows pitch dpitch.
 // `s` (default: the context stream) carries the DMA.
+void prefault_host_async_part(double* dst, size_t bytes);  // first touch + note for d2h_rows
+bool take_prefaulted(const void* p, size_t bytes);
 void h2d_bytes(Ctx& c, void* dst, const void* src, size_t bytes);
 void h2d_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t rows,
               int64_t cols, cudaStream_t s = nullptr);
@@ -136,6 +138,7 @@ void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, d
 // Single-rank dense problems after full_iterate: Z to the host on ctx.stream2, safe to run
 // on another host thread while full_finalize uses ctx.stream (both only read Z).
 bool full_can_download_early(const FullProblem& P);
+int64_t full_n(const FullProblem& P);
 void full_prepare_download(FullProblem& P, bool want_re, bool want_im);
 void full_download_z(FullProblem& P, double* z_re, double* z_im);
 void full_release_download(FullProblem& P);

@@ -139,6 +139,9 @@ void host_copy_rows(double* dst, int64_t dpitch, const double* src, int64_t spit
 // parallel: transparent huge pages requested for the range, then every page touched
 // by all copy threads at once, so the staged copies below do not take ~2 M
 // serialised 4 KB page faults.
+std::mutex g_prefault_mu;
+std::vector<std::pair<const void*, size_t>> g_prefaulted;  // ranges already first-touched
+
 void prefault_host_destination(double* dst, size_t bytes) {
   if (bytes < (size_t(256) << 20)) return;
   const uintptr_t huge = uintptr_t(2) << 20;
@@ -165,6 +168,24 @@ void prefault_host_destination(double* dst, size_t bytes) {
 }
 
 }  // namespace
+
+// A result destination can be first-touched on a host thread while the device iterates;
+// d2h_rows then skips its own prefault for exactly that range.
+void prefault_host_async_part(double* dst, size_t bytes) {
+  prefault_host_destination(dst, bytes);
+  std::lock_guard<std::mutex> lk(g_prefault_mu);
+  g_prefaulted.emplace_back(dst, bytes);
+}
+
+bool take_prefaulted(const void* p, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_prefault_mu);
+  for (auto it = g_prefaulted.begin(); it != g_prefaulted.end(); ++it)
+    if (it->first == p && it->second == bytes) {
+      g_prefaulted.erase(it);
+      return true;
+    }
+  return false;
+}
 
 void release_staging(Ctx& c) {
   for (int b = 0; b < 2; ++b) {
@@ -259,7 +280,8 @@ void d2h_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t sp
   auto now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   const double t_start = now();
   issue(0);  // the first DMA runs while the destination is prefaulted
-  if (dpitch == cols) prefault_host_destination(dst, sizeof(double) * size_t(rows) * size_t(cols));
+  if (dpitch == cols && !take_prefaulted(dst, sizeof(double) * size_t(rows) * size_t(cols)))
+    prefault_host_destination(dst, sizeof(double) * size_t(rows) * size_t(cols));
   const double t_fault = now() - t_start;
   for (int64_t k = 0; k < nchunks; ++k) {
     if (k + 1 < nchunks) issue(k + 1);
