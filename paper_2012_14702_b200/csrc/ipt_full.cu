@@ -61,7 +61,7 @@ struct FullProblem {
   bool delta_finite = false;    // real dense Delta has no Inf/NaN (identity-start shortcut allowed)
   bool start_identity = false;  // Z[0] is the identity (no warm start)
   const double* z_after_loop = nullptr;  // current iterate when full_iterate returned
-  DevBuf rm[2];                          // row-major copies of Z for an overlapped download
+  double* rm_ptr[2] = {nullptr, nullptr};  // row-major copies of Z (in the free ping-pong buffer) for an overlapped download
   // Ozaki scheme II product (IPT_PRODUCT_OZAKI): Delta's residues (built once), the current
   // Z's residues, the product residues
   int product = IPT_PRODUCT_DMMA;
@@ -1314,10 +1314,15 @@ void full_prepare_download(FullProblem& P, bool want_re, bool want_im) {
   const int64_t n = P.n;
   const double* zsrc = P.z_after_loop;
   if (zsrc == nullptr) throw InvalidArgument("download: iterate must run first");
+  // The row-major copies go into the other ping-pong buffer (the previous iterate, no
+  // longer read; cols_pad x ldz >= n^2 per part, both parts for complex) -- no extra
+  // 8.6 GB allocation at N = 32768.
+  double* other = zsrc == P.Z[0].get() ? P.Z[1].get() : P.Z[0].get();
   for (int part = 0; part < 2; ++part) {
+    P.rm_ptr[part] = nullptr;
     if (!(part == 0 ? want_re : want_im) || (part == 1 && !P.cplx)) continue;
-    P.rm[part].alloc(size_t(n) * n, false);
-    transpose_to_rowmajor(c.stream, zsrc + (part ? P.ld : 0), P.ldz, n, n, P.rm[part].get(), n);
+    P.rm_ptr[part] = other + size_t(part) * size_t(n) * size_t(n);
+    transpose_to_rowmajor(c.stream, zsrc + (part ? P.ld : 0), P.ldz, n, n, P.rm_ptr[part], n);
   }
   c.sync();
 }
@@ -1332,15 +1337,14 @@ void full_download_z(FullProblem& P, double* z_re, double* z_im) {
       std::memset(dst, 0, sizeof(double) * n * n);
       continue;
     }
-    if (P.rm[part].get() == nullptr) throw InvalidArgument("download: prepare must run first");
-    d2h_rows(c, dst, n, P.rm[part].get(), n, n, n, c.stream2);
+    if (P.rm_ptr[part] == nullptr) throw InvalidArgument("download: prepare must run first");
+    d2h_rows(c, dst, n, P.rm_ptr[part], n, n, n, c.stream2);
   }
   IPT_CUDA(cudaStreamSynchronize(c.stream2));
 }
 
 void full_release_download(FullProblem& P) {
-  P.rm[0].release();
-  P.rm[1].release();
+  P.rm_ptr[0] = P.rm_ptr[1] = nullptr;
 }
 
 // Bench / profiling: exactly `count` further map applications (convergence ignored),
