@@ -4,8 +4,9 @@
 //
 //  1. Scale: row i of A by 2^eA[i], column j of B by 2^eB[j], with the row / column
 //     maximum landing in [2^52, 2^53); round to integers A', B' (|.| < 2^53, exact for
-//     every entry within a binade of its row maximum, absolute error <= 2^-54 of the
-//     row maximum otherwise -- within FP64 GEMM rounding, whose bound is K u |A||B|).
+//     every entry within a binade of its row maximum, absolute error <= 2^-53 of the
+//     row maximum otherwise: a product error <= 2^-53 (max|a_i.| |b_.j|_1 + max|b_.j|
+//     |a_i.|_1), the order of the FP64 GEMM's normwise bound).
 //  2. Residues: A' mod m_l and B' mod m_l in the symmetric range (int8), l = 1..16.
 //     A = Delta is fixed for a solve: its residues are made once.
 //  3. Products: P_l = A'_l . B'_l^T per modulus on tcgen05 (kind::i8, exact int32,
