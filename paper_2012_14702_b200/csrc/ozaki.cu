@@ -18,7 +18,7 @@
 //  5. The IPT map (or the closing residual) is applied in the same pass (the K1
 //     epilogue formulas), with the per-CTA partial sums of a fixed grid.
 // Everything is integer-exact up to the single rounding of P and of the scaling, so the
-// result is deterministic and as accurate as an FP64 GEMM; non-finite inputs are routed
+// result is deterministic with FP64-GEMM-order accuracy (step 1); non-finite inputs are routed
 // to the DMMA path by the caller.
 #include <algorithm>
 #include <cmath>
