@@ -172,21 +172,20 @@ def cpu_reference_sample(n=4096, reps=2):
     """The reference's own apply_map_full (solver.cpp:156-178; kernels.cpp dgemm) on the
     host cores, one map application at a bounded N of the same construction."""
     import oracle
-    from paper_2012_14702_b200 import synth
 
     threads = os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(threads))
-    p = synth.dense_uniform(n, 0.32 / math.sqrt(n), 42)
+    d, delta = oracle.port().dense_uniform(n, 0.32 / math.sqrt(n), 42)  # no product library here
     if oracle.have_ref():
         R, kind = oracle.ref(), "reference"
 
         def step(z):
-            return R.apply_map_full(p.d, p.delta, z)
+            return R.apply_map_full(d, delta, z)
     else:  # reference build absent: the plain-C restatement of the same map
         P, kind = oracle.port(), "port"
 
         def step(z):
-            return P.full_map_block(p.d, p.delta, 0, z)[0]
+            return P.full_map_block(d, delta, 0, z)[0]
     z = step(np.eye(n))  # warm
     ts = []
     for _ in range(reps):
@@ -255,21 +254,21 @@ def run_reference_arm(args):
     n = args.ref_n
     threads = os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(threads))
-    from paper_2012_14702_b200 import synth
-
-    p = synth.dense_uniform(n, 0.32 / math.sqrt(n), 42)
+    # Inputs from the reference's generator restated in the oracle (rng.hpp, SURVEY 8(d)
+    # draw order): this process loads only oracle/ libraries, never libipt_b200.so.
+    d, delta = oracle.port().dense_uniform(n, 0.32 / math.sqrt(n), 42)
     if oracle.have_ref():  # the reference's own apply_map_full (oracle/_ref, built from its sources)
         R = oracle.ref()
         kind = "reference"
 
         def step(z):
-            return R.apply_map_full(p.d, p.delta, z)
+            return R.apply_map_full(d, delta, z)
     else:  # the plain-C restatement of the same map (oracle/ipt_oracle.c)
         P = oracle.port()
         kind = "port"
 
         def step(z):
-            return P.full_map_block(p.d, p.delta, 0, z)[0]
+            return P.full_map_block(d, delta, 0, z)[0]
     z = np.eye(n, dtype=np.complex128)
     for _ in range(args.warmup):
         z = step(z)
@@ -278,14 +277,17 @@ def run_reference_arm(args):
         z = step(z)
     t = time.perf_counter() - t0
     value = 2.0 * n ** 3 * args.steps / t / 1e12
+    ref_config = workload_config(world, N_FULL, {"reference_sample_n": n, "same_config": False})
+    ref_config["workload"] += (f" | reference arm: each step is ONE reference apply_map_full at the bounded "
+                               f"sample N={n} of the same construction (reference_sample_n), rate per 2N^3 flops")
     sample = (f"reference apply_map_full (proj/src/solver.cpp:156-178, OpenMP kernels.cpp) at N={n} of the "
               f"same construction per step (the N={N_FULL} workload needs ~120 GB and hours per iteration "
               f"on the CPU); metric counts 2N^3 flops per step")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": max(world, args.gpus),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_config(world, N_FULL, {"reference_sample_n": n}),
+        "data": "synthetic", "config": ref_config,
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
                          "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -297,7 +299,7 @@ def run_reference_arm(args):
 # --------------------------------------------------------------------------- secondary: single pair
 
 
-def bench_single(ipt, lib, ctx, which, steps, warmup, hbm):
+def bench_single(ipt, lib, ctx, which, steps, warmup, hbm, reduce_max=lambda x: x, world=1):
     from paper_2012_14702_b200 import synth
     from paper_2012_14702_b200._lib import check, dptr, i32ptr, i64ptr
 
@@ -319,7 +321,7 @@ def bench_single(ipt, lib, ctx, which, steps, warmup, hbm):
         h = C.c_void_p()
         check(lib.ipt_single_upload_csr(ctx.handle, n, dptr(p.d), None, i64ptr(p.delta.row_offsets),
                                         i32ptr(p.delta.col_indices), dptr(p.delta.values), None, C.byref(h)))
-        kernel = "spmv_map_kernel<1>"
+        kernel = "spmv_group_kernel<1, 4, 4, 4, 0>"
         tol = 1e-10
         gaps_tol = 0.0
     setup_s = time.perf_counter() - t0
@@ -339,13 +341,17 @@ def bench_single(ipt, lib, ctx, which, steps, warmup, hbm):
     check(lib.ipt_single_run_steps(ctx.handle, h, warmup, C.byref(tot), C.byref(dom)))
     check(lib.ipt_single_run_steps(ctx.handle, h, steps, C.byref(tot), C.byref(dom)))
     lib.ipt_single_free(h)
-    step_ms = tot.value / steps
-    dom_ms = dom.value / steps
+    step_ms = reduce_max(tot.value / steps)
+    dom_ms_local = dom.value / steps
+    dom_ms = reduce_max(dom_ms_local)
+    solve["loop_ms"] = reduce_max(solve["loop_ms"])
     kbytes = nbytes - 8.0 * n  # the map kernel itself: matrix + z + d + fz
     del p
     out = {
         "workload": ("configs[3] dense GEMV single pair N=65536" if which == "gemv"
-                     else "configs[4] CSR SpMV single pair N=2^21 (~64 nnz/row)"),
+                     else f"configs[4] CSR SpMV single pair N=2^21 (~64 nnz/row), rows sharded over {world} "
+                          f"GPU(s) (strong scaling), fused peer-store all-gather of the iterate"),
+        "n_gpus": world,
         "metric": "single-pair IPT iteration GB/s (algorithmic bytes)",
         "value": nbytes / (step_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": step_ms,
         "time_to_solution": solve, "setup_s": setup_s,
@@ -354,6 +360,10 @@ def bench_single(ipt, lib, ctx, which, steps, warmup, hbm):
                      "frac": kbytes / (dom_ms * 1e-3) / 1e9 / hbm[0], "kernel_ms": dom_ms,
                      "bytes_per_launch": kbytes, "traffic": traffic_for(kernel, n)},
     }
+    if world > 1:  # per-rank kernel bytes: this rank's rows (a 1/world share of the matrix stream)
+        out["roofline"]["achieved"] = kbytes / world / (dom_ms_local * 1e-3) / 1e9
+        out["roofline"]["frac"] = out["roofline"]["achieved"] / hbm[0]
+        out["roofline"]["bytes_per_launch"] = kbytes / world
     if which == "spmv":
         # The random z gather (32-byte L2 sector per 8-byte use), not HBM, bounds this
         # kernel: measured ceiling = the same stream + gather without row structure.
@@ -452,6 +462,39 @@ def bench_ozaki(ipt, lib, ctx, n, dense_step_ms, dmma_solve):
     return out
 
 
+# --------------------------------------------------------------------------- launch
+
+
+def relaunch_if_needed(args):
+    """`--gpus N` (N > 1) outside torchrun: re-launch this command as N ranks under
+    torch.distributed.run (one process per GPU, 127.0.0.1 rendezvous); fail loudly when
+    fewer than N GPUs are visible. Returns an exit code, or None to run in-process."""
+    world = int(os.environ.get("WORLD_SIZE", "0") or 0)
+    if world:
+        if args.gpus > 1 and world != args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+            return 2
+        return None
+    if args.gpus <= 1 or args.impl == "reference":
+        return None  # the reference arm is CPU work on rank 0 only
+    import socket
+    import subprocess
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) are visible",
+              file=sys.stderr)
+        return 3
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 # --------------------------------------------------------------------------- main arm
 
 
@@ -469,6 +512,9 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
+    rc = relaunch_if_needed(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference_arm(args)
 
@@ -569,13 +615,18 @@ def main():
 
     # ---------------- secondary: single-pair paths (rank 0, N = 1 only)
     secondary = {}
-    if world == 1 and args.secondary != "none":
+    if args.secondary != "none":
         hbm = hbm_peak()
-        for which in (["gemv", "spmv"] if args.secondary == "all" else [args.secondary]):
+        # config 4 (dense GEMV) is "replicas only"; config 5 (CSR) is row-sharded
+        kinds = ["gemv", "spmv"] if args.secondary == "all" else [args.secondary]
+        for which in [k for k in kinds if world == 1 or k == "spmv"]:
             try:
-                secondary[which] = bench_single(ipt, lib, ctx, which, max(args.steps, 10), 3, hbm)
+                barrier()
+                secondary[which] = bench_single(ipt, lib, ctx, which, max(args.steps, 10), 3, hbm,
+                                                max_over_ranks, world)
             except Exception as exc:  # report, never hide
                 secondary[which] = {"error": repr(exc)}
+    if world == 1 and args.secondary != "none":
         if args.secondary == "all":
             try:  # the low end of the metric's N range: configs[1], N = 8192, through the C ABI
                 p2 = synth.config2()
@@ -587,7 +638,9 @@ def main():
                     "workload": "configs[1] full spectrum N=8192, eps=0.32/sqrt(N), tol 1e-12 (C ABI, host buffers)",
                     "time_to_solution_s": t2, "iterations": r2.iterations, "status": ipt.to_string(r2.status),
                     "e2e_tflops": 2.0 * 8192 ** 3 * r2.iterations / t2 / 1e12,
-                    "loop_tflops": 2.0 * 8192 ** 3 * r2.iterations / (r2.timings_ms["loop"] * 1e-3) / 1e12,
+                    # executed map GEMMs: the first map from Z = I needs no product (W = Delta I)
+                    "loop_gemms_executed": r2.iterations - 1,
+                    "loop_tflops": 2.0 * 8192 ** 3 * (r2.iterations - 1) / (r2.timings_ms["loop"] * 1e-3) / 1e12,
                     "timings_ms": r2.timings_ms, "lambda0": float(r2.eigenvalues[0]),
                     "residual_frobenius": r2.residual_frobenius, "sigma_min": r2.min_singular_value_estimate}
                 # the same solve with the Ozaki product (tcgen05 INT8)

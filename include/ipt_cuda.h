@@ -29,7 +29,7 @@ extern "C" {
 #define IPT_OK 0
 #define IPT_ERR_INVALID (-1)
 #define IPT_ERR_CUDA (-2)
-#define IPT_ERR_NCCL (-4)
+#define IPT_ERR_NCCL (-4) /* communicator error: NCCL, or an aborted / timed-out local group */
 #define IPT_ERR_INTERNAL (-5)
 
 #define IPT_STATUS_CONVERGED 0
@@ -94,6 +94,21 @@ int ipt_ctx_device(const ipt_ctx* ctx);
 int ipt_nccl_get_unique_id(void* out128);
 int ipt_ctx_init_comm(ipt_ctx* ctx, const void* unique_id128, int rank, int nranks);
 int ipt_ctx_rank(const ipt_ctx* ctx, int* rank, int* nranks);
+/* In-process communicator: nranks contexts of ONE process (one host thread per rank,
+ * on one device or several) form a group. Collectives are host rendezvous plus
+ * stream-ordered event waits and a fixed-order reduction kernel reading every rank's
+ * buffer; the fused all-gather stores into the other ranks' buffers directly. No kernel
+ * waits on another, so all ranks may share one GPU: the library's multi-rank code runs
+ * unchanged on a single device. Each rank's thread must issue the same sequence of
+ * sharded calls (as with NCCL). An error on one rank aborts the group (the others'
+ * calls fail with IPT_ERR_NCCL instead of hanging; IPT_LOCAL_COMM_TIMEOUT_S bounds a
+ * rendezvous, default 600 s). */
+typedef struct ipt_local_group ipt_local_group;
+int ipt_local_group_create(int nranks, ipt_local_group** out);
+void ipt_local_group_destroy(ipt_local_group* group); /* after every member context */
+int ipt_ctx_init_local_comm(ipt_ctx* ctx, ipt_local_group* group, int rank);
+/* "none", "nccl" or "local" */
+const char* ipt_ctx_comm_kind(const ipt_ctx* ctx);
 int ipt_ctx_synchronize(ipt_ctx* ctx);
 
 /* ---- full spectrum: solve_full (solver.cpp:180-273) ----

@@ -288,6 +288,16 @@ class PortArm(_Arm):
             self.lib.orc_matvec(C.c_int64(n), C.c_int(0), _p(_c(a)), None, None, None, _p(_c(x)), _p(y))
         return y
 
+    def dense_uniform(self, n, eps, seed=42):
+        """Configs 1-3 inputs (d, Delta) from the reference's generator restated in C
+        (rng.hpp:13-82, SURVEY 8(d) draw order): no product library involved."""
+        d = np.empty(n)
+        delta = np.empty((n, n))
+        rc = self.lib.orc_dense_uniform(C.c_int64(n), C.c_double(eps), C.c_uint64(seed), _p(d), _p(delta))
+        if rc != 0:
+            raise ValueError("orc_dense_uniform: bad size")
+        return d, delta
+
     def full_map_block(self, d, delta, c0, z_block):
         """One map application on the column block [c0, c0+nc) (z_block: n x nc)."""
         n = len(d)

@@ -433,3 +433,46 @@ int orc_solve_single(int64_t n, const double* d_, int is_csr, const double* dens
   free(w); free(fz); free(g);
   return 0;
 }
+
+/* ---- inputs of configs 1-3 without the product library (bench.py reference arm) ----
+ * The reference's generator (proj/include/ipt/rng.hpp:13-82): xoshiro256++ seeded by
+ * splitmix64, substream seed = splitmix64(seed ^ 0x5851f42d4c957f2d * (stream + 1)),
+ * uniform = (next >> 11) * 2^-53. Draw order of SURVEY 8(d): one stream (42, 0), upper
+ * triangle row-major, Delta_ij = Delta_ji = eps (2u - 1), d_i = i + 1. */
+static uint64_t orc_splitmix(uint64_t* x) {
+  uint64_t z = (*x += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+static uint64_t orc_rotl(uint64_t v, int k) { return (v << k) | (v >> (64 - k)); }
+static uint64_t orc_next(uint64_t s[4]) {
+  const uint64_t r = orc_rotl(s[0] + s[3], 23) + s[0];
+  const uint64_t t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = orc_rotl(s[3], 45);
+  return r;
+}
+
+int orc_dense_uniform(int64_t n, double eps, uint64_t seed, double* d, double* delta) {
+  if (n <= 0) return -1;
+  uint64_t x = seed ^ (0x5851f42d4c957f2dull * 1ull);
+  uint64_t s0 = orc_splitmix(&x), st[4];
+  for (int w = 0; w < 4; ++w) st[w] = orc_splitmix(&s0);
+  for (int64_t i = 0; i < n; ++i) {
+    d[i] = (double)(i + 1);
+    delta[i * n + i] = 0.0;
+    for (int64_t j = i + 1; j < n; ++j) {
+      const double u = (double)(orc_next(st) >> 11) * 0x1.0p-53;
+      delta[i * n + j] = eps * (2.0 * u - 1.0);
+    }
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < i; ++j) delta[i * n + j] = delta[j * n + i];
+  return 0;
+}

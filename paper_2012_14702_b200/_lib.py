@@ -81,6 +81,10 @@ SIGNATURES = {
     "ipt_ctx_init_comm": (C.c_int, [_vp, _vp, C.c_int, C.c_int]),
     "ipt_ctx_rank": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "ipt_ctx_synchronize": (C.c_int, [_vp]),
+    "ipt_local_group_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+    "ipt_local_group_destroy": (None, [_vp]),
+    "ipt_ctx_init_local_comm": (C.c_int, [_vp, _vp, C.c_int]),
+    "ipt_ctx_comm_kind": (C.c_char_p, [_vp]),
     "ipt_full_solve": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, C.POINTER(Params),
                                  _dp, _dp, _dp, _dp, C.POINTER(Stats)]),
     "ipt_full_upload": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, _dp, C.POINTER(_vp)]),

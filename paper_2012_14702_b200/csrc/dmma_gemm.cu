@@ -44,8 +44,8 @@ CUtensorMap make_map(const double* base, int64_t inner, int64_t outer, int64_t l
 
 template <int MODE>
 void launch_mode(const GemmParams& p, cudaStream_t s) {
-  static std::once_flag once;
-  std::call_once(once, [] {
+  static PerDeviceOnce attr;
+  attr.run([] {
     IPT_CUDA(cudaFuncSetAttribute(dmma_tma_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kGemmSmemBytes)));
   });

@@ -445,8 +445,8 @@ void launch_i8gemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, const int8_t
                    int64_t ldb, const Epi& epi) {
   if (M % kI8BM || N % kI8BN || K % kI8BK || M <= 0 || N <= 0 || K <= 0)
     throw InvalidArgument("i8 gemm: M % 128, N % 256 and K % 128 must be 0");
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  attr.run([] {
     IPT_CUDA(cudaFuncSetAttribute(i8gemm_kernel<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kI8SmemBytes)));
     IPT_CUDA(cudaFuncSetAttribute(i8gemm_mc_kernel<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -455,8 +455,7 @@ void launch_i8gemm(cudaStream_t s, int64_t M, int64_t N, int64_t K, const int8_t
                                   static_cast<int>(I8S2<1>::kSmem)));
     IPT_CUDA(cudaFuncSetAttribute(i8gemm_2sm_kernel<Epi, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(I8S2<2>::kSmem)));
-    attr = true;
-  }
+  });
   const int tiles_m = static_cast<int>(M / kI8BM);
   // IPT_I8_GROUP: M tiles (pairs for the 2-SM kernels) per rasterisation group
   const char* genv = std::getenv("IPT_I8_GROUP");

@@ -43,22 +43,36 @@ struct HostPhases {
   }
 };
 
+// Context of the entry point running on this thread (set by check_ctx): on an error
+// its communicator is aborted, so ranks waiting for this one in a collective fail
+// instead of hanging (local backend; NCCL ranks time out in NCCL itself).
+thread_local Ctx* g_entry_ctx = nullptr;
+
+void abort_entry_comm() {
+  if (g_entry_ctx && g_entry_ctx->comm) g_entry_ctx->comm->abort();
+}
+
 template <typename F>
 int guarded(F&& f) {
+  g_entry_ctx = nullptr;
   try {
     f();
     return IPT_OK;
   } catch (const std::invalid_argument& e) {
     g_last_error = e.what();
+    abort_entry_comm();
     return IPT_ERR_INVALID;
   } catch (const NcclError& e) {
     g_last_error = e.what();
+    abort_entry_comm();
     return IPT_ERR_NCCL;
   } catch (const CudaError& e) {
     g_last_error = e.what();
+    abort_entry_comm();
     return IPT_ERR_CUDA;
   } catch (const std::exception& e) {
     g_last_error = e.what();
+    abort_entry_comm();
     return IPT_ERR_INTERNAL;
   }
 }
@@ -71,6 +85,7 @@ ipt_params params_or_default(const ipt_params* p) {
 
 void check_ctx(ipt_ctx* ctx) {
   if (ctx == nullptr) throw InvalidArgument("null ipt_ctx");
+  g_entry_ctx = &ctx->c;
 }
 
 // host row-major (rows x cols) -> device column-major with leading dimension ld (zero-padded dst)
@@ -253,7 +268,7 @@ int ipt_ctx_create(int device, ipt_ctx** out) {
 void ipt_ctx_destroy(ipt_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->c.device);
-  if (ctx->c.comm) ncclCommDestroy(ctx->c.comm);
+  ctx->c.comm.reset();
   for (auto& e : ctx->c.ev) cudaEventDestroy(e);
   if (ctx->c.h_state) cudaFreeHost(ctx->c.h_state);
   if (ctx->c.h_aux) cudaFreeHost(ctx->c.h_aux);
@@ -268,10 +283,8 @@ int ipt_ctx_device(const ipt_ctx* ctx) { return ctx ? ctx->c.device : -1; }
 
 int ipt_nccl_get_unique_id(void* out128) {
   return guarded([&] {
-    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
-    ncclUniqueId id;
-    IPT_NCCL(ncclGetUniqueId(&id));
-    std::memcpy(out128, &id, sizeof(id));
+    if (out128 == nullptr) throw InvalidArgument("ipt_nccl_get_unique_id: null out");
+    nccl_unique_id(out128);
   });
 }
 
@@ -280,16 +293,47 @@ int ipt_ctx_init_comm(ipt_ctx* ctx, const void* unique_id128, int rank, int nran
     check_ctx(ctx);
     if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArgument("ipt_ctx_init_comm: bad rank");
     DeviceGuard g(ctx->c.device);
-    if (ctx->c.comm) {
-      ncclCommDestroy(ctx->c.comm);
-      ctx->c.comm = nullptr;
-    }
-    ncclUniqueId id;
-    std::memcpy(&id, unique_id128, sizeof(id));
-    IPT_NCCL(ncclCommInitRank(&ctx->c.comm, nranks, id, rank));
+    ctx->c.comm.reset();
+    ctx->c.rank = 0;
+    ctx->c.nranks = 1;
+    ctx->c.comm = make_nccl_comm(unique_id128, rank, nranks, ctx->c.device);
     ctx->c.rank = rank;
     ctx->c.nranks = nranks;
   });
+}
+
+struct ipt_local_group {
+  std::shared_ptr<iptb::LocalGroup> g;
+};
+
+int ipt_local_group_create(int nranks, ipt_local_group** out) {
+  return guarded([&] {
+    if (out == nullptr) throw InvalidArgument("ipt_local_group_create: null out");
+    auto* h = new ipt_local_group();
+    h->g = make_local_group(nranks);
+    *out = h;
+  });
+}
+
+void ipt_local_group_destroy(ipt_local_group* group) { delete group; }
+
+int ipt_ctx_init_local_comm(ipt_ctx* ctx, ipt_local_group* group, int rank) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (group == nullptr) throw InvalidArgument("ipt_ctx_init_local_comm: null group");
+    DeviceGuard g(ctx->c.device);
+    ctx->c.comm.reset();
+    ctx->c.rank = 0;
+    ctx->c.nranks = 1;
+    ctx->c.comm = make_local_comm(group->g, rank, ctx->c.device);
+    ctx->c.rank = rank;
+    ctx->c.nranks = ctx->c.comm->nranks;
+  });
+}
+
+const char* ipt_ctx_comm_kind(const ipt_ctx* ctx) {
+  if (ctx == nullptr) return "";
+  return ctx->c.comm ? ctx->c.comm->kind() : "none";
 }
 
 int ipt_ctx_rank(const ipt_ctx* ctx, int* rank, int* nranks) {
@@ -409,8 +453,11 @@ int ipt_full_solve(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_
   return guarded([&] {
     check_ctx(ctx);
     DeviceGuard g(ctx->c.device);
+    // a complex warm start on real data runs the complex map (solve_full works in complex
+    // arithmetic throughout, solver.cpp:188-201)
+    const bool wc = n > 0 && any_nonzero(warm_im, n * n);
     solve_full_impl(
-        ctx->c, params, [&] { return full_upload(ctx->c, n, d_re, d_im, delta_re, delta_im); }, warm_re,
+        ctx->c, params, [&] { return full_upload(ctx->c, n, d_re, d_im, delta_re, delta_im, wc); }, warm_re,
         warm_im, z_re, z_im, lam_re, lam_im, stats);
   });
 }
@@ -423,9 +470,10 @@ int ipt_full_solve_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const double
   return guarded([&] {
     check_ctx(ctx);
     DeviceGuard g(ctx->c.device);
+    const bool wc = n > 0 && any_nonzero(warm_im, n * n);
     solve_full_impl(
         ctx->c, params,
-        [&] { return open_full_csr(ctx->c, n, d_re, d_im, rowptr, cols, val_re, val_im, false); }, warm_re,
+        [&] { return open_full_csr(ctx->c, n, d_re, d_im, rowptr, cols, val_re, val_im, wc); }, warm_re,
         warm_im, z_re, z_im, lam_re, lam_im, stats);
   });
 }
@@ -734,8 +782,9 @@ int ipt_single_solve_dense(ipt_ctx* ctx, int64_t n, const double* d_re, const do
     if (!(prm.tolerance > 0.0)) throw InvalidArgument("config: tolerance must be positive");
     if (prm.max_iterations <= 0) throw InvalidArgument("config: max_iterations must be positive");
     if (anchor < 0 || anchor >= n) throw InvalidArgument("solver: anchor out of range");
+    const bool wc = prm.schedule != IPT_SCHEDULE_CONTINUATION && any_nonzero(warm_im, n);
     single_solve_common(ctx, single_upload(ctx->c, n, d_re, d_im, false, delta_re, delta_im, nullptr,
-                                           nullptr, nullptr, nullptr, true),
+                                           nullptr, nullptr, nullptr, true, wc),
                         anchor, warm_re, warm_im, params, z_re, z_im, stats);
   });
 }
@@ -752,8 +801,9 @@ int ipt_single_solve_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const doub
     if (!(prm.tolerance > 0.0)) throw InvalidArgument("config: tolerance must be positive");
     if (prm.max_iterations <= 0) throw InvalidArgument("config: max_iterations must be positive");
     if (anchor < 0 || anchor >= n) throw InvalidArgument("solver: anchor out of range");
+    const bool wc = prm.schedule != IPT_SCHEDULE_CONTINUATION && any_nonzero(warm_im, n);
     single_solve_common(ctx, single_upload(ctx->c, n, d_re, d_im, true, nullptr, nullptr, rowptr, cols,
-                                           val_re, val_im, true),
+                                           val_re, val_im, true, wc),
                         anchor, warm_re, warm_im, params, z_re, z_im, stats);
   });
 }

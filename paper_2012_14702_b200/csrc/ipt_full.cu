@@ -678,9 +678,8 @@ void launch_complex_products(FullProblem& P, const double* zs, double* zd, int m
 void allreduce_sums(FullProblem& P, bool with_max) {
   Ctx& c = *P.ctx;
   if (c.nranks <= 1) return;
-  IPT_NCCL(ncclAllReduce(P.sums.get(), P.sums.get(), 3, ncclDouble, ncclSum, c.comm, c.stream));
-  if (with_max)
-    IPT_NCCL(ncclAllReduce(P.sums.get() + 3, P.sums.get() + 3, 1, ncclDouble, ncclMax, c.comm, c.stream));
+  c.comm->all_reduce(P.sums.get(), 3, CommType::F64, CommOp::Sum, c.stream);
+  if (with_max) c.comm->all_reduce(P.sums.get() + 3, 1, CommType::F64, CommOp::Max, c.stream);
 }
 
 bool use_ozaki(const FullProblem& P) {
@@ -854,8 +853,7 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
   if (sharded_upload) {
     const int64_t r0 = std::min<int64_t>(n, c.rank * up_chunk), r1 = std::min<int64_t>(n, (c.rank + 1) * up_chunk);
     if (r1 > r0) h2d_rows(c, P->A1.get() + r0 * P->lda, P->lda, delta_re + r0 * n, n, r1 - r0, n);
-    IPT_NCCL(ncclAllGather(P->A1.get() + c.rank * up_chunk * P->lda, P->A1.get(), size_t(up_chunk * P->lda),
-                           ncclDouble, c.comm, s));
+    c.comm->all_gather(P->A1.get(), size_t(up_chunk * P->lda), CommType::F64, s);
     pm.mark("h2d+allgather");
   } else if (!P->cplx) {
     h2d_rows(c, P->A1.get(), P->lda, delta_re, n, n, n);  // pinned, double-buffered
@@ -992,6 +990,10 @@ void full_reset(FullProblem& P, const double* warm_re, const double* warm_im, in
       const bool zero = warm_re[jg * n + jg] == 0.0 && (warm_im == nullptr || warm_im[jg * n + jg] == 0.0);
       if (zero) throw InvalidArgument("solve_full: warm start has zero diagonal entry");
     }
+    if (!P.cplx && warm_im)
+      for (int64_t t = 0; t < n * n; ++t)
+        if (warm_im[t] != 0.0)
+          throw InvalidArgument("solve_full: complex warm start on a real problem (open it complex)");
     DevBuf rm;
     rm.alloc(size_t(n) * std::max<int64_t>(P.ncols, 1), false);
     for (int part = 0; part < (warm_im && P.cplx ? 2 : 1); ++part) {
@@ -1075,7 +1077,10 @@ void full_iterate(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
   // Large problems: one host check per iteration is free next to a >=10 ms GEMM.
   // Small problems: enqueue several iterations per check; the done flag makes the
   // surplus launches exit immediately.
-  const int batch = P.n * P.ncols >= (int64_t(2048) * 2048) ? 1 : 16;
+  // The batch must be the same on every rank (each map carries collectives): size it from
+  // the global shard width, not this rank's column count.
+  const int64_t work = c.nranks > 1 ? P.n * ceil_div(P.n, int64_t(c.nranks)) : P.n * P.ncols;
+  const int batch = work >= (int64_t(2048) * 2048) ? 1 : 16;
   IPT_CUDA(cudaEventRecord(c.ev[0], c.stream));
   while (P.enq < prm.max_iterations) {
     for (int b = 0; b < batch && P.enq < prm.max_iterations; ++b) enqueue_map(P, P.enq++, prm);
@@ -1164,22 +1169,13 @@ void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
   // Gather the column shards on rank 0 (one final eigenvector gather).
   if (c.nranks > 1) {
     if (c.rank == 0) P.gathered.alloc(size_t(round_up(P.n, kBN)) * P.ldz);
-    IPT_NCCL(ncclGroupStart());
-    if (c.rank == 0) {
-      for (int r = 0; r < c.nranks; ++r) {
-        const int64_t r0 = P.n * r / c.nranks, r1 = P.n * (r + 1) / c.nranks;
-        if (r1 == r0) continue;
-        double* dst = P.gathered.get() + r0 * P.ldz;
-        if (r == 0)
-          IPT_CUDA(cudaMemcpyAsync(dst, z, sizeof(double) * (r1 - r0) * P.ldz, cudaMemcpyDeviceToDevice, s));
-        else
-          IPT_NCCL(ncclRecv(dst, size_t(r1 - r0) * P.ldz, ncclDouble, r, c.comm, s));
-      }
-    } else if (P.ncols > 0) {
-      IPT_NCCL(ncclSend(z, size_t(P.ncols) * P.ldz, ncclDouble, 0, c.comm, s));
+    std::vector<size_t> counts(c.nranks), displs(c.nranks);
+    for (int r = 0; r < c.nranks; ++r) {
+      const int64_t r0 = P.n * r / c.nranks, r1 = P.n * (r + 1) / c.nranks;
+      counts[r] = size_t(r1 - r0) * P.ldz;
+      displs[r] = size_t(r0) * P.ldz;
     }
-    // eigenvalues: each rank's lam block
-    IPT_NCCL(ncclGroupEnd());
+    c.comm->gather(z, size_t(P.ncols) * P.ldz, P.gathered.get(), counts.data(), displs.data(), CommType::F64, 0, s);
     c.sync();
   }
 
@@ -1250,24 +1246,14 @@ void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, d
     DevBuf all_r, all_i;
     all_r.alloc(n);
     all_i.alloc(n);
-    IPT_NCCL(ncclGroupStart());
-    if (c.rank == 0) {
-      for (int r = 0; r < c.nranks; ++r) {
-        const int64_t r0 = n * r / c.nranks, r1 = n * (r + 1) / c.nranks;
-        if (r1 == r0) continue;
-        if (r == 0) {
-          IPT_CUDA(cudaMemcpyAsync(all_r.get(), P.lam.get(), sizeof(double) * (r1 - r0), cudaMemcpyDeviceToDevice, s));
-          IPT_CUDA(cudaMemcpyAsync(all_i.get(), P.lami.get(), sizeof(double) * (r1 - r0), cudaMemcpyDeviceToDevice, s));
-        } else {
-          IPT_NCCL(ncclRecv(all_r.get() + r0, r1 - r0, ncclDouble, r, c.comm, s));
-          IPT_NCCL(ncclRecv(all_i.get() + r0, r1 - r0, ncclDouble, r, c.comm, s));
-        }
-      }
-    } else if (P.ncols > 0) {
-      IPT_NCCL(ncclSend(P.lam.get(), P.ncols, ncclDouble, 0, c.comm, s));
-      IPT_NCCL(ncclSend(P.lami.get(), P.ncols, ncclDouble, 0, c.comm, s));
+    std::vector<size_t> counts(c.nranks), displs(c.nranks);
+    for (int r = 0; r < c.nranks; ++r) {
+      const int64_t r0 = n * r / c.nranks, r1 = n * (r + 1) / c.nranks;
+      counts[r] = size_t(r1 - r0);
+      displs[r] = size_t(r0);
     }
-    IPT_NCCL(ncclGroupEnd());
+    c.comm->gather(P.lam.get(), size_t(P.ncols), all_r.get(), counts.data(), displs.data(), CommType::F64, 0, s);
+    c.comm->gather(P.lami.get(), size_t(P.ncols), all_i.get(), counts.data(), displs.data(), CommType::F64, 0, s);
     if (c.rank == 0) {
       IPT_CUDA(cudaMemcpyAsync(lr.data(), all_r.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
       IPT_CUDA(cudaMemcpyAsync(li.data(), all_i.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));

@@ -1,14 +1,14 @@
 // Internal host-side structures shared by the IPT CUDA translation units.
 #pragma once
 
-#include <nccl.h>
-
 #include <atomic>
 #include <string>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "ipt_common.cuh"
+#include "ipt_comm.cuh"
 #include "../../include/ipt_cuda.h"
 
 namespace iptb {
@@ -16,15 +16,13 @@ namespace iptb {
 extern std::atomic<int64_t> g_launches;
 inline void count_launch(int64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
+// Communicator failures (NCCL errors, an aborted or timed-out local group): IPT_ERR_NCCL.
 struct NcclError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
-inline void nccl_check(ncclResult_t r, const char* what, const char* file, int line) {
-  if (r != ncclSuccess)
-    throw NcclError(std::string("NCCL error ") + ncclGetErrorString(r) + " in " + what + " at " +
-                    file + ":" + std::to_string(line));
-}
-#define IPT_NCCL(x) ::iptb::nccl_check((x), #x, __FILE__, __LINE__)
+struct CommAborted : NcclError {
+  using NcclError::NcclError;
+};
 
 // Device buffer owned by a problem; freed in the destructor.
 struct DevBuf {
@@ -45,7 +43,7 @@ struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t stream2 = nullptr;  // transfers overlapped with compute on `stream`
-  ncclComm_t comm = nullptr;
+  std::unique_ptr<Comm> comm;  // NCCL or local backend (ipt_comm.cuh); null: single rank
   int rank = 0, nranks = 1;
   LoopState* h_state = nullptr;  // pinned mirror of the device loop state
   double* h_aux = nullptr;       // pinned scratch (256 B) for other device -> host scalars
@@ -72,6 +70,23 @@ struct ProfMarks {
   explicit ProfMarks(const char* n);
   void mark(const char* what, bool sync_device = false);
   ~ProfMarks();
+};
+
+// Per-device one-time setup (function attributes such as the >48 KB dynamic shared memory
+// opt-in apply per device): run(fn) calls fn once for each device it is used on,
+// thread-safe (contexts on several devices / host threads).
+struct PerDeviceOnce {
+  std::mutex mu;
+  bool done[64] = {};
+  template <class F>
+  void run(F&& fn) {
+    int dev = 0;
+    IPT_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 0 || dev >= 64 || done[dev]) return;
+    fn();
+    done[dev] = true;
+  }
 };
 
 struct DeviceGuard {

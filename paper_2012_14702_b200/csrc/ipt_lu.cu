@@ -556,17 +556,21 @@ LuProblem* lu_factor_device(Ctx& c, int64_t n, const double* a_re, const double*
   // reference's updates; only those of A22 are summed per panel instead of one by one.
   CgemmScratch S;
   // cooperative grid for the panel kernel: every resident CTA, one wave
-  static int panel_grid = 0;
-  if (panel_grid == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    IPT_CUDA(cudaGetDevice(&dev));
-    IPT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // (per device: the SM count and the shared-memory opt-in belong to the current device)
+  static PerDeviceOnce setup;
+  static int grid_of[64] = {};
+  int cur_dev = 0;
+  IPT_CUDA(cudaGetDevice(&cur_dev));
+  setup.run([cur_dev] {
+    int sms = 0, per_sm = 0;
+    IPT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur_dev));
     IPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lu_panel_kernel, kPanelThreads, 0));
     if (per_sm < 1) throw CudaError("lu: panel kernel cannot be resident");
-    panel_grid = sms;  // one CTA per SM
     IPT_CUDA(cudaFuncSetAttribute(lu_trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kTrsmSmem)));
-  }
+    grid_of[cur_dev] = sms;  // one CTA per SM
+  });
+  const int panel_grid = grid_of[cur_dev];
   DevBuf pv, pidx;
   pv.alloc(panel_grid, false);
   pidx.alloc(panel_grid, false);

@@ -601,16 +601,15 @@ double sigma_min_device(Ctx& c, int64_t n, const double* zr, const double* zi, i
   constexpr int64_t kW = 4 * NB;
   DevBuf Pb;  // L21 of the current outer panel, row-major, row i = matrix row kb + i
   Pb.alloc((size_t(round_up(m, kBM)) + kW) * kW);
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  attr.run([] {
     IPT_CUDA(cudaFuncSetAttribute(potrf_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(NB * LDS * sizeof(double))));
     IPT_CUDA(cudaFuncSetAttribute(trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int((NB + 32) * LDS * sizeof(double))));
     IPT_CUDA(cudaFuncSetAttribute(tri_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(NB * LDS * sizeof(double))));
-    attr = true;
-  }
+  });
   auto sub_update = [&](const double* panel, int64_t k, int64_t r0, int64_t rows, int64_t cols) {
     // H[r0.., r0..r0+cols) -= panel[r0..] panel[r0..r0+cols)^T, lower tiles of the block
     if (rows <= 0 || cols <= 0) return;

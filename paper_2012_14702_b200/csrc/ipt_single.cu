@@ -27,6 +27,7 @@
 namespace iptb {
 
 constexpr int kMaxPeers = 7;  // one 8-GPU node
+enum PeerKind : int { kPeerNone = 0, kPeerIpc = 1, kPeerOwned = 2, kPeerBorrowed = 3 };
 
 struct SingleProblem {
   Ctx* ctx = nullptr;
@@ -70,14 +71,16 @@ struct SingleProblem {
   bool p2p = false;
   int npeers = 0;
   double* peer_z[2][kMaxPeers] = {};
-  bool peer_ipc = false;  // peer_z opened by cudaIpcOpenMemHandle (else: local emulation)
+  // peer_z opened by cudaIpcOpenMemHandle (NCCL ranks), owned stand-ins (single-rank
+  // test hook), or borrowed from ranks of the same process (local communicator)
+  int peer_kind = 0;
   ~SingleProblem() {
     if (state) cudaFree(state);
     for (int b = 0; b < 2; ++b)
       for (int q = 0; q < npeers; ++q)
         if (peer_z[b][q]) {
-          if (peer_ipc) cudaIpcCloseMemHandle(peer_z[b][q]);
-          else cudaFree(peer_z[b][q]);
+          if (peer_kind == kPeerIpc) cudaIpcCloseMemHandle(peer_z[b][q]);
+          else if (peer_kind == kPeerOwned) cudaFree(peer_z[b][q]);
         }
   }
 };
@@ -704,26 +707,22 @@ void enqueue_cmatvec(SingleProblem& P, int src) {
 void allgather_z(SingleProblem& P, int buf) {
   Ctx& c = *P.ctx;
   if (c.nranks <= 1) return;
-  IPT_NCCL(ncclAllGather(P.z[buf].get() + c.rank * P.chunk, P.z[buf].get(), P.chunk, ncclDouble,
-                         c.comm, c.stream));
-  if (P.cplx)
-    IPT_NCCL(ncclAllGather(P.zi[buf].get() + c.rank * P.chunk, P.zi[buf].get(), P.chunk, ncclDouble,
-                           c.comm, c.stream));
+  c.comm->all_gather(P.z[buf].get(), P.chunk, CommType::F64, c.stream);
+  if (P.cplx) c.comm->all_gather(P.zi[buf].get(), P.chunk, CommType::F64, c.stream);
 }
 void allgather_w(SingleProblem& P) {
   Ctx& c = *P.ctx;
   if (c.nranks <= 1) return;
-  IPT_NCCL(ncclAllGather(P.w.get() + c.rank * P.chunk, P.w.get(), P.chunk, ncclDouble, c.comm, c.stream));
-  IPT_NCCL(ncclAllGather(P.wi.get() + c.rank * P.chunk, P.wi.get(), P.chunk, ncclDouble, c.comm, c.stream));
+  c.comm->all_gather(P.w.get(), P.chunk, CommType::F64, c.stream);
+  c.comm->all_gather(P.wi.get(), P.chunk, CommType::F64, c.stream);
 }
 
 void reduce_and_allreduce(SingleProblem& P, const LoopState* st, bool with_max) {
   Ctx& c = *P.ctx;
   reduce_partials(c.stream, P.partials.get(), map_blocks(P), P.sums.get(), st);
   if (c.nranks > 1) {
-    IPT_NCCL(ncclAllReduce(P.sums.get(), P.sums.get(), 3, ncclDouble, ncclSum, c.comm, c.stream));
-    if (with_max)
-      IPT_NCCL(ncclAllReduce(P.sums.get() + 3, P.sums.get() + 3, 1, ncclDouble, ncclMax, c.comm, c.stream));
+    c.comm->all_reduce(P.sums.get(), 3, CommType::F64, CommOp::Sum, c.stream);
+    if (with_max) c.comm->all_reduce(P.sums.get() + 3, 1, CommType::F64, CommOp::Max, c.stream);
   }
 }
 
@@ -810,68 +809,29 @@ void upload_anchor_row(SingleProblem& P) {
   P.ctx->sync();
 }
 
-// Fused all-gather setup: both z buffers become cudaMalloc'd (IPC-exportable), their
-// handles are all-gathered over the library communicator and every rank maps its peers'
-// buffers. The outcome is agreed by a min all-reduce, so if any rank cannot map a peer all
-// of them keep the NCCL all-gather. IPT_P2P=0 keeps it too.
+// Fused all-gather setup: both z buffers become cudaMalloc'd and are exchanged over the
+// library communicator (NCCL: CUDA IPC handles, every rank maps its peers' buffers; local
+// ranks: the pointers themselves). The outcome is agreed by all ranks, so if any rank
+// cannot map a peer all of them keep the collective all-gather. IPT_P2P=0 keeps it too.
 void setup_peer_gather(SingleProblem& P, int64_t zlen) {
   Ctx& c = *P.ctx;
   const int g = c.nranks;
   if (g <= 1 || P.cplx || g - 1 > kMaxPeers) return;
   const char* e = std::getenv("IPT_P2P");
   if (e && e[0] == '0') return;
-  cudaStream_t s = c.stream;
+  // cudaMalloc'd: exportable by CUDA IPC (NCCL ranks) and peer-accessible without pool
+  // access grants (local ranks on several devices)
   for (int b = 0; b < 2; ++b) P.z[b].alloc_plain(zlen);
-  struct Handles {
-    cudaIpcMemHandle_t h[2];
-  };
-  Handles mine{};
-  int ok = 1;
+  void* mine[2] = {P.z[0].get(), P.z[1].get()};
+  void* peers[2][8] = {};
+  bool ipc = false;
+  const bool all_ok = c.comm->map_peers(mine, 2, peers, &ipc);
+  if (!all_ok) return;
   for (int b = 0; b < 2; ++b)
-    if (cudaIpcGetMemHandle(&mine.h[b], P.z[b].get()) != cudaSuccess) ok = 0;
-  cudaGetLastError();
-  const size_t hb = sizeof(Handles);
-  DevBuf dev;
-  dev.alloc(ceil_div(int64_t(hb) * g, 8) + 1);
-  char* dv = reinterpret_cast<char*>(dev.get());
-  IPT_CUDA(cudaMemcpyAsync(dv + hb * c.rank, &mine, hb, cudaMemcpyHostToDevice, s));
-  IPT_NCCL(ncclAllGather(dv + hb * c.rank, dv, hb, ncclChar, c.comm, s));
-  std::vector<Handles> all(g);
-  IPT_CUDA(cudaMemcpyAsync(all.data(), dv, hb * g, cudaMemcpyDeviceToHost, s));
-  IPT_CUDA(cudaStreamSynchronize(s));
-  int q = 0;
-  for (int r = 0; r < g && ok; ++r) {
-    if (r == c.rank) continue;
-    for (int b = 0; b < 2 && ok; ++b) {
-      void* ptr = nullptr;
-      if (cudaIpcOpenMemHandle(&ptr, all[r].h[b], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-        cudaGetLastError();
-        ok = 0;
-      } else {
-        P.peer_z[b][q] = static_cast<double*>(ptr);
-      }
-    }
-    ++q;
-  }
-  P.npeers = q;
-  P.peer_ipc = true;
-  int* dok = reinterpret_cast<int*>(dev.get());
-  IPT_CUDA(cudaMemcpyAsync(dok, &ok, sizeof(int), cudaMemcpyHostToDevice, s));
-  IPT_NCCL(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, c.comm, s));
-  int all_ok = 0;
-  IPT_CUDA(cudaMemcpyAsync(&all_ok, dok, sizeof(int), cudaMemcpyDeviceToHost, s));
-  IPT_CUDA(cudaStreamSynchronize(s));
-  if (all_ok) {
-    P.p2p = true;
-    return;
-  }
-  for (int b = 0; b < 2; ++b)
-    for (int k = 0; k < kMaxPeers; ++k)
-      if (P.peer_z[b][k]) {
-        cudaIpcCloseMemHandle(P.peer_z[b][k]);
-        P.peer_z[b][k] = nullptr;
-      }
-  P.npeers = 0;
+    for (int q = 0; q < g - 1; ++q) P.peer_z[b][q] = static_cast<double*>(peers[b][q]);
+  P.npeers = g - 1;
+  P.peer_kind = ipc ? kPeerIpc : kPeerBorrowed;
+  P.p2p = true;
 }
 
 }  // namespace
@@ -887,7 +847,7 @@ void single_debug_peers(SingleProblem& P, int npeers) {
       IPT_CUDA(cudaMemset(P.peer_z[b][q], 0, sizeof(double) * P.z[b].count));
     }
   P.npeers = npeers;
-  P.peer_ipc = false;
+  P.peer_kind = kPeerOwned;
   P.p2p = npeers > 0;
 }
 
@@ -990,7 +950,7 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
   P->wa.alloc(2);
   P->npart = std::max<int64_t>(map_blocks(*P), 1);
   P->partials.alloc(size_t(P->npart) * 4);
-  P->sums.alloc(4);
+  P->sums.alloc(5);  // 4 stop sums + a barrier token (single_reset)
   IPT_CUDA(cudaMalloc(&P->state, sizeof(LoopState)));
   c.sync();
   return P.release();
@@ -1053,6 +1013,11 @@ void single_reset(SingleProblem& P, int64_t anchor, const double* warm_re, const
     P.trace_cap = max_iter_hint;
   }
   P.enq = 0;
+  // Fused all-gather: peers store rows of step 0 into this rank's z[1] (zeroed above) and,
+  // across solves, into buffers this rank may still be reading (a previous finalize). A
+  // stream-ordered all-reduce here orders every rank's reset (and everything before it)
+  // before any rank's first map.
+  if (P.p2p && c.nranks > 1) c.comm->all_reduce(P.sums.get() + 4, 1, CommType::F64, CommOp::Sum, s);
   c.sync();
 }
 

@@ -11,7 +11,10 @@ from __future__ import annotations
 
 import os
 
-from .ipt import Context, nccl_unique_id
+import threading
+from typing import Callable, Sequence
+
+from .ipt import Context, LocalGroup, nccl_unique_id
 
 
 def column_shard(n: int, rank: int, nranks: int) -> tuple[int, int]:
@@ -41,3 +44,40 @@ def init_context_from_env() -> Context:
         dist.broadcast_object_list(obj, src=0)
         ctx.init_comm(obj[0], rank, world)
     return ctx
+
+
+def local_contexts(nranks: int, devices: Sequence[int] = (0,)) -> list[Context]:
+    """nranks contexts of this process joined in one in-process communicator group
+    (ipt_ctx_init_local_comm); rank r runs on devices[r % len(devices)]. With one
+    device this drives the library's multi-rank code (sharded upload, per-iteration
+    all-reduce, fused peer-store all-gather, gathers) on a single GPU."""
+    group = LocalGroup(nranks)
+    ctxs = []
+    for r in range(nranks):
+        c = Context(devices[r % len(devices)])
+        c.init_local_comm(group, r)
+        ctxs.append(c)
+    return ctxs
+
+
+def run_ranks(fn: Callable[[Context], object], ctxs: Sequence[Context]) -> list:
+    """fn(ctx) on one host thread per rank (ctypes releases the GIL inside the library);
+    returns the per-rank results, re-raising the first rank's exception."""
+    out: list = [None] * len(ctxs)
+    err: list = [None] * len(ctxs)
+
+    def body(r):
+        try:
+            out[r] = fn(ctxs[r])
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            err[r] = e
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(len(ctxs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    return out

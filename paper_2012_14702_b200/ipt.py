@@ -282,6 +282,16 @@ class Context:
         check(_lib.load().ipt_ctx_init_comm(self.handle, buf, int(rank), int(nranks)))
         self.rank, self.nranks = rank, nranks
 
+    def init_local_comm(self, group: "LocalGroup", rank: int) -> None:
+        """Join an in-process group as `rank` (ipt_ctx_init_local_comm)."""
+        check(_lib.load().ipt_ctx_init_local_comm(self.handle, group.handle, int(rank)))
+        self.rank, self.nranks = rank, group.nranks
+        self._group = group  # the group outlives its member contexts
+
+    @property
+    def comm_kind(self) -> str:
+        return _lib.load().ipt_ctx_comm_kind(self.handle).decode()
+
     def synchronize(self) -> None:
         check(_lib.load().ipt_ctx_synchronize(self.handle))
 
@@ -293,6 +303,25 @@ class Context:
     def __del__(self):
         try:
             self.close()
+        except Exception:
+            pass
+
+
+class LocalGroup:
+    """In-process communicator group (ipt_local_group_create): nranks contexts of this
+    process, one host thread per rank, on one GPU or several (include/ipt_cuda.h)."""
+
+    def __init__(self, nranks: int):
+        h = C.c_void_p()
+        check(_lib.load().ipt_local_group_create(int(nranks), C.byref(h)))
+        self.handle = h
+        self.nranks = nranks
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib.load().ipt_local_group_destroy(self.handle)
+                self.handle = None
         except Exception:
             pass
 

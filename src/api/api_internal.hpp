@@ -3,6 +3,7 @@
 // conversion std::complex (interleaved) <-> planar re / im at the boundary.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -107,7 +108,7 @@ inline Planar split(const cplx* v, std::size_t count) {
     Planar p;
     p.re.resize(count);
     p.im.resize(count);
-    std::vector<char> flag(host_threads() + 1, 0);
+    std::atomic<bool> any_im{false};
     parallel_chunks(count, [&](std::size_t b, std::size_t e) {
         bool any = false;
         for (std::size_t i = b; i < e; ++i) {
@@ -115,9 +116,9 @@ inline Planar split(const cplx* v, std::size_t count) {
             p.im[i] = v[i].imag();
             any = any || v[i].imag() != 0.0;
         }
-        if (any) flag[0] = 1;  // benign race: every writer stores the same value
+        if (any) any_im.store(true, std::memory_order_relaxed);
     });
-    p.any_im = flag[0] != 0;
+    p.any_im = any_im.load();
     return p;
 }
 

@@ -41,3 +41,35 @@ def test_bench_value_is_the_metric_of_the_step_time():
     d = _line()
     n = d["config"]["n"]
     assert abs(d["value"] - 2.0 * n ** 3 / (d["ms_per_step"] * 1e-3) / 1e12) <= 1e-6 * d["value"]
+
+
+def test_bench_gpus_n_without_n_devices_fails_loudly():
+    """`bench.py --gpus N` outside torchrun re-launches itself as N ranks; with fewer than N
+    visible GPUs (none here) it must exit non-zero instead of timing one GPU."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode != 0
+    assert "--gpus 2" in r.stderr
+
+
+def test_reference_arm_does_not_load_the_product_library():
+    """The reference arm's process maps only oracle/ libraries (its inputs come from the
+    oracle's restatement of the reference generator)."""
+    import subprocess
+    import sys
+
+    code = ("import sys, runpy; sys.argv=['bench.py','--impl','reference','--steps','1','--warmup','0',"
+            "'--ref-n','64']; import bench; bench.main(); "
+            "maps=open('/proc/self/maps').read(); print('PRODUCT_LOADED' if 'libipt_b200' in maps else 'CLEAN')")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert "CLEAN" in r.stdout
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][0])
+    assert line["impl"] == "reference" and line["config"]["reference_sample_n"] == 64
+    assert line["config"]["same_config"] is False
