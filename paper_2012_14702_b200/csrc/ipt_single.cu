@@ -74,6 +74,10 @@ struct SingleProblem {
   // peer_z opened by cudaIpcOpenMemHandle (NCCL ranks), owned stand-ins (single-rank
   // test hook), or borrowed from ranks of the same process (local communicator)
   int peer_kind = 0;
+  // fused step tail: arrival counter of the map kernel's CTAs; w_a of z[enq & 1] already
+  // formed by the previous step's tail (else the next step launches the anchor kernel)
+  std::unique_ptr<unsigned, void (*)(void*)> tail_counter{nullptr, [](void* p) { cudaFree(p); }};
+  bool wa_fresh = false;
   ~SingleProblem() {
     if (state) cudaFree(state);
     for (int b = 0; b < 2; ++b)
@@ -120,6 +124,7 @@ inline int spmv_rows_per_block() {
   const SpmvVariant& v = kSpmvVariants[spmv_variant()];
   return v.lanes ? 256 / v.lanes : 8 * v.rows;
 }
+
 constexpr int kSpmvMinBlocks = 5;       // 48 registers (no spills): 5 CTAs (40 warps) per SM
 
 enum MapMode : int { kMvStore = 0, kMvMap = 1, kMvFinal = 2, kMvAccel = 3 };
@@ -317,6 +322,24 @@ struct MapArgs {
   double* partials;
   double* peer[kMaxPeers];  // kMvMap: the same rows of the new iterate in every peer's z
   int npeers;
+  // Fused step tail (kMvMap; tail_mode 0: none). The last CTA to finish sums the per-CTA
+  // partials in reduce_partials_kernel's order into tail_sums; mode 2 (one rank) then also
+  // applies the stop decision (decide_single_dev) and forms w_a of the new iterate for the
+  // next step (the anchor kernels' arithmetic), so a step is ONE launch. Mode 1 (several
+  // ranks) stops after the sums: the all-reduce and decide_anchor_kernel follow.
+  int tail_mode;
+  unsigned* tail_counter;  // zero between launches (reset by the last CTA)
+  LoopState* tail_state;
+  double* tail_sums;
+  int tail_k, tail_max_iter, tail_schedule, tail_ignore;
+  double tail_tol, tail_div, tail_alpha, tail_snap;
+  double* tail_trace;
+  // anchor row of the next w_a: CSR (columns, values, nnz, lane phase) or dense (row, lda)
+  const int32_t* a_cols;
+  const double* a_vals;
+  int64_t a_nnz;
+  int a_phase;
+  int64_t a_lda;
 };
 
 // Remote stores of the fused all-gather must be visible system-wide before the
@@ -375,6 +398,145 @@ __device__ __forceinline__ double schedule_scale(const MapArgs& a) {
   return ak <= a.snap ? 1.0 : 1.0 - ak;
 }
 
+// The reference's per-iteration tests (solver.cpp:69-80): divergence first (from the
+// NaN-propagating |fz|^2), then convergence (gated by the continuation schedule,
+// solver.cpp:146-152), then the iteration cap.
+__device__ __forceinline__ void decide_single_dev(LoopState* st, double diff2, double base2, double new2, double mx,
+                                                  int k, double tol, int max_iter, double div_thr, int schedule,
+                                                  double alpha, double snap, int ignore_conv, double* trace) {
+  const double step = sqrt(diff2) / sqrt(base2);
+  st->iterations = k + 1;
+  st->final_step = step;
+  st->final_max_abs = mx;
+  if (trace) trace[k] = step;
+  const double ak = st->scale_ak;
+  const bool gate = schedule == IPT_SCHEDULE_PLAIN || ak <= snap;
+  const double zn = sqrt(new2);
+  if (!isfinite(zn) || zn > div_thr) {
+    st->status = kDiverged;
+    st->done = 1;
+  } else if (!ignore_conv && gate && step <= tol) {
+    st->status = kConverged;
+    st->done = 1;
+  } else if (k + 1 >= max_iter) {
+    st->status = kMaxIterations;
+    st->done = 1;
+  }
+  if (schedule == IPT_SCHEDULE_CONTINUATION) st->scale_ak = ak * alpha;
+}
+
+// w_a = Delta[a, :] . z by one warp, bit for bit the anchor kernels' sums (CSR: entry k on
+// lane (phase + k) mod 32, ascending per lane, xor tree; dense: rows_dot<1>). z is read
+// through L2 (other CTAs of this launch wrote it).
+__device__ __forceinline__ void anchor_value_warp(const MapArgs& a, const double* __restrict__ z) {
+  const int lane = threadIdx.x & 31;
+  double sacc = 0.0;
+  if (a.a_cols != nullptr) {
+    for (int64_t k = (lane - a.a_phase + 32) & 31; k < a.a_nnz; k += 32)
+      sacc = __fma_rn(a.a_vals[k], __ldcg(z + a.a_cols[k]), sacc);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, off);
+  } else {
+    // rows_dot<1> with the z loads through L2
+    const double2* a2 = reinterpret_cast<const double2*>(a.a_vals);
+    const double2* z2 = reinterpret_cast<const double2*>(z);
+    const int64_t K2 = a.a_lda / 2;
+    double ax = 0.0, ay = 0.0;
+    int64_t k = lane;
+    for (; k + 96 < K2; k += 128) {
+      double2 zz[4], av[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) zz[u] = __ldcg(z2 + k + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) av[u] = ld_stream(a2 + k + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ax = __fma_rn(av[u].x, zz[u].x, ax);
+        ay = __fma_rn(av[u].y, zz[u].y, ay);
+      }
+    }
+    for (; k < K2; k += 32) {
+      const double2 zz = __ldcg(z2 + k);
+      const double2 av = ld_stream(a2 + k);
+      ax = __fma_rn(av.x, zz.x, ax);
+      ay = __fma_rn(av.y, zz.y, ay);
+    }
+    sacc = ax + ay;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, off);
+  }
+  if (lane == 0) *const_cast<double*>(a.wa) = sacc;
+}
+
+// Fused step tail, called by every thread of every CTA after its partials are written
+// (blockDim.x == 256). See MapArgs::tail_mode.
+__device__ __forceinline__ void step_tail(const MapArgs& a) {
+  __shared__ int s_last;
+  __shared__ double s_red[16][4];
+  __threadfence();  // this thread's fz / peer / partial stores before the arrival count
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(a.tail_counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // reduce_partials_kernel's order: 512 virtual threads (t and t + 256 here), each summing
+  // partials t, t + 512, ...; xor tree per virtual warp; virtual warps 0..15 in order.
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  double lo[4] = {0.0, 0.0, 0.0, 0.0}, hi[4] = {0.0, 0.0, 0.0, 0.0};
+  const int64_t count = gridDim.x;
+  for (int64_t i = t; i < count; i += 512) {
+    lo[0] += __ldcg(a.partials + 4 * i + 0);
+    lo[1] += __ldcg(a.partials + 4 * i + 1);
+    lo[2] += __ldcg(a.partials + 4 * i + 2);
+    lo[3] = nan_max(lo[3], __ldcg(a.partials + 4 * i + 3));
+  }
+  for (int64_t i = t + 256; i < count; i += 512) {
+    hi[0] += __ldcg(a.partials + 4 * i + 0);
+    hi[1] += __ldcg(a.partials + 4 * i + 1);
+    hi[2] += __ldcg(a.partials + 4 * i + 2);
+    hi[3] = nan_max(hi[3], __ldcg(a.partials + 4 * i + 3));
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      lo[q] += __shfl_xor_sync(0xffffffffu, lo[q], off);
+      hi[q] += __shfl_xor_sync(0xffffffffu, hi[q], off);
+    }
+    lo[3] = nan_max(lo[3], __shfl_xor_sync(0xffffffffu, lo[3], off));
+    hi[3] = nan_max(hi[3], __shfl_xor_sync(0xffffffffu, hi[3], off));
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      s_red[warp][q] = lo[q];
+      s_red[warp + 8][q] = hi[q];
+    }
+  }
+  __syncthreads();
+  if (t == 0) {
+    double r0 = s_red[0][0], r1 = s_red[0][1], r2 = s_red[0][2], r3 = s_red[0][3];
+#pragma unroll
+    for (int w = 1; w < 16; ++w) {
+      r0 += s_red[w][0];
+      r1 += s_red[w][1];
+      r2 += s_red[w][2];
+      r3 = nan_max(r3, s_red[w][3]);
+    }
+    a.tail_sums[0] = r0;
+    a.tail_sums[1] = r1;
+    a.tail_sums[2] = r2;
+    a.tail_sums[3] = r3;
+    if (a.tail_mode == 2)
+      decide_single_dev(a.tail_state, r0, r1, r2, r3, a.tail_k, a.tail_tol, a.tail_max_iter, a.tail_div,
+                        a.tail_schedule, a.tail_alpha, a.tail_snap, a.tail_ignore, a.tail_trace);
+    *a.tail_counter = 0u;
+  }
+  if (a.tail_mode != 2) return;
+  __syncthreads();
+  if (warp == 0 && !a.tail_state->done) anchor_value_warp(a, a.fz);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kGemvWarps * 32) gemv_map_kernel(const double* __restrict__ A,
                                                                    int64_t lda, MapArgs a) {
@@ -399,6 +561,7 @@ __global__ void __launch_bounds__(kGemvWarps * 32) gemv_map_kernel(const double*
     double* o = a.partials + size_t(blockIdx.x) * 4;
     o[0] = v[0]; o[1] = v[1]; o[2] = v[2]; o[3] = v[3];
   }
+  if (MODE == kMvMap && a.tail_mode != 0) step_tail(a);
 }
 
 template <int MODE, int LANES, int U>
@@ -466,6 +629,7 @@ __global__ void __launch_bounds__(256, MINB) spmv_group_kernel(const int64_t* __
     double* o = a.partials + size_t(blockIdx.x) * 4;
     o[0] = v[0]; o[1] = v[1]; o[2] = v[2]; o[3] = v[3];
   }
+  if (MODE == kMvMap && a.tail_mode != 0) step_tail(a);
 }
 
 // The anchor row's sum exactly as spmv_group_kernel forms it: entry k of the row on
@@ -503,26 +667,26 @@ __global__ void decide_single_kernel(LoopState* st, const double* __restrict__ s
                                      int max_iter, double div_thr, int schedule, double alpha,
                                      double snap, int ignore_conv, double* trace) {
   if (st->done) return;
-  const double diff2 = sums[0], base2 = sums[1], new2 = sums[2];
-  const double step = sqrt(diff2) / sqrt(base2);
-  st->iterations = k + 1;
-  st->final_step = step;
-  st->final_max_abs = sums[3];
-  if (trace) trace[k] = step;
-  const double ak = st->scale_ak;
-  const bool gate = schedule == IPT_SCHEDULE_PLAIN || ak <= snap;
-  const double zn = sqrt(new2);
-  if (!isfinite(zn) || zn > div_thr) {
-    st->status = kDiverged;
-    st->done = 1;
-  } else if (!ignore_conv && gate && step <= tol) {
-    st->status = kConverged;
-    st->done = 1;
-  } else if (k + 1 >= max_iter) {
-    st->status = kMaxIterations;
-    st->done = 1;
+  decide_single_dev(st, sums[0], sums[1], sums[2], sums[3], k, tol, max_iter, div_thr, schedule, alpha, snap,
+                    ignore_conv, trace);
+}
+
+// Several ranks: after the all-reduce of the stop sums, the decision and (if the loop goes
+// on) w_a of the new iterate, which every rank's fused all-gather has completed by now.
+__global__ void decide_anchor_kernel(LoopState* st, const double* __restrict__ sums, int k, double tol,
+                                     int max_iter, double div_thr, int schedule, double alpha, double snap,
+                                     int ignore_conv, double* trace, MapArgs a) {
+  __shared__ int s_go;
+  if (threadIdx.x == 0) {
+    s_go = 0;
+    if (!st->done) {
+      decide_single_dev(st, sums[0], sums[1], sums[2], sums[3], k, tol, max_iter, div_thr, schedule, alpha, snap,
+                        ignore_conv, trace);
+      s_go = !st->done;
+    }
   }
-  if (schedule == IPT_SCHEDULE_CONTINUATION) st->scale_ak = ak * alpha;
+  __syncthreads();
+  if (s_go) anchor_value_warp(a, a.fz);
 }
 
 // ---- complex correctness path: generic complex matvec then an elementwise map ----
@@ -726,10 +890,54 @@ void reduce_and_allreduce(SingleProblem& P, const LoopState* st, bool with_max) 
   }
 }
 
+// The step's reduction / decision / next anchor value fused into the map kernel (one launch
+// per step on one rank, map + decide_anchor_kernel with several): dense GEMV and the
+// grouped CSR kernels (whose anchor sum the tail reproduces). IPT_SINGLE_FUSED=0: the
+// separate anchor / reduction / decision launches.
+bool fused_step(const SingleProblem& P) {
+  static const bool on = [] {
+    const char* e = std::getenv("IPT_SINGLE_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  return on && !P.cplx && (!P.csr || spmv_grouped());
+}
+
+void set_anchor_args(const SingleProblem& P, MapArgs& a) {
+  if (P.csr) {
+    a.a_cols = P.acols.get();
+    a.a_vals = P.arow.get();
+    a.a_nnz = P.annz;
+    a.a_phase = P.anchor_phase;
+  } else {
+    a.a_cols = nullptr;
+    a.a_vals = P.arow.get();
+    a.a_lda = P.lda;
+  }
+}
+
+void set_tail_args(SingleProblem& P, MapArgs& a, int mode, int k, const ipt_params& prm) {
+  a.tail_mode = mode;
+  a.tail_counter = P.tail_counter.get();
+  a.tail_state = P.state;
+  a.tail_sums = P.sums.get();
+  a.tail_k = k;
+  a.tail_max_iter = prm.max_iterations;
+  a.tail_schedule = prm.schedule;
+  a.tail_ignore = prm.ignore_convergence;
+  a.tail_tol = prm.tolerance;
+  a.tail_div = prm.divergence_threshold;
+  a.tail_alpha = prm.shrink_alpha;
+  a.tail_snap = 0.25 * prm.tolerance;
+  a.tail_trace = prm.record_trace ? P.trace.get() : nullptr;
+  set_anchor_args(P, a);
+}
+
 template <int MODE>
-void enqueue_real_map(SingleProblem& P, int src, const ipt_params* prm, double* fz_out = nullptr) {
+void enqueue_real_map(SingleProblem& P, int src, const ipt_params* prm, double* fz_out = nullptr,
+                      int tail_mode = 0, int k = 0) {
   cudaStream_t s = P.ctx->stream;
   MapArgs a = map_args(P, src);
+  if (tail_mode) set_tail_args(P, a, tail_mode, k, *prm);
   if (MODE == kMvFinal || MODE == kMvAccel) a.state = nullptr;
   if (fz_out) {
     a.fz = fz_out;
@@ -754,6 +962,28 @@ void enqueue_iteration(SingleProblem& P, int k, const ipt_params& prm, cudaEvent
   Ctx& c = *P.ctx;
   const int src = k & 1;
   LoopState* st = P.state;
+  if (fused_step(P)) {
+    // w_a of z[src]: formed by the previous step's tail, else by the anchor kernel
+    if (!P.wa_fresh) enqueue_anchor(P, src, st);
+    if (ev_a) IPT_CUDA(cudaEventRecord(ev_a, c.stream));
+    enqueue_real_map<kMvMap>(P, src, &prm, nullptr, c.nranks > 1 ? 1 : 2, k);
+    if (ev_b) IPT_CUDA(cudaEventRecord(ev_b, c.stream));
+    P.wa_fresh = true;
+    if (c.nranks > 1) {
+      if (!P.p2p) allgather_z(P, src ^ 1);
+      c.comm->all_reduce(P.sums.get(), 3, CommType::F64, CommOp::Sum, c.stream);
+      c.comm->all_reduce(P.sums.get() + 3, 1, CommType::F64, CommOp::Max, c.stream);
+      MapArgs a = map_args(P, src);
+      set_anchor_args(P, a);
+      decide_anchor_kernel<<<1, 32, 0, c.stream>>>(
+          st, P.sums.get(), k, prm.tolerance, prm.max_iterations, prm.divergence_threshold, prm.schedule,
+          prm.shrink_alpha, 0.25 * prm.tolerance, prm.ignore_convergence,
+          prm.record_trace ? P.trace.get() : nullptr, a);
+      IPT_LAUNCH_CHECK();
+      count_launch();
+    }
+    return;
+  }
   if (!P.cplx) {
     enqueue_anchor(P, src, st);
     if (ev_a) IPT_CUDA(cudaEventRecord(ev_a, c.stream));
@@ -951,6 +1181,12 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
   P->npart = std::max<int64_t>(map_blocks(*P), 1);
   P->partials.alloc(size_t(P->npart) * 4);
   P->sums.alloc(5);  // 4 stop sums + a barrier token (single_reset)
+  {
+    unsigned* cnt = nullptr;
+    IPT_CUDA(cudaMalloc(&cnt, sizeof(unsigned)));
+    IPT_CUDA(cudaMemset(cnt, 0, sizeof(unsigned)));
+    P->tail_counter.reset(cnt);
+  }
   IPT_CUDA(cudaMalloc(&P->state, sizeof(LoopState)));
   c.sync();
   return P.release();
@@ -1013,6 +1249,7 @@ void single_reset(SingleProblem& P, int64_t anchor, const double* warm_re, const
     P.trace_cap = max_iter_hint;
   }
   P.enq = 0;
+  P.wa_fresh = false;
   // Fused all-gather: peers store rows of step 0 into this rank's z[1] (zeroed above) and,
   // across solves, into buffers this rank may still be reading (a previous finalize). A
   // stream-ordered all-reduce here orders every rank's reset (and everything before it)
@@ -1065,6 +1302,7 @@ void single_iterate(SingleProblem& P, const ipt_params& prm, ipt_stats* stats) {
 // Post-loop product, eigenvalue lambda = d_a + (Delta z)_a and residual (solver.cpp:83-91).
 void single_finalize(SingleProblem& P, ipt_stats* stats) {
   Ctx& c = *P.ctx;
+  P.wa_fresh = false;
   cudaStream_t s = c.stream;
   IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
   c.sync();
@@ -1119,6 +1357,7 @@ void single_download(SingleProblem& P, double* z_re, double* z_im) {
 // library stream: the whole sequence and the fused GEMV/SpMV map kernel alone.
 void single_run_steps(SingleProblem& P, int count, double* ms_total, double* ms_map) {
   Ctx& c = *P.ctx;
+  P.wa_fresh = false;
   ipt_params prm;
   ipt_default_params(&prm);
   prm.max_iterations = 0x7fffffff;
@@ -1150,6 +1389,7 @@ void single_run_steps(SingleProblem& P, int count, double* ms_total, double* ms_
 // kernels::matvec on device-resident data: y = Delta x (one pass, no epilogue).
 void single_matvec(SingleProblem& P, const double* x_re, const double* x_im, double* y_re, double* y_im) {
   Ctx& c = *P.ctx;
+  P.wa_fresh = false;
   cudaStream_t s = c.stream;
   const int64_t n = P.n;
   IPT_CUDA(cudaMemcpyAsync(P.z[0].get(), x_re, sizeof(double) * n, cudaMemcpyHostToDevice, s));
@@ -1320,6 +1560,7 @@ bool small_lu_solve(std::vector<double> a, int h, std::vector<double> b, std::ve
 void single_accelerated(SingleProblem& P, const ipt_params& prm, int memory, double residual_tol,
                         double regularization, ipt_stats* stats) {
   Ctx& c = *P.ctx;
+  P.wa_fresh = false;
   if (P.cplx) throw InvalidArgument("solve_single_accelerated (device): real inputs only");
   if (c.nranks != 1) throw InvalidArgument("solve_single_accelerated (device): single GPU only");
   if (memory < 0 || memory > 16) throw InvalidArgument("anderson: memory must lie in [0, 16]");

@@ -37,6 +37,19 @@ def test_config2_n8192():
     _check_columns(r, golden("full_columns.npz"), 8192)
 
 
+@pytest.mark.slow
+def test_config3_max_abs_rule_iterations():
+    """configs[2] under BASELINE's stop rule max|A_new - A_old| < 1e-12, pinned like above."""
+    p = synth.config3()
+    r = ipt.solve_full(p, ipt.build_gaps(p), ipt.IterationConfig(tolerance=1e-12, stop_rule="max_abs",
+                                                                 record_trace=True), want_sigma_min=False)
+    pin = golden("config3_trace.npz")
+    assert r.status == ipt.SolveStatus.Converged and r.final_max_abs < 1e-12
+    assert r.iterations == int(pin["iterations_max_abs"])
+    mx = np.asarray(pin["max_abs"])
+    assert np.allclose(r.trace_max_abs[:3], mx[:3], rtol=1e-6, atol=0)
+
+
 def test_config2_max_abs_rule():
     p = synth.config2()
     r = ipt.solve_full(p, ipt.build_gaps(p), ipt.IterationConfig(tolerance=1e-12, stop_rule="max_abs"),
@@ -51,8 +64,19 @@ def test_config3_n32768(product):
     """configs[2] at full size against 16 columns of the reference's own solve_single(j)
     (tests/golden/full_columns.npz), with either FP64 product (DMMA / Ozaki on tcgen05)."""
     p = synth.config3()
-    r = ipt.solve_full(p, ipt.build_gaps(p), ipt.IterationConfig(tolerance=1e-12), product=product)
+    r = ipt.solve_full(p, ipt.build_gaps(p), ipt.IterationConfig(tolerance=1e-12, record_trace=True),
+                       product=product)
     assert r.status == ipt.SolveStatus.Converged
+    # iteration count pinned against the reference loop (solver.cpp:208-250) run to convergence
+    # on the same inputs (tests/golden/config3_trace.npz, make_config3_trace.py): north_star +-1,
+    # and the step trace agrees iteration by iteration
+    pin = golden("config3_trace.npz")
+    assert abs(r.iterations - int(pin["iterations_rel_fro"])) <= 1
+    assert r.iterations == int(pin["iterations_rel_fro"])
+    steps = np.asarray(pin["steps"])
+    m = min(len(steps), r.iterations)
+    assert np.allclose(r.trace[:m - 1], steps[:m - 1], rtol=1e-6, atol=0)
+    assert 0.5 < r.trace[m - 1] / steps[m - 1] < 2.0  # last step ~1e-14: rounding-level differences
     assert r.residual_frobenius <= 1e-10 * _frob(p)
     assert np.all(np.diag(r.Z) == 1.0)
     assert 0.9 < r.min_singular_value_estimate <= 1.0 + 1e-4

@@ -253,3 +253,20 @@ def test_port_real_dense_single_bitwise_equals_reference(port_arm):
     assert r["iterations"] == int(meta[0]) and r["status"] == int(meta[1])
     assert np.array_equal(r["z"], g["c4_4096_z"])
     assert r["eigenvalue"] == meta[2]
+
+
+def test_config3_iteration_pin_fixture_is_decisive():
+    """tests/golden/config3_trace.npz (make_config3_trace.py: the reference loop restated in
+    numpy at N = 32768 on the reference generator's inputs) decides the iteration count with
+    margin: the step before convergence is >= 10x above tol and the converged step >= 4x below,
+    so summation-order rounding (~1e-16 relative per entry) cannot move the count."""
+    g = golden("config3_trace.npz")
+    assert int(g["n"]) == 32768 and float(g["tol"]) == 1e-12
+    it = int(g["iterations_rel_fro"])
+    steps = np.asarray(g["steps"])
+    assert steps[it - 1] <= 1e-12 < steps[it - 2]
+    assert steps[it - 2] >= 10 * 1e-12 and steps[it - 1] <= 0.25e-12
+    itm = int(g["iterations_max_abs"])
+    mx = np.asarray(g["max_abs"])
+    assert mx[itm - 1] < 1e-12 <= mx[itm - 2]
+    assert np.all(np.diff(np.log10(steps)) < -1.5)  # monotone, geometric convergence

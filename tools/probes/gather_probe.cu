@@ -21,7 +21,19 @@ __device__ __forceinline__ int ld_stream_s32(const int* p) {
   return v;
 }
 
-template <int U, bool GATHER>
+// z gather load flavours: 0 ld.global.nc (L1 allocate), 1 nc + L1::no_allocate, 2 ld.global.cg (L2 only),
+// 3 ld.global.nc + L1::evict_first
+template <int KIND>
+__device__ __forceinline__ double ld_gather(const double* p) {
+  double v;
+  if (KIND == 0) v = __ldg(p);
+  else if (KIND == 1) asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  else if (KIND == 2) asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  else asm volatile("ld.global.nc.L1::evict_first.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+template <int U, bool GATHER, int KIND = 0>
 __global__ void __launch_bounds__(256) probe(const int* __restrict__ cols, const double* __restrict__ vals,
                                              const double* __restrict__ z, int64_t nnz, double* out) {
   double s = 0.0;
@@ -38,7 +50,7 @@ __global__ void __launch_bounds__(256) probe(const int* __restrict__ cols, const
     if (GATHER) {
       double zz[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) zz[u] = __ldg(z + c[u]);
+      for (int u = 0; u < U; ++u) zz[u] = ld_gather<KIND>(z + c[u]);
 #pragma unroll
       for (int u = 0; u < U; ++u) s = fma(v[u], zz[u], s);
     } else {
@@ -50,16 +62,16 @@ __global__ void __launch_bounds__(256) probe(const int* __restrict__ cols, const
   if (s == 1234.5678) out[0] = s;
 }
 
-template <int U, bool G>
+template <int U, bool G, int KIND = 0>
 void run(const char* name, int grid, const int* c, const double* v, const double* z, int64_t nnz, double* out) {
-  probe<U, G><<<grid, 256>>>(c, v, z, nnz, out);
+  probe<U, G, KIND><<<grid, 256>>>(c, v, z, nnz, out);
   cudaDeviceSynchronize();
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const int reps = 10;
   cudaEventRecord(a);
-  for (int r = 0; r < reps; ++r) probe<U, G><<<grid, 256>>>(c, v, z, nnz, out);
+  for (int r = 0; r < reps; ++r) probe<U, G, KIND><<<grid, 256>>>(c, v, z, nnz, out);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms = 0;
@@ -90,6 +102,9 @@ int main() {
     run<4, false>("stream u4", sms * per, c, v, z, nnz, out);
     run<4, true>("gather u4", sms * per, c, v, z, nnz, out);
     run<8, true>("gather u8", sms * per, c, v, z, nnz, out);
+    run<4, true, 1>("gather u4 noalloc", sms * per, c, v, z, nnz, out);
+    run<4, true, 2>("gather u4 cg", sms * per, c, v, z, nnz, out);
+    run<4, true, 3>("gather u4 evict1st", sms * per, c, v, z, nnz, out);
   }
   return 0;
 }
