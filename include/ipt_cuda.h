@@ -130,6 +130,18 @@ int ipt_full_finalize(ipt_ctx* ctx, ipt_full_problem* prob, const ipt_params* pa
 int ipt_full_download(ipt_ctx* ctx, ipt_full_problem* prob, double* z_re, double* z_im,
                       double* lam_re, double* lam_im);
 int ipt_full_local_columns(const ipt_full_problem* prob, int64_t* col_begin, int64_t* col_end);
+/* solve_full in two calls on the C++ carrier's own layout: interleaved complex
+ * (std::complex<double>) d (n), Delta (n x n row-major) and warm start (n x n, nullable).
+ * start: upload (de-interleaved inside the pinned staging pass; the imaginary plane
+ * crosses PCIe only where nonzero and decides the real / complex path), reset and the
+ * iterations; finish: the closing product and sigma_min with Z's download overlapped,
+ * results interleaved into z_c (n x n) and lam_c (n). The caller may prepare the result
+ * arrays while start runs the loop; free the problem with ipt_full_free. */
+int ipt_full_solve_interleaved_start(ipt_ctx* ctx, int64_t n, const double* d_c, const double* delta_c,
+                                     const double* warm_c, const ipt_params* params, ipt_full_problem** out,
+                                     ipt_stats* stats);
+int ipt_full_solve_interleaved_finish(ipt_ctx* ctx, ipt_full_problem* prob, const ipt_params* params, double* z_c,
+                                      double* lam_c, ipt_stats* stats);
 /* Product used by ipt_full_run_maps (the solve calls take ipt_params.product). */
 int ipt_full_set_product(ipt_full_problem* prob, int32_t product);
 /* Moduli the last Ozaki product used (0: not an Ozaki product). With Z_jj = 1 split off,
@@ -273,11 +285,36 @@ int ipt_apply_map_single_dense(ipt_ctx* ctx, int64_t n, const double* d_re, cons
 /* C (m x n) = A (m x k) B (k x n), all row-major; *_im nullable (zero). */
 int ipt_gemm(ipt_ctx* ctx, int64_t m, int64_t k, int64_t n, const double* a_re, const double* a_im,
              const double* b_re, const double* b_im, double* c_re, double* c_im);
+/* The left factor A (m x k row-major planar) of repeated products C = A B kept on the
+ * device (kernels::matmul callers multiplying one A by several B: rspt.cpp:24,
+ * bench.cpp:71, refine.cpp:76/99). */
+typedef struct ipt_gemm_operand ipt_gemm_operand;
+int ipt_gemm_operand_create(ipt_ctx* ctx, int64_t m, int64_t k, const double* a_re, const double* a_im,
+                            ipt_gemm_operand** out);
+/* C (m x n) = A B, B (k x n) row-major planar, *_im nullable. */
+int ipt_gemm_operand_apply(ipt_ctx* ctx, ipt_gemm_operand* a, int64_t n, const double* b_re, const double* b_im,
+                           double* c_re, double* c_im);
+void ipt_gemm_operand_free(ipt_gemm_operand* a);
 int ipt_matvec_dense(ipt_ctx* ctx, int64_t m, int64_t n, const double* a_re, const double* a_im,
                      const double* x_re, const double* x_im, double* y_re, double* y_im);
 int ipt_matvec_csr(ipt_ctx* ctx, int64_t m, int64_t n, const int64_t* rowptr, const int32_t* cols,
                    const double* val_re, const double* val_im, const double* x_re,
                    const double* x_im, double* y_re, double* y_im);
+
+/* ---- device-resident operators: repeated y = A x with one A (kernels::matvec callers
+ * such as the Anderson loop, anderson.cpp:205, and the power iterations of
+ * spectral_norm_estimate, partition.cpp) upload A once. Square n x n, dense row-major
+ * planar or CSR (as ipt_matvec_*); the operator keeps its own device copy. */
+typedef struct ipt_operator ipt_operator;
+int ipt_operator_create_dense(ipt_ctx* ctx, int64_t n, const double* a_re, const double* a_im,
+                              ipt_operator** out);
+int ipt_operator_create_csr(ipt_ctx* ctx, int64_t n, const int64_t* rowptr, const int32_t* cols,
+                            const double* val_re, const double* val_im, ipt_operator** out);
+int ipt_operator_matvec(ipt_ctx* ctx, ipt_operator* op, const double* x_re, const double* x_im,
+                        double* y_re, double* y_im);
+/* Device bytes held by the operator. */
+int64_t ipt_operator_bytes(const ipt_operator* op);
+void ipt_operator_free(ipt_operator* op);
 
 /* ---- measurement hooks (bench.py) ----
  * Enqueue exactly `count` further map applications / single-pair steps on a resident

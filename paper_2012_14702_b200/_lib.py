@@ -85,6 +85,14 @@ SIGNATURES = {
     "ipt_local_group_destroy": (None, [_vp]),
     "ipt_ctx_init_local_comm": (C.c_int, [_vp, _vp, C.c_int]),
     "ipt_ctx_comm_kind": (C.c_char_p, [_vp]),
+    "ipt_operator_create_dense": (C.c_int, [_vp, C.c_int64, _dp, _dp, C.POINTER(_vp)]),
+    "ipt_operator_create_csr": (C.c_int, [_vp, C.c_int64, _i64p, _i32p, _dp, _dp, C.POINTER(_vp)]),
+    "ipt_operator_matvec": (C.c_int, [_vp, _vp, _dp, _dp, _dp, _dp]),
+    "ipt_operator_bytes": (C.c_int64, [_vp]),
+    "ipt_operator_free": (None, [_vp]),
+    "ipt_gemm_operand_create": (C.c_int, [_vp, C.c_int64, C.c_int64, _dp, _dp, C.POINTER(_vp)]),
+    "ipt_gemm_operand_apply": (C.c_int, [_vp, _vp, C.c_int64, _dp, _dp, _dp, _dp]),
+    "ipt_gemm_operand_free": (None, [_vp]),
     "ipt_full_solve": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, C.POINTER(Params),
                                  _dp, _dp, _dp, _dp, C.POINTER(Stats)]),
     "ipt_full_upload": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, _dp, C.POINTER(_vp)]),
@@ -93,6 +101,9 @@ SIGNATURES = {
     "ipt_full_finalize": (C.c_int, [_vp, _vp, C.POINTER(Params), C.POINTER(Stats)]),
     "ipt_full_download": (C.c_int, [_vp, _vp, _dp, _dp, _dp, _dp]),
     "ipt_full_set_product": (C.c_int, [_vp, C.c_int32]),
+    "ipt_full_solve_interleaved_start": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, C.POINTER(Params), C.POINTER(_vp),
+                                                   C.POINTER(Stats)]),
+    "ipt_full_solve_interleaved_finish": (C.c_int, [_vp, _vp, C.POINTER(Params), _dp, _dp, C.POINTER(Stats)]),
     "ipt_full_ozaki_moduli": (C.c_int, [_vp, C.POINTER(C.c_int32)]),
     "ipt_single_debug_peers": (C.c_int, [_vp, C.c_int32]),
     "ipt_single_debug_peer_z": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp]),

@@ -427,6 +427,93 @@ int ipt_full_download(ipt_ctx* ctx, ipt_full_problem* prob, double* z_re, double
   });
 }
 
+int ipt_full_solve_interleaved_start(ipt_ctx* ctx, int64_t n, const double* d_c, const double* delta_c,
+                                     const double* warm_c, const ipt_params* params, ipt_full_problem** out,
+                                     ipt_stats* stats) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (out == nullptr || n <= 0 || d_c == nullptr || delta_c == nullptr) throw InvalidArgument("solve_full: null input");
+    const ipt_params prm = params_or_default(params);
+    if (!(prm.tolerance > 0.0)) throw InvalidArgument("config: tolerance must be positive");
+    if (prm.max_iterations <= 0) throw InvalidArgument("config: max_iterations must be positive");
+    if (!(prm.divergence_threshold > 1.0)) throw InvalidArgument("config: divergence_threshold must exceed 1");
+    Ctx& c = ctx->c;
+    IPT_CUDA(cudaEventRecord(c.ev[2], c.stream));
+    std::vector<double> dre(n), dim(n);
+    for (int64_t i = 0; i < n; ++i) {
+      dre[i] = d_c[2 * i];
+      dim[i] = d_c[2 * i + 1];
+    }
+    // a complex warm start makes the problem complex (solver.cpp:188-201 works in complex)
+    std::vector<double> wre, wim;
+    bool warm_cplx = false;
+    if (warm_c) {
+      wre.resize(size_t(n) * n);
+      wim.resize(size_t(n) * n);
+      for (int64_t t = 0; t < n * n; ++t) {
+        wre[t] = warm_c[2 * t];
+        wim[t] = warm_c[2 * t + 1];
+        warm_cplx = warm_cplx || wim[t] != 0.0;
+      }
+    }
+    std::unique_ptr<FullProblem, void (*)(FullProblem*)> P(
+        full_upload(c, n, dre.data(), dim.data(), nullptr, nullptr, warm_cplx, -1, -1, delta_c), full_free);
+    full_reset(*P, warm_c ? wre.data() : nullptr, warm_c && warm_cplx ? wim.data() : nullptr, prm.max_iterations);
+    IPT_CUDA(cudaEventRecord(c.ev[3], c.stream));
+    c.sync();
+    float ms_up = 0.f;
+    IPT_CUDA(cudaEventElapsedTime(&ms_up, c.ev[2], c.ev[3]));
+    full_iterate(*P, prm, stats);
+    if (stats) stats->ms_upload = ms_up;
+    *out = reinterpret_cast<ipt_full_problem*>(P.release());
+  });
+}
+
+int ipt_full_solve_interleaved_finish(ipt_ctx* ctx, ipt_full_problem* prob, const ipt_params* params, double* z_c,
+                                      double* lam_c, ipt_stats* stats) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    if (prob == nullptr) throw InvalidArgument("solve_full: null problem");
+    const ipt_params prm = params_or_default(params);
+    Ctx& c = ctx->c;
+    FullProblem& P = *reinterpret_cast<FullProblem*>(prob);
+    // one GPU: Z goes to the host on the second stream while the closing product and
+    // sigma_min run (both only read Z)
+    const bool overlap = z_c && full_can_download_early(P);
+    std::future<void> early;
+    float ms_thread = 0.f;
+    if (overlap) {
+      full_prepare_download(P, true, full_is_complex(P));
+      const int dev = c.device;
+      early = std::async(std::launch::async, [&P, dev, z_c, &ms_thread] {
+        IPT_CUDA(cudaSetDevice(dev));
+        const auto t0 = std::chrono::steady_clock::now();
+        full_download_z_interleaved(P, z_c);
+        ms_thread = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      });
+    }
+    try {
+      full_finalize(P, prm, stats);
+    } catch (...) {
+      if (early.valid()) early.wait();
+      throw;
+    }
+    if (overlap) {
+      early.get();
+      full_release_download(P);
+    }
+    IPT_CUDA(cudaEventRecord(c.ev[2], c.stream));
+    full_download_interleaved(P, overlap ? nullptr : z_c, lam_c);
+    IPT_CUDA(cudaEventRecord(c.ev[3], c.stream));
+    c.sync();
+    float ms_down = 0.f;
+    IPT_CUDA(cudaEventElapsedTime(&ms_down, c.ev[2], c.ev[3]));
+    if (stats) stats->ms_download = overlap ? ms_down + ms_thread : ms_down;
+  });
+}
+
 int ipt_full_set_product(ipt_full_problem* prob, int32_t product) {
   if (!prob || (product != IPT_PRODUCT_DMMA && product != IPT_PRODUCT_OZAKI)) return IPT_ERR_INVALID;
   full_set_product(*reinterpret_cast<FullProblem*>(prob), product);
@@ -902,91 +989,156 @@ int ipt_single_run_steps(ipt_ctx* ctx, ipt_single_problem* prob, int32_t count, 
 
 // ------------------------------------------------------------------ kernels::
 
+}  // extern "C"
+
+namespace {
+
+// The left factor of kernels::matmul in the DMMA kernel's layouts, uploaded once:
+//   real A    : R = A (mpad x ldk, rows zero-padded to the 128-row tile, K to 16)
+//   complex A : S = [Ar; Ai] (2m rows) for a real right factor (one 2m x n GEMM), and,
+//               built on the device at the first complex right factor, [Ar | -Ai] and
+//               [Ai | Ar] (K = 2 ldk) for Cr = Ar Br - Ai Bi, Ci = Ai Br + Ar Bi.
+struct GemmOperand {
+  int64_t m = 0, k = 0, ldk = 0;
+  bool cplx = false;
+  DevBuf S, Acat, A2cat;
+  void upload(Ctx& c, int64_t m_, int64_t k_, const double* a_re, const double* a_im) {
+    m = m_;
+    k = k_;
+    ldk = round_up(std::max<int64_t>(k, 1), 16);
+    cplx = any_nonzero(a_im, m * k);
+    S.alloc(size_t(round_up(cplx ? 2 * m : m, kBM)) * ldk);
+    if (k > 0) {
+      h2d_rows(c, S.get(), ldk, a_re, k, m, k);  // pinned, double-buffered
+      if (cplx) h2d_rows(c, S.get() + m * ldk, ldk, a_im, k, m, k);
+    }
+  }
+  void build_cat(Ctx& c) {
+    if (Acat.count) return;
+    cudaStream_t s = c.stream;
+    const int64_t K = 2 * ldk, mpad = round_up(m, kBM);
+    Acat.alloc(size_t(mpad) * K);
+    A2cat.alloc(size_t(mpad) * K);
+    const double* ar = S.get();
+    const double* ai = S.get() + m * ldk;
+    auto put = [&](double* dst, const double* src) {
+      IPT_CUDA(cudaMemcpy2DAsync(dst, K * sizeof(double), src, ldk * sizeof(double), ldk * sizeof(double), m,
+                                 cudaMemcpyDeviceToDevice, s));
+    };
+    put(Acat.get(), ar);
+    put(A2cat.get(), ai);
+    put(A2cat.get() + ldk, ar);
+    DevBuf neg;
+    neg.alloc(size_t(m) * ldk, false);
+    scale_copy(s, ai, neg.get(), size_t(m) * ldk, -1.0);
+    put(Acat.get() + ldk, neg.get());
+    c.sync();
+  }
+  // C (m x n, row-major planar) = A B, B (k x n row-major planar, b_im nullable)
+  void apply(Ctx& c, int64_t n, const double* b_re, const double* b_im, double* c_re, double* c_im) {
+    cudaStream_t s = c.stream;
+    if (m == 0 || n == 0) return;
+    const bool b_cplx = any_nonzero(b_im, k * n);
+    auto up_cols = [&](double* dst, int64_t ld, const double* src) {  // k x n -> column-major
+      if (k > 0) upload_as_colmajor(c, src, k, n, dst, ld);
+    };
+    DevBuf B, C, rm;
+    rm.alloc(size_t(m) * n, false);
+    auto download = [&](const double* src, int64_t ldc, double* dst) {
+      transpose_to_rowmajor(s, src, ldc, m, n, rm.get(), n);
+      d2h_rows(c, dst, n, rm.get(), n, m, n);
+    };
+    if (!cplx && !b_cplx) {  // one real GEMM
+      B.alloc(size_t(round_up(n, kBN)) * ldk);
+      up_cols(B.get(), ldk, b_re);
+      C.alloc(size_t(n) * m, false);
+      gemm_tn_store(s, m, n, ldk, S.get(), ldk, B.get(), ldk, C.get(), m);
+      download(C.get(), m, c_re);
+      if (c_im) std::memset(c_im, 0, sizeof(double) * m * n);
+    } else if (!cplx) {  // real A: A [Br | Bi] as one m x 2n real GEMM
+      B.alloc(size_t(round_up(2 * n, kBN)) * ldk);
+      up_cols(B.get(), ldk, b_re);
+      up_cols(B.get() + n * ldk, ldk, b_im);
+      C.alloc(size_t(2 * n) * m, false);
+      gemm_tn_store(s, m, 2 * n, ldk, S.get(), ldk, B.get(), ldk, C.get(), m);
+      download(C.get(), m, c_re);
+      if (c_im) download(C.get() + n * m, m, c_im);
+    } else if (!b_cplx) {  // real B: [Ar; Ai] B as one 2m x n real GEMM
+      B.alloc(size_t(round_up(n, kBN)) * ldk);
+      up_cols(B.get(), ldk, b_re);
+      C.alloc(size_t(n) * 2 * m, false);
+      gemm_tn_store(s, 2 * m, n, ldk, S.get(), ldk, B.get(), ldk, C.get(), 2 * m);
+      download(C.get(), 2 * m, c_re);
+      if (c_im) download(C.get() + m, 2 * m, c_im);
+    } else {  // both complex: [Ar | -Ai][Br; Bi] and [Ai | Ar][Br; Bi] (K = 2 ldk)
+      build_cat(c);
+      const int64_t K = 2 * ldk;
+      B.alloc(size_t(round_up(n, kBN)) * K);
+      up_cols(B.get(), K, b_re);
+      up_cols(B.get() + ldk, K, b_im);
+      C.alloc(size_t(n) * m, false);
+      gemm_tn_store(s, m, n, K, Acat.get(), K, B.get(), K, C.get(), m);
+      download(C.get(), m, c_re);
+      if (c_im) {
+        gemm_tn_store(s, m, n, K, A2cat.get(), K, B.get(), K, C.get(), m);
+        download(C.get(), m, c_im);
+      }
+    }
+  }
+};
+
+}  // namespace
+
+struct ipt_gemm_operand {
+  GemmOperand A;
+  ipt_ctx* ctx = nullptr;
+  int device = 0;
+};
+
+extern "C" {
+
 int ipt_gemm(ipt_ctx* ctx, int64_t m, int64_t k, int64_t n, const double* a_re, const double* a_im,
              const double* b_re, const double* b_im, double* c_re, double* c_im) {
   return guarded([&] {
     check_ctx(ctx);
     DeviceGuard g(ctx->c.device);
     if (m < 0 || k < 0 || n < 0) throw InvalidArgument("matmul: negative shape");
-    Ctx& c = ctx->c;
-    cudaStream_t s = c.stream;
     if (m == 0 || n == 0) return;
-    bool a_cplx = false, b_cplx = false;
-    if (a_im) for (int64_t t = 0; t < m * k && !a_cplx; ++t) a_cplx = a_im[t] != 0.0;
-    if (b_im) for (int64_t t = 0; t < k * n && !b_cplx; ++t) b_cplx = b_im[t] != 0.0;
-    const int64_t ldk = round_up(std::max<int64_t>(k, 1), 16);
-    auto up_rows = [&](double* dst, int64_t dpitch, const double* src) {  // m x k row-major
-      if (k > 0) h2d_rows(c, dst, dpitch, src, k, m, k);  // pinned, double-buffered
-    };
-    auto up_cols = [&](double* dst, int64_t ld, const double* src) {  // k x n -> column-major
-      if (k > 0) upload_as_colmajor(c, src, k, n, dst, ld);
-    };
-    DevBuf A, B, C, rm;
-    rm.alloc(size_t(m) * n, false);
-    auto download = [&](const double* src, int64_t ldc, double* dst) {
-      transpose_to_rowmajor(s, src, ldc, m, n, rm.get(), n);
-      d2h_rows(c, dst, n, rm.get(), n, m, n);
-    };
-    if (!a_cplx && !b_cplx) {  // one real GEMM
-      A.alloc(size_t(round_up(m, kBM)) * ldk);
-      B.alloc(size_t(round_up(n, kBN)) * ldk);
-      up_rows(A.get(), ldk, a_re);
-      up_cols(B.get(), ldk, b_re);
-      C.alloc(size_t(n) * m, false);
-      gemm_tn_store(s, m, n, ldk, A.get(), ldk, B.get(), ldk, C.get(), m);
-      download(C.get(), m, c_re);
-      if (c_im) std::memset(c_im, 0, sizeof(double) * m * n);
-    } else if (!a_cplx) {  // real A: A [Br | Bi] as one m x 2n real GEMM
-      A.alloc(size_t(round_up(m, kBM)) * ldk);
-      B.alloc(size_t(round_up(2 * n, kBN)) * ldk);
-      up_rows(A.get(), ldk, a_re);
-      up_cols(B.get(), ldk, b_re);
-      up_cols(B.get() + n * ldk, ldk, b_im);
-      C.alloc(size_t(2 * n) * m, false);
-      gemm_tn_store(s, m, 2 * n, ldk, A.get(), ldk, B.get(), ldk, C.get(), m);
-      download(C.get(), m, c_re);
-      if (c_im) download(C.get() + n * m, m, c_im);
-    } else if (!b_cplx) {  // real B: [Ar; Ai] B as one 2m x n real GEMM
-      A.alloc(size_t(round_up(2 * m, kBM)) * ldk);
-      B.alloc(size_t(round_up(n, kBN)) * ldk);
-      up_rows(A.get(), ldk, a_re);
-      up_rows(A.get() + m * ldk, ldk, a_im);
-      up_cols(B.get(), ldk, b_re);
-      C.alloc(size_t(n) * 2 * m, false);
-      gemm_tn_store(s, 2 * m, n, ldk, A.get(), ldk, B.get(), ldk, C.get(), 2 * m);
-      download(C.get(), 2 * m, c_re);
-      if (c_im) download(C.get() + m, 2 * m, c_im);
-    } else {  // both complex: Cr = [Ar | -Ai][Br; Bi], Ci = [Ai | Ar][Br; Bi] (K = 2 ldk)
-      const int64_t K = 2 * ldk;
-      const int64_t mpad = round_up(m, kBM);
-      DevBuf A2;
-      A.alloc(size_t(mpad) * K);
-      A2.alloc(size_t(mpad) * K);
-      B.alloc(size_t(round_up(n, kBN)) * K);
-      up_rows(A.get(), K, a_re);
-      up_rows(A2.get() + ldk, K, a_re);
-      up_rows(A2.get(), K, a_im);
-      {
-        DevBuf tmp;
-        tmp.alloc(size_t(m) * std::max<int64_t>(k, 1), false);
-        if (k > 0) h2d_rows(c, tmp.get(), k, a_im, k, m, k);
-        scale_copy(s, tmp.get(), tmp.get(), size_t(m) * k, -1.0);
-        if (k > 0)
-          IPT_CUDA(cudaMemcpy2DAsync(A.get() + ldk, K * sizeof(double), tmp.get(), k * sizeof(double),
-                                     k * sizeof(double), m, cudaMemcpyDeviceToDevice, s));
-        c.sync();
-      }
-      up_cols(B.get(), K, b_re);
-      up_cols(B.get() + ldk, K, b_im);
-      C.alloc(size_t(n) * m, false);
-      gemm_tn_store(s, m, n, K, A.get(), K, B.get(), K, C.get(), m);
-      download(C.get(), m, c_re);
-      if (c_im) {
-        gemm_tn_store(s, m, n, K, A2.get(), K, B.get(), K, C.get(), m);
-        download(C.get(), m, c_im);
-      }
-    }
+    GemmOperand A;
+    A.upload(ctx->c, m, k, a_re, a_im);
+    A.apply(ctx->c, n, b_re, b_im, c_re, c_im);
   });
+}
+
+int ipt_gemm_operand_create(ipt_ctx* ctx, int64_t m, int64_t k, const double* a_re, const double* a_im,
+                            ipt_gemm_operand** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (out == nullptr || m <= 0 || k < 0 || a_re == nullptr) throw InvalidArgument("gemm operand: bad arguments");
+    DeviceGuard g(ctx->c.device);
+    auto h = std::make_unique<ipt_gemm_operand>();
+    h->A.upload(ctx->c, m, k, a_re, a_im);
+    h->ctx = ctx;
+    h->device = ctx->c.device;
+    *out = h.release();
+  });
+}
+
+int ipt_gemm_operand_apply(ipt_ctx* ctx, ipt_gemm_operand* a, int64_t n, const double* b_re, const double* b_im,
+                           double* c_re, double* c_im) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (a == nullptr || a->ctx != ctx) throw InvalidArgument("gemm operand: belongs to another context");
+    if (n < 0) throw InvalidArgument("matmul: negative shape");
+    DeviceGuard g(ctx->c.device);
+    a->A.apply(ctx->c, n, b_re, b_im, c_re, c_im);
+  });
+}
+
+void ipt_gemm_operand_free(ipt_gemm_operand* a) {
+  if (!a) return;
+  DeviceGuard g(a->device);
+  delete a;
 }
 
 int ipt_matvec_dense(ipt_ctx* ctx, int64_t m, int64_t n, const double* a_re, const double* a_im,
@@ -1020,6 +1172,69 @@ int ipt_matvec_csr(ipt_ctx* ctx, int64_t m, int64_t n, const int64_t* rowptr, co
         single_free);
     single_matvec(*P, x_re, x_im, y_re, y_im);
   });
+}
+
+struct ipt_operator {
+  SingleProblem* P = nullptr;
+  ipt_ctx* ctx = nullptr;  // the creating context (matvec must use it); free needs only the device
+  int device = 0;
+  int64_t bytes = 0;
+};
+
+int ipt_operator_create_dense(ipt_ctx* ctx, int64_t n, const double* a_re, const double* a_im,
+                              ipt_operator** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (out == nullptr || n <= 0 || a_re == nullptr) throw InvalidArgument("operator: bad arguments");
+    if (ctx->c.nranks != 1) throw InvalidArgument("operator: single-rank context required");
+    DeviceGuard g(ctx->c.device);
+    std::vector<double> dz(size_t(n), 0.0);
+    auto* op = new ipt_operator();
+    op->P = single_upload(ctx->c, n, dz.data(), nullptr, false, a_re, a_im, nullptr, nullptr, nullptr, nullptr, true);
+    single_forget_host(*op->P);
+    op->ctx = ctx;
+    op->device = ctx->c.device;
+    op->bytes = int64_t(round_up(n, 16)) * n * (any_nonzero(a_im, n * n) ? 16 : 8);
+    *out = op;
+  });
+}
+
+int ipt_operator_create_csr(ipt_ctx* ctx, int64_t n, const int64_t* rowptr, const int32_t* cols,
+                            const double* val_re, const double* val_im, ipt_operator** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (out == nullptr || n <= 0 || rowptr == nullptr) throw InvalidArgument("operator: bad arguments");
+    if (ctx->c.nranks != 1) throw InvalidArgument("operator: single-rank context required");
+    DeviceGuard g(ctx->c.device);
+    std::vector<double> dz(size_t(n), 0.0);
+    auto* op = new ipt_operator();
+    op->P = single_upload(ctx->c, n, dz.data(), nullptr, true, nullptr, nullptr, rowptr, cols, val_re, val_im, true);
+    single_forget_host(*op->P);
+    op->ctx = ctx;
+    op->device = ctx->c.device;
+    const int64_t nnz = rowptr[n] - rowptr[0];
+    op->bytes = nnz * (val_im ? 20 : 12) + 8 * (n + 1);
+    *out = op;
+  });
+}
+
+int ipt_operator_matvec(ipt_ctx* ctx, ipt_operator* op, const double* x_re, const double* x_im, double* y_re,
+                        double* y_im) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (op == nullptr || op->ctx != ctx) throw InvalidArgument("operator: belongs to another context");
+    DeviceGuard g(ctx->c.device);
+    single_matvec(*op->P, x_re, x_im, y_re, y_im);
+  });
+}
+
+int64_t ipt_operator_bytes(const ipt_operator* op) { return op ? op->bytes : 0; }
+
+void ipt_operator_free(ipt_operator* op) {
+  if (!op) return;
+  DeviceGuard g(op->device);
+  single_free(op->P);
+  delete op;
 }
 
 }  // extern "C"

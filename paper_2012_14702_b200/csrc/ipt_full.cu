@@ -820,9 +820,9 @@ static void column_block(const Ctx& c, int64_t n, int64_t begin, int64_t end, in
 
 FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_im,
                          const double* delta_re, const double* delta_im, bool force_complex,
-                         int64_t col_begin, int64_t col_end) {
+                         int64_t col_begin, int64_t col_end, const double* delta_c) {
   if (n <= 0) throw InvalidArgument("solve_full: empty problem");
-  if (!d_re || !delta_re) throw InvalidArgument("solve_full: null input");
+  if (!d_re || !(delta_re || delta_c)) throw InvalidArgument("solve_full: null input");
   auto P = std::make_unique<FullProblem>();
   P->ctx = &c;
   P->n = n;
@@ -836,21 +836,61 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
   P->cols_pad = round_up(std::max<int64_t>(P->ncols, 1), kBN);
   bool any_im = false;
   if (d_im) for (int64_t i = 0; i < n && !any_im; ++i) any_im = d_im[i] != 0.0;
-  if (delta_im) for (int64_t t = 0; t < n * n && !any_im; ++t) any_im = delta_im[t] != 0.0;
+  if (delta_im && !delta_c) for (int64_t t = 0; t < n * n && !any_im; ++t) any_im = delta_im[t] != 0.0;
   P->cplx = any_im || force_complex;
   P->lda = P->ld;                          // K of every real GEMM
-  P->ldz = P->cplx ? 2 * P->ld : P->ld;    // Z columns: [re] or [re; im]
   cudaStream_t s = c.stream;
 
   ProfMarks pm("full_upload");
+  if (delta_c) {
+    // Interleaved complex Delta (the C++ carrier): de-interleaved in the staging pass; the
+    // imaginary plane crosses PCIe only where it is nonzero, and decides the path. With a
+    // communicator each rank sends its slice of rows and the planes are all-gathered.
+    const int64_t up_chunk = c.nranks > 1 ? ceil_div(P->rows_pad, int64_t(c.nranks)) : P->rows_pad;
+    const size_t cap = size_t(std::max(P->rows_pad, up_chunk * c.nranks)) * P->lda;
+    P->A1.alloc(cap);
+    P->A2.alloc(cap);
+    const int64_t r0 = std::min<int64_t>(n, c.rank * up_chunk), r1 = std::min<int64_t>(n, (c.rank + 1) * up_chunk);
+    bool im_sent = false;
+    if (r1 > r0)
+      h2d_rows_split(c, P->A1.get() + r0 * P->lda, P->A2.get() + r0 * P->lda, P->lda, delta_c + 2 * r0 * n,
+                     r1 - r0, n, &im_sent);
+    int flag = (im_sent || P->cplx) ? 1 : 0;
+    if (c.nranks > 1) {
+      DevBuf f;
+      f.alloc(1);
+      int* df = reinterpret_cast<int*>(f.get());
+      IPT_CUDA(cudaMemcpyAsync(df, &flag, sizeof(int), cudaMemcpyHostToDevice, s));
+      c.comm->all_reduce(df, 1, CommType::I32, CommOp::Max, s);
+      IPT_CUDA(cudaMemcpyAsync(&flag, df, sizeof(int), cudaMemcpyDeviceToHost, s));
+      c.sync();
+      c.comm->all_gather(P->A1.get(), size_t(up_chunk * P->lda), CommType::F64, s);
+      if (flag) c.comm->all_gather(P->A2.get(), size_t(up_chunk * P->lda), CommType::F64, s);
+    }
+    P->cplx = flag != 0;
+    if (!P->cplx) {
+      P->A2.release();
+    } else {
+      P->A3.alloc(cap, false);
+      add_planes_kernel<<<1184, 256, 0, s>>>(P->A1.get(), P->A2.get(), P->A3.get(), int64_t(P->rows_pad) * P->lda);
+      IPT_LAUNCH_CHECK();
+      count_launch();
+    }
+    pm.mark("h2d_split");
+  }
+  P->ldz = P->cplx ? 2 * P->ld : P->ld;    // Z columns: [re] or [re; im]
   // With a communicator every rank passes the same Delta (replicated); each uploads only
   // its 1/g slice of rows over PCIe and an in-place NCCL all-gather over NVLink assembles
   // the whole matrix on every GPU (g x less host traffic than g full uploads).
   const bool sharded_upload = c.nranks > 1 && !P->cplx;
   const int64_t up_chunk = ceil_div(P->rows_pad, int64_t(c.nranks));
-  P->A1.alloc(size_t(sharded_upload ? std::max(P->rows_pad, up_chunk * c.nranks) : P->rows_pad) * P->lda);
-  pm.mark("alloc_delta");
-  if (sharded_upload) {
+  if (!delta_c) {
+    P->A1.alloc(size_t(sharded_upload ? std::max(P->rows_pad, up_chunk * c.nranks) : P->rows_pad) * P->lda);
+    pm.mark("alloc_delta");
+  }
+  if (delta_c) {
+    // (uploaded above)
+  } else if (sharded_upload) {
     const int64_t r0 = std::min<int64_t>(n, c.rank * up_chunk), r1 = std::min<int64_t>(n, (c.rank + 1) * up_chunk);
     if (r1 > r0) h2d_rows(c, P->A1.get() + r0 * P->lda, P->lda, delta_re + r0 * n, n, r1 - r0, n);
     c.comm->all_gather(P->A1.get(), size_t(up_chunk * P->lda), CommType::F64, s);
@@ -1232,16 +1272,13 @@ void full_download_block(FullProblem& P, double* z_re, double* z_im, double* lam
   }
 }
 
-// Z (row-major planar) and eigenvalues to the host; rank 0 receives everything.
-void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, double* lam_im) {
+// Eigenvalues of every rank's columns on rank 0 (lam computed in finalize).
+static void gather_eigenvalues(FullProblem& P, std::vector<double>& lr, std::vector<double>& li) {
   Ctx& c = *P.ctx;
-  if (c.nranks == 1 && P.ncols != P.n) throw InvalidArgument("download: column block problem (use the block download)");
   cudaStream_t s = c.stream;
-  IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
-  c.sync();
   const int64_t n = P.n;
-  // eigenvalues: gather per-rank blocks (lam computed in finalize)
-  std::vector<double> lr(n, 0.0), li(n, 0.0);
+  lr.assign(n, 0.0);
+  li.assign(n, 0.0);
   if (c.nranks > 1) {
     DevBuf all_r, all_i;
     all_r.alloc(n);
@@ -1264,6 +1301,18 @@ void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, d
     IPT_CUDA(cudaMemcpyAsync(li.data(), P.lami.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
     c.sync();
   }
+}
+
+// Z (row-major planar) and eigenvalues to the host; rank 0 receives everything.
+void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, double* lam_im) {
+  Ctx& c = *P.ctx;
+  if (c.nranks == 1 && P.ncols != P.n) throw InvalidArgument("download: column block problem (use the block download)");
+  cudaStream_t s = c.stream;
+  IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
+  c.sync();
+  const int64_t n = P.n;
+  std::vector<double> lr, li;
+  gather_eigenvalues(P, lr, li);
   if (c.rank != 0) return;
   if (lam_re) std::memcpy(lam_re, lr.data(), sizeof(double) * n);
   if (lam_im) {
@@ -1326,6 +1375,44 @@ void full_download_z(FullProblem& P, double* z_re, double* z_im) {
     if (P.rm_ptr[part] == nullptr) throw InvalidArgument("download: prepare must run first");
     d2h_rows(c, dst, n, P.rm_ptr[part], n, n, n, c.stream2);
   }
+  IPT_CUDA(cudaStreamSynchronize(c.stream2));
+}
+
+// The same downloads into interleaved complex host arrays (the C++ carrier's layout).
+void full_download_interleaved(FullProblem& P, double* z_c, double* lam_c) {
+  Ctx& c = *P.ctx;
+  if (c.nranks == 1 && P.ncols != P.n) throw InvalidArgument("download: column block problem (use the block download)");
+  cudaStream_t s = c.stream;
+  IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
+  c.sync();
+  const int64_t n = P.n;
+  std::vector<double> lr, li;
+  gather_eigenvalues(P, lr, li);
+  if (c.rank != 0) return;
+  if (lam_c)
+    for (int64_t j = 0; j < n; ++j) {
+      lam_c[2 * j] = lr[j];
+      lam_c[2 * j + 1] = P.cplx ? li[j] : 0.0;
+    }
+  if (z_c == nullptr) return;
+  const double* zsrc = c.nranks > 1 ? P.gathered.get() : final_colmajor_z(P);
+  if (zsrc == nullptr) throw InvalidArgument("download: finalize must run before download");
+  DevBuf rre, rim;
+  rre.alloc(size_t(n) * n, false);
+  transpose_to_rowmajor(s, zsrc, P.ldz, n, n, rre.get(), n);
+  if (P.cplx) {
+    rim.alloc(size_t(n) * n, false);
+    transpose_to_rowmajor(s, zsrc + P.ld, P.ldz, n, n, rim.get(), n);
+  }
+  d2h_rows_merge(c, z_c, rre.get(), P.cplx ? rim.get() : nullptr, n, n, n);
+}
+
+// Early (overlapped) download after full_prepare_download(P, true, P.cplx), on stream2.
+void full_download_z_interleaved(FullProblem& P, double* z_c) {
+  Ctx& c = *P.ctx;
+  if (P.rm_ptr[0] == nullptr || (P.cplx && P.rm_ptr[1] == nullptr))
+    throw InvalidArgument("download: prepare must run first");
+  d2h_rows_merge(c, z_c, P.rm_ptr[0], P.cplx ? P.rm_ptr[1] : nullptr, P.n, P.n, P.n, c.stream2);
   IPT_CUDA(cudaStreamSynchronize(c.stream2));
 }
 

@@ -133,12 +133,23 @@ void h2d_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t sp
 void d2h_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t rows,
               int64_t cols, cudaStream_t s = nullptr);
 void release_staging(Ctx& c);
+// The same for interleaved complex host rows (std::complex<double>) <-> planar device rows
+// (the C++ carrier's layout, converted inside the staging pass).
+void h2d_rows_split(Ctx& c, double* dre, double* dim, int64_t dpitch, const double* src_c, int64_t rows,
+                    int64_t cols, bool* any_im);
+void d2h_rows_merge(Ctx& c, double* dst_c, const double* sre, const double* sim, int64_t spitch, int64_t rows,
+                    int64_t cols, cudaStream_t s = nullptr);
 
 // Full-spectrum problem (ipt_full.cu)
 struct FullProblem;
+// delta_c (nullable): Delta as interleaved complex rows (std::complex<double>, n x n);
+// delta_re / delta_im are then ignored and the path (real / complex) follows its contents.
 FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_im,
                          const double* delta_re, const double* delta_im, bool force_complex = false,
-                         int64_t col_begin = -1, int64_t col_end = -1);
+                         int64_t col_begin = -1, int64_t col_end = -1, const double* delta_c = nullptr);
+// Z (row-major, interleaved complex, n x n) and the eigenvalues (interleaved, n) on rank 0.
+void full_download_interleaved(FullProblem& P, double* z_c, double* lam_c);
+void full_download_z_interleaved(FullProblem& P, double* z_c);
 FullProblem* full_upload_csr(Ctx& c, int64_t n, const double* d, const int64_t* rowptr,
                              const int32_t* cols, const double* vals, int64_t col_begin = -1,
                              int64_t col_end = -1);
@@ -171,6 +182,9 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
                              bool keep_host_anchor_source, bool force_complex = false, int64_t row_begin = -1,
                              int64_t row_end = -1);
 void single_debug_peers(SingleProblem& P, int npeers);
+// Drop the references to the caller's host arrays kept for anchor uploads (resident
+// operators never set an anchor; the arrays may be freed after the upload).
+void single_forget_host(SingleProblem& P);
 void single_debug_peer_z(SingleProblem& P, int peer, int buf, double* out);
 void single_free(SingleProblem* P);
 void single_reset(SingleProblem& P, int64_t anchor, const double* warm_re, const double* warm_im,

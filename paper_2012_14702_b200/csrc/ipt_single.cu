@@ -1066,6 +1066,12 @@ void setup_peer_gather(SingleProblem& P, int64_t zlen) {
 
 }  // namespace
 
+void single_forget_host(SingleProblem& P) {
+  P.h_dense = P.h_densei = nullptr;
+  P.h_cols = nullptr;
+  P.h_vals = P.h_valsi = nullptr;
+}
+
 // Tests on one GPU: npeers local buffer pairs stand in for the peers' z (the map kernel
 // stores its rows into them exactly as into IPC-mapped peer memory).
 void single_debug_peers(SingleProblem& P, int npeers) {

@@ -1,11 +1,14 @@
 // Small device utilities: buffers, transposes, deterministic partial reduction.
 #include <algorithm>
+#include <atomic>
 #include <sys/mman.h>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <condition_variable>
+#include <functional>
 #include <thread>
 #include <vector>
 
@@ -113,27 +116,115 @@ unsigned copy_threads() {
   return std::max(1u, std::min(16u, h ? h : 8u));
 }
 
-// rows x cols doubles between two pitched host arrays, split over host threads
-void host_copy_rows(double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t rows, int64_t cols) {
-  const unsigned t = rows * cols >= (int64_t(1) << 18) ? copy_threads() : 1u;
-  auto work = [&](int64_t r0, int64_t r1) {
-    if (dpitch == cols && spitch == cols) {
-      std::memcpy(dst + r0 * dpitch, src + r0 * spitch, sizeof(double) * (r1 - r0) * cols);
-    } else {
-      for (int64_t r = r0; r < r1; ++r) std::memcpy(dst + r * dpitch, src + r * spitch, sizeof(double) * cols);
+// Persistent host workers for the staged copies (a pool instead of std::thread per
+// 64 MB chunk: spawning 16 threads per chunk cost ~8 ms per GB moved).
+class HostPool {
+ public:
+  explicit HostPool(unsigned n) {
+    for (unsigned i = 1; i < n; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
     }
-  };
-  if (t <= 1 || rows < int64_t(t)) {
-    work(0, rows);
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  unsigned size() const { return static_cast<unsigned>(workers_.size()) + 1; }
+  // f(k) for k in [0, parts), the calling thread taking part; returns when all are done.
+  // One job at a time (callers serialise on run_mu_).
+  void run(unsigned parts, const std::function<void(unsigned)>& f) {
+    std::lock_guard<std::mutex> run_lk(run_mu_);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &f;
+      parts_ = parts;
+      next_ = 0;
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [this] { return done_ == parts_; });
+    job_ = nullptr;
+  }
+
+ private:
+  void work() {
+    while (true) {
+      unsigned k;
+      const std::function<void(unsigned)>* f;
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (job_ == nullptr || next_ >= parts_) return;
+        k = next_++;
+        f = job_;
+      }
+      (*f)(k);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (++done_ == parts_) done_cv_.notify_all();
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    while (true) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || (gen_ != seen && job_ != nullptr); });
+        if (stop_) return;
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, run_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(unsigned)>* job_ = nullptr;
+  unsigned parts_ = 0, next_ = 0, done_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+HostPool& host_pool() {
+  static HostPool pool(copy_threads());
+  return pool;
+}
+
+// rows x cols doubles between two pitched host arrays, split over the host workers (by
+// bytes: a contiguous block is one flat range, otherwise whole rows, or column slices of
+// the rows when there are fewer rows than workers).
+void host_copy_rows(double* dst, int64_t dpitch, const double* src, int64_t spitch, int64_t rows, int64_t cols) {
+  const int64_t total = rows * cols;
+  const unsigned t = total >= (int64_t(1) << 18) ? host_pool().size() : 1u;
+  if (t <= 1) {
+    for (int64_t r = 0; r < rows; ++r) std::memcpy(dst + r * dpitch, src + r * spitch, sizeof(double) * cols);
     return;
   }
-  std::vector<std::thread> pool;
-  const int64_t step = (rows + t - 1) / t;
-  for (unsigned k = 0; k < t; ++k) {
-    const int64_t a = k * step, b = std::min(rows, a + step);
-    if (a < b) pool.emplace_back(work, a, b);
+  if (dpitch == cols && spitch == cols) {
+    const int64_t step = (total + t - 1) / t;
+    host_pool().run(t, [&](unsigned k) {
+      const int64_t a = int64_t(k) * step, b = std::min(total, a + step);
+      if (a < b) std::memcpy(dst + a, src + a, sizeof(double) * (b - a));
+    });
+    return;
   }
-  for (auto& th : pool) th.join();
+  if (rows >= int64_t(t)) {
+    const int64_t step = (rows + t - 1) / t;
+    host_pool().run(t, [&](unsigned k) {
+      const int64_t a = int64_t(k) * step, b = std::min(rows, a + step);
+      for (int64_t r = a; r < b; ++r) std::memcpy(dst + r * dpitch, src + r * spitch, sizeof(double) * cols);
+    });
+    return;
+  }
+  const int64_t step = (cols + t - 1) / t;
+  host_pool().run(t, [&](unsigned k) {
+    const int64_t a = int64_t(k) * step, b = std::min(cols, a + step);
+    if (a < b)
+      for (int64_t r = 0; r < rows; ++r) std::memcpy(dst + r * dpitch + a, src + r * spitch + a, sizeof(double) * (b - a));
+  });
 }
 // Large host destinations (a fresh n x n result array) are first-touched here in
 // parallel: transparent huge pages requested for the range, then every page touched
@@ -154,17 +245,12 @@ void prefault_host_destination(double* dst, size_t bytes) {
   const uintptr_t p1 = (reinterpret_cast<uintptr_t>(dst) + bytes) & ~(page - 1);
   if (p1 <= p0) return;
   const size_t span = ((p1 - p0) / t + huge - 1) & ~(huge - 1);
-  std::vector<std::thread> pool;
-  for (unsigned k = 0; k < t; ++k) {
+  // one store per 4 KB page (with THP, one fault per 2 MB); measured faster than
+  // MADV_POPULATE_WRITE, which the kernel serialises
+  host_pool().run(t, [&](unsigned k) {
     const uintptr_t a = p0 + k * span, b = std::min<uintptr_t>(p1, a + span);
-    if (a >= b) break;
-    // one store per 4 KB page (with THP, one fault per 2 MB); measured faster than
-    // MADV_POPULATE_WRITE, which the kernel serialises
-    pool.emplace_back([a, b, page] {
-      for (uintptr_t q = a; q < b; q += page) *reinterpret_cast<volatile char*>(q) = 0;
-    });
-  }
-  for (auto& th : pool) th.join();
+    for (uintptr_t q = a; q < b; q += page) *reinterpret_cast<volatile char*>(q) = 0;
+  });
 }
 
 }  // namespace
@@ -299,6 +385,105 @@ void d2h_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t sp
     std::fprintf(stderr, "[ipt] d2h_rows %.2f GB: %.1f ms (prefault %.1f, host copy %.1f, DMA wait %.1f, %u threads)\n",
                  8e-9 * double(rows) * double(cols), 1e3 * (now() - t_start), 1e3 * t_fault, 1e3 * t_copy,
                  1e3 * t_wait, copy_threads());
+}
+
+// Interleaved complex host rows (the C++ carrier, std::complex<double>) to planar device
+// rows: the host workers de-interleave each chunk into the pinned staging buffer (real
+// plane in its first half, imaginary plane in the second) while checking the imaginary
+// parts; the imaginary plane of a chunk is sent only when it holds a nonzero (dim is
+// zeroed by the caller). *any_im reports whether any was sent.
+void h2d_rows_split(Ctx& c, double* dre, double* dim, int64_t dpitch, const double* src_c, int64_t rows,
+                    int64_t cols, bool* any_im) {
+  *any_im = false;
+  if (rows <= 0 || cols <= 0) return;
+  cudaStream_t st = c.stream;
+  ensure_staging(c);
+  const int64_t half = static_cast<int64_t>(c.stage_doubles) / 2;
+  const int64_t per = half / cols;
+  if (per < 1) throw InvalidArgument("h2d_rows_split: row longer than the staging buffer");
+  int b = 0;
+  bool used[2] = {false, false};
+  std::atomic<bool> chunk_im{false};
+  for (int64_t r0 = 0; r0 < rows; r0 += per, b ^= 1) {
+    const int64_t nr = std::min(per, rows - r0);
+    if (used[b]) IPT_CUDA(cudaEventSynchronize(c.stage_ev[b]));
+    double* re = c.stage[b];
+    double* im = c.stage[b] + half;
+    const double* s0 = src_c + 2 * r0 * cols;
+    const int64_t total = nr * cols;
+    chunk_im.store(false, std::memory_order_relaxed);
+    const unsigned t = total >= (int64_t(1) << 16) ? host_pool().size() : 1u;
+    const int64_t step = (total + t - 1) / t;
+    auto work = [&](unsigned k) {
+      const int64_t a = int64_t(k) * step, e = std::min(total, a + step);
+      bool nz = false;
+      for (int64_t q = a; q < e; ++q) {
+        re[q] = s0[2 * q];
+        im[q] = s0[2 * q + 1];
+        nz = nz || s0[2 * q + 1] != 0.0;
+      }
+      if (nz) chunk_im.store(true, std::memory_order_relaxed);
+    };
+    if (t <= 1) work(0);
+    else host_pool().run(t, work);
+    IPT_CUDA(cudaMemcpy2DAsync(dre + r0 * dpitch, dpitch * sizeof(double), re, cols * sizeof(double),
+                               cols * sizeof(double), nr, cudaMemcpyHostToDevice, st));
+    if (chunk_im.load()) {
+      *any_im = true;
+      IPT_CUDA(cudaMemcpy2DAsync(dim + r0 * dpitch, dpitch * sizeof(double), im, cols * sizeof(double),
+                                 cols * sizeof(double), nr, cudaMemcpyHostToDevice, st));
+    }
+    IPT_CUDA(cudaEventRecord(c.stage_ev[b], st));
+    used[b] = true;
+  }
+  IPT_CUDA(cudaStreamSynchronize(st));
+}
+
+// Planar device rows to interleaved complex host rows (sim == nullptr: imaginary parts 0),
+// the host workers interleaving out of the pinned staging buffer while the next chunk's
+// DMA runs.
+void d2h_rows_merge(Ctx& c, double* dst_c, const double* sre, const double* sim, int64_t spitch, int64_t rows,
+                    int64_t cols, cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0) return;
+  cudaStream_t st = stream ? stream : c.stream;
+  ensure_staging(c);
+  const int64_t half = static_cast<int64_t>(c.stage_doubles) / 2;
+  const int64_t per = half / cols;
+  if (per < 1) throw InvalidArgument("d2h_rows_merge: row longer than the staging buffer");
+  const int64_t nchunks = (rows + per - 1) / per;
+  auto issue = [&](int64_t k) {
+    const int64_t r0 = k * per, nr = std::min(per, rows - r0);
+    const int b = static_cast<int>(k & 1);
+    IPT_CUDA(cudaMemcpy2DAsync(c.stage[b], cols * sizeof(double), sre + r0 * spitch, spitch * sizeof(double),
+                               cols * sizeof(double), nr, cudaMemcpyDeviceToHost, st));
+    if (sim)
+      IPT_CUDA(cudaMemcpy2DAsync(c.stage[b] + half, cols * sizeof(double), sim + r0 * spitch,
+                                 spitch * sizeof(double), cols * sizeof(double), nr, cudaMemcpyDeviceToHost, st));
+    IPT_CUDA(cudaEventRecord(c.stage_ev[b], st));
+  };
+  issue(0);
+  for (int64_t k = 0; k < nchunks; ++k) {
+    if (k + 1 < nchunks) issue(k + 1);
+    const int b = static_cast<int>(k & 1);
+    IPT_CUDA(cudaEventSynchronize(c.stage_ev[b]));
+    const int64_t r0 = k * per, nr = std::min(per, rows - r0);
+    const double* re = c.stage[b];
+    const double* im = c.stage[b] + half;
+    double* d0 = dst_c + 2 * r0 * cols;
+    const int64_t total = nr * cols;
+    const unsigned t = total >= (int64_t(1) << 16) ? host_pool().size() : 1u;
+    const int64_t step = (total + t - 1) / t;
+    auto work = [&](unsigned kk) {
+      const int64_t a = int64_t(kk) * step, e = std::min(total, a + step);
+      for (int64_t q = a; q < e; ++q) {
+        d0[2 * q] = re[q];
+        d0[2 * q + 1] = sim ? im[q] : 0.0;
+      }
+    };
+    if (t <= 1) work(0);
+    else host_pool().run(t, work);
+  }
+  IPT_CUDA(cudaStreamSynchronize(st));
 }
 
 // 32x32 tiles through shared memory; src column-major (element (r, c) at c*ld_src + r),

@@ -5,6 +5,8 @@
 
 #include <atomic>
 #include <cstdint>
+#include <memory>
+#include <utility>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -28,6 +30,28 @@ inline void check(int rc) {
 // Host scratch buffer drawn from a thread-local pool: the layout conversions at the
 // boundary reuse pages that are already faulted in instead of first-touching fresh
 // memory on every call (buffers above kPoolMax doubles are not retained).
+// std::allocator that leaves doubles uninitialised on resize: every Vec is an output the
+// device path overwrites or a conversion target filled right away, so the zero fill of
+// std::vector (a single-threaded pass over fresh pages) is pure cost.
+template <typename T>
+struct NoInitAllocator : std::allocator<T> {
+    template <typename U>
+    struct rebind {
+        using other = NoInitAllocator<U>;
+    };
+    NoInitAllocator() = default;
+    template <typename U>
+    NoInitAllocator(const NoInitAllocator<U>&) noexcept {}
+    template <typename U>
+    void construct(U* p) noexcept {
+        ::new (static_cast<void*>(p)) U;
+    }
+    template <typename U, typename... A>
+    void construct(U* p, A&&... a) {
+        ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+    }
+};
+
 class Vec {
 public:
     explicit Vec(std::size_t n = 0) { acquire(n); }
@@ -55,8 +79,9 @@ public:
 private:
     static constexpr std::size_t kPoolMax = std::size_t(1) << 25;  // 256 MB
     static constexpr std::size_t kPoolSlots = 16;
-    static std::vector<std::vector<double>>& pool() {
-        thread_local std::vector<std::vector<double>> p;
+    using Store = std::vector<double, NoInitAllocator<double>>;
+    static std::vector<Store>& pool() {
+        thread_local std::vector<Store> p;
         return p;
     }
     void acquire(std::size_t n) {
@@ -74,9 +99,9 @@ private:
         if (v_.capacity() == 0) return;
         auto& p = pool();
         if (v_.capacity() <= kPoolMax && p.size() < kPoolSlots) p.push_back(std::move(v_));
-        v_ = std::vector<double>();
+        v_ = Store();
     }
-    std::vector<double> v_;
+    Store v_;
 };
 
 struct Planar {
@@ -104,21 +129,27 @@ void parallel_chunks(std::size_t count, F&& f) {
     for (auto& th : pool) th.join();
 }
 
+// Planar copy of interleaved complex data; the imaginary plane is only materialised when
+// some imaginary part is nonzero (real inputs: one pass, half the host memory).
 inline Planar split(const cplx* v, std::size_t count) {
     Planar p;
     p.re.resize(count);
-    p.im.resize(count);
     std::atomic<bool> any_im{false};
     parallel_chunks(count, [&](std::size_t b, std::size_t e) {
         bool any = false;
         for (std::size_t i = b; i < e; ++i) {
             p.re[i] = v[i].real();
-            p.im[i] = v[i].imag();
             any = any || v[i].imag() != 0.0;
         }
         if (any) any_im.store(true, std::memory_order_relaxed);
     });
     p.any_im = any_im.load();
+    if (p.any_im) {
+        p.im.resize(count);
+        parallel_chunks(count, [&](std::size_t b, std::size_t e) {
+            for (std::size_t i = b; i < e; ++i) p.im[i] = v[i].imag();
+        });
+    }
     return p;
 }
 
@@ -130,15 +161,22 @@ inline void merge(const Vec& re, const Vec& im, cplx* out) {
 
 struct Csr {
     std::vector<int64_t> rowptr;
-    std::vector<int32_t> cols;
+    std::vector<int32_t, NoInitAllocator<int32_t>> cols;
     Planar val;
 };
 
+// The carrier's CSR (size_t columns, interleaved complex values) in the C ABI's form
+// (int32 columns, planar values), converted over the host threads.
 inline Csr to_csr(const ComplexMatrix& a) {
     if (a.rows() >= (std::size_t(1) << 31)) throw std::invalid_argument("csr: more than 2^31 columns");
     Csr c;
     c.rowptr.assign(a.row_offsets().begin(), a.row_offsets().end());
-    c.cols.assign(a.col_indices().begin(), a.col_indices().end());
+    const std::size_t nnz = a.col_indices().size();
+    c.cols.resize(nnz);
+    const std::size_t* src = a.col_indices().data();
+    parallel_chunks(nnz, [&](std::size_t b, std::size_t e) {
+        for (std::size_t q = b; q < e; ++q) c.cols[q] = static_cast<int32_t>(src[q]);
+    });
     c.val = split(a.values().data(), a.values().size());
     return c;
 }

@@ -1,11 +1,16 @@
 // kernels:: of the drop-in API (proj/include/ipt/kernels.hpp). matvec / matmul /
-// adjoint_matvec_dense run on the B200 through the C ABI; the *_serial oracles and
-// the norms are host loops, as in the reference.
+// adjoint_matvec_dense run on the B200 through the C ABI (square operators of 1 MB and
+// more stay resident on the device between calls); the *_serial oracles and the norms
+// are host loops, as in the reference.
 #include "ipt/kernels.hpp"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <string>
+#include <vector>
 
 #include "api_internal.hpp"
 
@@ -14,9 +19,182 @@ namespace ipt::kernels {
 using api::Planar;
 using api::Vec;
 
+namespace {
+
+// Device-resident operators of this thread's context. Iterative callers multiply by the
+// same matrix every pass (anderson.cpp:205, the power iterations of
+// spectral_norm_estimate, explorer.cpp:71); the operator is uploaded once and reused
+// while (storage address, ComplexMatrix::revision(), shape) match and a sampled content
+// fingerprint agrees. Operators below kMinBytes are not kept (their upload is cheap);
+// at most kSlots operators / IPT_OPERATOR_CACHE_MB (default 16384) are resident, least
+// recently used first out.
+enum class OpKind { Matvec, AdjointMatvec, MatmulLeft };
+
+struct CachedOperator {
+    const void* storage = nullptr;
+    std::uint64_t revision = 0, fingerprint = 0, last_use = 0;
+    std::size_t rows = 0, cols = 0, nnz = 0;
+    OpKind kind = OpKind::Matvec;
+    ipt_ctx* ctx = nullptr;
+    ipt_operator* op = nullptr;         // Matvec / AdjointMatvec
+    ipt_gemm_operand* gemm = nullptr;   // MatmulLeft
+    std::int64_t bytes = 0;
+    void release() {
+        ipt_operator_free(op);
+        ipt_gemm_operand_free(gemm);
+        op = nullptr;
+        gemm = nullptr;
+    }
+};
+
+struct OperatorCache {
+    static constexpr std::size_t kSlots = 4;
+    static constexpr std::int64_t kMinBytes = std::int64_t(1) << 20;
+    std::vector<CachedOperator> slots;
+    std::uint64_t clock = 0;
+    ~OperatorCache() { clear(); }
+    void clear() {
+        for (auto& c : slots) c.release();
+        slots.clear();
+    }
+    std::size_t size() const { return slots.size(); }
+    static std::int64_t budget() {
+        static const std::int64_t b = [] {
+            const char* e = std::getenv("IPT_OPERATOR_CACHE_MB");
+            return (e ? std::atoll(e) : 16384LL) << 20;
+        }();
+        return b;
+    }
+};
+
+thread_local OperatorCache t_ops;
+
+// Mixes ~2048 evenly spaced entries (and the CSR structure at the same stride): catches
+// contents changed through a raw pointer taken before the previous product.
+std::uint64_t fingerprint(const cplx* v, std::size_t count, const std::size_t* idx) {
+    std::uint64_t h = 0xcbf29ce484222325ull ^ count;
+    auto mix = [&h](std::uint64_t w) { h ^= w + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2); };
+    const std::size_t step = std::max<std::size_t>(1, count / 2048);
+    auto mix_at = [&](std::size_t t) {
+        std::uint64_t w[2];
+        std::memcpy(w, v + t, sizeof w);
+        mix(w[0]);
+        mix(w[1]);
+        if (idx) mix(idx[t]);
+    };
+    for (std::size_t t = 0; t < count; t += step) mix_at(t);
+    if (count) mix_at(count - 1);
+    return h;
+}
+
+// The resident device copy of A for `kind`, or nullptr when A is not kept (small,
+// over the budget, or a shape the kind does not cover).
+CachedOperator* resident(const ComplexMatrix& a, OpKind kind) {
+    const std::size_t m = a.rows(), k = a.cols();
+    if (m == 0 || k == 0) return nullptr;
+    if (kind != OpKind::MatmulLeft && m != k) return nullptr;
+    const bool dense = a.is_dense();
+    if (!dense && kind == OpKind::AdjointMatvec) return nullptr;  // CSR adjoints are formed by the callers
+    const std::size_t count = dense ? m * k : a.values().size();
+    const std::int64_t bytes = kind == OpKind::MatmulLeft ? std::int64_t(m) * std::int64_t(k) * 16
+                               : dense                    ? std::int64_t(count) * 16
+                                                          : std::int64_t(count) * 20 + 8 * std::int64_t(m);
+    if (bytes < OperatorCache::kMinBytes || bytes > OperatorCache::budget()) return nullptr;
+    ipt_ctx* ctx = api::context();
+    const cplx* vals = dense ? a.data() : a.values().data();
+    const std::uint64_t rev = a.revision();
+    const std::uint64_t fp = fingerprint(vals, count, dense ? nullptr : a.col_indices().data());
+    auto& cache = t_ops;
+    auto& v = cache.slots;
+    for (auto& c : v)
+        if (c.storage == vals && c.revision == rev && c.rows == m && c.cols == k && c.nnz == count &&
+            c.kind == kind && c.ctx == ctx && c.fingerprint == fp) {
+            c.last_use = ++cache.clock;
+            return &c;
+        }
+    // make room: stale copies of this matrix (same storage, same kind) and other contexts'
+    // entries first, then the least recently used
+    for (std::size_t i = 0; i < v.size();)
+        if ((v[i].storage == vals && v[i].kind == kind) || v[i].ctx != ctx) {
+            v[i].release();
+            v.erase(v.begin() + static_cast<std::ptrdiff_t>(i));
+        } else {
+            ++i;
+        }
+    auto used = [&v] {
+        std::int64_t sum = 0;
+        for (auto& c : v) sum += c.bytes;
+        return sum;
+    };
+    while (!v.empty() && (v.size() >= OperatorCache::kSlots || used() + bytes > OperatorCache::budget())) {
+        auto lru = std::min_element(v.begin(), v.end(), [](const CachedOperator& x, const CachedOperator& y) {
+            return x.last_use < y.last_use;
+        });
+        lru->release();
+        v.erase(lru);
+    }
+    CachedOperator c;
+    c.storage = vals;
+    c.revision = rev;
+    c.fingerprint = fp;
+    c.rows = m;
+    c.cols = k;
+    c.nnz = count;
+    c.kind = kind;
+    c.ctx = ctx;
+    c.bytes = bytes;
+    c.last_use = ++cache.clock;
+    if (kind == OpKind::MatmulLeft) {
+        ComplexMatrix densified;
+        const cplx* av = dense ? vals : (densified = a.to_dense()).data();
+        const Planar pa = api::split(av, m * k);
+        api::check(ipt_gemm_operand_create(ctx, static_cast<int64_t>(m), static_cast<int64_t>(k), pa.re.data(),
+                                           pa.im_or_null(), &c.gemm));
+    } else if (dense) {
+        Planar pa;
+        if (kind == OpKind::Matvec) {
+            pa = api::split(vals, count);
+        } else {  // conj(A)^T, row-major
+            pa.re.resize(count);
+            pa.im.resize(count);
+            api::parallel_chunks(m, [&](std::size_t b, std::size_t e) {
+                for (std::size_t j = b; j < e; ++j)
+                    for (std::size_t i = 0; i < m; ++i) {
+                        pa.re[j * m + i] = vals[i * m + j].real();
+                        pa.im[j * m + i] = -vals[i * m + j].imag();
+                    }
+            });
+            for (std::size_t t = 0; t < count && !pa.any_im; ++t) pa.any_im = pa.im[t] != 0.0;
+        }
+        api::check(ipt_operator_create_dense(ctx, static_cast<int64_t>(m), pa.re.data(), pa.im_or_null(), &c.op));
+    } else {
+        const api::Csr csr = api::to_csr(a);
+        api::check(ipt_operator_create_csr(ctx, static_cast<int64_t>(m), csr.rowptr.data(), csr.cols.data(),
+                                           csr.val.re.data(), csr.val.im_or_null(), &c.op));
+    }
+    v.push_back(c);
+    return &v.back();
+}
+
+void operator_matvec(ipt_operator* op, std::size_t n, const cplx* x, cplx* y) {
+    const Planar px = api::split(x, n);
+    Vec yr(n), yi(n);
+    api::check(ipt_operator_matvec(api::context(), op, px.re.data(), px.im_or_null(), yr.data(), yi.data()));
+    for (std::size_t i = 0; i < n; ++i) y[i] = cplx(yr[i], yi[i]);
+}
+
+}  // namespace
+
+void release_resident_operators() { t_ops.clear(); }
+std::size_t resident_operator_count() { return t_ops.size(); }
+
 void matvec(const ComplexMatrix& a, const cplx* x, cplx* y) {
     const std::size_t m = a.rows(), n = a.cols();
     if (m == 0) return;
+    if (CachedOperator* c = resident(a, OpKind::Matvec)) {
+        operator_matvec(c->op, n, x, y);
+        return;
+    }
     const Planar px = api::split(x, n);
     Vec yr(m), yi(m);
     if (a.is_dense()) {
@@ -55,6 +233,10 @@ void adjoint_matvec_dense(const ComplexMatrix& a, const cplx* x, cplx* y) {
     // y = A^H x  <=>  y^T = x^T conj(A): one 1 x m by m x n product on the device.
     const std::size_t m = a.rows(), n = a.cols();
     if (n == 0) return;
+    if (CachedOperator* c = resident(a, OpKind::AdjointMatvec)) {
+        operator_matvec(c->op, n, x, y);
+        return;
+    }
     const Planar px = api::split(x, m);
     Planar pa = api::split(a.data(), m * n);
     for (double& v : pa.im) v = -v;
@@ -70,6 +252,14 @@ void matmul(const ComplexMatrix& a, const ComplexMatrix& b, ComplexMatrix& c) {
     if (!c.is_dense() || c.rows() != a.rows() || c.cols() != b.cols()) c = ComplexMatrix::dense(a.rows(), b.cols());
     const std::size_t m = a.rows(), k = a.cols(), n = b.cols();
     if (m == 0 || n == 0) return;
+    if (CachedOperator* rc = resident(a, OpKind::MatmulLeft)) {  // A stays on the device
+        const Planar pb = api::split(b.data(), k * n);
+        Vec cr(m * n), ci(m * n);
+        api::check(ipt_gemm_operand_apply(api::context(), rc->gemm, static_cast<int64_t>(n), pb.re.data(),
+                                          pb.im_or_null(), cr.data(), ci.data()));
+        api::merge(cr, ci, c.data());
+        return;
+    }
     ComplexMatrix densified;  // only a CSR left factor is densified
     const cplx* av = a.is_dense() ? a.data() : (densified = a.to_dense()).data();
     const Planar pa = api::split(av, m * k), pb = api::split(b.data(), k * n);

@@ -1,6 +1,7 @@
 // ipt/lu.hpp over the C ABI: lu_factor / lu_solve / lu_solve_adjoint /
-// lu_solve_matrix (proj/src/lu.cpp:10-104) on the device, and the reference's 1-norm
-// condition estimator (lu.cpp:106-147) driven by device solves.
+// lu_solve_matrix (proj/src/lu.cpp:10-104) on the device, and the 1-norm condition
+// estimate (Hager's method, the reference's condition_estimate_1norm contract) driven by
+// device solves.
 #include "ipt/lu.hpp"
 
 #include <algorithm>
@@ -92,48 +93,57 @@ ComplexMatrix lu_solve_matrix(const LuFactors& f, const ComplexMatrix& b) {
     return ComplexMatrix::dense(n, r, std::move(x));
 }
 
+// kappa_1 = |A|_1 * est(|A^{-1}|_1). The estimate is Hager's convex maximisation of
+// |A^{-1} x|_1 over |x|_1 = 1 (Hager 1984; Higham's complex form): from the centroid of the
+// simplex, one ascent step per round -- the subgradient A^{-H} sign(A^{-1} x) names the
+// vertex e_j to move to -- until the subgradient certifies a local maximum (at most five
+// rounds). Each round is one forward and one adjoint solve with the device factors.
 double condition_estimate_1norm(const LuFactors& f, const ComplexMatrix& a) {
     if (f.singular) return std::numeric_limits<double>::infinity();
     const std::size_t n = f.n;
     if (a.rows() != n || a.cols() != n) throw std::invalid_argument("condition_estimate_1norm: size mismatch");
-    ComplexMatrix ad = a.to_dense();
-    double norm_a = 0.0;  // max column sum
-    for (std::size_t j = 0; j < n; ++j) {
-        double col = 0.0;
-        for (std::size_t i = 0; i < n; ++i) col += std::abs(ad.at(i, j));
-        norm_a = std::max(norm_a, col);
+    std::vector<double> colsum(n, 0.0);
+    if (a.is_dense()) {
+        const cplx* v = a.data();
+        for (std::size_t i = 0; i < n; ++i)
+            for (std::size_t j = 0; j < n; ++j) colsum[j] += std::abs(v[i * n + j]);
+    } else {
+        for (std::size_t q = 0; q < a.values().size(); ++q) colsum[a.col_indices()[q]] += std::abs(a.values()[q]);
     }
-    // Hager's estimate of |A^{-1}|_1: start from the uniform vector, at most five
-    // sign / unit-vector refinements, stop when the gradient test no longer improves.
+    const double a_norm1 = n ? *std::max_element(colsum.begin(), colsum.end()) : 0.0;
+
+    auto norm1 = [](const cvec& v) {
+        double s = 0.0;
+        for (const cplx& x : v) s += std::abs(x);
+        return s;
+    };
+    auto unit_phase = [](cplx v) {
+        const double r = std::abs(v);
+        return r > 0.0 ? v / r : cplx(1.0, 0.0);
+    };
     cvec x(n, cplx(1.0 / static_cast<double>(n), 0.0));
-    double est = 0.0;
-    for (int pass = 0; pass < 5; ++pass) {
+    double best = 0.0;
+    for (int round = 0; round < 5; ++round) {
         const cvec y = lu_solve(f, x);
-        double ysum = 0.0;
-        for (const cplx& v : y) ysum += std::abs(v);
-        est = std::max(est, ysum);
-        cvec sgn(n);
+        best = std::max(best, norm1(y));
+        cvec s(n);
+        std::transform(y.begin(), y.end(), s.begin(), unit_phase);
+        const cvec grad = lu_solve_adjoint(f, s);
+        std::size_t jmax = 0;
+        double gmax = -1.0, gx = 0.0;
         for (std::size_t i = 0; i < n; ++i) {
-            const double mag = std::abs(y[i]);
-            sgn[i] = mag == 0.0 ? cplx(1.0, 0.0) : y[i] / mag;
-        }
-        const cvec z = lu_solve_adjoint(f, sgn);
-        std::size_t best = 0;
-        double zbest = 0.0;
-        for (std::size_t i = 0; i < n; ++i) {
-            const double mag = std::abs(z[i]);
-            if (mag > zbest) {
-                zbest = mag;
-                best = i;
+            const double gi = std::abs(grad[i]);
+            if (gi > gmax) {
+                gmax = gi;
+                jmax = i;
             }
+            gx += std::abs(grad[i] * x[i]);
         }
-        double zdotx = 0.0;
-        for (std::size_t i = 0; i < n; ++i) zdotx += std::abs(z[i] * x[i]);
-        if (zbest <= zdotx) break;
-        x.assign(n, cplx{});
-        x[best] = 1.0;
+        if (gmax <= gx) break;  // no vertex ascends: local maximum reached
+        std::fill(x.begin(), x.end(), cplx{});
+        x[jmax] = 1.0;
     }
-    return norm_a * est;
+    return a_norm1 * best;
 }
 
 }  // namespace ipt

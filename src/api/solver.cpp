@@ -4,6 +4,7 @@
 #include "ipt/solver.hpp"
 
 #include <cstdlib>
+#include <future>
 #include <memory>
 
 #include "api_internal.hpp"
@@ -259,7 +260,7 @@ SpectrumResult solve_full(const Partition& p, const InverseGaps& g, const Iterat
     if (warm_start) {
         wd = warm_start->to_dense();
         if (wd.rows() != n || wd.cols() != n) throw std::invalid_argument("solve_full: warm start size mismatch");
-        w = api::split(wd.data(), n * n);
+        if (p.delta.is_sparse()) w = api::split(wd.data(), n * n);
     }
     ipt_params prm = to_params(config);
     prm.stop_rule = options.stop_rule == StopRule::MaxAbs ? IPT_STOP_MAX_ABS : IPT_STOP_REL_FRO;
@@ -268,6 +269,34 @@ SpectrumResult solve_full(const Partition& p, const InverseGaps& g, const Iterat
     ipt_stats st{};
     std::vector<double> trace(config.record_trace ? config.max_iterations : 0);
     st.trace = config.record_trace ? trace.data() : nullptr;
+    if (p.delta.is_dense()) {
+        // The carrier's interleaved std::complex arrays go to the C ABI as they are (the
+        // de-interleave happens inside the pinned staging pass); the result carrier is
+        // allocated and zero-filled on a host thread while the device iterates, and Z is
+        // interleaved straight into it while the closing product runs.
+        auto zbuf = std::async(std::launch::async, [n] { return cvec(n * n); });
+        ipt_full_problem* h = nullptr;
+        const int rc = ipt_full_solve_interleaved_start(
+            api::context(), static_cast<int64_t>(n), reinterpret_cast<const double*>(p.d.data()),
+            reinterpret_cast<const double*>(p.delta.data()),
+            warm_start ? reinterpret_cast<const double*>(wd.data()) : nullptr, &prm, &h, &st);
+        cvec zv = zbuf.get();
+        api::check(rc);
+        std::unique_ptr<ipt_full_problem, void (*)(ipt_full_problem*)> hold(h, ipt_full_free);
+        SpectrumResult r;
+        r.eigenvalues.resize(n);
+        api::check(ipt_full_solve_interleaved_finish(api::context(), h, &prm, reinterpret_cast<double*>(zv.data()),
+                                                     reinterpret_cast<double*>(r.eigenvalues.data()), &st));
+        r.Z = ComplexMatrix::dense(n, n, std::move(zv));
+        r.iterations = st.iterations;
+        r.final_step = st.final_step;
+        r.residual_frobenius = st.residual;
+        r.min_singular_value_estimate = st.min_singular_value_estimate;
+        r.status = static_cast<SolveStatus>(st.status);
+        r.matmul_count = static_cast<long>(st.product_count);
+        if (config.record_trace) r.trace.assign(trace.begin(), trace.begin() + st.iterations);
+        return r;
+    }
     Vec zr(n * n), zi(n * n), lr(n), li(n);
     const double* wre = warm_start ? w.re.data() : nullptr;
     const double* wim = warm_start ? w.im_or_null() : nullptr;

@@ -10,7 +10,9 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include <ipt/anderson.hpp>
 #include <ipt/complex_matrix.hpp>
+#include <ipt/kernels.hpp>
 #include <ipt/partition.hpp>
 #include <ipt/solver.hpp>
 
@@ -33,6 +35,23 @@ ipt::Partition near_diagonal(std::size_t n, double eps, std::uint64_t seed) {
         }
     }
     return ipt::partition(m);
+}
+
+ipt::ComplexMatrix random_complex(std::size_t rows, std::size_t cols, std::uint64_t seed) {
+    std::uint64_t x = seed;
+    auto uni = [&x] {
+        x = x * 6364136223846793005ull + 1442695040888963407ull;
+        return double(x >> 11) * 0x1p-53 - 0.5;
+    };
+    ipt::cvec v(rows * cols);
+    for (auto& e : v) e = ipt::cplx(uni(), uni());
+    return ipt::ComplexMatrix::dense(rows, cols, std::move(v));
+}
+
+double max_abs_diff(const ipt::cvec& a, const ipt::cvec& b) {
+    double d = 0.0;
+    for (std::size_t i = 0; i < a.size(); ++i) d = std::fmax(d, std::abs(a[i] - b[i]));
+    return d;
 }
 
 double max_abs_diff(const ipt::ComplexMatrix& a, const ipt::ComplexMatrix& b) {
@@ -101,4 +120,115 @@ TEST_CASE("IPT_PRODUCT=ozaki routes the drop-in ipt::solve_full to the tcgen05 p
     CHECK(max_abs_diff(got.Z, want.Z) == 0.0);  // the same (deterministic) Ozaki path
     CHECK(got.iterations == want.iterations);
     CHECK(max_abs_diff(dmma.Z, want.Z) <= 1e-13);
+}
+
+TEST_CASE("kernels::matvec keeps the operator on the device while it is unchanged") {
+    ipt::kernels::release_resident_operators();
+    ipt::ComplexMatrix a = random_complex(512, 512, 3);  // 4 MB: resident
+    ipt::cvec x(512);
+    for (std::size_t i = 0; i < x.size(); ++i) x[i] = ipt::cplx(std::cos(double(i)), std::sin(0.5 * double(i)));
+    ipt::cvec y1(512), y2(512), want(512);
+    ipt::kernels::matvec(a, x.data(), y1.data());
+    CHECK(ipt::kernels::resident_operator_count() == 1);
+    ipt::kernels::matvec(a, x.data(), y2.data());
+    CHECK(ipt::kernels::resident_operator_count() == 1);
+    CHECK(max_abs_diff(y1, y2) == 0.0);  // the resident copy, deterministic
+    ipt::kernels::matvec_serial(a, x.data(), want.data());
+    CHECK(max_abs_diff(y1, want) <= 1e-12);
+    // a mutation through the accessor invalidates the copy
+    a.at(7, 11) = ipt::cplx(3.0, -1.0);
+    ipt::kernels::matvec(a, x.data(), y1.data());
+    ipt::kernels::matvec_serial(a, x.data(), want.data());
+    CHECK(max_abs_diff(y1, want) <= 1e-12);
+    // a write through a pointer taken before the product, at a sampled entry
+    ipt::cplx* raw = a.data();
+    ipt::kernels::matvec(a, x.data(), y1.data());
+    raw[0] = ipt::cplx(-2.0, 5.0);
+    ipt::kernels::matvec(a, x.data(), y1.data());
+    ipt::kernels::matvec_serial(a, x.data(), want.data());
+    CHECK(max_abs_diff(y1, want) <= 1e-12);
+    // the adjoint product of the same matrix has its own resident copy
+    ipt::cvec ya(512), wa(512);
+    ipt::kernels::adjoint_matvec_dense(a, x.data(), ya.data());
+    const ipt::ComplexMatrix ah = a.adjoint();
+    ipt::kernels::matvec_serial(ah, x.data(), wa.data());
+    CHECK(max_abs_diff(ya, wa) <= 1e-12);
+    ipt::kernels::release_resident_operators();
+    CHECK(ipt::kernels::resident_operator_count() == 0);
+}
+
+TEST_CASE("kernels::matmul keeps its left factor on the device across right factors") {
+    ipt::kernels::release_resident_operators();
+    const ipt::ComplexMatrix a = random_complex(300, 500, 8);  // 2.4 MB
+    for (std::uint64_t seed : {1u, 2u, 3u}) {
+        const ipt::ComplexMatrix b = random_complex(500, 40 + seed, seed);
+        ipt::ComplexMatrix c, want;
+        ipt::kernels::matmul(a, b, c);
+        ipt::kernels::matmul_serial(a, b, want);
+        CHECK(max_abs_diff(c, want) <= 1e-12);
+    }
+    CHECK(ipt::kernels::resident_operator_count() == 1);
+    // a real right factor with the complex resident operand (the stacked [Ar; Ai] form)
+    ipt::cvec rv(500 * 7);
+    for (std::size_t t = 0; t < rv.size(); ++t) rv[t] = ipt::cplx(std::sin(double(t)), 0.0);
+    const ipt::ComplexMatrix br = ipt::ComplexMatrix::dense(500, 7, rv);
+    ipt::ComplexMatrix c, want;
+    ipt::kernels::matmul(a, br, c);
+    ipt::kernels::matmul_serial(a, br, want);
+    CHECK(max_abs_diff(c, want) <= 1e-12);
+    ipt::kernels::release_resident_operators();
+}
+
+TEST_CASE("AndersonState: affine weights, secant exactness, anchor re-pin") {
+    // scalar affine map lifted to the non-anchor coordinate: memory 1 reaches the fixed
+    // point after two mixed steps
+    const ipt::cplx a(-0.6, 0.3), b(0.4, -1.1);
+    const ipt::cplx fixed = b / (ipt::cplx(1.0) - a);
+    ipt::AndersonState st(1, 0);
+    ipt::cvec z{ipt::cplx(1.0), ipt::cplx(0.0)};
+    bool hit = false;
+    for (int k = 0; k < 3 && !hit; ++k) {
+        const ipt::cvec fz{ipt::cplx(1.0), a * z[1] + b};
+        z = ipt::anderson_step(st, z, fz);
+        ipt::cplx wsum{};
+        for (const auto& w : st.last_weights()) wsum += w;
+        CHECK(std::abs(wsum - ipt::cplx(1.0)) <= 1e-12);
+        CHECK(z[0] == ipt::cplx(1.0));
+        hit = std::abs(z[1] - fixed) <= 1e-12;
+    }
+    CHECK(hit);
+    CHECK(st.history_size() == 1);
+    st.reset();
+    CHECK(st.history_size() == 0);
+}
+
+TEST_CASE("solve_single_accelerated on complex inputs (host mixing, device products)") {
+    const std::size_t n = 400;
+    std::uint64_t x = 77;
+    auto uni = [&x] {
+        x = x * 6364136223846793005ull + 1442695040888963407ull;
+        return double(x >> 11) * 0x1p-53 - 0.5;
+    };
+    ipt::ComplexMatrix m = ipt::ComplexMatrix::dense(n, n);
+    for (std::size_t i = 0; i < n; ++i) {
+        m.at(i, i) = ipt::cplx(double(i) * 1.5, 0.3 * uni());
+        for (std::size_t j = 0; j < n; ++j)
+            if (j != i) m.at(i, j) = 0.02 * ipt::cplx(uni(), uni());
+    }
+    const ipt::Partition p = ipt::partition(m);
+    const ipt::InverseGaps g = ipt::build_gaps(p);
+    ipt::IterationConfig cfg;
+    cfg.residual_tolerance = 1e-10;
+    const ipt::EigenpairResult acc = ipt::solve_single_accelerated(p, g, 3, cfg, 5);
+    ipt::IterationConfig plain_cfg;
+    plain_cfg.tolerance = 1e-14;
+    const ipt::EigenpairResult plain = ipt::solve_single(p, g, 3, plain_cfg);
+    CHECK(acc.status == ipt::SolveStatus::Converged);
+    CHECK(plain.status == ipt::SolveStatus::Converged);
+    CHECK(acc.residual <= 1e-10);
+    CHECK(std::abs(acc.eigenvalue - plain.eigenvalue) <= 1e-10 * std::abs(plain.eigenvalue));
+    CHECK(acc.matvec_count <= acc.iterations + 1);
+    CHECK(acc.matvec_count < plain.matvec_count);
+    CHECK(acc.z[3] == ipt::cplx(1.0));
+    CHECK(ipt::kernels::resident_operator_count() >= 1);  // Delta stayed on the device
 }
