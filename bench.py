@@ -229,6 +229,7 @@ def per_config_e2e(ipt, ctx):
     p5 = synth.config5()
     g5gaps = ipt.build_gaps(p5, 0.0)
     cfg5 = ipt.IterationConfig(tolerance=1e-10)
+    ipt.solve_single(p5, g5gaps, 0, cfg5, ctx=ctx)  # warm (pools, staging), as for config 1
     t0 = time.perf_counter()
     g5 = ipt.solve_single(p5, g5gaps, 0, cfg5, ctx=ctx)
     tg = time.perf_counter() - t0
@@ -374,6 +375,27 @@ def bench_single(ipt, lib, ctx, which, steps, warmup, hbm, reduce_max=lambda x: 
     return out
 
 
+def cpp_dropin_phases():
+    """The C++ drop-in API (include/ipt/*.hpp) timed with the reference's own phase method
+    (proj/src/bench.cpp:50-99, medians of the repetitions) by tools/cpp/dropin_bench: the
+    caller's std::complex ComplexMatrix carriers in and out, so the layout conversion at
+    the boundary is inside every number."""
+    import subprocess
+
+    exe = os.path.join(ROOT, "tools", "cpp", "dropin_bench")
+    if not os.path.exists(exe):
+        return {"error": "tools/cpp/dropin_bench not built (make -C paper_2012_14702_b200)"}
+    out = {"method": "proj/src/bench.cpp:50-99 phases through ipt::solve_full / solve_single / kernels:: (C++)"}
+    for cfg, reps in (("2", "3"), ("5", "3"), ("3", "2")):
+        try:
+            r = subprocess.run([exe, cfg, reps], capture_output=True, text=True, timeout=900)
+            line = [x for x in r.stdout.splitlines() if x.startswith("{")]
+            out[f"config{cfg}"] = json.loads(line[-1]) if line else {"error": r.stderr[-300:]}
+        except Exception as exc:  # report, never hide
+            out[f"config{cfg}"] = {"error": repr(exc)}
+    return out
+
+
 def bench_sparse_full(lib, ctx, n, per_row, steps, dense_step_ms):
     """Sparse-Delta full map: CSR Delta with per_row entries per row at the
     headline N, fused SpMM map (spmm_full_kernel<0,4>), Z row-major in HBM. Bound: the
@@ -460,6 +482,36 @@ def bench_ozaki(ipt, lib, ctx, n, dense_step_ms, dmma_solve):
         out["lambda0"] = float(r.eigenvalues[0])
         out["lambda0_rel_diff_vs_dmma"] = abs(float(r.eigenvalues[0]) - dmma_solve["lambda0"]) / abs(dmma_solve["lambda0"])
     return out
+
+
+def shared_outputs(n, rank, barrier):
+    """Full-size Z / eigenvalue host arrays mapped by every rank (/dev/shm), for the
+    column-local output of a sharded solve; None when /dev/shm cannot hold them."""
+    import shutil
+
+    need = 8 * n * n + 8 * n
+    tag = os.environ.get("MASTER_PORT", "0")
+    paths = [f"/dev/shm/ipt_bench_{tag}_z", f"/dev/shm/ipt_bench_{tag}_lam"]
+    ok = [0]
+    if rank == 0:
+        try:
+            ok[0] = int(shutil.disk_usage("/dev/shm").free > 1.2 * need)
+        except OSError:
+            ok[0] = 0
+        if ok[0]:
+            np.memmap(paths[0], dtype=np.float64, mode="w+", shape=(n, n)).flush()
+            np.memmap(paths[1], dtype=np.float64, mode="w+", shape=(n,)).flush()
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(ok, dtype=torch.int32, device="cuda")
+    dist.broadcast(t, 0)
+    barrier()
+    if not int(t.item()):
+        return None, None
+    zr = np.memmap(paths[0], dtype=np.float64, mode="r+", shape=(n, n))
+    lr = np.memmap(paths[1], dtype=np.float64, mode="r+", shape=(n,))
+    return (zr, None, lr, None), paths
 
 
 # --------------------------------------------------------------------------- launch
@@ -583,10 +635,17 @@ def main():
     if not args.no_e2e:
         torch.cuda.empty_cache()
         barrier()
+        # N > 1: every rank writes its own columns of Z into one shared host array
+        # (IPT_OUTPUT_LOCAL_COLUMNS, a /dev/shm mapping), no gather through rank 0
+        out, shm = None, None
+        if world > 1:
+            out, shm = shared_outputs(n, rank, barrier)
+        barrier()
         t0 = time.perf_counter()
         gaps = ipt.build_gaps(p)
         t_gaps = time.perf_counter() - t0
-        r = ipt.solve_full(p, gaps, ipt.IterationConfig(tolerance=1e-12), ctx=ctx)
+        r = ipt.solve_full(p, gaps, ipt.IterationConfig(tolerance=1e-12), ctx=ctx,
+                           output="local" if out is not None else "root", out=out)
         t_call = time.perf_counter() - t0 - t_gaps
         barrier()
         e2e_s = max_over_ranks(time.perf_counter() - t0)
@@ -595,10 +654,12 @@ def main():
                   f"total {1e3 * e2e_s:.1f} ms", file=sys.stderr, flush=True)
         e2e = {"value": flops_step * r.iterations / e2e_s / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": int(8 * n * n + 8 * n),
-               "d2h_bytes_per_step": int(8 * n * n + 8 * n) if rank == 0 else 0,
+               "d2h_bytes_per_step": int(8 * n * n + 8 * n),
                "step": "one drop-in solve_full call (C ABI ipt_full_solve, host buffers, pageable memory); "
-                       "h2d bytes are the whole job's (with g GPUs each rank uploads 1/g of Delta's rows "
-                       "and an NVLink all-gather replicates it)",
+                       "h2d / d2h bytes are the whole job's (with g GPUs each rank uploads 1/g of Delta's rows "
+                       "and an NVLink all-gather replicates it; each rank downloads its own columns of Z into "
+                       "a shared host mapping when output is local)",
+               "output": "local columns (shared /dev/shm mapping)" if out is not None else "root",
                "seconds": e2e_s,
                "flop_convention": "2N^3 per IPT iteration (the metric's definition) x iterations / wall time; "
                                   "iteration 1 from Z = I is evaluated exactly without a product (W = Delta I = "
@@ -611,6 +672,15 @@ def main():
                       "time_to_solution_s": e2e_s,
                       "lambda0": float(r.eigenvalues[0]) if rank == 0 else None}
         del r
+        if shm is not None:
+            barrier()
+            del out
+            if rank == 0:
+                for f in shm:
+                    try:
+                        os.unlink(f)
+                    except OSError:
+                        pass
     del p
 
     # ---------------- secondary: single-pair paths (rank 0, N = 1 only)
@@ -666,6 +736,11 @@ def main():
                 secondary["ozaki"] = bench_ozaki(ipt, lib, ctx, n, step_ms, solve_info)
             except Exception as exc:
                 secondary["ozaki"] = {"error": repr(exc)}
+
+    if world == 1 and args.secondary == "all":
+        lib.ipt_ctx_trim(ctx.handle)  # the subprocess needs the device memory this process keeps cached
+        torch.cuda.empty_cache()
+        secondary["cpp_dropin"] = cpp_dropin_phases()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

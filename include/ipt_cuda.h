@@ -58,7 +58,17 @@ typedef struct {
   double shrink_alpha;         /* continuation factor in [0, 1) */
   int32_t ignore_convergence;  /* bench only: apply exactly max_iterations maps */
   int32_t product;             /* IPT_PRODUCT_*: how the full-spectrum map forms W = Delta Z */
+  int32_t output_mode;         /* IPT_OUTPUT_*: where a column-sharded solve leaves Z and Lambda */
 } ipt_params;
+
+/* Column-sharded full spectrum (communicator of g ranks): ROOT gathers Z and the
+ * eigenvalues to rank 0 (other ranks may pass NULL outputs); LOCAL_COLUMNS has every rank
+ * write only its own columns [r n/g, (r+1) n/g) of Z (and its eigenvalues) into full-size
+ * n x n / n outputs -- one host array mapped by every rank (shared memory), filled by all
+ * ranks' copy engines at once with no gather. sigma_min is computed on the shards either
+ * way (y = Z p all-reduced per CG step). */
+#define IPT_OUTPUT_ROOT 0
+#define IPT_OUTPUT_LOCAL_COLUMNS 1
 
 /* W = Delta Z of the real dense full-spectrum map: FP64 tensor cores (DMMA, default), or
  * FP64-accurate Ozaki scheme II on the tcgen05 INT8 datapath (16 exact modular products,
@@ -110,6 +120,9 @@ int ipt_ctx_init_local_comm(ipt_ctx* ctx, ipt_local_group* group, int rank);
 /* "none", "nccl" or "local" */
 const char* ipt_ctx_comm_kind(const ipt_ctx* ctx);
 int ipt_ctx_synchronize(ipt_ctx* ctx);
+/* Return the device memory the library keeps cached for reuse (freed buffers of earlier
+ * solves stay mapped to avoid re-mapping costs) to the driver. */
+int ipt_ctx_trim(ipt_ctx* ctx);
 
 /* ---- full spectrum: solve_full (solver.cpp:180-273) ----
  * With a communicator of g ranks, Z is column-sharded: rank r iterates columns

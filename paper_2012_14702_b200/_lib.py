@@ -32,6 +32,8 @@ _vp = C.c_void_p
 
 PRODUCT_DMMA = 0
 PRODUCT_OZAKI = 1
+OUTPUT_ROOT = 0
+OUTPUT_LOCAL_COLUMNS = 1
 
 
 class Params(C.Structure):
@@ -46,6 +48,7 @@ class Params(C.Structure):
         ("shrink_alpha", C.c_double),
         ("ignore_convergence", C.c_int32),
         ("product", C.c_int32),
+        ("output_mode", C.c_int32),
     ]
 
 
@@ -81,6 +84,7 @@ SIGNATURES = {
     "ipt_ctx_init_comm": (C.c_int, [_vp, _vp, C.c_int, C.c_int]),
     "ipt_ctx_rank": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "ipt_ctx_synchronize": (C.c_int, [_vp]),
+    "ipt_ctx_trim": (C.c_int, [_vp]),
     "ipt_local_group_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
     "ipt_local_group_destroy": (None, [_vp]),
     "ipt_ctx_init_local_comm": (C.c_int, [_vp, _vp, C.c_int]),

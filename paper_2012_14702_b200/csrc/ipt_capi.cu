@@ -343,6 +343,15 @@ int ipt_ctx_rank(const ipt_ctx* ctx, int* rank, int* nranks) {
   return IPT_OK;
 }
 
+int ipt_ctx_trim(ipt_ctx* ctx) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    ctx->c.sync();
+    release_cached_device_memory(ctx->c.device);
+  });
+}
+
 int ipt_ctx_synchronize(ipt_ctx* ctx) {
   return guarded([&] {
     check_ctx(ctx);
@@ -849,11 +858,16 @@ static int single_solve_common(ipt_ctx* ctx, SingleProblem* raw, int64_t anchor,
                                double* z_im, ipt_stats* stats) {
   std::unique_ptr<SingleProblem, void (*)(SingleProblem*)> P(raw, single_free);
   const ipt_params prm = params_or_default(params);
+  HostPhases ph("single_solve");
   single_reset(*P, anchor, prm.schedule == IPT_SCHEDULE_CONTINUATION ? nullptr : warm_re,
                prm.schedule == IPT_SCHEDULE_CONTINUATION ? nullptr : warm_im, prm.max_iterations);
+  ph.mark("reset");
   single_iterate(*P, prm, stats);
+  ph.mark("iterate");
   single_finalize(*P, stats);
+  ph.mark("finalize");
   single_download(*P, z_re, z_im);
+  ph.mark("download");
   (void)ctx;
   return IPT_OK;
 }
@@ -889,6 +903,7 @@ int ipt_single_solve_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const doub
     if (prm.max_iterations <= 0) throw InvalidArgument("config: max_iterations must be positive");
     if (anchor < 0 || anchor >= n) throw InvalidArgument("solver: anchor out of range");
     const bool wc = prm.schedule != IPT_SCHEDULE_CONTINUATION && any_nonzero(warm_im, n);
+    HostPhases ph("ipt_single_solve_csr");
     single_solve_common(ctx, single_upload(ctx->c, n, d_re, d_im, true, nullptr, nullptr, rowptr, cols,
                                            val_re, val_im, true, wc),
                         anchor, warm_re, warm_im, params, z_re, z_im, stats);

@@ -41,14 +41,17 @@ struct NcclComm final : Comm {
   const char* kind() const override { return "nccl"; }
 
   void all_reduce(void* buf, size_t count, CommType t, CommOp op, cudaStream_t s) override {
+    NvtxRange nvtx_("ipt:all_reduce");
     IPT_NCCL(ncclAllReduce(buf, buf, count, nccl_type(t), nccl_op(op), comm, s));
   }
   void all_gather(void* buf, size_t count, CommType t, cudaStream_t s) override {
+    NvtxRange nvtx_("ipt:all_gather");
     char* b = static_cast<char*>(buf);
     IPT_NCCL(ncclAllGather(b + size_t(rank) * count * comm_type_size(t), b, count, nccl_type(t), comm, s));
   }
   void gather(const void* send, size_t count, void* recv, const size_t* counts, const size_t* displs, CommType t,
               int root, cudaStream_t s) override {
+    NvtxRange nvtx_("ipt:gather");
     const size_t sz = comm_type_size(t);
     IPT_NCCL(ncclGroupStart());
     if (rank == root) {
@@ -224,6 +227,7 @@ struct LocalComm final : Comm {
   }
 
   void all_reduce(void* buf, size_t count, CommType t, CommOp op, cudaStream_t s) override {
+    NvtxRange nvtx_("ipt:all_reduce");
     if (t == CommType::Byte) throw InvalidArgument("local comm: byte all-reduce");
     const size_t bytes = count * comm_type_size(t);
     if (bytes > scratch_bytes) {
@@ -252,6 +256,7 @@ struct LocalComm final : Comm {
   }
 
   void all_gather(void* buf, size_t count, CommType t, cudaStream_t s) override {
+    NvtxRange nvtx_("ipt:all_gather");
     const size_t bytes = count * comm_type_size(t);
     post(buf, s);
     wait_peers(G->ready, s);
@@ -265,6 +270,7 @@ struct LocalComm final : Comm {
 
   void gather(const void* send, size_t count, void* recv, const size_t* counts, const size_t* displs, CommType t,
               int root, cudaStream_t s) override {
+    NvtxRange nvtx_("ipt:gather");
     const size_t sz = comm_type_size(t);
     (void)count;
     post(send, s);

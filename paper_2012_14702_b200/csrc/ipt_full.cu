@@ -48,6 +48,7 @@ struct FullProblem {
   int trace_cap = 0;
   int enq = 0;              // maps enqueued since reset
   DevBuf gathered;          // rank 0 with nranks > 1: full Z (n columns, ldz)
+  bool local_output = false;  // IPT_OUTPUT_LOCAL_COLUMNS: each rank downloads its own columns
   bool finalized = false;
   // Sparse real Delta (CSR, f2): during the loop Z[2] hold the local columns ROW-major
   // (n rows x cols_pad, ldr = cols_pad), the layout a CSR x dense product gathers
@@ -821,6 +822,7 @@ static void column_block(const Ctx& c, int64_t n, int64_t begin, int64_t end, in
 FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_im,
                          const double* delta_re, const double* delta_im, bool force_complex,
                          int64_t col_begin, int64_t col_end, const double* delta_c) {
+  NvtxRange nvtx_("ipt:full_upload");
   if (n <= 0) throw InvalidArgument("solve_full: empty problem");
   if (!d_re || !(delta_re || delta_c)) throw InvalidArgument("solve_full: null input");
   auto P = std::make_unique<FullProblem>();
@@ -951,6 +953,7 @@ FullProblem* full_upload(Ctx& c, int64_t n, const double* d_re, const double* d_
 // Real CSR Delta (rowptr[n+1] with any base, cols in [0, n)): the sparse map path.
 FullProblem* full_upload_csr(Ctx& c, int64_t n, const double* d, const int64_t* rowptr,
                              const int32_t* cols, const double* vals, int64_t col_begin, int64_t col_end) {
+  NvtxRange nvtx_("ipt:full_upload_csr");
   if (n <= 0) throw InvalidArgument("solve_full: empty problem");
   if (!d || !rowptr) throw InvalidArgument("solve_full: null input");
   const int64_t b = rowptr[0], nnz = rowptr[n] - rowptr[0];
@@ -1009,6 +1012,7 @@ void full_free(FullProblem* P) { delete P; }
 
 void full_reset(FullProblem& P, const double* warm_re, const double* warm_im, int max_iter_hint,
                 bool renormalize) {
+  NvtxRange nvtx_("ipt:full_reset");
   Ctx& c = *P.ctx;
   cudaStream_t s = c.stream;
   const int64_t n = P.n;
@@ -1104,6 +1108,7 @@ int full_ozaki_moduli(FullProblem& P) {
 }
 
 void full_iterate(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
+  NvtxRange nvtx_("ipt:full_iterate");
   Ctx& c = *P.ctx;
   P.product = effective_product(P, prm.product);
   if (!(prm.tolerance > 0.0)) throw InvalidArgument("config: tolerance must be positive");
@@ -1176,6 +1181,7 @@ static const double* final_colmajor_z(FullProblem& P) {
 // Closing product: Lambda and |MZ - Z Lambda|_F (solver.cpp:252-270), then the
 // eigenvector gather to rank 0 and sigma_min (solver.cpp:271) on rank 0.
 void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
+  NvtxRange nvtx_("ipt:full_finalize");
   Ctx& c = *P.ctx;
   cudaStream_t s = c.stream;
   IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
@@ -1206,8 +1212,13 @@ void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
   IPT_CUDA(cudaEventElapsedTime(&ms_final, c.ev[0], c.ev[1]));
   z = final_colmajor_z(P);
 
-  // Gather the column shards on rank 0 (one final eigenvector gather).
-  if (c.nranks > 1) {
+  // Gather the column shards on rank 0 (one final eigenvector gather), unless every rank
+  // writes its own columns to the host (IPT_OUTPUT_LOCAL_COLUMNS).
+  P.local_output = c.nranks > 1 && prm.output_mode == IPT_OUTPUT_LOCAL_COLUMNS;
+  bool gathered = false;  // (every rank takes part in the gather exactly once)
+  auto gather_z = [&] {
+    if (gathered) return;
+    gathered = true;
     if (c.rank == 0) P.gathered.alloc(size_t(round_up(P.n, kBN)) * P.ldz);
     std::vector<size_t> counts(c.nranks), displs(c.nranks);
     for (int r = 0; r < c.nranks; ++r) {
@@ -1217,14 +1228,32 @@ void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
     }
     c.comm->gather(z, size_t(P.ncols) * P.ldz, P.gathered.get(), counts.data(), displs.data(), CommType::F64, 0, s);
     c.sync();
-  }
+  };
+  if (c.nranks > 1 && !P.local_output) gather_z();
 
   double sig = 0.0;
   float ms_sigma = 0.f;
-  if (prm.want_sigma_min && c.rank == 0 && (c.nranks > 1 || P.ncols == P.n)) {
-    const double* zfull = c.nranks > 1 ? P.gathered.get() : z;
+  if (prm.want_sigma_min && (c.nranks > 1 || P.ncols == P.n)) {
     IPT_CUDA(cudaEventRecord(c.ev[2], s));
-    sig = sigma_min_device(c, P.n, zfull, P.cplx ? zfull + P.ld : nullptr, P.ldz, 50, 1e-4);
+    if (c.nranks > 1) {
+      // on the shards: y = Z p all-reduced per CG step, no gather of Z
+      bool ok = false;
+      sig = sigma_min_sharded(c, P.n, P.col0, P.ncols, z, P.cplx ? z + P.ld : nullptr, P.ldz, 50, 1e-4, &ok);
+      if (!ok) {  // CG missed: the factor path on rank 0 over the gathered Z, shared by a sum
+        gather_z();
+        DevBuf one;
+        one.alloc(1);
+        if (c.rank == 0) {
+          sig = sigma_min_device(c, P.n, P.gathered.get(), P.cplx ? P.gathered.get() + P.ld : nullptr, P.ldz, 50,
+                                 1e-4);
+          IPT_CUDA(cudaMemcpyAsync(one.get(), &sig, sizeof(double), cudaMemcpyHostToDevice, s));
+        }
+        c.comm->all_reduce(one.get(), 1, CommType::F64, CommOp::Sum, s);
+        IPT_CUDA(cudaMemcpyAsync(&sig, one.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+      }
+    } else {
+      sig = sigma_min_device(c, P.n, z, P.cplx ? z + P.ld : nullptr, P.ldz, 50, 1e-4);
+    }
     IPT_CUDA(cudaEventRecord(c.ev[3], s));
     c.sync();
     IPT_CUDA(cudaEventElapsedTime(&ms_sigma, c.ev[2], c.ev[3]));
@@ -1242,6 +1271,7 @@ void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
 // Single-rank column block [col0, col0 + ncols): Z block (n x ncols, row-major planar)
 // and its eigenvalues.
 void full_download_block(FullProblem& P, double* z_re, double* z_im, double* lam_re, double* lam_im) {
+  NvtxRange nvtx_("ipt:full_download_block");
   Ctx& c = *P.ctx;
   if (c.nranks != 1) throw InvalidArgument("download: column blocks are single-rank");
   cudaStream_t s = c.stream;
@@ -1305,12 +1335,36 @@ static void gather_eigenvalues(FullProblem& P, std::vector<double>& lr, std::vec
 
 // Z (row-major planar) and eigenvalues to the host; rank 0 receives everything.
 void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, double* lam_im) {
+  NvtxRange nvtx_("ipt:full_download");
   Ctx& c = *P.ctx;
   if (c.nranks == 1 && P.ncols != P.n) throw InvalidArgument("download: column block problem (use the block download)");
   cudaStream_t s = c.stream;
   IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
   c.sync();
   const int64_t n = P.n;
+  if (P.local_output) {  // this rank's columns into the full-size outputs
+    const int64_t c0 = P.col0, nc = P.ncols;
+    std::vector<double> lr(nc), li(nc);
+    IPT_CUDA(cudaMemcpyAsync(lr.data(), P.lam.get(), sizeof(double) * nc, cudaMemcpyDeviceToHost, s));
+    IPT_CUDA(cudaMemcpyAsync(li.data(), P.lami.get(), sizeof(double) * nc, cudaMemcpyDeviceToHost, s));
+    c.sync();
+    if (lam_re) std::memcpy(lam_re + c0, lr.data(), sizeof(double) * nc);
+    if (lam_im) for (int64_t j = 0; j < nc; ++j) lam_im[c0 + j] = P.cplx ? li[j] : 0.0;
+    const double* zsrc = final_colmajor_z(P);
+    DevBuf rm;
+    rm.alloc(size_t(n) * std::max<int64_t>(nc, 1), false);
+    for (int part = 0; part < 2; ++part) {
+      double* dst = part == 0 ? z_re : z_im;
+      if (dst == nullptr || nc == 0) continue;
+      if (part == 1 && !P.cplx) {
+        for (int64_t i = 0; i < n; ++i) std::memset(dst + i * n + c0, 0, sizeof(double) * nc);
+        continue;
+      }
+      transpose_to_rowmajor(s, zsrc + (part ? P.ld : 0), P.ldz, n, nc, rm.get(), nc);
+      d2h_rows(c, dst + c0, n, rm.get(), nc, n, nc);
+    }
+    return;
+  }
   std::vector<double> lr, li;
   gather_eigenvalues(P, lr, li);
   if (c.rank != 0) return;
@@ -1363,6 +1417,7 @@ void full_prepare_download(FullProblem& P, bool want_re, bool want_im) {
 }
 
 void full_download_z(FullProblem& P, double* z_re, double* z_im) {
+  NvtxRange nvtx_("ipt:full_download_z");
   Ctx& c = *P.ctx;
   const int64_t n = P.n;
   for (int part = 0; part < 2; ++part) {
@@ -1380,12 +1435,36 @@ void full_download_z(FullProblem& P, double* z_re, double* z_im) {
 
 // The same downloads into interleaved complex host arrays (the C++ carrier's layout).
 void full_download_interleaved(FullProblem& P, double* z_c, double* lam_c) {
+  NvtxRange nvtx_("ipt:full_download");
   Ctx& c = *P.ctx;
   if (c.nranks == 1 && P.ncols != P.n) throw InvalidArgument("download: column block problem (use the block download)");
   cudaStream_t s = c.stream;
   IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
   c.sync();
   const int64_t n = P.n;
+  if (P.local_output) {  // this rank's columns into the full-size outputs
+    const int64_t c0 = P.col0, nc = P.ncols;
+    std::vector<double> lr(nc), li(nc);
+    IPT_CUDA(cudaMemcpyAsync(lr.data(), P.lam.get(), sizeof(double) * nc, cudaMemcpyDeviceToHost, s));
+    IPT_CUDA(cudaMemcpyAsync(li.data(), P.lami.get(), sizeof(double) * nc, cudaMemcpyDeviceToHost, s));
+    c.sync();
+    if (lam_c)
+      for (int64_t j = 0; j < nc; ++j) {
+        lam_c[2 * (c0 + j)] = lr[j];
+        lam_c[2 * (c0 + j) + 1] = P.cplx ? li[j] : 0.0;
+      }
+    if (z_c == nullptr || nc == 0) return;
+    const double* zsrc = final_colmajor_z(P);
+    DevBuf rre, rim;
+    rre.alloc(size_t(n) * nc, false);
+    transpose_to_rowmajor(s, zsrc, P.ldz, n, nc, rre.get(), nc);
+    if (P.cplx) {
+      rim.alloc(size_t(n) * nc, false);
+      transpose_to_rowmajor(s, zsrc + P.ld, P.ldz, n, nc, rim.get(), nc);
+    }
+    d2h_rows_merge(c, z_c + 2 * c0, n, rre.get(), P.cplx ? rim.get() : nullptr, nc, n, nc);
+    return;
+  }
   std::vector<double> lr, li;
   gather_eigenvalues(P, lr, li);
   if (c.rank != 0) return;
@@ -1404,15 +1483,16 @@ void full_download_interleaved(FullProblem& P, double* z_c, double* lam_c) {
     rim.alloc(size_t(n) * n, false);
     transpose_to_rowmajor(s, zsrc + P.ld, P.ldz, n, n, rim.get(), n);
   }
-  d2h_rows_merge(c, z_c, rre.get(), P.cplx ? rim.get() : nullptr, n, n, n);
+  d2h_rows_merge(c, z_c, n, rre.get(), P.cplx ? rim.get() : nullptr, n, n, n);
 }
 
 // Early (overlapped) download after full_prepare_download(P, true, P.cplx), on stream2.
 void full_download_z_interleaved(FullProblem& P, double* z_c) {
+  NvtxRange nvtx_("ipt:full_download_z");
   Ctx& c = *P.ctx;
   if (P.rm_ptr[0] == nullptr || (P.cplx && P.rm_ptr[1] == nullptr))
     throw InvalidArgument("download: prepare must run first");
-  d2h_rows_merge(c, z_c, P.rm_ptr[0], P.cplx ? P.rm_ptr[1] : nullptr, P.n, P.n, P.n, c.stream2);
+  d2h_rows_merge(c, z_c, P.n, P.rm_ptr[0], P.cplx ? P.rm_ptr[1] : nullptr, P.n, P.n, P.n, c.stream2);
   IPT_CUDA(cudaStreamSynchronize(c.stream2));
 }
 

@@ -1,6 +1,8 @@
 // Internal host-side structures shared by the IPT CUDA translation units.
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <atomic>
 #include <string>
 #include <memory>
@@ -58,6 +60,15 @@ struct Ctx {
     c0 = n * rank / nranks;
     c1 = n * (rank + 1) / nranks;
   }
+};
+
+// NVTX range over a host phase (upload, iterations, closing product, sigma_min, gathers,
+// downloads, collectives): visible in nsys / ncu timelines; a no-op without a tool.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 // IPT_PROFILE=1: host wall time between marks of one routine, printed on destruction.
@@ -137,8 +148,9 @@ void release_staging(Ctx& c);
 // (the C++ carrier's layout, converted inside the staging pass).
 void h2d_rows_split(Ctx& c, double* dre, double* dim, int64_t dpitch, const double* src_c, int64_t rows,
                     int64_t cols, bool* any_im);
-void d2h_rows_merge(Ctx& c, double* dst_c, const double* sre, const double* sim, int64_t spitch, int64_t rows,
-                    int64_t cols, cudaStream_t s = nullptr);
+// (dpitch: complex elements between host rows)
+void d2h_rows_merge(Ctx& c, double* dst_c, int64_t dpitch, const double* sre, const double* sim, int64_t spitch,
+                    int64_t rows, int64_t cols, cudaStream_t s = nullptr);
 
 // Full-spectrum problem (ipt_full.cu)
 struct FullProblem;
@@ -215,6 +227,8 @@ void i8_gemm_device(cudaStream_t s, int64_t M, int64_t N, int64_t K, const int8_
 // sigma_min (ipt_sigma.cu): Z column-major (ldz), real or complex (zi nullable).
 double sigma_min_device(Ctx& ctx, int64_t n, const double* zr, const double* zi, int64_t ldz,
                         int max_iters, double tol);
+double sigma_min_sharded(Ctx& c, int64_t n, int64_t col0, int64_t ncols, const double* zr, const double* zi,
+                         int64_t ldz, int max_iters, double tol, bool* ok);
 
 }  // namespace iptb
 

@@ -511,6 +511,7 @@ constexpr size_t kTrsmSmem = sizeof(double) * (2 * kPanel * kPanel + 2 * kPanel 
 }  // namespace
 
 LuProblem* lu_factor_device(Ctx& c, int64_t n, const double* a_re, const double* a_im) {
+  NvtxRange nvtx_("ipt:lu_factor");
   if (n <= 0) throw InvalidArgument("lu_factor: matrix must be square");
   if (!a_re) throw InvalidArgument("lu_factor: null input");
   auto F = std::make_unique<LuProblem>();
@@ -662,6 +663,7 @@ LuProblem* lu_from_host(Ctx& c, int64_t n, const double* lu_re, const double* lu
 // host arrays (b_im / x_im nullable on input / output).
 void lu_solve_device(LuProblem& F, int64_t r, const double* b_re, const double* b_im, double* x_re, double* x_im,
                      bool adjoint) {
+  NvtxRange nvtx_("ipt:lu_solve");
   Ctx& c = *F.ctx;
   cudaStream_t s = c.stream;
   const int64_t n = F.n;

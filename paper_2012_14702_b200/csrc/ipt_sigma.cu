@@ -211,17 +211,18 @@ __global__ void tri_bwd_update_kernel(const double* __restrict__ H, int64_t ldh,
   if (lane == 0) x[r] -= s;
 }
 
-__global__ void norm2_kernel(const double* __restrict__ u, int64_t m, double* out) {
+// |u|_2 into out[0] (squared when `squared`: column shards all-reduce it first).
+__global__ void norm2_kernel(const double* __restrict__ u, int64_t m, double* out, int squared) {
   __shared__ double red[32][4];
   double v[4] = {0.0, 0.0, 0.0, 0.0};
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x) v[0] = __fma_rn(u[i], u[i], v[0]);
   block_reduce4<32>(v, red);
-  if (threadIdx.x == 0) out[0] = sqrt(v[0]);
+  if (threadIdx.x == 0) out[0] = squared ? v[0] : sqrt(v[0]);
 }
 
 __global__ void normalize_kernel(const double* __restrict__ u, double* __restrict__ v, int64_t m,
-                                 const double* un) {
-  const double s = *un;
+                                 const double* un, int squared) {
+  const double s = squared ? sqrt(*un) : *un;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
     v[i] = u[i] / s;
 }
@@ -237,6 +238,22 @@ __global__ void embed_complex_kernel(const double* __restrict__ zr, const double
     E[j * lde + n + i] = b;
     E[(n + j) * lde + i] = -b;
     E[(n + j) * lde + n + i] = a;
+  }
+}
+
+// A column block of the embedding: E = [[Zr, -Zi], [Zi, Zr]] restricted to this rank's
+// columns j and n + j, stored as 2 ncols local columns (2n rows each).
+__global__ void embed_complex_cols_kernel(const double* __restrict__ zr, const double* __restrict__ zi,
+                                          int64_t ldz, int64_t n, int64_t ncols, double* __restrict__ E,
+                                          int64_t lde) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n * ncols;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = e / n, i = e % n;
+    const double a = zr[j * ldz + i], b = zi[j * ldz + i];
+    E[j * lde + i] = a;
+    E[j * lde + n + i] = b;
+    E[(ncols + j) * lde + i] = -b;
+    E[(ncols + j) * lde + n + i] = a;
   }
 }
 
@@ -259,15 +276,16 @@ struct CgState {
   int done, iters;
 };
 
-// ypart[c][i] = sum_{j in chunk c} Z[i, j] p_j (column-major Z, 2 rows per thread).
-__global__ void __launch_bounds__(256) cg_zp_kernel(const double* __restrict__ Z, int64_t ld, int64_t m,
-                                                    const double* __restrict__ p, double* __restrict__ ypart,
-                                                    const CgState* st) {
+// ypart[c][i] = sum_{j in chunk c} Z[i, j] p_j (column-major Z, rows x cols, 2 rows per
+// thread). One rank: rows == cols (square Z); column shards: cols = the local columns.
+__global__ void __launch_bounds__(256) cg_zp_kernel(const double* __restrict__ Z, int64_t ld, int64_t rows,
+                                                    int64_t cols, const double* __restrict__ p,
+                                                    double* __restrict__ ypart, const CgState* st) {
   if (st->done) return;
   const int64_t i = int64_t(blockIdx.x) * kZpRows + 2 * threadIdx.x;
   const int64_t j0 = int64_t(blockIdx.y) * kZpCols;
-  const int64_t j1 = j0 + kZpCols < m ? j0 + kZpCols : m;
-  if (i >= m) return;
+  const int64_t j1 = j0 + kZpCols < cols ? j0 + kZpCols : cols;
+  if (i >= rows) return;
   double a0 = 0.0, a1 = 0.0;
   const double* zc = Z + i;
   int64_t j = j0;
@@ -288,35 +306,35 @@ __global__ void __launch_bounds__(256) cg_zp_kernel(const double* __restrict__ Z
     a0 = __fma_rn(z0.x, pj, a0);
     a1 = __fma_rn(z0.y, pj, a1);
   }
-  double* out = ypart + int64_t(blockIdx.y) * (m + 2) + i;
+  double* out = ypart + int64_t(blockIdx.y) * (rows + 2) + i;
   out[0] = a0;
-  if (i + 1 < m) out[1] = a1;
+  if (i + 1 < rows) out[1] = a1;
 }
 
-__global__ void cg_yreduce_kernel(const double* __restrict__ ypart, int64_t m, int nchunks, double* __restrict__ y,
-                                  const CgState* st) {
+__global__ void cg_yreduce_kernel(const double* __restrict__ ypart, int64_t rows, int nchunks,
+                                  double* __restrict__ y, const CgState* st) {
   if (st->done) return;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < rows; i += int64_t(gridDim.x) * blockDim.x) {
     double s = 0.0;
-    for (int c = 0; c < nchunks; ++c) s += ypart[int64_t(c) * (m + 2) + i];
+    for (int c = 0; c < nchunks; ++c) s += ypart[int64_t(c) * (rows + 2) + i];
     y[i] = s;
   }
 }
 
 // q_j = Z[:, j] . y (warp per column, y zero beyond m) and per-CTA partials of p . q.
-__global__ void __launch_bounds__(256) cg_ztq_kernel(const double* __restrict__ Z, int64_t ld, int64_t m,
-                                                     const double* __restrict__ y, const double* __restrict__ p,
-                                                     double* __restrict__ q, double* __restrict__ partials,
-                                                     const CgState* st) {
+__global__ void __launch_bounds__(256) cg_ztq_kernel(const double* __restrict__ Z, int64_t ld, int64_t rows,
+                                                     int64_t cols, const double* __restrict__ y,
+                                                     const double* __restrict__ p, double* __restrict__ q,
+                                                     double* __restrict__ partials, const CgState* st) {
   if (st->done) return;
   __shared__ double red[8][4];
   const int lane = threadIdx.x & 31;
   const int64_t j = blockIdx.x * int64_t(8) + (threadIdx.x >> 5);
   double v[4] = {0.0, 0.0, 0.0, 0.0};
-  if (j < m) {
+  if (j < cols) {
     const double2* zc = reinterpret_cast<const double2*>(Z + j * ld);
     const double2* yy = reinterpret_cast<const double2*>(y);
-    const int64_t K2 = (m + 1) / 2;
+    const int64_t K2 = (rows + 1) / 2;
     double sx = 0.0, sy = 0.0;
     int64_t k = lane;
     for (; k + 96 < K2; k += 128) {
@@ -350,9 +368,19 @@ __device__ double cg_sum_partials(const double* __restrict__ partials, int64_t c
   return v[0];  // valid in thread 0
 }
 
-__global__ void cg_alpha_kernel(const double* __restrict__ partials, int64_t count, CgState* st) {
+// Column shards: the fixed-order local sum goes to out[0]; the all-reduce of it across
+// ranks is the `global` operand of the kernels below (nullptr: one rank, the partials).
+__global__ void cg_local_sum_kernel(const double* __restrict__ partials, int64_t count, double* out,
+                                    const CgState* st) {
+  if (st != nullptr && st->done) return;
+  const double s = cg_sum_partials(partials, count);
+  if (threadIdx.x == 0) out[0] = s;
+}
+
+__global__ void cg_alpha_kernel(const double* __restrict__ partials, int64_t count, CgState* st,
+                                const double* global) {
   if (st->done) return;
-  const double pq = cg_sum_partials(partials, count);
+  const double pq = global ? *global : cg_sum_partials(partials, count);
   if (threadIdx.x == 0) st->alpha = st->rr / pq;
 }
 
@@ -374,9 +402,10 @@ __global__ void cg_update_kernel(int64_t m, const double* __restrict__ p, const 
   if (threadIdx.x == 0) partials[blockIdx.x * 4] = v[0];
 }
 
-__global__ void cg_beta_kernel(const double* __restrict__ partials, int64_t count, CgState* st) {
+__global__ void cg_beta_kernel(const double* __restrict__ partials, int64_t count, CgState* st,
+                               const double* global) {
   if (st->done) return;
-  const double rr = cg_sum_partials(partials, count);
+  const double rr = global ? *global : cg_sum_partials(partials, count);
   if (threadIdx.x == 0) {
     st->beta = rr / st->rr;
     st->rr = rr;
@@ -408,8 +437,9 @@ __global__ void cg_init_kernel(int64_t m, const double* __restrict__ b, double* 
   if (threadIdx.x == 0) partials[blockIdx.x * 4] = v[0];
 }
 
-__global__ void cg_start_kernel(const double* __restrict__ partials, int64_t count, CgState* st) {
-  const double bb = cg_sum_partials(partials, count);
+__global__ void cg_start_kernel(const double* __restrict__ partials, int64_t count, CgState* st,
+                                const double* global) {
+  const double bb = global ? *global : cg_sum_partials(partials, count);
   if (threadIdx.x == 0) {
     st->rr = bb;
     st->bb = bb;
@@ -440,59 +470,76 @@ std::vector<double> deterministic_unit(int64_t n) {
 
 // The reference's inverse power iteration (solver.cpp:283-296) with the solves done
 // by CG on Z^T Z. Returns false (caller factors instead) if any inner solve misses
-// the tolerance within kCgMaxIters steps.
-bool sigma_min_cg(Ctx& c, int64_t m, int64_t n_start, const double* Z, int64_t ld, int max_iters, double tol,
-                  double* estimate, int* outer_steps, int* cg_steps) {
+// the tolerance within kCgMaxIters steps. Z is rows x cols; v0 is the start vector's
+// entries for these columns. With `comm` the columns are this rank's shard: y = Z p is
+// all-reduced over the ranks and every dot product is a local fixed-order sum followed
+// by an all-reduce, so all ranks take the same decisions (one rank: comm == nullptr,
+// rows == cols, the partials are summed directly).
+bool sigma_min_cg(Ctx& c, int64_t rows, int64_t cols, const std::vector<double>& v0, const double* Z, int64_t ld,
+                  int max_iters, double tol, Comm* comm, double* estimate, int* outer_steps, int* cg_steps) {
   cudaStream_t s = c.stream;
   const bool prof = std::getenv("IPT_PROFILE") != nullptr;
   auto wall = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   double t_mark = wall();
-  const int nchunks = static_cast<int>(ceil_div(m, kZpCols));
-  const int64_t vlen = m + 2;
-  DevBuf x, r, p, q, y, ypart, v, un, parts;
-  x.alloc(vlen);
-  r.alloc(vlen);
-  p.alloc(vlen);
-  q.alloc(vlen);
-  y.alloc(vlen);
-  v.alloc(vlen);
+  const int nchunks = static_cast<int>(std::max<int64_t>(1, ceil_div(cols, kZpCols)));
+  const int64_t clen = cols + 2, rlen = rows + 2;
+  DevBuf x, r, p, q, y, ypart, v, un, parts, glob;
+  x.alloc(clen);
+  r.alloc(clen);
+  p.alloc(clen);
+  q.alloc(clen);
+  v.alloc(clen);
+  y.alloc(rlen);
   un.alloc(1);
-  ypart.alloc(size_t(nchunks) * vlen, false);
-  const int64_t ztq_blocks = ceil_div(m, 8);
+  glob.alloc(4);
+  ypart.alloc(size_t(nchunks) * rlen, false);
+  const int64_t ztq_blocks = std::max<int64_t>(1, ceil_div(cols, 8));
   parts.alloc(size_t(std::max<int64_t>(ztq_blocks, kVecBlocks)) * 4);
   CgState* st = nullptr;
   IPT_CUDA(cudaMalloc(&st, sizeof(CgState)));
-  std::unique_ptr<CgState, void (*)(CgState*)> st_guard(st, [](CgState* p) { cudaFree(p); });
+  std::unique_ptr<CgState, void (*)(CgState*)> st_guard(st, [](CgState* pp) { cudaFree(pp); });
   CgState* h_st = reinterpret_cast<CgState*>(c.h_aux);  // pinned scratch
   static_assert(sizeof(CgState) <= 256, "pinned scratch too small");
-
-  std::vector<double> v0 = deterministic_unit(n_start);
-  IPT_CUDA(cudaMemcpyAsync(v.get(), v0.data(), sizeof(double) * n_start, cudaMemcpyHostToDevice, s));
+  if (cols > 0) IPT_CUDA(cudaMemcpyAsync(v.get(), v0.data(), sizeof(double) * cols, cudaMemcpyHostToDevice, s));
   if (prof) {
     c.sync();
     std::fprintf(stderr, "[ipt]   cg setup %.1f ms\n", 1e3 * (wall() - t_mark));
     t_mark = wall();
   }
-  const dim3 zp_grid(static_cast<unsigned>(ceil_div(m, kZpRows)), static_cast<unsigned>(nchunks));
+  const int sq = comm ? 1 : 0;
+  // all-reduced sum of the local partials into glob[slot] (column shards only)
+  auto global_sum = [&](int64_t count, int slot, const CgState* gate) -> const double* {
+    if (!comm) return nullptr;
+    cg_local_sum_kernel<<<1, 512, 0, s>>>(parts.get(), count, glob.get() + slot, gate);
+    count_launch();
+    comm->all_reduce(glob.get() + slot, 1, CommType::F64, CommOp::Sum, s);
+    return glob.get() + slot;
+  };
+  const dim3 zp_grid(static_cast<unsigned>(std::max<int64_t>(1, ceil_div(rows, kZpRows))), static_cast<unsigned>(nchunks));
   double rho = 0.0;
   int steps = 0, total_cg = 0;
   for (int it = 0; it < max_iters; ++it) {
     steps = it + 1;
-    cg_init_kernel<<<kVecBlocks, 256, 0, s>>>(m, v.get(), x.get(), r.get(), p.get(), parts.get());
-    cg_start_kernel<<<1, 512, 0, s>>>(parts.get(), kVecBlocks, st);
-    count_launch(2);
+    cg_init_kernel<<<kVecBlocks, 256, 0, s>>>(cols, v.get(), x.get(), r.get(), p.get(), parts.get());
+    count_launch();
+    cg_start_kernel<<<1, 512, 0, s>>>(parts.get(), kVecBlocks, st, global_sum(kVecBlocks, 0, nullptr));
+    count_launch();
     int done = 0;
     for (int k = 0; k < kCgMaxIters && !done; k += kCgBatch) {
       for (int b = 0; b < kCgBatch; ++b) {
-        cg_zp_kernel<<<zp_grid, 256, 0, s>>>(Z, ld, m, p.get(), ypart.get(), st);
-        cg_yreduce_kernel<<<kVecBlocks, 256, 0, s>>>(ypart.get(), m, nchunks, y.get(), st);
-        cg_ztq_kernel<<<static_cast<unsigned>(ztq_blocks), 256, 0, s>>>(Z, ld, m, y.get(), p.get(), q.get(),
+        cg_zp_kernel<<<zp_grid, 256, 0, s>>>(Z, ld, rows, cols, p.get(), ypart.get(), st);
+        cg_yreduce_kernel<<<kVecBlocks, 256, 0, s>>>(ypart.get(), rows, nchunks, y.get(), st);
+        count_launch(2);
+        if (comm) comm->all_reduce(y.get(), size_t(rows), CommType::F64, CommOp::Sum, s);
+        cg_ztq_kernel<<<static_cast<unsigned>(ztq_blocks), 256, 0, s>>>(Z, ld, rows, cols, y.get(), p.get(), q.get(),
                                                                         parts.get(), st);
-        cg_alpha_kernel<<<1, 512, 0, s>>>(parts.get(), ztq_blocks, st);
-        cg_update_kernel<<<kVecBlocks, 256, 0, s>>>(m, p.get(), q.get(), x.get(), r.get(), parts.get(), st);
-        cg_beta_kernel<<<1, 512, 0, s>>>(parts.get(), kVecBlocks, st);
-        cg_p_kernel<<<kVecBlocks, 256, 0, s>>>(m, r.get(), p.get(), st);
-        count_launch(7);
+        count_launch();
+        cg_alpha_kernel<<<1, 512, 0, s>>>(parts.get(), ztq_blocks, st, global_sum(ztq_blocks, 1, st));
+        cg_update_kernel<<<kVecBlocks, 256, 0, s>>>(cols, p.get(), q.get(), x.get(), r.get(), parts.get(), st);
+        count_launch(2);
+        cg_beta_kernel<<<1, 512, 0, s>>>(parts.get(), kVecBlocks, st, global_sum(kVecBlocks, 2, st));
+        cg_p_kernel<<<kVecBlocks, 256, 0, s>>>(cols, r.get(), p.get(), st);
+        count_launch(2);
       }
       IPT_LAUNCH_CHECK();
       IPT_CUDA(cudaMemcpyAsync(h_st, st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
@@ -505,13 +552,16 @@ bool sigma_min_cg(Ctx& c, int64_t m, int64_t n_start, const double* Z, int64_t l
     }
     total_cg += h_st->iters;
     if (!done || !(h_st->rr <= kCgRelTol * kCgRelTol * h_st->bb)) return false;
-    norm2_kernel<<<1, 1024, 0, s>>>(x.get(), m, un.get());
-    normalize_kernel<<<kVecBlocks, 256, 0, s>>>(x.get(), v.get(), m, un.get());
-    count_launch(2);
+    norm2_kernel<<<1, 1024, 0, s>>>(x.get(), cols, un.get(), sq);
+    count_launch();
+    if (comm) comm->all_reduce(un.get(), 1, CommType::F64, CommOp::Sum, s);
+    normalize_kernel<<<kVecBlocks, 256, 0, s>>>(x.get(), v.get(), cols, un.get(), sq);
+    count_launch();
     IPT_LAUNCH_CHECK();
     double h_un = 0.0;
     IPT_CUDA(cudaMemcpyAsync(&h_un, un.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
     c.sync();
+    if (comm) h_un = std::sqrt(h_un);
     if (!std::isfinite(h_un) || h_un == 0.0) return false;
     if (it > 0 && std::fabs(h_un - rho) <= tol * h_un) {
       rho = h_un;
@@ -529,6 +579,7 @@ bool sigma_min_cg(Ctx& c, int64_t m, int64_t n_start, const double* Z, int64_t l
 
 double sigma_min_device(Ctx& c, int64_t n, const double* zr, const double* zi, int64_t ldz,
                         int max_iters, double tol) {
+  NvtxRange nvtx_("ipt:sigma_min");
   cudaStream_t s = c.stream;
   const bool cplx = zi != nullptr;
   const int64_t m = cplx ? 2 * n : n;
@@ -552,7 +603,9 @@ double sigma_min_device(Ctx& c, int64_t n, const double* zr, const double* zi, i
       const double t0 = wall();
       double est = 0.0;
       int outer = 0, inner = 0;
-      const bool ok = sigma_min_cg(c, m, n, Z, ld, max_iters, tol, &est, &outer, &inner);
+      std::vector<double> v0 = deterministic_unit(n);  // complex: the iteration from [v; 0]
+      v0.resize(m, 0.0);
+      const bool ok = sigma_min_cg(c, m, m, v0, Z, ld, max_iters, tol, nullptr, &est, &outer, &inner);
       if (prof)
         std::fprintf(stderr, "[ipt] sigma_min n=%lld: matrix-free CG %s, %.1f ms (%d outer steps, %d CG steps)\n",
                      static_cast<long long>(m), ok ? "converged" : "fell back", 1e3 * (wall() - t0), outer, inner);
@@ -691,8 +744,8 @@ double sigma_min_device(Ctx& c, int64_t n, const double* zr, const double* zi, i
       }
     }
     IPT_LAUNCH_CHECK();
-    norm2_kernel<<<1, 1024, 0, s>>>(u.get(), m, un.get());
-    normalize_kernel<<<296, 256, 0, s>>>(u.get(), v.get(), m, un.get());
+    norm2_kernel<<<1, 1024, 0, s>>>(u.get(), m, un.get(), 0);
+    normalize_kernel<<<296, 256, 0, s>>>(u.get(), v.get(), m, un.get(), 0);
     count_launch(2);
     IPT_LAUNCH_CHECK();
     double h_un = 0.0;
@@ -709,6 +762,39 @@ double sigma_min_device(Ctx& c, int64_t n, const double* zr, const double* zi, i
     std::fprintf(stderr, "[ipt] sigma_min n=%lld: cholesky %.1f ms, inverse iteration %.1f ms (%d steps)\n",
                  static_cast<long long>(m), 1e3 * (t_chol - t_syrk), 1e3 * (wall() - t_chol), iters_done);
   return 1.0 / std::sqrt(rho);
+}
+
+// Column shards (rank's columns [col0, col0 + ncols) of the n x n Z, column-major, ldz):
+// the same inverse iteration by CG with y = Z p all-reduced, so Z is never gathered.
+// *ok == false: CG missed its tolerance (the caller gathers Z for the factor path).
+double sigma_min_sharded(Ctx& c, int64_t n, int64_t col0, int64_t ncols, const double* zr, const double* zi,
+                         int64_t ldz, int max_iters, double tol, bool* ok) {
+  NvtxRange nvtx_("ipt:sigma_min_sharded");
+  cudaStream_t s = c.stream;
+  const bool cplx = zi != nullptr;
+  const std::vector<double> unit = deterministic_unit(n);
+  std::vector<double> v0(size_t(cplx ? 2 : 1) * ncols, 0.0);  // complex: [v; 0] restricted to columns j, n + j
+  for (int64_t j = 0; j < ncols; ++j) v0[j] = unit[col0 + j];
+  const double* Z = zr;
+  int64_t ld = ldz, rows = n, cols = ncols;
+  DevBuf E;
+  if (cplx) {
+    rows = 2 * n;
+    cols = 2 * ncols;
+    ld = round_up(rows, 16);
+    E.alloc(size_t(std::max<int64_t>(cols, 1)) * ld);
+    embed_complex_cols_kernel<<<1184, 256, 0, s>>>(zr, zi, ldz, n, ncols, E.get(), ld);
+    IPT_LAUNCH_CHECK();
+    count_launch();
+    Z = E.get();
+  }
+  double est = 0.0;
+  int outer = 0, inner = 0;
+  *ok = sigma_min_cg(c, rows, cols, v0, Z, ld, max_iters, tol, c.comm.get(), &est, &outer, &inner);
+  if (std::getenv("IPT_PROFILE"))
+    std::fprintf(stderr, "[ipt] sigma_min (column shards) n=%lld: CG %s (%d outer steps, %d CG steps)\n",
+                 static_cast<long long>(rows), *ok ? "converged" : "missed", outer, inner);
+  return est;
 }
 
 }  // namespace iptb

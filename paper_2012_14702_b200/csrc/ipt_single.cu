@@ -48,7 +48,9 @@ struct SingleProblem {
   int anchor_phase = 0;  // grouped CSR kernels: lane phase of the anchor row in its row group
   int64_t anchor = -1;
   // host copies needed to (re)build the anchor row for a new anchor
-  std::vector<int64_t> h_rowptr;
+  const int64_t* h_rowptr = nullptr;  // the caller's row offsets (or h_rowptr_copy)
+  std::vector<int64_t> h_rowptr_copy;
+  int64_t nnz_total = 0;
   const int32_t* h_cols = nullptr;
   const double *h_vals = nullptr, *h_valsi = nullptr, *h_dense = nullptr, *h_densei = nullptr;
   std::vector<int32_t> h_cols_copy;
@@ -1067,6 +1069,7 @@ void setup_peer_gather(SingleProblem& P, int64_t zlen) {
 }  // namespace
 
 void single_forget_host(SingleProblem& P) {
+  P.h_rowptr = nullptr;
   P.h_dense = P.h_densei = nullptr;
   P.h_cols = nullptr;
   P.h_vals = P.h_valsi = nullptr;
@@ -1101,6 +1104,7 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
                              const int32_t* cols, const double* val_re, const double* val_im,
                              bool keep_host_anchor_source, bool force_complex, int64_t row_begin,
                              int64_t row_end) {
+  NvtxRange nvtx_("ipt:single_upload");
   if (n <= 0) throw InvalidArgument("solve_single: empty problem");
   auto P = std::make_unique<SingleProblem>();
   P->ctx = &c;
@@ -1123,6 +1127,7 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
   const int64_t rows = P->r1 - P->r0;
   const int64_t vlen = P->chunk * c.nranks;
   cudaStream_t s = c.stream;
+  ProfMarks pm("single_upload");
   if (!csr) {
     P->lda = round_up(n, 16);
     P->A.alloc(size_t(std::max<int64_t>(rows, 1)) * P->lda);
@@ -1136,29 +1141,40 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
     P->h_dense = dense_re;
     P->h_densei = dense_im;
   } else {
-    for (int64_t i = 0; i < n; ++i)
-      if (rowptr[i + 1] < rowptr[i]) throw InvalidArgument("csr: row offsets must be non-decreasing");
     const int64_t b = rowptr[P->r0], e = rowptr[P->r1];
     const int64_t nnz = e - b;
+    // one pass: monotonicity check of all offsets and this rank's rebased offsets
     std::vector<int64_t> rp(rows + 1);
-    for (int64_t i = 0; i <= rows; ++i) rp[i] = rowptr[P->r0 + i] - b;
+    for (int64_t i = 0; i < n; ++i) {
+      if (rowptr[i + 1] < rowptr[i]) throw InvalidArgument("csr: row offsets must be non-decreasing");
+      if (i >= P->r0 && i <= P->r1) rp[i - P->r0] = rowptr[i] - b;
+    }
+    rp[rows] = e - b;
     int64_t* drp = nullptr;
     IPT_CUDA(cudaMalloc(&drp, sizeof(int64_t) * (rows + 1)));
     P->rowptr.reset(drp);
-    IPT_CUDA(cudaMemcpyAsync(drp, rp.data(), sizeof(int64_t) * (rows + 1), cudaMemcpyHostToDevice, s));
+    h2d_bytes(c, drp, rp.data(), sizeof(int64_t) * (rows + 1));
     int32_t* dc = nullptr;
     IPT_CUDA(cudaMalloc(&dc, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
     P->cols.reset(dc);
     P->vals.alloc(std::max<int64_t>(nnz, 1), false);
+    pm.mark("rowptr");
     if (nnz) {  // pinned staging: ~4x the pageable copy rate for the 1.6 GB of config 5
       h2d_bytes(c, dc, cols + b, sizeof(int32_t) * nnz);
       h2d_bytes(c, P->vals.get(), val_re + b, sizeof(double) * nnz);
     }
+    pm.mark("h2d");
     if (P->cplx && val_im) {
       P->valsi.alloc(std::max<int64_t>(nnz, 1), false);
       if (nnz) IPT_CUDA(cudaMemcpyAsync(P->valsi.get(), val_im + b, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
     }
-    P->h_rowptr.assign(rowptr, rowptr + n + 1);
+    P->nnz_total = rowptr[n] - rowptr[0];
+    if (keep_host_anchor_source) {
+      P->h_rowptr = rowptr;
+    } else {
+      P->h_rowptr_copy.assign(rowptr, rowptr + n + 1);
+      P->h_rowptr = P->h_rowptr_copy.data();
+    }
     if (keep_host_anchor_source) {
       P->h_cols = cols;
       P->h_vals = val_re;
@@ -1172,14 +1188,15 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
   }
   P->dre.alloc(n);
   P->dim.alloc(n);
-  IPT_CUDA(cudaMemcpyAsync(P->dre.get(), d_re, sizeof(double) * n, cudaMemcpyHostToDevice, s));
-  if (d_im) IPT_CUDA(cudaMemcpyAsync(P->dim.get(), d_im, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  h2d_bytes(c, P->dre.get(), d_re, sizeof(double) * n);
+  if (d_im) h2d_bytes(c, P->dim.get(), d_im, sizeof(double) * n);
   // z vectors padded to a multiple of 2 for the 16-byte GEMV loads (pad stays zero)
   const int64_t zlen = round_up(std::max(vlen, P->lda), 16);
   for (int b2 = 0; b2 < 2; ++b2) {
     P->z[b2].alloc(zlen);
     P->zi[b2].alloc(zlen);
   }
+  pm.mark("host_copies");
   setup_peer_gather(*P, zlen);
   P->w.alloc(zlen);
   P->wi.alloc(zlen);
@@ -1193,6 +1210,7 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
     IPT_CUDA(cudaMemset(cnt, 0, sizeof(unsigned)));
     P->tail_counter.reset(cnt);
   }
+  pm.mark("allocs");
   IPT_CUDA(cudaMalloc(&P->state, sizeof(LoopState)));
   c.sync();
   return P.release();
@@ -1200,20 +1218,13 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
 
 void single_free(SingleProblem* P) { delete P; }
 
-void single_reset(SingleProblem& P, int64_t anchor, const double* warm_re, const double* warm_im,
-                  int max_iter_hint, bool renormalize) {
-  Ctx& c = *P.ctx;
-  cudaStream_t s = c.stream;
-  if (anchor < 0 || anchor >= P.n) throw InvalidArgument("solver: anchor out of range");
-  if (anchor != P.anchor) {
-    P.anchor = anchor;
-    if (!P.cplx) upload_anchor_row(P);
-  }
+// Warm start: renormalised to z[anchor] = 1 (solver.cpp:39-43), uploaded.
+static void single_reset_warm(SingleProblem& P, int64_t anchor, const double* warm_re, const double* warm_im,
+                       bool renormalize) {
+  cudaStream_t s = P.ctx->stream;
   const int64_t n = P.n;
   std::vector<double> zr(n, 0.0), zi(n, 0.0);
-  if (warm_re == nullptr) {
-    zr[anchor] = 1.0;
-  } else if (!renormalize) {
+  if (!renormalize) {
     for (int64_t j = 0; j < n; ++j) {
       zr[j] = warm_re[j];
       zi[j] = warm_im ? warm_im[j] : 0.0;
@@ -1246,10 +1257,12 @@ void single_reset(SingleProblem& P, int64_t anchor, const double* warm_re, const
   fill_zero(s, P.zi[1].get(), P.zi[1].count);
   IPT_CUDA(cudaMemcpyAsync(P.z[0].get(), zr.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
   IPT_CUDA(cudaMemcpyAsync(P.zi[0].get(), zi.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
-  LoopState init{};
-  init.status = kMaxIterations;
-  init.scale_ak = 1.0;
-  IPT_CUDA(cudaMemcpyAsync(P.state, &init, sizeof(LoopState), cudaMemcpyHostToDevice, s));
+  P.ctx->sync();  // (zr / zi are about to go out of scope)
+}
+
+static void finish_reset(SingleProblem& P, int max_iter_hint) {
+  Ctx& c = *P.ctx;
+  cudaStream_t s = c.stream;
   if (P.trace_cap < max_iter_hint) {
     P.trace.alloc(max_iter_hint);
     P.trace_cap = max_iter_hint;
@@ -1264,7 +1277,35 @@ void single_reset(SingleProblem& P, int64_t anchor, const double* warm_re, const
   c.sync();
 }
 
+void single_reset(SingleProblem& P, int64_t anchor, const double* warm_re, const double* warm_im,
+                  int max_iter_hint, bool renormalize) {
+  NvtxRange nvtx_("ipt:single_reset");
+  Ctx& c = *P.ctx;
+  cudaStream_t s = c.stream;
+  if (anchor < 0 || anchor >= P.n) throw InvalidArgument("solver: anchor out of range");
+  if (anchor != P.anchor) {
+    P.anchor = anchor;
+    if (!P.cplx) upload_anchor_row(P);
+  }
+  if (warm_re == nullptr) {  // e_anchor, set on the device (no host vector of n doubles)
+    fill_zero(s, P.z[0].get(), P.z[0].count);
+    fill_zero(s, P.z[1].get(), P.z[1].count);
+    fill_zero(s, P.zi[0].get(), P.zi[0].count);
+    fill_zero(s, P.zi[1].get(), P.zi[1].count);
+    const double one = 1.0;
+    IPT_CUDA(cudaMemcpyAsync(P.z[0].get() + anchor, &one, sizeof(double), cudaMemcpyHostToDevice, s));
+  } else {
+    single_reset_warm(P, anchor, warm_re, warm_im, renormalize);
+  }
+  LoopState init{};
+  init.status = kMaxIterations;
+  init.scale_ak = 1.0;
+  IPT_CUDA(cudaMemcpyAsync(P.state, &init, sizeof(LoopState), cudaMemcpyHostToDevice, s));
+  finish_reset(P, max_iter_hint);
+}
+
 void single_iterate(SingleProblem& P, const ipt_params& prm, ipt_stats* stats) {
+  NvtxRange nvtx_("ipt:single_iterate");
   Ctx& c = *P.ctx;
   if (!(prm.tolerance > 0.0)) throw InvalidArgument("config: tolerance must be positive");
   if (prm.max_iterations <= 0) throw InvalidArgument("config: max_iterations must be positive");
@@ -1278,7 +1319,7 @@ void single_iterate(SingleProblem& P, const ipt_params& prm, ipt_stats* stats) {
   }
   // Iterations are enqueued in batches between host checks; iterations past the
   // decision exit at their first instruction (LoopState::done).
-  const int64_t bytes_per_it = P.csr ? (P.h_rowptr.empty() ? 0 : P.h_rowptr.back() * 12) : P.n * P.n * 8;
+  const int64_t bytes_per_it = P.csr ? P.nnz_total * 12 : P.n * P.n * 8;
   const int batch = bytes_per_it >= (int64_t(1) << 31) ? 2 : 32;
   IPT_CUDA(cudaEventRecord(c.ev[0], c.stream));
   while (P.enq < prm.max_iterations) {
@@ -1307,6 +1348,7 @@ void single_iterate(SingleProblem& P, const ipt_params& prm, ipt_stats* stats) {
 
 // Post-loop product, eigenvalue lambda = d_a + (Delta z)_a and residual (solver.cpp:83-91).
 void single_finalize(SingleProblem& P, ipt_stats* stats) {
+  NvtxRange nvtx_("ipt:single_finalize");
   Ctx& c = *P.ctx;
   P.wa_fresh = false;
   cudaStream_t s = c.stream;
@@ -1350,6 +1392,7 @@ void single_finalize(SingleProblem& P, ipt_stats* stats) {
 }
 
 void single_download(SingleProblem& P, double* z_re, double* z_im) {
+  NvtxRange nvtx_("ipt:single_download");
   Ctx& c = *P.ctx;
   const int cur = c.h_state->iterations & 1;
   if (z_re) IPT_CUDA(cudaMemcpy(z_re, P.z[cur].get(), sizeof(double) * P.n, cudaMemcpyDeviceToHost));
@@ -1394,6 +1437,7 @@ void single_run_steps(SingleProblem& P, int count, double* ms_total, double* ms_
 
 // kernels::matvec on device-resident data: y = Delta x (one pass, no epilogue).
 void single_matvec(SingleProblem& P, const double* x_re, const double* x_im, double* y_re, double* y_im) {
+  NvtxRange nvtx_("ipt:single_matvec");
   Ctx& c = *P.ctx;
   P.wa_fresh = false;
   cudaStream_t s = c.stream;
@@ -1565,6 +1609,7 @@ bool small_lu_solve(std::vector<double> a, int h, std::vector<double> b, std::ve
 
 void single_accelerated(SingleProblem& P, const ipt_params& prm, int memory, double residual_tol,
                         double regularization, ipt_stats* stats) {
+  NvtxRange nvtx_("ipt:single_accelerated");
   Ctx& c = *P.ctx;
   P.wa_fresh = false;
   if (P.cplx) throw InvalidArgument("solve_single_accelerated (device): real inputs only");

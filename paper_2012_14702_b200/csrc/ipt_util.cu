@@ -442,8 +442,8 @@ void h2d_rows_split(Ctx& c, double* dre, double* dim, int64_t dpitch, const doub
 // Planar device rows to interleaved complex host rows (sim == nullptr: imaginary parts 0),
 // the host workers interleaving out of the pinned staging buffer while the next chunk's
 // DMA runs.
-void d2h_rows_merge(Ctx& c, double* dst_c, const double* sre, const double* sim, int64_t spitch, int64_t rows,
-                    int64_t cols, cudaStream_t stream) {
+void d2h_rows_merge(Ctx& c, double* dst_c, int64_t dpitch, const double* sre, const double* sim, int64_t spitch,
+                    int64_t rows, int64_t cols, cudaStream_t stream) {
   if (rows <= 0 || cols <= 0) return;
   cudaStream_t st = stream ? stream : c.stream;
   ensure_staging(c);
@@ -469,15 +469,27 @@ void d2h_rows_merge(Ctx& c, double* dst_c, const double* sre, const double* sim,
     const int64_t r0 = k * per, nr = std::min(per, rows - r0);
     const double* re = c.stage[b];
     const double* im = c.stage[b] + half;
-    double* d0 = dst_c + 2 * r0 * cols;
     const int64_t total = nr * cols;
     const unsigned t = total >= (int64_t(1) << 16) ? host_pool().size() : 1u;
     const int64_t step = (total + t - 1) / t;
     auto work = [&](unsigned kk) {
       const int64_t a = int64_t(kk) * step, e = std::min(total, a + step);
-      for (int64_t q = a; q < e; ++q) {
-        d0[2 * q] = re[q];
-        d0[2 * q + 1] = sim ? im[q] : 0.0;
+      if (dpitch == cols) {  // whole rows: one flat range
+        double* d0 = dst_c + 2 * r0 * cols;
+        for (int64_t q = a; q < e; ++q) {
+          d0[2 * q] = re[q];
+          d0[2 * q + 1] = sim ? im[q] : 0.0;
+        }
+        return;
+      }
+      for (int64_t q = a; q < e;) {  // a column block: row segments
+        const int64_t row = q / cols, col = q % cols, len = std::min(e - q, cols - col);
+        double* d = dst_c + 2 * ((r0 + row) * dpitch + col);
+        for (int64_t t = 0; t < len; ++t) {
+          d[2 * t] = re[q + t];
+          d[2 * t + 1] = sim ? im[q + t] : 0.0;
+        }
+        q += len;
       }
     };
     if (t <= 1) work(0);

@@ -419,9 +419,16 @@ def apply_map_full(p: Partition, g: InverseGaps, Z, ctx: Optional[Context] = Non
 
 
 def solve_full(p: Partition, g: InverseGaps, config: IterationConfig = None, warm_start=None,
-               ctx: Optional[Context] = None, want_sigma_min: bool = True, product: str = "dmma") -> SpectrumResult:
+               ctx: Optional[Context] = None, want_sigma_min: bool = True, product: str = "dmma",
+               output: str = "root", out=None) -> SpectrumResult:
     """Fixed-point iteration of F from I (or a renormalised warm start), then the
-    closing product, |MZ - Z Lambda|_F and sigma_min (solver.cpp:180-273)."""
+    closing product, |MZ - Z Lambda|_F and sigma_min (solver.cpp:180-273).
+
+    With a communicator (column shards): output="root" gathers Z and the eigenvalues to
+    rank 0; output="local" has every rank write only its own columns into full-size
+    outputs -- pass out=(z_re, z_im|None, lam_re, lam_im|None), float64 C-contiguous arrays
+    that all ranks share (e.g. np.memmap on /dev/shm, or the same arrays across threads),
+    and no gather runs (IPT_OUTPUT_LOCAL_COLUMNS)."""
     config = config or IterationConfig()
     _validate(config)
     _check_sizes(p, g, 0)
@@ -435,15 +442,27 @@ def solve_full(p: Partition, g: InverseGaps, config: IterationConfig = None, war
             raise ValueError("solve_full: warm start size mismatch")
         wr, wi = _planar(warm_start)
     cx = _out_complex(p, warm_start)
-    root = ctx.rank == 0
-    zr = np.empty((n, n)) if root else None
-    zi = np.empty((n, n)) if (root and cx) else None
-    lr = np.empty(n) if root else None
-    li = np.empty(n) if (root and cx) else None
+    if output not in ("root", "local"):
+        raise ValueError("solve_full: output must be 'root' or 'local'")
+    local = output == "local"
+    root = ctx.rank == 0 or local
+    if out is not None:
+        zr, zi, lr, li = out
+        for a, shape in ((zr, (n, n)), (zi, (n, n)), (lr, (n,)), (li, (n,))):
+            if a is not None and (a.shape != shape or a.dtype != np.float64 or not a.flags.c_contiguous):
+                raise ValueError("solve_full: out arrays must be float64, C-contiguous, (n, n) / (n,)")
+        if cx and (zi is None or li is None):
+            raise ValueError("solve_full: complex results need the imaginary out arrays")
+    else:
+        zr = np.empty((n, n)) if root else None
+        zi = np.empty((n, n)) if (root and cx) else None
+        lr = np.empty(n) if root else None
+        li = np.empty(n) if (root and cx) else None
     if product not in ("dmma", "ozaki"):
         raise ValueError("solve_full: product must be 'dmma' or 'ozaki'")
     prm = _params(config, want_sigma_min=1 if want_sigma_min else 0,
-                  product=_lib.PRODUCT_OZAKI if product == "ozaki" else _lib.PRODUCT_DMMA)
+                  product=_lib.PRODUCT_OZAKI if product == "ozaki" else _lib.PRODUCT_DMMA,
+                  output_mode=_lib.OUTPUT_LOCAL_COLUMNS if local else _lib.OUTPUT_ROOT)
     st = _lib.Stats()
     tr = np.zeros(config.max_iterations) if config.record_trace else None
     tm = np.zeros(config.max_iterations) if config.record_trace else None

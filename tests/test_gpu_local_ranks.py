@@ -184,3 +184,59 @@ def test_a_rank_that_never_joins_fails_the_others_instead_of_hanging():
     with pytest.raises(RuntimeError, match="local comm"):
         ipt.solve_full(p, ipt.build_gaps(p), ipt.IterationConfig(tolerance=1e-12), ctx=ctxs[0])
     assert time.time() - t0 < 60
+
+
+def test_iteration_batch_is_the_same_on_every_rank():
+    """N = 5793 on 8 ranks: shards of 724 and 725 columns fall on either side of the
+    per-rank work threshold that sets how many maps are enqueued per host check. The
+    batch must follow the global shard width (ipt_full.cu full_iterate), or the ranks'
+    collective sequences diverge after convergence (wrong residual, then a hang)."""
+    n = 5793
+    assert n * 724 < 2048 * 2048 <= n * 725
+    p = synth.dense_uniform(n, 0.32 / np.sqrt(n), 11)
+    os.environ["IPT_LOCAL_COMM_TIMEOUT_S"] = "120"
+    try:
+        one, outs = _solve_full(p, 8)
+    finally:
+        del os.environ["IPT_LOCAL_COMM_TIMEOUT_S"]
+    _check_full(one, outs)
+
+
+@pytest.mark.parametrize("g", [2, 3])
+def test_local_column_output_writes_every_block_without_a_gather(g):
+    """IPT_OUTPUT_LOCAL_COLUMNS: every rank downloads its own columns of Z and its
+    eigenvalues into one shared host array (here: the same numpy arrays across the rank
+    threads; across processes a shared mapping) -- no gather to rank 0 -- and sigma_min is
+    computed on the shards (y = Z p all-reduced per CG step)."""
+    p = synth.dense_uniform(900, 0.02, 17)
+    gaps = ipt.build_gaps(p)
+    cfg = ipt.IterationConfig(tolerance=1e-12)
+    one = ipt.solve_full(p, gaps, cfg)
+    zr = np.full((900, 900), np.nan)
+    lr = np.full(900, np.nan)
+    ctxs = dist.local_contexts(g)
+    outs = dist.run_ranks(lambda c: ipt.solve_full(p, gaps, cfg, ctx=c, output="local", out=(zr, None, lr, None)),
+                          ctxs)
+    assert np.array_equal(zr, one.Z) and np.array_equal(lr, one.eigenvalues)
+    for o in outs:
+        assert o.iterations == one.iterations
+        assert o.min_singular_value_estimate == outs[0].min_singular_value_estimate  # the same on every rank
+    assert outs[0].min_singular_value_estimate == pytest.approx(one.min_singular_value_estimate, rel=1e-12)
+
+
+def test_local_column_output_complex():
+    rng = np.random.default_rng(21)
+    n = 260
+    d = np.arange(1, n + 1) + 0.2j * rng.random(n)
+    a = 0.01 * (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    np.fill_diagonal(a, 0)
+    p = ipt.Partition(d, a)
+    gaps = ipt.build_gaps(p)
+    cfg = ipt.IterationConfig(tolerance=1e-12)
+    one = ipt.solve_full(p, gaps, cfg)
+    zr, zi = np.full((n, n), np.nan), np.full((n, n), np.nan)
+    lr, li = np.full(n, np.nan), np.full(n, np.nan)
+    ctxs = dist.local_contexts(2)
+    outs = dist.run_ranks(lambda c: ipt.solve_full(p, gaps, cfg, ctx=c, output="local", out=(zr, zi, lr, li)), ctxs)
+    assert np.array_equal(zr + 1j * zi, one.Z) and np.array_equal(lr + 1j * li, one.eigenvalues)
+    assert outs[1].min_singular_value_estimate == pytest.approx(one.min_singular_value_estimate, rel=1e-12)

@@ -39,13 +39,12 @@ def test_reference_unit_tests_against_b200_library(product):
 
 
 def test_reference_acceptance_hot_path_criteria():
-    """Criteria 1, 2, 5 (hot path) and 4, 6, 7, 8 (off-path modules calling our solvers)
+    """Criteria 1, 2, 5, 9 (hot path) and 4, 6, 7, 8 (off-path modules calling our solvers)
     must pass. Criterion 3 (explorer, off-path, run on the reference's own CPU kernels)
     fails identically on the reference build (flip 0.8634, cardioid 30/32).
-    Criterion 9 is the reference's CPU cost model T_eig/T_mm per product in [0.5, 2]:
-    it passes on the B200 (0.53 per product measured) but sits at the lower edge, since
-    the first map from I needs no product and host<->device costs dominate at N = 1024,
-    so it is reported, not asserted."""
+    Criterion 9 is the reference's cost model T_eig/T_mm per product in [0.5, 2]; with the
+    left factor of kernels::matmul kept on the device across the bench repetitions it
+    measures 0.83 per product (was 0.53 when every matmul re-uploaded Delta)."""
     r = _run("acceptance_b200", 1800)
     _check_acceptance(r)
 
@@ -58,6 +57,6 @@ def test_reference_acceptance_with_the_ozaki_product():
 def _check_acceptance(r):
     print(r.stdout)
     status = {int(m.group(2)): m.group(1) for m in re.finditer(r"\[(PASS|FAIL)\] criterion (\d+)", r.stdout)}
-    for crit in (1, 2, 4, 5, 6, 7, 8):
+    for crit in (1, 2, 4, 5, 6, 7, 8, 9):
         assert status.get(crit) == "PASS", (crit, r.stdout)
     assert "flip 0.8634" in r.stdout  # criterion 3: same numbers as the reference build
