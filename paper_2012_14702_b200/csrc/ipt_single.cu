@@ -78,7 +78,7 @@ struct SingleProblem {
   int peer_kind = 0;
   // fused step tail: arrival counter of the map kernel's CTAs; w_a of z[enq & 1] already
   // formed by the previous step's tail (else the next step launches the anchor kernel)
-  std::unique_ptr<unsigned, void (*)(void*)> tail_counter{nullptr, [](void* p) { cudaFree(p); }};
+  unsigned* tail_counter = nullptr;  // inside `sums`
   bool wa_fresh = false;
   ~SingleProblem() {
     if (state) cudaFree(state);
@@ -919,7 +919,7 @@ void set_anchor_args(const SingleProblem& P, MapArgs& a) {
 
 void set_tail_args(SingleProblem& P, MapArgs& a, int mode, int k, const ipt_params& prm) {
   a.tail_mode = mode;
-  a.tail_counter = P.tail_counter.get();
+  a.tail_counter = P.tail_counter;
   a.tail_state = P.state;
   a.tail_sums = P.sums.get();
   a.tail_k = k;
@@ -1203,15 +1203,12 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
   P->wa.alloc(2);
   P->npart = std::max<int64_t>(map_blocks(*P), 1);
   P->partials.alloc(size_t(P->npart) * 4);
-  P->sums.alloc(5);  // 4 stop sums + a barrier token (single_reset)
-  {
-    unsigned* cnt = nullptr;
-    IPT_CUDA(cudaMalloc(&cnt, sizeof(unsigned)));
-    IPT_CUDA(cudaMemset(cnt, 0, sizeof(unsigned)));
-    P->tail_counter.reset(cnt);
-  }
-  pm.mark("allocs");
+  // 4 stop sums, a barrier token (single_reset) and the fused tail's arrival counter (a
+  // zeroed 8-byte slot: the counter is an unsigned in it)
+  P->sums.alloc(6);
+  P->tail_counter = reinterpret_cast<unsigned*>(P->sums.get() + 5);
   IPT_CUDA(cudaMalloc(&P->state, sizeof(LoopState)));
+  pm.mark("allocs");
   c.sync();
   return P.release();
 }
