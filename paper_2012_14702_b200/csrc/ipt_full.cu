@@ -684,7 +684,7 @@ void allreduce_sums(FullProblem& P, bool with_max) {
 }
 
 bool use_ozaki(const FullProblem& P) {
-  return P.product == IPT_PRODUCT_OZAKI && !P.sparse && P.oz_finite && P.n <= kOzakiMaxK;
+  return P.product == IPT_PRODUCT_OZAKI && !P.sparse && P.oz_finite && P.n <= kOzakiMaxK && P.ncols > 0;
 }
 
 int64_t map_partials(const FullProblem& P) { return use_ozaki(P) ? kOzakiGrid : num_partials(P); }
@@ -759,9 +759,11 @@ void enqueue_map(FullProblem& P, int k, const ipt_params& prm, cudaEvent_t ev_a 
     if (k == 0 && P.start_identity && P.delta_finite && identity_shortcut_enabled()) {
       const unsigned tiles = static_cast<unsigned>(gemm_tiles(P.n, P.ncols));
       if (ev_a) IPT_CUDA(cudaEventRecord(ev_a, c.stream));
-      map_identity_kernel<<<tiles, kGemmThreads, 0, c.stream>>>(g);
-      IPT_LAUNCH_CHECK();
-      count_launch();
+      if (tiles) {  // (a rank may own no column when g > n)
+        map_identity_kernel<<<tiles, kGemmThreads, 0, c.stream>>>(g);
+        IPT_LAUNCH_CHECK();
+        count_launch();
+      }
       if (ev_b) IPT_CUDA(cudaEventRecord(ev_b, c.stream));
     } else if (use_ozaki(P)) {
       ozaki_apply(P, zs, zd, 0, st, ev_a, ev_b);  // events around the INT8 GEMMs only
@@ -1026,7 +1028,7 @@ void full_reset(FullProblem& P, const double* warm_re, const double* warm_im, in
       IPT_LAUNCH_CHECK();
       count_launch();
     }
-  } else {
+  } else if (P.ncols > 0) {
     // Host row-major n x n -> this rank's column-major block: upload the row-major rows of
     // the column slice, then transpose on the device.
     for (int64_t j = 0; j < P.ncols && renormalize; ++j) {

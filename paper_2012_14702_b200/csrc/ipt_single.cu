@@ -100,8 +100,10 @@ constexpr int kRowsPerBlock = kGemvRows * kGemvWarps;
 // config 5 (N = 2^21, 64 nnz/row, profiles/r01_spmv_variants.txt): {8,4} 0.674 ms,
 // {16,4} 0.689, {16,6} 0.753, {32,2} 0.832, {8,8} 0.905. Warp-contiguous row groups
 // (spmv_group_kernel): 4 rows x 4 in flight 0.644 ms with L2 cache hints, 0.632 ms
-// without (default, variant 9); the memory ceiling of the same traffic is 0.518 ms
-// (profiles/r01_gather_probe.txt). IPT_SPMV_VARIANT selects another.
+// without (variant 9); with the next group's row offsets loaded while the current group
+// streams 0.627 ms (default, variant 16; round 2, with the fused step tail); the memory
+// ceiling of the same traffic is 0.517 ms (profiles/r01_gather_probe.txt).
+// IPT_SPMV_VARIANT selects another.
 // Variants 5-7: warp-contiguous row groups (spmv_group_kernel), lanes = 0 marks them,
 // u = entries in flight per lane, rows = rows per warp.
 struct SpmvVariant {
@@ -110,9 +112,10 @@ struct SpmvVariant {
 constexpr SpmvVariant kSpmvVariants[] = {{16, 4, 0, 5}, {8, 8, 0, 5}, {32, 2, 0, 5}, {8, 4, 0, 5}, {16, 6, 0, 5},
                                          {0, 4, 4, 4},  {0, 2, 8, 4}, {0, 2, 4, 5}, {0, 4, 4, 3},
                                          {0, 4, 4, 4},  {0, 4, 16, 3}, {0, 8, 4, 3},  {0, 4, 2, 4},
-                                         {0, 8, 2, 4},  {0, 8, 4, 4},  {0, 4, 8, 4}};
+                                         {0, 8, 2, 4},  {0, 8, 4, 4},  {0, 4, 8, 4},
+                                         {0, 4, 4, 4},  {0, 4, 4, 3},  {0, 2, 4, 5}};  // 16-18: + offset prefetch
 constexpr int kNumSpmvVariants = sizeof(kSpmvVariants) / sizeof(kSpmvVariants[0]);
-constexpr int kSpmvDefault = 9;  // warp-contiguous groups of 4 rows, 4 in flight, plain nc loads
+constexpr int kSpmvDefault = 16;  // warp-contiguous groups of 4 rows, 4 in flight, plain nc loads, offset prefetch
 inline int spmv_variant() {
   static const int v = [] {
     const char* e = std::getenv("IPT_SPMV_VARIANT");
@@ -262,12 +265,32 @@ __device__ __forceinline__ double ld_nc_f64(const double* p) {
   return v;
 }
 
+// Row offsets of the group starting at local row lr0: lane k <= R holds rowptr[lr0 + k]
+// (clamped at the end of the rows).
+template <int R>
+__device__ __forceinline__ long long group_offsets(const int64_t* __restrict__ rowptr, int64_t lr0, int64_t rows,
+                                                   int lane) {
+  return lane <= R ? rowptr[lr0 + lane < rows ? lr0 + lane : rows] : 0;
+}
+
+template <int R, int U, bool POL = true>
+__device__ __forceinline__ void group_row_sums_at(long long mine, const int32_t* __restrict__ cols,
+                                                  const double* __restrict__ vals, const double* __restrict__ z,
+                                                  int lane, uint64_t pol_stream, uint64_t pol_keep, double (&s)[R]);
+
 template <int R, int U, bool POL = true>
 __device__ __forceinline__ void group_row_sums(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
                                                const double* __restrict__ vals, const double* __restrict__ z,
                                                int64_t lr0, int64_t rows, int lane, uint64_t pol_stream,
                                                uint64_t pol_keep, double (&s)[R]) {
-  const long long mine = lane <= R ? rowptr[lr0 + lane < rows ? lr0 + lane : rows] : 0;
+  group_row_sums_at<R, U, POL>(group_offsets<R>(rowptr, lr0, rows, lane), cols, vals, z, lane, pol_stream, pol_keep,
+                               s);
+}
+
+template <int R, int U, bool POL>
+__device__ __forceinline__ void group_row_sums_at(long long mine, const int32_t* __restrict__ cols,
+                                                  const double* __restrict__ vals, const double* __restrict__ z,
+                                                  int lane, uint64_t pol_stream, uint64_t pol_keep, double (&s)[R]) {
   int64_t rb[R + 1];
 #pragma unroll
   for (int k = 0; k <= R; ++k) rb[k] = __shfl_sync(0xffffffffu, mine, k);
@@ -598,7 +621,7 @@ __global__ void __launch_bounds__(256, kSpmvMinBlocks) spmv_map_kernel(const int
   }
 }
 
-template <int MODE, int R, int U, int MINB, bool POL = true>
+template <int MODE, int R, int U, int MINB, bool POL = true, bool PF = false>
 __global__ void __launch_bounds__(256, MINB) spmv_group_kernel(const int64_t* __restrict__ rowptr,
                                                                          const int32_t* __restrict__ cols,
                                                                          const double* __restrict__ vals, MapArgs a) {
@@ -612,10 +635,20 @@ __global__ void __launch_bounds__(256, MINB) spmv_group_kernel(const int64_t* __
   // Persistent fixed grid: warp w of block b owns row groups (b*8 + w) + k*(grid*8).
   const int64_t groups = ceil_div(a.rows, int64_t(R));
   const int64_t nwarps = int64_t(gridDim.x) * 8;
-  for (int64_t grp = blockIdx.x * int64_t(8) + (threadIdx.x >> 5); grp < groups; grp += nwarps) {
+  // PF: the next group's row offsets load while this group streams (one dependent
+  // load off the critical path per group)
+  const int64_t first = blockIdx.x * int64_t(8) + (threadIdx.x >> 5);
+  long long next_off = PF && first < groups ? group_offsets<R>(rowptr, first * R, a.rows, lane) : 0;
+  for (int64_t grp = first; grp < groups; grp += nwarps) {
     const int64_t lr0 = grp * R;
     double sum[R];
-    group_row_sums<R, U, POL>(rowptr, cols, vals, a.z, lr0, a.rows, lane, pol_s, pol_k, sum);
+    if (PF) {
+      const long long off = next_off;
+      if (grp + nwarps < groups) next_off = group_offsets<R>(rowptr, (grp + nwarps) * R, a.rows, lane);
+      group_row_sums_at<R, U, POL>(off, cols, vals, a.z, lane, pol_s, pol_k, sum);
+    } else {
+      group_row_sums<R, U, POL>(rowptr, cols, vals, a.z, lr0, a.rows, lane, pol_s, pol_k, sum);
+    }
     if (lane < R && lr0 + lane < a.rows) {
       double w = sum[0];
 #pragma unroll
@@ -800,6 +833,9 @@ void launch_spmv(unsigned grid, cudaStream_t s, const int64_t* rowptr, const int
     case 13: spmv_group_kernel<MODE, 2, 8, 4, false><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
     case 14: spmv_group_kernel<MODE, 4, 8, 4, false><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
     case 15: spmv_group_kernel<MODE, 8, 4, 4, false><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 16: spmv_group_kernel<MODE, 4, 4, 4, false, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 17: spmv_group_kernel<MODE, 4, 4, 3, false, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 18: spmv_group_kernel<MODE, 4, 2, 5, false, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
 #undef IPT_SPMV
 #undef IPT_SPMVG
   }
@@ -940,6 +976,8 @@ void enqueue_real_map(SingleProblem& P, int src, const ipt_params* prm, double* 
   cudaStream_t s = P.ctx->stream;
   MapArgs a = map_args(P, src);
   if (tail_mode) set_tail_args(P, a, tail_mode, k, *prm);
+  // a rank without rows still runs one CTA when the tail writes its (zero) stop sums
+  const unsigned min_grid = tail_mode ? 1u : 0u;
   if (MODE == kMvFinal || MODE == kMvAccel) a.state = nullptr;
   if (fz_out) {
     a.fz = fz_out;
@@ -949,7 +987,7 @@ void enqueue_real_map(SingleProblem& P, int src, const ipt_params* prm, double* 
     a.schedule = prm->schedule;
     a.snap = 0.25 * prm->tolerance;
   }
-  const unsigned grid = static_cast<unsigned>(map_blocks(P));
+  const unsigned grid = std::max(static_cast<unsigned>(map_blocks(P)), min_grid);
   if (grid == 0) return;
   if (P.csr)
     launch_spmv<MODE>(grid, s, P.rowptr.get(), P.cols.get(), P.vals.get(), a);

@@ -240,3 +240,22 @@ def test_local_column_output_complex():
     outs = dist.run_ranks(lambda c: ipt.solve_full(p, gaps, cfg, ctx=c, output="local", out=(zr, zi, lr, li)), ctxs)
     assert np.array_equal(zr + 1j * zi, one.Z) and np.array_equal(lr + 1j * li, one.eigenvalues)
     assert outs[1].min_singular_value_estimate == pytest.approx(one.min_singular_value_estimate, rel=1e-12)
+
+
+@pytest.mark.parametrize("n", [1, 5, 9])
+def test_more_ranks_than_columns(n):
+    """g = 8 ranks on N = 1, 5, 9: some ranks own no column (full spectrum) / no row
+    (single pair); they still take part in every collective with zero contributions."""
+    p = synth.dense_uniform(n, 0.05, 3)
+    one, outs = _solve_full(p, 8)
+    _check_full(one, outs)
+    q = synth.dense_normal(max(n, 2))
+    one_s, outs_s = _solve_single(q, 8, cfg=ipt.IterationConfig(tolerance=1e-12))
+    for o in outs_s:
+        assert o.iterations == one_s.iterations
+        assert np.max(np.abs(o.z - one_s.z)) <= 1e-14
+    c = synth.csr_ci(max(n, 4) * 2, 2, 0.01, 1)
+    one_c, outs_c = _solve_single(c, 8)
+    for o in outs_c:
+        assert o.iterations == one_c.iterations
+        assert np.max(np.abs(o.z - one_c.z)) <= 1e-14
