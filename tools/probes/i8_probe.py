@@ -1,6 +1,6 @@
 """tcgen05 INT8 GEMM (ipt_i8_gemm): exactness against numpy and throughput.
 
-    python tools/i8_probe.py
+    python tools/probes/i8_probe.py
 """
 import ctypes as C
 import json
@@ -9,7 +9,7 @@ import sys
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_2012_14702_b200 as ipt  # noqa: E402
 from paper_2012_14702_b200 import _lib  # noqa: E402
 from paper_2012_14702_b200._lib import check  # noqa: E402

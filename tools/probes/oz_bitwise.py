@@ -1,13 +1,13 @@
 """Ozaki solve result for A/B comparison of two library builds (IPT_B200_LIB selects one).
 
-    IPT_B200_LIB=... python tools/oz_bitwise.py out.npz [n]
+    IPT_B200_LIB=... python tools/probes/oz_bitwise.py out.npz [n]
 """
 import os
 import sys
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_2012_14702_b200 as ipt  # noqa: E402
 from paper_2012_14702_b200 import synth  # noqa: E402
 

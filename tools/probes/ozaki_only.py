@@ -1,14 +1,14 @@
 """Ozaki-product map sequence: 2 untimed maps (the first from Z = I needs no product),
 then `steps` timed maps (also usable under ncu for launch lists).
 
-    python tools/ozaki_only.py N [steps]
+    python tools/probes/ozaki_only.py N [steps]
 """
 import ctypes as C
 import json
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_2012_14702_b200 as ipt  # noqa: E402
 from paper_2012_14702_b200 import _lib, synth  # noqa: E402
 from paper_2012_14702_b200._lib import check, dptr  # noqa: E402

@@ -1,14 +1,14 @@
 """Full-spectrum map with W = Delta Z by DMMA (FP64 tensor cores) vs Ozaki scheme II
 (tcgen05 INT8 datapath), configs 2/3 construction.
 
-    python tools/ozaki_probe.py 8192 16384 32768
+    python tools/probes/ozaki_probe.py 8192 16384 32768
 """
 import ctypes as C
 import json
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_2012_14702_b200 as ipt  # noqa: E402
 from paper_2012_14702_b200 import _lib, synth  # noqa: E402
 from paper_2012_14702_b200._lib import check, dptr  # noqa: E402

@@ -1,6 +1,6 @@
 """Time sigma_min (SYRK + blocked Cholesky + inverse iteration) on a near-identity Z.
 
-    IPT_PROFILE=1 python tools/sigma_probe.py 8192 32768
+    IPT_PROFILE=1 python tools/probes/sigma_probe.py 8192 32768
 """
 import os
 import sys
@@ -8,7 +8,7 @@ import time
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_2012_14702_b200 as ipt  # noqa: E402
 
 for n in [int(a) for a in sys.argv[1:]] or [8192]:
