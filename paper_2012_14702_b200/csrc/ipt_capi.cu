@@ -164,7 +164,11 @@ void solve_full_impl(Ctx& c, const ipt_params* params, Open&& open, const double
     // device iterates, instead of inside the download.
     std::future<void> touch;
     const size_t zbytes = sizeof(double) * size_t(full_n(*P)) * size_t(full_n(*P));
-    if ((z_re || z_im) && zbytes >= (size_t(256) << 20))
+    // (only the rank that writes all of Z: with column-local output each rank writes its
+    // own columns into a shared mapping, and touching all of it would be n^2 of page work
+    // per rank)
+    const bool writes_all = c.nranks == 1 || (c.rank == 0 && prm.output_mode != IPT_OUTPUT_LOCAL_COLUMNS);
+    if ((z_re || z_im) && writes_all && zbytes >= (size_t(256) << 20))
       touch = std::async(std::launch::async, [z_re, z_im, zbytes] {
         if (z_re) prefault_host_async_part(z_re, zbytes);
         if (z_im) prefault_host_async_part(z_im, zbytes);
@@ -182,6 +186,7 @@ void solve_full_impl(Ctx& c, const ipt_params* params, Open&& open, const double
     std::future<void> early;
     float ms_thread = 0.f;  // the overlapped download itself (it runs beside the closing product)
     const bool overlap = (z_re || z_im) && full_can_download_early(*P);
+    full_prepare_closing(*P);  // (before the download staging reuses the previous iterate's buffer)
     if (overlap) {
       full_prepare_download(*P, z_re != nullptr, z_im != nullptr);
       const int dev = c.device;
@@ -493,6 +498,7 @@ int ipt_full_solve_interleaved_finish(ipt_ctx* ctx, ipt_full_problem* prob, cons
     const bool overlap = z_c && full_can_download_early(P);
     std::future<void> early;
     float ms_thread = 0.f;
+    full_prepare_closing(P);  // (before the download staging reuses the previous iterate's buffer)
     if (overlap) {
       full_prepare_download(P, true, full_is_complex(P));
       const int dev = c.device;

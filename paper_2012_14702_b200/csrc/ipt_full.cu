@@ -74,6 +74,9 @@ struct FullProblem {
   DevBuf oz_dt;     // Delta transposed (the split-off diagonal term reads Delta_ij by column)
   DevBuf oz_mods;   // device int: moduli the current product needs
   bool oz_split = true;
+  // K16 closing residual from the last map + an INT8 correction (ipt_closing.cu)
+  ClosingWork closing;
+  bool closing_on = false;
   ~FullProblem() {
     if (state) cudaFree(state);
   }
@@ -1077,6 +1080,7 @@ void full_reset(FullProblem& P, const double* warm_re, const double* warm_im, in
   P.enq = 0;
   P.finalized = false;
   P.gathered.release();
+  P.closing_on = false;
 }
 
 // The Ozaki product needs residue planes of Delta, Z and the products (16 bytes per
@@ -1180,6 +1184,31 @@ static const double* final_colmajor_z(FullProblem& P) {
   return P.zcm;
 }
 
+// K16 (ipt_closing.cu): after a converged loop with a small last step the closing residual
+// needs no second FP64 product -- the last map's product plus an INT8 tensor-core correction
+// Delta (Z_new - Z_old) give it. Its inputs are taken here, while Z_old (the other ping-pong
+// buffer) is still intact: callers that stage a download in that buffer call this first.
+// IPT_CLOSING=exact keeps the full closing product.
+void full_prepare_closing(FullProblem& P) {
+  Ctx& c = *P.ctx;
+  if (P.closing_on || P.sparse || P.cplx || !P.delta_finite) return;
+  const char* e = std::getenv("IPT_CLOSING");
+  if (e && std::strcmp(e, "exact") == 0) return;
+  IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  const LoopState& h = *c.h_state;
+  if (h.iterations < 1 || h.status != kConverged || !(h.final_step <= 1e-6) || P.n < 512 || P.n > (int64_t(1) << 17))
+    return;
+  cudaStream_t s = c.stream;
+  ProfMarks pm("closing_prepare");
+  if (!P.closing.delta_ready) P.closing.delta_digits(s, P.A1.get(), P.lda, P.n);
+  pm.mark("delta_digits", true);
+  const int cur = h.iterations & 1;
+  P.closing.step_digits(s, P.Z[cur].get(), P.Z[cur ^ 1].get(), P.ldz, P.ncols, P.wd.get());
+  pm.mark("step_digits", true);
+  P.closing_on = true;
+}
+
 // Closing product: Lambda and |MZ - Z Lambda|_F (solver.cpp:252-270), then the
 // eigenvector gather to rank 0 and sigma_min (solver.cpp:271) on rank 0.
 void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
@@ -1189,8 +1218,15 @@ void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
   IPT_CUDA(cudaMemcpyAsync(c.h_state, P.state, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
   c.sync();
   const double* z = current_z(P);
+  full_prepare_closing(P);
   IPT_CUDA(cudaEventRecord(c.ev[0], s));
-  if (P.sparse) {
+  int64_t nparts = map_partials(P);
+  if (P.closing_on) {
+    launch_diag(P, P.A1.get(), z, P.wd.get(), P.lam.get(), P.dre.get(), nullptr);  // wd_new, Lambda
+    P.closing.residual(s, z, P.ldz, P.col0, P.wd.get(), P.partials.get());
+    nparts = closing_partials();
+    P.closing_on = false;
+  } else if (P.sparse) {
     launch_sparse_diag(P, z, P.lam.get(), nullptr);
     launch_spmm(P, 1, z, nullptr, nullptr);
   } else if (!P.cplx && use_ozaki(P)) {
@@ -1204,7 +1240,7 @@ void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats) {
   } else {
     launch_complex_products(P, z, nullptr, kGemmResidC, nullptr, nullptr, nullptr);
   }
-  reduce_partials(s, P.partials.get(), map_partials(P), P.sums.get(), nullptr);
+  reduce_partials(s, P.partials.get(), nparts, P.sums.get(), nullptr);
   allreduce_sums(P, false);
   double h4[4];
   IPT_CUDA(cudaMemcpyAsync(h4, P.sums.get(), sizeof(h4), cudaMemcpyDeviceToHost, s));

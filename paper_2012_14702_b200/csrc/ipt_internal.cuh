@@ -172,6 +172,9 @@ void full_reset(FullProblem& P, const double* warm_re, const double* warm_im, in
                 bool renormalize = true);
 void full_iterate(FullProblem& P, const ipt_params& prm, ipt_stats* stats);
 void full_finalize(FullProblem& P, const ipt_params& prm, ipt_stats* stats);
+// Takes the closing residual's inputs (K16) while the previous iterate is intact; call it
+// before anything reuses the other ping-pong buffer (full_prepare_download).
+void full_prepare_closing(FullProblem& P);
 void full_download(FullProblem& P, double* z_re, double* z_im, double* lam_re, double* lam_im);
 // Single-rank dense problems after full_iterate: Z to the host on ctx.stream2, safe to run
 // on another host thread while full_finalize uses ctx.stream (both only read Z).
@@ -185,6 +188,23 @@ void full_set_product(FullProblem& P, int product);
 int full_ozaki_moduli(FullProblem& P);
 bool full_is_complex(const FullProblem& P);
 void full_run_maps(FullProblem& P, int count, double* ms_total, double* ms_gemm);
+
+// Closing residual of a converged real dense full-spectrum solve from the last map and
+// an INT8 tensor-core correction (ipt_closing.cu, K16): Delta's digits once per problem,
+// the last step's digits after the loop (while Z_old is intact), then the residual.
+struct ClosingWork {
+  DevBuf adig, aexp;           // Delta: arows x 2 kpad int8 ([lo | hi]), int exponent per row
+  DevBuf zdig, zexp, wd_old;   // the step D = Z_new - Z_old: mpad x 2 kpad ([hi | lo]), per column
+  int64_t n = 0, kpad = 0, arows = 0, ncols = 0, mpad = 0;
+  bool delta_ready = false, step_ready = false;
+  void delta_digits(cudaStream_t s, const double* A, int64_t lda, int64_t n);
+  void step_digits(cudaStream_t s, const double* znew, const double* zold, int64_t ldz, int64_t ncols,
+                   const double* wd_old_src);
+  // per-CTA partials {sum r^2, 0, 0, 0} of the local columns (closing_partials() of them)
+  void residual(cudaStream_t s, const double* znew, int64_t ldz, int64_t col0, const double* wd_new,
+                double* partials);
+};
+int64_t closing_partials();
 
 // Single-pair problem (ipt_single.cu)
 struct SingleProblem;
