@@ -52,9 +52,22 @@ void abort_entry_comm() {
   if (g_entry_ctx && g_entry_ctx->comm) g_entry_ctx->comm->abort();
 }
 
+// Per entry point: the context of this thread, and the stream DevBuf frees are ordered
+// after, are reset on the way out.
+struct EntryScope {
+  EntryScope() {
+    g_entry_ctx = nullptr;
+    set_release_stream(nullptr);
+  }
+  ~EntryScope() {
+    g_entry_ctx = nullptr;
+    set_release_stream(nullptr);
+  }
+};
+
 template <typename F>
 int guarded(F&& f) {
-  g_entry_ctx = nullptr;
+  EntryScope scope;
   try {
     f();
     return IPT_OK;
@@ -86,6 +99,7 @@ ipt_params params_or_default(const ipt_params* p) {
 void check_ctx(ipt_ctx* ctx) {
   if (ctx == nullptr) throw InvalidArgument("null ipt_ctx");
   g_entry_ctx = &ctx->c;
+  set_release_stream(ctx->c.stream);
 }
 
 // host row-major (rows x cols) -> device column-major with leading dimension ld (zero-padded dst)

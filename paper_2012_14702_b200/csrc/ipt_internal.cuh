@@ -128,6 +128,12 @@ void transpose_to_rowmajor(cudaStream_t s, const double* src_colmajor, int64_t l
 void fill_zero(cudaStream_t s, double* p, size_t count);
 // Return the stream-ordered pool's cached (freed) memory to the device.
 void release_cached_device_memory(int device);
+// Stream that DevBuf::release orders its free after: the library stream of the entry point
+// running on this thread (set for the duration of each C-ABI call that takes a context),
+// else the legacy stream. A buffer freed while a kernel on the library stream still reads
+// it is then not handed to another allocation (another rank's thread, or a later
+// allocation on the legacy stream) before that kernel completes.
+void set_release_stream(cudaStream_t s);
 void reduce_partials(cudaStream_t s, const double* partials, int64_t count, double* out4,
                      const LoopState* state);
 void scale_copy(cudaStream_t s, const double* src, double* dst, size_t count, double factor);

@@ -37,9 +37,12 @@ ProfMarks::~ProfMarks() {
 
 // Device buffers come from the stream-ordered pool (cudaMallocAsync on the legacy
 // stream) so the many small, short-lived buffers of the kernels:: / apply_map entry
-// points do not pay cudaMalloc / cudaFree (a device-wide sync) per call. Every entry
-// point synchronises the library stream before its buffers are released, so a free on
-// the legacy stream never races a kernel still reading the buffer.
+// points do not pay cudaMalloc / cudaFree (a device-wide sync) per call. A buffer is
+// freed in stream order after the calling entry point's library stream
+// (set_release_stream), so a scratch buffer that goes out of scope while a kernel on
+// that stream still reads it is not reused before the kernel completes (this raced
+// between ranks sharing one device: the K16 closing residual read its int32 products
+// after another rank's allocation had been handed the same memory).
 namespace {
 void configure_pool_once() {
   static std::mutex mu;
@@ -68,6 +71,11 @@ void release_cached_device_memory(int device) {
   }
 }
 
+namespace {
+thread_local cudaStream_t g_release_stream = nullptr;
+}
+void set_release_stream(cudaStream_t s) { g_release_stream = s; }
+
 void DevBuf::alloc(size_t n, bool zero) {
   release();
   if (n == 0) n = 1;
@@ -90,7 +98,7 @@ void DevBuf::alloc_plain(size_t n) {
 void DevBuf::release() {
   if (p) {
     if (plain) cudaFree(p);
-    else cudaFreeAsync(p, nullptr);
+    else cudaFreeAsync(p, g_release_stream);
   }
   p = nullptr;
   plain = false;
