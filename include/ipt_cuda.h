@@ -348,6 +348,16 @@ int ipt_single_debug_peer_z(ipt_single_problem* prob, int32_t peer, int32_t buf,
 
 /* Counters for gpu_launches accounting: kernels this library has launched. */
 int64_t ipt_kernel_launch_count(void);
+/* Debug aid (compute-sanitizer is unavailable on the GPU pool): with IPT_GUARD=1 in the
+ * environment every device scratch / problem buffer is allocated with 4 KB guard zones of a
+ * byte pattern on both sides, checked when the buffer is released; this returns how many
+ * released buffers found a guard overwritten (an out-of-bounds write). */
+int64_t ipt_guard_violations(void);
+/* Buffers whose guard zones were checked so far (IPT_GUARD=1). */
+int64_t ipt_guard_checked(void);
+/* Negative control: writes one element past a 100-double buffer and returns how many new
+ * violations were detected (1 with IPT_GUARD=1, 0 without; -1 on a CUDA error). */
+int64_t ipt_guard_selftest(void);
 
 #ifdef __cplusplus
 }

@@ -261,6 +261,13 @@ void ipt_default_params(ipt_params* p) {
 }
 
 int64_t ipt_kernel_launch_count(void) { return g_launches.load(); }
+int64_t ipt_guard_violations(void) { return guard_violations(); }
+int64_t ipt_guard_checked(void) { return guard_checked(); }
+int64_t ipt_guard_selftest(void) {
+  int64_t r = -1;
+  if (guarded([&] { r = guard_selftest(); }) != IPT_OK) return -1;
+  return r;
+}
 
 int ipt_ctx_create(int device, ipt_ctx** out) {
   return guarded([&] {

@@ -134,6 +134,10 @@ void release_cached_device_memory(int device);
 // it is then not handed to another allocation (another rank's thread, or a later
 // allocation on the legacy stream) before that kernel completes.
 void set_release_stream(cudaStream_t s);
+// IPT_GUARD=1: out-of-bounds writes detected next to pool buffers (ipt_util.cu)
+int64_t guard_violations();
+int64_t guard_selftest();
+int64_t guard_checked();
 void reduce_partials(cudaStream_t s, const double* partials, int64_t count, double* out4,
                      const LoopState* state);
 void scale_copy(cudaStream_t s, const double* src, double* dst, size_t count, double factor);

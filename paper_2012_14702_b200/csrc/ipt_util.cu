@@ -10,6 +10,7 @@
 #include <condition_variable>
 #include <functional>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "ipt_internal.cuh"
@@ -76,10 +77,89 @@ thread_local cudaStream_t g_release_stream = nullptr;
 }
 void set_release_stream(cudaStream_t s) { g_release_stream = s; }
 
+// Guard zones (IPT_GUARD=1; compute-sanitizer is not available on this pool): every pool
+// buffer gets kGuardDoubles of a byte pattern before and after it; the release checks
+// both zones after a device synchronisation and counts a violation (an out-of-bounds
+// write by some kernel near this buffer) in ipt_guard_violations(). Off by default.
+namespace {
+constexpr size_t kGuardDoubles = 512;  // 4 KB each side
+constexpr unsigned char kGuardByte = 0xA5;
+bool guard_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("IPT_GUARD");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+std::mutex g_guard_mu;
+std::unordered_map<const double*, std::pair<double*, size_t>> g_guard_bufs;  // p -> (base, doubles)
+std::atomic<int64_t> g_guard_bad{0};
+std::atomic<int64_t> g_guard_checked{0};
+
+bool guard_release(double* p) {
+  double* base = nullptr;
+  size_t n = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    auto it = g_guard_bufs.find(p);
+    if (it == g_guard_bufs.end()) return false;
+    base = it->second.first;
+    n = it->second.second;
+    g_guard_bufs.erase(it);
+  }
+  cudaDeviceSynchronize();
+  std::vector<unsigned char> h(2 * kGuardDoubles * sizeof(double));
+  const size_t gb = kGuardDoubles * sizeof(double);
+  cudaMemcpy(h.data(), base, gb, cudaMemcpyDeviceToHost);
+  cudaMemcpy(h.data() + gb, base + kGuardDoubles + n, gb, cudaMemcpyDeviceToHost);
+  g_guard_checked.fetch_add(1);
+  for (size_t b = 0; b < h.size(); ++b)
+    if (h[b] != kGuardByte) {
+      g_guard_bad.fetch_add(1);
+      std::fprintf(stderr, "[ipt] guard violation: %s guard of a %zu-double buffer, byte %zu\n",
+                   b < gb ? "leading" : "trailing", n, b < gb ? gb - b : b - gb);
+      break;
+    }
+  cudaFree(base);
+  return true;
+}
+}  // namespace
+
+int64_t guard_violations() { return g_guard_bad.load(); }
+int64_t guard_checked() { return g_guard_checked.load(); }
+
+namespace {
+__global__ void write_past_end_kernel(double* p, int64_t n) { p[n] = 1.0; }
+}  // namespace
+
+// Negative control of the guard zones: one write one element past a 100-double buffer.
+int64_t guard_selftest() {
+  const int64_t before = guard_violations();
+  {
+    DevBuf b;
+    b.alloc(100);
+    write_past_end_kernel<<<1, 1>>>(b.get(), 100);
+    IPT_CUDA(cudaDeviceSynchronize());
+  }
+  return guard_violations() - before;
+}
+
 void DevBuf::alloc(size_t n, bool zero) {
   release();
   if (n == 0) n = 1;
   configure_pool_once();
+  if (guard_on()) {
+    double* base = nullptr;
+    IPT_CUDA(cudaMalloc(&base, (n + 2 * kGuardDoubles) * sizeof(double)));
+    IPT_CUDA(cudaMemset(base, kGuardByte, (n + 2 * kGuardDoubles) * sizeof(double)));
+    p = base + kGuardDoubles;
+    if (zero) IPT_CUDA(cudaMemset(p, 0, n * sizeof(double)));
+    IPT_CUDA(cudaDeviceSynchronize());
+    count = n;
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    g_guard_bufs[p] = {base, n};
+    return;
+  }
   IPT_CUDA(cudaMallocAsync(&p, n * sizeof(double), nullptr));
   count = n;
   if (zero) IPT_CUDA(cudaMemsetAsync(p, 0, n * sizeof(double), nullptr));
@@ -96,6 +176,11 @@ void DevBuf::alloc_plain(size_t n) {
   IPT_CUDA(cudaMemset(p, 0, n * sizeof(double)));
 }
 void DevBuf::release() {
+  if (p && !plain && guard_on() && guard_release(p)) {
+    p = nullptr;
+    count = 0;
+    return;
+  }
   if (p) {
     if (plain) cudaFree(p);
     else cudaFreeAsync(p, g_release_stream);

@@ -1,4 +1,9 @@
-"""Smoke-size workload for compute-sanitizer (one tool per gpurun call):
+"""Smoke-size workload for the memory-safety checks.
+
+compute-sanitizer is closed on this GPU pool; the library's own guard zones stand in for
+memcheck's out-of-bounds write detection (IPT_GUARD=1: 4 KB byte-pattern zones on both
+sides of every device buffer, checked at release; tests/test_gpu_guard.py runs this script
+that way and requires zero violations). Where compute-sanitizer is available:
 
     compute-sanitizer --tool memcheck  python tools/sanitize_smoke.py
     compute-sanitizer --tool racecheck python tools/sanitize_smoke.py
@@ -67,4 +72,15 @@ outs = dist.run_ranks(lambda c: ipt.solve_full(p, g, cfg, ctx=c), ctxs)
 assert np.array_equal(outs[0].Z, r.Z)
 outs = dist.run_ranks(lambda c: ipt.solve_single(q, gq, 0, ipt.IterationConfig(tolerance=1e-10), ctx=c), ctxs)
 assert np.array_equal(outs[0].z, s1.z)
-print(f"sanitize smoke ok: {lib.ipt_kernel_launch_count()} kernel launches")
+for c in ctxs:
+    c.close()
+del outs, r, rz, s1, s2, s3, f
+import gc  # noqa: E402
+
+gc.collect()
+ctx.close()
+bad = lib.ipt_guard_violations()
+print(f"sanitize smoke ok: {lib.ipt_kernel_launch_count()} kernel launches, guard zones checked on "
+      f"{lib.ipt_guard_checked()} buffers, guard violations {bad}"
+      f" (IPT_GUARD={os.environ.get('IPT_GUARD', '0')})")
+sys.exit(1 if bad else 0)
