@@ -97,6 +97,8 @@ const char* ipt_last_error(void);
 void ipt_default_params(ipt_params* p);
 
 /* ---- context: one CUDA device, one stream, optional NCCL communicator ---- */
+/* Number of visible CUDA devices. */
+int ipt_device_count(int* count);
 int ipt_ctx_create(int device, ipt_ctx** out);
 void ipt_ctx_destroy(ipt_ctx* ctx);
 int ipt_ctx_device(const ipt_ctx* ctx);

@@ -77,6 +77,7 @@ class Stats(C.Structure):
 SIGNATURES = {
     "ipt_last_error": (C.c_char_p, []),
     "ipt_default_params": (None, [C.POINTER(Params)]),
+    "ipt_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "ipt_ctx_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
     "ipt_ctx_destroy": (None, [_vp]),
     "ipt_ctx_device": (C.c_int, [_vp]),

@@ -269,6 +269,13 @@ int64_t ipt_guard_selftest(void) {
   return r;
 }
 
+int ipt_device_count(int* count) {
+  return guarded([&] {
+    if (count == nullptr) throw InvalidArgument("ipt_device_count: null out");
+    IPT_CUDA(cudaGetDeviceCount(count));
+  });
+}
+
 int ipt_ctx_create(int device, ipt_ctx** out) {
   return guarded([&] {
     if (out == nullptr) throw InvalidArgument("ipt_ctx_create: null out");

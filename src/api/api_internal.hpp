@@ -10,6 +10,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <functional>
 #include <vector>
 
 #include "ipt/complex_matrix.hpp"
@@ -19,6 +20,14 @@ namespace ipt::api {
 
 ipt_ctx* context();  // thread-local, created on first use
 void set_device(int device);
+// Several GPUs in this process (IPT_DEVICES, b200::set_devices): the device list, the
+// calling thread's contexts joined by the in-process communicator (empty below two ranks),
+// and f(rank, ctx) on one host thread per rank (rank 0 on the caller's), rethrowing the
+// first rank's own error.
+void set_devices(const std::vector<int>& devices);
+std::vector<int> devices();
+std::vector<ipt_ctx*> group_contexts();
+void run_ranks(const std::vector<ipt_ctx*>& ctxs, const std::function<void(int, ipt_ctx*)>& f);
 
 inline void check(int rc) {
     if (rc == IPT_OK) return;

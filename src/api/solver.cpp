@@ -3,9 +3,15 @@
 // product, map application and reduction runs on the device via include/ipt_cuda.h.
 #include "ipt/solver.hpp"
 
+#include <algorithm>
 #include <cstdlib>
+#include <exception>
 #include <future>
 #include <memory>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
 
 #include "api_internal.hpp"
 #include "ipt/kernels.hpp"
@@ -27,6 +33,117 @@ thread_local CtxHolder t_ctx;
 }  // namespace
 
 void set_device(int device) { t_device = device; }
+
+// ---- one process, several GPUs (IPT_DEVICES / b200::set_devices) -----------------------
+// The column-sharded full spectrum and the row-sharded CSR single pair run with the ranks
+// as contexts of this process, one host thread per rank, joined by the library's in-process
+// communicator (peer copies / peer stores over NVLink between devices; collectives are
+// event-ordered, so a device may also host several ranks). Each rank writes its own
+// columns of Z straight into the caller's result (IPT_OUTPUT_LOCAL_COLUMNS).
+namespace {
+thread_local bool t_devices_set = false;
+thread_local std::vector<int> t_devices;
+struct GroupHolder {
+    std::vector<int> devices;
+    std::vector<ipt_ctx*> ctxs;
+    ipt_local_group* group = nullptr;
+    void reset() {
+        for (ipt_ctx* c : ctxs) ipt_ctx_destroy(c);
+        ctxs.clear();
+        if (group) ipt_local_group_destroy(group);  // after every member context
+        group = nullptr;
+        devices.clear();
+    }
+    ~GroupHolder() { reset(); }
+};
+thread_local GroupHolder t_group;
+}  // namespace
+
+void set_devices(const std::vector<int>& devices) {
+    t_devices = devices;
+    t_devices_set = !devices.empty();  // an empty list returns to $IPT_DEVICES
+}
+
+std::vector<int> devices() {
+    if (t_devices_set) return t_devices;
+    std::vector<int> out;
+    const char* env = std::getenv("IPT_DEVICES");
+    if (env == nullptr || *env == 0) return out;
+    const std::string s(env);
+    if (s == "all") {
+        int count = 0;
+        check(ipt_device_count(&count));
+        for (int d = 0; d < count; ++d) out.push_back(d);
+        return out;
+    }
+    std::stringstream ss(s);
+    std::string item;
+    while (std::getline(ss, item, ',')) {
+        std::size_t used = 0;
+        int d = -1;
+        try {
+            d = std::stoi(item, &used);
+        } catch (const std::exception&) {
+            used = 0;
+        }
+        if (used == 0 || used != item.size() || d < 0)
+            throw std::invalid_argument("IPT_DEVICES: expected 'all' or a comma-separated list of device indices");
+        out.push_back(d);
+    }
+    return out;
+}
+
+std::vector<ipt_ctx*> group_contexts() {
+    const std::vector<int> devs = devices();
+    if (devs.size() < 2) return {};
+    if (t_group.devices != devs) {
+        t_group.reset();
+        check(ipt_local_group_create(static_cast<int>(devs.size()), &t_group.group));
+        for (std::size_t r = 0; r < devs.size(); ++r) {
+            ipt_ctx* c = nullptr;
+            check(ipt_ctx_create(devs[r], &c));
+            t_group.ctxs.push_back(c);
+            check(ipt_ctx_init_local_comm(c, t_group.group, static_cast<int>(r)));
+        }
+        t_group.devices = devs;
+    }
+    return t_group.ctxs;
+}
+
+void run_ranks(const std::vector<ipt_ctx*>& ctxs, const std::function<void(int, ipt_ctx*)>& f) {
+    const std::size_t g = ctxs.size();
+    std::vector<std::exception_ptr> err(g);
+    std::vector<std::thread> th;
+    for (std::size_t r = 1; r < g; ++r)
+        th.emplace_back([&, r] {
+            try {
+                f(static_cast<int>(r), ctxs[r]);
+            } catch (...) {
+                err[r] = std::current_exception();
+            }
+        });
+    try {
+        f(0, ctxs[0]);
+    } catch (...) {
+        err[0] = std::current_exception();
+    }
+    for (auto& t : th) t.join();
+    // report the rank that failed first-hand, not the ranks its abort released
+    std::exception_ptr first, any;
+    for (auto& e : err) {
+        if (!e) continue;
+        if (!any) any = e;
+        try {
+            std::rethrow_exception(e);
+        } catch (const std::exception& x) {
+            if (!first && std::string(x.what()).find("aborted") == std::string::npos) first = e;
+        } catch (...) {
+            if (!first) first = e;
+        }
+    }
+    if (first) std::rethrow_exception(first);
+    if (any) std::rethrow_exception(any);
+}
 
 ipt_ctx* context() {
     int dev = t_device;
@@ -116,7 +233,32 @@ EigenpairResult run_single(const Partition& p, std::size_t anchor, const Iterati
     Vec zr(n), zi(n);
     const double* wre = warm ? w.re.data() : nullptr;
     const double* wim = warm ? w.im_or_null() : nullptr;
-    if (p.delta.is_sparse()) {
+    const std::vector<ipt_ctx*> ranks = p.delta.is_sparse() ? api::group_contexts() : std::vector<ipt_ctx*>{};
+    if (!ranks.empty()) {
+        // CSR rows sharded over the multi-device group; the iterate is all-gathered every
+        // step (fused peer stores), so every rank ends with all of z: rank 0's is returned
+        const api::Csr c = api::to_csr(p.delta);
+        std::vector<ipt_stats> sts(ranks.size());
+        std::vector<std::vector<double>> traces(ranks.size(), trace);
+        std::vector<Vec> zrs(ranks.size()), zis(ranks.size());
+        api::run_ranks(ranks, [&](int rank, ipt_ctx* ctx) {
+            ipt_stats& s = sts[rank];
+            s = ipt_stats{};
+            s.trace = cfg.record_trace ? traces[rank].data() : nullptr;
+            Vec& r_re = rank == 0 ? zr : zrs[rank];
+            Vec& r_im = rank == 0 ? zi : zis[rank];
+            if (rank != 0) {
+                r_re.resize(n);
+                r_im.resize(n);
+            }
+            api::check(ipt_single_solve_csr(ctx, static_cast<int64_t>(n), d.re.data(), d.im_or_null(),
+                                            c.rowptr.data(), c.cols.data(), c.val.re.data(), c.val.im_or_null(),
+                                            static_cast<int64_t>(anchor), wre, wim, &prm, r_re.data(), r_im.data(),
+                                            &s));
+        });
+        st = sts[0];
+        trace = traces[0];
+    } else if (p.delta.is_sparse()) {
         const api::Csr c = api::to_csr(p.delta);
         api::check(ipt_single_solve_csr(api::context(), static_cast<int64_t>(n), d.re.data(), d.im_or_null(),
                                         c.rowptr.data(), c.cols.data(), c.val.re.data(), c.val.im_or_null(),
@@ -137,6 +279,69 @@ EigenpairResult run_single(const Partition& p, std::size_t anchor, const Iterati
     r.status = static_cast<SolveStatus>(st.status);
     r.matvec_count = static_cast<long>(st.product_count);
     if (cfg.record_trace) r.trace.assign(trace.begin(), trace.begin() + st.iterations);
+    return r;
+}
+
+
+// solve_full with the columns sharded over the calling thread's multi-device group: every
+// rank runs the same C-ABI solve on its context, writes its own columns of Z and Lambda into
+// the shared result, and reports the same global scalars (all-reduced).
+SpectrumResult solve_full_ranks(const Partition& p, const IterationConfig& config, ipt_params prm,
+                                const ComplexMatrix* warm_dense, const Planar& warm_planar,
+                                const std::vector<ipt_ctx*>& ranks) {
+    const std::size_t n = p.size();
+    const std::size_t g = ranks.size();
+    prm.output_mode = IPT_OUTPUT_LOCAL_COLUMNS;
+    std::vector<ipt_stats> sts(g);
+    std::vector<std::vector<double>> traces(g, std::vector<double>(config.record_trace ? config.max_iterations : 0));
+    SpectrumResult r;
+    if (p.delta.is_dense()) {
+        cvec zv;
+        std::shared_future<void> zready = std::async(std::launch::async, [&zv, n] { zv = cvec(n * n); }).share();
+        r.eigenvalues.resize(n);
+        api::run_ranks(ranks, [&](int rank, ipt_ctx* c) {
+            ipt_stats& st = sts[rank];
+            st = ipt_stats{};
+            st.trace = config.record_trace ? traces[rank].data() : nullptr;
+            ipt_full_problem* h = nullptr;
+            const int rc = ipt_full_solve_interleaved_start(
+                c, static_cast<int64_t>(n), reinterpret_cast<const double*>(p.d.data()),
+                reinterpret_cast<const double*>(p.delta.data()),
+                warm_dense ? reinterpret_cast<const double*>(warm_dense->data()) : nullptr, &prm, &h, &st);
+            zready.get();
+            api::check(rc);
+            std::unique_ptr<ipt_full_problem, void (*)(ipt_full_problem*)> hold(h, ipt_full_free);
+            api::check(ipt_full_solve_interleaved_finish(c, h, &prm, reinterpret_cast<double*>(zv.data()),
+                                                         reinterpret_cast<double*>(r.eigenvalues.data()), &st));
+        });
+        zready.get();
+        r.Z = ComplexMatrix::dense(n, n, std::move(zv));
+    } else {  // CSR Delta: the sparse-Delta map per rank
+        const Planar d = api::split(p.d.data(), n);
+        const api::Csr c = api::to_csr(p.delta);
+        Vec zr(n * n), zi(n * n), lr(n), li(n);
+        const double* wre = warm_dense ? warm_planar.re.data() : nullptr;
+        const double* wim = warm_dense ? warm_planar.im_or_null() : nullptr;
+        api::run_ranks(ranks, [&](int rank, ipt_ctx* ctx) {
+            ipt_stats& st = sts[rank];
+            st = ipt_stats{};
+            st.trace = config.record_trace ? traces[rank].data() : nullptr;
+            api::check(ipt_full_solve_csr(ctx, static_cast<int64_t>(n), d.re.data(), d.im_or_null(), c.rowptr.data(),
+                                          c.cols.data(), c.val.re.data(), c.val.im_or_null(), wre, wim, &prm,
+                                          zr.data(), zi.data(), lr.data(), li.data(), &st));
+        });
+        r.Z = ComplexMatrix::dense(n, n);
+        api::merge(zr, zi, r.Z.data());
+        r.eigenvalues = combine(lr, li);
+    }
+    const ipt_stats& st = sts[0];
+    r.iterations = st.iterations;
+    r.final_step = st.final_step;
+    r.residual_frobenius = st.residual;
+    r.min_singular_value_estimate = st.min_singular_value_estimate;
+    r.status = static_cast<SolveStatus>(st.status);
+    r.matmul_count = static_cast<long>(st.product_count);
+    if (config.record_trace) r.trace.assign(traces[0].begin(), traces[0].begin() + st.iterations);
     return r;
 }
 
@@ -205,6 +410,8 @@ ComplexMatrix apply_map_full(const Partition& p, const InverseGaps& g, const Com
 namespace b200 {
 
 void set_device(int device) { api::set_device(device); }
+void set_devices(const std::vector<int>& devices) { api::set_devices(devices); }
+int devices_in_use() { return std::max<int>(1, static_cast<int>(api::devices().size())); }
 
 EigenpairResult solve_single_accelerated(const Partition& p, const InverseGaps& g, std::size_t anchor,
                                          const IterationConfig& config, int memory) {
@@ -269,6 +476,8 @@ SpectrumResult solve_full(const Partition& p, const InverseGaps& g, const Iterat
     ipt_stats st{};
     std::vector<double> trace(config.record_trace ? config.max_iterations : 0);
     st.trace = config.record_trace ? trace.data() : nullptr;
+    const std::vector<ipt_ctx*> ranks = api::group_contexts();
+    if (!ranks.empty()) return solve_full_ranks(p, config, prm, warm_start ? &wd : nullptr, w, ranks);
     if (p.delta.is_dense()) {
         // The carrier's interleaved std::complex arrays go to the C ABI as they are (the
         // de-interleave happens inside the pinned staging pass); the result carrier is

@@ -9,6 +9,10 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <algorithm>
+#include <tuple>
+#include <utility>
+#include <vector>
 
 #include <ipt/anderson.hpp>
 #include <ipt/complex_matrix.hpp>
@@ -231,4 +235,79 @@ TEST_CASE("solve_single_accelerated on complex inputs (host mixing, device produ
     CHECK(acc.matvec_count < plain.matvec_count);
     CHECK(acc.z[3] == ipt::cplx(1.0));
     CHECK(ipt::kernels::resident_operator_count() >= 1);  // Delta stayed on the device
+}
+
+namespace {
+
+// symmetric CSR, `per_row` random off-diagonal columns per row (symmetrised), CI-like diagonal
+ipt::Partition ci_like(std::size_t n, int per_row, std::uint64_t seed) {
+    std::uint64_t x = seed;
+    auto next = [&x] {
+        x = x * 6364136223846793005ull + 1442695040888963407ull;
+        return x >> 11;
+    };
+    std::vector<ipt::Triplet> t;
+    std::vector<std::vector<char>> seen(n);
+    for (std::size_t i = 0; i < n; ++i) t.push_back({i, i, ipt::cplx(10.0 * std::log1p(double(i)) + 0.5 * double(next() % 1000) / 1000.0, 0.0)});
+    std::vector<std::pair<std::size_t, std::size_t>> pairs;
+    for (std::size_t i = 0; i < n; ++i)
+        for (int k = 0; k < per_row; ++k) {
+            const std::size_t j = next() % n;
+            if (j != i) pairs.emplace_back(std::min(i, j), std::max(i, j));
+        }
+    std::sort(pairs.begin(), pairs.end());
+    pairs.erase(std::unique(pairs.begin(), pairs.end()), pairs.end());
+    for (const auto& [i, j] : pairs) {
+        const double v = 0.01 * (double(next() % 2000) / 1000.0 - 1.0);
+        t.push_back({i, j, ipt::cplx(v, 0.0)});
+        t.push_back({j, i, ipt::cplx(v, 0.0)});
+    }
+    return ipt::partition(ipt::ComplexMatrix::sparse_from_triplets(n, n, t));
+}
+
+}  // namespace
+
+TEST_CASE("b200::set_devices: the sharded solves reproduce one GPU bit for bit") {
+    // Ranks of one process joined by the in-process communicator; on this one-GPU pool the
+    // device is listed several times (the ranks time-share it), on a node every GPU once.
+    const ipt::Partition p = near_diagonal(1000, 0.3 / std::sqrt(1000.0), 31);  // uneven shards for 3
+    const ipt::InverseGaps g = ipt::build_gaps(p);
+    ipt::IterationConfig cfg;
+    cfg.tolerance = 1e-12;
+    cfg.record_trace = true;
+    const ipt::SpectrumResult one = ipt::solve_full(p, g, cfg);
+    const ipt::Partition q = ci_like(6000, 8, 77);
+    const ipt::InverseGaps gq = ipt::build_gaps(q, 0.0);
+    ipt::IterationConfig c1;
+    c1.tolerance = 1e-10;
+    const ipt::EigenpairResult s_one = ipt::solve_single(q, gq, 0, c1);
+    const ipt::SpectrumResult f_one = ipt::solve_full(ci_like(700, 6, 5), ipt::build_gaps(ci_like(700, 6, 5), 0.0), cfg);
+    for (const std::vector<int>& devs : {std::vector<int>{0, 0}, std::vector<int>{0, 0, 0}, std::vector<int>{0, 0, 0, 0}}) {
+        ipt::b200::set_devices(devs);
+        const ipt::SpectrumResult r = ipt::solve_full(p, g, cfg);
+        CHECK(r.iterations == one.iterations);
+        CHECK(r.status == one.status);
+        CHECK(max_abs_diff(r.Z, one.Z) == 0.0);
+        CHECK(max_abs_diff(r.eigenvalues, one.eigenvalues) == 0.0);
+        CHECK(r.trace.size() == one.trace.size());
+        CHECK(std::abs(r.residual_frobenius - one.residual_frobenius) <= 1e-6 * one.residual_frobenius + 1e-13);
+        CHECK(std::abs(r.min_singular_value_estimate - one.min_singular_value_estimate) <=
+              1e-12 * one.min_singular_value_estimate);
+        const ipt::EigenpairResult s = ipt::solve_single(q, gq, 0, c1);
+        CHECK(s.iterations == s_one.iterations);
+        CHECK(std::abs(s.eigenvalue - s_one.eigenvalue) <= 1e-12 * std::abs(s_one.eigenvalue));
+        CHECK(max_abs_diff(s.z, s_one.z) <= 1e-14);
+        const ipt::SpectrumResult f = ipt::solve_full(ci_like(700, 6, 5), ipt::build_gaps(ci_like(700, 6, 5), 0.0), cfg);
+        CHECK(f.iterations == f_one.iterations);
+        CHECK(max_abs_diff(f.Z, f_one.Z) == 0.0);
+    }
+    ipt::b200::set_devices({});
+    setenv("IPT_DEVICES", "0,0", 1);
+    CHECK(ipt::b200::devices_in_use() == 2);
+    const ipt::SpectrumResult e = ipt::solve_full(p, g, cfg);
+    CHECK(max_abs_diff(e.Z, one.Z) == 0.0);
+    setenv("IPT_DEVICES", "0,x", 1);
+    CHECK_THROWS_AS(ipt::solve_full(p, g, cfg), std::invalid_argument);
+    unsetenv("IPT_DEVICES");
+    CHECK(ipt::b200::devices_in_use() == 1);
 }
