@@ -273,6 +273,12 @@ int ipt_single_upload_csr_rows(ipt_ctx* ctx, int64_t n, const double* d_re, cons
 int ipt_single_upload_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
                           const int64_t* rowptr, const int32_t* cols, const double* val_re,
                           const double* val_im, ipt_single_problem** out);
+/* As ipt_single_upload_csr, but the host CSR arrays are referenced instead of copied (the
+ * anchor row of a later reset is rebuilt from them): they must stay valid and unchanged
+ * until ipt_single_free. ipt_single_upload_dense always references its host Delta. */
+int ipt_single_upload_csr_shared(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                                 const int64_t* rowptr, const int32_t* cols, const double* val_re,
+                                 const double* val_im, ipt_single_problem** out);
 int ipt_single_reset(ipt_ctx* ctx, ipt_single_problem* prob, int64_t anchor, const double* warm_re,
                      const double* warm_im);
 int ipt_single_iterate(ipt_ctx* ctx, ipt_single_problem* prob, const ipt_params* params,

@@ -142,6 +142,8 @@ SIGNATURES = {
     "ipt_single_upload_dense": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, _dp, C.POINTER(_vp)]),
     "ipt_single_upload_csr": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, _i32p, _dp, _dp,
                                         C.POINTER(_vp)]),
+    "ipt_single_upload_csr_shared": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, _i32p, _dp, _dp,
+                                        C.POINTER(_vp)]),
     "ipt_single_upload_dense_rows": (C.c_int, [_vp, C.c_int64, _dp, _dp, _dp, _dp, C.c_int64, C.c_int64,
                                                C.POINTER(_vp)]),
     "ipt_single_upload_csr_rows": (C.c_int, [_vp, C.c_int64, _dp, _dp, _i64p, _i32p, _dp, _dp, C.c_int64,

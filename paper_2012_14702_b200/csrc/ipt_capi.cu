@@ -825,6 +825,18 @@ int ipt_single_upload_csr(ipt_ctx* ctx, int64_t n, const double* d_re, const dou
   });
 }
 
+int ipt_single_upload_csr_shared(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
+                                 const int64_t* rowptr, const int32_t* cols, const double* val_re,
+                                 const double* val_im, ipt_single_problem** out) {
+  return guarded([&] {
+    check_ctx(ctx);
+    DeviceGuard g(ctx->c.device);
+    *out = reinterpret_cast<ipt_single_problem*>(single_upload(ctx->c, n, d_re, d_im, true, nullptr,
+                                                               nullptr, rowptr, cols, val_re, val_im,
+                                                               true));
+  });
+}
+
 int ipt_single_upload_dense_rows(ipt_ctx* ctx, int64_t n, const double* d_re, const double* d_im,
                                  const double* delta_re, const double* delta_im, int64_t row_begin,
                                  int64_t row_end, ipt_single_problem** out) {

@@ -5,6 +5,8 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstring>
+#include <algorithm>
 #include <memory>
 #include <utility>
 #include <stdexcept>
@@ -173,6 +175,27 @@ struct Csr {
     std::vector<int32_t, NoInitAllocator<int32_t>> cols;
     Planar val;
 };
+
+// Mixes ~2048 evenly spaced entries (and the CSR structure at the same stride): catches
+// contents changed through a raw pointer taken before the previous product.
+inline std::uint64_t fingerprint(const cplx* v, std::size_t count, const std::size_t* idx) {
+    std::uint64_t h = 0xcbf29ce484222325ull ^ count;
+    auto mix = [&h](std::uint64_t w) { h ^= w + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2); };
+    const std::size_t step = std::max<std::size_t>(1, count / 2048);
+    auto mix_at = [&](std::size_t t) {
+        std::uint64_t w[2];
+        std::memcpy(w, v + t, sizeof w);
+        mix(w[0]);
+        mix(w[1]);
+        if (idx) mix(idx[t]);
+    };
+    for (std::size_t t = 0; t < count; t += step) mix_at(t);
+    if (count) mix_at(count - 1);
+    return h;
+}
+
+// solve_single's device-resident problem (solver.cpp): freed with the resident operators.
+void release_resident_single();
 
 // The carrier's CSR (size_t columns, interleaved complex values) in the C ABI's form
 // (int32 columns, planar values), converted over the host threads.

@@ -69,24 +69,6 @@ struct OperatorCache {
 
 thread_local OperatorCache t_ops;
 
-// Mixes ~2048 evenly spaced entries (and the CSR structure at the same stride): catches
-// contents changed through a raw pointer taken before the previous product.
-std::uint64_t fingerprint(const cplx* v, std::size_t count, const std::size_t* idx) {
-    std::uint64_t h = 0xcbf29ce484222325ull ^ count;
-    auto mix = [&h](std::uint64_t w) { h ^= w + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2); };
-    const std::size_t step = std::max<std::size_t>(1, count / 2048);
-    auto mix_at = [&](std::size_t t) {
-        std::uint64_t w[2];
-        std::memcpy(w, v + t, sizeof w);
-        mix(w[0]);
-        mix(w[1]);
-        if (idx) mix(idx[t]);
-    };
-    for (std::size_t t = 0; t < count; t += step) mix_at(t);
-    if (count) mix_at(count - 1);
-    return h;
-}
-
 // The resident device copy of A for `kind`, or nullptr when A is not kept (small,
 // over the budget, or a shape the kind does not cover).
 CachedOperator* resident(const ComplexMatrix& a, OpKind kind) {
@@ -103,7 +85,7 @@ CachedOperator* resident(const ComplexMatrix& a, OpKind kind) {
     ipt_ctx* ctx = api::context();
     const cplx* vals = dense ? a.data() : a.values().data();
     const std::uint64_t rev = a.revision();
-    const std::uint64_t fp = fingerprint(vals, count, dense ? nullptr : a.col_indices().data());
+    const std::uint64_t fp = api::fingerprint(vals, count, dense ? nullptr : a.col_indices().data());
     auto& cache = t_ops;
     auto& v = cache.slots;
     for (auto& c : v)
@@ -185,7 +167,10 @@ void operator_matvec(ipt_operator* op, std::size_t n, const cplx* x, cplx* y) {
 
 }  // namespace
 
-void release_resident_operators() { t_ops.clear(); }
+void release_resident_operators() {
+    t_ops.clear();
+    api::release_resident_single();
+}
 std::size_t resident_operator_count() { return t_ops.size(); }
 
 void matvec(const ComplexMatrix& a, const cplx* x, cplx* y) {

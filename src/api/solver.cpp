@@ -214,10 +214,96 @@ Planar dense_delta(const Partition& p) {
     return api::split(dd.data(), p.size() * p.size());
 }
 
+// solve_single's problem stays on the device between calls on the same Partition (several
+// anchors of one matrix, repeated solves): Delta and d are uploaded once and each further
+// call only resets the anchor, iterates and downloads z. Kept while Delta's storage,
+// ComplexMatrix::revision() and a sampled content fingerprint match and d is unchanged
+// (compared in full); within IPT_OPERATOR_CACHE_MB (default 16384) like the resident
+// kernels:: operators, and freed with them (kernels::release_resident_operators).
+struct ResidentSingle {
+    const void* storage = nullptr;
+    std::uint64_t revision = 0, fingerprint = 0;
+    std::size_t n = 0, count = 0;
+    bool sparse = false;
+    ipt_ctx* ctx = nullptr;
+    ipt_single_problem* prob = nullptr;
+    cvec d;         // the diagonal it was opened with
+    Planar dense;   // the host sources anchor rows are rebuilt from (referenced by the problem)
+    api::Csr csr;
+    void release() {
+        if (prob) ipt_single_free(prob);
+        prob = nullptr;
+        storage = nullptr;
+        d = cvec();
+        dense = Planar();
+        csr = api::Csr();
+    }
+    ~ResidentSingle() { release(); }
+};
+thread_local ResidentSingle t_single;
+
+std::int64_t resident_budget() {
+    static const std::int64_t b = [] {
+        const char* e = std::getenv("IPT_OPERATOR_CACHE_MB");
+        return (e ? std::atoll(e) : 16384LL) << 20;
+    }();
+    return b;
+}
+
+// The device-resident problem for p, opened now if need be; nullptr when it is not kept
+// (small, complex Delta or d, or over the budget).
+ipt_single_problem* resident_single(const Partition& p) {
+    const std::size_t n = p.size();
+    const bool sparse = p.delta.is_sparse();
+    const std::size_t count = sparse ? p.delta.values().size() : n * n;
+    const std::int64_t bytes = sparse ? std::int64_t(count) * 12 + 8 * std::int64_t(n + 1) : std::int64_t(count) * 8;
+    if (bytes < (std::int64_t(1) << 20) || bytes > resident_budget()) return nullptr;
+    ipt_ctx* ctx = api::context();
+    const cplx* vals = sparse ? p.delta.values().data() : p.delta.data();
+    const std::uint64_t rev = p.delta.revision();
+    const std::uint64_t fp = api::fingerprint(vals, count, sparse ? p.delta.col_indices().data() : nullptr);
+    ResidentSingle& r = t_single;
+    if (r.prob && r.storage == vals && r.revision == rev && r.fingerprint == fp && r.n == n && r.count == count &&
+        r.sparse == sparse && r.ctx == ctx && r.d == p.d)
+        return r.prob;
+    r.release();
+    const Planar d = api::split(p.d.data(), n);
+    if (d.any_im) return nullptr;
+    ipt_single_problem* h = nullptr;
+    if (sparse) {
+        r.csr = api::to_csr(p.delta);
+        if (r.csr.val.any_im) {
+            r.csr = api::Csr();
+            return nullptr;
+        }
+        api::check(ipt_single_upload_csr_shared(ctx, static_cast<int64_t>(n), d.re.data(), nullptr,
+                                                r.csr.rowptr.data(), r.csr.cols.data(), r.csr.val.re.data(), nullptr,
+                                                &h));
+    } else {
+        r.dense = api::split(vals, count);
+        if (r.dense.any_im) {
+            r.dense = Planar();
+            return nullptr;
+        }
+        api::check(ipt_single_upload_dense(ctx, static_cast<int64_t>(n), d.re.data(), nullptr, r.dense.re.data(),
+                                           nullptr, &h));
+    }
+    r.prob = h;
+    r.storage = vals;
+    r.revision = rev;
+    r.fingerprint = fp;
+    r.n = n;
+    r.count = count;
+    r.sparse = sparse;
+    r.ctx = ctx;
+    r.d = p.d;
+    return h;
+}
+
 EigenpairResult run_single(const Partition& p, std::size_t anchor, const IterationConfig& cfg, const cvec* warm,
                            int schedule, double alpha) {
     const std::size_t n = p.size();
-    const Planar d = api::split(p.d.data(), n);
+    Planar d;  // split only where Delta is uploaded (not for the resident problem)
     Planar w;
     if (warm) {
         if (warm->size() != n) throw std::invalid_argument("solver: warm start size mismatch");
@@ -235,6 +321,7 @@ EigenpairResult run_single(const Partition& p, std::size_t anchor, const Iterati
     const double* wim = warm ? w.im_or_null() : nullptr;
     const std::vector<ipt_ctx*> ranks = p.delta.is_sparse() ? api::group_contexts() : std::vector<ipt_ctx*>{};
     if (!ranks.empty()) {
+        d = api::split(p.d.data(), n);
         // CSR rows sharded over the multi-device group; the iterate is all-gathered every
         // step (fused peer stores), so every rank ends with all of z: rank 0's is returned
         const api::Csr c = api::to_csr(p.delta);
@@ -258,12 +345,21 @@ EigenpairResult run_single(const Partition& p, std::size_t anchor, const Iterati
         });
         st = sts[0];
         trace = traces[0];
+    } else if (ipt_single_problem* h = (w.any_im ? nullptr : resident_single(p))) {
+        ipt_ctx* ctx = api::context();
+        api::check(ipt_single_reset(ctx, h, static_cast<int64_t>(anchor), schedule == IPT_SCHEDULE_CONTINUATION ? nullptr : wre,
+                                    schedule == IPT_SCHEDULE_CONTINUATION ? nullptr : wim));
+        api::check(ipt_single_iterate(ctx, h, &prm, &st));
+        api::check(ipt_single_finalize(ctx, h, &st));
+        api::check(ipt_single_download(ctx, h, zr.data(), zi.data()));
     } else if (p.delta.is_sparse()) {
+        d = api::split(p.d.data(), n);
         const api::Csr c = api::to_csr(p.delta);
         api::check(ipt_single_solve_csr(api::context(), static_cast<int64_t>(n), d.re.data(), d.im_or_null(),
                                         c.rowptr.data(), c.cols.data(), c.val.re.data(), c.val.im_or_null(),
                                         static_cast<int64_t>(anchor), wre, wim, &prm, zr.data(), zi.data(), &st));
     } else {
+        d = api::split(p.d.data(), n);
         const Planar a = api::split(p.delta.data(), n * n);
         api::check(ipt_single_solve_dense(api::context(), static_cast<int64_t>(n), d.re.data(), d.im_or_null(),
                                           a.re.data(), a.im_or_null(), static_cast<int64_t>(anchor), wre, wim, &prm,
@@ -555,5 +651,9 @@ double smallest_singular_value_estimate(const ComplexMatrix& z, int max_iters, d
                              &out));
     return out;
 }
+
+namespace api {
+void release_resident_single() { t_single.release(); }
+}  // namespace api
 
 }  // namespace ipt

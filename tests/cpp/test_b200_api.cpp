@@ -311,3 +311,60 @@ TEST_CASE("b200::set_devices: the sharded solves reproduce one GPU bit for bit")
     unsetenv("IPT_DEVICES");
     CHECK(ipt::b200::devices_in_use() == 1);
 }
+
+TEST_CASE("solve_single keeps its problem on the device across calls on the same Partition") {
+    ipt::Partition q = ci_like(6000, 8, 91);
+    const ipt::InverseGaps gq = ipt::build_gaps(q, 0.0);
+    ipt::IterationConfig c;
+    c.tolerance = 1e-10;
+    c.record_trace = true;
+    // fresh uploads (the resident problem released before each call) vs the resident one
+    std::vector<ipt::EigenpairResult> fresh;
+    for (std::size_t a : {0u, 5u, 17u}) {
+        ipt::kernels::release_resident_operators();
+        fresh.push_back(ipt::solve_single(q, gq, a, c));
+    }
+    ipt::kernels::release_resident_operators();
+    std::size_t k = 0;
+    for (int rep = 0; rep < 2; ++rep) {
+        k = 0;
+        for (std::size_t a : {0u, 5u, 17u}) {
+            const ipt::EigenpairResult r = ipt::solve_single(q, gq, a, c);
+            CHECK(r.iterations == fresh[k].iterations);
+            CHECK(r.eigenvalue == fresh[k].eigenvalue);
+            CHECK(max_abs_diff(r.z, fresh[k].z) == 0.0);
+            CHECK(r.trace == fresh[k].trace);
+            ++k;
+        }
+    }
+    const ipt::EigenpairResult cont = ipt::solve_single_continuation(q, gq, 3, c, 0.5);
+    ipt::kernels::release_resident_operators();
+    const ipt::EigenpairResult cont_fresh = ipt::solve_single_continuation(q, gq, 3, c, 0.5);
+    CHECK(max_abs_diff(cont.z, cont_fresh.z) == 0.0);
+    // a changed Delta is uploaded again (revision stamp / fingerprint), a changed d as well
+    const ipt::EigenpairResult before = ipt::solve_single(q, gq, 0, c);
+    ipt::Partition q2 = ci_like(6000, 8, 92);
+    q.delta = q2.delta;
+    const ipt::EigenpairResult after = ipt::solve_single(q, gq, 0, c);
+    ipt::kernels::release_resident_operators();
+    const ipt::EigenpairResult want = ipt::solve_single(q, gq, 0, c);
+    CHECK(max_abs_diff(after.z, want.z) == 0.0);
+    CHECK(max_abs_diff(after.z, before.z) > 0.0);
+    q.d[7] += 1e-3;
+    const ipt::InverseGaps g3 = ipt::build_gaps(q, 0.0);
+    const ipt::EigenpairResult d_changed = ipt::solve_single(q, g3, 0, c);
+    ipt::kernels::release_resident_operators();
+    const ipt::EigenpairResult d_fresh = ipt::solve_single(q, g3, 0, c);
+    CHECK(max_abs_diff(d_changed.z, d_fresh.z) == 0.0);
+    // dense Delta, warm start
+    const ipt::Partition p = near_diagonal(1200, 0.3 / std::sqrt(1200.0), 3);
+    const ipt::InverseGaps gp = ipt::build_gaps(p);
+    ipt::cvec warm(1200, ipt::cplx(0.0, 0.0));
+    warm[4] = 1.0;
+    warm[5] = 1e-3;
+    ipt::kernels::release_resident_operators();
+    const ipt::EigenpairResult w_fresh = ipt::solve_single(p, gp, 4, c, &warm);
+    const ipt::EigenpairResult w_res = ipt::solve_single(p, gp, 4, c, &warm);
+    CHECK(max_abs_diff(w_fresh.z, w_res.z) == 0.0);
+    CHECK(w_fresh.iterations == w_res.iterations);
+}
