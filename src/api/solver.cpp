@@ -4,6 +4,8 @@
 #include "ipt/solver.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <exception>
 #include <future>
@@ -579,19 +581,29 @@ SpectrumResult solve_full(const Partition& p, const InverseGaps& g, const Iterat
         // de-interleave happens inside the pinned staging pass); the result carrier is
         // allocated and zero-filled on a host thread while the device iterates, and Z is
         // interleaved straight into it while the closing product runs.
+        const bool prof = std::getenv("IPT_PROFILE") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
         auto zbuf = std::async(std::launch::async, [n] { return cvec(n * n); });
         ipt_full_problem* h = nullptr;
         const int rc = ipt_full_solve_interleaved_start(
             api::context(), static_cast<int64_t>(n), reinterpret_cast<const double*>(p.d.data()),
             reinterpret_cast<const double*>(p.delta.data()),
             warm_start ? reinterpret_cast<const double*>(wd.data()) : nullptr, &prm, &h, &st);
+        const auto t1 = std::chrono::steady_clock::now();
         cvec zv = zbuf.get();
+        const auto t2 = std::chrono::steady_clock::now();
         api::check(rc);
         std::unique_ptr<ipt_full_problem, void (*)(ipt_full_problem*)> hold(h, ipt_full_free);
         SpectrumResult r;
         r.eigenvalues.resize(n);
         api::check(ipt_full_solve_interleaved_finish(api::context(), h, &prm, reinterpret_cast<double*>(zv.data()),
                                                      reinterpret_cast<double*>(r.eigenvalues.data()), &st));
+        if (prof) {
+            const auto t3 = std::chrono::steady_clock::now();
+            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            std::fprintf(stderr, "[ipt] C++ solve_full ms: start %.1f, result carrier wait %.1f, finish %.1f\n",
+                         ms(t0, t1), ms(t1, t2), ms(t2, t3));
+        }
         r.Z = ComplexMatrix::dense(n, n, std::move(zv));
         r.iterations = st.iterations;
         r.final_step = st.final_step;
