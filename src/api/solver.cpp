@@ -143,6 +143,8 @@ void run_ranks(const std::vector<ipt_ctx*>& ctxs, const std::function<void(int, 
             if (!first) first = e;
         }
     }
+    // an error aborts the in-process communicator: the next call opens a fresh group
+    if (any) t_group.reset();
     if (first) std::rethrow_exception(first);
     if (any) std::rethrow_exception(any);
 }

@@ -301,6 +301,12 @@ TEST_CASE("b200::set_devices: the sharded solves reproduce one GPU bit for bit")
         CHECK(f.iterations == f_one.iterations);
         CHECK(max_abs_diff(f.Z, f_one.Z) == 0.0);
     }
+    // an error on the ranks surfaces as the single-GPU call's exception, and the group stays usable
+    ipt::b200::set_devices({0, 0});
+    ipt::ComplexMatrix bad_warm = ipt::ComplexMatrix::identity(1000);
+    bad_warm.at(3, 3) = 0.0;
+    CHECK_THROWS_AS(ipt::solve_full(p, g, cfg, &bad_warm), std::invalid_argument);
+    CHECK(max_abs_diff(ipt::solve_full(p, g, cfg).Z, one.Z) == 0.0);
     ipt::b200::set_devices({});
     setenv("IPT_DEVICES", "0,0", 1);
     CHECK(ipt::b200::devices_in_use() == 2);
@@ -313,6 +319,7 @@ TEST_CASE("b200::set_devices: the sharded solves reproduce one GPU bit for bit")
 }
 
 TEST_CASE("solve_single keeps its problem on the device across calls on the same Partition") {
+    ipt::b200::set_devices({});
     ipt::Partition q = ci_like(6000, 8, 91);
     const ipt::InverseGaps gq = ipt::build_gaps(q, 0.0);
     ipt::IterationConfig c;
