@@ -237,6 +237,9 @@ void solve_full_impl(Ctx& c, const ipt_params* params, Open&& open, const double
       // overlapped: host wall time from the end of the loop until Z was on the host
       stats->ms_download = overlap ? ms_down + ms_overlapped : ms_down;
     }
+    ph.mark("stats");
+    P.reset();
+    ph.mark("free");
   }
   ph.mark("release");
 }

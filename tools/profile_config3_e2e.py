@@ -9,11 +9,12 @@ import paper_2012_14702_b200 as ipt  # noqa: E402
 from paper_2012_14702_b200 import synth  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
+product = sys.argv[2] if len(sys.argv) > 2 else "dmma"
 p = synth.config3(n=n)
 g = ipt.build_gaps(p)
 cfg = ipt.IterationConfig(tolerance=1e-12)
 for rep in range(2):
     t0 = time.perf_counter()
-    r = ipt.solve_full(p, g, cfg)
+    r = ipt.solve_full(p, g, cfg, product=product)
     print(f"rep {rep}: {time.perf_counter() - t0:.3f} s, {r.iterations} it, residual {r.residual_frobenius:.4e}, "
           f"timings {r.timings_ms}", flush=True)
