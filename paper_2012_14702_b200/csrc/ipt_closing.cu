@@ -110,22 +110,43 @@ __global__ void __launch_bounds__(256) closing_residual_kernel(
     const int32_t* c1j = c1 + j * ldc;
     const int32_t* c2j = c2 + j * ldc;
     const double* zj = Z + j * ldz;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-      const int si = ea[i];
-      if (sj == 0x7fffffff || si == 0x7fffffff) {  // (non-finite input: the caller keeps the exact path)
-        v[0] = NAN;
-        continue;
+    // four rows per thread in flight (the pass is HBM-latency bound otherwise); the sum
+    // order per thread stays i = t, t + 256, ... as in the one-row loop
+    constexpr int kU = 4;
+    for (int64_t i0 = threadIdx.x; i0 < n; i0 += int64_t(kU) * blockDim.x) {
+      int32_t a1[kU], a2[kU], si[kU];
+      int8_t dh[kU], dl[kU];
+      double z[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t i = i0 + int64_t(u) * blockDim.x;
+        const bool in = i < n;
+        a1[u] = in ? c1j[i] : 0;
+        a2[u] = in ? c2j[i] : 0;
+        si[u] = in ? ea[i] : 0;
+        dh[u] = in ? dj[i] : int8_t(0);
+        dl[u] = in ? dj[kpad + i] : int8_t(0);
+        z[u] = in ? zj[i] : 0.0;
       }
-      // (Delta D)_ij = (2^14 c1 + 2^7 c2) 2^-(si + sj)
-      const double corr = ldexp(fma(128.0, double(c1j[i]), double(c2j[i])), 7 - (si + sj));
-      double r;
-      if (i == jg) {
-        r = (wo + corr) - wn;
-      } else {
-        const double dij = ldexp(fma(128.0, double(dj[i]), double(dj[kpad + i])), -sj);
-        r = fma(zj[i], wo - wn, fma(-dij, wo, corr));
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t i = i0 + int64_t(u) * blockDim.x;
+        if (i >= n) break;
+        if (sj == 0x7fffffff || si[u] == 0x7fffffff) {  // (non-finite input: the caller keeps the exact path)
+          v[0] = NAN;
+          continue;
+        }
+        // (Delta D)_ij = (2^14 c1 + 2^7 c2) 2^-(si + sj)
+        const double corr = ldexp(fma(128.0, double(a1[u]), double(a2[u])), 7 - (si[u] + sj));
+        double r;
+        if (i == jg) {
+          r = (wo + corr) - wn;
+        } else {
+          const double dij = ldexp(fma(128.0, double(dh[u]), double(dl[u])), -sj);
+          r = fma(z[u], wo - wn, fma(-dij, wo, corr));
+        }
+        v[0] = fma(r, r, v[0]);
       }
-      v[0] = fma(r, r, v[0]);
     }
   }
   block_reduce4<8>(v, red);
