@@ -58,6 +58,7 @@ struct SingleProblem {
   DevBuf dre, dim;
   DevBuf z[2], zi[2];
   DevBuf w, wi;              // complex path / matvec scratch
+  DevBuf zc;                 // complex CSR path: the iterate interleaved (re, im) for 16-byte gathers
   DevBuf wa;                 // anchor value (re, im)
   DevBuf partials;
   int64_t npart = 0;
@@ -766,6 +767,93 @@ __global__ void cmatvec_csr_kernel(const int64_t* __restrict__ rowptr, const int
 }
 
 
+
+// Complex CSR matvec, w = Delta z over the local rows, as the real map streams it: a warp
+// takes R consecutive rows as ONE contiguous entry range (coalesced column / value loads),
+// gathers z from an interleaved copy (one 16-byte load, one L2 sector, per entry instead of
+// two) and keeps per-row (re, im) accumulators, combined per row by the xor tree.
+__global__ void interleave_kernel(const double* __restrict__ re, const double* __restrict__ im, int64_t n,
+                                  double2* __restrict__ out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = make_double2(re[i], im[i]);
+}
+
+template <int R, int U, bool VI>
+__global__ void __launch_bounds__(256) cspmv_group_kernel(const int64_t* __restrict__ rowptr,
+                                                          const int32_t* __restrict__ cols,
+                                                          const double* __restrict__ vr,
+                                                          const double* __restrict__ vi,
+                                                          const double2* __restrict__ zc, int64_t rows,
+                                                          double* __restrict__ wr, double* __restrict__ wi,
+                                                          int64_t row0) {
+  const int lane = threadIdx.x & 31;
+  const int64_t groups = ceil_div(rows, int64_t(R));
+  const int64_t nwarps = int64_t(gridDim.x) * 8;
+  for (int64_t grp = blockIdx.x * int64_t(8) + (threadIdx.x >> 5); grp < groups; grp += nwarps) {
+    const int64_t lr0 = grp * R;
+    const long long mine = group_offsets<R>(rowptr, lr0, rows, lane);
+    int64_t rb[R + 1];
+#pragma unroll
+    for (int k = 0; k <= R; ++k) rb[k] = __shfl_sync(0xffffffffu, mine, k);
+    double sr[R], si[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) sr[k] = si[k] = 0.0;
+    const int64_t end = rb[R];
+    for (int64_t p0 = rb[0] + lane; p0 < end; p0 += 32 * U) {
+      int32_t c[U];
+      double a[U], b[U];
+      double2 zz[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t p = p0 + 32 * u;
+        c[u] = p < end ? ld_nc_i32(cols + p) : 0;
+        a[u] = p < end ? ld_nc_f64(vr + p) : 0.0;
+        b[u] = (VI && p < end) ? ld_nc_f64(vi + p) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) zz[u] = p0 + 32 * u < end ? __ldg(zc + c[u]) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t p = p0 + 32 * u;
+        if (p < end) {
+          int r = 0;
+#pragma unroll
+          for (int k = 1; k < R; ++k) r += p >= rb[k];
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+            if (k == r) {
+              // (a + ib)(x + iy): re += a x - b y, im += a y + b x
+              sr[k] = __fma_rn(a[u], zz[u].x, sr[k]);
+              si[k] = __fma_rn(a[u], zz[u].y, si[k]);
+              if (VI) {
+                sr[k] = __fma_rn(-b[u], zz[u].y, sr[k]);
+                si[k] = __fma_rn(b[u], zz[u].x, si[k]);
+              }
+            }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        sr[k] += __shfl_xor_sync(0xffffffffu, sr[k], off);
+        si[k] += __shfl_xor_sync(0xffffffffu, si[k], off);
+      }
+    if (lane < R && lr0 + lane < rows) {
+      double xr = sr[0], xi = si[0];
+#pragma unroll
+      for (int k = 1; k < R; ++k)
+        if (lane == k) {
+          xr = sr[k];
+          xi = si[k];
+        }
+      wr[row0 + lr0 + lane] = xr;
+      wi[row0 + lr0 + lane] = xi;
+    }
+  }
+}
+
 // mode 1: map ; mode 2: final residual. Fixed grid => deterministic partials.
 __global__ void cmap_kernel(int mode, const double* __restrict__ zr, const double* __restrict__ zi,
                             const double* __restrict__ wr, const double* __restrict__ wi,
@@ -893,7 +981,22 @@ void enqueue_cmatvec(SingleProblem& P, int src) {
   cudaStream_t s = P.ctx->stream;
   const int64_t rows = P.r1 - P.r0;
   if (rows <= 0) return;
-  if (P.csr) {
+  if (P.csr && std::getenv("IPT_CSPMV_SIMPLE") == nullptr) {
+    const int64_t vlen = P.n;  // the replicated iterate (global indexing)
+    interleave_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(vlen, 256), 1184)), 256, 0, s>>>(
+        P.z[src].get(), P.zi[src].get(), vlen, reinterpret_cast<double2*>(P.zc.get()));
+    IPT_LAUNCH_CHECK();
+    count_launch();
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(int64_t(kNumSMs) * 4, ceil_div(rows, int64_t(32))));
+    if (P.valsi.count)
+      cspmv_group_kernel<4, 4, true><<<grid, 256, 0, s>>>(P.rowptr.get(), P.cols.get(), P.vals.get(),
+                                                         P.valsi.get(), reinterpret_cast<const double2*>(P.zc.get()),
+                                                         rows, P.w.get(), P.wi.get(), P.r0);
+    else
+      cspmv_group_kernel<4, 4, false><<<grid, 256, 0, s>>>(P.rowptr.get(), P.cols.get(), P.vals.get(), nullptr,
+                                                          reinterpret_cast<const double2*>(P.zc.get()), rows,
+                                                          P.w.get(), P.wi.get(), P.r0);
+  } else if (P.csr) {
     cmatvec_csr_kernel<<<static_cast<unsigned>(ceil_div(rows, 256)), 256, 0, s>>>(
         P.rowptr.get(), P.cols.get(), P.vals.get(), P.valsi.count ? P.valsi.get() : nullptr, rows,
         P.z[src].get(), P.zi[src].get(), P.w.get(), P.wi.get(), P.r0);
@@ -1238,6 +1341,7 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
   setup_peer_gather(*P, zlen);
   P->w.alloc(zlen);
   P->wi.alloc(zlen);
+  if (P->csr && P->cplx) P->zc.alloc(2 * size_t(zlen), false);
   P->wa.alloc(2);
   P->npart = std::max<int64_t>(map_blocks(*P), 1);
   P->partials.alloc(size_t(P->npart) * 4);
