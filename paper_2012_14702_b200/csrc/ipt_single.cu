@@ -983,6 +983,8 @@ void enqueue_cmatvec(SingleProblem& P, int src) {
   if (rows <= 0) return;
   if (P.csr && std::getenv("IPT_CSPMV_SIMPLE") == nullptr) {
     const int64_t vlen = P.n;  // the replicated iterate (global indexing)
+    // (a real Delta meets a complex vector here too: kernels::matvec with complex x)
+    if (P.zc.count < 2 * size_t(vlen)) P.zc.alloc(2 * size_t(std::max<int64_t>(vlen, 1)), false);
     interleave_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(vlen, 256), 1184)), 256, 0, s>>>(
         P.z[src].get(), P.zi[src].get(), vlen, reinterpret_cast<double2*>(P.zc.get()));
     IPT_LAUNCH_CHECK();
@@ -1341,7 +1343,7 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
   setup_peer_gather(*P, zlen);
   P->w.alloc(zlen);
   P->wi.alloc(zlen);
-  if (P->csr && P->cplx) P->zc.alloc(2 * size_t(zlen), false);
+  if (P->csr && P->cplx) P->zc.alloc(2 * size_t(std::max<int64_t>(n, 1)), false);
   P->wa.alloc(2);
   P->npart = std::max<int64_t>(map_blocks(*P), 1);
   P->partials.alloc(size_t(P->npart) * 4);

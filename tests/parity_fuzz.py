@@ -1,0 +1,108 @@
+"""Randomised parity cases against the reference build (oracle/_ref, the unmodified
+reference compiled from its sources): shared by tests/test_gpu_fuzz_parity.py (a fixed
+seeded subset) and tools/parity_sweep.py (a long sweep whose summary is committed under
+profiles/). Each case draws an entry point, a size from the edge set the reference's own
+tests use (1, 2, 3, 5, 7, 8, 16, 33, 64, ... and tile / row-group boundaries), real or
+complex values, dense or CSR storage, a coupling and a seed, runs the device path through
+the public Python API and the reference on the same inputs, and checks north_star's
+tolerances: eigenvalues 1e-10 relative, eigenvectors 1e-9, iterations +-1, same status."""
+import numpy as np
+
+import paper_2012_14702_b200 as ipt
+
+SIZES = [1, 2, 3, 5, 7, 8, 15, 16, 17, 31, 33, 63, 64, 65, 127, 128, 129, 200, 255, 256, 257, 300, 511, 513]
+KINDS = ["full", "full_csr", "single", "single_csr", "continuation", "accelerated", "apply_map_full",
+         "matmul", "matvec", "matvec_csr"]
+
+
+def _matrix(rng, n, cplx, csr, eps):
+    gaps = rng.uniform(0.6, 1.6, n)
+    d = np.cumsum(gaps) + rng.uniform(-0.2, 0.2)
+    if cplx:
+        d = d + 1j * rng.uniform(-0.3, 0.3, n)
+    if csr:
+        density = min(1.0, rng.uniform(2.0, 12.0) / max(n, 1))
+        mask = rng.random((n, n)) < density
+    else:
+        mask = np.ones((n, n), bool)
+    np.fill_diagonal(mask, False)
+    vals = rng.uniform(-1.0, 1.0, (n, n))
+    if cplx:
+        vals = vals + 1j * rng.uniform(-1.0, 1.0, (n, n))
+    delta = np.where(mask, eps * vals, 0.0)
+    if csr:
+        r, c = np.nonzero(delta)
+        return d, ipt.CsrMatrix.from_triplets(n, n, r, c, delta[r, c]), delta
+    return d, delta, delta
+
+
+def draw(case_seed):
+    rng = np.random.default_rng(case_seed)
+    kind = KINDS[rng.integers(len(KINDS))]
+    n = int(SIZES[rng.integers(len(SIZES))])
+    cplx = bool(rng.random() < 0.35) and kind != "accelerated"
+    csr = kind.endswith("csr")
+    eps = float(rng.uniform(0.02, 0.5) / np.sqrt(max(n, 1)))
+    return rng, kind, n, cplx, csr, eps
+
+
+def run_case(case_seed, ref):
+    """One case: returns (kind, n, cplx, max eigenvector diff, max eigenvalue rel diff, note);
+    raises AssertionError on a parity failure."""
+    rng, kind, n, cplx, csr, eps = draw(case_seed)
+    d, delta, dense = _matrix(rng, n, cplx, csr or kind == "matvec_csr", eps)
+    p = ipt.Partition(d, delta)
+    tol = 1e-12
+    cfg = ipt.IterationConfig(tolerance=tol)
+    dz = dl = 0.0
+    if kind in ("full", "full_csr"):
+        r = ipt.solve_full(p, ipt.build_gaps(p), cfg)
+        o = ref.solve_full_csr(d, delta, tol=tol) if csr else ref.solve_full(d, delta, tol=tol)
+        assert r.status.value == o["status"], (r.status, o["status"])
+        if o["status"] == 0:
+            assert abs(r.iterations - o["iterations"]) <= 1, (r.iterations, o["iterations"])
+            dz = float(np.max(np.abs(r.Z - o["Z"])))
+            lam = o["eigenvalues"]
+            dl = float(np.max(np.abs(r.eigenvalues - lam) / np.maximum(np.abs(lam), 1e-300)))
+            assert dz <= 1e-9 and dl <= 1e-10, (dz, dl)
+    elif kind in ("single", "single_csr", "continuation", "accelerated"):
+        a = int(rng.integers(n))
+        g = ipt.build_gaps(p)
+        if kind == "continuation":
+            r = ipt.solve_single_continuation(p, g, a, cfg, 0.6)
+            o = ref.solve_single(d, delta, a, tol=tol, mode="continuation", alpha=0.6)
+        elif kind == "accelerated":
+            c2 = ipt.IterationConfig(tolerance=tol, residual_tolerance=1e-11)
+            r = ipt.solve_single_accelerated(p, g, a, c2, memory=3)
+            o = ref.solve_single(d, delta, a, tol=tol, mode="accelerated", memory=3, residual_tol=1e-11)
+        else:
+            r = ipt.solve_single(p, g, a, cfg)
+            o = ref.solve_single(d, delta, a, tol=tol)
+        assert r.status.value == o["status"], (r.status, o["status"])
+        if o["status"] == 0:
+            assert abs(r.iterations - o["iterations"]) <= (2 if kind == "accelerated" else 1), \
+                (r.iterations, o["iterations"])
+            dz = float(np.max(np.abs(r.z - o["z"])))
+            dl = float(abs(r.eigenvalue - o["eigenvalue"]) / max(abs(o["eigenvalue"]), 1e-300))
+            assert dz <= 1e-9 and dl <= 1e-10, (dz, dl)
+    elif kind == "apply_map_full":
+        z = np.eye(n) + 0.01 * rng.standard_normal((n, n)) * (1 + (1j if cplx else 0))
+        np.fill_diagonal(z, 1.0)
+        f = ipt.apply_map_full(p, ipt.build_gaps(p), z)
+        o = ref.apply_map_full(d, delta, z)
+        dz = float(np.max(np.abs(f - o)))
+        assert dz <= 1e-12 * max(1.0, float(np.max(np.abs(o)))), dz
+    elif kind == "matmul":
+        b = rng.standard_normal((n, n)) + (1j * rng.standard_normal((n, n)) if cplx else 0)
+        c = ipt.kernels.matmul(dense, b)
+        o = ref.matmul(dense, b)
+        scale = max(1e-300, float(np.linalg.norm(dense) * np.linalg.norm(b)))
+        dz = float(np.max(np.abs(c - o)))
+        assert dz <= 1e-13 * scale, (dz, scale)  # test_kernels.cpp:40-50
+    else:  # matvec / matvec_csr
+        x = rng.standard_normal(n) + (1j * rng.standard_normal(n) if cplx else 0)
+        y = ipt.kernels.matvec(delta, x)
+        o = ref.matvec(delta, x)
+        dz = float(np.max(np.abs(y - o)))
+        assert dz <= 1e-13 * max(1.0, float(np.max(np.abs(o)))), dz
+    return kind, n, cplx, dz, dl

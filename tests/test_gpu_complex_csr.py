@@ -68,3 +68,18 @@ def test_grouped_and_thread_per_row_kernels_agree(monkeypatch):
     rows = np.repeat(np.arange(1 << 15), np.diff(dense.row_offsets))
     np.add.at(ref, rows, dense.values * x[dense.col_indices])
     assert np.max(np.abs(y - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("n", [1, 2, 37])
+def test_real_csr_times_complex_vector(n):
+    """kernels::matvec with a real (possibly empty) CSR and a complex x takes the complex
+    path on a real problem: the interleaved gather copy is allocated there too."""
+    rng = np.random.default_rng(n)
+    mask = rng.random((n, n)) < 0.2
+    np.fill_diagonal(mask, False)
+    a = np.where(mask, rng.standard_normal((n, n)), 0.0)
+    r, c = np.nonzero(a)
+    csr = ipt.CsrMatrix.from_triplets(n, n, r, c, a[r, c])
+    x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    y = ipt.kernels.matvec(csr, x)
+    assert np.max(np.abs(y - a @ x), initial=0.0) <= 1e-14

@@ -1,0 +1,17 @@
+"""Seeded randomised parity against the reference build (tests/parity_fuzz.py): 120 cases
+over every entry point, edge sizes (1 .. 513, tile and row-group boundaries), real and
+complex, dense and CSR. tools/parity_sweep.py runs the long sweep
+(profiles/r02_parity_sweep.txt)."""
+import pytest
+
+from parity_fuzz import run_case
+
+pytestmark = pytest.mark.gpu
+
+
+# 100230: a 1 x 1 CSR with no entries times a complex vector -- the case that found the
+# unallocated interleaved gather buffer of the complex CSR matvec (a real Delta meeting a
+# complex x), fixed in the same round
+@pytest.mark.parametrize("seed", list(range(1000, 1120)) + [100230])
+def test_random_case_matches_the_reference(ref_arm, seed):
+    run_case(seed, ref_arm)
