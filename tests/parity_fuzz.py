@@ -106,3 +106,118 @@ def run_case(case_seed, ref):
         dz = float(np.max(np.abs(y - o)))
         assert dz <= 1e-13 * max(1.0, float(np.max(np.abs(o)))), dz
     return kind, n, cplx, dz, dl
+
+
+# ---- extended cases: warm starts, the max-abs stop rule, the Ozaki product, in-process
+# ranks, non-convergent couplings (Diverged / MaxIterations parity) and traces
+KINDS_EXT = ["full_warm", "single_warm", "full_maxabs", "full_ozaki", "full_ranks", "single_ranks_csr",
+             "full_hard", "single_hard"]
+
+
+def draw_ext(case_seed):
+    rng = np.random.default_rng(case_seed)
+    kind = KINDS_EXT[rng.integers(len(KINDS_EXT))]
+    n = int(SIZES[rng.integers(len(SIZES))])
+    cplx = bool(rng.random() < 0.35) and kind not in ("full_ozaki", "single_ranks_csr")
+    eps = float(rng.uniform(0.02, 0.5) / np.sqrt(max(n, 1)))
+    if kind.endswith("hard"):
+        eps = float(rng.uniform(0.3, 3.0))  # gaps ~1: divergence or slow convergence
+    return rng, kind, n, cplx, eps
+
+
+STATUS_COUNTS = {0: 0, 1: 0, 2: 0}  # reference statuses met by the extended cases (sweep summary)
+
+
+def _compare_full(r, o, trace=False):
+    assert r.status.value == o["status"], (r.status, o["status"])
+    STATUS_COUNTS[o["status"]] += 1
+    if o["status"] != 0:
+        assert abs(r.iterations - o["iterations"]) <= 1, (r.iterations, o["iterations"])
+        return 0.0, 0.0
+    assert abs(r.iterations - o["iterations"]) <= 1, (r.iterations, o["iterations"])
+    dz = float(np.max(np.abs(r.Z - o["Z"])))
+    lam = o["eigenvalues"]
+    dl = float(np.max(np.abs(r.eigenvalues - lam) / np.maximum(np.abs(lam), 1e-300)))
+    assert dz <= 1e-9 and dl <= 1e-10, (dz, dl)
+    if trace and r.iterations == o["iterations"]:
+        tr = np.asarray(r.trace)
+        assert np.allclose(tr, o["trace"], rtol=1e-6, atol=1e-15), (tr, o["trace"])
+    return dz, dl
+
+
+def _compare_single(r, o):
+    assert r.status.value == o["status"], (r.status, o["status"])
+    STATUS_COUNTS[o["status"]] += 1
+    assert abs(r.iterations - o["iterations"]) <= 1, (r.iterations, o["iterations"])
+    if o["status"] != 0:
+        return 0.0, 0.0
+    dz = float(np.max(np.abs(r.z - o["z"])))
+    dl = float(abs(r.eigenvalue - o["eigenvalue"]) / max(abs(o["eigenvalue"]), 1e-300))
+    assert dz <= 1e-9 and dl <= 1e-10, (dz, dl)
+    return dz, dl
+
+
+def run_case_ext(case_seed, ref):
+    from paper_2012_14702_b200 import dist
+
+    rng, kind, n, cplx, eps = draw_ext(case_seed)
+    csr = kind.endswith("csr")
+    d, delta, dense = _matrix(rng, n, cplx, csr, eps)
+    p = ipt.Partition(d, delta)
+    g = ipt.build_gaps(p)
+    tol = 1e-12
+    cfg = ipt.IterationConfig(tolerance=tol, max_iterations=60, record_trace=True)
+    if kind == "full_warm":
+        w = np.eye(n) + 0.05 * eps * rng.standard_normal((n, n))
+        w = w.astype(complex) if cplx else w
+        np.fill_diagonal(w, 1.0 + (0.3j if cplx else 0.0))
+        r = ipt.solve_full(p, g, cfg, warm_start=w)
+        o = ref.solve_full(d, delta, tol=tol, max_iter=60, record_trace=True, warm=w)
+        dz, dl = _compare_full(r, o, trace=True)
+    elif kind == "single_warm":
+        a = int(rng.integers(n))
+        w = 0.01 * rng.standard_normal(n) + (0.01j * rng.standard_normal(n) if cplx else 0)
+        w[a] = 1.0 + (0.5j if cplx else 0.0)
+        r = ipt.solve_single(p, g, a, cfg, warm_start=w)
+        o = ref.solve_single(d, delta, a, tol=tol, max_iter=60, warm=w)
+        dz, dl = _compare_single(r, o)
+    elif kind == "full_maxabs":
+        c2 = ipt.IterationConfig(tolerance=tol, max_iterations=60, stop_rule="max_abs")
+        r = ipt.solve_full(p, g, c2)
+        o = ref.solve_full(d, delta, tol=tol, max_iter=60, stop_rule="max_abs")
+        dz, dl = _compare_full(r, o)
+    elif kind == "full_ozaki":
+        r = ipt.solve_full(p, g, cfg, product="ozaki")
+        o = ref.solve_full(d, delta, tol=tol, max_iter=60, record_trace=True)
+        dz, dl = _compare_full(r, o, trace=True)
+    elif kind == "full_ranks":
+        k = int(rng.integers(2, 4))
+        ctxs = dist.local_contexts(k)
+        try:
+            r = dist.run_ranks(lambda c: ipt.solve_full(p, g, cfg, ctx=c), ctxs)[0]
+        finally:
+            for c in ctxs:
+                c.close()
+        o = ref.solve_full(d, delta, tol=tol, max_iter=60, record_trace=True)
+        dz, dl = _compare_full(r, o, trace=True)
+    elif kind == "single_ranks_csr":
+        k = int(rng.integers(2, 4))
+        a = int(rng.integers(n))
+        ctxs = dist.local_contexts(k)
+        try:
+            r = dist.run_ranks(lambda c: ipt.solve_single(p, g, a, cfg, ctx=c), ctxs)[0]
+        finally:
+            for c in ctxs:
+                c.close()
+        o = ref.solve_single(d, delta, a, tol=tol, max_iter=60)
+        dz, dl = _compare_single(r, o)
+    elif kind == "full_hard":
+        r = ipt.solve_full(p, g, cfg)
+        o = ref.solve_full(d, delta, tol=tol, max_iter=60, record_trace=True)
+        dz, dl = _compare_full(r, o)
+    else:  # single_hard
+        a = int(rng.integers(n))
+        r = ipt.solve_single(p, g, a, cfg)
+        o = ref.solve_single(d, delta, a, tol=tol, max_iter=60)
+        dz, dl = _compare_single(r, o)
+    return kind, n, cplx, dz, dl

@@ -4,7 +4,7 @@ complex, dense and CSR. tools/parity_sweep.py runs the long sweep
 (profiles/r02_parity_sweep.txt)."""
 import pytest
 
-from parity_fuzz import run_case
+from parity_fuzz import run_case, run_case_ext
 
 pytestmark = pytest.mark.gpu
 
@@ -15,3 +15,10 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("seed", list(range(1000, 1120)) + [100230])
 def test_random_case_matches_the_reference(ref_arm, seed):
     run_case(seed, ref_arm)
+
+
+@pytest.mark.parametrize("seed", range(5000, 5080))
+def test_random_extended_case_matches_the_reference(ref_arm, seed):
+    """Warm starts, the max-abs stop rule, the Ozaki product, 2-3 in-process ranks, and
+    couplings that diverge or run out of iterations (status parity)."""
+    run_case_ext(seed, ref_arm)
