@@ -46,3 +46,12 @@ if ext:
     c = parity_fuzz.STATUS_COUNTS
     print(f"reference statuses over the solves: converged {c[0]}, max_iterations {c[1]}, diverged {c[2]} "
           f"(the device matched each, iterations +-1)")
+if os.environ.get("IPT_GUARD") == "1":
+    import gc
+
+    import paper_2012_14702_b200 as ipt
+
+    gc.collect()
+    lib = ipt.load_library()
+    print(f"IPT_GUARD=1: guard zones checked on {lib.ipt_guard_checked()} buffers, "
+          f"{lib.ipt_guard_violations()} violations")
