@@ -598,6 +598,14 @@ def main():
         return t.item()
 
     peak = fp64_peak(torch) if rank == 0 else 0.0
+    # FP64 DMMA issue rate measured in this run by the library's probe (m16n8k4 from
+    # registers on every SM); the round-1 pool constant is only a fallback
+    dmma_probe = None
+    if rank == 0:
+        v = C.c_double()
+        if lib.ipt_fp64_issue_probe(ctx.handle, C.byref(v)) == 0:
+            dmma_probe = v.value
+    fp64_den = max(peak, dmma_probe if dmma_probe else DMMA_ISSUE_PEAK)
     n = args.n
     t0 = time.perf_counter()
     p = synth.config3(n=n)
@@ -772,12 +780,15 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE configs[2] construction, seed 42)",
             "config": workload_config(world, n),
             "roofline": {"bound": "tensor", "kernel": "dmma_tma_kernel<1> (K1: TMA-fed DMMA GEMM + fused map epilogue)",
-                         "achieved": achieved, "peak": max(peak, DMMA_ISSUE_PEAK),
+                         "achieved": achieved, "peak": fp64_den,
                          "peak_source": "FP64 tensor peak (absent from MEASURED_PEAKS.json): the larger of the DMMA "
-                                        "issue-rate probe on this pool (37.1 TF/s, profiles/r01_fp64_probe.txt) and "
-                                        "cuBLAS DGEMM 8192^3 measured in this run",
+                                        "issue-rate probe (ipt_fp64_issue_probe: m16n8k4 DMMAs from registers on "
+                                        "every SM) and cuBLAS DGEMM 8192^3, both measured in this run"
+                                        + ("" if dmma_probe else " (probe failed: pool constant 37.1 TF/s, "
+                                           "profiles/r01_fp64_probe.txt)"),
+                         "dmma_issue_probe_in_run": dmma_probe,
                          "cublas_dgemm_in_run": peak,
-                         "unit": "TFLOP/s", "frac": achieved / max(peak, DMMA_ISSUE_PEAK),
+                         "unit": "TFLOP/s", "frac": achieved / fp64_den,
                          "frac_of_cublas_dgemm": achieved / peak if peak else None,
                          "flops_per_launch": gemm_flops_local, "kernel_ms": gemm_ms_local,
                          "kernel_share_of_step": gemm_ms / step_ms,

@@ -354,6 +354,11 @@ int ipt_single_run_steps(ipt_ctx* ctx, ipt_single_problem* prob, int32_t count, 
 int ipt_single_debug_peers(ipt_single_problem* prob, int32_t npeers);
 int ipt_single_debug_peer_z(ipt_single_problem* prob, int32_t peer, int32_t buf, double* out);
 
+/* FP64 tensor issue rate of the context's device in TF/s: back-to-back m16n8k4 DMMAs (the
+ * instruction of the FP64 GEMM) from registers on every SM, best of 3 ~50 ms launches --
+ * the roofline denominator of the FP64 kernels, measured in the same run. */
+int ipt_fp64_issue_probe(ipt_ctx* ctx, double* tflops);
+
 /* Counters for gpu_launches accounting: kernels this library has launched. */
 int64_t ipt_kernel_launch_count(void);
 /* Debug aid (compute-sanitizer is unavailable on the GPU pool): with IPT_GUARD=1 in the

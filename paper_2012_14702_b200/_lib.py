@@ -167,6 +167,7 @@ SIGNATURES = {
     "ipt_single_run_steps": (C.c_int, [_vp, _vp, C.c_int32, _dp, _dp]),
     "ipt_kernel_launch_count": (C.c_int64, []),
     "ipt_guard_violations": (C.c_int64, []),
+    "ipt_fp64_issue_probe": (C.c_int, [_vp, C.POINTER(C.c_double)]),
     "ipt_guard_selftest": (C.c_int64, []),
     "ipt_guard_checked": (C.c_int64, []),
     "ipt_synth_dense_uniform": (C.c_int, [C.c_int64, C.c_double, C.c_uint64, _dp, _dp]),

@@ -58,7 +58,58 @@ void launch_mode(const GemmParams& p, cudaStream_t s) {
   count_launch();
 }
 
+// FP64 tensor issue-rate probe: back-to-back m16n8k4 DMMAs (K1's instruction) from
+// registers, 8 independent accumulators per warp, 8 warps on every SM: the roofline
+// denominator of the FP64 kernels, measured in the caller's run instead of a constant.
+__global__ void __launch_bounds__(256) dmma_issue_probe_kernel(double* out, int iters) {
+  double acc[8][4];
+  const double a0 = 1e-9 * threadIdx.x, a1 = 2e-9 * threadIdx.x, b0 = 3e-9 * threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[j][i] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dmma_16x8x4(acc[j], a0, a1, b0);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s += acc[j][i];
+  if (s == 12345.678) out[0] = s;  // keeps the loop
+}
+
 }  // namespace
+
+double fp64_issue_probe_tflops(cudaStream_t s, int device) {
+  int sms = 0;
+  IPT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  DevBuf out;
+  out.alloc(1);
+  cudaEvent_t e0, e1;
+  IPT_CUDA(cudaEventCreate(&e0));
+  IPT_CUDA(cudaEventCreate(&e1));
+  const int iters = 20000;
+  dmma_issue_probe_kernel<<<sms, 256, 0, s>>>(out.get(), iters / 10);  // warm-up / clocks up
+  IPT_LAUNCH_CHECK();
+  double best = 0.0;
+  for (int rep = 0; rep < 3; ++rep) {
+    IPT_CUDA(cudaEventRecord(e0, s));
+    dmma_issue_probe_kernel<<<sms, 256, 0, s>>>(out.get(), iters);
+    IPT_CUDA(cudaEventRecord(e1, s));
+    IPT_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    IPT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    // per warp and iteration: 8 DMMAs of 2 * 16 * 8 * 4 flops
+    const double flops = double(sms) * 8.0 * iters * 8.0 * (2.0 * 16 * 8 * 4);
+    best = std::max(best, flops / (double(ms) * 1e-3) / 1e12);
+  }
+  count_launch(4);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return best;
+}
 
 size_t gemm_tiles(int64_t rows, int64_t cols) {
   return static_cast<size_t>(ceil_div(rows, kBM) * ceil_div(cols, kBN));

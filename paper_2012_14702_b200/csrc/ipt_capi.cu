@@ -265,6 +265,15 @@ void ipt_default_params(ipt_params* p) {
 
 int64_t ipt_kernel_launch_count(void) { return g_launches.load(); }
 int64_t ipt_guard_violations(void) { return guard_violations(); }
+
+int ipt_fp64_issue_probe(ipt_ctx* ctx, double* tflops) {
+  return guarded([&] {
+    check_ctx(ctx);
+    if (tflops == nullptr) throw InvalidArgument("ipt_fp64_issue_probe: null out");
+    DeviceGuard g(ctx->c.device);
+    *tflops = fp64_issue_probe_tflops(ctx->c.stream, ctx->c.device);
+  });
+}
 int64_t ipt_guard_checked(void) { return guard_checked(); }
 int64_t ipt_guard_selftest(void) {
   int64_t r = -1;

@@ -136,6 +136,8 @@ void release_cached_device_memory(int device);
 void set_release_stream(cudaStream_t s);
 // IPT_GUARD=1: out-of-bounds writes detected next to pool buffers (ipt_util.cu)
 int64_t guard_violations();
+// FP64 DMMA issue-rate probe (TF/s) on the stream's device (dmma_gemm.cu)
+double fp64_issue_probe_tflops(cudaStream_t s, int device);
 int64_t guard_selftest();
 int64_t guard_checked();
 void reduce_partials(cudaStream_t s, const double* partials, int64_t count, double* out4,
