@@ -10,7 +10,11 @@ import numpy as np
 
 import paper_2012_14702_b200 as ipt
 
+import os
+
 SIZES = [1, 2, 3, 5, 7, 8, 15, 16, 17, 31, 33, 63, 64, 65, 127, 128, 129, 200, 255, 256, 257, 300, 511, 513]
+if os.environ.get("PARITY_BIG") == "1":  # several K1 / INT8 tiles, ragged (slow on the CPU reference)
+    SIZES = [700, 1000, 1023, 1100, 1500]
 KINDS = ["full", "full_csr", "single", "single_csr", "continuation", "accelerated", "apply_map_full",
          "matmul", "matvec", "matvec_csr"]
 
