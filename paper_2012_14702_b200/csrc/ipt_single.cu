@@ -59,6 +59,7 @@ struct SingleProblem {
   DevBuf z[2], zi[2];
   DevBuf w, wi;              // complex path / matvec scratch
   DevBuf zc;                 // complex CSR path: the iterate interleaved (re, im) for 16-byte gathers
+  bool cspmv_simple = false; // IPT_CSPMV_SIMPLE at upload: the thread-per-row complex CSR kernel
   DevBuf wa;                 // anchor value (re, im)
   DevBuf partials;
   int64_t npart = 0;
@@ -981,7 +982,7 @@ void enqueue_cmatvec(SingleProblem& P, int src) {
   cudaStream_t s = P.ctx->stream;
   const int64_t rows = P.r1 - P.r0;
   if (rows <= 0) return;
-  if (P.csr && std::getenv("IPT_CSPMV_SIMPLE") == nullptr) {
+  if (P.csr && !P.cspmv_simple) {
     const int64_t vlen = P.n;  // the replicated iterate (global indexing)
     // (a real Delta meets a complex vector here too: kernels::matvec with complex x)
     if (P.zc.count < 2 * size_t(vlen)) P.zc.alloc(2 * size_t(std::max<int64_t>(vlen, 1)), false);
@@ -1344,6 +1345,7 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
   P->w.alloc(zlen);
   P->wi.alloc(zlen);
   if (P->csr && P->cplx) P->zc.alloc(2 * size_t(std::max<int64_t>(n, 1)), false);
+  P->cspmv_simple = std::getenv("IPT_CSPMV_SIMPLE") != nullptr;
   P->wa.alloc(2);
   P->npart = std::max<int64_t>(map_blocks(*P), 1);
   P->partials.alloc(size_t(P->npart) * 4);
