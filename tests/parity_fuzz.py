@@ -225,3 +225,111 @@ def run_case_ext(case_seed, ref):
         o = ref.solve_single(d, delta, a, tol=tol, max_iter=60)
         dz, dl = _compare_single(r, o)
     return kind, n, cplx, dz, dl
+
+
+# ---- the C++ drop-in layer (tests/cpp/cpp_api_shim.cpp): the reference's own entry points
+# on ComplexMatrix carriers, against the Python mirror (the same device path: bitwise) and
+# the reference build (north_star tolerances); with several in-process ranks
+# (ipt::b200::set_devices) and repeated solve_single calls (device-resident problem)
+KINDS_CPP = ["cpp_full", "cpp_full_csr", "cpp_single", "cpp_single_csr", "cpp_continuation", "cpp_matvec",
+             "cpp_matmul", "cpp_full_devices", "cpp_single_repeat"]
+_SHIM = None
+
+
+def shim():
+    global _SHIM
+    if _SHIM is None:
+        import ctypes as C
+
+        path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2012_14702_b200",
+                            "_build", "libcpp_api_shim.so")
+        _SHIM = C.CDLL(path)
+        _SHIM.shim_last_error.restype = C.c_char_p
+    return _SHIM
+
+
+def _ic(a):
+    """interleaved complex128 view (C-contiguous)"""
+    return np.ascontiguousarray(np.asarray(a, dtype=np.complex128))
+
+
+def draw_cpp(case_seed):
+    rng = np.random.default_rng(case_seed)
+    kind = KINDS_CPP[rng.integers(len(KINDS_CPP))]
+    n = int(SIZES[rng.integers(len(SIZES))])
+    cplx = bool(rng.random() < 0.35)
+    eps = float(rng.uniform(0.02, 0.5) / np.sqrt(max(n, 1)))
+    return rng, kind, n, cplx, eps
+
+
+def run_case_cpp(case_seed, ref):
+    import ctypes as C
+
+    rng, kind, n, cplx, eps = draw_cpp(case_seed)
+    csr = kind.endswith("csr") or kind == "cpp_matvec" and rng.random() < 0.5
+    d, delta_obj, dense = _matrix(rng, n, cplx, csr, eps)
+    L = shim()
+    P = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    dc, ac = _ic(d), _ic(dense)
+    tol = 1e-12
+    stats = np.zeros(5)
+
+    def chk(rc):
+        if rc != 0:
+            raise RuntimeError(L.shim_last_error().decode())
+
+    p = ipt.Partition(d, delta_obj)
+    g = ipt.build_gaps(p)
+    cfg = ipt.IterationConfig(tolerance=tol)
+    dz = dl = 0.0
+    if kind in ("cpp_full", "cpp_full_csr", "cpp_full_devices"):
+        devs = np.zeros(int(rng.integers(2, 4)) if kind == "cpp_full_devices" else 0, dtype=np.int32)
+        z = np.empty((n, n), np.complex128)
+        lam = np.empty(n, np.complex128)
+        chk(L.shim_solve_full(C.c_int64(n), P(dc), P(ac), C.c_int(1 if csr else 0), C.c_double(tol), C.c_int(1000),
+                              C.c_int(devs.size), P(devs), P(z), P(lam), P(stats)))
+        r = ipt.solve_full(p, g, cfg)
+        assert int(stats[0]) == r.iterations and int(stats[1]) == r.status.value
+        assert np.array_equal(z, r.Z.astype(np.complex128)), np.max(np.abs(z - r.Z))  # same device path
+        assert np.array_equal(lam, np.asarray(r.eigenvalues, dtype=np.complex128))
+        o = ref.solve_full_csr(d, delta_obj, tol=tol) if csr else ref.solve_full(d, dense, tol=tol)
+        if o["status"] == 0:
+            assert abs(int(stats[0]) - o["iterations"]) <= 1
+            dz = float(np.max(np.abs(z - o["Z"])))
+            dl = float(np.max(np.abs(lam - o["eigenvalues"]) / np.maximum(np.abs(o["eigenvalues"]), 1e-300)))
+            assert dz <= 1e-9 and dl <= 1e-10, (dz, dl)
+    elif kind in ("cpp_single", "cpp_single_csr", "cpp_continuation", "cpp_single_repeat"):
+        a = int(rng.integers(n))
+        mode = 1 if kind == "cpp_continuation" else 0
+        repeat = 3 if kind == "cpp_single_repeat" else 1
+        z = np.empty(n, np.complex128)
+        lam = np.empty(1, np.complex128)
+        chk(L.shim_solve_single(C.c_int64(n), P(dc), P(ac), C.c_int(1 if csr else 0), C.c_int64(a),
+                                C.c_double(tol), C.c_int(1000), C.c_int(mode), C.c_double(0.6), C.c_int(repeat),
+                                C.c_int(0), None, P(z), P(lam), P(stats)))
+        r = (ipt.solve_single_continuation(p, g, a, cfg, 0.6) if mode else ipt.solve_single(p, g, a, cfg))
+        assert int(stats[0]) == r.iterations and int(stats[1]) == r.status.value
+        assert np.array_equal(z, np.asarray(r.z, dtype=np.complex128)), np.max(np.abs(z - r.z))
+        o = (ref.solve_single(d, delta_obj, a, tol=tol, mode="continuation", alpha=0.6) if mode
+             else ref.solve_single(d, delta_obj, a, tol=tol))
+        if o["status"] == 0:
+            assert abs(int(stats[0]) - o["iterations"]) <= 1
+            dz = float(np.max(np.abs(z - o["z"])))
+            dl = float(abs(lam[0] - o["eigenvalue"]) / max(abs(o["eigenvalue"]), 1e-300))
+            assert dz <= 1e-9 and dl <= 1e-10, (dz, dl)
+    elif kind == "cpp_matvec":
+        x = _ic(rng.standard_normal(n) + (1j * rng.standard_normal(n) if cplx else 0))
+        y = np.empty(n, np.complex128)
+        chk(L.shim_matvec(C.c_int64(n), P(ac), C.c_int(1 if csr else 0), P(x), P(y)))
+        o = ref.matvec(dense, x)
+        dz = float(np.max(np.abs(y - o), initial=0.0))
+        assert dz <= 1e-13 * max(1.0, float(np.max(np.abs(o), initial=0.0))), dz
+    else:  # cpp_matmul
+        b = _ic(rng.standard_normal((n, n)) + (1j * rng.standard_normal((n, n)) if cplx else 0))
+        c = np.empty((n, n), np.complex128)
+        chk(L.shim_matmul(C.c_int64(n), P(ac), P(b), P(c)))
+        o = ref.matmul(dense, b)
+        scale = max(1e-300, float(np.linalg.norm(dense) * np.linalg.norm(b)))
+        dz = float(np.max(np.abs(c - o)))
+        assert dz <= 1e-13 * scale, (dz, scale)
+    return kind, n, cplx, dz, dl

@@ -13,12 +13,13 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 import oracle  # noqa: E402
 import parity_fuzz  # noqa: E402
-from parity_fuzz import draw, draw_ext, run_case, run_case_ext  # noqa: E402
+from parity_fuzz import draw, draw_cpp, draw_ext, run_case, run_case_cpp, run_case_ext  # noqa: E402
 
 first = int(sys.argv[1]) if len(sys.argv) > 1 else 100000
 count = int(sys.argv[2]) if len(sys.argv) > 2 else 1000
 ext = len(sys.argv) > 3 and sys.argv[3] == "ext"
-run, drawf = (run_case_ext, draw_ext) if ext else (run_case, draw)
+cpp = len(sys.argv) > 3 and sys.argv[3] == "cpp"
+run, drawf = (run_case_ext, draw_ext) if ext else (run_case_cpp, draw_cpp) if cpp else (run_case, draw)
 ref = oracle.ref()
 stats = collections.defaultdict(lambda: [0, 0.0, 0.0, 0])
 fails = 0
