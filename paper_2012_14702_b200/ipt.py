@@ -418,11 +418,43 @@ def apply_map_full(p: Partition, g: InverseGaps, Z, ctx: Optional[Context] = Non
     return _combine(fr, fi, cx)
 
 
+_DEVICE_GROUPS: dict = {}
+
+
+def _device_group(devices) -> list:
+    """Contexts of this process on `devices`, joined by the in-process communicator
+    (kept for later calls with the same device list)."""
+    key = tuple(int(d) for d in devices)
+    if key not in _DEVICE_GROUPS:
+        from . import dist
+
+        _DEVICE_GROUPS[key] = dist.local_contexts(len(key), key)
+    return _DEVICE_GROUPS[key]
+
+
+def _run_on_devices(devices, fn):
+    """fn(ctx) on one host thread per device of the group; rank 0's result. A failed
+    call drops the group (its communicator is aborted) so the next call opens a new one."""
+    from . import dist
+
+    ctxs = _device_group(devices)
+    try:
+        return dist.run_ranks(fn, ctxs)[0]
+    except Exception:
+        for c in _DEVICE_GROUPS.pop(tuple(int(d) for d in devices), []):
+            c.close()
+        raise
+
+
 def solve_full(p: Partition, g: InverseGaps, config: IterationConfig = None, warm_start=None,
                ctx: Optional[Context] = None, want_sigma_min: bool = True, product: str = "dmma",
-               output: str = "root", out=None) -> SpectrumResult:
+               output: str = "root", out=None, devices=None) -> SpectrumResult:
     """Fixed-point iteration of F from I (or a renormalised warm start), then the
     closing product, |MZ - Z Lambda|_F and sigma_min (solver.cpp:180-273).
+
+    devices=[0, 1, ...] (two or more; a device may repeat): the columns are sharded over
+    ranks of this process on those GPUs (in-process communicator, one host thread per
+    rank), each writing its own columns of the result -- bitwise the one-GPU result.
 
     With a communicator (column shards): output="root" gathers Z and the eigenvalues to
     rank 0; output="local" has every rank write only its own columns into full-size
@@ -433,6 +465,17 @@ def solve_full(p: Partition, g: InverseGaps, config: IterationConfig = None, war
     _validate(config)
     _check_sizes(p, g, 0)
     n = p.size()
+    if devices is not None and len(devices) > 1:
+        if ctx is not None or out is not None:
+            raise ValueError("solve_full: devices= runs its own ranks (no ctx / out)")
+        cxd = _out_complex(p, warm_start)
+        shared = (np.empty((n, n)), np.empty((n, n)) if cxd else None, np.empty(n), np.empty(n) if cxd else None)
+        r = _run_on_devices(devices, lambda c: solve_full(p, g, config, warm_start, ctx=c,
+                                                          want_sigma_min=want_sigma_min, product=product,
+                                                          output="local", out=shared))
+        r.Z = _combine(shared[0], shared[1], cxd)
+        r.eigenvalues = _combine(shared[2], shared[3], cxd)
+        return r
     ctx = ctx or default_context()
     dr, di = _planar(p.d)
     wr = wi = None
@@ -637,8 +680,14 @@ def _single_call(p, g, anchor, config, warm, schedule, alpha, ctx):
 
 
 def solve_single(p: Partition, g: InverseGaps, anchor: int, config: IterationConfig = None,
-                 warm_start=None, ctx: Optional[Context] = None) -> EigenpairResult:
-    """solver.cpp:132-136."""
+                 warm_start=None, ctx: Optional[Context] = None, devices=None) -> EigenpairResult:
+    """solver.cpp:132-136. devices=[0, 1, ...] (two or more): the rows are sharded over ranks
+    of this process on those GPUs (the iterate all-gathered every step by peer stores)."""
+    if devices is not None and len(devices) > 1:
+        if ctx is not None:
+            raise ValueError("solve_single: devices= runs its own ranks (no ctx)")
+        return _run_on_devices(devices, lambda c: _single_call(p, g, anchor, config, warm_start,
+                                                               _lib.SCHEDULE_PLAIN, 0.9, c))
     return _single_call(p, g, anchor, config, warm_start, _lib.SCHEDULE_PLAIN, 0.9, ctx)
 
 

@@ -259,3 +259,28 @@ def test_more_ranks_than_columns(n):
     for o in outs_c:
         assert o.iterations == one_c.iterations
         assert np.max(np.abs(o.z - one_c.z)) <= 1e-14
+
+
+@pytest.mark.parametrize("devices", [(0, 0), (0, 0, 0)])
+def test_devices_argument_is_bitwise_one_gpu(devices):
+    """solve_full / solve_single(devices=[...]): ranks of this process on those GPUs (here one
+    B200 listed several times), bitwise the one-GPU result; a failed call reopens the group."""
+    p = synth.dense_uniform(1000, 0.3 / np.sqrt(1000), 21)
+    g = ipt.build_gaps(p)
+    cfg = ipt.IterationConfig(tolerance=1e-12)
+    one = ipt.solve_full(p, g, cfg)
+    r = ipt.solve_full(p, g, cfg, devices=list(devices))
+    assert r.iterations == one.iterations
+    assert np.array_equal(r.Z, one.Z) and np.array_equal(r.eigenvalues, one.eigenvalues)
+    q = synth.csr_ci(1 << 14, 16, 0.01, 3)
+    gq = ipt.build_gaps(q, 0.0)
+    s1 = ipt.solve_single(q, gq, 0, ipt.IterationConfig(tolerance=1e-10))
+    s = ipt.solve_single(q, gq, 0, ipt.IterationConfig(tolerance=1e-10), devices=list(devices))
+    assert s.iterations == s1.iterations
+    assert np.max(np.abs(s.z - s1.z)) <= 1e-14
+    bad = np.eye(1000)
+    bad[5, 5] = 0.0
+    with pytest.raises(Exception):
+        ipt.solve_full(p, g, cfg, warm_start=bad, devices=list(devices))
+    r2 = ipt.solve_full(p, g, cfg, devices=list(devices))
+    assert np.array_equal(r2.Z, one.Z)
