@@ -127,6 +127,18 @@ def test_invalid_config_is_rejected_before_any_device_call():
         ipt.solve_single_continuation(p, ipt.build_gaps(p), 0, shrink_alpha=1.5)
 
 
+def test_devices_argument_is_validated_before_any_device_call():
+    p = ipt.Partition(np.array([0.0, 1.0]), np.zeros((2, 2)))
+    g = ipt.build_gaps(p)
+    fake_ctx = object()
+    with pytest.raises(ValueError):
+        ipt.solve_full(p, g, devices=[0, 1], ctx=fake_ctx)
+    with pytest.raises(ValueError):
+        ipt.solve_full(p, g, devices=[0, 1], out=(None, None, None, None))
+    with pytest.raises(ValueError):
+        ipt.solve_single(p, g, 0, devices=[0, 1], ctx=fake_ctx)
+
+
 def test_product_does_not_import_oracle():
     """The product path must never route through the CPU oracle."""
     pkg = os.path.join(ROOT, "paper_2012_14702_b200")
