@@ -16,6 +16,7 @@
 // HBM layout: dense Delta row-major, ld = round_up(n,16) (rows of this rank only);
 // CSR int64 row offsets (rebased to the shard), int32 columns, fp64 values;
 // z ping-pong vectors of length nranks*chunk, replicated.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <complex>
@@ -41,6 +42,9 @@ struct SingleProblem {
   std::unique_ptr<int64_t, void (*)(void*)> rowptr{nullptr, [](void* p) { cudaFree(p); }};
   std::unique_ptr<int32_t, void (*)(void*)> cols{nullptr, [](void* p) { cudaFree(p); }};
   DevBuf vals, valsi;
+  // balanced CSR variants: first row group of every warp of the map grid (nwarps + 1)
+  std::unique_ptr<int32_t, void (*)(void*)> wgroups{nullptr, [](void* p) { cudaFree(p); }};
+  bool spmv_bal = false;  // the map runs the balanced group ranges (wgroups)
   // anchor row copy (dense: lda doubles; csr: its nonzeros)
   DevBuf arow, arowi;
   std::unique_ptr<int32_t, void (*)(void*)> acols{nullptr, [](void* p) { cudaFree(p); }};
@@ -115,7 +119,8 @@ constexpr SpmvVariant kSpmvVariants[] = {{16, 4, 0, 5}, {8, 8, 0, 5}, {32, 2, 0,
                                          {0, 4, 4, 4},  {0, 2, 8, 4}, {0, 2, 4, 5}, {0, 4, 4, 3},
                                          {0, 4, 4, 4},  {0, 4, 16, 3}, {0, 8, 4, 3},  {0, 4, 2, 4},
                                          {0, 8, 2, 4},  {0, 8, 4, 4},  {0, 4, 8, 4},
-                                         {0, 4, 4, 4},  {0, 4, 4, 3},  {0, 2, 4, 5}};  // 16-18: + offset prefetch
+                                         {0, 4, 4, 4},  {0, 4, 4, 3},  {0, 2, 4, 5},   // 16-18: + offset prefetch
+                                         {0, 4, 4, 4}};  // 19: 16 with nnz-balanced contiguous group ranges per warp
 constexpr int kNumSpmvVariants = sizeof(kSpmvVariants) / sizeof(kSpmvVariants[0]);
 constexpr int kSpmvDefault = 16;  // warp-contiguous groups of 4 rows, 4 in flight, plain nc loads, offset prefetch
 inline int spmv_variant() {
@@ -349,6 +354,7 @@ struct MapArgs {
   double* partials;
   double* peer[kMaxPeers];  // kMvMap: the same rows of the new iterate in every peer's z
   int npeers;
+  const int32_t* wgroups;   // balanced CSR variants: first row group of each warp (else null)
   // Fused step tail (kMvMap; tail_mode 0: none). The last CTA to finish sums the per-CTA
   // partials in reduce_partials_kernel's order into tail_sums; mode 2 (one rank) then also
   // applies the stop decision (decide_single_dev) and forms w_a of the new iterate for the
@@ -623,7 +629,7 @@ __global__ void __launch_bounds__(256, kSpmvMinBlocks) spmv_map_kernel(const int
   }
 }
 
-template <int MODE, int R, int U, int MINB, bool POL = true, bool PF = false>
+template <int MODE, int R, int U, int MINB, bool POL = true, bool PF = false, bool BAL = false>
 __global__ void __launch_bounds__(256, MINB) spmv_group_kernel(const int64_t* __restrict__ rowptr,
                                                                          const int32_t* __restrict__ cols,
                                                                          const double* __restrict__ vals, MapArgs a) {
@@ -634,19 +640,24 @@ __global__ void __launch_bounds__(256, MINB) spmv_group_kernel(const int64_t* __
   const double scale = MODE == kMvMap ? schedule_scale(a) : 1.0;
   const double lam = (MODE == kMvFinal || MODE == kMvAccel) ? a.d[a.anchor] + *a.wa : 0.0;
   const uint64_t pol_s = policy_stream(), pol_k = policy_keep();
-  // Persistent fixed grid: warp w of block b owns row groups (b*8 + w) + k*(grid*8).
+  // Persistent fixed grid: warp w of block b owns row groups (b*8 + w) + k*(grid*8), or
+  // (BAL) the contiguous group range [wgroups[w], wgroups[w+1]) cut at equal nonzero counts.
+  // The groups themselves (R consecutive rows from a multiple of R) and so every row's sum
+  // are the same either way; only which warp -- and CTA partial -- takes them changes.
   const int64_t groups = ceil_div(a.rows, int64_t(R));
-  const int64_t nwarps = int64_t(gridDim.x) * 8;
+  const int64_t wglob = blockIdx.x * int64_t(8) + (threadIdx.x >> 5);
+  const int64_t g_begin = BAL ? a.wgroups[wglob] : wglob;
+  const int64_t g_end = BAL ? a.wgroups[wglob + 1] : groups;
+  const int64_t g_step = BAL ? 1 : int64_t(gridDim.x) * 8;
   // PF: the next group's row offsets load while this group streams (one dependent
   // load off the critical path per group)
-  const int64_t first = blockIdx.x * int64_t(8) + (threadIdx.x >> 5);
-  long long next_off = PF && first < groups ? group_offsets<R>(rowptr, first * R, a.rows, lane) : 0;
-  for (int64_t grp = first; grp < groups; grp += nwarps) {
+  long long next_off = PF && g_begin < g_end ? group_offsets<R>(rowptr, g_begin * R, a.rows, lane) : 0;
+  for (int64_t grp = g_begin; grp < g_end; grp += g_step) {
     const int64_t lr0 = grp * R;
     double sum[R];
     if (PF) {
       const long long off = next_off;
-      if (grp + nwarps < groups) next_off = group_offsets<R>(rowptr, (grp + nwarps) * R, a.rows, lane);
+      if (grp + g_step < g_end) next_off = group_offsets<R>(rowptr, (grp + g_step) * R, a.rows, lane);
       group_row_sums_at<R, U, POL>(off, cols, vals, a.z, lane, pol_s, pol_k, sum);
     } else {
       group_row_sums<R, U, POL>(rowptr, cols, vals, a.z, lr0, a.rows, lane, pol_s, pol_k, sum);
@@ -909,6 +920,10 @@ constexpr int kCmapBlocks = 296;
 template <int MODE>
 void launch_spmv(unsigned grid, cudaStream_t s, const int64_t* rowptr, const int32_t* cols, const double* vals,
                  const MapArgs& a) {
+  if (a.wgroups != nullptr) {  // balanced group ranges (decided per problem at upload)
+    spmv_group_kernel<MODE, 4, 4, 4, false, true, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a);
+    return;
+  }
   switch (spmv_variant()) {
 #define IPT_SPMV(K, L, UU) \
   case K: spmv_map_kernel<MODE, L, UU><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
@@ -925,6 +940,7 @@ void launch_spmv(unsigned grid, cudaStream_t s, const int64_t* rowptr, const int
     case 16: spmv_group_kernel<MODE, 4, 4, 4, false, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
     case 17: spmv_group_kernel<MODE, 4, 4, 3, false, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
     case 18: spmv_group_kernel<MODE, 4, 2, 5, false, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 19: spmv_group_kernel<MODE, 4, 4, 4, false, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
 #undef IPT_SPMV
 #undef IPT_SPMVG
   }
@@ -947,6 +963,7 @@ MapArgs map_args(SingleProblem& P, int src) {
     for (int q = 0; q < P.npeers; ++q) a.peer[q] = P.peer_z[src ^ 1][q];
   }
   a.wa = P.wa.get();
+  a.wgroups = P.wgroups.get();
   a.anchor = P.anchor;
   a.row0 = P.r0;
   a.rows = P.r1 - P.r0;
@@ -1298,6 +1315,75 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
     IPT_CUDA(cudaMalloc(&drp, sizeof(int64_t) * (rows + 1)));
     P->rowptr.reset(drp);
     h2d_bytes(c, drp, rp.data(), sizeof(int64_t) * (rows + 1));
+    const int vdef = spmv_variant();
+    if ((vdef == kSpmvDefault || vdef == 19) && !P->cplx) {
+      // Balanced group ranges: warp w of the map grid takes groups [gs[w], gs[w+1]),
+      // cut where the running cost (nonzeros + kRowCost per row) crosses w / nwarps of the
+      // total -- a few very long rows no longer pile onto one warp of the round-robin.
+      // Taken when the round-robin's busiest warp would carry more than kImbalance x the
+      // mean cost (tools/probes/skew_probe.py: 0.2 % of rows with 8000 entries, imbalance
+      // 2.14: 0.957 -> 0.690 ms; lognormal row lengths, 1.27: 0.556 -> 0.515 ms; heavy rows
+      // clustered in blocks, 1.27: 0.583 -> 0.650 ms, slower; config 5, 1.01: the
+      // round-robin's interleaved streams are ~1 % faster). IPT_SPMV_VARIANT=19: always
+      // balanced, IPT_SPMV_BALANCE=0: never.
+      static const int64_t kRowCost = [] {  // a row's offsets and epilogue, in entry-equivalents
+        const char* e = std::getenv("IPT_SPMV_ROWCOST");
+        return e ? std::max<int64_t>(0, std::atoll(e)) : int64_t(16);
+      }();
+      constexpr double kImbalance = 1.5;
+      const int R = kSpmvVariants[vdef].rows;
+      const int64_t groups = ceil_div(rows, int64_t(R));
+      const int64_t nw = std::max<int64_t>(map_blocks(*P), 1) * 8;
+      auto cost = [&](int64_t g) {
+        const int64_t r = std::min<int64_t>(g * R, rows);
+        return rp[r] + kRowCost * r;
+      };
+      const int64_t total = cost(groups);
+      bool balance = vdef == 19;
+      if (!balance && groups > 0) {
+        static const bool allowed = [] {
+          const char* e = std::getenv("IPT_SPMV_BALANCE");
+          return !(e && e[0] == '0');
+        }();
+        if (allowed) {
+          std::vector<int64_t> rr(nw, 0);
+          for (int64_t g = 0; g < groups; ++g) rr[g % nw] += cost(g + 1) - cost(g);
+          const int64_t mx = *std::max_element(rr.begin(), rr.end());
+          const double imb = double(mx) * double(nw) / double(std::max<int64_t>(total, 1));
+          balance = imb > kImbalance;
+          if (std::getenv("IPT_PROFILE"))
+            std::fprintf(stderr, "[ipt] csr map: round-robin imbalance %.3f -> %s group ranges\n", imb,
+                         balance ? "balanced" : "round-robin");
+        }
+      }
+      P->spmv_bal = balance;
+    }
+    if (P->spmv_bal) {
+      static const int64_t kRowCost = [] {
+        const char* e = std::getenv("IPT_SPMV_ROWCOST");
+        return e ? std::max<int64_t>(0, std::atoll(e)) : int64_t(16);
+      }();
+      const int R = kSpmvVariants[spmv_variant()].rows;
+      const int64_t groups = ceil_div(rows, int64_t(R));
+      const int64_t nw = std::max<int64_t>(map_blocks(*P), 1) * 8;
+      auto cost = [&](int64_t g) {
+        const int64_t r = std::min<int64_t>(g * R, rows);
+        return rp[r] + kRowCost * r;
+      };
+      const int64_t total = cost(groups);
+      std::vector<int32_t> gs(nw + 1);
+      int64_t g = 0;
+      for (int64_t w = 0; w < nw; ++w) {
+        const int64_t target = static_cast<int64_t>((static_cast<__int128>(total) * w) / nw);
+        while (g < groups && cost(g) < target) ++g;
+        gs[w] = static_cast<int32_t>(g);
+      }
+      gs[nw] = static_cast<int32_t>(groups);
+      int32_t* dgs = nullptr;
+      IPT_CUDA(cudaMalloc(&dgs, sizeof(int32_t) * (nw + 1)));
+      P->wgroups.reset(dgs);
+      h2d_bytes(c, dgs, gs.data(), sizeof(int32_t) * (nw + 1));
+    }
     int32_t* dc = nullptr;
     IPT_CUDA(cudaMalloc(&dc, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
     P->cols.reset(dc);
