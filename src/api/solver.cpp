@@ -156,7 +156,12 @@ ipt_ctx* context() {
         dev = env ? std::atoi(env) : 0;
     }
     if (t_ctx.ctx == nullptr || t_ctx.device != dev) {
-        if (t_ctx.ctx) ipt_ctx_destroy(t_ctx.ctx);
+        if (t_ctx.ctx) {
+            // device-resident operators / problems belong to this context: drop them before
+            // it goes (a new context could reuse its address)
+            kernels::release_resident_operators();
+            ipt_ctx_destroy(t_ctx.ctx);
+        }
         t_ctx.ctx = nullptr;
         check(ipt_ctx_create(dev, &t_ctx.ctx));
         t_ctx.device = dev;
