@@ -394,8 +394,12 @@ void h2d_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t sp
   double t_wait = 0.0, t_copy = 0.0;
   auto now = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   const double t_start = now();
-  for (int64_t r0 = 0; r0 < rows; r0 += per, b ^= 1) {
-    const int64_t nr = std::min(per, rows - r0);
+  // a transfer that fits one staging buffer still goes in >= 4 chunks of >= 1 MB, so the
+  // host copy of chunk k+1 overlaps the DMA of chunk k
+  const int64_t min_rows = std::max<int64_t>(1, (int64_t(1) << 17) / cols);
+  const int64_t step = std::max(min_rows, std::min(per, (rows + 3) / 4));
+  for (int64_t r0 = 0; r0 < rows; r0 += step, b ^= 1) {
+    const int64_t nr = std::min(step, rows - r0);
     double t0 = now();
     if (used[b]) IPT_CUDA(cudaEventSynchronize(c.stage_ev[b]));  // DMA of this buffer done
     double t1 = now();
@@ -438,14 +442,16 @@ void d2h_rows(Ctx& c, double* dst, int64_t dpitch, const double* src, int64_t sp
   if (rows <= 0 || cols <= 0) return;
   cudaStream_t st = stream ? stream : c.stream;
   ensure_staging(c);
-  const int64_t per = static_cast<int64_t>(c.stage_doubles) / cols;
-  if (per < 1) {
+  const int64_t per_max = static_cast<int64_t>(c.stage_doubles) / cols;
+  if (per_max < 1) {
     IPT_CUDA(cudaMemcpy2DAsync(dst, dpitch * sizeof(double), src, spitch * sizeof(double), cols * sizeof(double),
                                rows, cudaMemcpyDeviceToHost, st));
     IPT_CUDA(cudaStreamSynchronize(st));
     return;
   }
-  // DMA chunk k+1 into one buffer while the host drains chunk k from the other.
+  // DMA chunk k+1 into one buffer while the host drains chunk k from the other (a
+  // transfer that fits one buffer still goes in >= 4 chunks of >= 1 MB to overlap them).
+  const int64_t per = std::max(std::max<int64_t>(1, (int64_t(1) << 17) / cols), std::min(per_max, (rows + 3) / 4));
   const int64_t nchunks = (rows + per - 1) / per;
   auto issue = [&](int64_t k) {
     const int64_t r0 = k * per, nr = std::min(per, rows - r0);
