@@ -168,13 +168,25 @@ def traffic_for(kernel, n=None):
 # --------------------------------------------------------------------------- CPU baseline
 
 
+def use_all_host_threads():
+    """The reference's OpenMP on every host core (torchrun exports OMP_NUM_THREADS=1 to
+    each rank; torch may have initialised libgomp already): the environment for libraries
+    loaded later, and the calling thread's ICV for the one already loaded."""
+    threads = os.cpu_count() or 1
+    os.environ["OMP_NUM_THREADS"] = str(threads)
+    try:
+        C.CDLL("libgomp.so.1").omp_set_num_threads(threads)
+    except OSError:
+        pass
+    return threads
+
+
 def cpu_reference_sample(n=4096, reps=2):
     """The reference's own apply_map_full (solver.cpp:156-178; kernels.cpp dgemm) on the
     host cores, one map application at a bounded N of the same construction."""
     import oracle
 
-    threads = os.cpu_count() or 1
-    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    use_all_host_threads()
     d, delta = oracle.port().dense_uniform(n, 0.32 / math.sqrt(n), 42)  # no product library here
     if oracle.have_ref():
         R, kind = oracle.ref(), "reference"
@@ -211,7 +223,7 @@ def per_config_e2e(ipt, ctx):
     if not oracle.have_ref():
         return {"error": "reference build absent (oracle/_ref)"}
     R = oracle.ref()
-    out = {"cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))}
+    out = {"cores": use_all_host_threads()}
     p1 = synth.config1()
     cfg1 = ipt.IterationConfig(tolerance=1e-12)
     ipt.solve_full(p1, ipt.build_gaps(p1), cfg1, ctx=ctx)  # warm
@@ -253,8 +265,7 @@ def run_reference_arm(args):
     import oracle
 
     n = args.ref_n
-    threads = os.cpu_count() or 1
-    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    use_all_host_threads()  # every host core, also under torchrun (OMP_NUM_THREADS=1 there)
     # Inputs from the reference's generator restated in the oracle (rng.hpp, SURVEY 8(d)
     # draw order): this process loads only oracle/ libraries, never libipt_b200.so.
     d, delta = oracle.port().dense_uniform(n, 0.32 / math.sqrt(n), 42)
