@@ -18,6 +18,7 @@
 // z ping-pong vectors of length nranks*chunk, replicated.
 #include <algorithm>
 #include <cmath>
+#include <climits>
 #include <cstdlib>
 #include <complex>
 #include <cstring>
@@ -107,8 +108,11 @@ constexpr int kRowsPerBlock = kGemvRows * kGemvWarps;
 // {16,4} 0.689, {16,6} 0.753, {32,2} 0.832, {8,8} 0.905. Warp-contiguous row groups
 // (spmv_group_kernel): 4 rows x 4 in flight 0.644 ms with L2 cache hints, 0.632 ms
 // without (variant 9); with the next group's row offsets loaded while the current group
-// streams 0.627 ms (default, variant 16; round 2, with the fused step tail); the memory
-// ceiling of the same traffic is 0.517 ms (profiles/r01_gather_probe.txt).
+// streams 0.627 ms (variant 16; round 2, with the fused step tail); the four xor trees
+// folded into one and 32-bit relative positions 0.613 ms (variant 20); that with the index /
+// value loads software-pipelined 0.601 ms (variant 24, spmv_pipe_kernel, the default; all
+// three give the same bits). The memory ceiling of the same traffic is 0.517 ms
+// (profiles/r01_gather_probe.txt): one L1 -> crossbar request per clock per SM.
 // IPT_SPMV_VARIANT selects another.
 // Variants 5-7: warp-contiguous row groups (spmv_group_kernel), lanes = 0 marks them,
 // u = entries in flight per lane, rows = rows per warp.
@@ -120,9 +124,12 @@ constexpr SpmvVariant kSpmvVariants[] = {{16, 4, 0, 5}, {8, 8, 0, 5}, {32, 2, 0,
                                          {0, 4, 4, 4},  {0, 4, 16, 3}, {0, 8, 4, 3},  {0, 4, 2, 4},
                                          {0, 8, 2, 4},  {0, 8, 4, 4},  {0, 4, 8, 4},
                                          {0, 4, 4, 4},  {0, 4, 4, 3},  {0, 2, 4, 5},   // 16-18: + offset prefetch
-                                         {0, 4, 4, 4}};  // 19: 16 with nnz-balanced contiguous group ranges per warp
+                                         {0, 4, 4, 4},   // 19: 16 with nnz-balanced contiguous group ranges per warp
+                                         {0, 4, 4, 4},  {0, 4, 4, 5},  {0, 8, 4, 4},   // 20-22: 16 with folded row sums
+                                         {0, 4, 4, 4},  {0, 2, 4, 4},  {0, 2, 4, 5},  {0, 4, 4, 3},
+                                         {0, 2, 4, 6}};  // 23-27: 20 with software-pipelined loads
 constexpr int kNumSpmvVariants = sizeof(kSpmvVariants) / sizeof(kSpmvVariants[0]);
-constexpr int kSpmvDefault = 16;  // warp-contiguous groups of 4 rows, 4 in flight, plain nc loads, offset prefetch
+constexpr int kSpmvDefault = 24;  // warp-contiguous groups of 4 rows, folded row sums, software-pipelined loads (2 + 2 in flight)
 inline int spmv_variant() {
   static const int v = [] {
     const char* e = std::getenv("IPT_SPMV_VARIANT");
@@ -340,6 +347,63 @@ __device__ __forceinline__ void group_row_sums_at(long long mine, const int32_t*
     for (int off = 16; off > 0; off >>= 1) s[k] += __shfl_xor_sync(0xffffffffu, s[k], off);
 }
 
+// group_row_sums_at for R = 4 with the same sums at lower instruction cost (round 2):
+//  * entry positions relative to the group start in 32 bits (one 64-bit base broadcast +
+//    four 32-bit offsets: 6 SHFL instead of 10; 32-bit row selection);
+//  * the four xor trees folded into one transposed tree: after level 16 a lane keeps two
+//    rows, after level 8 one row (row 2 bit4 + bit3 of the lane), levels 4/2/1 as before,
+//    and one shuffle returns row k to lane k: 7 double shuffles instead of 20. Every
+//    level adds the same two numbers the full xor tree adds on that lane, so each row sum
+//    is bit for bit group_row_sums_at's.
+// Returns this lane's row sum (row k on lane k < 4).
+template <int U>
+__device__ __forceinline__ double group_row_sums4_folded(long long mine, const int32_t* __restrict__ cols,
+                                                         const double* __restrict__ vals,
+                                                         const double* __restrict__ z, int lane) {
+  const long long base = __shfl_sync(0xffffffffu, mine, 0);
+  const int rel = static_cast<int>(mine - base);
+  const int r1 = __shfl_sync(0xffffffffu, rel, 1), r2 = __shfl_sync(0xffffffffu, rel, 2),
+            r3 = __shfl_sync(0xffffffffu, rel, 3), end = __shfl_sync(0xffffffffu, rel, 4);
+  const int32_t* __restrict__ gc = cols + base;
+  const double* __restrict__ gv = vals + base;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  for (int q0 = lane; q0 < end; q0 += 32 * U) {
+    int32_t c[U];
+    double v[U], zz[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int q = q0 + 32 * u;
+      c[u] = q < end ? ld_nc_i32(gc + q) : 0;
+      v[u] = q < end ? ld_nc_f64(gv + q) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) zz[u] = (q0 + 32 * u < end) ? __ldg(z + c[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int q = q0 + 32 * u;
+      if (q < end) {
+        if (q < r2) {
+          if (q < r1) s0 = __fma_rn(v[u], zz[u], s0);
+          else s1 = __fma_rn(v[u], zz[u], s1);
+        } else {
+          if (q < r3) s2 = __fma_rn(v[u], zz[u], s2);
+          else s3 = __fma_rn(v[u], zz[u], s3);
+        }
+      }
+    }
+  }
+  const bool b16 = lane & 16, b8 = lane & 8;
+  double k0 = b16 ? s2 : s0, k1 = b16 ? s3 : s1;
+  k0 += __shfl_xor_sync(0xffffffffu, b16 ? s0 : s2, 16);
+  k1 += __shfl_xor_sync(0xffffffffu, b16 ? s1 : s3, 16);
+  double k = b8 ? k1 : k0;
+  k += __shfl_xor_sync(0xffffffffu, b8 ? k0 : k1, 8);
+  k += __shfl_xor_sync(0xffffffffu, k, 4);
+  k += __shfl_xor_sync(0xffffffffu, k, 2);
+  k += __shfl_xor_sync(0xffffffffu, k, 1);
+  return __shfl_sync(0xffffffffu, k, (lane & 3) * 8);
+}
+
 struct MapArgs {
   const double* d;     // global diagonal
   const double* z;     // current iterate (global indexing)
@@ -383,9 +447,18 @@ __device__ __forceinline__ void peer_fence(const MapArgs& a) {
 
 // Per-row epilogue shared by dense and CSR kernels. Accumulates into v.
 template <int MODE>
+__device__ __forceinline__ void row_epilogue_vals(const MapArgs& a, int64_t i, double zi, double di, double w,
+                                                  double scale, double lam, double v[4]);
+template <int MODE>
 __device__ __forceinline__ void row_epilogue(const MapArgs& a, int64_t i, double w, double scale,
                                              double lam, double v[4]) {
-  const double zi = a.z[i];
+  row_epilogue_vals<MODE>(a, i, a.z[i], MODE == kMvStore ? 0.0 : a.d[i], w, scale, lam, v);
+}
+// The same epilogue with z_i and d_i already loaded (the pipelined CSR kernel loads them
+// while the row's entries stream).
+template <int MODE>
+__device__ __forceinline__ void row_epilogue_vals(const MapArgs& a, int64_t i, double zi, double di, double w,
+                                                  double scale, double lam, double v[4]) {
   if (MODE == kMvStore) {
     a.fz[i] = w;
   } else if (MODE == kMvMap) {
@@ -393,7 +466,7 @@ __device__ __forceinline__ void row_epilogue(const MapArgs& a, int64_t i, double
     if (i == a.anchor) {
       f = 1.0;
     } else {
-      const double g = __ddiv_rn(1.0, __dsub_rn(a.d[i], a.d[a.anchor]));
+      const double g = __ddiv_rn(1.0, __dsub_rn(di, a.d[a.anchor]));
       f = __dmul_rn(scale, __dmul_rn(g, __dsub_rn(__dmul_rn(zi, *a.wa), w)));
     }
     a.fz[i] = f;
@@ -404,16 +477,16 @@ __device__ __forceinline__ void row_epilogue(const MapArgs& a, int64_t i, double
     v[2] = __fma_rn(f, f, v[2]);
     v[3] = nan_max(v[3], fabs(df));
   } else if (MODE == kMvFinal) {  // residual |d z + w - lam z|^2 and |z|^2 (solver.cpp:86-91)
-    const double r = __dsub_rn(__dadd_rn(__dmul_rn(a.d[i], zi), w), __dmul_rn(lam, zi));
+    const double r = __dsub_rn(__dadd_rn(__dmul_rn(di, zi), w), __dmul_rn(lam, zi));
     v[0] = __fma_rn(r, r, v[0]);
     v[1] = __fma_rn(zi, zi, v[1]);
   } else {  // kMvAccel: true residual AND the plain image f(z) (anderson.cpp:204-223)
-    const double r = __dsub_rn(__dadd_rn(__dmul_rn(a.d[i], zi), w), __dmul_rn(lam, zi));
+    const double r = __dsub_rn(__dadd_rn(__dmul_rn(di, zi), w), __dmul_rn(lam, zi));
     double f;
     if (i == a.anchor) {
       f = 1.0;
     } else {
-      const double g = __ddiv_rn(1.0, __dsub_rn(a.d[i], a.d[a.anchor]));
+      const double g = __ddiv_rn(1.0, __dsub_rn(di, a.d[a.anchor]));
       f = __dmul_rn(g, __dsub_rn(__dmul_rn(zi, *a.wa), w));
     }
     a.fz[i] = f;
@@ -629,7 +702,7 @@ __global__ void __launch_bounds__(256, kSpmvMinBlocks) spmv_map_kernel(const int
   }
 }
 
-template <int MODE, int R, int U, int MINB, bool POL = true, bool PF = false, bool BAL = false>
+template <int MODE, int R, int U, int MINB, bool POL = true, bool PF = false, bool BAL = false, bool FOLD = false>
 __global__ void __launch_bounds__(256, MINB) spmv_group_kernel(const int64_t* __restrict__ rowptr,
                                                                          const int32_t* __restrict__ cols,
                                                                          const double* __restrict__ vals, MapArgs a) {
@@ -655,6 +728,14 @@ __global__ void __launch_bounds__(256, MINB) spmv_group_kernel(const int64_t* __
   for (int64_t grp = g_begin; grp < g_end; grp += g_step) {
     const int64_t lr0 = grp * R;
     double sum[R];
+    if (FOLD) {  // PF, R = 4, plain nc loads: the folded tree leaves row k's sum on lane k
+      static_assert(!FOLD || (R == 4 && PF && !POL), "folded sums: R = 4, offset prefetch, plain loads");
+      const long long off = next_off;
+      if (grp + g_step < g_end) next_off = group_offsets<R>(rowptr, (grp + g_step) * R, a.rows, lane);
+      const double w = group_row_sums4_folded<U>(off, cols, vals, a.z, lane);
+      if (lane < R && lr0 + lane < a.rows) row_epilogue<MODE>(a, a.row0 + lr0 + lane, w, scale, lam, v);
+      continue;
+    }
     if (PF) {
       const long long off = next_off;
       if (grp + g_step < g_end) next_off = group_offsets<R>(rowptr, (grp + g_step) * R, a.rows, lane);
@@ -669,6 +750,125 @@ __global__ void __launch_bounds__(256, MINB) spmv_group_kernel(const int64_t* __
         if (lane == k) w = sum[k];
       row_epilogue<MODE>(a, a.row0 + lr0 + lane, w, scale, lam, v);
     }
+  }
+  if (MODE == kMvStore) return;
+  if (MODE == kMvMap) peer_fence(a);
+  block_reduce4<8>(v, red);
+  if (threadIdx.x == 0) {
+    double* o = a.partials + size_t(blockIdx.x) * 4;
+    o[0] = v[0]; o[1] = v[1]; o[2] = v[2]; o[3] = v[3];
+  }
+  if (MODE == kMvMap && a.tail_mode != 0) step_tail(a);
+}
+
+// spmv_group_kernel<MODE, 4, U, MINB, plain loads, offset prefetch, folded sums> with the
+// loads software-pipelined (round 2): the K8 map is bound by load latency, not by a
+// throughput (ncu: issue slots 36 % busy, long-scoreboard stalls, the L1 -> crossbar request
+// path 80 % busy), because a warp alternates between waiting for a chunk's index / value
+// loads and waiting for its z gathers. Here the next chunk's indices and values (the next
+// group's first chunk after a group's last, its offsets known two groups ahead) are
+// requested before the current chunk's gathers are consumed, and the rows' d_i, z_i of the
+// epilogue load at the group's start. Same groups, same lanes, same order of operations:
+// every row sum, iterate and stop sum is bit for bit spmv_group_kernel's.
+__device__ __forceinline__ double ld_nc_gather_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+template <int MODE, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) spmv_pipe_kernel(const int64_t* __restrict__ rowptr,
+                                                              const int32_t* __restrict__ cols,
+                                                              const double* __restrict__ vals, MapArgs a) {
+  if (a.state != nullptr && a.state->done) return;
+  constexpr int R = 4;
+  __shared__ double red[8][4];
+  const int lane = threadIdx.x & 31;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  const double scale = MODE == kMvMap ? schedule_scale(a) : 1.0;
+  const double lam = (MODE == kMvFinal || MODE == kMvAccel) ? a.d[a.anchor] + *a.wa : 0.0;
+  const int64_t groups = ceil_div(a.rows, int64_t(R));
+  const int64_t g_begin = blockIdx.x * int64_t(8) + (threadIdx.x >> 5);
+  const int64_t g_step = int64_t(gridDim.x) * 8;
+  // offsets of this group and the next one in registers, the one after that in flight
+  long long off0 = g_begin < groups ? group_offsets<R>(rowptr, g_begin * R, a.rows, lane) : 0;
+  long long off1 = g_begin + g_step < groups ? group_offsets<R>(rowptr, (g_begin + g_step) * R, a.rows, lane) : 0;
+  int32_t c[U];
+  double x[U];
+  {  // first chunk of the first group
+    const long long base = __shfl_sync(0xffffffffu, off0, 0);
+    const int end = static_cast<int>(__shfl_sync(0xffffffffu, off0, R) - base);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int q = lane + 32 * u;
+      c[u] = q < end ? ld_nc_i32(cols + base + q) : 0;
+      x[u] = q < end ? ld_nc_f64(vals + base + q) : 0.0;
+    }
+  }
+  for (int64_t grp = g_begin; grp < groups; grp += g_step) {
+    const int64_t lr0 = grp * R;
+    const long long off2 =
+        grp + 2 * g_step < groups ? group_offsets<R>(rowptr, (grp + 2 * g_step) * R, a.rows, lane) : 0;
+    const bool mine = lane < R && lr0 + lane < a.rows;
+    const int64_t gi = a.row0 + lr0 + lane;
+    const double zi = (mine && MODE != kMvStore) ? a.z[gi] : 0.0;  // store mode: a plain matvec, z may be shorter
+    const double di = (mine && MODE != kMvStore) ? a.d[gi] : 0.0;
+    const long long base = __shfl_sync(0xffffffffu, off0, 0);
+    const int rel = static_cast<int>(off0 - base);
+    const int r1 = __shfl_sync(0xffffffffu, rel, 1), r2 = __shfl_sync(0xffffffffu, rel, 2),
+              r3 = __shfl_sync(0xffffffffu, rel, 3), end = __shfl_sync(0xffffffffu, rel, 4);
+    const bool more = grp + g_step < groups;
+    const long long nbase = __shfl_sync(0xffffffffu, off1, 0);
+    const int nend = more ? static_cast<int>(__shfl_sync(0xffffffffu, off1, R) - nbase) : 0;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int qc = 0;
+    do {  // a group without entries still takes one (empty) pass: its chunk registers are consumed
+      double zz[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) zz[u] = (qc + lane + 32 * u < end) ? ld_nc_gather_f64(a.z + c[u]) : 0.0;
+      int32_t nc[U];
+      double nx[U];
+      const bool last = qc + 32 * U >= end;
+      const long long pb = last ? nbase : base;
+      const int pq = last ? lane : qc + 32 * U + lane, pe = last ? nend : end;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = pq + 32 * u;
+        nc[u] = q < pe ? ld_nc_i32(cols + pb + q) : 0;
+        nx[u] = q < pe ? ld_nc_f64(vals + pb + q) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = qc + lane + 32 * u;
+        if (q < end) {
+          if (q < r2) {
+            if (q < r1) s0 = __fma_rn(x[u], zz[u], s0);
+            else s1 = __fma_rn(x[u], zz[u], s1);
+          } else {
+            if (q < r3) s2 = __fma_rn(x[u], zz[u], s2);
+            else s3 = __fma_rn(x[u], zz[u], s3);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        c[u] = nc[u];
+        x[u] = nx[u];
+      }
+      qc += 32 * U;
+    } while (qc < end);
+    const bool b16 = lane & 16, b8 = lane & 8;
+    double k0 = b16 ? s2 : s0, k1 = b16 ? s3 : s1;
+    k0 += __shfl_xor_sync(0xffffffffu, b16 ? s0 : s2, 16);
+    k1 += __shfl_xor_sync(0xffffffffu, b16 ? s1 : s3, 16);
+    double k = b8 ? k1 : k0;
+    k += __shfl_xor_sync(0xffffffffu, b8 ? k0 : k1, 8);
+    k += __shfl_xor_sync(0xffffffffu, k, 4);
+    k += __shfl_xor_sync(0xffffffffu, k, 2);
+    k += __shfl_xor_sync(0xffffffffu, k, 1);
+    const double w = __shfl_sync(0xffffffffu, k, (lane & 3) * 8);
+    if (mine) row_epilogue_vals<MODE>(a, gi, zi, di, w, scale, lam, v);
+    off0 = off1;
+    off1 = off2;
   }
   if (MODE == kMvStore) return;
   if (MODE == kMvMap) peer_fence(a);
@@ -941,6 +1141,14 @@ void launch_spmv(unsigned grid, cudaStream_t s, const int64_t* rowptr, const int
     case 17: spmv_group_kernel<MODE, 4, 4, 3, false, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
     case 18: spmv_group_kernel<MODE, 4, 2, 5, false, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
     case 19: spmv_group_kernel<MODE, 4, 4, 4, false, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 20: spmv_group_kernel<MODE, 4, 4, 4, false, true, false, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 21: spmv_group_kernel<MODE, 4, 4, 5, false, true, false, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 22: spmv_group_kernel<MODE, 4, 8, 4, false, true, false, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 23: spmv_pipe_kernel<MODE, 4, 4><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 24: spmv_pipe_kernel<MODE, 2, 4><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 25: spmv_pipe_kernel<MODE, 2, 5><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 26: spmv_pipe_kernel<MODE, 4, 3><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 27: spmv_pipe_kernel<MODE, 2, 6><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
 #undef IPT_SPMV
 #undef IPT_SPMVG
   }
@@ -1356,6 +1564,9 @@ SingleProblem* single_upload(Ctx& c, int64_t n, const double* d_re, const double
                          balance ? "balanced" : "round-robin");
         }
       }
+      // the round-robin kernel keeps entry positions relative to the group start in 32 bits
+      for (int64_t g = 0; g < groups && !balance; ++g)
+        balance = rp[std::min<int64_t>((g + 1) * R, rows)] - rp[g * R] > int64_t(INT32_MAX) - 4096;
       P->spmv_bal = balance;
     }
     if (P->spmv_bal) {
