@@ -127,7 +127,7 @@ constexpr SpmvVariant kSpmvVariants[] = {{16, 4, 0, 5}, {8, 8, 0, 5}, {32, 2, 0,
                                          {0, 4, 4, 4},   // 19: 16 with nnz-balanced contiguous group ranges per warp
                                          {0, 4, 4, 4},  {0, 4, 4, 5},  {0, 8, 4, 4},   // 20-22: 16 with folded row sums
                                          {0, 4, 4, 4},  {0, 2, 4, 4},  {0, 2, 4, 5},  {0, 4, 4, 3},
-                                         {0, 2, 4, 6}};  // 23-27: 20 with software-pipelined loads
+                                         {0, 2, 4, 6},  {0, 3, 4, 4}};  // 23-28: 20 with software-pipelined loads
 constexpr int kNumSpmvVariants = sizeof(kSpmvVariants) / sizeof(kSpmvVariants[0]);
 constexpr int kSpmvDefault = 24;  // warp-contiguous groups of 4 rows, folded row sums, software-pipelined loads (2 + 2 in flight)
 inline int spmv_variant() {
@@ -1149,6 +1149,7 @@ void launch_spmv(unsigned grid, cudaStream_t s, const int64_t* rowptr, const int
     case 25: spmv_pipe_kernel<MODE, 2, 5><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
     case 26: spmv_pipe_kernel<MODE, 4, 3><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
     case 27: spmv_pipe_kernel<MODE, 2, 6><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 28: spmv_pipe_kernel<MODE, 3, 4><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
 #undef IPT_SPMV
 #undef IPT_SPMVG
   }
