@@ -242,15 +242,18 @@ def per_config_e2e(ipt, ctx):
     g5gaps = ipt.build_gaps(p5, 0.0)
     cfg5 = ipt.IterationConfig(tolerance=1e-10)
     ipt.solve_single(p5, g5gaps, 0, cfg5, ctx=ctx)  # warm (pools, staging), as for config 1
-    t0 = time.perf_counter()
-    g5 = ipt.solve_single(p5, g5gaps, 0, cfg5, ctx=ctx)
-    tg = time.perf_counter() - t0
+    tg_all = []
+    for _ in range(3):  # host-side staging of 1.6 GB varies run to run (58-130 ms): median of three calls
+        t0 = time.perf_counter()
+        g5 = ipt.solve_single(p5, g5gaps, 0, cfg5, ctx=ctx)
+        tg_all.append(time.perf_counter() - t0)
+    tg = sorted(tg_all)[1]
     t0 = time.perf_counter()
     r5 = R.solve_single(p5.d, p5.delta, 0, tol=1e-10, degeneracy_tol=0.0)
     tr = time.perf_counter() - t0
     out["config5_csr_single_n2097152"] = {
-        "gpu_s": tg, "reference_s": tr, "reference_inner_s": r5["seconds"], "speedup": r5["seconds"] / tg,
-        "iterations": [g5.iterations, r5["iterations"]],
+        "gpu_s": tg, "gpu_s_all": tg_all, "reference_s": tr, "reference_inner_s": r5["seconds"],
+        "speedup": r5["seconds"] / tg, "iterations": [g5.iterations, r5["iterations"]],
         "eigenvalue_rel_diff": abs(g5.eigenvalue - r5["eigenvalue"].real) / abs(r5["eigenvalue"].real),
         "note": "gpu_s: the drop-in call with host buffers (H2D of the 1.6 GB CSR arrays included); "
                 "reference_inner_s: the reference solve itself (its timer, inputs already in its CSR "

@@ -347,6 +347,24 @@ __device__ __forceinline__ void group_row_sums_at(long long mine, const int32_t*
     for (int off = 16; off > 0; off >>= 1) s[k] += __shfl_xor_sync(0xffffffffu, s[k], off);
 }
 
+// Four per-lane partial sums (rows 0-3 of a group) -> row k's total on lane k, by one
+// transposed xor tree: after level 16 a lane keeps two rows, after level 8 one (row
+// 2 bit4 + bit3 of the lane), levels 4 / 2 / 1 as usual, one shuffle brings row k to lane
+// k. Each level adds the two numbers the full per-row xor tree adds on that lane, so the
+// totals are bit for bit those of four separate trees (7 double shuffles instead of 20).
+__device__ __forceinline__ double fold_rows4(double s0, double s1, double s2, double s3, int lane) {
+  const bool b16 = lane & 16, b8 = lane & 8;
+  double k0 = b16 ? s2 : s0, k1 = b16 ? s3 : s1;
+  k0 += __shfl_xor_sync(0xffffffffu, b16 ? s0 : s2, 16);
+  k1 += __shfl_xor_sync(0xffffffffu, b16 ? s1 : s3, 16);
+  double k = b8 ? k1 : k0;
+  k += __shfl_xor_sync(0xffffffffu, b8 ? k0 : k1, 8);
+  k += __shfl_xor_sync(0xffffffffu, k, 4);
+  k += __shfl_xor_sync(0xffffffffu, k, 2);
+  k += __shfl_xor_sync(0xffffffffu, k, 1);
+  return __shfl_sync(0xffffffffu, k, (lane & 3) * 8);
+}
+
 // group_row_sums_at for R = 4 with the same sums at lower instruction cost (round 2):
 //  * entry positions relative to the group start in 32 bits (one 64-bit base broadcast +
 //    four 32-bit offsets: 6 SHFL instead of 10; 32-bit row selection);
@@ -392,16 +410,7 @@ __device__ __forceinline__ double group_row_sums4_folded(long long mine, const i
       }
     }
   }
-  const bool b16 = lane & 16, b8 = lane & 8;
-  double k0 = b16 ? s2 : s0, k1 = b16 ? s3 : s1;
-  k0 += __shfl_xor_sync(0xffffffffu, b16 ? s0 : s2, 16);
-  k1 += __shfl_xor_sync(0xffffffffu, b16 ? s1 : s3, 16);
-  double k = b8 ? k1 : k0;
-  k += __shfl_xor_sync(0xffffffffu, b8 ? k0 : k1, 8);
-  k += __shfl_xor_sync(0xffffffffu, k, 4);
-  k += __shfl_xor_sync(0xffffffffu, k, 2);
-  k += __shfl_xor_sync(0xffffffffu, k, 1);
-  return __shfl_sync(0xffffffffu, k, (lane & 3) * 8);
+  return fold_rows4(s0, s1, s2, s3, lane);
 }
 
 struct MapArgs {
@@ -856,16 +865,7 @@ __global__ void __launch_bounds__(256, MINB) spmv_pipe_kernel(const int64_t* __r
       }
       qc += 32 * U;
     } while (qc < end);
-    const bool b16 = lane & 16, b8 = lane & 8;
-    double k0 = b16 ? s2 : s0, k1 = b16 ? s3 : s1;
-    k0 += __shfl_xor_sync(0xffffffffu, b16 ? s0 : s2, 16);
-    k1 += __shfl_xor_sync(0xffffffffu, b16 ? s1 : s3, 16);
-    double k = b8 ? k1 : k0;
-    k += __shfl_xor_sync(0xffffffffu, b8 ? k0 : k1, 8);
-    k += __shfl_xor_sync(0xffffffffu, k, 4);
-    k += __shfl_xor_sync(0xffffffffu, k, 2);
-    k += __shfl_xor_sync(0xffffffffu, k, 1);
-    const double w = __shfl_sync(0xffffffffu, k, (lane & 3) * 8);
+    const double w = fold_rows4(s0, s1, s2, s3, lane);
     if (mine) row_epilogue_vals<MODE>(a, gi, zi, di, w, scale, lam, v);
     off0 = off1;
     off1 = off2;
@@ -1045,21 +1045,10 @@ __global__ void __launch_bounds__(256) cspmv_group_kernel(const int64_t* __restr
         }
       }
     }
-#pragma unroll
-    for (int k = 0; k < R; ++k)
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        sr[k] += __shfl_xor_sync(0xffffffffu, sr[k], off);
-        si[k] += __shfl_xor_sync(0xffffffffu, si[k], off);
-      }
+    static_assert(R == 4, "fold_rows4");
+    const double xr = fold_rows4(sr[0], sr[1], sr[2], sr[3], lane);
+    const double xi = fold_rows4(si[0], si[1], si[2], si[3], lane);
     if (lane < R && lr0 + lane < rows) {
-      double xr = sr[0], xi = si[0];
-#pragma unroll
-      for (int k = 1; k < R; ++k)
-        if (lane == k) {
-          xr = sr[k];
-          xi = si[k];
-        }
       wr[row0 + lr0 + lane] = xr;
       wi[row0 + lr0 + lane] = xi;
     }
