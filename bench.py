@@ -336,7 +336,7 @@ def bench_single(ipt, lib, ctx, which, steps, warmup, hbm, reduce_max=lambda x: 
         h = C.c_void_p()
         check(lib.ipt_single_upload_csr(ctx.handle, n, dptr(p.d), None, i64ptr(p.delta.row_offsets),
                                         i32ptr(p.delta.col_indices), dptr(p.delta.values), None, C.byref(h)))
-        kernel = "spmv_pipe_kernel<1, 2, 4>"
+        kernel = "spmv_pipe_kernel<1, 3, 4, 1>"
         tol = 1e-10
         gaps_tol = 0.0
     setup_s = time.perf_counter() - t0

@@ -110,9 +110,12 @@ constexpr int kRowsPerBlock = kGemvRows * kGemvWarps;
 // without (variant 9); with the next group's row offsets loaded while the current group
 // streams 0.627 ms (variant 16; round 2, with the fused step tail); the four xor trees
 // folded into one and 32-bit relative positions 0.613 ms (variant 20); that with the index /
-// value loads software-pipelined 0.601 ms (variant 24, spmv_pipe_kernel, the default; all
-// three give the same bits). The memory ceiling of the same traffic is 0.517 ms
-// (profiles/r01_gather_probe.txt): one L1 -> crossbar request per clock per SM.
+// value loads software-pipelined 0.601 ms (variant 24, spmv_pipe_kernel); only the indices
+// a chunk ahead, the values loaded beside the gathers, 3 entries per lane 0.583 ms
+// (variant 30, the default: 64 registers, no spill; 4 per lane spills or, with the stop
+// sums parked in shared memory, fits and runs 0.596 ms). All give the same bits. The memory
+// ceiling of the same traffic is 0.517 ms (profiles/r01_gather_probe.txt): one L1 ->
+// crossbar request per clock per SM.
 // IPT_SPMV_VARIANT selects another.
 // Variants 5-7: warp-contiguous row groups (spmv_group_kernel), lanes = 0 marks them,
 // u = entries in flight per lane, rows = rows per warp.
@@ -127,9 +130,10 @@ constexpr SpmvVariant kSpmvVariants[] = {{16, 4, 0, 5}, {8, 8, 0, 5}, {32, 2, 0,
                                          {0, 4, 4, 4},   // 19: 16 with nnz-balanced contiguous group ranges per warp
                                          {0, 4, 4, 4},  {0, 4, 4, 5},  {0, 8, 4, 4},   // 20-22: 16 with folded row sums
                                          {0, 4, 4, 4},  {0, 2, 4, 4},  {0, 2, 4, 5},  {0, 4, 4, 3},
-                                         {0, 2, 4, 6},  {0, 3, 4, 4}};  // 23-28: 20 with software-pipelined loads
+                                         {0, 2, 4, 6},  {0, 3, 4, 4},   // 23-28: 20 with software-pipelined loads
+                                         {0, 4, 4, 4},  {0, 3, 4, 4},  {0, 2, 4, 4},  {0, 2, 4, 5}};  // 29-32: only the indices run ahead
 constexpr int kNumSpmvVariants = sizeof(kSpmvVariants) / sizeof(kSpmvVariants[0]);
-constexpr int kSpmvDefault = 24;  // warp-contiguous groups of 4 rows, folded row sums, software-pipelined loads (2 + 2 in flight)
+constexpr int kSpmvDefault = 30;  // warp-contiguous groups of 4 rows, folded row sums, indices one chunk ahead, 3 entries per lane in flight
 inline int spmv_variant() {
   static const int v = [] {
     const char* e = std::getenv("IPT_SPMV_VARIANT");
@@ -777,14 +781,16 @@ __global__ void __launch_bounds__(256, MINB) spmv_group_kernel(const int64_t* __
 // loads and waiting for its z gathers. Here the next chunk's indices and values (the next
 // group's first chunk after a group's last, its offsets known two groups ahead) are
 // requested before the current chunk's gathers are consumed, and the rows' d_i, z_i of the
-// epilogue load at the group's start. Same groups, same lanes, same order of operations:
-// every row sum, iterate and stop sum is bit for bit spmv_group_kernel's.
+// epilogue load at the group's start. XL (the default): only the indices run a chunk ahead
+// and the values load beside the gathers, which frees the registers for a third entry per
+// lane at 4 CTAs per SM. Same groups, same lanes, same order of operations: every row sum,
+// iterate and stop sum is bit for bit spmv_group_kernel's.
 __device__ __forceinline__ double ld_nc_gather_f64(const double* p) {
   double v;
   asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
-template <int MODE, int U, int MINB>
+template <int MODE, int U, int MINB, bool XL = false>
 __global__ void __launch_bounds__(256, MINB) spmv_pipe_kernel(const int64_t* __restrict__ rowptr,
                                                               const int32_t* __restrict__ cols,
                                                               const double* __restrict__ vals, MapArgs a) {
@@ -810,7 +816,7 @@ __global__ void __launch_bounds__(256, MINB) spmv_pipe_kernel(const int64_t* __r
     for (int u = 0; u < U; ++u) {
       const int q = lane + 32 * u;
       c[u] = q < end ? ld_nc_i32(cols + base + q) : 0;
-      x[u] = q < end ? ld_nc_f64(vals + base + q) : 0.0;
+      if (!XL) x[u] = q < end ? ld_nc_f64(vals + base + q) : 0.0;
     }
   }
   for (int64_t grp = g_begin; grp < groups; grp += g_step) {
@@ -834,6 +840,10 @@ __global__ void __launch_bounds__(256, MINB) spmv_pipe_kernel(const int64_t* __r
       double zz[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) zz[u] = (qc + lane + 32 * u < end) ? ld_nc_gather_f64(a.z + c[u]) : 0.0;
+      if (XL) {  // XL: only the indices run a chunk ahead; the values load beside the gathers
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = (qc + lane + 32 * u < end) ? ld_nc_f64(vals + base + qc + lane + 32 * u) : 0.0;
+      }
       int32_t nc[U];
       double nx[U];
       const bool last = qc + 32 * U >= end;
@@ -843,7 +853,7 @@ __global__ void __launch_bounds__(256, MINB) spmv_pipe_kernel(const int64_t* __r
       for (int u = 0; u < U; ++u) {
         const int q = pq + 32 * u;
         nc[u] = q < pe ? ld_nc_i32(cols + pb + q) : 0;
-        nx[u] = q < pe ? ld_nc_f64(vals + pb + q) : 0.0;
+        if (!XL) nx[u] = q < pe ? ld_nc_f64(vals + pb + q) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -861,7 +871,7 @@ __global__ void __launch_bounds__(256, MINB) spmv_pipe_kernel(const int64_t* __r
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         c[u] = nc[u];
-        x[u] = nx[u];
+        if (!XL) x[u] = nx[u];
       }
       qc += 32 * U;
     } while (qc < end);
@@ -1139,6 +1149,10 @@ void launch_spmv(unsigned grid, cudaStream_t s, const int64_t* rowptr, const int
     case 26: spmv_pipe_kernel<MODE, 4, 3><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
     case 27: spmv_pipe_kernel<MODE, 2, 6><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
     case 28: spmv_pipe_kernel<MODE, 3, 4><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 29: spmv_pipe_kernel<MODE, 4, 4, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 30: spmv_pipe_kernel<MODE, 3, 4, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 31: spmv_pipe_kernel<MODE, 2, 4, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
+    case 32: spmv_pipe_kernel<MODE, 2, 5, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a); break;
 #undef IPT_SPMV
 #undef IPT_SPMVG
   }

@@ -1,5 +1,5 @@
 """The CSR map's kernels give the same bits: the default (spmv_pipe_kernel: folded row
-sums, software-pipelined loads, variant 24), the folded-sum kernel (20) and the round-1/2
+sums, software-pipelined loads, variant 30), the folded-sum kernel (20) and the round-1/2
 group kernel (16) form every row sum over the same lanes in the same order, so iterates,
 eigenvalues, stop sums and the plain matvec agree bit for bit (ipt_single.cu). Each variant
 runs in its own process (IPT_SPMV_VARIANT is read once)."""
@@ -75,7 +75,7 @@ def default_run():
     return _run(None)
 
 
-@pytest.mark.parametrize("variant", [16, 20, 24])
+@pytest.mark.parametrize("variant", [16, 20, 24, 31])
 def test_csr_map_kernels_agree_bit_for_bit(default_run, variant):
     other = _run(variant)
     assert other.keys() == default_run.keys()
