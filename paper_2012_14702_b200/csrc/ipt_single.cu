@@ -790,7 +790,7 @@ __device__ __forceinline__ double ld_nc_gather_f64(const double* p) {
   asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
-template <int MODE, int U, int MINB, bool XL = false>
+template <int MODE, int U, int MINB, bool XL = false, bool BAL = false>
 __global__ void __launch_bounds__(256, MINB) spmv_pipe_kernel(const int64_t* __restrict__ rowptr,
                                                               const int32_t* __restrict__ cols,
                                                               const double* __restrict__ vals, MapArgs a) {
@@ -801,12 +801,17 @@ __global__ void __launch_bounds__(256, MINB) spmv_pipe_kernel(const int64_t* __r
   double v[4] = {0.0, 0.0, 0.0, 0.0};
   const double scale = MODE == kMvMap ? schedule_scale(a) : 1.0;
   const double lam = (MODE == kMvFinal || MODE == kMvAccel) ? a.d[a.anchor] + *a.wa : 0.0;
-  const int64_t groups = ceil_div(a.rows, int64_t(R));
-  const int64_t g_begin = blockIdx.x * int64_t(8) + (threadIdx.x >> 5);
-  const int64_t g_step = int64_t(gridDim.x) * 8;
+  // round-robin over the grid's warps, or (BAL) this warp's contiguous nonzero-balanced
+  // range of groups, as in spmv_group_kernel
+  // (group indices fit 32 bits: rows < 2^31 for int32 columns)
+  const int wglob = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int g_begin = BAL ? a.wgroups[wglob] : wglob;
+  const int groups = BAL ? a.wgroups[wglob + 1] : static_cast<int>(ceil_div(a.rows, int64_t(R)));
+  const int g_step = BAL ? 1 : static_cast<int>(gridDim.x) * 8;
   // offsets of this group and the next one in registers, the one after that in flight
-  long long off0 = g_begin < groups ? group_offsets<R>(rowptr, g_begin * R, a.rows, lane) : 0;
-  long long off1 = g_begin + g_step < groups ? group_offsets<R>(rowptr, (g_begin + g_step) * R, a.rows, lane) : 0;
+  long long off0 = g_begin < groups ? group_offsets<R>(rowptr, int64_t(g_begin) * R, a.rows, lane) : 0;
+  long long off1 =
+      g_begin + g_step < groups ? group_offsets<R>(rowptr, int64_t(g_begin + g_step) * R, a.rows, lane) : 0;
   int32_t c[U];
   double x[U];
   {  // first chunk of the first group
@@ -819,10 +824,10 @@ __global__ void __launch_bounds__(256, MINB) spmv_pipe_kernel(const int64_t* __r
       if (!XL) x[u] = q < end ? ld_nc_f64(vals + base + q) : 0.0;
     }
   }
-  for (int64_t grp = g_begin; grp < groups; grp += g_step) {
-    const int64_t lr0 = grp * R;
+  for (int grp = g_begin; grp < groups; grp += g_step) {
+    const int64_t lr0 = int64_t(grp) * R;
     const long long off2 =
-        grp + 2 * g_step < groups ? group_offsets<R>(rowptr, (grp + 2 * g_step) * R, a.rows, lane) : 0;
+        grp + 2 * g_step < groups ? group_offsets<R>(rowptr, int64_t(grp + 2 * g_step) * R, a.rows, lane) : 0;
     const bool mine = lane < R && lr0 + lane < a.rows;
     const int64_t gi = a.row0 + lr0 + lane;
     const double zi = (mine && MODE != kMvStore) ? a.z[gi] : 0.0;  // store mode: a plain matvec, z may be shorter
@@ -1120,7 +1125,10 @@ template <int MODE>
 void launch_spmv(unsigned grid, cudaStream_t s, const int64_t* rowptr, const int32_t* cols, const double* vals,
                  const MapArgs& a) {
   if (a.wgroups != nullptr) {  // balanced group ranges (decided per problem at upload)
-    spmv_group_kernel<MODE, 4, 4, 4, false, true, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a);
+    if (spmv_variant() == 19)
+      spmv_group_kernel<MODE, 4, 4, 4, false, true, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a);
+    else
+      spmv_pipe_kernel<MODE, 3, 4, true, true><<<grid, 256, 0, s>>>(rowptr, cols, vals, a);
     return;
   }
   switch (spmv_variant()) {

@@ -39,10 +39,27 @@ def ragged(n, seed):
     d = np.cumsum(rng.uniform(0.8, 1.2, n))
     return ipt.Partition(d, ipt.CsrMatrix.from_triplets(n, n, rows, cols, vals))
 
+def heavy(n, seed):
+    # 1 % of the rows 200x longer than the rest: the upload cuts nonzero-balanced group ranges
+    rng = np.random.default_rng(seed)
+    lengths = np.where(rng.random(n) < 0.01, 2500, 12)
+    rows = np.repeat(np.arange(n), lengths)
+    cols = rng.integers(0, n, rows.size)
+    keep = cols != rows
+    rows, cols = rows[keep], cols[keep]
+    key = rows * n + cols
+    _, first = np.unique(key, return_index=True)
+    rows, cols = rows[first], cols[first]
+    vals = 0.3 / np.sqrt(2500.0) * rng.standard_normal(rows.size)
+    d = np.cumsum(np.random.default_rng(seed + 1).uniform(0.8, 1.2, n))
+    return ipt.Partition(d, ipt.CsrMatrix.from_triplets(n, n, rows, cols, vals))
+
 out = {}
 h = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
-for name, p, tol in (("ci4096", synth.csr_ci(4096, 32, 0.01, 42), 1e-10), ("ragged4099", ragged(4099, 5), 1e-12),
-                     ("ragged7", ragged(7, 2), 1e-12), ("ci65536", synth.csr_ci(65536, 32, 0.01, 7), 1e-10)):
+cases = (("heavy16384", heavy(1 << 14, 3), 1e-12),) if sys.argv[2] == "heavy" else (
+    ("ci4096", synth.csr_ci(4096, 32, 0.01, 42), 1e-10), ("ragged4099", ragged(4099, 5), 1e-12),
+    ("ragged7", ragged(7, 2), 1e-12), ("ci65536", synth.csr_ci(65536, 32, 0.01, 7), 1e-10))
+for name, p, tol in cases:
     g = ipt.build_gaps(p, 0.0)
     for anchor in (0, p.size() // 2):
         r = ipt.solve_single(p, g, anchor, ipt.IterationConfig(tolerance=tol, record_trace=True))
@@ -58,13 +75,16 @@ print("RESULT " + json.dumps(out))
 """
 
 
-def _run(variant):
+def _run(variant, cases="plain"):
     env = dict(os.environ)
     env.pop("IPT_SPMV_VARIANT", None)
     if variant is not None:
         env["IPT_SPMV_VARIANT"] = str(variant)
-    env["IPT_SPMV_BALANCE"] = "0"  # the ragged patterns stay on the round-robin kernels under test
-    r = subprocess.run([sys.executable, "-c", _SCRIPT, ROOT], env=env, capture_output=True, text=True, timeout=600)
+    env.pop("IPT_SPMV_BALANCE", None)
+    if cases == "plain":
+        env["IPT_SPMV_BALANCE"] = "0"  # the ragged patterns stay on the round-robin kernels under test
+    r = subprocess.run([sys.executable, "-c", _SCRIPT, ROOT, cases], env=env, capture_output=True, text=True,
+                       timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     line = [l for l in r.stdout.splitlines() if l.startswith("RESULT ")][-1]
     return json.loads(line[len("RESULT "):])
@@ -81,6 +101,15 @@ def test_csr_map_kernels_agree_bit_for_bit(default_run, variant):
     assert other.keys() == default_run.keys()
     for k in default_run:
         assert other[k] == default_run[k], k
+
+
+def test_balanced_ranges_agree_bit_for_bit():
+    """Skewed rows: the default runs spmv_pipe_kernel over nonzero-balanced group ranges,
+    variant 19 the group kernel over the same ranges."""
+    a, b = _run(None, "heavy"), _run(19, "heavy")
+    assert a.keys() == b.keys() and len(a) == 5
+    for k in a:
+        assert a[k] == b[k], k
 
 
 def test_default_matches_numpy(default_run):
