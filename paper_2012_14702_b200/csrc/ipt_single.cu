@@ -1070,6 +1070,93 @@ __global__ void __launch_bounds__(256) cspmv_group_kernel(const int64_t* __restr
   }
 }
 
+// cspmv_group_kernel<4, ., VI> with the real map's pipelining (spmv_pipe_kernel, XL): the
+// next chunk's indices are requested before the current chunk's gathers are consumed, the
+// values load beside the gathers, offsets run two groups ahead. Same groups, lanes and
+// order of operations: the same sums bit for bit.
+template <int U, bool VI>
+__global__ void __launch_bounds__(256, VI ? 3 : 4) cspmv_pipe_kernel(const int64_t* __restrict__ rowptr,
+                                                            const int32_t* __restrict__ cols,
+                                                            const double* __restrict__ vr,
+                                                            const double* __restrict__ vi,
+                                                            const double2* __restrict__ zc, int64_t rows,
+                                                            double* __restrict__ wr, double* __restrict__ wi,
+                                                            int64_t row0) {
+  constexpr int R = 4;
+  const int lane = threadIdx.x & 31;
+  const int groups = static_cast<int>(ceil_div(rows, int64_t(R)));
+  const int g_begin = blockIdx.x * 8 + (threadIdx.x >> 5), g_step = static_cast<int>(gridDim.x) * 8;
+  long long off0 = g_begin < groups ? group_offsets<R>(rowptr, int64_t(g_begin) * R, rows, lane) : 0;
+  long long off1 = g_begin + g_step < groups ? group_offsets<R>(rowptr, int64_t(g_begin + g_step) * R, rows, lane) : 0;
+  int32_t c[U];
+  {
+    const long long base = __shfl_sync(0xffffffffu, off0, 0);
+    const int end = static_cast<int>(__shfl_sync(0xffffffffu, off0, R) - base);
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = lane + 32 * u < end ? ld_nc_i32(cols + base + lane + 32 * u) : 0;
+  }
+  for (int grp = g_begin; grp < groups; grp += g_step) {
+    const int64_t lr0 = int64_t(grp) * R;
+    const long long off2 =
+        grp + 2 * g_step < groups ? group_offsets<R>(rowptr, int64_t(grp + 2 * g_step) * R, rows, lane) : 0;
+    const long long base = __shfl_sync(0xffffffffu, off0, 0);
+    const int rel = static_cast<int>(off0 - base);
+    const int r1 = __shfl_sync(0xffffffffu, rel, 1), r2 = __shfl_sync(0xffffffffu, rel, 2),
+              r3 = __shfl_sync(0xffffffffu, rel, 3), end = __shfl_sync(0xffffffffu, rel, 4);
+    const bool more = grp + g_step < groups;
+    const long long nbase = __shfl_sync(0xffffffffu, off1, 0);
+    const int nend = more ? static_cast<int>(__shfl_sync(0xffffffffu, off1, R) - nbase) : 0;
+    double sr[R] = {0.0, 0.0, 0.0, 0.0}, si[R] = {0.0, 0.0, 0.0, 0.0};
+    int qc = 0;
+    do {
+      double2 zz[U];
+      double a[U], b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = qc + lane + 32 * u;
+        zz[u] = q < end ? __ldg(zc + c[u]) : make_double2(0.0, 0.0);
+        a[u] = q < end ? ld_nc_f64(vr + base + q) : 0.0;
+        b[u] = (VI && q < end) ? ld_nc_f64(vi + base + q) : 0.0;
+      }
+      const bool last = qc + 32 * U >= end;
+      const long long pb = last ? nbase : base;
+      const int pq = last ? lane : qc + 32 * U + lane, pe = last ? nend : end;
+      int32_t nc[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) nc[u] = pq + 32 * u < pe ? ld_nc_i32(cols + pb + pq + 32 * u) : 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = qc + lane + 32 * u;
+        if (q < end) {
+          const int r = (q >= r1) + (q >= r2) + (q >= r3);
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+            if (k == r) {
+              // (a + ib)(x + iy): re += a x - b y, im += a y + b x
+              sr[k] = __fma_rn(a[u], zz[u].x, sr[k]);
+              si[k] = __fma_rn(a[u], zz[u].y, si[k]);
+              if (VI) {
+                sr[k] = __fma_rn(-b[u], zz[u].y, sr[k]);
+                si[k] = __fma_rn(b[u], zz[u].x, si[k]);
+              }
+            }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) c[u] = nc[u];
+      qc += 32 * U;
+    } while (qc < end);
+    const double xr = fold_rows4(sr[0], sr[1], sr[2], sr[3], lane);
+    const double xi = fold_rows4(si[0], si[1], si[2], si[3], lane);
+    if (lane < R && lr0 + lane < rows) {
+      wr[row0 + lr0 + lane] = xr;
+      wi[row0 + lr0 + lane] = xi;
+    }
+    off0 = off1;
+    off1 = off2;
+  }
+}
+
 // mode 1: map ; mode 2: final residual. Fixed grid => deterministic partials.
 __global__ void cmap_kernel(int mode, const double* __restrict__ zr, const double* __restrict__ zi,
                             const double* __restrict__ wr, const double* __restrict__ wi,
@@ -1227,15 +1314,41 @@ void enqueue_cmatvec(SingleProblem& P, int src) {
         P.z[src].get(), P.zi[src].get(), vlen, reinterpret_cast<double2*>(P.zc.get()));
     IPT_LAUNCH_CHECK();
     count_launch();
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(int64_t(kNumSMs) * 4, ceil_div(rows, int64_t(32))));
-    if (P.valsi.count)
-      cspmv_group_kernel<4, 4, true><<<grid, 256, 0, s>>>(P.rowptr.get(), P.cols.get(), P.vals.get(),
-                                                         P.valsi.get(), reinterpret_cast<const double2*>(P.zc.get()),
-                                                         rows, P.w.get(), P.wi.get(), P.r0);
-    else
-      cspmv_group_kernel<4, 4, false><<<grid, 256, 0, s>>>(P.rowptr.get(), P.cols.get(), P.vals.get(), nullptr,
-                                                          reinterpret_cast<const double2*>(P.zc.get()), rows,
-                                                          P.w.get(), P.wi.get(), P.r0);
+    // IPT_CSPMV=0: the group kernel; 2 / 3: the pipelined kernel, entries per lane in flight.
+    // Complex Hermitian config-5 pattern, step with its elementwise map: 0.968 / 0.758 /
+    // 0.716 ms (the thread-per-row kernel of round 1: 2.37 ms). Same sums bit for bit.
+    static const int ckind = [] {
+      const char* e = std::getenv("IPT_CSPMV");
+      return e ? std::atoi(e) : 3;
+    }();
+    const double2* zc = reinterpret_cast<const double2*>(P.zc.get());
+    // resident CTAs per SM: 4, or 3 for the pipelined kernel with complex values (70-78 registers)
+    const int per_sm = (ckind != 0 && P.valsi.count) ? 3 : 4;
+    const unsigned grid =
+        static_cast<unsigned>(std::min<int64_t>(int64_t(kNumSMs) * per_sm, ceil_div(rows, int64_t(32))));
+#define IPT_CSPMV_ARGS P.rowptr.get(), P.cols.get(), P.vals.get()
+    if (P.valsi.count) {
+      if (ckind == 0)
+        cspmv_group_kernel<4, 4, true><<<grid, 256, 0, s>>>(IPT_CSPMV_ARGS, P.valsi.get(), zc, rows, P.w.get(),
+                                                           P.wi.get(), P.r0);
+      else if (ckind == 3)
+        cspmv_pipe_kernel<3, true><<<grid, 256, 0, s>>>(IPT_CSPMV_ARGS, P.valsi.get(), zc, rows, P.w.get(),
+                                                        P.wi.get(), P.r0);
+      else
+        cspmv_pipe_kernel<2, true><<<grid, 256, 0, s>>>(IPT_CSPMV_ARGS, P.valsi.get(), zc, rows, P.w.get(),
+                                                        P.wi.get(), P.r0);
+    } else {
+      if (ckind == 0)
+        cspmv_group_kernel<4, 4, false><<<grid, 256, 0, s>>>(IPT_CSPMV_ARGS, nullptr, zc, rows, P.w.get(),
+                                                            P.wi.get(), P.r0);
+      else if (ckind == 3)
+        cspmv_pipe_kernel<3, false><<<grid, 256, 0, s>>>(IPT_CSPMV_ARGS, nullptr, zc, rows, P.w.get(),
+                                                         P.wi.get(), P.r0);
+      else
+        cspmv_pipe_kernel<2, false><<<grid, 256, 0, s>>>(IPT_CSPMV_ARGS, nullptr, zc, rows, P.w.get(),
+                                                         P.wi.get(), P.r0);
+    }
+#undef IPT_CSPMV_ARGS
   } else if (P.csr) {
     cmatvec_csr_kernel<<<static_cast<unsigned>(ceil_div(rows, 256)), 256, 0, s>>>(
         P.rowptr.get(), P.cols.get(), P.vals.get(), P.valsi.count ? P.valsi.get() : nullptr, rows,

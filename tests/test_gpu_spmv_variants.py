@@ -126,3 +126,47 @@ def test_default_matches_numpy(default_run):
     np.add.at(ref, rows, p.delta.values * x[p.delta.col_indices])
     assert np.max(np.abs(y - ref)) <= 1e-13 * np.max(np.abs(ref))
     assert hashlib.sha256(np.ascontiguousarray(y).tobytes()).hexdigest() == default_run["ci4096/matvec"]
+
+
+_CSCRIPT = r"""
+import hashlib, json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2012_14702_b200 as ipt
+from paper_2012_14702_b200 import synth
+h = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+out = {}
+for n in (4099, 65536):
+    p = synth.csr_ci(n, 32, 0.01, 11)
+    rp, ci, va = p.delta.row_offsets, p.delta.col_indices, p.delta.values
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    vi = 0.003 * np.sign(ci - rows) * np.abs(va)  # antisymmetric imaginary part: Hermitian
+    q = ipt.Partition(p.d, ipt.CsrMatrix(n, n, rp, ci, va + 1j * vi))
+    r = ipt.solve_single(q, ipt.build_gaps(q, 0.0), 3, ipt.IterationConfig(tolerance=1e-11))
+    out[f"hermitian{n}"] = [h(r.z), repr(r.eigenvalue), r.iterations, repr(r.residual)]
+    x = np.random.default_rng(2).standard_normal(n) + 1j * np.random.default_rng(3).standard_normal(n)
+    out[f"matvec{n}"] = h(ipt.kernels.matvec(q.delta, x))
+    out[f"real_times_complex{n}"] = h(ipt.kernels.matvec(p.delta, x))
+print("RESULT " + json.dumps(out))
+"""
+
+
+def _crun(kind):
+    env = dict(os.environ)
+    env.pop("IPT_CSPMV", None)
+    if kind is not None:
+        env["IPT_CSPMV"] = str(kind)
+    r = subprocess.run([sys.executable, "-c", _CSCRIPT, ROOT], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [l for l in r.stdout.splitlines() if l.startswith("RESULT ")][-1]
+    return json.loads(line[len("RESULT "):])
+
+
+def test_complex_csr_kernels_agree_bit_for_bit():
+    """cspmv_pipe_kernel (default, 3 entries per lane; 2) against cspmv_group_kernel."""
+    base = _crun(None)
+    assert len(base) == 6
+    for kind in (0, 2):
+        other = _crun(kind)
+        for k in base:
+            assert other[k] == base[k], (kind, k)
