@@ -233,42 +233,66 @@ __device__ __forceinline__ void gemm_epilogue(const GemmParams& p, double (&acc)
       }
     return;
   }
+  // Real map / residual. The thread's 8 rows' d_i load once, and each column's 8 entries of
+  // Z load together, one column ahead of the column being computed and stored (round 2:
+  // with the load of every Z_ij behind the store of the previous F_ij, which the compiler
+  // may not reorder -- C could alias B -- the 64 elements of a thread were 64 dependent
+  // memory round trips, ~50 us per 128 x 128 tile). The arithmetic per element is unchanged.
+  double di[4][2];
 #pragma unroll
-  for (int ni = 0; ni < 4; ++ni)
+  for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int64_t j = n0 + wn * 32 + ni * 8 + 2 * t + e;
-      if (j >= p.n_cols) continue;
-      const int64_t jg = p.col0 + j;
-      const double dj = p.d[jg];
-      const double wj = MODE == kGemmMap ? p.wd[j] : p.lam[j];
-      const double* zcol = p.B + j * p.ldb;
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int64_t i = m0 + wm * 64 + mi * 16 + g + h * 8;
-          if (i >= p.n_rows) continue;
-          const int64_t ig = p.row0 + i;
-          const double w = acc[mi][ni][h * 2 + e];
-          const double z = zcol[i];
-          if (MODE == kGemmMap) {
-            // (z * wd - w) / (d_i - d_j): each operation rounded on its own, as
-            // the reference's complex arithmetic does for zero imaginary parts.
-            const double f = (ig == jg) ? 1.0
-                                        : __ddiv_rn(__dsub_rn(__dmul_rn(z, wj), w), __dsub_rn(p.d[ig], dj));
-            p.C[j * p.ldc + i] = f;
-            const double df = __dsub_rn(f, z);
-            v[0] = __fma_rn(df, df, v[0]);
-            v[1] = __fma_rn(z, z, v[1]);
-            v[2] = __fma_rn(f, f, v[2]);
-            v[3] = nan_max(v[3], fabs(df));
-          } else {  // kGemmResid
-            const double r = __dsub_rn(__dadd_rn(__dmul_rn(p.d[ig], z), w), __dmul_rn(z, wj));
-            v[0] = __fma_rn(r, r, v[0]);
-          }
-        }
+    for (int h = 0; h < 2; ++h) {
+      const int64_t i = m0 + wm * 64 + mi * 16 + g + h * 8;
+      di[mi][h] = i < p.n_rows ? p.d[p.row0 + i] : 0.0;
     }
+  double zb[2][4][2];
+  auto load_col = [&](int c, double (&z)[4][2]) {
+    const int64_t j = n0 + wn * 32 + (c >> 1) * 8 + 2 * t + (c & 1);
+    const double* zcol = p.B + j * p.ldb;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t i = m0 + wm * 64 + mi * 16 + g + h * 8;
+        z[mi][h] = (j < p.n_cols && i < p.n_rows) ? zcol[i] : 0.0;
+      }
+  };
+  load_col(0, zb[0]);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int ni = c >> 1, e = c & 1;
+    if (c + 1 < 8) load_col(c + 1, zb[(c + 1) & 1]);
+    const int64_t j = n0 + wn * 32 + ni * 8 + 2 * t + e;
+    if (j >= p.n_cols) continue;
+    const int64_t jg = p.col0 + j;
+    const double dj = p.d[jg];
+    const double wj = MODE == kGemmMap ? p.wd[j] : p.lam[j];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t i = m0 + wm * 64 + mi * 16 + g + h * 8;
+        if (i >= p.n_rows) continue;
+        const int64_t ig = p.row0 + i;
+        const double w = acc[mi][ni][h * 2 + e];
+        const double z = zb[c & 1][mi][h];
+        if (MODE == kGemmMap) {
+          // (z * wd - w) / (d_i - d_j): each operation rounded on its own, as
+          // the reference's complex arithmetic does for zero imaginary parts.
+          const double f = (ig == jg) ? 1.0 : __ddiv_rn(__dsub_rn(__dmul_rn(z, wj), w), __dsub_rn(di[mi][h], dj));
+          p.C[j * p.ldc + i] = f;
+          const double df = __dsub_rn(f, z);
+          v[0] = __fma_rn(df, df, v[0]);
+          v[1] = __fma_rn(z, z, v[1]);
+          v[2] = __fma_rn(f, f, v[2]);
+          v[3] = nan_max(v[3], fabs(df));
+        } else {  // kGemmResid
+          const double r = __dsub_rn(__dadd_rn(__dmul_rn(di[mi][h], z), w), __dmul_rn(z, wj));
+          v[0] = __fma_rn(r, r, v[0]);
+        }
+      }
+  }
 }
 
 // ------------------------------------------------------------------ TMA pipeline kernel
